@@ -1,0 +1,427 @@
+"""Pins of the CPU oracle (oracle/oracle.c) against what the paper and the mathematics fix.
+
+CPU only (no GPU marker).  Each test names the passage or closed form it checks and is chosen so
+that a plausible mistake (dropped term, wrong sign or index, transposed operand) fails it.
+Independent arithmetic here is plain numpy (np.tanh, np.linalg.pinv / lstsq, finite differences),
+never the oracle's own routines re-called.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as WL
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "pins.json")))
+
+
+def mkcfg(k=None, **kw):
+    if k is not None:
+        c = WL.config(k)
+        c.update(kw)
+    else:
+        c = dict(P=2, M=16, p=6, q=5, problem=0, seed=7, init_scheme=0, init_c=0.125, r_over_diam=0.5)
+        c.update(kw)
+    return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0),
+                 c.get("init_c", 0.125), c.get("r_over_diam", 0.5), c["seed"])
+
+
+# ------------------------------------------------------------------------------------------------
+# geometry (readings R1, R14)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", range(5))
+def test_geometry_counts(k):
+    g = O.geometry(mkcfg(k))
+    assert g["m"] == GOLD["geometry"]["m"][k]
+    assert g["G"] == GOLD["geometry"]["G"][k]
+
+
+def test_shared_interface_points_bitwise_and_opposite_normals():
+    """A face's points are the same in both neighbours (bit for bit, same global index) and the
+    two neighbours see it through opposite edges, i.e. opposite outward normals."""
+    c = mkcfg(P=3, M=8, p=4, q=5)
+    P, q = 3, 5
+    seen = {}
+    for s in range(P * P):
+        xy, edge, gidx = O.rows(c, s)
+        for r in np.where(gidx >= 0)[0]:
+            seen.setdefault(int(gidx[r]), []).append((s, int(edge[r]), tuple(xy[r])))
+    G = O.geometry(c)["G"]
+    assert sorted(seen) == list(range(G))
+    opposite = {0: 1, 1: 0, 2: 3, 3: 2}
+    for gi, lst in seen.items():
+        assert len(lst) == 2
+        (s1, e1, p1), (s2, e2, p2) = lst
+        assert p1 == p2                       # bitwise identical coordinates
+        assert opposite[e1] == e2             # opposite outward normals
+    # points strictly inside the face (endpoints excluded, reading R1)
+    xy, edge, gidx = O.rows(c, 4)
+    h = 1.0 / P
+    for e in range(4):
+        pts = xy[edge == e]
+        along = pts[:, 1] if e < 2 else pts[:, 0]
+        lo = (4 // P if e < 2 else 4 % P) * h
+        assert np.all(along > lo) and np.all(along < lo + h)
+        assert np.all(np.diff(along) > 0)      # increasing coordinate
+    assert (edge == -1).sum() == 16 and len(edge) == 16 + 4 * q
+
+
+# ------------------------------------------------------------------------------------------------
+# initialisation eqn:init
+# ------------------------------------------------------------------------------------------------
+def test_init_l_from_paper_table1():
+    """n = 2^16 and c = 1/8 give l = 32 (Table 1 P:564 'sqrt(n/64)')."""
+    g = GOLD["init_l_paper_table1"]
+    c = mkcfg(P=4, M=4096, p=2, q=2, init_c=g["c"])   # N*M = 65536
+    W, b, xi, tries = O.init_hidden(c)
+    l = g["l"]
+    assert np.abs(W).max() <= l
+    assert np.abs(W).max() > 0.999 * l                    # U([-l,l]^2) fills the box
+    assert abs(np.mean(W)) < 0.01 * l
+    assert abs(np.var(W) - l * l / 3) < 0.02 * l * l / 3    # variance of U(-l,l)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_init_l_configs(k):
+    W, b, xi, tries = O.init_hidden(mkcfg(k))
+    l = GOLD["init_l_configs"]["l"][k]
+    assert np.abs(W).max() <= l and np.abs(W).max() > 0.99 * l
+
+
+def test_init_bias_centres_and_collar():
+    """b = -w.xi so phi_j(xi_j) = sigma(0) = 0 (eqn:init); dist(xi, Omega_s) <= r with
+    r = diam/2; rejection acceptance = area ratio (closed form in golden/pins.json)."""
+    c = mkcfg(P=4, M=4000, p=2, q=2, seed=11)
+    W, b, xi, tries = O.init_hidden(c)
+    z = W[..., 0] * xi[..., 0] + W[..., 1] * xi[..., 1] + b
+    scale = np.abs(W[..., 0] * xi[..., 0]) + np.abs(W[..., 1] * xi[..., 1])
+    assert np.all(np.abs(z) <= 4 * np.finfo(float).eps * (scale + 1e-300))
+    P = 4
+    h = 1.0 / P
+    r = 0.5 * math.sqrt(2) * h
+    for s in range(P * P):
+        i, j = s % P, s // P
+        dx = np.maximum(np.maximum(i * h - xi[s, :, 0], xi[s, :, 0] - (i + 1) * h), 0)
+        dy = np.maximum(np.maximum(j * h - xi[s, :, 1], xi[s, :, 1] - (j + 1) * h), 0)
+        assert np.all(dx * dx + dy * dy <= r * r * (1 + 1e-12))
+    acc = tries.size / tries.sum()
+    p = GOLD["collar_acceptance"]["value"]
+    se = math.sqrt(p * (1 - p) / tries.sum())
+    assert abs(acc - p) < 4 * se
+    # the sampled xi fill the collar: some lie outside Omega_s, some near the rounded corners
+    s = 5
+    i, j = s % P, s // P
+    out = (xi[s, :, 0] < i * h) | (xi[s, :, 0] > (i + 1) * h)
+    assert 0.2 < out.mean() < 0.6
+
+
+def test_init_he_and_manual():
+    W, b, xi, _ = O.init_hidden(mkcfg(P=2, M=500, init_scheme=2))
+    assert np.all(b == 0.0)
+    l = math.sqrt(2.0 / 500)
+    assert np.abs(W).max() <= l and np.abs(W).max() > 0.98 * l
+    W, b, xi, _ = O.init_hidden(mkcfg(P=2, M=500, init_scheme=1))
+    assert np.abs(W).max() <= 1.0 and np.abs(W).max() > 0.98
+    z = W[..., 0] * xi[..., 0] + W[..., 1] * xi[..., 1] + b
+    assert np.abs(z).max() < 1e-15
+
+
+def test_init_deterministic_and_seed_dependent():
+    a = O.init_hidden(mkcfg(seed=3))
+    b_ = O.init_hidden(mkcfg(seed=3))
+    c = O.init_hidden(mkcfg(seed=4))
+    assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1])
+    assert not np.array_equal(a[0], c[0])
+
+
+# ------------------------------------------------------------------------------------------------
+# manufactured problems and assembly (eqn:nonoverlap_discrete P:231-280)
+# ------------------------------------------------------------------------------------------------
+def test_rhs_pinned_value():
+    g = GOLD["poisson_rhs_problem1"]
+    u, f = O.problem(1, g["x"], g["y"])
+    assert abs(f - g["f"]) < 1e-12 * abs(g["f"])
+
+
+@pytest.mark.parametrize("pid", [0, 1, 2, 3, 4])
+def test_rhs_is_minus_laplacian(pid):
+    rng = np.random.default_rng(pid)
+    h = 1e-4
+    for x, y in rng.uniform(0.05, 0.95, size=(20, 2)):
+        U = lambda a, b: WL.exact(pid, np.array([[a, b]]))[0]
+        lap = (U(x + h, y) + U(x - h, y) + U(x, y + h) + U(x, y - h) - 4 * U(x, y)) / h**2
+        u, f = O.problem(pid, x, y)
+        assert abs(u - U(x, y)) < 1e-13 * (1 + abs(u))
+        assert abs(f + lap) < 2e-5 * (1 + abs(f))
+    assert O.problem(5, 0.3, 0.7) == (0.0, 0.0)
+
+
+def test_tanh_derivatives_at_zero_in_rows():
+    """Place a neuron so that z = 0 exactly at chosen rows: value rows give sigma(0) = 0,
+    interior rows -|w|^2 sigma''(0) = 0 and flux rows (w.n) sigma'(0) = w.n."""
+    c = mkcfg(P=2, M=3, p=3, q=3)
+    xy, edge, gidx = O.rows(c, 3)  # subdomain (1,1): left and bottom edges are interface
+    N = 4
+    W = np.zeros((N, 3, 2))
+    b = np.zeros((N, 3))
+    rl = np.where(edge == 0)[0][1]      # a left-edge (interface) point
+    ri = 4                              # an interior point
+    W[3, 0] = (2.0, 1.0)
+    b[3, 0] = -(2.0 * xy[rl, 0] + 1.0 * xy[rl, 1])
+    W[3, 1] = (-3.0, 0.5)
+    b[3, 1] = -(-3.0 * xy[ri, 0] + 0.5 * xy[ri, 1])
+    K, F, A = O.assemble(c, 3, W, b)
+    gold = GOLD["tanh_derivatives_at_0"]
+    assert K[rl, 0] == gold["sigma"]
+    ar = rl - 9                          # flux row index e*q + k
+    assert A[ar, 0] == -2.0 * gold["sigma1"]      # n = (-1, 0) on the left edge
+    assert K[ri, 1] == -(9.0 + 0.25) * gold["sigma2"]
+    # a zero neuron (w = 0, b = 0) gives sigma = 0 everywhere and no flux
+    assert np.all(K[:, 2] == 0.0) and np.all(A[:, 2] == 0.0)
+
+
+@pytest.mark.parametrize("s", [0, 3])
+def test_assembly_rows_vs_finite_differences(s):
+    """Interior rows = -Lap phi, value rows = phi, flux rows = d phi / d n_s, checked against
+    np.tanh and central differences (1e-6 relative); F = [f; g; 0]."""
+    c = mkcfg(P=2, M=24, p=5, q=4, problem=1, seed=5)
+    W, b, xi, _ = O.init_hidden(c)
+    K, F, A = O.assemble(c, s, W, b)
+    xy, edge, gidx = O.rows(c, s)
+    w = W[s]
+    bb = b[s]
+    phi = lambda p: np.tanh(w[:, 0] * p[0] + w[:, 1] * p[1] + bb)
+    h = 1e-4
+    normals = {0: (-1, 0), 1: (1, 0), 2: (0, -1), 3: (0, 1)}
+    q = 4
+    for r in range(len(edge)):
+        p = xy[r]
+        if edge[r] < 0:
+            lap = (phi(p + [h, 0]) + phi(p - [h, 0]) + phi(p + [0, h]) + phi(p - [0, h]) - 4 * phi(p)) / h**2
+            assert np.allclose(K[r], -lap, rtol=0, atol=1e-6 * np.abs(lap).max())
+            u, f = O.problem(1, p[0], p[1])
+            assert F[r] == f
+        else:
+            assert np.allclose(K[r], phi(p), rtol=0, atol=2e-15)
+            e = edge[r]
+            ar = r - 25
+            assert ar // q == e
+            n = np.array(normals[e], float)
+            d = (phi(p + h * n) - phi(p - h * n)) / (2 * h)
+            if gidx[r] >= 0:
+                assert np.allclose(A[ar], d, rtol=0, atol=1e-7 * np.abs(d).max())
+                assert F[r] == 0.0
+            else:
+                assert np.all(A[ar] == 0.0)
+                assert F[r] == WL.exact(1, p[None])[0] or abs(F[r] - WL.exact(1, p[None])[0]) < 1e-14
+
+
+# ------------------------------------------------------------------------------------------------
+# Householder QR (reading R11/R20)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", [(1, 1), (7, 3), (50, 10), (200, 120), (37, 37)])
+def test_qr_reconstruction_and_orthogonality(shape):
+    rng = np.random.default_rng(sum(shape))
+    A = rng.standard_normal(shape)
+    Af, tau = O.qr(A)
+    m, n = shape
+    R = np.triu(Af[: min(m, n), :])
+    QR = np.stack([O.apply_q(Af, tau, np.concatenate([R[:, j], np.zeros(m - R.shape[0])])) for j in range(n)], 1)
+    assert np.linalg.norm(QR - A) <= 1e-12 * np.linalg.norm(A)
+    v = rng.standard_normal(m)
+    assert np.allclose(O.apply_qt(Af, tau, O.apply_q(Af, tau, v)), v, atol=1e-13 * np.linalg.norm(v))
+    # |R| diagonal = |numpy R| diagonal (QR unique up to signs)
+    Rn = np.linalg.qr(A, mode="r")
+    assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(Rn)), rtol=1e-10)
+
+
+def test_qr_zero_column_and_lstsq_mean():
+    A = np.zeros((4, 2))
+    A[:, 1] = [1, 2, 3, 4]
+    Af, tau = O.qr(A)
+    assert tau[0] == 0.0
+    g = GOLD["lstsq_mean"]
+    K = np.array(g["K"])
+    Af, tau = O.qr(K)
+    y = O.apply_qt(Af, tau, np.array(g["rhs"]))
+    c = y[:1] / Af[0, 0]
+    assert np.allclose(c, g["c"], rtol=1e-15)
+    # least-squares optimality K^T (K c - rhs) = 0 on a random tall system
+    rng = np.random.default_rng(1)
+    K = rng.standard_normal((50, 10))
+    rhs = rng.standard_normal(50)
+    Af, tau = O.qr(K)
+    y = O.apply_qt(Af, tau, rhs)
+    c = np.linalg.solve(np.triu(Af[:10, :10]), y[:10])
+    assert np.linalg.norm(K.T @ (K @ c - rhs)) < 1e-12 * np.linalg.norm(K) * np.linalg.norm(rhs)
+
+
+def test_cholesky_pins():
+    g = GOLD["spd_2x2"]
+    L, rc = O.cholesky(np.array(g["A"]))
+    assert rc == 0
+    assert np.allclose(O.chol_solve(L, g["b"]), g["x"], rtol=1e-15)
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((300, 200))
+    S = X.T @ X + np.eye(200)
+    L, rc = O.cholesky(S, nthreads=4)
+    assert rc == 0 and np.allclose(L @ L.T, S, atol=1e-10 * np.abs(S).max())
+    bb = rng.standard_normal(200)
+    assert np.allclose(O.chol_solve(L, bb), np.linalg.solve(S, bb), rtol=1e-9)
+    S[5, 5] = -1.0
+    _, rc = O.cholesky(S)
+    assert rc == 6                        # 1 + column of the first non-positive pivot
+
+
+# ------------------------------------------------------------------------------------------------
+# Schur system (eqn:eliminated P:351-373, LS_system P:398-406, eqn:schur P:407-410)
+# ------------------------------------------------------------------------------------------------
+def _global_blocks(c, W, b):
+    """Dense K (block diag), B (stacked -E), A (flux rows, globally indexed), F, from the oracle's
+    assembly; numpy builds everything else."""
+    geo = O.geometry(c)
+    N, G, M = geo["N"], geo["G"], c.M
+    Ks, Fs, Bs, As = [], [], [], []
+    for s in range(N):
+        K, F, A4 = O.assemble(c, s, W, b)
+        xy, edge, gidx = O.rows(c, s)
+        m = len(edge)
+        B = np.zeros((m, G))
+        Ag = np.zeros((G, M))
+        for r in np.where(gidx >= 0)[0]:
+            B[r, gidx[r]] = -1.0
+            Ag[gidx[r]] += A4[r - (m - 4 * c.q)]
+        Ks.append(K)
+        Fs.append(F)
+        Bs.append(B)
+        As.append(Ag)
+    from scipy.linalg import block_diag
+
+    return block_diag(*Ks), np.vstack(Bs), np.hstack(As), np.concatenate(Fs)
+
+
+def _tiny_cfg(P=2, **kw):
+    # well-conditioned tiny instance: few neurons, many points, larger l (init_c = 1)
+    base = dict(P=P, M=10, p=7, q=6, problem=0, seed=2, init_c=1.0)
+    base.update(kw)
+    return mkcfg(**base)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_schur_matches_literal_eqn_schur(P):
+    """Oracle M, g == B^T (I + K^{+T} A^T A K^+ - K K^+) B and ... F with np.linalg.pinv."""
+    c = _tiny_cfg(P)
+    W, b, _, _ = O.init_hidden(c)
+    K, B, A, F = _global_blocks(c, W, b)
+    assert np.linalg.cond(K) < 1e8
+    Kp = np.linalg.pinv(K)
+    I = np.eye(K.shape[0])
+    Op = I + Kp.T @ A.T @ A @ Kp - K @ Kp
+    M_lit = B.T @ Op @ B
+    g_lit = B.T @ Op @ F
+    r = O.solve(c, W, b, want_system=True)
+    assert np.abs(r["M"] - M_lit).max() <= 1e-10 * np.abs(M_lit).max()
+    assert np.abs(r["g"] - g_lit).max() <= 1e-10 * np.abs(g_lit).max()
+    assert np.array_equal(r["M"], r["M"].T) or np.abs(r["M"] - r["M"].T).max() < 1e-14 * np.abs(r["M"]).max()
+    assert np.linalg.eigvalsh(r["M"]).min() > 0      # SPD
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_schur_solution_equals_monolithic_lstsq_of_eliminated_system(P):
+    """Central equivalence: (c, u_Gamma) of the Schur route == the least-squares solution of the
+    monolithic eqn:eliminated system [[K, B], [0, -AK^+B]] [c; u] = [F; -AK^+F]."""
+    c = _tiny_cfg(P)
+    W, b, _, _ = O.init_hidden(c)
+    K, B, A, F = _global_blocks(c, W, b)
+    Kp = np.linalg.pinv(K)
+    top = np.hstack([K, B])
+    bot = np.hstack([np.zeros((A.shape[0], K.shape[1])), -A @ Kp @ B])
+    sol = np.linalg.lstsq(np.vstack([top, bot]), np.concatenate([F, -A @ Kp @ F]), rcond=None)[0]
+    n = K.shape[1]
+    r = O.solve(c, W, b)
+    assert np.allclose(r["uG"], sol[n:], rtol=0, atol=1e-8 * np.abs(sol[n:]).max())
+    assert np.allclose(r["coef"].ravel(), sol[:n], rtol=0, atol=1e-8 * np.abs(sol[:n]).max())
+    # ... and it is NOT the LS solution of the uneliminated eqn:nonoverlap_discrete (reading R10)
+    full = np.vstack([np.hstack([K, B]), np.hstack([A, np.zeros((A.shape[0], B.shape[1]))])])
+    sol2 = np.linalg.lstsq(full, np.concatenate([F, np.zeros(A.shape[0])]), rcond=None)[0]
+    assert np.abs(sol2[n:] - sol[n:]).max() > 1e-6 * np.abs(sol[n:]).max()
+
+
+def test_single_subdomain_is_classical_elm():
+    """P = 1: no interface (G = 0) and c = argmin ||K c - F||."""
+    c = mkcfg(P=1, M=30, p=12, q=8, problem=4, seed=9, init_c=0.125)
+    W, b, _, _ = O.init_hidden(c)
+    K, F, _ = O.assemble(c, 0, W, b)
+    assert O.geometry(c)["G"] == 0
+    r = O.solve(c, W, b)
+    ref = np.linalg.lstsq(K, F, rcond=None)[0]
+    assert np.allclose(K @ r["coef"][0], K @ ref, rtol=0, atol=1e-10 * np.abs(F).max())
+    assert abs(r["resid"][0] - np.linalg.norm(K @ ref - F)) < 1e-10 * np.linalg.norm(F)
+
+
+def test_homogeneous_problem_gives_zero():
+    c = mkcfg(P=3, M=20, p=6, q=5, problem=5)
+    W, b, _, _ = O.init_hidden(c)
+    r = O.solve(c, W, b, WL.eval_grid(11))
+    assert np.all(r["uG"] == 0) and np.all(r["coef"] == 0) and np.all(r["u"] == 0)
+
+
+# ------------------------------------------------------------------------------------------------
+# properties of the solution at a BASELINE geometry
+# ------------------------------------------------------------------------------------------------
+def _u_local(W, b, coef, s, pts):
+    w = W[s]
+    return np.tanh(pts @ w.T + b[s]) @ coef[s]
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_interface_continuity_bound(k):
+    """|u_s(x_k) - u_Gamma,k| <= r_s (value row of the local residual), hence
+    |u_s - u_t| <= r_s + r_t at every interface point."""
+    c = mkcfg(k)
+    W, b, _, _ = O.init_hidden(c)
+    r = O.solve(c, W, b, want_system=True)
+    N = O.geometry(c)["N"]
+    vals = {}
+    for s in range(N):
+        xy, edge, gidx = O.rows(c, s)
+        sel = gidx >= 0
+        us = _u_local(W, b, r["coef"], s, xy[sel])
+        dev = np.abs(us - r["uG"][gidx[sel]])
+        assert np.all(dev <= r["resid"][s] * (1 + 1e-6) + 1e-13)
+        for gi, v in zip(gidx[sel], us):
+            vals.setdefault(int(gi), []).append((s, v))
+    for gi, lst in vals.items():
+        (s1, v1), (s2, v2) = lst
+        assert abs(v1 - v2) <= (r["resid"][s1] + r["resid"][s2]) * (1 + 1e-6) + 1e-13
+    # the interface system is solved to rounding (eqn:schur)
+    M, g, u = r["M"], r["g"], r["uG"]
+    assert np.linalg.norm(M @ u - g) <= 1e-12 * np.linalg.norm(g)
+
+
+def test_error_falls_as_neurons_are_added():
+    """Reading R21 ladder at config-0 geometry (P:75 observation, valid while M << m)."""
+    errs = []
+    xy = WL.eval_grid(41)
+    ue = WL.exact(0, xy)
+    for M in [8, 16, 32, 64, 128]:
+        c = mkcfg(0, M=M)
+        W, b, _, _ = O.init_hidden(c)
+        r = O.solve(c, W, b, xy)
+        errs.append(np.linalg.norm(r["u"] - ue) / np.linalg.norm(ue))
+    assert all(e2 < e1 for e1, e2 in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-6
+
+
+def test_config1_accuracy_vs_exact():
+    """Config 1 reaches rounding-level accuracy vs the exact solution (SURVEY scratch 2.5e-13);
+    this fails if the flux term is formed as A (K^+ B) column by column (reading R23)."""
+    c = mkcfg(1)
+    W, b, _, _ = O.init_hidden(c)
+    xy = WL.eval_grid()
+    r = O.solve(c, W, b, xy)
+    ue = WL.exact(0, xy)
+    assert np.linalg.norm(r["u"] - ue) / np.linalg.norm(ue) < 1e-10

@@ -1,0 +1,55 @@
+"""Seeded synthetic workloads shared by tests, bench.py and smoke().
+
+Holds none of the method's arithmetic: only the five BASELINE.json configurations (restated in
+SURVEY.md §8(d)), a few small test geometries, and the 101 x 101 evaluation grid (reading R15,
+x_i = i / 100).  The random numbers the method draws are generated inside each implementation by
+the same counter-based generator (reading R9), not here.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# problem ids: 0 sin(pi x) sin(pi y) | 1 e^{x+y} sin(2 pi x) cos(2 pi y) | 2 sin(4 pi x) sin(4 pi y)
+#              3 sin(8 pi x) sin(8 pi y) | 4 sin(2 pi x) e^y (paper Table 2) | 5 u = 0
+CONFIGS = [
+    dict(name="cfg0", P=2, M=64, p=16, q=16, problem=0, seed=0),
+    dict(name="cfg1", P=4, M=400, p=30, q=40, problem=0, seed=1),
+    dict(name="cfg2", P=8, M=1000, p=40, q=60, problem=1, seed=2),
+    dict(name="cfg3", P=16, M=1600, p=50, q=80, problem=2, seed=3),
+    dict(name="cfg4", P=32, M=1024, p=40, q=64, problem=3, seed=4),
+]
+
+# the bench workload: config 3 (16 x 16 subdomains, 2820 x 1600 local LS, ~9 GB of local
+# matrices) -- the largest local least-squares problem of BASELINE.json that fits one B200.
+BENCH_CONFIG = 3
+
+
+def config(k: int, **over) -> dict:
+    c = dict(CONFIGS[k])
+    c.update(init_scheme=0, init_c=0.125, r_over_diam=0.5)
+    c.update(over)
+    return c
+
+
+def eval_grid(n: int = 101) -> np.ndarray:
+    """(n*n, 2) points x_i = i/(n-1), y-major (row j, column i)."""
+    t = np.arange(n, dtype=np.float64) / float(n - 1)
+    X, Y = np.meshgrid(t, t, indexing="xy")
+    return np.stack([X.ravel(), Y.ravel()], axis=1)
+
+
+def exact(problem: int, xy: np.ndarray) -> np.ndarray:
+    """Manufactured exact solutions (the configs' stated u) for error-vs-exact reporting."""
+    x, y = xy[:, 0], xy[:, 1]
+    pi = np.pi
+    if problem == 0:
+        return np.sin(pi * x) * np.sin(pi * y)
+    if problem == 1:
+        return np.exp(x + y) * np.sin(2 * pi * x) * np.cos(2 * pi * y)
+    if problem == 2:
+        return np.sin(4 * pi * x) * np.sin(4 * pi * y)
+    if problem == 3:
+        return np.sin(8 * pi * x) * np.sin(8 * pi * y)
+    if problem == 4:
+        return np.sin(2 * pi * x) * np.exp(y)
+    return np.zeros_like(x)
