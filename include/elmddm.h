@@ -1,0 +1,164 @@
+/*
+ * elmddm.h -- C ABI of the B200-native DDM-ELM hot path
+ * (arxiv 2406.15959: "nonoverlapping domain decomposition for extreme learning machines").
+ *
+ * The calls follow Algorithm 1:
+ *     Set theta^s randomly                     -> elmddm_init_hidden   (eqn:init)
+ *     for s in parallel: construct K,A,B,F     -> elmddm_assemble      (eqn:nonoverlap_discrete)
+ *     [factor every local LS]                  -> elmddm_local_factor  (K^+ of P:356 via Householder QR)
+ *     [eliminate c into the Schur system]      -> elmddm_schur_accumulate  (eqn:eliminated..eqn:schur)
+ *     Solve eqn:schur for u_Gamma              -> elmddm_interface_assemble + elmddm_interface_factor_solve
+ *                                                 (= elmddm_interface_solve)
+ *     for s in parallel: solve for c^s         -> elmddm_back_solve
+ *     [evaluate the solution]                  -> elmddm_evaluate      (error tables, e.g. P:593)
+ *
+ * Conventions (DESIGN.md §2 has the full statement):
+ *  - Geometry: (0,1)^2 split into P x P squares, subdomain s = j*P + i (i along x).  Each subdomain
+ *    has p*p interior collocation points and q points on each of its 4 edges (endpoints excluded),
+ *    m = p*p + 4q rows ordered [interior (row-major b, a) | left | right | bottom | top].
+ *  - Interface unknowns u_Gamma: G = 2P(P-1)q, face-major in strip order, points in increasing
+ *    coordinate (elmddm_interface_points exports the coordinates).
+ *  - Every array argument is a DEVICE pointer owned by the caller (e.g. a torch tensor), fp64,
+ *    column-major, 16-byte aligned; the library never allocates or frees caller memory.  Sizes
+ *    and leading dimensions come from elmddm_sizes.  The library owns only its opaque context and
+ *    small internal tables (< a few MB).  Work is enqueued on the given stream; calls return
+ *    after enqueueing (asynchronous) except where stated.
+ *  - A rank owns the contiguous subdomain range [s_begin, s_end); per-subdomain arrays are
+ *    indexed by the local index s - s_begin ("S_local" slots) unless stated "global".
+ *  - Errors: arguments are validated synchronously before any launch (ELMDDM_EINVAL, nothing
+ *    enqueued).  Numerical failures detected on the device (non-positive Cholesky pivot,
+ *    non-finite value) set a device status word, reported by elmddm_sync and by the return of
+ *    elmddm_interface_factor_solve (which synchronises its stream); elmddm_last_error gives text.
+ *  - Threading: one context per device per host thread.
+ */
+#ifndef ELMDDM_H
+#define ELMDDM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ELMDDM_OK = 0,
+    ELMDDM_EINVAL = 1,   /* bad argument / configuration (nothing was enqueued) */
+    ELMDDM_ENUMERIC = 2, /* non-positive pivot or non-finite value detected on the device */
+    ELMDDM_ECUDA = 3,    /* CUDA runtime error (text in elmddm_last_error) */
+    ELMDDM_ENOMEM = 4    /* internal table allocation failed */
+} elmddm_status;
+
+typedef struct elmddm_ctx elmddm_ctx;
+
+typedef struct {
+    int32_t P;              /* subdomains per axis (N = P*P subdomains of side h = 1/P)        */
+    int32_t M;              /* hidden neurons per subdomain, n_N of P:199 (multiple of 8)      */
+    int32_t p;              /* interior collocation points per axis per subdomain              */
+    int32_t q;              /* collocation points per subdomain edge (even)                    */
+    int32_t problem;        /* manufactured solution: 0 sin(pi x)sin(pi y) | 1 e^{x+y}sin(2pi x)cos(2pi y)
+                               | 2 sin(4pi x)sin(4pi y) | 3 sin(8pi x)sin(8pi y) | 4 sin(2pi x)e^y
+                                | 5 u = 0                                                */
+    int32_t init_scheme;    /* 0 paper eqn:init l = c sqrt(N*M) | 1 manual l = 1 | 2 He l = sqrt(2/M), b = 0 */
+    double init_c;          /* c of eqn:init (1/8 for Poisson)                          */
+    double r_over_diam;     /* r = r_over_diam * diam(Omega_s) (1/2)                    */
+    uint64_t seed;          /* counter-based RNG key (reading R9)                    */
+    int32_t s_begin, s_end; /* subdomains owned by this rank: [s_begin, s_end) of 0..N-1       */
+    int32_t interface_mode; /* 0 auto | 1 dense | 2 banded storage of the Schur matrix         */
+    int32_t reserved;
+} elmddm_config;
+
+typedef struct {
+    int64_t N;          /* total subdomains P*P                                               */
+    int64_t S;          /* local subdomains s_end - s_begin                                   */
+    int64_t m;          /* rows of K^s: p*p + 4q                                              */
+    int64_t ld;         /* leading dimension of K_aug (m rounded up to 32; rows m..ld-1 are 0) */
+    int64_t ncols;      /* columns of K_aug: M + 4q + 1  ([K | E_Gamma | F])                  */
+    int64_t kaug;       /* augmented columns 4q + 1                                            */
+    int64_t G;          /* interface unknowns 2P(P-1)q                                         */
+    int64_t faces;      /* interface faces 2P(P-1)                                             */
+    int64_t kaug_elems; /* doubles of K_aug for the S local subdomains: S*ld*ncols            */
+    int64_t at_elems;   /* doubles of At (flux rows, transposed): S*M*4q                      */
+    int64_t tau_elems;  /* S*M                                                                 */
+    int64_t pbuf_ld, pbuf_elems; /* flux Schur block per subdomain: 4q x kaug, ld pbuf_ld; N slots (global) */
+    int64_t sbuf_ld, sbuf_elems; /* Gram block per subdomain: kaug x kaug, ld sbuf_ld; N slots (global) */
+    int64_t work_elems;          /* doubles of the caller-provided work buffer (max over calls)  */
+    int64_t band_ld, band_nbw, band_elems; /* Schur matrix storage, see elmddm_band_index       */
+    int64_t G_pad;                          /* G rounded up to the 64-tile                       */
+    int64_t halfband;                       /* exact half-bandwidth of the Schur matrix          */
+} elmddm_sizes_t;
+
+/* ---- context ------------------------------------------------------------------------------ */
+/* Validates cfg (P>=1, M%8==0, q even, p>=1, m >= M, 0<=s_begin<s_end<=N), builds the geometry
+ * and face tables and uploads them to `device`.  Synchronous.                                 */
+elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** out);
+void elmddm_destroy(elmddm_ctx* ctx);
+const char* elmddm_last_error(const elmddm_ctx* ctx);
+elmddm_status elmddm_sizes(const elmddm_ctx* ctx, elmddm_sizes_t* out);
+/* Waits for `stream` (a cudaStream_t), then reads and clears the device status word.          */
+elmddm_status elmddm_sync(elmddm_ctx* ctx, void* stream);
+/* Host export of the u_Gamma ordering: xy_host[G][2] coordinates of the interface unknowns.   */
+elmddm_status elmddm_interface_points(const elmddm_ctx* ctx, double* xy_host);
+/* Offset of Schur-matrix element (i, j), i >= j, |i-j| <= halfband, in the band storage.     */
+int64_t elmddm_band_index(const elmddm_ctx* ctx, int64_t i, int64_t j);
+
+/* ---- hot path ----------------------------------------------------------------------------- */
+/* eqn:init: W[S][M][2], b[S][M] for the local subdomains; xi[S][M][2] (may be NULL)
+ * receives the sampled centres.  w ~ U([-l,l]^2), xi ~ U(closed r-neighbourhood of Omega_s),
+ * b = -w.xi, bit-identical to the oracle's counter-based draw (reading R9).                   */
+elmddm_status elmddm_init_hidden(elmddm_ctx* ctx, double* W, double* b, double* xi, void* stream);
+
+/* eqn:nonoverlap_discrete, L = -Laplacian:
+ *   Kaug[S][ncols][ld]: columns 0..M-1 = K^s (interior rows -|w|^2 sigma''(z), boundary and
+ *   interface rows sigma(z)); columns M..M+4q-1 = E_Gamma (unit column at each interface row;
+ *   zero column for a Dirichlet edge point; B^s = -E_Gamma); column M+4q = F^s = [f; g; 0];
+ *   rows m..ld-1 = 0.
+ *   At[S][4q][M] = (A^s)^T: flux row e*q+k holds (w_j . n_e) sigma'(z) at edge e point k,
+ *   outward axis normals; zero for Dirichlet edges.                                            */
+elmddm_status elmddm_assemble(elmddm_ctx* ctx, const double* W, const double* b, double* Kaug, double* At,
+                              void* stream);
+
+/* Batched blocked Householder QR (no pivoting) of every K^s, applied to all ncols columns:
+ *   Q^T [K | E_Gamma | F] = [[R11, R12, y], [0, T_E, t_F]]  (in place in Kaug; Householder vectors
+ *   below the diagonal of the first M columns, tau[S][M]).  work: >= work_elems doubles.       */
+elmddm_status elmddm_local_factor(elmddm_ctx* ctx, double* Kaug, double* tau, double* work, void* stream);
+
+/* Elimination of c^s (eqn:eliminated -> eqn:schur), per local subdomain s:
+ *   At <- R11^{-T} At (so At^T = W_s = A^s R11^{-1}, the flux operator A^s K^{s+} restricted to
+ *   range(Q_1));  Pbuf[s] = W_s [R12 | y]  (4q x kaug: flux of c^s(u) = q_s + P_s u_s);
+ *   Sbuf[s] = [T_E | t_F]^T [T_E | t_F]   (kaug x kaug Gram).
+ * Pbuf and Sbuf are GLOBAL (N slots); only slots [s_begin, s_end) are written, so a sum over
+ * ranks of zero-filled buffers is their exact union (the NCCL reduce of DESIGN.md §6).        */
+elmddm_status elmddm_schur_accumulate(elmddm_ctx* ctx, double* Kaug, double* At, double* Pbuf, double* Sbuf,
+                                      double* work, void* stream);
+
+/* Rank-0 interface system (eqn:schur) from the global Pbuf/Sbuf:
+ *   M = sum_s scatter(T_E^T T_E) + Q^T Q,  g = -sum_s scatter(T_E^T t_F) - Q^T q,
+ *   Q = sum_s scatter(P_s), q = sum_s scatter(q_s)   (reading R13; fixed summation order).
+ * Writes Mband (band_elems doubles, lower band, see elmddm_band_index; padding diagonal = 1)
+ * and g[G_pad].  work: >= work_elems doubles.                                                 */
+elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
+                                        double* g, double* work, void* stream);
+/* Cholesky M = L L^T in place (band-limited, tiles of 64) and u = M^{-1} g into uG[G_pad].
+ * Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot.                     */
+elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
+                                            double* work, void* stream);
+/* = interface_assemble + interface_factor_solve. */
+elmddm_status elmddm_interface_solve(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
+                                     double* g, double* uG, double* work, void* stream);
+
+/* Local back-solve (Alg. 1) with the global uG[G]:
+ *   u_s = uG at s's interface points (0 on Dirichlet edges);
+ *   coef[S][M] = R11^{-1} (y + R12 u_s);  resid[S] = || t_F + T_E u_s ||_2.                     */
+elmddm_status elmddm_back_solve(elmddm_ctx* ctx, const double* Kaug, const double* uG, double* coef,
+                                double* resid, double* work, void* stream);
+
+/* u(x) = sum_j c_j^s tanh(w_j^s . x + b_j^s) with s = owner of x (column min(floor(xP), P-1),
+ * same for y; reading R15) for points xy[n][2] owned by this rank; other u[i] are left as is. */
+elmddm_status elmddm_evaluate(elmddm_ctx* ctx, const double* W, const double* b, const double* coef,
+                              const double* xy, int64_t n, double* u, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELMDDM_H */

@@ -1,0 +1,322 @@
+// assemble.cu -- hidden-layer initialisation (eqn:init), collocation assembly
+// (eqn:nonoverlap_discrete) and solution evaluation, for sm_100a.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// ---- counter-based RNG (reading R9) ---------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+// uniform double in [0,1) keyed by (seed, subdomain, neuron, draw number)
+__device__ __forceinline__ double uniform01(uint64_t key, int s, int j, int d) {
+    uint64_t ctr = ((uint64_t)(uint32_t)s << 40) ^ ((uint64_t)(uint32_t)j << 16) ^ (uint64_t)(uint32_t)d;
+    uint64_t x = mix64(ctr + key);
+    return __dmul_rn(__ull2double_rn(x >> 11), 0x1.0p-53);
+}
+
+constexpr int kMaxCollarTries = 1000;
+
+// eqn:init.  Every floating-point step is an explicitly rounded IEEE op so that the
+// draw is bit-identical to any other implementation of the same recipe (no FMA contraction).
+__global__ void k_init_hidden(elmddm_config cfg, double* __restrict__ W, double* __restrict__ b,
+                              double* __restrict__ xi) {
+    const int P = cfg.P, M = cfg.M, N = P * P;
+    const int S = cfg.s_end - cfg.s_begin;
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)S * M) return;
+    const int sl = (int)(t / M), n = (int)(t % M);
+    const int s = cfg.s_begin + sl;
+    const int i = s % P, j = s / P;
+    const uint64_t key = mix64(cfg.seed + 0x9E3779B97F4A7C15ULL);
+    const double h = 1.0 / (double)P;
+    double l;
+    if (cfg.init_scheme == 0) l = __dmul_rn(cfg.init_c, sqrt(__dmul_rn((double)N, (double)M)));
+    else if (cfg.init_scheme == 1) l = 1.0;
+    else l = sqrt(2.0 / (double)M);
+    const double r = __dmul_rn(cfg.r_over_diam, __dmul_rn(sqrt(2.0), h));
+    const double r2 = __dmul_rn(r, r);
+    const double span = __dadd_rn(h, __dmul_rn(2.0, r));
+    const double x0 = (double)i / (double)P, y0 = (double)j / (double)P;
+    const double x1 = (double)(i + 1) / (double)P, y1 = (double)(j + 1) / (double)P;
+    const double lox = __dsub_rn(x0, r), loy = __dsub_rn(y0, r);
+    const double wx = __dmul_rn(__dsub_rn(__dmul_rn(2.0, uniform01(key, s, n, 0)), 1.0), l);
+    const double wy = __dmul_rn(__dsub_rn(__dmul_rn(2.0, uniform01(key, s, n, 1)), 1.0), l);
+    double ex = __dmul_rn(0.5, __dadd_rn(x0, x1)), ey = __dmul_rn(0.5, __dadd_rn(y0, y1));
+    if (cfg.init_scheme != 2) {
+        for (int tr = 0; tr < kMaxCollarTries; ++tr) {
+            double px = __dadd_rn(lox, __dmul_rn(uniform01(key, s, n, 2 + 2 * tr), span));
+            double py = __dadd_rn(loy, __dmul_rn(uniform01(key, s, n, 3 + 2 * tr), span));
+            double dx = fmax(fmax(__dsub_rn(x0, px), __dsub_rn(px, x1)), 0.0);
+            double dy = fmax(fmax(__dsub_rn(y0, py), __dsub_rn(py, y1)), 0.0);
+            if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= r2) {
+                ex = px;
+                ey = py;
+                break;
+            }
+        }
+    }
+    W[2 * t] = wx;
+    W[2 * t + 1] = wy;
+    b[t] = cfg.init_scheme == 2 ? 0.0 : -__dadd_rn(__dmul_rn(wx, ex), __dmul_rn(wy, ey));
+    if (xi) {
+        xi[2 * t] = ex;
+        xi[2 * t + 1] = ey;
+    }
+}
+
+// ---- manufactured problems -----------------------------------------------------
+__device__ void problem_uf(int pid, double x, double y, double& u, double& f) {
+    switch (pid) {
+        case 0: {
+            double s = sin(kPi * x) * sin(kPi * y);
+            u = s;
+            f = 2.0 * kPi * kPi * s;
+        } break;
+        case 1: {
+            double E = exp(x + y);
+            double sx, cx, sy, cy;
+            sincos(2.0 * kPi * x, &sx, &cx);
+            sincos(2.0 * kPi * y, &sy, &cy);
+            u = E * sx * cy;
+            f = -E * (2.0 * (1.0 - 4.0 * kPi * kPi) * sx * cy + 4.0 * kPi * (cx * cy - sx * sy));
+        } break;
+        case 2: {
+            double s = sin(4.0 * kPi * x) * sin(4.0 * kPi * y);
+            u = s;
+            f = 32.0 * kPi * kPi * s;
+        } break;
+        case 3: {
+            double s = sin(8.0 * kPi * x) * sin(8.0 * kPi * y);
+            u = s;
+            f = 128.0 * kPi * kPi * s;
+        } break;
+        case 4: {
+            double s = sin(2.0 * kPi * x) * exp(y);
+            u = s;
+            f = (4.0 * kPi * kPi - 1.0) * s;
+        } break;
+        default:
+            u = 0.0;
+            f = 0.0;
+    }
+}
+
+// Collocation point of row r of subdomain (i, j); kind = -1 interior, 0..3 edge, -2 padding.
+// Each coordinate is one correctly rounded division of integers (shared face points are
+// bit-identical in both neighbours).
+__device__ __forceinline__ void row_point(const elmddm_config& c, int i, int j, int r, double& x, double& y,
+                                          int& kind, int& k) {
+    const int P = c.P, p = c.p, q = c.q, pp = p * p;
+    if (r < pp) {
+        int a = r % p, bb = r / p;
+        double den = (double)(P * (p + 1));
+        x = (double)(i * (p + 1) + a + 1) / den;
+        y = (double)(j * (p + 1) + bb + 1) / den;
+        kind = -1;
+        k = 0;
+        return;
+    }
+    r -= pp;
+    if (r >= 4 * q) {
+        kind = -2;
+        x = y = 0.0;
+        k = 0;
+        return;
+    }
+    int e = r / q;
+    k = r % q;
+    kind = e;
+    double den = (double)(P * (q + 1));
+    double ty = (double)(j * (q + 1) + k + 1) / den;
+    double tx = (double)(i * (q + 1) + k + 1) / den;
+    switch (e) {
+        case 0: x = (double)i / (double)P; y = ty; break;
+        case 1: x = (double)(i + 1) / (double)P; y = ty; break;
+        case 2: x = tx; y = (double)j / (double)P; break;
+        default: x = tx; y = (double)(j + 1) / (double)P; break;
+    }
+}
+
+__device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
+    switch (e) {
+        case 0: return i > 0;
+        case 1: return i < P - 1;
+        case 2: return j > 0;
+        default: return j < P - 1;
+    }
+}
+
+// tanh and its derivatives sigma' = 1 - sigma^2 written as 4E/(1+E)^2 (no cancellation),
+// sigma'' = -2 sigma sigma', from E = exp(2z) with |z| bounded (clamped at 40: tanh == +-1).
+__device__ __forceinline__ void tanh_derivs(double z, double& s0, double& s1, double& s2) {
+    double za = fmin(fabs(z), 40.0);
+    double E = exp(-2.0 * za);             // in (0, 1]
+    double d = 1.0 / (1.0 + E);
+    double t = (1.0 - E) * d;               // tanh |z|
+    s0 = copysign(t, z);
+    s1 = 4.0 * E * d * d;                   // sech^2
+    s2 = -2.0 * s0 * s1;
+}
+
+constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
+constexpr int AS_NT = 256;
+
+// Kaug[s][col][row]: grid (ceil(ncols / AS_COLS), S).
+__global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
+                                                    const double* __restrict__ W, const double* __restrict__ b,
+                                                    double* __restrict__ Kaug) {
+    const int M = cfg.M, q = cfg.q, P = cfg.P, pp = cfg.p * cfg.p;
+    const int m = pp + 4 * q;
+    const int sl = blockIdx.y, s = cfg.s_begin + sl;
+    const int i = s % P, j = s / P;
+    const int c0 = blockIdx.x * AS_COLS;
+    double* Ks = Kaug + (int64_t)sl * ld * ncols;
+    __shared__ double sw[AS_COLS][3];
+    if (threadIdx.x < AS_COLS) {
+        int col = c0 + threadIdx.x;
+        if (col < M) {
+            sw[threadIdx.x][0] = W[((int64_t)sl * M + col) * 2];
+            sw[threadIdx.x][1] = W[((int64_t)sl * M + col) * 2 + 1];
+            sw[threadIdx.x][2] = b[(int64_t)sl * M + col];
+        }
+    }
+    __syncthreads();
+    if (c0 < M) {
+        // neuron columns: interior rows -|w|^2 sigma'', boundary / interface rows sigma
+        for (int r = threadIdx.x; r < ld; r += AS_NT) {
+            double x = 0.0, y = 0.0;
+            int kind = -2, k = 0;
+            if (r < m) row_point(cfg, i, j, r, x, y, kind, k);
+#pragma unroll
+            for (int cc = 0; cc < AS_COLS; ++cc) {
+                const int col = c0 + cc;
+                if (col >= M) break;
+                double v = 0.0;
+                if (kind != -2) {
+                    double wx = sw[cc][0], wy = sw[cc][1];
+                    double z = wx * x + wy * y + sw[cc][2];
+                    double s0, s1, s2;
+                    tanh_derivs(z, s0, s1, s2);
+                    v = (kind == -1) ? -(wx * wx + wy * wy) * s2 : s0;
+                }
+                Ks[(int64_t)col * ld + r] = v;
+            }
+        }
+        return;
+    }
+    // augmented columns: E_Gamma (unit interface columns) and F = [f; g; 0]
+    for (int cc = 0; cc < AS_COLS; ++cc) {
+        const int col = c0 + cc;
+        if (col >= ncols) break;
+        if (col < M + 4 * q) {
+            const int t = col - M;
+            const bool iface = edge_is_interface(P, i, j, t / q);
+            for (int r = threadIdx.x; r < ld; r += AS_NT)
+                Ks[(int64_t)col * ld + r] = (iface && r == pp + t) ? 1.0 : 0.0;
+        } else {
+            for (int r = threadIdx.x; r < ld; r += AS_NT) {
+                double v = 0.0;
+                if (r < m) {
+                    double x, y, u, f;
+                    int kind, k;
+                    row_point(cfg, i, j, r, x, y, kind, k);
+                    if (kind == -1) {
+                        problem_uf(cfg.problem, x, y, u, f);
+                        v = f;
+                    } else if (!edge_is_interface(P, i, j, kind)) {
+                        problem_uf(cfg.problem, x, y, u, f);
+                        v = u;
+                    }
+                }
+                Ks[(int64_t)col * ld + r] = v;
+            }
+        }
+    }
+}
+
+// At[s][t][j] (t = e*q + k flux row, j neuron fastest): grid (4, S), threads over j.
+__global__ void __launch_bounds__(AS_NT) k_assemble_at(elmddm_config cfg, const double* __restrict__ W,
+                                                       const double* __restrict__ b, double* __restrict__ At) {
+    const int M = cfg.M, q = cfg.q, P = cfg.P, pp = cfg.p * cfg.p;
+    const int e = blockIdx.x, sl = blockIdx.y, s = cfg.s_begin + sl;
+    const int i = s % P, j = s / P;
+    const bool iface = edge_is_interface(P, i, j, e);
+    const double nx = e == 0 ? -1.0 : (e == 1 ? 1.0 : 0.0);
+    const double ny = e == 2 ? -1.0 : (e == 3 ? 1.0 : 0.0);
+    double* A = At + (int64_t)sl * M * 4 * q;
+    for (int k = 0; k < q; ++k) {
+        double x, y;
+        int kind, kk;
+        row_point(cfg, i, j, pp + e * q + k, x, y, kind, kk);
+        double* Arow = A + (int64_t)(e * q + k) * M;
+        for (int n = threadIdx.x; n < M; n += AS_NT) {
+            double v = 0.0;
+            if (iface) {
+                double wx = W[((int64_t)sl * M + n) * 2], wy = W[((int64_t)sl * M + n) * 2 + 1];
+                double z = wx * x + wy * y + b[(int64_t)sl * M + n];
+                double s0, s1, s2;
+                tanh_derivs(z, s0, s1, s2);
+                v = (wx * nx + wy * ny) * s1;
+            }
+            Arow[n] = v;
+        }
+    }
+}
+
+__global__ void k_evaluate(elmddm_config cfg, const double* __restrict__ W, const double* __restrict__ b,
+                           const double* __restrict__ coef, const double* __restrict__ xy, int64_t n,
+                           double* __restrict__ u) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int P = cfg.P, M = cfg.M;
+    double x = xy[2 * t], y = xy[2 * t + 1];
+    int i = (int)floor(x * (double)P), j = (int)floor(y * (double)P);
+    i = min(max(i, 0), P - 1);
+    j = min(max(j, 0), P - 1);
+    int s = j * P + i;
+    if (s < cfg.s_begin || s >= cfg.s_end) return;
+    int sl = s - cfg.s_begin;
+    const double* Ws = W + (int64_t)sl * M * 2;
+    const double* bs = b + (int64_t)sl * M;
+    const double* cs = coef + (int64_t)sl * M;
+    double acc = 0.0;
+    for (int k = 0; k < M; ++k) acc += cs[k] * tanh(Ws[2 * k] * x + Ws[2 * k + 1] * y + bs[k]);
+    u[t] = acc;
+}
+
+}  // namespace
+
+cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double* xi, cudaStream_t st) {
+    int64_t n = c->sz.S * c->cfg.M;
+    int nt = 128;
+    k_init_hidden<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, xi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
+                            cudaStream_t st) {
+    dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
+    k_assemble<<<g1, AS_NT, 0, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 g2(4, (unsigned)c->sz.S);
+    k_assemble_at<<<g2, AS_NT, 0, st>>>(c->cfg, W, b, At);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_evaluate(const elmddm_ctx* c, const double* W, const double* b, const double* coef,
+                            const double* xy, int64_t n, double* u, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int nt = 128;
+    k_evaluate<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, coef, xy, n, u);
+    return cudaGetLastError();
+}

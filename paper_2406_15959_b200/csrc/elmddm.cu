@@ -1,0 +1,464 @@
+// elmddm.cu -- the C ABI (include/elmddm.h): context, geometry / face tables, argument
+// validation, error reporting and the per-call launch sequences.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+bool set_err(elmddm_ctx* c, const std::string& s) {
+    if (c) c->err = s;
+    return false;
+}
+
+elmddm_status cuda_fail(elmddm_ctx* c, cudaError_t e, const char* where) {
+    if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return ELMDDM_ECUDA;
+}
+
+// face of edge e (0 L, 1 R, 2 B, 3 T) of subdomain (i, j); strip order (reading R14):
+// strip j = [V(0..P-2, j) | H(0..P-1, j)], V between (i,j)-(i+1,j), H between (i,j)-(i,j+1).
+int face_id(int P, int i, int j, int e) {
+    const int strip = 2 * P - 1;
+    if (e == 0) return i > 0 ? j * strip + (i - 1) : -1;
+    if (e == 1) return i < P - 1 ? j * strip + i : -1;
+    if (e == 2) return j > 0 ? (j - 1) * strip + (P - 1) + i : -1;
+    return j < P - 1 ? j * strip + (P - 1) + i : -1;
+}
+
+template <typename T>
+cudaError_t upload(T** dptr, const std::vector<T>& v) {
+    size_t n = std::max<size_t>(v.size(), 1);
+    cudaError_t e = cudaMalloc((void**)dptr, n * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (!v.empty()) e = cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+bool validate(const elmddm_config* cfg, std::string& why) {
+    if (!cfg) return why = "null config", false;
+    if (cfg->P < 1 || cfg->P > 1024) return why = "P out of range", false;
+    if (cfg->M < 8 || cfg->M % 8 != 0) return why = "M must be a positive multiple of 8", false;
+    if (cfg->p < 1) return why = "p must be >= 1", false;
+    if (cfg->q < 2 || cfg->q % 2 != 0) return why = "q must be even and >= 2", false;
+    int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
+    if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
+    if (round_up(m, 32) > 3400) return why = "m too large for the shared-memory panel (ld <= 3400)", false;
+    if (cfg->problem < 0 || cfg->problem > 5) return why = "unknown problem id", false;
+    if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
+    if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
+    int64_t N = (int64_t)cfg->P * cfg->P;
+    if (cfg->s_begin < 0 || cfg->s_end > N || cfg->s_begin >= cfg->s_end) return why = "bad [s_begin, s_end)", false;
+    if (cfg->interface_mode < 0 || cfg->interface_mode > 2) return why = "bad interface_mode", false;
+    if (cfg->q > 256) return why = "q too large", false;
+    return true;
+}
+
+elmddm_status build_tables(elmddm_ctx* c) {
+    const int P = c->cfg.P, q = c->cfg.q, N = P * P;
+    const int F = 2 * P * (P - 1);
+    c->faces = F;
+    c->sub_face.assign((size_t)N * 4, -1);
+    c->face_sub.assign((size_t)F * 2, -1);
+    c->face_edge.assign((size_t)F * 2, -1);
+    for (int s = 0; s < N; ++s) {
+        int i = s % P, j = s / P;
+        for (int e = 0; e < 4; ++e) {
+            int f = face_id(P, i, j, e);
+            c->sub_face[s * 4 + e] = f;
+            if (f < 0) continue;
+            // slot 0 = left/lower subdomain (edges R or T), slot 1 = right/upper (edges L or B)
+            int slot = (e == 1 || e == 3) ? 0 : 1;
+            c->face_sub[f * 2 + slot] = s;
+            c->face_edge[f * 2 + slot] = e;
+        }
+    }
+    // neighbour slots of each flux face a: [a, other faces of sub 0, other faces of sub 1]
+    c->nbr.assign((size_t)F * 7, -1);
+    std::vector<int> qsrc((size_t)F * 8 * 6, -1);
+    for (int a = 0; a < F; ++a) {
+        int n = 0;
+        c->nbr[a * 7 + n++] = a;
+        for (int k = 0; k < 2; ++k) {
+            int s = c->face_sub[a * 2 + k];
+            for (int e = 0; e < 4; ++e) {
+                int f = c->sub_face[s * 4 + e];
+                if (f < 0 || f == a) continue;
+                c->nbr[a * 7 + n++] = f;
+            }
+        }
+        for (int t = 0; t < 8; ++t) {
+            for (int k = 0; k < 2; ++k) {
+                int s = c->face_sub[a * 2 + k];
+                int er = c->face_edge[a * 2 + k];
+                int ec = -1;
+                if (t < 7) {
+                    int b = c->nbr[a * 7 + t];
+                    if (b < 0) continue;
+                    for (int e = 0; e < 4; ++e)
+                        if (c->sub_face[s * 4 + e] == b) ec = e;
+                    if (ec < 0) continue;
+                } else {
+                    ec = 4;
+                }
+                int* d = &qsrc[((size_t)a * 8 + t) * 6 + k * 3];
+                d[0] = s;
+                d[1] = er;
+                d[2] = ec;
+            }
+        }
+    }
+    // face-block pattern of M (b >= c) and its contributions, in a fixed order
+    std::map<std::pair<int, int>, std::vector<FaceTerm>> pairs;
+    for (int s = 0; s < N; ++s)
+        for (int e1 = 0; e1 < 4; ++e1)
+            for (int e2 = 0; e2 < 4; ++e2) {
+                int b = c->sub_face[s * 4 + e1], cc = c->sub_face[s * 4 + e2];
+                if (b < 0 || cc < 0 || b < cc) continue;
+                pairs[{b, cc}].push_back(FaceTerm{0, s, e1 * q, e2 * q});
+            }
+    for (int a = 0; a < F; ++a)
+        for (int t1 = 0; t1 < 7; ++t1)
+            for (int t2 = 0; t2 < 7; ++t2) {
+                int b = c->nbr[a * 7 + t1], cc = c->nbr[a * 7 + t2];
+                if (b < 0 || cc < 0 || b < cc) continue;
+                pairs[{b, cc}].push_back(FaceTerm{1, a, t1 * q, t2 * q});
+            }
+    std::vector<int> pptr, pbc;
+    std::vector<FaceTerm> terms;
+    int64_t hb = 0;
+    pptr.push_back(0);
+    for (auto& kv : pairs) {
+        pbc.push_back(kv.first.first);
+        pbc.push_back(kv.first.second);
+        for (auto& t : kv.second) terms.push_back(t);
+        pptr.push_back((int)terms.size());
+        hb = std::max<int64_t>(hb, (int64_t)(kv.first.first - kv.first.second) * q + q - 1);
+    }
+    c->npairs = (int)pairs.size();
+    c->nterms = (int)terms.size();
+    // g terms per face b
+    std::vector<int> gptr(1, 0);
+    std::vector<FaceTerm> gterms;
+    for (int b = 0; b < F; ++b) {
+        for (int k = 0; k < 2; ++k) {
+            int s = c->face_sub[b * 2 + k];
+            if (s < 0) continue;
+        }
+        // ascending s
+        int s0 = c->face_sub[b * 2 + 0], s1 = c->face_sub[b * 2 + 1];
+        int sa = std::min(s0, s1), sb = std::max(s0, s1);
+        for (int s : {sa, sb}) {
+            int eb = -1;
+            for (int e = 0; e < 4; ++e)
+                if (c->sub_face[s * 4 + e] == b) eb = e;
+            gterms.push_back(FaceTerm{0, s, eb * q, 4 * q});
+        }
+        for (int a = 0; a < F; ++a) {
+            // only faces within reach can contain b; scan the 7 slots
+            for (int t = 0; t < 7; ++t)
+                if (c->nbr[a * 7 + t] == b) gterms.push_back(FaceTerm{1, a, t * q, 7 * q});
+        }
+        gptr.push_back((int)gterms.size());
+    }
+    c->ngterms = (int)gterms.size();
+
+    const int64_t G = (int64_t)F * q;
+    c->sz.G = G;
+    c->sz.faces = F;
+    c->sz.G_pad = round_up(std::max<int64_t>(G, 1), ELM_NB);
+    c->sz.halfband = F > 0 ? hb : 0;
+    const int64_t nblk = c->sz.G_pad / ELM_NB;
+    int64_t nbw = (c->sz.halfband + ELM_NB - 1) / ELM_NB;
+    int64_t LD = (nbw + 2) * ELM_NB;
+    bool dense = c->cfg.interface_mode == 1 || (c->cfg.interface_mode == 0 && LD >= c->sz.G_pad);
+    if (dense || nbw >= nblk - 1) {
+        nbw = nblk - 1;
+        LD = c->sz.G_pad;
+    }
+    c->sz.band_nbw = nbw;
+    c->sz.band_ld = LD;
+    c->sz.band_elems = c->sz.G_pad * LD + (dense ? 0 : 0);
+    if (!dense) c->sz.band_elems = (c->sz.G_pad - 1) + (c->sz.G_pad - 1) * LD + 1;
+
+    c->qrow_ld = q;
+    c->qrow_cols = 7 * q + 1;
+    c->ga_ld = 7 * q + 2;
+
+    cudaError_t e;
+    if ((e = upload(&c->d_sub_face, c->sub_face)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_qsrc, qsrc)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_pair_ptr, pptr)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_pair_bc, pbc)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_terms, terms)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_gterm_ptr, gptr)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_gterms, gterms)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    return ELMDDM_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define CHECK_CTX(c)                   \
+    do {                               \
+        if (!(c)) return ELMDDM_EINVAL; \
+    } while (0)
+#define CHECK_PTR(c, p)                                                                         \
+    do {                                                                                        \
+        if (!(p) || ((uintptr_t)(p) & 15)) {                                                    \
+            (c)->err = std::string("null or misaligned (needs 16 B) pointer argument: ") + #p; \
+            return ELMDDM_EINVAL;                                                               \
+        }                                                                                       \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** out) {
+    if (!out) return ELMDDM_EINVAL;
+    *out = nullptr;
+    std::string why;
+    if (!validate(cfg, why)) return ELMDDM_EINVAL;
+    elmddm_ctx* c = new (std::nothrow) elmddm_ctx();
+    if (!c) return ELMDDM_ENOMEM;
+    c->cfg = *cfg;
+    c->device = device;
+    DeviceGuard dg(device);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete c;
+        return ELMDDM_ECUDA;
+    }
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) c->nsm = nsm;
+    elmddm_sizes_t& z = c->sz;
+    std::memset(&z, 0, sizeof(z));
+    const int64_t P = cfg->P, M = cfg->M, q = cfg->q;
+    z.N = P * P;
+    z.S = cfg->s_end - cfg->s_begin;
+    z.m = (int64_t)cfg->p * cfg->p + 4 * q;
+    z.ld = round_up(z.m, 32);
+    z.kaug = 4 * q + 1;
+    z.ncols = M + z.kaug;
+    z.kaug_elems = z.S * z.ld * z.ncols;
+    z.at_elems = z.S * M * 4 * q;
+    z.tau_elems = z.S * M;
+    z.pbuf_ld = 4 * q;
+    z.pbuf_elems = z.N * z.pbuf_ld * z.kaug;
+    z.sbuf_ld = z.kaug + 1;
+    z.sbuf_elems = z.N * z.sbuf_ld * z.kaug;
+    elmddm_status st = build_tables(c);
+    if (st != ELMDDM_OK) {
+        elmddm_destroy(c);
+        return st;
+    }
+    c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB + 2 * ELM_NB * z.ncols);
+    c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
+                                                          (int64_t)c->ga_ld * c->qrow_cols),
+                                      2 * z.G_pad);
+    c->work_back = z.S * z.ld;
+    z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
+    if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
+        (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess) {
+        elmddm_destroy(c);
+        return ELMDDM_ECUDA;
+    }
+    *out = c;
+    return ELMDDM_OK;
+}
+
+void elmddm_destroy(elmddm_ctx* c) {
+    if (!c) return;
+    DeviceGuard dg(c->device);
+    cudaFree(c->d_status);
+    cudaFree(c->d_sub_face);
+    cudaFree(c->d_qsrc);
+    cudaFree(c->d_pair_ptr);
+    cudaFree(c->d_pair_bc);
+    cudaFree(c->d_terms);
+    cudaFree(c->d_gterm_ptr);
+    cudaFree(c->d_gterms);
+    delete c;
+}
+
+const char* elmddm_last_error(const elmddm_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+elmddm_status elmddm_sizes(const elmddm_ctx* c, elmddm_sizes_t* out) {
+    CHECK_CTX(c);
+    if (!out) return ELMDDM_EINVAL;
+    *out = c->sz;
+    return ELMDDM_OK;
+}
+
+int64_t elmddm_band_index(const elmddm_ctx* c, int64_t i, int64_t j) {
+    if (!c) return -1;
+    return i + j * c->sz.band_ld;
+}
+
+elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {
+    CHECK_CTX(c);
+    DeviceGuard dg(c->device);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_sync");
+    ElmStatus h{0, 0};
+    if ((e = cudaMemcpy(&h, c->d_status, sizeof(h), cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return cuda_fail(c, e, "elmddm_sync");
+    if (h.code != 0) {
+        cudaMemset(c->d_status, 0, sizeof(ElmStatus));
+        c->err = "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info);
+        return (elmddm_status)h.code;
+    }
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_interface_points(const elmddm_ctx* c, double* xy) {
+    CHECK_CTX(c);
+    if (!xy) return ELMDDM_EINVAL;
+    const int P = c->cfg.P, q = c->cfg.q;
+    for (int f = 0; f < c->faces; ++f) {
+        int s = c->face_sub[f * 2], e = c->face_edge[f * 2];
+        int i = s % P, j = s / P;
+        for (int k = 0; k < q; ++k) {
+            double t_along, fixed;
+            if (e == 1) {  // vertical face at x = (i+1)/P
+                fixed = (double)(i + 1) / (double)P;
+                t_along = (double)(j * (q + 1) + k + 1) / (double)(P * (q + 1));
+                xy[2 * ((int64_t)f * q + k)] = fixed;
+                xy[2 * ((int64_t)f * q + k) + 1] = t_along;
+            } else {  // horizontal face at y = (j+1)/P
+                fixed = (double)(j + 1) / (double)P;
+                t_along = (double)(i * (q + 1) + k + 1) / (double)(P * (q + 1));
+                xy[2 * ((int64_t)f * q + k)] = t_along;
+                xy[2 * ((int64_t)f * q + k) + 1] = fixed;
+            }
+        }
+    }
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_init_hidden(elmddm_ctx* c, double* W, double* b, double* xi, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, W);
+    CHECK_PTR(c, b);
+    DeviceGuard dg(c->device);
+    cudaError_t e = launch_init_hidden(c, W, b, xi, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_init_hidden");
+}
+
+elmddm_status elmddm_assemble(elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
+                              void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, W);
+    CHECK_PTR(c, b);
+    CHECK_PTR(c, Kaug);
+    CHECK_PTR(c, At);
+    DeviceGuard dg(c->device);
+    cudaError_t e = launch_assemble(c, W, b, Kaug, At, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_assemble");
+}
+
+elmddm_status elmddm_local_factor(elmddm_ctx* c, double* Kaug, double* tau, double* work, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Kaug);
+    CHECK_PTR(c, tau);
+    CHECK_PTR(c, work);
+    DeviceGuard dg(c->device);
+    cudaError_t e = run_local_factor(c, Kaug, tau, work, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_local_factor");
+}
+
+elmddm_status elmddm_schur_accumulate(elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
+                                      double* work, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Kaug);
+    CHECK_PTR(c, At);
+    CHECK_PTR(c, Pbuf);
+    CHECK_PTR(c, Sbuf);
+    DeviceGuard dg(c->device);
+    cudaError_t e = run_schur_accumulate(c, Kaug, At, Pbuf, Sbuf, work, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_schur_accumulate");
+}
+
+elmddm_status elmddm_interface_assemble(elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
+                                        double* g, double* work, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Pbuf);
+    CHECK_PTR(c, Sbuf);
+    CHECK_PTR(c, Mband);
+    CHECK_PTR(c, g);
+    CHECK_PTR(c, work);
+    DeviceGuard dg(c->device);
+    cudaError_t e = run_interface_assemble(c, Pbuf, Sbuf, Mband, g, work, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_interface_assemble");
+}
+
+elmddm_status elmddm_interface_factor_solve(elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
+                                            void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Mband);
+    CHECK_PTR(c, g);
+    CHECK_PTR(c, uG);
+    CHECK_PTR(c, work);
+    DeviceGuard dg(c->device);
+    cudaError_t e = run_cholesky_solve(c, Mband, g, uG, work, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_interface_factor_solve");
+    return elmddm_sync(c, stream);
+}
+
+elmddm_status elmddm_interface_solve(elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband, double* g,
+                                     double* uG, double* work, void* stream) {
+    elmddm_status s = elmddm_interface_assemble(c, Pbuf, Sbuf, Mband, g, work, stream);
+    if (s != ELMDDM_OK) return s;
+    return elmddm_interface_factor_solve(c, Mband, g, uG, work, stream);
+}
+
+elmddm_status elmddm_back_solve(elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,
+                                double* work, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Kaug);
+    CHECK_PTR(c, uG);
+    CHECK_PTR(c, coef);
+    CHECK_PTR(c, resid);
+    CHECK_PTR(c, work);
+    DeviceGuard dg(c->device);
+    cudaError_t e = run_back_solve(c, Kaug, uG, coef, resid, work, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_back_solve");
+}
+
+elmddm_status elmddm_evaluate(elmddm_ctx* c, const double* W, const double* b, const double* coef, const double* xy,
+                              int64_t n, double* u, void* stream) {
+    CHECK_CTX(c);
+    if (n < 0) return ELMDDM_EINVAL;
+    if (n == 0) return ELMDDM_OK;
+    CHECK_PTR(c, W);
+    CHECK_PTR(c, b);
+    CHECK_PTR(c, coef);
+    CHECK_PTR(c, xy);
+    CHECK_PTR(c, u);
+    DeviceGuard dg(c->device);
+    cudaError_t e = launch_evaluate(c, W, b, coef, xy, n, u, (cudaStream_t)stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_evaluate");
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// gemm.cu -- batched fp64 GEMM on the FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64) for sm_100a.
+//
+// Used for every dense contraction of the hot path: the compact-WY trailing updates of the
+// blocked Householder QR (W = V^T C, Z = T^T W, C -= V Z), the TRSM update and flux product of
+// the Schur elimination (W_s = A R11^{-1}, P_s = W_s [R12|y]), the Gram blocks T^T T, the Q-row
+// Grams of the interface system and the band-Cholesky SYRK updates.
+//
+// tcgen05/UMMA has no f64 kind, so on B200 the FP64 tensor path is warp-level DMMA.8x8x4
+// (DESIGN.md §5).  Tile 64x64x16, 8 warps (2 x 4), each warp 32x16 = 4x2 DMMA tiles; operands
+// staged global -> shared with a 3-stage cp.async pipeline; shared layouts padded so that every
+// DMMA fragment load is conflict-free (2 wavefronts per 32 x 8 B).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 256;
+constexpr int PAD_MN = BM + 8;  // stride of [k][m|n] layouts (== 8 mod 16 doubles)
+constexpr int PAD_K = BK + 4;   // stride of [m|n][k] layouts (== 4 mod 16 doubles)
+constexpr int A_ELEMS = (BM * PAD_K > BK * PAD_MN) ? BM * PAD_K : BK * PAD_MN;
+constexpr int B_ELEMS = A_ELEMS;
+constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8;
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Load a (rows x cols) tile whose contiguous (first) dimension has extent `nc` elements, from
+// src (leading dim ld) into shared dst with row stride `pad` (dst[j*pad + i] = src[i + j*ld]).
+// rows_valid / cols_valid clip the tile (zero fill).  Chunks of 2 doubles (16 B).
+template <int NC, int NS>  // NC contiguous extent, NS strided extent of the tile
+__device__ __forceinline__ void load_tile(double* dst, int pad, const double* src, int64_t ld, int c_valid,
+                                          int s_valid, int tid) {
+    constexpr int CH = NC / 2;  // chunks per strided index
+    constexpr int TOTAL = CH * NS;
+#pragma unroll
+    for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+        int ch = tid + it * NT;
+        if (TOTAL % NT != 0 && ch >= TOTAL) break;
+        int j = ch / CH;
+        int i = (ch % CH) * 2;
+        int bytes = 0;
+        if (j < s_valid) bytes = (i + 1 < c_valid) ? 16 : (i < c_valid ? 8 : 0);
+        const double* s = bytes ? src + i + (int64_t)j * ld : src;
+        cp_async16(dst + j * pad + i, s, bytes);
+    }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, bz = blockIdx.z;
+    if (g.lower_only && m0 + BM <= n0) return;
+    const double* A = g.A + (int64_t)bz * g.sA;
+    const double* B = g.B + (int64_t)bz * g.sB;
+    double* C = g.C + (int64_t)bz * g.sC;
+
+    const int mv = min(BM, g.M - m0), nv = min(BN, g.N - n0);
+    const int ktiles = (g.K + BK - 1) / BK;
+
+    auto issue = [&](int kt, int stage) {
+        double* As = smem + stage * STAGE_ELEMS;
+        double* Bs = As + A_ELEMS;
+        const int k0 = kt * BK, kv = min(BK, g.K - k0);
+        if (!TA)  // A[i + k lda]: contiguous m, layout As[k][m]
+            load_tile<BM, BK>(As, PAD_MN, A + m0 + (int64_t)k0 * g.lda, g.lda, mv, kv, tid);
+        else  // A[k + i lda]: contiguous k, layout As[m][k]
+            load_tile<BK, BM>(As, PAD_K, A + k0 + (int64_t)m0 * g.lda, g.lda, kv, mv, tid);
+        if (!TB)  // B[k + n ldb]: contiguous k, layout Bs[n][k]
+            load_tile<BK, BN>(Bs, PAD_K, B + k0 + (int64_t)n0 * g.ldb, g.ldb, kv, nv, tid);
+        else  // B[n + k ldb]: contiguous n, layout Bs[k][n]
+            load_tile<BN, BK>(Bs, PAD_MN, B + n0 + (int64_t)k0 * g.ldb, g.ldb, nv, kv, tid);
+    };
+
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) issue(s, s);
+        cp_commit();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            int nk = kt + STAGES - 1;
+            if (nk < ktiles) issue(nk, nk % STAGES);
+            cp_commit();
+        }
+        const double* As = smem + (kt % STAGES) * STAGE_ELEMS;
+        const double* Bs = As + A_ELEMS;
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                int i = wm * 32 + mt * 8 + (lane >> 2);
+                af[mt] = TA ? As[i * PAD_K + kk] : As[kk * PAD_MN + i];
+            }
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                int n = wn * 16 + nt * 8 + (lane >> 2);
+                bf[nt] = TB ? Bs[kk * PAD_MN + n] : Bs[n * PAD_K + kk];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+    }
+    cp_wait<0>();
+
+    // epilogue: C = alpha acc + beta C
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        int i = wm * 32 + mt * 8 + (lane >> 2);
+        if (i >= mv) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int j = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                if (j >= nv) continue;
+                double* cp = C + (m0 + i) + (int64_t)(n0 + j) * g.ldc;
+                double v = g.alpha * acc[mt][nt][e];
+                if (g.beta != 0.0) v += g.beta * *cp;
+                *cp = v;
+            }
+        }
+    }
+}
+
+template <bool TA, bool TB>
+cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
+    k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, st>>>(g);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+    if (g.K <= 0) {
+        // C = beta C (only used with beta = 1 in this library)
+        return cudaSuccess;
+    }
+    if (transA) return transB ? launch<true, true>(g, st) : launch<true, false>(g, st);
+    return transB ? launch<false, true>(g, st) : launch<false, false>(g, st);
+}

@@ -1,0 +1,91 @@
+// internal.h -- private declarations of the elmddm CUDA library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/elmddm.h"
+
+#define ELM_NB 64      // panel width of the blocked QR, tile of the band Cholesky
+#define ELM_BB 8       // base block width inside a QR panel
+
+// Device status word: [0] error code (ELMDDM_ENUMERIC), [1] info (column / index).
+struct ElmStatus {
+    int code;
+    int info;
+};
+
+// One contribution to an interface-matrix face block, see schur.cu.
+struct FaceTerm {
+    int kind;  // 0: S1 block of Sbuf[s], 1: Ga block of face a
+    int src;   // s or a
+    int r0;    // row offset inside the source block
+    int c0;    // column offset inside the source block
+};
+
+struct elmddm_ctx {
+    elmddm_config cfg;
+    int device;
+    elmddm_sizes_t sz;
+    std::string err;
+    ElmStatus* d_status = nullptr;
+    int nsm = 148;
+
+    // geometry (host)
+    int faces = 0;
+    std::vector<int> face_sub;   // [faces][2] subdomains (lower/left first)
+    std::vector<int> face_edge;  // [faces][2] local edge of the face in each subdomain
+    std::vector<int> sub_face;   // [N][4] face of edge e of subdomain s, -1 = Dirichlet
+    // flux-face neighbour slots (Q row blocks): nbr[a][7] faces, -1 = empty
+    std::vector<int> nbr;
+    // device copies
+    int* d_sub_face = nullptr;   // [N][4]
+    int* d_qsrc = nullptr;       // [faces][8 slots][2 contributors][3] = (s, row edge, col edge) or -1
+    int* d_pair_ptr = nullptr;   // CSR over face-block pairs (b, c), b >= c
+    int* d_pair_bc = nullptr;    // [npairs][2]
+    FaceTerm* d_terms = nullptr; // contributions of each pair
+    int* d_gterm_ptr = nullptr;  // CSR over faces b for g terms
+    FaceTerm* d_gterms = nullptr;
+    int npairs = 0, nterms = 0, ngterms = 0;
+    int qrow_ld = 0, qrow_cols = 0, ga_ld = 0;  // Q row block: q x (7q+1), ld qrow_ld; Ga: ga_ld^2
+    int64_t work_factor = 0, work_iface = 0, work_back = 0;
+};
+
+// ------------------------------------------------------------------------------------------
+// batched DMMA GEMM:  C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], column-major, fp64
+// ------------------------------------------------------------------------------------------
+struct GemmArgs {
+    int M, N, K;
+    const double* A;
+    int64_t lda, sA;
+    const double* B;
+    int64_t ldb, sB;
+    double* C;
+    int64_t ldc, sC;
+    double alpha, beta;
+    int batch;
+    int lower_only;  // skip 64x64 output tiles strictly above the diagonal
+};
+cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st);
+
+// kernels in the other translation units
+cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double* xi, cudaStream_t st);
+cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
+                            cudaStream_t st);
+cudaError_t launch_evaluate(const elmddm_ctx* c, const double* W, const double* b, const double* coef,
+                            const double* xy, int64_t n, double* u, cudaStream_t st);
+cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, double* work, cudaStream_t st);
+cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
+                                 double* work, cudaStream_t st);
+cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
+                                   double* g, double* work, cudaStream_t st);
+cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
+                               cudaStream_t st);
+cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,
+                           double* work, cudaStream_t st);
+
+__device__ __forceinline__ void elm_set_status(ElmStatus* st, int code, int info) {
+    if (atomicCAS(&st->code, 0, code) == 0) st->info = info;
+}

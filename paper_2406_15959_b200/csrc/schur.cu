@@ -1,0 +1,291 @@
+// schur.cu -- elimination of the output weights into the interface Schur system, the rank-0
+// interface assembly, and the local back-solve.
+//
+//   W_s   = A^s R11^{-1}            (TRSM on At = (A^s)^T, in place; the flux operator formed once)
+//   P_s   = W_s [R12 | y]           (flux of c^s(u) = q_s + P_s u_s)
+//   S_s   = [T_E | t_F]^T [T_E | t_F]
+//   M     = sum_s scatter(T_E^T T_E) + Q^T Q,   g = -sum_s scatter(T_E^T t_F) - Q^T q
+//   c^s   = R11^{-1}(y + R12 u_s),  r_s = ||t_F + T_E u_s||
+// (eqn:eliminated .. eqn:schur; readings R13 and R23 in DESIGN.md.)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace {
+
+// ---- TRSM diagonal block: X = R_ii^{-T} At_i  (R_ii upper 64x64 -> lower solve) --------------
+// grid (ceil(4q/64), S), 64 threads: one column of At per thread.
+__global__ void __launch_bounds__(64) k_trsm_lt_diag(const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
+                                                     double* __restrict__ At, int M, int ncol_at, int i0, int bi) {
+    __shared__ double Rs[64][65];
+    const int sl = blockIdx.y;
+    const double* A = Kaug + (int64_t)sl * ld * ncols;
+    for (int t = threadIdx.x; t < bi * bi; t += 64) {
+        int r = t % bi, c = t / bi;
+        Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];  // R[r][c], upper part used
+    }
+    __syncthreads();
+    const int col = blockIdx.x * 64 + threadIdx.x;
+    if (col >= ncol_at) return;
+    double* x = At + (int64_t)sl * M * ncol_at + (int64_t)col * M + i0;
+    double xv[64];
+#pragma unroll
+    for (int r = 0; r < 64; ++r)
+        if (r < bi) xv[r] = x[r];
+    // R^T x = a: x_r = (a_r - sum_{l<r} R[l][r] x_l) / R[r][r]
+#pragma unroll
+    for (int r = 0; r < 64; ++r) {
+        if (r < bi) {
+            double s = xv[r];
+#pragma unroll
+            for (int l = 0; l < 64; ++l)
+                if (l < r) s -= Rs[l][r] * xv[l];
+            xv[r] = s / Rs[r][r];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 64; ++r)
+        if (r < bi) x[r] = xv[r];
+}
+
+// ---- interface: Q row blocks ------------------------------------------------------------------
+// Qrow[a] (q x (7q+1), ld qrow_ld): slot t (t < 7) = sum over the (<= 2) subdomains touching both
+// face a and face nbr[a][t] of P_s[e_a rows, e_b cols]; slot 7 = sum_s q_s[e_a rows].
+// qsrc[a][t][c][3] = (s, e_row, e_col) or s = -1.  grid (faces, 8).
+__global__ void k_qrow(const double* __restrict__ Pbuf, int64_t pstride, int64_t pld, const int* __restrict__ qsrc,
+                       int q, double* __restrict__ Qrow, int64_t qld, int64_t qstride) {
+    const int a = blockIdx.x, t = blockIdx.y;
+    const int* src = qsrc + ((int64_t)a * 8 + t) * 6;
+    const int ncolblk = t < 7 ? q : 1;
+    double* dst = Qrow + (int64_t)a * qstride + (int64_t)t * q * qld;
+    for (int e = threadIdx.x; e < q * ncolblk; e += blockDim.x) {
+        int i = e % q, j = e / q;
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            int s = src[c * 3];
+            if (s >= 0) {
+                int er = src[c * 3 + 1], ec = src[c * 3 + 2];
+                int64_t col = t < 7 ? (int64_t)ec * q + j : 4 * (int64_t)q;
+                v += Pbuf[(int64_t)s * pstride + (int64_t)er * q + i + col * pld];
+            }
+        }
+        dst[i + (int64_t)j * qld] = v;
+    }
+}
+
+__device__ __forceinline__ int64_t band_idx(int64_t i, int64_t j, int64_t bld) { return i + j * bld; }
+
+// M block (b, c) = sum of terms, written in the band storage (b == c: lower triangle only).
+__global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restrict__ pair_bc,
+                            const FaceTerm* __restrict__ terms, const double* __restrict__ Sbuf, int64_t sstride,
+                            int64_t sld, const double* __restrict__ Ga, int64_t gstride, int64_t gld, int q,
+                            double* __restrict__ Mband, int64_t bld) {
+    const int p = blockIdx.x;
+    const int b = pair_bc[2 * p], c = pair_bc[2 * p + 1];
+    const int t0 = pair_ptr[p], t1 = pair_ptr[p + 1];
+    for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+        int i = e % q, j = e / q;
+        if (b == c && i < j) continue;
+        double v = 0.0;
+        for (int t = t0; t < t1; ++t) {
+            FaceTerm ft = terms[t];
+            if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * sld];
+            else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * gld];
+        }
+        Mband[band_idx((int64_t)b * q + i, (int64_t)c * q + j, bld)] = v;
+    }
+}
+
+// g[b q + i] = -(sum of terms); grid faces.
+__global__ void k_gassemble(const int* __restrict__ gptr, const FaceTerm* __restrict__ gterms,
+                            const double* __restrict__ Sbuf, int64_t sstride, int64_t sld, const double* __restrict__ Ga,
+                            int64_t gstride, int64_t gld, int q, double* __restrict__ g) {
+    const int b = blockIdx.x;
+    for (int i = threadIdx.x; i < q; i += blockDim.x) {
+        double v = 0.0;
+        for (int t = gptr[b]; t < gptr[b + 1]; ++t) {
+            FaceTerm ft = gterms[t];
+            if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + (ft.r0 + i) + (int64_t)ft.c0 * sld];
+            else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)ft.c0 * gld];
+        }
+        g[(int64_t)b * q + i] = -v;
+    }
+}
+
+__global__ void k_pad(double* Mband, int64_t bld, double* g, int64_t G, int64_t G_pad) {
+    int64_t i = G + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G_pad) return;
+    Mband[band_idx(i, i, bld)] = 1.0;
+    g[i] = 0.0;
+}
+
+// ---- back-solve -----------------------------------------------------------------------------
+// z[s][r] = sum_t Kaug[s][r][M + t] v_t, v = [u_s ; 1].   grid (ceil(ld/256), S)
+__global__ void __launch_bounds__(256) k_bs_gemv(elmddm_config cfg, const double* __restrict__ Kaug, int64_t ld,
+                                                 int64_t ncols, const int* __restrict__ sub_face,
+                                                 const double* __restrict__ uG, double* __restrict__ z) {
+    extern __shared__ double v[];
+    const int M = cfg.M, q = cfg.q, kaug = 4 * q + 1;
+    const int sl = blockIdx.y, s = cfg.s_begin + sl;
+    for (int t = threadIdx.x; t < kaug; t += blockDim.x) {
+        double val = 1.0;
+        if (t < 4 * q) {
+            int e = t / q, k = t % q;
+            int f = sub_face[s * 4 + e];
+            val = f >= 0 ? uG[(int64_t)f * q + k] : 0.0;
+        }
+        v[t] = val;
+    }
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= ld) return;
+    const double* A = Kaug + (int64_t)sl * ld * ncols + (int64_t)M * ld + r;
+    double acc = 0.0;
+    for (int t = 0; t < kaug; ++t) acc += A[(int64_t)t * ld] * v[t];
+    z[(int64_t)sl * ld + r] = acc;
+}
+
+// per subdomain: resid = ||z[M:ld]||, coef = R11^{-1} z[0:M] (blocked column-oriented
+// back substitution; 64-row diagonal blocks solved by warp 0).  grid S, 512 threads.
+__global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
+                                                 double* __restrict__ z, double* __restrict__ coef,
+                                                 double* __restrict__ resid) {
+    __shared__ double Rs[64][65];
+    __shared__ double cs[64];
+    __shared__ double red[16];
+    const int sl = blockIdx.x;
+    const double* A = Kaug + (int64_t)sl * ld * ncols;
+    double* zs = z + (int64_t)sl * ld;
+    // residual norm (deterministic)
+    double ss = 0.0;
+    for (int r = M + threadIdx.x; r < ld; r += blockDim.x) ss += zs[r] * zs[r];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        resid[sl] = sqrt(t);
+    }
+    const int nblk = (M + 63) / 64;
+    for (int ib = nblk - 1; ib >= 0; --ib) {
+        const int i0 = ib * 64, bi = min(64, M - i0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < bi * bi; t += blockDim.x) {
+            int r = t % bi, c = t / bi;
+            Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            double z0 = lane < bi ? zs[i0 + lane] : 0.0;
+            double z1 = lane + 32 < bi ? zs[i0 + lane + 32] : 0.0;
+            for (int r = bi - 1; r >= 0; --r) {
+                double cr;
+                if (r >= 32) cr = __shfl_sync(0xffffffffu, z1, r - 32);
+                else cr = __shfl_sync(0xffffffffu, z0, r);
+                cr = cr / Rs[r][r];
+                if (lane < r) z0 -= Rs[lane][r] * cr;
+                if (lane + 32 < r) z1 -= Rs[lane + 32][r] * cr;
+                if (lane == (r & 31)) {
+                    if (r >= 32) z1 = cr;
+                    else z0 = cr;
+                }
+            }
+            if (lane < bi) cs[lane] = z0;
+            if (lane + 32 < bi) cs[lane + 32] = z1;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < bi; t += blockDim.x) coef[(int64_t)sl * M + i0 + t] = cs[t];
+        // z[0:i0] -= R[0:i0, i0:i0+bi] c_i
+        for (int r = threadIdx.x; r < i0; r += blockDim.x) {
+            double acc = 0.0;
+            for (int k = 0; k < bi; ++k) acc += A[(int64_t)(i0 + k) * ld + r] * cs[k];
+            zs[r] -= acc;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
+                                 double* work, cudaStream_t st) {
+    (void)work;
+    const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols, kaug = c->sz.kaug;
+    const int M = c->cfg.M, q = c->cfg.q, nat = 4 * q;
+    cudaError_t e;
+    // W_s^T = R11^{-T} A^T  (blocked forward substitution on At, in place)
+    for (int i0 = 0; i0 < M; i0 += 64) {
+        const int bi = (M - i0) < 64 ? (M - i0) : 64;
+        dim3 g((nat + 63) / 64, (unsigned)S);
+        k_trsm_lt_diag<<<g, 64, 0, st>>>(Kaug, ld, ncols, At, M, nat, i0, bi);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const int rest = M - (i0 + bi);
+        if (rest > 0) {
+            // At[i0+bi:, :] -= R[i0:i0+bi, i0+bi:]^T X_i
+            GemmArgs ga{rest, nat, bi, Kaug + i0 + (int64_t)(i0 + bi) * ld, ld, ld * ncols, At + i0, M,
+                        (int64_t)M * nat, At + i0 + bi, M, (int64_t)M * nat, -1.0, 1.0, (int)S, 0};
+            if ((e = gemm_launch(true, false, ga, st)) != cudaSuccess) return e;
+        }
+    }
+    const int64_t s0 = c->cfg.s_begin;
+    const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
+    // P_s = W_s [R12 | y]   (4q x kaug)
+    GemmArgs gp{nat, (int)kaug, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
+                Pbuf + s0 * pstride, c->sz.pbuf_ld, pstride, 1.0, 0.0, (int)S, 0};
+    if ((e = gemm_launch(true, false, gp, st)) != cudaSuccess) return e;
+    // S_s = [T_E | t_F]^T [T_E | t_F]
+    const int Kt = (int)(ld - M);
+    GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
+                ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 0};
+    return gemm_launch(true, false, gs, st);
+}
+
+cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
+                                   double* g, double* work, cudaStream_t st) {
+    const int q = c->cfg.q;
+    const int64_t F = c->faces, kaug = c->sz.kaug;
+    const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
+    const int64_t qstride = (int64_t)c->qrow_ld * c->qrow_cols;
+    const int64_t gstride = (int64_t)c->ga_ld * c->qrow_cols;
+    double* Qrow = work;
+    double* Ga = Qrow + F * qstride;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(Mband, 0, sizeof(double) * c->sz.band_elems, st)) != cudaSuccess) return e;
+    if (F > 0) {
+        k_qrow<<<dim3((unsigned)F, 8), 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_qsrc, q, Qrow, c->qrow_ld,
+                                                      qstride);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        // Ga[a] = Qrow[a]^T Qrow[a]
+        GemmArgs gg{c->qrow_cols, c->qrow_cols, q, Qrow, c->qrow_ld, qstride, Qrow, c->qrow_ld, qstride, Ga, c->ga_ld,
+                    gstride, 1.0, 0.0, (int)F, 0};
+        if ((e = gemm_launch(true, false, gg, st)) != cudaSuccess) return e;
+        k_massemble<<<(unsigned)c->npairs, 256, 0, st>>>(c->d_pair_ptr, c->d_pair_bc, c->d_terms, Sbuf, sstride,
+                                                          c->sz.sbuf_ld, Ga, gstride, c->ga_ld, q, Mband,
+                                                          c->sz.band_ld);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        k_gassemble<<<(unsigned)F, 128, 0, st>>>(c->d_gterm_ptr, c->d_gterms, Sbuf, sstride, c->sz.sbuf_ld, Ga,
+                                                  gstride, c->ga_ld, q, g);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    const int64_t npad = c->sz.G_pad - c->sz.G;
+    if (npad > 0) {
+        k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->sz.band_ld, g, c->sz.G, c->sz.G_pad);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,
+                           double* work, cudaStream_t st) {
+    const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols;
+    double* z = work;
+    dim3 g1((unsigned)((ld + 255) / 256), (unsigned)S);
+    k_bs_gemv<<<g1, 256, sizeof(double) * c->sz.kaug, st>>>(c->cfg, Kaug, ld, ncols, c->d_sub_face, uG, z);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_bs_trsv<<<(unsigned)S, 512, 0, st>>>(Kaug, ld, ncols, c->cfg.M, z, coef, resid);
+    return cudaGetLastError();
+}

@@ -1,0 +1,236 @@
+"""Thin Python layer over the C ABI: one context per rank/device, torch tensors as device memory,
+torch.distributed (NCCL) for the two exchange steps of Algorithm 1.
+
+    rank r:  init_hidden -> assemble -> local_factor -> schur_accumulate        (own subdomains)
+             reduce(Pbuf, Sbuf) to rank 0                                        (NCCL, NVLink)
+    rank 0:  interface_solve  (eqn:schur)
+             broadcast(u_Gamma)                                                  (NCCL)
+    rank r:  back_solve -> evaluate                                              (own subdomains)
+
+The wrappers below do argument marshalling only; every arithmetic step runs in libelmddm.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise _lib.ElmddmError("elmddm arrays must be CUDA tensors")
+    if t.dtype != torch.float64:
+        raise _lib.ElmddmError("elmddm arrays must be float64")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def partition(N: int, world: int, rank: int):
+    """Contiguous row-major slab of subdomains for `rank`: ceil(N/world) each."""
+    per = -(-N // world)
+    s0 = min(N, rank * per)
+    s1 = min(N, s0 + per)
+    return s0, s1
+
+
+@dataclass
+class Problem:
+    P: int
+    M: int
+    p: int
+    q: int
+    problem: int = 0
+    seed: int = 0
+    init_scheme: int = 0
+    init_c: float = 0.125
+    r_over_diam: float = 0.5
+    interface_mode: int = 0
+
+    @classmethod
+    def from_config(cls, c: dict) -> "Problem":
+        keys = cls.__dataclass_fields__.keys()
+        return cls(**{k: v for k, v in c.items() if k in keys})
+
+
+class Context:
+    """One elmddm context (one device, one subdomain range)."""
+
+    def __init__(self, prob: Problem, s_begin: int = 0, s_end: int | None = None, device: int | None = None):
+        L = _lib.load()
+        self.L = L
+        self.prob = prob
+        N = prob.P * prob.P
+        if s_end is None:
+            s_end = N
+        self.device = torch.cuda.current_device() if device is None else device
+        cfg = _lib.Config(prob.P, prob.M, prob.p, prob.q, prob.problem, prob.init_scheme, prob.init_c,
+                          prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, 0)
+        h = C.c_void_p()
+        rc = L.elmddm_create(C.byref(cfg), self.device, C.byref(h))
+        if rc != 0:
+            raise _lib.ElmddmError(f"elmddm_create failed: {_lib.STATUS.get(rc, rc)} (config {prob}, "
+                                   f"range [{s_begin},{s_end}))")
+        self.h = h
+        sz = _lib.Sizes()
+        self._check(L.elmddm_sizes(h, C.byref(sz)), "elmddm_sizes")
+        self.sizes = sz.as_dict()
+        self.s_begin, self.s_end = s_begin, s_end
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.L.elmddm_destroy(h)
+            self.h = None
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self.L.elmddm_last_error(self.h)
+            raise _lib.ElmddmError(f"{what}: {_lib.STATUS.get(rc, rc)}: {msg.decode() if msg else ''}")
+
+    # ---- buffers ---------------------------------------------------------------------------
+    def alloc(self) -> dict:
+        z, M = self.sizes, self.prob.M
+        dev = torch.device("cuda", self.device)
+        f = dict(dtype=torch.float64, device=dev)
+        S, q = z["S"], self.prob.q
+        return {
+            "W": torch.empty(S * M * 2, **f), "b": torch.empty(S * M, **f), "xi": torch.empty(S * M * 2, **f),
+            "Kaug": torch.empty(z["kaug_elems"], **f), "At": torch.empty(z["at_elems"], **f),
+            "tau": torch.empty(z["tau_elems"], **f), "work": torch.empty(max(z["work_elems"], 2), **f),
+            "Pbuf": torch.zeros(z["pbuf_elems"], **f), "Sbuf": torch.zeros(z["sbuf_elems"], **f),
+            "Mband": torch.empty(max(z["band_elems"], 2), **f), "g": torch.empty(z["G_pad"], **f),
+            "uG": torch.zeros(z["G_pad"], **f), "coef": torch.empty(S * M, **f), "resid": torch.empty(S, **f),
+        }
+
+    # ---- the C ABI, one wrapper per entry point ----------------------------------------------
+    def init_hidden(self, W, b, xi=None, stream=None):
+        self._check(self.L.elmddm_init_hidden(self.h, _ptr(W), _ptr(b), _ptr(xi), _stream(stream)), "init_hidden")
+
+    def assemble(self, W, b, Kaug, At, stream=None):
+        self._check(self.L.elmddm_assemble(self.h, _ptr(W), _ptr(b), _ptr(Kaug), _ptr(At), _stream(stream)),
+                    "assemble")
+
+    def local_factor(self, Kaug, tau, work, stream=None):
+        self._check(self.L.elmddm_local_factor(self.h, _ptr(Kaug), _ptr(tau), _ptr(work), _stream(stream)),
+                    "local_factor")
+
+    def schur_accumulate(self, Kaug, At, Pbuf, Sbuf, work, stream=None):
+        self._check(self.L.elmddm_schur_accumulate(self.h, _ptr(Kaug), _ptr(At), _ptr(Pbuf), _ptr(Sbuf), _ptr(work),
+                                                   _stream(stream)), "schur_accumulate")
+
+    def interface_assemble(self, Pbuf, Sbuf, Mband, g, work, stream=None):
+        self._check(self.L.elmddm_interface_assemble(self.h, _ptr(Pbuf), _ptr(Sbuf), _ptr(Mband), _ptr(g), _ptr(work),
+                                                     _stream(stream)), "interface_assemble")
+
+    def interface_factor_solve(self, Mband, g, uG, work, stream=None):
+        self._check(self.L.elmddm_interface_factor_solve(self.h, _ptr(Mband), _ptr(g), _ptr(uG), _ptr(work),
+                                                         _stream(stream)), "interface_factor_solve")
+
+    def interface_solve(self, Pbuf, Sbuf, Mband, g, uG, work, stream=None):
+        self._check(self.L.elmddm_interface_solve(self.h, _ptr(Pbuf), _ptr(Sbuf), _ptr(Mband), _ptr(g), _ptr(uG),
+                                                  _ptr(work), _stream(stream)), "interface_solve")
+
+    def back_solve(self, Kaug, uG, coef, resid, work, stream=None):
+        self._check(self.L.elmddm_back_solve(self.h, _ptr(Kaug), _ptr(uG), _ptr(coef), _ptr(resid), _ptr(work),
+                                             _stream(stream)), "back_solve")
+
+    def evaluate(self, W, b, coef, xy, u, stream=None):
+        n = xy.numel() // 2
+        self._check(self.L.elmddm_evaluate(self.h, _ptr(W), _ptr(b), _ptr(coef), _ptr(xy), n, _ptr(u),
+                                           _stream(stream)), "evaluate")
+
+    def sync(self, stream=None):
+        self._check(self.L.elmddm_sync(self.h, _stream(stream)), "sync")
+
+    def interface_points(self):
+        import numpy as np
+
+        xy = np.zeros((self.sizes["G"], 2))
+        self._check(self.L.elmddm_interface_points(self.h, xy.ctypes.data_as(C.c_void_p)), "interface_points")
+        return xy
+
+    def band_index(self, i, j):
+        return int(self.L.elmddm_band_index(self.h, i, j))
+
+    # ---- Algorithm 1 -------------------------------------------------------------------------
+    def run(self, buf: dict, xy=None, u=None, group=None, stream=None, timer=None):
+        """One pass of the hot path on this rank.  With a process group of size > 1 the Schur
+        contributions are summed on rank 0 (NCCL reduce) and u_Gamma is broadcast back."""
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group) if (group is not None or (dist.is_available() and dist.is_initialized())) else 1
+        rank = dist.get_rank(group) if world > 1 else 0
+        mark = timer.mark if timer is not None else (lambda name: None)
+        self.init_hidden(buf["W"], buf["b"], None, stream)
+        mark("init_hidden")
+        self.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"], stream)
+        mark("assemble")
+        self.local_factor(buf["Kaug"], buf["tau"], buf["work"], stream)
+        mark("local_factor")
+        if world > 1:
+            buf["Pbuf"].zero_()
+            buf["Sbuf"].zero_()
+        self.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"], stream)
+        mark("schur_accumulate")
+        if world > 1:
+            dist.reduce(buf["Pbuf"], dst=0, group=group)
+            dist.reduce(buf["Sbuf"], dst=0, group=group)
+            mark("reduce")
+        if self.sizes["G"] > 0:
+            if rank == 0:
+                self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
+                mark("interface_assemble")
+                self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
+                mark("interface_factor_solve")
+            if world > 1:
+                dist.broadcast(buf["uG"], src=0, group=group)
+                mark("broadcast")
+        self.back_solve(buf["Kaug"], buf["uG"], buf["coef"], buf["resid"], buf["work"], stream)
+        mark("back_solve")
+        if xy is not None:
+            if world > 1:
+                u.zero_()
+            self.evaluate(buf["W"], buf["b"], buf["coef"], xy, u, stream)
+            if world > 1:
+                dist.reduce(u, dst=0, group=group)
+            mark("evaluate")
+        return buf
+
+
+def solve(prob: Problem, xy_host=None, device: int | None = None, group=None, return_all: bool = False):
+    """Public one-call API: solve the configured DDM-ELM problem and return host results.
+
+    xy_host: optional (n, 2) host array/tensor of evaluation points.  Returns a dict with
+    u (on rank 0), uG, coef, resid (own subdomains) as host tensors."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    N = prob.P * prob.P
+    s0, s1 = partition(N, world, rank)
+    ctx = Context(prob, s0, s1, device)
+    buf = ctx.alloc()
+    dev = buf["W"].device
+    xy = u = None
+    if xy_host is not None:
+        xy_t = torch.as_tensor(xy_host, dtype=torch.float64).reshape(-1)
+        xy = xy_t.to(dev, non_blocking=True)
+        u = torch.zeros(xy.numel() // 2, dtype=torch.float64, device=dev)
+    ctx.run(buf, xy, u, group)
+    out = {"uG": buf["uG"][: ctx.sizes["G"]].cpu(), "coef": buf["coef"].view(-1, prob.M).cpu(),
+           "resid": buf["resid"].cpu(), "range": (s0, s1)}
+    if u is not None:
+        out["u"] = u.cpu()
+    if return_all:
+        out["ctx"], out["buf"] = ctx, buf
+    return out

@@ -1,0 +1,95 @@
+"""Shared test helpers: run the CUDA path phase by phase and map its layouts onto the oracle's."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+import workloads as WL
+
+EPS = np.finfo(float).eps
+
+
+def ocfg(c: dict):
+    return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0), c.get("init_c", 0.125),
+                 c.get("r_over_diam", 0.5), c["seed"])
+
+
+def small(**kw):
+    base = dict(P=2, M=16, p=6, q=4, problem=0, seed=7, init_scheme=0, init_c=0.125, r_over_diam=0.5)
+    base.update(kw)
+    return base
+
+
+def gpu_ctx(c: dict, s_begin=0, s_end=None):
+    import paper_2406_15959_b200 as E
+
+    pr = E.Problem.from_config(c)
+    ctx = E.Context(pr, s_begin, s_end)
+    return ctx, ctx.alloc()
+
+
+def run_gpu(c: dict, xy=None, upto="all"):
+    """Run the hot path on cuda:0 for config dict c; returns (ctx, buf, u or None)."""
+    import torch
+
+    ctx, buf = gpu_ctx(c)
+    xy_t = u = None
+    if xy is not None:
+        xy_t = torch.as_tensor(np.ascontiguousarray(xy), dtype=torch.float64, device="cuda").reshape(-1)
+        u = torch.zeros(xy.shape[0], dtype=torch.float64, device="cuda")
+    if upto == "all":
+        ctx.run(buf, xy_t, u)
+    else:
+        ctx.init_hidden(buf["W"], buf["b"], buf["xi"])
+        ctx.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"])
+        if upto in ("factor", "schur"):
+            ctx.local_factor(buf["Kaug"], buf["tau"], buf["work"])
+        if upto == "schur":
+            ctx.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"])
+    torch.cuda.synchronize()
+    return ctx, buf, u
+
+
+def kaug_np(ctx, buf, sl):
+    z = ctx.sizes
+    K = buf["Kaug"].view(z["S"], z["ncols"], z["ld"])[sl].cpu().numpy()
+    return K.T  # (ld, ncols)
+
+
+def at_np(ctx, buf, sl, M, q):
+    return buf["At"].view(-1, 4 * q, M)[sl].cpu().numpy()  # (4q, M) = A rows
+
+
+def local_iface_index(c: dict, s: int):
+    """GPU local index (e*q + k) of the oracle's interface points, in the oracle's row order."""
+    xy, edge, gidx = O.rows(ocfg(c), s)
+    m = len(edge)
+    rows = np.where(gidx >= 0)[0]
+    return rows - (m - 4 * c["q"]), gidx[rows]
+
+
+def pbuf_np(ctx, buf, s, q):
+    z = ctx.sizes
+    return buf["Pbuf"].view(z["N"], z["kaug"], z["pbuf_ld"])[s].cpu().numpy().T  # (4q, kaug)
+
+
+def sbuf_np(ctx, buf, s):
+    z = ctx.sizes
+    return buf["Sbuf"].view(z["N"], z["kaug"], z["sbuf_ld"])[s].cpu().numpy().T[: z["kaug"], :]  # (kaug, kaug)
+
+
+def band_to_dense(ctx, Mband):
+    """Full symmetric G x G matrix from the band storage (host)."""
+    z = ctx.sizes
+    G, LD, hb = z["G"], z["band_ld"], z["halfband"]
+    Mb = Mband.cpu().numpy()
+    D = np.zeros((G, G))
+    for j in range(G):
+        i1 = min(G, j + hb + 1)
+        idx = np.arange(j, i1) + j * LD
+        D[j:i1, j] = Mb[idx]
+    return np.tril(D) + np.tril(D, -1).T
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))

@@ -1,0 +1,348 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances:
+  * init_hidden: bit-exact (integer RNG + explicitly rounded fp64, reading R9);
+  * assemble: |dK| <= 32 eps * scale_j * (1 + |w_j.x| + |b_j|): each side rounds z = w.x + b
+    with |dz| <= 3 eps (1 + |w.x| + |b|) and the two orders differ; |sigma^(k+1)| <= 2 turns that
+    into <= 12 eps of sigma^(k), plus a few eps of evaluation rounding, times the row scale
+    (|w|^2 for the Laplacian rows, |w| for flux rows, 1 for value rows);
+  * Schur intermediates entrywise only at config 0 (reading R22), cross-residual at config >= 1;
+  * u on the 101^2 grid: relative L2 <= 1e-6 (BASELINE.json north star);
+  * r_s with the same u_Gamma: |dr| <= 1e-8 r + 10 m eps ||F - B u|| (reading R17).
+"""
+import concurrent.futures as cf
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as WL
+from helpers import (EPS, band_to_dense, gpu_ctx, kaug_np, local_iface_index, ocfg, pbuf_np, rel_l2, run_gpu,
+                     sbuf_np, small, at_np)
+
+pytestmark = pytest.mark.gpu
+NCPU = len(os.sched_getaffinity(0))
+
+
+def _oracle_init(c):
+    W, b, xi, _ = O.init_hidden(ocfg(c))
+    return W, b, xi
+
+
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", range(5))
+def test_init_hidden_bit_exact(k):
+    c = WL.config(k)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, xi = _oracle_init(c)
+    assert np.array_equal(buf["W"].cpu().numpy(), W.ravel())
+    assert np.array_equal(buf["b"].cpu().numpy(), b.ravel())
+    assert np.array_equal(buf["xi"].cpu().numpy(), xi.ravel())
+
+
+@pytest.mark.parametrize("scheme", [1, 2])
+def test_init_other_schemes_bit_exact(scheme):
+    c = small(P=3, M=40, init_scheme=scheme, seed=5)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, xi = _oracle_init(c)
+    assert np.array_equal(buf["W"].cpu().numpy(), W.ravel())
+    assert np.array_equal(buf["b"].cpu().numpy(), b.ravel())
+
+
+def _check_assembly(c, ctx, buf, W, b, subdomains):
+    M, q = c["M"], c["q"]
+    oc = ocfg(c)
+    z = ctx.sizes
+    for s in subdomains:
+        K, F, A = O.assemble(oc, s, W, b)
+        xy, edge, gidx = O.rows(oc, s)
+        m = len(edge)
+        Kg = kaug_np(ctx, buf, s)
+        w = W[s]
+        w2 = (w ** 2).sum(1)
+        zabs = 1.0 + np.abs(xy @ w.T) + np.abs(b[s])[None, :]
+        scale = np.where(edge[:, None] < 0, np.maximum(w2[None, :], 1.0), 1.0)
+        err = np.abs(Kg[:m, :M] - K)
+        assert np.all(err <= 32 * EPS * scale * zabs + 1e-300), (s, (err / (scale * zabs)).max() / EPS)
+        assert np.all(Kg[m:, :] == 0.0)
+        # E_Gamma: unit columns at interface rows, zero for Dirichlet edges
+        E = Kg[:, M:M + 4 * q]
+        ref = np.zeros_like(E)
+        for r in np.where(gidx >= 0)[0]:
+            ref[r, r - (m - 4 * q)] = 1.0
+        assert np.array_equal(E, ref)
+        # F = [f; g; 0]
+        Fg = Kg[:m, M + 4 * q]
+        assert np.allclose(Fg, F, rtol=0, atol=4 * EPS * max(1.0, np.abs(F).max()))
+        assert np.all(Fg[gidx >= 0] == 0.0)
+        # flux rows (A^s)^T
+        Ag = at_np(ctx, buf, s, M, q)
+        wn = np.abs(w).max(1)
+        rowpts = xy[m - 4 * q:]
+        zabs_e = 1.0 + np.abs(rowpts @ w.T) + np.abs(b[s])[None, :]
+        errA = np.abs(Ag - A)
+        assert np.all(errA <= 32 * EPS * np.maximum(wn, 1.0)[None, :] * zabs_e), s
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
+def test_assemble_matches_oracle(k):
+    c = WL.config(k)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, _ = _oracle_init(c)
+    N = c["P"] ** 2
+    subs = list(range(N)) if N <= 16 else sorted({0, 1, c["P"] - 1, c["P"] + 1, N // 2 + c["P"] // 2, N - 1})
+    _check_assembly(c, ctx, buf, W, b, subs)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_qr_backward_stable(k):
+    """Q^T [K|E|F] = R_aug: the Gram identity A^T A = R_aug^T R_aug holds to rounding, and the
+    first M columns are upper triangular below their diagonal in the R part (any size)."""
+    c = WL.config(k)
+    M = c["M"]
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    N = c["P"] ** 2
+    subs = [0, N - 1]
+    A0 = {s: kaug_np(ctx, buf, s).copy() for s in subs}
+    ctx.local_factor(buf["Kaug"], buf["tau"], buf["work"])
+    import torch
+
+    torch.cuda.synchronize()
+    for s in subs:
+        A = A0[s]
+        Rf = kaug_np(ctx, buf, s)
+        R = np.zeros_like(Rf)
+        R[:M, :M] = np.triu(Rf[:M, :M])
+        R[:, M:] = Rf[:, M:]
+        nA = np.linalg.norm(A)
+        assert np.linalg.norm(A.T @ A - R.T @ R) <= 1e-12 * nA * nA
+        tau = buf["tau"].view(-1, M)[s].cpu().numpy()
+        assert np.all((tau == 0) | ((tau >= 1.0 - 1e-12) & (tau <= 2.0 + 1e-12)))
+
+
+def test_schur_pieces_entrywise_config0():
+    """Config 0 (well resolved): S1, T_E^T t_F, P_s, q_s equal the oracle's literal pieces of
+    eqn:schur to relative Frobenius 1e-8 (reading R22)."""
+    c = WL.config(0)
+    q = c["q"]
+    ctx, buf, _ = run_gpu(c, upto="schur")
+    W, b, _ = _oracle_init(c)
+    for s in range(4):
+        o = O.local_pieces(ocfg(c), s, W, b)
+        loc, _ = local_iface_index(c, s)
+        Sg = sbuf_np(ctx, buf, s)
+        Pg = pbuf_np(ctx, buf, s, q)
+        ix = np.ix_(loc, loc)
+        assert rel_l2(Sg[ix], o["S1"]) < 1e-8
+        assert rel_l2(Sg[loc, 4 * q], -o["g1"]) < 1e-8
+        assert rel_l2(Pg[ix], -o["PB"]) < 1e-8
+        assert rel_l2(Pg[loc, 4 * q], o["pF"]) < 1e-8
+        # Dirichlet-edge rows / columns are exactly zero
+        dir_ = np.setdiff1d(np.arange(4 * q), loc)
+        assert np.all(Pg[dir_, :] == 0) and np.all(Pg[:, dir_] == 0) and np.all(Sg[dir_, :] == 0)
+
+
+def _interface_system(c):
+    import torch
+
+    ctx, buf, _ = run_gpu(c, upto="schur")
+    ctx.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"])
+    torch.cuda.synchronize()
+    Md = band_to_dense(ctx, buf["Mband"])
+    g = buf["g"].cpu().numpy()[: ctx.sizes["G"]]
+    return ctx, buf, Md, g
+
+
+def test_interface_system_entrywise_config0():
+    c = WL.config(0)
+    ctx, buf, Md, g = _interface_system(c)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, want_system=True)
+    assert rel_l2(Md, r["M"]) < 1e-8
+    assert rel_l2(g, r["g"]) < 1e-8
+
+
+@pytest.mark.parametrize("k", [1])
+def test_interface_cross_residual(k):
+    """Config >= 1: M_gpu u_orc - g_gpu small (the minimiser is unique even where the quadratic
+    form depends on the near-null resolution of K^s, reading R22)."""
+    c = WL.config(k)
+    ctx, buf, Md, g = _interface_system(c)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b)
+    assert np.linalg.norm(Md @ r["uG"] - g) <= 1e-9 * np.linalg.norm(g)
+    assert np.allclose(Md, Md.T)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_end_to_end_u_parity(k):
+    """u on the 101^2 grid: relative L2 <= 1e-6 against the oracle; r_s parity with the oracle's
+    u_Gamma fed to elmddm_back_solve."""
+    import torch
+
+    c = WL.config(k)
+    xy = WL.eval_grid()
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy, nthreads=NCPU)
+    ug = u.cpu().numpy()
+    assert rel_l2(ug, r["u"]) <= 1e-6, rel_l2(ug, r["u"])
+    G = ctx.sizes["G"]
+    assert rel_l2(buf["uG"].cpu().numpy()[:G], r["uG"]) <= 1e-6
+    # residual parity with the SAME u_Gamma (reading R17)
+    uG = torch.zeros(ctx.sizes["G_pad"], dtype=torch.float64, device="cuda")
+    uG[:G] = torch.as_tensor(r["uG"], device="cuda")
+    coef = torch.empty_like(buf["coef"])
+    resid = torch.empty_like(buf["resid"])
+    ctx.back_solve(buf["Kaug"], uG, coef, resid, buf["work"])
+    torch.cuda.synchronize()
+    rg = resid.cpu().numpy()
+    m = ctx.sizes["m"]
+    oc = ocfg(c)
+    for s in range(c["P"] ** 2):
+        K, F, _ = O.assemble(oc, s, W, b) if s < 2 else (None, None, None)
+        if F is None:
+            continue
+        xy_, edge, gidx = O.rows(oc, s)
+        rhs = F.copy()
+        rhs[gidx >= 0] += r["uG"][gidx[gidx >= 0]]
+        floor = 10 * m * EPS * np.linalg.norm(rhs)
+        assert abs(rg[s] - r["resid"][s]) <= 1e-8 * r["resid"][s] + floor
+    # accuracy vs the exact solution is in the same range as the oracle's
+    ue = WL.exact(c["problem"], xy)
+    assert rel_l2(ug, ue) < 10 * rel_l2(r["u"], ue) + 1e-12
+
+
+def _sampled_subdomains(P):
+    N = P * P
+    return sorted({0, P - 1, P * (P // 2) + P // 2, N - 1})
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_large_config_sampled_parity(k):
+    """Full BASELINE sizes in the bench launch configuration: for sampled subdomains the oracle
+    back-solves with the GPU's u_Gamma; r_s and u at the owned grid points must agree."""
+    import torch
+
+    c = WL.config(k)
+    xy = WL.eval_grid()
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    G = ctx.sizes["G"]
+    uG = buf["uG"].cpu().numpy()[:G]
+    rg = buf["resid"].cpu().numpy()
+    coef_g = buf["coef"].view(-1, c["M"]).cpu().numpy()
+    ug = u.cpu().numpy()
+    oc = ocfg(c)
+    subs = _sampled_subdomains(c["P"])
+
+    def one(s):
+        return s, O.local_pieces(oc, s, W, b, uG)
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(NCPU, len(subs)))) as ex:
+        res = dict(ex.map(one, subs))
+    P = c["P"]
+    own = np.minimum((xy * P).astype(int), P - 1)
+    owner = own[:, 1] * P + own[:, 0]
+    m = ctx.sizes["m"]
+    for s in subs:
+        o = res[s]
+        K, F, _ = O.assemble(oc, s, W, b)
+        xy_, edge, gidx = O.rows(oc, s)
+        rhs = F.copy()
+        rhs[gidx >= 0] += uG[gidx[gidx >= 0]]
+        floor = 10 * m * EPS * np.linalg.norm(rhs)
+        assert abs(rg[s] - o["resid"]) <= 1e-8 * o["resid"] + floor, (s, rg[s], o["resid"], floor)
+        pts = xy[owner == s]
+        if len(pts):
+            uo = O.evaluate(oc, W, b, np.where(np.arange(P * P)[:, None] == s, o["coef"][None, :], coef_g), pts)
+            assert rel_l2(ug[owner == s], uo) <= 1e-6
+    # and the global solution is accurate (SURVEY §8(c) convergence row magnitudes)
+    ue = WL.exact(c["problem"], xy)
+    assert rel_l2(ug, ue) < 1e-8
+
+
+# ------------------------------------------------------------------------------------------------
+# edge cases
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfgkw", [
+    dict(P=1, M=24, p=10, q=6, problem=4),          # single subdomain: classical ELM, G = 0
+    dict(P=2, M=40, p=9, q=6, problem=1),           # M not a multiple of the 64-panel, odd p
+    dict(P=3, M=72, p=11, q=10, problem=2),         # 3 x 3 (interior subdomain with 4 faces)
+    dict(P=2, M=8, p=3, q=2, problem=0),            # minimal sizes
+    dict(P=4, M=136, p=13, q=14, problem=0, init_scheme=1),
+])
+def test_edge_configs_end_to_end(cfgkw):
+    c = small(**cfgkw)
+    xy = WL.eval_grid(21)
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy)
+    assert rel_l2(u.cpu().numpy(), r["u"]) <= 1e-6
+    if c["P"] == 1:
+        assert ctx.sizes["G"] == 0
+        K, F, _ = O.assemble(ocfg(c), 0, W, b)
+        cg = buf["coef"].cpu().numpy()
+        ref = np.linalg.lstsq(K, F, rcond=None)[0]
+        assert np.allclose(K @ cg, K @ ref, atol=1e-9 * np.abs(F).max())
+
+
+def test_homogeneous_problem_is_exactly_zero():
+    c = small(P=3, M=24, p=7, q=6, problem=5)
+    xy = WL.eval_grid(11)
+    ctx, buf, u = run_gpu(c, xy)
+    assert np.all(u.cpu().numpy() == 0.0)
+    assert np.all(buf["uG"].cpu().numpy() == 0.0)
+    assert np.all(buf["resid"].cpu().numpy() == 0.0)
+
+
+def test_evaluate_empty_and_outside_range():
+    import torch
+
+    c = small()
+    ctx, buf, _ = run_gpu(c)
+    u = torch.full((3,), 7.0, dtype=torch.float64, device="cuda")
+    ctx.evaluate(buf["W"], buf["b"], buf["coef"], torch.empty(0, dtype=torch.float64, device="cuda"), u)
+    assert torch.all(u == 7.0)
+
+
+def test_deterministic_and_rank_split_bit_identical():
+    """Two runs are bit-identical, and splitting the subdomains over two contexts (emulated
+    ranks, run one after the other) and summing their zero-filled Pbuf/Sbuf gives the same bits
+    as one context -- the NCCL reduce of DESIGN.md §6 is exact."""
+    import torch
+
+    c = WL.config(1)
+    xy = WL.eval_grid(31)
+    _, b1, u1 = run_gpu(c, xy)
+    _, b2, u2 = run_gpu(c, xy)
+    assert torch.equal(u1, u2) and torch.equal(b1["uG"], b2["uG"])
+    N = c["P"] ** 2
+    parts = []
+    for s0, s1 in [(0, N // 2), (N // 2, N)]:
+        ctx, buf = gpu_ctx(c, s0, s1)
+        ctx.init_hidden(buf["W"], buf["b"])
+        ctx.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"])
+        ctx.local_factor(buf["Kaug"], buf["tau"], buf["work"])
+        ctx.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"])
+        parts.append((ctx, buf))
+    torch.cuda.synchronize()
+    Psum = parts[0][1]["Pbuf"] + parts[1][1]["Pbuf"]
+    Ssum = parts[0][1]["Sbuf"] + parts[1][1]["Sbuf"]
+    assert torch.equal(Psum, b1["Pbuf"]) and torch.equal(Ssum, b1["Sbuf"])
+    ctx0, buf0 = parts[0]
+    ctx0.interface_solve(Psum, Ssum, buf0["Mband"], buf0["g"], buf0["uG"], buf0["work"])
+    assert torch.equal(buf0["uG"], b1["uG"])
+
+
+def test_interface_points_export():
+    c = WL.config(1)
+    ctx, buf = gpu_ctx(c)
+    xy = ctx.interface_points()
+    oc = ocfg(c)
+    ref = np.zeros_like(xy)
+    for s in range(16):
+        p, edge, gidx = O.rows(oc, s)
+        ref[gidx[gidx >= 0]] = p[gidx >= 0]
+    assert np.array_equal(xy, ref)
