@@ -1,0 +1,357 @@
+"""bench.py -- DDM-ELM hot path on B200: time-to-solution and subdomain LSQ solves/s.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl elmddm|reference]
+For N > 1 the driver launches it with torch.distributed.run (one rank per GPU, NCCL).
+
+A step = one pass of the whole hot path: init_hidden, assemble,
+local_factor, schur_accumulate, [NCCL reduce], interface_solve (rank 0), [NCCL broadcast],
+back_solve, evaluate on the 101^2 grid.  value = subdomains solved per second over the whole job
+(N_subdomains * K / max-over-ranks device time).  Inputs are generated on the device from the
+seed (synthetic, seeded); the 11 GB K_aug written every step exceeds L2 (126 MB),
+so no extra flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as WL  # noqa: E402
+
+METRIC = "ddm_elm_subdomain_lsq_solves_per_s"
+UNIT = "subdomain-solves/s"
+NOMINAL_FP64_TFLOPS = 40.0     # B200 FP64 / FP64-tensor datasheet figure
+NOMINAL_BF16_TFLOPS = 2250.0   # B200 dense bf16 (B200_PROFILING.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=WL.BENCH_CONFIG)
+    ap.add_argument("--impl", default="elmddm", choices=["elmddm", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="print per-phase breakdown to stderr")
+    return ap.parse_args()
+
+
+def workload_desc(k: int) -> str:
+    c = WL.config(k)
+    m = c["p"] ** 2 + 4 * c["q"]
+    names = {0: "sin(pi x)sin(pi y)", 1: "e^(x+y)sin(2pi x)cos(2pi y)", 2: "sin(4pi x)sin(4pi y)",
+             3: "sin(8pi x)sin(8pi y)"}
+    return (f"cfg{k}: 2D Poisson -Lap u=f on (0,1)^2, u={names.get(c['problem'])}, {c['P']}x{c['P']} subdomains, "
+            f"M={c['M']} tanh neurons/subdomain, {c['p']}x{c['p']} interior + {c['q']}/edge points "
+            f"(local LS {m}x{c['M']}), seed {c['seed']}, eval 101x101")
+
+
+# ------------------------------------------------------------------------------------------------
+# algorithmic work, per subdomain summed over the ranks' subdomains
+# ------------------------------------------------------------------------------------------------
+def algorithmic(c: dict, s_range) -> dict:
+    P, M, p, q = c["P"], c["M"], c["p"], c["q"]
+    m = p * p + 4 * q
+    fl_qr = 0.0
+    bytes_asm = 0.0
+    fl_schur = 0.0
+    for s in range(*s_range):
+        i, j = s % P, s // P
+        n_if = (i > 0) + (i < P - 1) + (j > 0) + (j < P - 1)
+        mg = n_if * q
+        k = mg + 1
+        fl_qr += 2 * m * M * M - 2.0 / 3.0 * M ** 3 + 2 * M * k * (2 * m - M)
+        bytes_asm += 8.0 * (m * M + m + mg * M)
+        fl_schur += mg * M * M + 2 * mg * k * M + 2 * (m - M) * k * k / 2
+    return {"flop_qr": fl_qr, "bytes_assemble": bytes_asm, "flop_schur": fl_schur}
+
+
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args, world, rank):
+    """The oracle (plain C, fp64) on the box's host cores: each step is a bounded sample of the
+    workload -- the local phase (assembly + unblocked QR + literal Schur pieces + back-solve) of
+    n_cores subdomains; value = subdomains per second."""
+    if rank != 0:
+        return
+    import oracle as O
+
+    c = WL.config(args.config)
+    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
+    W, b, _, _ = O.init_hidden(oc)
+    cores = len(os.sched_getaffinity(0))
+    N = c["P"] ** 2
+    G = O.geometry(oc)["G"]
+    uG = np.zeros(max(G, 1))
+    rng = np.random.default_rng(0)
+    n = cores
+    times = []
+    for it in range(args.warmup + args.steps):
+        s_list = rng.choice(N, size=min(n, N), replace=False)
+        t = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
+        if it >= args.warmup:
+            times.append((t, len(s_list)))
+    tot_t = sum(t for t, _ in times)
+    tot_n = sum(k for _, k in times)
+    val = tot_n / tot_t
+    sample = (f"per step: local phase (assemble, unblocked Householder QR, literal eqn:schur pieces, back-solve) "
+              f"of {n} random subdomains of cfg{args.config} on {cores} threads; interface solve excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config)},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(c, k):
+    """Oracle timed on a bounded sample of the same workload (about 10-30 s)."""
+    import oracle as O
+
+    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
+    W, b, _, _ = O.init_hidden(oc)
+    cores = len(os.sched_getaffinity(0))
+    N = c["P"] ** 2
+    G = O.geometry(oc)["G"]
+    uG = np.zeros(max(G, 1))
+    n = min(N, cores)
+    s_list = np.random.default_rng(1).choice(N, size=n, replace=False)
+    t = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
+    return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"local phase (assemble + unblocked QR + literal Schur pieces + back-solve) of {n} random "
+                      f"subdomains of cfg{k}, {t:.1f} s on {cores} threads; interface solve excluded"}
+
+
+class PhaseTimer:
+    def __init__(self, torch, stream):
+        self.torch, self.stream = torch, stream
+        self.events = []
+
+    def mark(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        self.events.append((name, e))
+
+    def result(self):
+        self.torch.cuda.synchronize()
+        out = {}
+        for (n0, e0), (n1, e1) in zip(self.events, self.events[1:]):
+            out[n1] = out.get(n1, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_15959_b200 as E
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    c = WL.config(args.config)
+    prob = E.Problem.from_config(c)
+    N = c["P"] ** 2
+    s0, s1 = E.partition(N, world, rank)
+    ctx = E.Context(prob, s0, s1, local_rank)
+    buf = ctx.alloc()
+    stream = torch.cuda.current_stream()
+    xy_host = WL.eval_grid()
+    xy = torch.as_tensor(xy_host.reshape(-1), device="cuda")
+    u = torch.zeros(xy_host.shape[0], dtype=torch.float64, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ctx.run(buf, xy, u)
+    barrier()
+    ctx.timing(reset=True)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            ctx.run(buf, xy, u)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1)
+    launches = ctx.timing(reset=True)["launches"]
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_per_step = ms_max / args.steps
+    value = N * args.steps / (ms_max * 1e-3)
+
+    # accuracy of the measured solution (u on rank 0 after the reduce)
+    ue = WL.exact(c["problem"], xy_host)
+    err = float(np.linalg.norm(u.cpu().numpy() - ue) / np.linalg.norm(ue)) if rank == 0 else None
+
+    # per-kernel-class device time over K instrumented steps (CUDA events on the launch stream)
+    ctx.set_timing(True)
+    ph = PhaseTimer(torch, stream)
+    barrier()
+    ph.mark("start")
+    for _ in range(args.steps):
+        ctx.run(buf, xy, u, timer=ph)
+    barrier()
+    phases = ph.result()
+    kt = ctx.timing(reset=True)
+    ctx.set_timing(False)
+    phases = {k: v / args.steps for k, v in phases.items()}
+    kms = {k: v / args.steps for k, v in kt["ms"].items()}
+
+    # end to end through the public API with host buffers: H2D of the evaluation points from
+    # pinned memory, the hot path, D2H of u, u_Gamma, coefficients and residuals, every step
+    e2e = None
+    if not args.no_e2e:
+        xy_pin = torch.as_tensor(xy_host.reshape(-1)).pin_memory()
+        G = ctx.sizes["G"]
+        u_pin = torch.empty(u.numel(), dtype=torch.float64).pin_memory()
+        uG_pin = torch.empty(G, dtype=torch.float64).pin_memory()
+        coef_pin = torch.empty(buf["coef"].numel(), dtype=torch.float64).pin_memory()
+        res_pin = torch.empty(buf["resid"].numel(), dtype=torch.float64).pin_memory()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            xy.copy_(xy_pin, non_blocking=True)
+            ctx.run(buf, xy, u)
+            u_pin.copy_(u, non_blocking=True)
+            uG_pin.copy_(buf["uG"][:G], non_blocking=True)
+            coef_pin.copy_(buf["coef"], non_blocking=True)
+            res_pin.copy_(buf["resid"], non_blocking=True)
+        e1.record(stream)
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": N * args.steps / (float(ems.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(xy_pin.numel() * 8),
+               "d2h_bytes_per_step": int((u_pin.numel() + uG_pin.numel() + coef_pin.numel() + res_pin.numel()) * 8),
+               "ms_per_step": float(ems.item()) / args.steps}
+
+    # roofline of the dominant kernel class (QR trailing-update GEMMs on the FP64 tensor pipe)
+    work = algorithmic(c, (s0, s1))
+    pk, src = peaks()
+    dmma = E.solver.dmma_peak_tflops(local_rank, 300.0)
+    fp64_peak = pk["bf16_tflops_sustained"] * NOMINAL_FP64_TFLOPS / NOMINAL_BF16_TFLOPS
+    qr_ms = kms["gemm_qr"] + kms["panel"]
+    # algorithmic Householder flop of the whole factorisation (H3), attributed to the phase time
+    achieved_qr = work["flop_qr"] / (qr_ms * 1e-3) / 1e12 if qr_ms > 0 else None
+    gemm_share = kms["gemm_qr"] / max(sum(kms.values()), 1e-12)
+    roof = {"bound": "tensor", "achieved": achieved_qr, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": (achieved_qr / fp64_peak) if achieved_qr else None, "traffic": None,
+            "kernel": "local_factor (QR panel blocks + DMMA trailing GEMMs), fp64",
+            "peak_source": f"{src}: bf16_tflops_sustained x {NOMINAL_FP64_TFLOPS}/{NOMINAL_BF16_TFLOPS} "
+                           f"(nominal FP64/bf16 ratio)",
+            "dmma_probe_tflops": dmma, "frac_of_dmma_probe": (achieved_qr / dmma) if achieved_qr and dmma else None,
+            "share_of_step": (qr_ms / max(sum(kms.values()), 1e-12)), "gemm_qr_share": gemm_share}
+    asm_ms = kms["assemble"]
+    roof_asm = {"bound": "hbm", "achieved": work["bytes_assemble"] / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
+                "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    roof_asm["frac"] = roof_asm["achieved"] / roof_asm["peak"] if roof_asm["achieved"] else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(c, args.config)
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_desc(args.config), "subdomains": N, "l2_flush":
+                           "inputs larger than L2: every step writes K_aug (S*ld*ncols*8 B) >> 126 MB",
+                           "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast"},
+                "time_to_solution_ms": ms_per_step, "rel_l2_vs_exact": err,
+                "roofline": roof, "roofline_assembly": roof_asm, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "launches_per_step": launches / args.steps, "clocks": clocks,
+                "phases_ms": phases, "kernel_class_ms": kms,
+                "algorithmic": {k: v for k, v in work.items()}}
+        print(json.dumps(line), flush=True)
+        if args.phases:
+            print(json.dumps({"phases_ms": phases, "kernel_class_ms": kms}, indent=1), file=sys.stderr)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -158,6 +158,37 @@ elmddm_status elmddm_back_solve(elmddm_ctx* ctx, const double* Kaug, const doubl
 elmddm_status elmddm_evaluate(elmddm_ctx* ctx, const double* W, const double* b, const double* coef,
                               const double* xy, int64_t n, double* u, void* stream);
 
+/* ---- instrumentation (measurement only; no effect on results) ------------------------------ */
+/* kernel classes timed by elmddm_timing */
+enum {
+    ELMDDM_K_INIT = 0,       /* init_hidden                                   */
+    ELMDDM_K_ASSEMBLE = 1,   /* assembly of K_aug and At                      */
+    ELMDDM_K_PANEL = 2,      /* QR panel base blocks                          */
+    ELMDDM_K_GEMM_QR = 3,    /* QR compact-WY trailing-update GEMMs (DMMA)    */
+    ELMDDM_K_TRSM = 4,       /* R11^{-T} At diagonal-block solves             */
+    ELMDDM_K_GEMM_SCHUR = 5, /* TRSM updates, flux product, Gram (DMMA)       */
+    ELMDDM_K_IFACE = 6,      /* Q-row gather, M / g assembly (+ Q^T Q GEMM)   */
+    ELMDDM_K_POTRF = 7,      /* band Cholesky diagonal + panel solves         */
+    ELMDDM_K_GEMM_CHOL = 8,  /* band Cholesky SYRK updates (DMMA)             */
+    ELMDDM_K_TRSV = 9,       /* interface forward / backward substitution     */
+    ELMDDM_K_BACK = 10,      /* local back-solve                              */
+    ELMDDM_K_EVAL = 11,      /* evaluation                                    */
+    ELMDDM_NCLASS = 12
+};
+typedef struct {
+    int64_t launches;              /* kernels launched by this context since the last reset    */
+    int64_t count[ELMDDM_NCLASS];  /* launches per class                                        */
+    double ms[ELMDDM_NCLASS];      /* summed device time per class (CUDA events on the launch
+                                      stream; only while timing is enabled)                     */
+} elmddm_timing_t;
+/* enable != 0: record a CUDA event pair around every kernel launch (adds ~2 us per launch). */
+elmddm_status elmddm_set_timing(elmddm_ctx* ctx, int enable);
+/* Synchronises the device, fills *out (may be NULL) and, if reset != 0, clears the counters. */
+elmddm_status elmddm_timing(elmddm_ctx* ctx, elmddm_timing_t* out, int reset);
+/* Diagnostic: sustained FP64 tensor (DMMA.8x8x4) throughput of `device`, measured with a
+ * register-resident mma.sync loop on every SM for about `ms` milliseconds.  Synchronous.        */
+elmddm_status elmddm_dmma_probe(int device, double ms, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

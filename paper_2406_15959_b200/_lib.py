@@ -44,7 +44,15 @@ EXPORTS = [
     "elmddm_interface_points", "elmddm_band_index", "elmddm_init_hidden", "elmddm_assemble",
     "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
     "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
+    "elmddm_set_timing", "elmddm_timing", "elmddm_dmma_probe",
 ]
+
+KCLASSES = ["init", "assemble", "panel", "gemm_qr", "trsm", "gemm_schur", "iface", "potrf", "gemm_chol", "trsv",
+            "back", "eval"]
+
+
+class Timing(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("count", C.c_int64 * 12), ("ms", C.c_double * 12)]
 
 _lib = None
 
@@ -79,13 +87,17 @@ def load():
     L.elmddm_interface_solve.argtypes = [ctxp, vp, vp, vp, vp, vp, vp, vp]
     L.elmddm_back_solve.argtypes = [ctxp, vp, vp, vp, vp, vp, vp]
     L.elmddm_evaluate.argtypes = [ctxp, vp, vp, vp, vp, i64, vp, vp]
+    L.elmddm_set_timing.argtypes = [ctxp, C.c_int]
+    L.elmddm_timing.argtypes = [ctxp, C.POINTER(Timing), C.c_int]
+    L.elmddm_dmma_probe.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_double)]
     for name in EXPORTS:
         f = getattr(L, name)
         if f.restype is C.c_int or name in ("elmddm_create",):
             f.restype = st
     for name in ["elmddm_create", "elmddm_sizes", "elmddm_sync", "elmddm_interface_points", "elmddm_init_hidden",
                  "elmddm_assemble", "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
-                 "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate"]:
+                 "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
+                 "elmddm_set_timing", "elmddm_timing", "elmddm_dmma_probe"]:
         getattr(L, name).restype = st
     _lib = L
     return L

@@ -298,6 +298,7 @@ __global__ void k_evaluate(elmddm_config cfg, const double* __restrict__ W, cons
 cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double* xi, cudaStream_t st) {
     int64_t n = c->sz.S * c->cfg.M;
     int nt = 128;
+    KTimer kt(c, ELMDDM_K_INIT, st);
     k_init_hidden<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, xi);
     return cudaGetLastError();
 }
@@ -305,10 +306,12 @@ cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double
 cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
                             cudaStream_t st) {
     dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
-    k_assemble<<<g1, AS_NT, 0, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug);
+    { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
+    k_assemble<<<g1, AS_NT, 0, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 g2(4, (unsigned)c->sz.S);
+    KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
     k_assemble_at<<<g2, AS_NT, 0, st>>>(c->cfg, W, b, At);
     return cudaGetLastError();
 }
@@ -317,6 +320,7 @@ cudaError_t launch_evaluate(const elmddm_ctx* c, const double* W, const double* 
                             const double* xy, int64_t n, double* u, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int nt = 128;
+    KTimer kt(c, ELMDDM_K_EVAL, st);
     k_evaluate<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, coef, xy, n, u);
     return cudaGetLastError();
 }

@@ -183,22 +183,25 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     if ((e = cudaMemcpyAsync(y, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
     for (int k = 0; k < nblk; ++k) {
         const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
-        k_potrf_trsm<<<1 + nsub, 256, 0, st>>>(Mband, LD, k, NB, c->d_status);
+        { KTimer kt(c, ELMDDM_K_POTRF, st);
+        k_potrf_trsm<<<1 + nsub, 256, 0, st>>>(Mband, LD, k, NB, c->d_status); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (nsub > 0) {
             const int64_t r0 = (int64_t)(k + 1) * NB, k0 = (int64_t)k * NB;
             GemmArgs gs{nsub * NB, nsub * NB, NB, Mband + r0 + k0 * LD, LD, 0, Mband + r0 + k0 * LD, LD, 0,
                         Mband + r0 + r0 * LD, LD, 0, -1.0, 1.0, 1, 1};
-            if ((e = gemm_launch(false, true, gs, st)) != cudaSuccess) return e;
+            if ((e = gemm_launch(false, true, gs, st, c, ELMDDM_K_GEMM_CHOL)) != cudaSuccess) return e;
         }
     }
     for (int k = 0; k < nblk; ++k) {
         const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
+        KTimer kt(c, ELMDDM_K_TRSV, st);
         k_fwd<<<1 + nsub, 128, 0, st>>>(Mband, LD, k, NB, y, z);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     for (int k = nblk - 1; k >= 0; --k) {
         const int nsub = k < nbw ? k : nbw;
+        KTimer kt(c, ELMDDM_K_TRSV, st);
         k_bwd<<<1 + nsub, 128, 0, st>>>(Mband, LD, k, NB, z, uG);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -16,11 +16,6 @@ namespace {
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
-bool set_err(elmddm_ctx* c, const std::string& s) {
-    if (c) c->err = s;
-    return false;
-}
-
 elmddm_status cuda_fail(elmddm_ctx* c, cudaError_t e, const char* where) {
     if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
     return ELMDDM_ECUDA;
@@ -291,6 +286,11 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
 void elmddm_destroy(elmddm_ctx* c) {
     if (!c) return;
     DeviceGuard dg(c->device);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto& p : c->ev_pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
     cudaFree(c->d_status);
     cudaFree(c->d_sub_face);
     cudaFree(c->d_qsrc);
@@ -459,6 +459,41 @@ elmddm_status elmddm_evaluate(elmddm_ctx* c, const double* W, const double* b, c
     DeviceGuard dg(c->device);
     cudaError_t e = launch_evaluate(c, W, b, coef, xy, n, u, (cudaStream_t)stream);
     return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_evaluate");
+}
+
+elmddm_status elmddm_set_timing(elmddm_ctx* c, int enable) {
+    CHECK_CTX(c);
+    c->timing = enable != 0;
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_timing(elmddm_ctx* c, elmddm_timing_t* out, int reset) {
+    CHECK_CTX(c);
+    DeviceGuard dg(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_timing");
+    for (auto& p : c->ev_pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) c->cls_ms[p.first] += ms;
+        c->ev_pool.push_back(p.second.first);
+        c->ev_pool.push_back(p.second.second);
+    }
+    c->ev_pending.clear();
+    if (out) {
+        out->launches = c->launches;
+        for (int k = 0; k < ELMDDM_NCLASS; ++k) {
+            out->count[k] = c->cls_count[k];
+            out->ms[k] = c->cls_ms[k];
+        }
+    }
+    if (reset) {
+        c->launches = 0;
+        for (int k = 0; k < ELMDDM_NCLASS; ++k) {
+            c->cls_count[k] = 0;
+            c->cls_ms[k] = 0.0;
+        }
+    }
+    return ELMDDM_OK;
 }
 
 }  // extern "C"

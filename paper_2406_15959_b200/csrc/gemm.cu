@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
 }
 
 template <bool TA, bool TB>
-cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
+cudaError_t launch(const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c, int cls) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -160,18 +160,69 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
         attr = true;
     }
     dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
+    KTimer kt(c, cls, st);
     k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, st>>>(g);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st) {
+cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c,
+                        int cls) {
     if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
     if (g.K <= 0) {
         // C = beta C (only used with beta = 1 in this library)
         return cudaSuccess;
     }
-    if (transA) return transB ? launch<true, true>(g, st) : launch<true, false>(g, st);
-    return transB ? launch<false, true>(g, st) : launch<false, false>(g, st);
+    if (transA) return transB ? launch<true, true>(g, st, c, cls) : launch<true, false>(g, st, c, cls);
+    return transB ? launch<false, true>(g, st, c, cls) : launch<false, false>(g, st, c, cls);
+}
+
+// ---- diagnostic: sustained DMMA throughput (register-resident operands, 8 independent chains) ----
+namespace {
+__global__ void __launch_bounds__(256) k_dmma_probe(int64_t iters, double* out) {
+    double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 1.2345) out[0] = s;  // keep the work alive
+}
+}  // namespace
+
+extern "C" elmddm_status elmddm_dmma_probe(int device, double ms, double* tflops) {
+    if (!tflops || !(ms > 0)) return ELMDDM_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return ELMDDM_ECUDA;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    double* out;
+    if (cudaMalloc(&out, 8) != cudaSuccess) return ELMDDM_ECUDA;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = nsm * 4, threads = 256;
+    int64_t iters = 4096;
+    float t = 0.f;
+    for (int pass = 0; pass < 8; ++pass) {
+        cudaEventRecord(e0);
+        k_dmma_probe<<<blocks, threads>>>(iters, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&t, e0, e1);
+        if (t >= ms) break;
+        iters = (int64_t)(iters * (ms / (t > 0.01f ? t : 0.01f)) * 1.1);
+    }
+    // one DMMA.8x8x4 = 256 FMA = 512 flop per warp instruction
+    double flop = (double)blocks * (threads / 32) * (double)iters * 8.0 * 512.0;
+    *tflops = flop / (t * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return cudaGetLastError() == cudaSuccess ? ELMDDM_OK : ELMDDM_ECUDA;
 }

@@ -51,6 +51,49 @@ struct elmddm_ctx {
     int npairs = 0, nterms = 0, ngterms = 0;
     int qrow_ld = 0, qrow_cols = 0, ga_ld = 0;  // Q row block: q x (7q+1), ld qrow_ld; Ga: ga_ld^2
     int64_t work_factor = 0, work_iface = 0, work_back = 0;
+
+    // instrumentation (mutable: launch wrappers take a const context)
+    mutable int timing = 0;
+    mutable int64_t launches = 0;
+    mutable int64_t cls_count[ELMDDM_NCLASS] = {};
+    mutable double cls_ms[ELMDDM_NCLASS] = {};
+    mutable std::vector<cudaEvent_t> ev_pool;                 // free events
+    mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+};
+
+// RAII probe around one kernel launch: counts it and, when timing is on, brackets it with a
+// CUDA event pair on the launch stream.
+struct KTimer {
+    const elmddm_ctx* c;
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KTimer(const elmddm_ctx* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+        if (!c) return;
+        ++c->launches;
+        ++c->cls_count[cls];
+        if (c->timing) {
+            a = take();
+            b = take();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~KTimer() {
+        if (c && c->timing && a) {
+            cudaEventRecord(b, st);
+            c->ev_pending.push_back({cls, {a, b}});
+        }
+    }
+    cudaEvent_t take() {
+        if (!c->ev_pool.empty()) {
+            cudaEvent_t e = c->ev_pool.back();
+            c->ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
 };
 
 // ------------------------------------------------------------------------------------------
@@ -68,7 +111,8 @@ struct GemmArgs {
     int batch;
     int lower_only;  // skip 64x64 output tiles strictly above the diagonal
 };
-cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st);
+cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st,
+                        const elmddm_ctx* c = nullptr, int cls = ELMDDM_K_GEMM_QR);
 
 // kernels in the other translation units
 cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double* xi, cudaStream_t st);

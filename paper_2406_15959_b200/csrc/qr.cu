@@ -304,6 +304,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         const size_t smem = panel_smem_bytes(ld - j0);
         for (int blk = 0; blk < nb / ELM_BB; ++blk) {
             pa.blk = blk;
+            KTimer kt(c, ELMDDM_K_PANEL, st);
             k_panel_block<<<(unsigned)S, PNT, smem, st>>>(pa);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
@@ -313,15 +314,15 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         // W = V^T C
         GemmArgs g1{nb, n_tr, R, Vbuf + j0, ld, ELM_NB * ld, Kaug + j0 + (int64_t)(j0 + nb) * ld, ld, ld * ncols,
                     Wbuf, ELM_NB, ELM_NB * ncols, 1.0, 0.0, (int)S, 0};
-        if ((e = gemm_launch(true, false, g1, st)) != cudaSuccess) return e;
+        if ((e = gemm_launch(true, false, g1, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
         // Z = T^T W
         GemmArgs g2{nb, n_tr, nb, Tbuf, ELM_NB, ELM_NB * ELM_NB, Wbuf, ELM_NB, ELM_NB * ncols, Zbuf, ELM_NB,
                     ELM_NB * ncols, 1.0, 0.0, (int)S, 0};
-        if ((e = gemm_launch(true, false, g2, st)) != cudaSuccess) return e;
+        if ((e = gemm_launch(true, false, g2, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
         // C -= V Z
         GemmArgs g3{R, n_tr, nb, Vbuf + j0, ld, ELM_NB * ld, Zbuf, ELM_NB, ELM_NB * ncols,
                     Kaug + j0 + (int64_t)(j0 + nb) * ld, ld, ld * ncols, -1.0, 1.0, (int)S, 0};
-        if ((e = gemm_launch(false, false, g3, st)) != cudaSuccess) return e;
+        if ((e = gemm_launch(false, false, g3, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

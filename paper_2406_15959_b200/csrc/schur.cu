@@ -220,6 +220,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     for (int i0 = 0; i0 < M; i0 += 64) {
         const int bi = (M - i0) < 64 ? (M - i0) : 64;
         dim3 g((nat + 63) / 64, (unsigned)S);
+        KTimer kt(c, ELMDDM_K_TRSM, st);
         k_trsm_lt_diag<<<g, 64, 0, st>>>(Kaug, ld, ncols, At, M, nat, i0, bi);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         const int rest = M - (i0 + bi);
@@ -227,7 +228,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
             // At[i0+bi:, :] -= R[i0:i0+bi, i0+bi:]^T X_i
             GemmArgs ga{rest, nat, bi, Kaug + i0 + (int64_t)(i0 + bi) * ld, ld, ld * ncols, At + i0, M,
                         (int64_t)M * nat, At + i0 + bi, M, (int64_t)M * nat, -1.0, 1.0, (int)S, 0};
-            if ((e = gemm_launch(true, false, ga, st)) != cudaSuccess) return e;
+            if ((e = gemm_launch(true, false, ga, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
         }
     }
     const int64_t s0 = c->cfg.s_begin;
@@ -235,12 +236,12 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     // P_s = W_s [R12 | y]   (4q x kaug)
     GemmArgs gp{nat, (int)kaug, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
                 Pbuf + s0 * pstride, c->sz.pbuf_ld, pstride, 1.0, 0.0, (int)S, 0};
-    if ((e = gemm_launch(true, false, gp, st)) != cudaSuccess) return e;
+    if ((e = gemm_launch(true, false, gp, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
     // S_s = [T_E | t_F]^T [T_E | t_F]
     const int Kt = (int)(ld - M);
     GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
                 ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 0};
-    return gemm_launch(true, false, gs, st);
+    return gemm_launch(true, false, gs, st, c, ELMDDM_K_GEMM_SCHUR);
 }
 
 cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
@@ -255,23 +256,27 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
     cudaError_t e;
     if ((e = cudaMemsetAsync(Mband, 0, sizeof(double) * c->sz.band_elems, st)) != cudaSuccess) return e;
     if (F > 0) {
+        { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_qrow<<<dim3((unsigned)F, 8), 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_qsrc, q, Qrow, c->qrow_ld,
-                                                      qstride);
+                                                      qstride); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         // Ga[a] = Qrow[a]^T Qrow[a]
         GemmArgs gg{c->qrow_cols, c->qrow_cols, q, Qrow, c->qrow_ld, qstride, Qrow, c->qrow_ld, qstride, Ga, c->ga_ld,
                     gstride, 1.0, 0.0, (int)F, 0};
-        if ((e = gemm_launch(true, false, gg, st)) != cudaSuccess) return e;
+        if ((e = gemm_launch(true, false, gg, st, c, ELMDDM_K_IFACE)) != cudaSuccess) return e;
+        { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_massemble<<<(unsigned)c->npairs, 256, 0, st>>>(c->d_pair_ptr, c->d_pair_bc, c->d_terms, Sbuf, sstride,
                                                           c->sz.sbuf_ld, Ga, gstride, c->ga_ld, q, Mband,
-                                                          c->sz.band_ld);
+                                                          c->sz.band_ld); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_gassemble<<<(unsigned)F, 128, 0, st>>>(c->d_gterm_ptr, c->d_gterms, Sbuf, sstride, c->sz.sbuf_ld, Ga,
-                                                  gstride, c->ga_ld, q, g);
+                                                  gstride, c->ga_ld, q, g); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const int64_t npad = c->sz.G_pad - c->sz.G;
     if (npad > 0) {
+        KTimer kt(c, ELMDDM_K_IFACE, st);
         k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->sz.band_ld, g, c->sz.G, c->sz.G_pad);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
@@ -283,9 +288,11 @@ cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols;
     double* z = work;
     dim3 g1((unsigned)((ld + 255) / 256), (unsigned)S);
-    k_bs_gemv<<<g1, 256, sizeof(double) * c->sz.kaug, st>>>(c->cfg, Kaug, ld, ncols, c->d_sub_face, uG, z);
+    { KTimer kt(c, ELMDDM_K_BACK, st);
+    k_bs_gemv<<<g1, 256, sizeof(double) * c->sz.kaug, st>>>(c->cfg, Kaug, ld, ncols, c->d_sub_face, uG, z); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    KTimer kt(c, ELMDDM_K_BACK, st);
     k_bs_trsv<<<(unsigned)S, 512, 0, st>>>(Kaug, ld, ncols, c->cfg.M, z, coef, resid);
     return cudaGetLastError();
 }

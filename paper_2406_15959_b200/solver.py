@@ -159,6 +159,16 @@ class Context:
         self._check(self.L.elmddm_interface_points(self.h, xy.ctypes.data_as(C.c_void_p)), "interface_points")
         return xy
 
+    def set_timing(self, enable: bool):
+        self._check(self.L.elmddm_set_timing(self.h, 1 if enable else 0), "set_timing")
+
+    def timing(self, reset: bool = True) -> dict:
+        t = _lib.Timing()
+        self._check(self.L.elmddm_timing(self.h, C.byref(t), 1 if reset else 0), "timing")
+        return {"launches": int(t.launches),
+                "count": {k: int(t.count[i]) for i, k in enumerate(_lib.KCLASSES)},
+                "ms": {k: float(t.ms[i]) for i, k in enumerate(_lib.KCLASSES)}}
+
     def band_index(self, i, j):
         return int(self.L.elmddm_band_index(self.h, i, j))
 
@@ -234,3 +244,13 @@ def solve(prob: Problem, xy_host=None, device: int | None = None, group=None, re
     if return_all:
         out["ctx"], out["buf"] = ctx, buf
     return out
+
+
+def dmma_peak_tflops(device: int = 0, ms: float = 200.0) -> float:
+    """Measured sustained FP64 tensor (DMMA) throughput of `device` (diagnostic)."""
+    L = _lib.load()
+    out = C.c_double()
+    rc = L.elmddm_dmma_probe(device, ms, C.byref(out))
+    if rc != 0:
+        raise _lib.ElmddmError(f"elmddm_dmma_probe: {_lib.STATUS.get(rc, rc)}")
+    return float(out.value)
