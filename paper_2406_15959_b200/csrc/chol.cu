@@ -15,25 +15,58 @@ namespace {
 
 constexpr int NB = ELM_NB;
 
-// Factor the diagonal tile A_kk (in smem, lower) in place: right-looking, 256 threads.
+// Factor the diagonal tile A_kk (in smem, lower) in place, blocked by 8 columns:
+// 8x8 diagonal block (thread 0) -> panel solve (one thread per row) -> rank-8 trailing update.
+// 3 barriers per 8 columns.  Returns false on a non-positive pivot.
 __device__ bool potrf_tile(double (*L)[NB + 1], int n) {
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
-    __syncthreads();
-    for (int j = 0; j < n; ++j) {
+    for (int j0 = 0; j0 < n; j0 += 8) {
+        const int jw = min(8, n - j0);
         if (threadIdx.x == 0) {
-            double d = L[j][j];
-            if (!(d > 0.0) && bad < 0) bad = j;
-            L[j][j] = sqrt(fmax(d, 1e-300));
+            for (int c = j0; c < j0 + jw; ++c) {
+                double d = L[c][c];
+                for (int l = j0; l < c; ++l) d -= L[c][l] * L[c][l];
+                if (!(d > 0.0) && bad < 0) bad = c;
+                d = sqrt(fmax(d, 1e-300));
+                L[c][c] = d;
+                for (int i = c + 1; i < j0 + jw; ++i) {
+                    double v = L[i][c];
+                    for (int l = j0; l < c; ++l) v -= L[i][l] * L[c][l];
+                    L[i][c] = v / d;
+                }
+            }
         }
         __syncthreads();
-        const double djj = L[j][j];
-        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) L[i][j] /= djj;
+        for (int i = j0 + jw + threadIdx.x; i < n; i += blockDim.x) {
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = c < jw ? L[i][j0 + c] : 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c < jw) {
+                    double v = x[c];
+#pragma unroll
+                    for (int l = 0; l < 8; ++l)
+                        if (l < c) v -= x[l] * L[j0 + c][j0 + l];
+                    x[c] = v / L[j0 + c][j0 + c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < jw) L[i][j0 + c] = x[c];
+        }
         __syncthreads();
-        const int m = n - j - 1;
+        const int b0 = j0 + jw, m = n - b0;
         for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-            int i = j + 1 + t % m, l = j + 1 + t / m;
-            if (l <= i) L[i][l] -= L[i][j] * L[l][j];
+            const int i = b0 + t % m, l = b0 + t / m;
+            if (l <= i) {
+                double v = L[i][l];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < jw) v -= L[i][j0 + c] * L[l][j0 + c];
+                L[i][l] = v;
+            }
         }
         __syncthreads();
     }

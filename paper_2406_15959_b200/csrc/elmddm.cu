@@ -48,7 +48,7 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (cfg->q < 2 || cfg->q % 2 != 0) return why = "q must be even and >= 2", false;
     int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
     if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
-    if (round_up(m, 32) > 3400) return why = "m too large for the shared-memory panel (ld <= 3400)", false;
+    if (round_up(m, 32) > 3008) return why = "m too large for the shared-memory panel (ld <= 3008)", false;
     if (cfg->problem < 0 || cfg->problem > 5) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
@@ -268,7 +268,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         elmddm_destroy(c);
         return st;
     }
-    c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB + 2 * ELM_NB * z.ncols);
+    c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB);
     c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
                                                           (int64_t)c->ga_ld * c->qrow_cols),
                                       2 * z.G_pad);

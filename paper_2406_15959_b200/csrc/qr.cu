@@ -53,39 +53,71 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* red, double* 
     __syncthreads();
 }
 
-// G (kp x 8, smem, col-major ld kp) = Vp^T X, Vp = V columns [0, kp) rows [j0, ld) (global,
-// explicit), X = 8 columns in smem (col-major, row stride R, rows relative to j0).
-__device__ void vt_times_block(const double* __restrict__ Vp, int64_t ld, int R, int kp, const double* X, double* G) {
+__device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+constexpr int RED_ELEMS = 8 * 7 * 64;  // tree-reduction scratch: 8 warps x 7 tiles x 8x8
+
+// G (kp x 8, smem, column-major ld kp) = Vp^T X on the FP64 tensor pipe.
+// Vp: columns [0, kp) of the panel's explicit V, rows relative to j0 (global, L2-resident);
+// X: 8 columns in smem, column stride RP, R rows.  Split-K over the 16 warps (4-row k-steps
+// interleaved), then a fixed-order tree reduction across warps (deterministic).
+__device__ void vt_block(const double* __restrict__ Vp, int64_t ld, int R, int kp, const double* X, int RP, double* G,
+                         double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ngroups = (kp + 3) / 4;
-    for (int grp = warp; grp < ngroups; grp += PNW) {
-        double acc[4][8];
+    const int mtiles = kp >> 3;
+    const int nks = R >> 2;
+    double acc[7][2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+    for (int t = 0; t < 7; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int kr = lane & 3, cn = lane >> 2;
+    for (int ks0 = warp; ks0 < nks; ks0 += 4 * PNW) {
+        double a[4][7], bfr[4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
-        const int cp0 = grp * 4;
-        for (int r = lane; r < R; r += 32) {
-            double x[8];
+        for (int u = 0; u < 4; ++u) {
+            const int ks = ks0 + u * PNW;
+            const bool ok = ks < nks;
+            const int r = ks * 4 + kr;
+            bfr[u] = ok ? X[cn * RP + r] : 0.0;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = X[c * R + r];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                if (cp0 + a < kp) {
-                    double v = Vp[(int64_t)(cp0 + a) * ld + r];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[a][c] += v * x[c];
-                }
-            }
+            for (int t = 0; t < 7; ++t) a[u][t] = (ok && t < mtiles) ? Vp[(int64_t)(t * 8 + cn) * ld + r] : 0.0;
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                double s = acc[a][c];
+            for (int t = 0; t < 7; ++t)
+                if (t < mtiles) dmma8(acc[t][0], acc[t][1], a[u][t], bfr[u]);
+    }
+    // tree reduction 16 -> 8 -> 4 -> 2 -> 1 warps
+    for (int half = PNW / 2; half >= 1; half >>= 1) {
+        if (warp >= half && warp < 2 * half) {
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0 && cp0 + a < kp) G[c * kp + cp0 + a] = s;
+            for (int t = 0; t < 7; ++t)
+                if (t < mtiles) {
+                    red[((warp - half) * 7 + t) * 64 + lane * 2] = acc[t][0];
+                    red[((warp - half) * 7 + t) * 64 + lane * 2 + 1] = acc[t][1];
+                }
+        }
+        __syncthreads();
+        if (warp < half) {
+#pragma unroll
+            for (int t = 0; t < 7; ++t)
+                if (t < mtiles) {
+                    acc[t][0] += red[(warp * 7 + t) * 64 + lane * 2];
+                    acc[t][1] += red[(warp * 7 + t) * 64 + lane * 2 + 1];
+                }
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t)
+            if (t < mtiles) {
+                // fragment: row i = t*8 + lane/4 (V column), col c = 2*(lane%4) + e
+                G[(2 * kr) * kp + t * 8 + cn] = acc[t][0];
+                G[(2 * kr + 1) * kp + t * 8 + cn] = acc[t][1];
             }
     }
 }
@@ -95,13 +127,14 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     const int sl = blockIdx.x;
     const int64_t ld = a.ld;
     const int j0 = a.j0, jb = j0 + ELM_BB * a.blk, kp = ELM_BB * a.blk;
-    const int R = (int)(ld - j0);     // rows held: [j0, ld)
+    const int R = (int)(ld - j0);     // rows held: [j0, ld)  (multiple of 32)
+    const int RP = R + 4;             // padded column stride (conflict-free DMMA fragments)
     const int d0 = jb - j0;           // local row of the block's first diagonal entry
-    double* Cb = sm;                  // [8][R]
-    double* Wsm = Cb + 8 * R;         // [8][kp]  (<= 8*56)
+    double* Cb = sm;                  // [8][RP]
+    double* Wsm = Cb + 8 * RP;        // [8][kp]  (<= 8*56)
     double* Zsm = Wsm + 8 * 56;       // [8][kp]
-    double* red = Zsm + 8 * 56;       // [PNW][36]
-    double* tot = red + PNW * 36;     // [36]
+    double* red = Zsm + 8 * 56;       // RED_ELEMS
+    double* tot = red + RED_ELEMS;    // [40]
     double* Tbb = tot + 40;           // [8][8]
     double* taus = Tbb + 64;          // [8]
 
@@ -111,13 +144,19 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     const double* Vp = V + j0;        // column c of Vp at Vp + c*ld, rows relative to j0
 
     // load the block: rows [j0, ld) of columns [jb, jb+8)
-    for (int c = 0; c < 8; ++c)
-        for (int r = threadIdx.x; r < R; r += PNT) Cb[c * R + r] = A[(int64_t)(jb + c) * ld + j0 + r];
+    for (int c = 0; c < 8; ++c) {
+        const double2* src = reinterpret_cast<const double2*>(A + (int64_t)(jb + c) * ld + j0);
+        for (int r2 = threadIdx.x; r2 < R / 2; r2 += PNT) {
+            double2 v = src[r2];
+            Cb[c * RP + 2 * r2] = v.x;
+            Cb[c * RP + 2 * r2 + 1] = v.y;
+        }
+    }
     __syncthreads();
 
     if (kp > 0) {
         // W = Vp^T Cb
-        vt_times_block(Vp, ld, R, kp, Cb, Wsm);
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red);
         __syncthreads();
         // Z = T^T W  (T upper triangular kp x kp)
         for (int t = threadIdx.x; t < kp * 8; t += PNT) {
@@ -132,32 +171,37 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             double acc[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-            for (int k = 0; k < kp; ++k) {
-                double v = Vp[(int64_t)k * ld + r];
+            int k = 0;
+            for (; k + 8 <= kp; k += 8) {
+                double v[8];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) acc[c] += v * Zsm[c * kp + k];
+                for (int u = 0; u < 8; ++u) v[u] = Vp[(int64_t)(k + u) * ld + r];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[c] += v[u] * Zsm[c * kp + k + u];
             }
 #pragma unroll
-            for (int c = 0; c < 8; ++c) Cb[c * R + r] -= acc[c];
+            for (int c = 0; c < 8; ++c) Cb[c * RP + r] -= acc[c];
         }
         __syncthreads();
     }
 
-    // factor the 8 columns
+    // factor the 8 columns: one block reduction per column
     for (int c = 0; c < 8; ++c) {
         const int d = d0 + c;
         double v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = 0.0;
         for (int r = d + 1 + threadIdx.x; r < R; r += PNT) {
-            double x = Cb[c * R + r];
+            double x = Cb[c * RP + r];
             v[0] += x * x;
 #pragma unroll
             for (int c2 = 1; c2 < 8; ++c2)
-                if (c + c2 < 8) v[c2] += x * Cb[(c + c2) * R + r];
+                if (c + c2 < 8) v[c2] += x * Cb[(c + c2) * RP + r];
         }
         block_sum<8>(v, red, tot);
-        const double x0 = Cb[c * R + d];
+        const double x0 = Cb[c * RP + d];
         const double nrm = sqrt(x0 * x0 + tot[0]);
         double alpha = x0, tau = 0.0, scale = 0.0;
         if (nrm != 0.0) {
@@ -165,38 +209,55 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             scale = 1.0 / (x0 - alpha);
             tau = (alpha - x0) / alpha;
         }
-        // apply H = I - tau v v^T to the remaining columns of the block
-        if (tau != 0.0) {
-            for (int c2 = 1; c + c2 < 8; ++c2) {
-                double yd = Cb[(c + c2) * R + d];
-                double w = tau * (yd + scale * tot[c2]);
-                for (int r = d + 1 + threadIdx.x; r < R; r += PNT) Cb[(c + c2) * R + r] -= w * scale * Cb[c * R + r];
-                __syncthreads();  // all threads read yd before thread 0 writes it
-                if (threadIdx.x == 0) Cb[(c + c2) * R + d] = yd - w;
-            }
-            for (int r = d + 1 + threadIdx.x; r < R; r += PNT) Cb[c * R + r] *= scale;
+        double w[8], yd[8];
+#pragma unroll
+        for (int c2 = 1; c2 < 8; ++c2) {
+            yd[c2] = (c + c2 < 8) ? Cb[(c + c2) * RP + d] : 0.0;
+            w[c2] = tau * (yd[c2] + scale * tot[c2]);
         }
-        __syncthreads();
+        __syncthreads();  // row d read by everyone before it is rewritten
+        if (tau != 0.0) {
+            for (int r = d + 1 + threadIdx.x; r < R; r += PNT) {
+                const double x = Cb[c * RP + r];
+                const double vs = scale * x;
+#pragma unroll
+                for (int c2 = 1; c2 < 8; ++c2)
+                    if (c + c2 < 8) Cb[(c + c2) * RP + r] -= w[c2] * vs;
+                Cb[c * RP + r] = vs;
+            }
+        }
         if (threadIdx.x == 0) {
-            Cb[c * R + d] = alpha;
+#pragma unroll
+            for (int c2 = 1; c2 < 8; ++c2)
+                if (c + c2 < 8) Cb[(c + c2) * RP + d] = yd[c2] - w[c2];
+            Cb[c * RP + d] = alpha;
             taus[c] = tau;
         }
         __syncthreads();
     }
 
     // write back R (upper) + V (below the diagonal) and tau
-    for (int c = 0; c < 8; ++c)
-        for (int r = threadIdx.x; r < R; r += PNT) A[(int64_t)(jb + c) * ld + j0 + r] = Cb[c * R + r];
+    for (int c = 0; c < 8; ++c) {
+        double2* dst = reinterpret_cast<double2*>(A + (int64_t)(jb + c) * ld + j0);
+        for (int r2 = threadIdx.x; r2 < R / 2; r2 += PNT) dst[r2] = make_double2(Cb[c * RP + 2 * r2], Cb[c * RP + 2 * r2 + 1]);
+    }
     if (threadIdx.x < 8) a.tau[(int64_t)sl * a.M + jb + threadIdx.x] = taus[threadIdx.x];
     __syncthreads();
     // explicit V of the block (zeros above, unit diagonal) -> smem and Vbuf
-    for (int c = 0; c < 8; ++c)
-        for (int r = threadIdx.x; r < R; r += PNT) {
-            const int d = d0 + c;
-            double v = r < d ? 0.0 : (r == d ? 1.0 : Cb[c * R + r]);
-            Cb[c * R + r] = v;
-            V[(int64_t)(kp + c) * ld + j0 + r] = v;
+    for (int c = 0; c < 8; ++c) {
+        const int d = d0 + c;
+        double2* dst = reinterpret_cast<double2*>(V + (int64_t)(kp + c) * ld + j0);
+        for (int r2 = threadIdx.x; r2 < R / 2; r2 += PNT) {
+            double v2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int r = 2 * r2 + e;
+                v2[e] = r < d ? 0.0 : (r == d ? 1.0 : Cb[c * RP + r]);
+                Cb[c * RP + r] = v2[e];
+            }
+            dst[r2] = make_double2(v2[0], v2[1]);
         }
+    }
     __syncthreads();
 
     // T of the block: Tbb[i][i] = tau_i, Tbb[0:i, i] = -tau_i Tbb[0:i,0:i] (Vb^T v_i)[0:i]
@@ -207,30 +268,14 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
         for (int r = d0 + threadIdx.x; r < R; r += PNT) {
             double x[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = Cb[c * R + r];
+            for (int c = 0; c < 8; ++c) x[c] = Cb[c * RP + r];
             int k = 0;
 #pragma unroll
             for (int c1 = 0; c1 < 8; ++c1)
 #pragma unroll
                 for (int c2 = c1 + 1; c2 < 8; ++c2) g[k++] += x[c1] * x[c2];
         }
-        // reduce 28 values (reuse the 36-wide scratch)
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int k = 0; k < 28; ++k) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) g[k] += __shfl_xor_sync(0xffffffffu, g[k], o);
-        }
-        if (lane == 0)
-#pragma unroll
-            for (int k = 0; k < 28; ++k) red[warp * 36 + k] = g[k];
-        __syncthreads();
-        if (threadIdx.x < 28) {
-            double s = 0.0;
-            for (int w = 0; w < PNW; ++w) s += red[w * 36 + threadIdx.x];
-            tot[threadIdx.x] = s;
-        }
-        __syncthreads();
+        block_sum<28>(g, red, tot);
         if (threadIdx.x == 0) {
             double G8[8][8];
             int k = 0;
@@ -250,7 +295,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     }
     // T[0:kp+8, kp:kp+8]
     if (kp > 0) {
-        vt_times_block(Vp, ld, R, kp, Cb, Wsm);  // Gx = Vp^T Vb   (kp x 8)
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red);  // Gx = Vp^T Vb   (kp x 8)
         __syncthreads();
         // Y = Gx Tbb (kp x 8)
         for (int t = threadIdx.x; t < kp * 8; t += PNT) {
@@ -276,15 +321,211 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     for (int t = threadIdx.x; t < 64; t += PNT) {
         int r = t % 8, c = t / 8;
         T[(kp + c) * ELM_NB + kp + r] = Tbb[c * 8 + r];
-        // zero below the diagonal block inside the panel's T (columns kp..kp+7, rows > kp+7)
     }
-    if (threadIdx.x < 8 * ELM_NB) {
-        int c = threadIdx.x / ELM_NB, r = threadIdx.x % ELM_NB;
+    {
+        int c = threadIdx.x / ELM_NB, r = threadIdx.x % ELM_NB;  // 512 threads = 8 columns x 64 rows
         if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
     }
 }
 
-size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * R + 8 * 56 * 2 + PNW * 36 + 40 + 64 + 8) * 8; }
+// ------------------------------------------------------------------------------------------
+// Fused compact-WY trailing update for one 64-column block of one subdomain:
+//     W = V^T C   (64 x 64, K = R rows)          phase 1, DMMA, 32-row chunks, 2-stage cp.async
+//     Z = -T^T W  (64 x 64)                      phase 2, DMMA
+//     C = C + V Z (R x 64)                       phase 3, DMMA, 32-row chunks, coalesced stores
+// V columns >= nb and T entries outside nb x nb are treated as zero (last, narrower panel).
+// grid (ceil(N/64), S), 256 threads (8 warps), ~108 KB dynamic shared memory -> 2 CTAs / SM.
+// ------------------------------------------------------------------------------------------
+namespace wy {
+constexpr int NT = 256, CH = 32, PADC = CH + 4, PADZ = 64 + 4;
+constexpr int STAGE = 2 * 64 * PADC;          // V chunk [64 cols][PADC] + C chunk [64 cols][PADC]
+constexpr int SMEM = (2 * STAGE + 64 * PADZ) * 8;
+
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// load rows [r0, r0+32) of 64 columns (col j at base + j*ld) into dst[j][k] (stride PADC);
+// columns >= nvalid are zero-filled
+__device__ __forceinline__ void load_chunk(double* dst, const double* base, int64_t ld, int nvalid, int tid) {
+#pragma unroll
+    for (int it = 0; it < (64 * CH / 2) / NT; ++it) {
+        int ch = tid + it * NT;
+        int j = ch / (CH / 2), k = (ch % (CH / 2)) * 2;
+        bool ok = j < nvalid;
+        cp16(dst + j * PADC + k, ok ? base + (int64_t)j * ld + k : base, ok ? 16 : 0);
+    }
+}
+}  // namespace wy
+
+__global__ void __launch_bounds__(wy::NT, 2) k_wy_update(const double* __restrict__ Vbuf, const double* __restrict__ Tbuf,
+                                                         double* __restrict__ Kaug, int64_t ld, int64_t ncols, int j0,
+                                                         int nb, int c0, int N) {
+    using namespace wy;
+    extern __shared__ __align__(16) double sm[];
+    double* st0 = sm;
+    double* Zs = sm + 2 * STAGE;  // [64 n][PADZ]  W, then -Z
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sl = blockIdx.y, nblk = blockIdx.x;
+    const int R = (int)(ld - j0);
+    const int nch = R / CH;
+    const int ncv = min(64, N - nblk * 64);
+    const double* V = Vbuf + (int64_t)sl * ELM_NB * ld + j0;                 // V[r + j*ld]
+    double* C = Kaug + (int64_t)sl * ld * ncols + j0 + (int64_t)(c0 + nblk * 64) * ld;  // C[r + n*ld]
+    const double* T = Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+
+    // ---------------- phase 1: W = V^T C ----------------
+    const int wm = warp & 1, wn = warp >> 1;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    load_chunk(st0, V, ld, nb, tid);
+    load_chunk(st0 + 64 * PADC, C, ld, ncv, tid);
+    commit();
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) {
+            double* nx = st0 + ((c + 1) & 1) * STAGE;
+            load_chunk(nx, V + (c + 1) * CH, ld, nb, tid);
+            load_chunk(nx + 64 * PADC, C + (c + 1) * CH, ld, ncv, tid);
+        }
+        commit();
+        wait<1>();
+        __syncthreads();
+        const double* Vs = st0 + (c & 1) * STAGE;
+        const double* Cs = Vs + 64 * PADC;
+#pragma unroll
+        for (int ks = 0; ks < CH / 4; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = Vs[(wm * 32 + mt * 8 + (lane >> 2)) * PADC + kk];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Cs[(wn * 16 + nt * 8 + (lane >> 2)) * PADC + kk];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();  // stage (c & 1) is overwritten by the load issued next iteration
+    }
+    wait<0>();
+    // ---------------- phase 2: Z = -T^T W ----------------
+    // W -> Zs[n][i]; T -> Ts[i][k] = T[k + 64 i] (masked to nb x nb)
+    double* Ts = st0;  // [64 i][PADZ]
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int i = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                Zs[n * PADZ + i] = acc[mt][nt][e];
+            }
+    for (int t = tid; t < 64 * 64; t += NT) {
+        int k = t & 63, i = t >> 6;
+        Ts[i * PADZ + k] = (i < nb && k < nb) ? T[k + 64 * i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int ks = 0; ks < 16; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double af[4], bf[2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = Ts[(wm * 32 + mt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bf[nt] = Zs[(wn * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int i = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                Zs[n * PADZ + i] = -acc[mt][nt][e];   // B operand of phase 3: [n][k]
+            }
+    __syncthreads();
+    // ---------------- phase 3: C += V (-Z), 32-row chunks ----------------
+    const int wm3 = warp & 1, wn3 = warp >> 1;  // warp tile 16 rows x 16 cols
+    load_chunk(st0, V, ld, nb, tid);
+    load_chunk(st0 + 64 * PADC, C, ld, ncv, tid);
+    commit();
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) {
+            double* nx = st0 + ((c + 1) & 1) * STAGE;
+            load_chunk(nx, V + (c + 1) * CH, ld, nb, tid);
+            load_chunk(nx + 64 * PADC, C + (c + 1) * CH, ld, ncv, tid);
+        }
+        commit();
+        wait<1>();
+        __syncthreads();
+        const double* Vs = st0 + (c & 1) * STAGE;  // [k = V col][r]
+        double* Cs = (double*)Vs + 64 * PADC;      // [n][r]
+        double a3[2][2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm3 * 16 + mt * 8 + (lane >> 2), n = wn3 * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    a3[mt][nt][e] = Cs[n * PADC + r];
+                }
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[2], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) af[mt] = Vs[kk * PADC + wm3 * 16 + mt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Zs[(wn3 * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma(a3[mt][nt][0], a3[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();  // all reads of Cs done before it is overwritten with results
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm3 * 16 + mt * 8 + (lane >> 2), n = wn3 * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    Cs[n * PADC + r] = a3[mt][nt][e];
+                }
+        __syncthreads();
+        double* Cg = C + c * CH;
+#pragma unroll
+        for (int it = 0; it < (64 * CH / 2) / NT; ++it) {
+            int ch = tid + it * NT;
+            int j = ch / (CH / 2), k = (ch % (CH / 2)) * 2;
+            if (j < ncv) *reinterpret_cast<double2*>(Cg + (int64_t)j * ld + k) = *reinterpret_cast<const double2*>(Cs + j * PADC + k);
+        }
+        __syncthreads();  // Cs of this stage is read by the stores before the next prefetch reuses it
+    }
+}
+
+size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * (R + 4) + 8 * 56 * 2 + RED_ELEMS + 40 + 64 + 8) * 8; }
 
 }  // namespace
 
@@ -293,8 +534,6 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     const int M = c->cfg.M;
     double* Vbuf = work;
     double* Tbuf = Vbuf + S * ELM_NB * ld;
-    double* Wbuf = Tbuf + S * ELM_NB * ELM_NB;
-    double* Zbuf = Wbuf + S * ELM_NB * ncols;
     const size_t smax = panel_smem_bytes(ld);
     cudaError_t e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
     if (e != cudaSuccess) return e;
@@ -310,19 +549,19 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         }
         const int n_tr = (int)(ncols - (j0 + nb));
         if (n_tr <= 0) continue;
-        const int R = (int)(ld - j0);
-        // W = V^T C
-        GemmArgs g1{nb, n_tr, R, Vbuf + j0, ld, ELM_NB * ld, Kaug + j0 + (int64_t)(j0 + nb) * ld, ld, ld * ncols,
-                    Wbuf, ELM_NB, ELM_NB * ncols, 1.0, 0.0, (int)S, 0};
-        if ((e = gemm_launch(true, false, g1, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
-        // Z = T^T W
-        GemmArgs g2{nb, n_tr, nb, Tbuf, ELM_NB, ELM_NB * ELM_NB, Wbuf, ELM_NB, ELM_NB * ncols, Zbuf, ELM_NB,
-                    ELM_NB * ncols, 1.0, 0.0, (int)S, 0};
-        if ((e = gemm_launch(true, false, g2, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
-        // C -= V Z
-        GemmArgs g3{R, n_tr, nb, Vbuf + j0, ld, ELM_NB * ld, Zbuf, ELM_NB, ELM_NB * ncols,
-                    Kaug + j0 + (int64_t)(j0 + nb) * ld, ld, ld * ncols, -1.0, 1.0, (int)S, 0};
-        if ((e = gemm_launch(false, false, g3, st, c, ELMDDM_K_GEMM_QR)) != cudaSuccess) return e;
+        {
+            static bool attr = false;
+            if (!attr) {
+                if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) !=
+                    cudaSuccess)
+                    return e;
+                attr = true;
+            }
+            dim3 grid((unsigned)((n_tr + 63) / 64), (unsigned)S);
+            KTimer kt(c, ELMDDM_K_GEMM_QR, st);
+            k_wy_update<<<grid, wy::NT, wy::SMEM, st>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
     }
     return cudaSuccess;
 }

@@ -220,9 +220,11 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     for (int i0 = 0; i0 < M; i0 += 64) {
         const int bi = (M - i0) < 64 ? (M - i0) : 64;
         dim3 g((nat + 63) / 64, (unsigned)S);
-        KTimer kt(c, ELMDDM_K_TRSM, st);
-        k_trsm_lt_diag<<<g, 64, 0, st>>>(Kaug, ld, ncols, At, M, nat, i0, bi);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        {
+            KTimer kt(c, ELMDDM_K_TRSM, st);
+            k_trsm_lt_diag<<<g, 64, 0, st>>>(Kaug, ld, ncols, At, M, nat, i0, bi);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
         const int rest = M - (i0 + bi);
         if (rest > 0) {
             // At[i0+bi:, :] -= R[i0:i0+bi, i0+bi:]^T X_i

@@ -38,7 +38,7 @@ def test_config_validation_is_synchronous_and_cpu_safe():
         dict(P=2, M=512, p=16, q=16),    # m < M (underdetermined local LS)
         dict(P=0, M=64, p=16, q=16),
         dict(P=2, M=64, p=16, q=16, s_begin=3, s_end=2),
-        dict(P=2, M=64, p=100, q=16),    # ld > 3400
+        dict(P=2, M=64, p=100, q=16),    # ld > 3008
     ]
     for b in bad:
         cfg = _lib.Config(b["P"], b["M"], b["p"], b["q"], 0, 0, 0.125, 0.5, 0, b.get("s_begin", 0),
