@@ -16,25 +16,52 @@ namespace {
 constexpr int NB = ELM_NB;
 
 // Factor the diagonal tile A_kk (in smem, lower) in place, blocked by 8 columns:
-// 8x8 diagonal block (thread 0) -> panel solve (one thread per row) -> rank-8 trailing update.
-// 3 barriers per 8 columns.  Returns false on a non-positive pivot.
-__device__ bool potrf_tile(double (*L)[NB + 1], int n) {
+// 8x8 diagonal block (one warp, lanes = rows) -> panel solve (one thread per row) -> rank-8
+// trailing update.  3 barriers per 8 columns; the reciprocal diagonal rd[] replaces every
+// division on the critical path.  Returns false on a non-positive pivot.
+__device__ bool potrf_tile(double (*L)[NB + 1], double* rd, int n) {
     __shared__ int bad;
     if (threadIdx.x == 0) bad = -1;
     for (int j0 = 0; j0 < n; j0 += 8) {
         const int jw = min(8, n - j0);
-        if (threadIdx.x == 0) {
-            for (int c = j0; c < j0 + jw; ++c) {
-                double d = L[c][c];
-                for (int l = j0; l < c; ++l) d -= L[c][l] * L[c][l];
-                if (!(d > 0.0) && bad < 0) bad = c;
-                d = sqrt(fmax(d, 1e-300));
-                L[c][c] = d;
-                for (int i = c + 1; i < j0 + jw; ++i) {
-                    double v = L[i][c];
-                    for (int l = j0; l < c; ++l) v -= L[i][l] * L[c][l];
-                    L[i][c] = v / d;
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            const int i = j0 + (lane & 7);
+            double row[8];
+#pragma unroll
+            for (int l = 0; l < 8; ++l) row[l] = (lane < jw && l < jw) ? L[i][j0 + l] : 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c < jw) {
+                    // diagonal: d = a_cc - sum_{l<c} L_cl^2, held by lane c
+                    double d = row[c];
+#pragma unroll
+                    for (int l = 0; l < 8; ++l)
+                        if (l < c) d -= row[l] * row[l];
+                    double dc = __shfl_sync(0xffffffffu, d, c);
+                    if (lane == 0 && !(dc > 0.0) && bad < 0) bad = j0 + c;
+                    dc = fmax(dc, 1e-300);
+                    const double r = rsqrt(dc);
+                    // L_cl for l < c (row c), broadcast
+                    double lc[8];
+#pragma unroll
+                    for (int l = 0; l < 8; ++l) lc[l] = __shfl_sync(0xffffffffu, row[l], c);
+                    if ((lane & 7) > c) {
+                        double v = row[c];
+#pragma unroll
+                        for (int l = 0; l < 8; ++l)
+                            if (l < c) v -= row[l] * lc[l];
+                        row[c] = v * r;
+                    } else if ((lane & 7) == c) {
+                        row[c] = dc * r;  // sqrt(d)
+                    }
+                    if (lane == c) rd[j0 + c] = r;
                 }
+            }
+            if (lane < jw) {
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l <= lane) L[i][j0 + l] = row[l];
             }
         }
         __syncthreads();
@@ -49,7 +76,7 @@ __device__ bool potrf_tile(double (*L)[NB + 1], int n) {
 #pragma unroll
                     for (int l = 0; l < 8; ++l)
                         if (l < c) v -= x[l] * L[j0 + c][j0 + l];
-                    x[c] = v / L[j0 + c][j0 + c];
+                    x[c] = v * rd[j0 + c];
                 }
             }
 #pragma unroll
@@ -57,15 +84,19 @@ __device__ bool potrf_tile(double (*L)[NB + 1], int n) {
                 if (c < jw) L[i][j0 + c] = x[c];
         }
         __syncthreads();
-        const int b0 = j0 + jw, m = n - b0;
-        for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-            const int i = b0 + t % m, l = b0 + t / m;
-            if (l <= i) {
-                double v = L[i][l];
+        const int b0 = j0 + jw;
+        {
+            const int i = b0 + (threadIdx.x >> 2), part = threadIdx.x & 3;  // 4 threads per row
+            if (i < n) {
+                double li[8];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    if (c < jw) v -= L[i][j0 + c] * L[l][j0 + c];
-                L[i][l] = v;
+                for (int c = 0; c < 8; ++c) li[c] = c < jw ? L[i][j0 + c] : 0.0;
+                for (int l = b0 + part; l <= i; l += 4) {
+                    double v = L[i][l];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) v -= li[c] * L[l][j0 + c];
+                    L[i][l] = v;
+                }
             }
         }
         __syncthreads();
@@ -73,18 +104,37 @@ __device__ bool potrf_tile(double (*L)[NB + 1], int n) {
     return bad < 0;
 }
 
-// grid 1 + nsub.  CTA 0 writes L_kk; CTA t >= 1 solves L_{k+t,k} = A_{k+t,k} L_kk^{-T}.
+__device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+constexpr int LP = NB + 4;  // padded row stride (== 4 mod 16): conflict-free DMMA fragments
+constexpr int POTRF_SMEM = (NB * (NB + 1) + 2 * NB * LP + NB) * 8;
+
+// grid 1 + nsub, 256 threads.  Every CTA factors A_kk = L L^T (shared memory) and forms
+// Linv = L^{-1}; CTA 0 writes L_kk, CTA t >= 1 overwrites A_{k+t,k} with A Linv^T (DMMA).
 __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int64_t LD, int k, int n,
                                                     ElmStatus* status) {
-    __shared__ double L[NB][NB + 1];
+    extern __shared__ __align__(16) double psm[];
+    double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(psm);
+    double* Li = psm + NB * (NB + 1);   // Linv[r][c] at Li[r*LP + c]  (B operand [n][k])
+    double* Xs = Li + NB * LP;          // A tile [i][k] at Xs[i*LP + k]
+    double* rd = Xs + NB * LP;
     const int64_t k0 = (int64_t)k * NB;
     double* Akk = Mb + k0 + k0 * LD;
     for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
         int i = t % NB, j = t / NB;
-        L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : 0.0;
+        L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
     }
+    double* Ap = Mb + (k0 + (int64_t)blockIdx.x * NB) + k0 * LD;
+    if (blockIdx.x > 0)
+        for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
+            int i = t % NB, j = t / NB;
+            Xs[i * LP + j] = Ap[i + (int64_t)j * LD];
+        }
     __syncthreads();
-    bool ok = potrf_tile(L, n);
+    bool ok = potrf_tile(L, rd, n);
     if (blockIdx.x == 0) {
         if (!ok && threadIdx.x == 0) elm_set_status(status, ELMDDM_ENUMERIC, (int)k0);
         for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
@@ -93,29 +143,173 @@ __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int
         }
         return;
     }
-    double* Ap = Mb + (k0 + (int64_t)blockIdx.x * NB) + k0 * LD;
-    // row r: x L^T = a  <=>  L x^T = a^T; thread (r, part) owns columns l = part + 4u
-    const int r = threadIdx.x >> 2, part = threadIdx.x & 3;
-    double xv[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) xv[u] = Ap[r + (int64_t)(part + 4 * u) * LD];
-    for (int cidx = 0; cidx < n; ++cidx) {
-        const int owner = cidx & 3, uo = cidx >> 2;
-        double xc = 0.0;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (u == uo) xc = xv[u];
-        xc = __shfl_sync(0xffffffffu, xc, (threadIdx.x & 31 & ~3) | owner);
-        xc = xc / L[cidx][cidx];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            int l = part + 4 * u;
-            if (l > cidx && l < n) xv[u] -= xc * L[l][cidx];
-            if (l == cidx) xv[u] = xc;
+    // Linv, column j by the 4 threads of a quad: Linv[i][j] = (d_ij - sum_{j<=l<i} L[i][l] Linv[l][j]) rd[i]
+    {
+        const int j = threadIdx.x >> 2, part = threadIdx.x & 3, lane = threadIdx.x & 31;
+        for (int i = 0; i < NB; ++i) Li[i * LP + j] = 0.0;  // (each quad thread writes the same zeros)
+        __syncwarp();
+        for (int i = 0; i < NB; ++i) {  // uniform trip count: the shuffles need the full warp
+            double s = 0.0;
+            if (i >= j)
+                for (int l = j + part; l < i; l += 4) s += L[i][l] * Li[l * LP + j];
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if (part == 0 && i >= j) Li[i * LP + j] = ((i == j ? 1.0 : 0.0) - s) * rd[i];
+            __syncwarp();
         }
+        (void)lane;
+    }
+    __syncthreads();
+    // X = A Linv^T : X[i][c] = sum_k A[i][k] Linv[c][k]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int ks = 0; ks < NB / 4; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double af[4], bf[2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[(wm * 32 + mt * 8 + (lane >> 2)) * LP + kk];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bf[nt] = Li[(wn * 16 + nt * 8 + (lane >> 2)) * LP + kk];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) Ap[r + (int64_t)(part + 4 * u) * LD] = xv[u];
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int i = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                Ap[i + (int64_t)c * LD] = acc[mt][nt][e];
+            }
+}
+
+// ------------------------------------------------------------------------------------------
+// Band SYRK update of step k: C_ij -= L_i L_j^T for the lower tiles 0 <= j <= i < nsub of the
+// window starting at block k+1 (L_i = tile (k+1+i, k)).  The tile list (column-major lower
+// triangle) is cut into contiguous chunks, one per CTA: the B tile L_j stays in shared memory
+// while j is unchanged, A tiles are double-buffered with cp.async, C tiles are prefetched into
+// registers one tile ahead.  grid min(ntiles, 2*SMs), 256 threads, ~104 KB shared memory.
+// ------------------------------------------------------------------------------------------
+constexpr int SYRK_SMEM = 3 * NB * LP * 8;
+
+__device__ __forceinline__ void cpa16(double* dst, const double* src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// tile (stored column-major in the band, rows r0.., cols c0..) -> dst[row][col] with stride LP?
+// We keep A and B as [row][k] (row-major, k = column of the panel) so that both DMMA fragments
+// read (row = lane/4, k = lane%4) with stride LP == 4 (mod 16).
+__device__ __forceinline__ void load_panel_tile(double* dst, const double* src, int64_t LD) {
+    // src: 64 rows x 64 cols column-major (ld LD); dst[r*LP + c].  16 B chunks along rows need a
+    // transpose, so copy column segments of 2 rows with two 8 B writes instead: use cp.async on
+    // the column-major layout into a [c][r] buffer and read fragments as [k][row] instead.
+    for (int ch = threadIdx.x; ch < NB * NB / 2; ch += 256) {
+        int c = ch / (NB / 2), r = (ch % (NB / 2)) * 2;
+        cpa16(dst + c * LP + r, src + r + (int64_t)c * LD);
+    }
+}
+
+__device__ __forceinline__ void tile_of(int t, int nsub, int& i, int& j) {
+    // column-major lower triangle: column j has nsub - j tiles
+    j = 0;
+    int rem = t;
+    while (rem >= nsub - j) {
+        rem -= nsub - j;
+        ++j;
+    }
+    i = j + rem;
+}
+
+__global__ void __launch_bounds__(256, 2) k_syrk_band(double* __restrict__ Mb, int64_t LD, int k, int nsub, int ntiles) {
+    extern __shared__ __align__(16) double ssm[];
+    double* Bs = ssm;                 // L_j  as [k][n]  (column-major tile: Bs[c*LP + r] = L_j[r][c])
+    double* As0 = ssm + NB * LP;      // L_i  as [k][row]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
+    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+    if (t0 >= t1) return;
+    const int64_t k0 = (int64_t)k * NB, w0 = k0 + NB;  // window origin
+    const double* P = Mb + w0 + k0 * LD;               // panel: tile i at P + i*NB
+    int i, j;
+    tile_of(t0, nsub, i, j);
+    int jb = -1;
+    // prefetch first A tile
+    load_panel_tile(As0, P + (int64_t)i * NB, LD);
+    cpa_commit();
+    double cn[4][2][2];
+    auto load_c = [&](int ti, int tj, double (&cr)[4][2][2]) {
+        const double* Ct = Mb + (w0 + (int64_t)ti * NB) + (w0 + (int64_t)tj * NB) * LD;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    cr[mt][nt][e] = Ct[r + (int64_t)c * LD];
+                }
+    };
+    load_c(i, j, cn);
+    for (int t = t0; t < t1; ++t) {
+        const int ci = i, cj = j, buf = (t - t0) & 1;
+        if (cj != jb) {
+            // (re)load B = L_j; previous readers of Bs are done (barrier at the end of the loop)
+            load_panel_tile(Bs, P + (int64_t)cj * NB, LD);
+            cpa_commit();
+            jb = cj;
+        }
+        double acc[4][2][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = cn[mt][nt][0], acc[mt][nt][1] = cn[mt][nt][1];
+        // next tile: prefetch its A into the other buffer and its C into registers
+        if (t + 1 < t1) {
+            tile_of(t + 1, nsub, i, j);
+            load_panel_tile(As0 + (buf ^ 1) * NB * LP, P + (int64_t)i * NB, LD);
+        }
+        cpa_commit();
+        if (t + 1 < t1) load_c(i, j, cn);
+        cpa_wait<1>();
+        __syncthreads();
+        const double* As = As0 + buf * NB * LP;
+#pragma unroll 4
+        for (int ks = 0; ks < NB / 4; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = -As[kk * LP + wm * 32 + mt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Bs[kk * LP + wn * 16 + nt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        double* Ct = Mb + (w0 + (int64_t)ci * NB) + (w0 + (int64_t)cj * NB) * LD;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    Ct[r + (int64_t)c * LD] = acc[mt][nt][e];
+                }
+        __syncthreads();  // buffers of this tile may be overwritten by the next prefetch
+    }
 }
 
 // forward step k: CTA 0 solves L_kk z_k = y_k; CTA t >= 1: y_{k+t} -= L_{k+t,k} z_k
@@ -123,6 +317,7 @@ __global__ void __launch_bounds__(128) k_fwd(const double* __restrict__ Mb, int6
                                              double* __restrict__ y, double* __restrict__ z) {
     __shared__ double L[NB][NB + 1];
     __shared__ double xs[NB];
+    __shared__ double rd[NB];
     const int64_t k0 = (int64_t)k * NB;
     const double* Akk = Mb + k0 + k0 * LD;
     for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
@@ -130,12 +325,14 @@ __global__ void __launch_bounds__(128) k_fwd(const double* __restrict__ Mb, int6
         L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
     }
     __syncthreads();
+    for (int t = threadIdx.x; t < NB; t += blockDim.x) rd[t] = 1.0 / L[t][t];
+    __syncthreads();
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         double z0 = lane < n ? y[k0 + lane] : 0.0, z1 = lane + 32 < n ? y[k0 + lane + 32] : 0.0;
         for (int c = 0; c < n; ++c) {
             double xc = __shfl_sync(0xffffffffu, c < 32 ? z0 : z1, c & 31);
-            xc /= L[c][c];
+            xc *= rd[c];
             if (lane > c) z0 -= L[lane][c] * xc;
             if (lane + 32 > c) z1 -= L[lane + 32][c] * xc;
             if (lane == (c & 31)) {
@@ -165,6 +362,7 @@ __global__ void __launch_bounds__(128) k_bwd(const double* __restrict__ Mb, int6
                                              double* __restrict__ z, double* __restrict__ u) {
     __shared__ double L[NB][NB + 1];
     __shared__ double xs[NB];
+    __shared__ double rd[NB];
     const int64_t k0 = (int64_t)k * NB;
     const double* Akk = Mb + k0 + k0 * LD;
     for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
@@ -172,12 +370,14 @@ __global__ void __launch_bounds__(128) k_bwd(const double* __restrict__ Mb, int6
         L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
     }
     __syncthreads();
+    for (int t = threadIdx.x; t < NB; t += blockDim.x) rd[t] = 1.0 / L[t][t];
+    __syncthreads();
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         double z0 = lane < n ? z[k0 + lane] : 0.0, z1 = lane + 32 < n ? z[k0 + lane + 32] : 0.0;
         for (int c = n - 1; c >= 0; --c) {
             double xc = __shfl_sync(0xffffffffu, c < 32 ? z0 : z1, c & 31);
-            xc /= L[c][c];
+            xc *= rd[c];
             // z_l -= L[c][l] x_c for l < c
             if (lane < c) z0 -= L[c][lane] * xc;
             if (lane + 32 < c) z1 -= L[c][lane + 32] * xc;
@@ -213,17 +413,27 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     double* y = work;
     double* z = y + Gp;
     cudaError_t e;
+    static bool attr = false;
+    if (!attr) {
+        if ((e = cudaFuncSetAttribute(k_potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_syrk_band, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM)) !=
+                cudaSuccess)
+            return e;
+        attr = true;
+    }
     if ((e = cudaMemcpyAsync(y, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
     for (int k = 0; k < nblk; ++k) {
         const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
         { KTimer kt(c, ELMDDM_K_POTRF, st);
-        k_potrf_trsm<<<1 + nsub, 256, 0, st>>>(Mband, LD, k, NB, c->d_status); }
+        k_potrf_trsm<<<1 + nsub, 256, POTRF_SMEM, st>>>(Mband, LD, k, NB, c->d_status); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (nsub > 0) {
-            const int64_t r0 = (int64_t)(k + 1) * NB, k0 = (int64_t)k * NB;
-            GemmArgs gs{nsub * NB, nsub * NB, NB, Mband + r0 + k0 * LD, LD, 0, Mband + r0 + k0 * LD, LD, 0,
-                        Mband + r0 + r0 * LD, LD, 0, -1.0, 1.0, 1, 1};
-            if ((e = gemm_launch(false, true, gs, st, c, ELMDDM_K_GEMM_CHOL)) != cudaSuccess) return e;
+            const int ntiles = nsub * (nsub + 1) / 2;
+            const int grid = ntiles < 2 * c->nsm ? ntiles : 2 * c->nsm;
+            KTimer kt(c, ELMDDM_K_GEMM_CHOL, st);
+            k_syrk_band<<<grid, 256, SYRK_SMEM, st>>>(Mband, LD, k, nsub, ntiles);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
     for (int k = 0; k < nblk; ++k) {

@@ -158,31 +158,41 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
         // W = Vp^T Cb
         vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red);
         __syncthreads();
-        // Z = T^T W  (T upper triangular kp x kp)
+        // T (kp x kp, upper) -> smem (reuse the reduction scratch), Z = T^T W
+        double* Ts = red;
+        for (int t = threadIdx.x; t < kp * kp; t += PNT) {
+            int r = t % kp, c = t / kp;
+            Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+        }
+        __syncthreads();
         for (int t = threadIdx.x; t < kp * 8; t += PNT) {
             int cp = t % kp, c = t / kp;
             double s = 0.0;
-            for (int k = 0; k <= cp; ++k) s += T[cp * ELM_NB + k] * Wsm[c * kp + k];
+            for (int k = 0; k <= cp; ++k) s += Ts[cp * kp + k] * Wsm[c * kp + k];
             Zsm[c * kp + cp] = s;
         }
         __syncthreads();
-        // Cb -= Vp Z
-        for (int r = threadIdx.x; r < R; r += PNT) {
-            double acc[8];
+        // Cb -= Vp Z on the FP64 tensor pipe: M = R rows (8-row tiles over the 16 warps),
+        // N = 8 columns, K = kp; the B fragments (Z) are held in registers.
+        {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const int kr = lane & 3, rn = lane >> 2;
+            const int ksteps = kp >> 2;
+            double zb[14];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-            int k = 0;
-            for (; k + 8 <= kp; k += 8) {
-                double v[8];
+            for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
+            for (int mt = warp; mt < R / 8; mt += PNW) {
+                const int r0 = mt * 8;
+                double c0 = Cb[(2 * kr) * RP + r0 + rn], c1 = Cb[(2 * kr + 1) * RP + r0 + rn];
+                double av[14];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = Vp[(int64_t)(k + u) * ld + r];
+                for (int t = 0; t < 14; ++t) av[t] = t < ksteps ? Vp[(int64_t)(t * 4 + kr) * ld + r0 + rn] : 0.0;
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[c] += v[u] * Zsm[c * kp + k + u];
+                for (int t = 0; t < 14; ++t)
+                    if (t < ksteps) dmma8(c0, c1, av[t], zb[t]);
+                Cb[(2 * kr) * RP + r0 + rn] = c0;
+                Cb[(2 * kr + 1) * RP + r0 + rn] = c1;
             }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) Cb[c * RP + r] -= acc[c];
         }
         __syncthreads();
     }
@@ -276,20 +286,28 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
                 for (int c2 = c1 + 1; c2 < 8; ++c2) g[k++] += x[c1] * x[c2];
         }
         block_sum<28>(g, red, tot);
-        if (threadIdx.x == 0) {
-            double G8[8][8];
-            int k = 0;
-            for (int c1 = 0; c1 < 8; ++c1)
-                for (int c2 = c1 + 1; c2 < 8; ++c2) G8[c1][c2] = tot[k++];
-            for (int i = 0; i < 8; ++i) {
-                for (int r = 0; r < 8; ++r) Tbb[i * 8 + r] = 0.0;
-                Tbb[i * 8 + i] = taus[i];
-                for (int r = 0; r < i; ++r) {
+        if (threadIdx.x < 32) {
+            // Tbb column i: Tbb[r][i] = -tau_i sum_{k=r}^{i-1} Tbb[r][k] G8[k][i]; lane r owns row r
+            const int r = threadIdx.x & 7;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
                     double s = 0.0;
-                    for (int k2 = r; k2 < i; ++k2) s += Tbb[k2 * 8 + r] * G8[k2][i];
-                    Tbb[i * 8 + r] = -taus[i] * s;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) {
+                            const int gi = (k * (15 - k)) / 2 + (i - k - 1);  // packed index of G8[k][i]
+                            s += trow[k] * tot[gi];
+                        }
+                    trow[i] = -taus[i] * s;
                 }
             }
+            if (threadIdx.x < 8)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Tbb[i * 8 + r] = trow[i];
         }
         __syncthreads();
     }
@@ -305,11 +323,17 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             Zsm[c * kp + r] = s;
         }
         __syncthreads();
-        // T[0:kp, kp+c] = -T[0:kp,0:kp] Y
+        // T[0:kp, kp+c] = -T[0:kp,0:kp] Y   (T staged in smem)
+        double* Ts = red;
+        for (int t = threadIdx.x; t < kp * kp; t += PNT) {
+            int r = t % kp, c = t / kp;
+            Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+        }
+        __syncthreads();
         for (int t = threadIdx.x; t < kp * 8; t += PNT) {
             int r = t % kp, c = t / kp;
             double s = 0.0;
-            for (int k = r; k < kp; ++k) s += T[k * ELM_NB + r] * Zsm[c * kp + k];
+            for (int k = r; k < kp; ++k) s += Ts[k * kp + r] * Zsm[c * kp + k];
             Wsm[c * kp + r] = -s;
         }
         __syncthreads();

@@ -19,12 +19,15 @@ namespace {
 __global__ void __launch_bounds__(64) k_trsm_lt_diag(const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
                                                      double* __restrict__ At, int M, int ncol_at, int i0, int bi) {
     __shared__ double Rs[64][65];
+    __shared__ double rdg[64];
     const int sl = blockIdx.y;
     const double* A = Kaug + (int64_t)sl * ld * ncols;
     for (int t = threadIdx.x; t < bi * bi; t += 64) {
         int r = t % bi, c = t / bi;
         Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];  // R[r][c], upper part used
     }
+    __syncthreads();
+    if (threadIdx.x < bi) rdg[threadIdx.x] = 1.0 / Rs[threadIdx.x][threadIdx.x];
     __syncthreads();
     const int col = blockIdx.x * 64 + threadIdx.x;
     if (col >= ncol_at) return;
@@ -41,7 +44,7 @@ __global__ void __launch_bounds__(64) k_trsm_lt_diag(const double* __restrict__ 
 #pragma unroll
             for (int l = 0; l < 64; ++l)
                 if (l < r) s -= Rs[l][r] * xv[l];
-            xv[r] = s / Rs[r][r];
+            xv[r] = s * rdg[r];
         }
     }
 #pragma unroll
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug
     __shared__ double Rs[64][65];
     __shared__ double cs[64];
     __shared__ double red[16];
+    __shared__ double rdg[64];
     const int sl = blockIdx.x;
     const double* A = Kaug + (int64_t)sl * ld * ncols;
     double* zs = z + (int64_t)sl * ld;
@@ -178,6 +182,8 @@ __global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug
             Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];
         }
         __syncthreads();
+        if (threadIdx.x < bi) rdg[threadIdx.x] = 1.0 / Rs[threadIdx.x][threadIdx.x];
+        __syncthreads();
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
             double z0 = lane < bi ? zs[i0 + lane] : 0.0;
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug
                 double cr;
                 if (r >= 32) cr = __shfl_sync(0xffffffffu, z1, r - 32);
                 else cr = __shfl_sync(0xffffffffu, z0, r);
-                cr = cr / Rs[r][r];
+                cr = cr * rdg[r];
                 if (lane < r) z0 -= Rs[lane][r] * cr;
                 if (lane + 32 < r) z1 -= Rs[lane + 32][r] * cr;
                 if (lane == (r & 31)) {
