@@ -10,99 +10,11 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include <cstdio>
 
 namespace {
 
 constexpr int NB = ELM_NB;
-
-// Factor the diagonal tile A_kk (in smem, lower) in place, blocked by 8 columns:
-// 8x8 diagonal block (one warp, lanes = rows) -> panel solve (one thread per row) -> rank-8
-// trailing update.  3 barriers per 8 columns; the reciprocal diagonal rd[] replaces every
-// division on the critical path.  Returns false on a non-positive pivot.
-__device__ bool potrf_tile(double (*L)[NB + 1], double* rd, int n) {
-    __shared__ int bad;
-    if (threadIdx.x == 0) bad = -1;
-    for (int j0 = 0; j0 < n; j0 += 8) {
-        const int jw = min(8, n - j0);
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            const int i = j0 + (lane & 7);
-            double row[8];
-#pragma unroll
-            for (int l = 0; l < 8; ++l) row[l] = (lane < jw && l < jw) ? L[i][j0 + l] : 0.0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (c < jw) {
-                    // diagonal: d = a_cc - sum_{l<c} L_cl^2, held by lane c
-                    double d = row[c];
-#pragma unroll
-                    for (int l = 0; l < 8; ++l)
-                        if (l < c) d -= row[l] * row[l];
-                    double dc = __shfl_sync(0xffffffffu, d, c);
-                    if (lane == 0 && !(dc > 0.0) && bad < 0) bad = j0 + c;
-                    dc = fmax(dc, 1e-300);
-                    const double r = rsqrt(dc);
-                    // L_cl for l < c (row c), broadcast
-                    double lc[8];
-#pragma unroll
-                    for (int l = 0; l < 8; ++l) lc[l] = __shfl_sync(0xffffffffu, row[l], c);
-                    if ((lane & 7) > c) {
-                        double v = row[c];
-#pragma unroll
-                        for (int l = 0; l < 8; ++l)
-                            if (l < c) v -= row[l] * lc[l];
-                        row[c] = v * r;
-                    } else if ((lane & 7) == c) {
-                        row[c] = dc * r;  // sqrt(d)
-                    }
-                    if (lane == c) rd[j0 + c] = r;
-                }
-            }
-            if (lane < jw) {
-#pragma unroll
-                for (int l = 0; l < 8; ++l)
-                    if (l <= lane) L[i][j0 + l] = row[l];
-            }
-        }
-        __syncthreads();
-        for (int i = j0 + jw + threadIdx.x; i < n; i += blockDim.x) {
-            double x[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = c < jw ? L[i][j0 + c] : 0.0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (c < jw) {
-                    double v = x[c];
-#pragma unroll
-                    for (int l = 0; l < 8; ++l)
-                        if (l < c) v -= x[l] * L[j0 + c][j0 + l];
-                    x[c] = v * rd[j0 + c];
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c < jw) L[i][j0 + c] = x[c];
-        }
-        __syncthreads();
-        const int b0 = j0 + jw;
-        {
-            const int i = b0 + (threadIdx.x >> 2), part = threadIdx.x & 3;  // 4 threads per row
-            if (i < n) {
-                double li[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) li[c] = c < jw ? L[i][j0 + c] : 0.0;
-                for (int l = b0 + part; l <= i; l += 4) {
-                    double v = L[i][l];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) v -= li[c] * L[l][j0 + c];
-                    L[i][l] = v;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    return bad < 0;
-}
 
 __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -110,22 +22,112 @@ __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double 
 }
 
 constexpr int LP = NB + 4;  // padded row stride (== 4 mod 16): conflict-free DMMA fragments
-constexpr int POTRF_SMEM = (NB * (NB + 1) + 2 * NB * LP + NB) * 8;
 
-// grid 1 + nsub, 256 threads.  Every CTA factors A_kk = L L^T (shared memory) and forms
-// Linv = L^{-1}; CTA 0 writes L_kk, CTA t >= 1 overwrites A_{k+t,k} with A Linv^T (DMMA).
+// In-place Cholesky of the 64x64 tile L[i*LP + j] (lower part used), blocked by 8 columns:
+//   8x8 diagonal block by warp 0 (lanes = rows, rsqrt, no divisions),
+//   panel solve below it (one thread per row, reciprocal diagonal),
+//   rank-8 trailing update of the lower 8x8 tiles on the FP64 tensor pipe.
+// rd[] receives the reciprocal diagonal.  Returns false on a non-positive pivot.
+__device__ bool potrf_tile(double* L, double* rd) {
+    __shared__ int bad;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) bad = -1;
+    for (int j0 = 0; j0 < NB; j0 += 8) {
+        if (warp == 0) {
+            const int r = lane & 7, i = j0 + r;
+            double row[8];
+#pragma unroll
+            for (int l = 0; l < 8; ++l) row[l] = L[i * LP + j0 + l];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                double d = row[c];
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l < c) d -= row[l] * row[l];
+                double dc = __shfl_sync(0xffffffffu, d, c);
+                if (lane == 0 && !(dc > 0.0) && bad < 0) bad = j0 + c;
+                dc = fmax(dc, 1e-300);
+                const double rs = rsqrt(dc);
+                double lc[8];
+#pragma unroll
+                for (int l = 0; l < 8; ++l) lc[l] = __shfl_sync(0xffffffffu, row[l], c);
+                if (r > c) {
+                    double v = row[c];
+#pragma unroll
+                    for (int l = 0; l < 8; ++l)
+                        if (l < c) v -= row[l] * lc[l];
+                    row[c] = v * rs;
+                } else if (r == c) {
+                    row[c] = dc * rs;
+                }
+                if (lane == c) rd[j0 + c] = rs;
+            }
+            if (lane < 8)
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l <= r) L[i * LP + j0 + l] = row[l];
+        }
+        __syncthreads();
+        // panel rows below the diagonal block
+        for (int i = j0 + 8 + threadIdx.x; i < NB; i += blockDim.x) {
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = L[i * LP + j0 + c];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                double v = x[c];
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l < c) v -= x[l] * L[(j0 + c) * LP + j0 + l];
+                x[c] = v * rd[j0 + c];
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) L[i * LP + j0 + c] = x[c];
+        }
+        __syncthreads();
+        // trailing update, lower 8x8 tiles (I >= J) of the remaining block, K = 8
+        const int b0 = j0 + 8, nt = (NB - b0) / 8;
+        const int ntiles = nt * (nt + 1) / 2;
+        for (int tt = warp; tt < ntiles; tt += blockDim.x / 32) {
+            int J = 0, rem = tt;
+            while (rem >= nt - J) {
+                rem -= nt - J;
+                ++J;
+            }
+            const int I = J + rem;
+            const int ri = b0 + 8 * I + (lane >> 2), cl = b0 + 8 * J + 2 * (lane & 3);
+            double c0 = L[ri * LP + cl], c1 = L[ri * LP + cl + 1];
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int kk = j0 + ks * 4 + (lane & 3);
+                dmma_c(c0, c1, -L[(b0 + 8 * I + (lane >> 2)) * LP + kk], L[(b0 + 8 * J + (lane >> 2)) * LP + kk]);
+            }
+            L[ri * LP + cl] = c0;
+            L[ri * LP + cl + 1] = c1;
+        }
+        __syncthreads();
+    }
+    return bad < 0;
+}
+
+constexpr int POTRF_SMEM = (2 * NB * LP + NB) * 8;
+
+// grid 1 + nsub, 256 threads.  Every CTA factors A_kk = L L^T in shared memory; CTA 0 writes
+// L_kk, CTA t >= 1 solves X L^T = A_{k+t,k} in place: 8-column blocks, each a DMMA update with
+// the already solved columns followed by an 8x8 triangular solve per row.
 __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int64_t LD, int k, int n,
                                                     ElmStatus* status) {
     extern __shared__ __align__(16) double psm[];
-    double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(psm);
-    double* Li = psm + NB * (NB + 1);   // Linv[r][c] at Li[r*LP + c]  (B operand [n][k])
-    double* Xs = Li + NB * LP;          // A tile [i][k] at Xs[i*LP + k]
+    double* L = psm;              // [i*LP + j]
+    double* Xs = L + NB * LP;     // [i*LP + j]  panel tile, solved in place
     double* rd = Xs + NB * LP;
+    (void)n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t k0 = (int64_t)k * NB;
     double* Akk = Mb + k0 + k0 * LD;
     for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
         int i = t % NB, j = t / NB;
-        L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
+        L[i * LP + j] = (i >= j) ? Akk[i + (int64_t)j * LD] : 0.0;
     }
     double* Ap = Mb + (k0 + (int64_t)blockIdx.x * NB) + k0 * LD;
     if (blockIdx.x > 0)
@@ -134,61 +136,51 @@ __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int
             Xs[i * LP + j] = Ap[i + (int64_t)j * LD];
         }
     __syncthreads();
-    bool ok = potrf_tile(L, rd, n);
+    const bool ok = potrf_tile(L, rd);
     if (blockIdx.x == 0) {
         if (!ok && threadIdx.x == 0) elm_set_status(status, ELMDDM_ENUMERIC, (int)k0);
         for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
             int i = t % NB, j = t / NB;
-            if (i < n && j < n && i >= j) Akk[i + (int64_t)j * LD] = L[i][j];
+            if (i >= j) Akk[i + (int64_t)j * LD] = L[i * LP + j];
         }
         return;
     }
-    // Linv, column j by the 4 threads of a quad: Linv[i][j] = (d_ij - sum_{j<=l<i} L[i][l] Linv[l][j]) rd[i]
-    {
-        const int j = threadIdx.x >> 2, part = threadIdx.x & 3, lane = threadIdx.x & 31;
-        for (int i = 0; i < NB; ++i) Li[i * LP + j] = 0.0;  // (each quad thread writes the same zeros)
-        __syncwarp();
-        for (int i = 0; i < NB; ++i) {  // uniform trip count: the shuffles need the full warp
-            double s = 0.0;
-            if (i >= j)
-                for (int l = j + part; l < i; l += 4) s += L[i][l] * Li[l * LP + j];
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if (part == 0 && i >= j) Li[i * LP + j] = ((i == j ? 1.0 : 0.0) - s) * rd[i];
-            __syncwarp();
-        }
-        (void)lane;
-    }
-    __syncthreads();
-    // X = A Linv^T : X[i][c] = sum_k A[i][k] Linv[c][k]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
-    double acc[4][2][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 4
-    for (int ks = 0; ks < NB / 4; ++ks) {
-        const int kk = ks * 4 + (lane & 3);
-        double af[4], bf[2];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[(wm * 32 + mt * 8 + (lane >> 2)) * LP + kk];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bf[nt] = Li[(wn * 16 + nt * 8 + (lane >> 2)) * LP + kk];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                int i = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
-                Ap[i + (int64_t)c * LD] = acc[mt][nt][e];
+    for (int b = 0; b < NB / 8; ++b) {
+        const int c8 = 8 * b;
+        if (b > 0 && warp < NB / 8) {
+            // Xs[:, c8:c8+8] -= Xs[:, 0:c8] L[c8:c8+8, 0:c8]^T   (warp = 8-row m-tile)
+            const int ri = warp * 8 + (lane >> 2), cl = c8 + 2 * (lane & 3);
+            double c0 = Xs[ri * LP + cl], c1 = Xs[ri * LP + cl + 1];
+            for (int ks = 0; ks < 2 * b; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                dmma_c(c0, c1, -Xs[(warp * 8 + (lane >> 2)) * LP + kk], L[(c8 + (lane >> 2)) * LP + kk]);
             }
+            Xs[ri * LP + cl] = c0;
+            Xs[ri * LP + cl + 1] = c1;
+        }
+        __syncthreads();
+        if (threadIdx.x < NB) {
+            const int i = threadIdx.x;
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = Xs[i * LP + c8 + c];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                double v = x[c];
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l < c) v -= x[l] * L[(c8 + c) * LP + c8 + l];
+                x[c] = v * rd[c8 + c];
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) Xs[i * LP + c8 + c] = x[c];
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
+        int i = t % NB, j = t / NB;
+        Ap[i + (int64_t)j * LD] = Xs[i * LP + j];
+    }
 }
 
 // ------------------------------------------------------------------------------------------

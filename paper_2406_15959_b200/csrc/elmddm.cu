@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -247,6 +248,13 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     }
     int nsm = 148;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) c->nsm = nsm;
+    {
+        // subdomain groups for the QR streams (ELMDDM_QR_GROUPS overrides; 1 disables)
+        const int64_t S = cfg->s_end - cfg->s_begin;
+        int g = S >= 64 ? 4 : 1;
+        if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
+        c->qr_groups = g < 1 ? 1 : g;
+    }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));
     const int64_t P = cfg->P, M = cfg->M, q = cfg->q;
@@ -287,6 +295,9 @@ void elmddm_destroy(elmddm_ctx* c) {
     if (!c) return;
     DeviceGuard dg(c->device);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto s : c->gstreams) cudaStreamDestroy(s);
+    for (auto e : c->ev_join) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (auto& p : c->ev_pending) {
         cudaEventDestroy(p.second.first);
         cudaEventDestroy(p.second.second);

@@ -59,6 +59,25 @@ struct elmddm_ctx {
     mutable double cls_ms[ELMDDM_NCLASS] = {};
     mutable std::vector<cudaEvent_t> ev_pool;                 // free events
     mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+
+    // internal streams for the subdomain groups of the QR (fork / join with events)
+    int qr_groups = 4;
+    mutable std::vector<cudaStream_t> gstreams;
+    mutable cudaEvent_t ev_fork = nullptr;
+    mutable std::vector<cudaEvent_t> ev_join;
+    cudaError_t ensure_streams(int n) const {
+        cudaError_t e = cudaSuccess;
+        if (!ev_fork && (e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+        while ((int)gstreams.size() < n) {
+            cudaStream_t s;
+            cudaEvent_t ev;
+            if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+            gstreams.push_back(s);
+            ev_join.push_back(ev);
+        }
+        return e;
+    }
 };
 
 // RAII probe around one kernel launch: counts it and, when timing is on, brackets it with a

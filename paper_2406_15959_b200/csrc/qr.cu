@@ -14,6 +14,9 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include <algorithm>
+#include <vector>
+#include <cstdio>
 
 namespace {
 
@@ -29,6 +32,7 @@ struct PanelArgs {
     double* Tbuf;  // [S][NB][NB]  compact-WY T of the current panel (column-major)
     int j0;        // panel start column
     int blk;       // base block index inside the panel
+    int s_off;     // first local subdomain of this launch (subdomain groups on separate streams)
 };
 
 // block-wide deterministic sum of NV values per thread; result broadcast in tot[0..NV)
@@ -58,73 +62,64 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-constexpr int RED_ELEMS = 8 * 7 * 64;  // tree-reduction scratch: 8 warps x 7 tiles x 8x8
+constexpr int RCH = 32;                 // rows per staged chunk of V_prev
+constexpr int RCP = RCH + 4;            // chunk column stride (== 4 mod 16)
+constexpr int RED_ELEMS = 2 * 56 * RCP; // 2-stage ring of V_prev chunks (also T staging / reduction scratch)
 
-// G (kp x 8, smem, column-major ld kp) = Vp^T X on the FP64 tensor pipe.
-// Vp: columns [0, kp) of the panel's explicit V, rows relative to j0 (global, L2-resident);
-// X: 8 columns in smem, column stride RP, R rows.  Split-K over the 16 warps (4-row k-steps
-// interleaved), then a fixed-order tree reduction across warps (deterministic).
+// stage rows [c*RCH, c*RCH+RCH) of V_prev columns [0, kp) into dst[col*RCP + row] (16 B cp.async)
+__device__ __forceinline__ void vp_chunk(double* dst, const double* __restrict__ Vp, int64_t ld, int kp, int c) {
+    const int n = kp * (RCH / 2);
+    for (int t = threadIdx.x; t < n; t += PNT) {
+        const int col = t / (RCH / 2), r = (t % (RCH / 2)) * 2;
+        unsigned d = (unsigned)__cvta_generic_to_shared(dst + col * RCP + r);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Vp + (int64_t)col * ld + c * RCH + r));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// G (kp x 8, column-major ld kp) = Vp^T X on the FP64 tensor pipe, V_prev streamed through the
+// ring in coalesced 32-row chunks.  Warp w owns m-tile w/2 (8 columns of V_prev) and the k-steps
+// of parity w%2 in every chunk; the two parities are summed at the end (fixed order).
 __device__ void vt_block(const double* __restrict__ Vp, int64_t ld, int R, int kp, const double* X, int RP, double* G,
-                         double* red) {
+                         double* ring, double* pairbuf) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int mtiles = kp >> 3;
-    const int nks = R >> 2;
-    double acc[7][2];
-#pragma unroll
-    for (int t = 0; t < 7; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
     const int kr = lane & 3, cn = lane >> 2;
-    for (int ks0 = warp; ks0 < nks; ks0 += 4 * PNW) {
-        double a[4][7], bfr[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int ks = ks0 + u * PNW;
-            const bool ok = ks < nks;
-            const int r = ks * 4 + kr;
-            bfr[u] = ok ? X[cn * RP + r] : 0.0;
-#pragma unroll
-            for (int t = 0; t < 7; ++t) a[u][t] = (ok && t < mtiles) ? Vp[(int64_t)(t * 8 + cn) * ld + r] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int t = 0; t < 7; ++t)
-                if (t < mtiles) dmma8(acc[t][0], acc[t][1], a[u][t], bfr[u]);
-    }
-    // tree reduction 16 -> 8 -> 4 -> 2 -> 1 warps
-    for (int half = PNW / 2; half >= 1; half >>= 1) {
-        if (warp >= half && warp < 2 * half) {
-#pragma unroll
-            for (int t = 0; t < 7; ++t)
-                if (t < mtiles) {
-                    red[((warp - half) * 7 + t) * 64 + lane * 2] = acc[t][0];
-                    red[((warp - half) * 7 + t) * 64 + lane * 2 + 1] = acc[t][1];
-                }
-        }
+    const int nch = R / RCH;
+    double a0 = 0.0, a1 = 0.0;
+    vp_chunk(ring, Vp, ld, kp, 0);
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * 56 * RCP, Vp, ld, kp, c + 1);
+        else asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::);
         __syncthreads();
-        if (warp < half) {
+        const double* st = ring + (c & 1) * 56 * RCP;
+        if (t < mtiles) {
 #pragma unroll
-            for (int t = 0; t < 7; ++t)
-                if (t < mtiles) {
-                    acc[t][0] += red[(warp * 7 + t) * 64 + lane * 2];
-                    acc[t][1] += red[(warp * 7 + t) * 64 + lane * 2 + 1];
-                }
-        }
-        __syncthreads();
-    }
-    if (warp == 0) {
-#pragma unroll
-        for (int t = 0; t < 7; ++t)
-            if (t < mtiles) {
-                // fragment: row i = t*8 + lane/4 (V column), col c = 2*(lane%4) + e
-                G[(2 * kr) * kp + t * 8 + cn] = acc[t][0];
-                G[(2 * kr + 1) * kp + t * 8 + cn] = acc[t][1];
+            for (int q = 0; q < RCH / 8; ++q) {
+                const int kk = (2 * q + par) * 4 + kr;  // row inside the chunk
+                dmma8(a0, a1, st[(t * 8 + cn) * RCP + kk], X[cn * RP + c * RCH + kk]);
             }
+        }
+        __syncthreads();
+    }
+    if (t < mtiles && par == 1) {
+        pairbuf[t * 64 + lane * 2] = a0;
+        pairbuf[t * 64 + lane * 2 + 1] = a1;
+    }
+    __syncthreads();
+    if (t < mtiles && par == 0) {
+        a0 += pairbuf[t * 64 + lane * 2];
+        a1 += pairbuf[t * 64 + lane * 2 + 1];
+        // fragment: row i = t*8 + lane/4 (V column), col c = 2*(lane%4) + e
+        G[(2 * kr) * kp + t * 8 + cn] = a0;
+        G[(2 * kr + 1) * kp + t * 8 + cn] = a1;
     }
 }
 
 __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     extern __shared__ __align__(16) double sm[];
-    const int sl = blockIdx.x;
+    const int sl = a.s_off + blockIdx.x;
     const int64_t ld = a.ld;
     const int j0 = a.j0, jb = j0 + ELM_BB * a.blk, kp = ELM_BB * a.blk;
     const int R = (int)(ld - j0);     // rows held: [j0, ld)  (multiple of 32)
@@ -142,22 +137,32 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
     double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
     const double* Vp = V + j0;        // column c of Vp at Vp + c*ld, rows relative to j0
+#ifdef ELM_PANEL_PROF
+    long long pst[12];
+    pst[0] = clock64();
+#define PSTAMP(k) pst[k] = clock64()
+#else
+#define PSTAMP(k)
+#endif
 
     // load the block: rows [j0, ld) of columns [jb, jb+8)
     for (int c = 0; c < 8; ++c) {
-        const double2* src = reinterpret_cast<const double2*>(A + (int64_t)(jb + c) * ld + j0);
+        const double* src = A + (int64_t)(jb + c) * ld + j0;
         for (int r2 = threadIdx.x; r2 < R / 2; r2 += PNT) {
-            double2 v = src[r2];
-            Cb[c * RP + 2 * r2] = v.x;
-            Cb[c * RP + 2 * r2 + 1] = v.y;
+            unsigned d = (unsigned)__cvta_generic_to_shared(Cb + c * RP + 2 * r2);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * r2));
         }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
+    PSTAMP(1);
 
     if (kp > 0) {
         // W = Vp^T Cb
-        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red);
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, Zsm);
         __syncthreads();
+        PSTAMP(2);
         // T (kp x kp, upper) -> smem (reuse the reduction scratch), Z = T^T W
         double* Ts = red;
         for (int t = threadIdx.x; t < kp * kp; t += PNT) {
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             Zsm[c * kp + cp] = s;
         }
         __syncthreads();
+        PSTAMP(3);
         // Cb -= Vp Z on the FP64 tensor pipe: M = R rows (8-row tiles over the 16 warps),
         // N = 8 columns, K = kp; the B fragments (Z) are held in registers.
         {
@@ -181,20 +187,29 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             double zb[14];
 #pragma unroll
             for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
-            for (int mt = warp; mt < R / 8; mt += PNW) {
-                const int r0 = mt * 8;
-                double c0 = Cb[(2 * kr) * RP + r0 + rn], c1 = Cb[(2 * kr + 1) * RP + r0 + rn];
-                double av[14];
+            // V_prev streamed through the ring; warps 0-3 each own one 8-row m-tile of the chunk
+            const int nch = R / RCH;
+            vp_chunk(red, Vp, ld, kp, 0);
+            for (int c = 0; c < nch; ++c) {
+                if (c + 1 < nch) vp_chunk(red + ((c + 1) & 1) * 56 * RCP, Vp, ld, kp, c + 1);
+                else asm volatile("cp.async.commit_group;\n" ::);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+                __syncthreads();
+                const double* st = red + (c & 1) * 56 * RCP;
+                if (warp < RCH / 8) {
+                    const int r0 = c * RCH + warp * 8;
+                    double c0 = Cb[(2 * kr) * RP + r0 + rn], c1 = Cb[(2 * kr + 1) * RP + r0 + rn];
 #pragma unroll
-                for (int t = 0; t < 14; ++t) av[t] = t < ksteps ? Vp[(int64_t)(t * 4 + kr) * ld + r0 + rn] : 0.0;
-#pragma unroll
-                for (int t = 0; t < 14; ++t)
-                    if (t < ksteps) dmma8(c0, c1, av[t], zb[t]);
-                Cb[(2 * kr) * RP + r0 + rn] = c0;
-                Cb[(2 * kr + 1) * RP + r0 + rn] = c1;
+                    for (int t = 0; t < 14; ++t)
+                        if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * RCP + warp * 8 + rn], zb[t]);
+                    Cb[(2 * kr) * RP + r0 + rn] = c0;
+                    Cb[(2 * kr + 1) * RP + r0 + rn] = c1;
+                }
+                __syncthreads();
             }
         }
         __syncthreads();
+        PSTAMP(4);
     }
 
     // factor the 8 columns: one block reduction per column
@@ -244,6 +259,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             taus[c] = tau;
         }
         __syncthreads();
+        PSTAMP(5);
     }
 
     // write back R (upper) + V (below the diagonal) and tau
@@ -253,6 +269,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     }
     if (threadIdx.x < 8) a.tau[(int64_t)sl * a.M + jb + threadIdx.x] = taus[threadIdx.x];
     __syncthreads();
+    PSTAMP(6);
     // explicit V of the block (zeros above, unit diagonal) -> smem and Vbuf
     for (int c = 0; c < 8; ++c) {
         const int d = d0 + c;
@@ -269,6 +286,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
         }
     }
     __syncthreads();
+    PSTAMP(7);
 
     // T of the block: Tbb[i][i] = tau_i, Tbb[0:i, i] = -tau_i Tbb[0:i,0:i] (Vb^T v_i)[0:i]
     {
@@ -310,11 +328,13 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
                 for (int i = 0; i < 8; ++i) Tbb[i * 8 + r] = trow[i];
         }
         __syncthreads();
+        PSTAMP(8);
     }
     // T[0:kp+8, kp:kp+8]
     if (kp > 0) {
-        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red);  // Gx = Vp^T Vb   (kp x 8)
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, Zsm);  // Gx = Vp^T Vb   (kp x 8)
         __syncthreads();
+        PSTAMP(9);
         // Y = Gx Tbb (kp x 8)
         for (int t = threadIdx.x; t < kp * 8; t += PNT) {
             int r = t % kp, c = t / kp;
@@ -350,6 +370,13 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
         int c = threadIdx.x / ELM_NB, r = threadIdx.x % ELM_NB;  // 512 threads = 8 columns x 64 rows
         if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
     }
+#ifdef ELM_PANEL_PROF
+    pst[10] = clock64();
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 200) && (a.blk == 4) && (a.j0 == 256 || a.j0 == 1024))
+        printf("PANELPROF j0=%d blk=%d cta=%d load %lld vt1 %lld z %lld upd %lld fact %lld wb %lld vexp %lld tbb %lld vt2 %lld text %lld\n",
+               a.j0, a.blk, blockIdx.x, pst[1] - pst[0], pst[2] - pst[1], pst[3] - pst[2], pst[4] - pst[3], pst[5] - pst[4],
+               pst[6] - pst[5], pst[7] - pst[6], pst[8] - pst[7], pst[9] - pst[8], pst[10] - pst[9]);
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
@@ -392,13 +419,13 @@ __device__ __forceinline__ void load_chunk(double* dst, const double* base, int6
 
 __global__ void __launch_bounds__(wy::NT, 2) k_wy_update(const double* __restrict__ Vbuf, const double* __restrict__ Tbuf,
                                                          double* __restrict__ Kaug, int64_t ld, int64_t ncols, int j0,
-                                                         int nb, int c0, int N) {
+                                                         int nb, int c0, int N, int s_off) {
     using namespace wy;
     extern __shared__ __align__(16) double sm[];
     double* st0 = sm;
     double* Zs = sm + 2 * STAGE;  // [64 n][PADZ]  W, then -Z
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int sl = blockIdx.y, nblk = blockIdx.x;
+    const int sl = s_off + blockIdx.y, nblk = blockIdx.x;
     const int R = (int)(ld - j0);
     const int nch = R / CH;
     const int ncv = min(64, N - nblk * 64);
@@ -561,30 +588,46 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     const size_t smax = panel_smem_bytes(ld);
     cudaError_t e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
     if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
+        return e;
+    // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
+    // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
+    // subdomains are independent).
+    const int ngroups = (int)std::min<int64_t>(c->qr_groups, S);
+    std::vector<cudaStream_t> streams(ngroups, st);
+    if (ngroups > 1) {
+        if ((e = c->ensure_streams(ngroups)) != cudaSuccess) return e;
+        cudaEventRecord(c->ev_fork, st);
+        for (int g = 0; g < ngroups; ++g) {
+            streams[g] = c->gstreams[g];
+            cudaStreamWaitEvent(streams[g], c->ev_fork, 0);
+        }
+    }
     for (int j0 = 0; j0 < M; j0 += ELM_NB) {
         const int nb = (M - j0) < ELM_NB ? (M - j0) : ELM_NB;
-        PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0};
         const size_t smem = panel_smem_bytes(ld - j0);
-        for (int blk = 0; blk < nb / ELM_BB; ++blk) {
-            pa.blk = blk;
-            KTimer kt(c, ELMDDM_K_PANEL, st);
-            k_panel_block<<<(unsigned)S, PNT, smem, st>>>(pa);
+        const int n_tr = (int)(ncols - (j0 + nb));
+        for (int g = 0; g < ngroups; ++g) {
+            const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
+            if (g1 <= g0) continue;
+            PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0};
+            for (int blk = 0; blk < nb / ELM_BB; ++blk) {
+                pa.blk = blk;
+                KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
+                k_panel_block<<<(unsigned)(g1 - g0), PNT, smem, streams[g]>>>(pa);
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            }
+            if (n_tr <= 0) continue;
+            dim3 grid((unsigned)((n_tr + 63) / 64), (unsigned)(g1 - g0));
+            KTimer kt(c, ELMDDM_K_GEMM_QR, streams[g]);
+            k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
-        const int n_tr = (int)(ncols - (j0 + nb));
-        if (n_tr <= 0) continue;
-        {
-            static bool attr = false;
-            if (!attr) {
-                if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) !=
-                    cudaSuccess)
-                    return e;
-                attr = true;
-            }
-            dim3 grid((unsigned)((n_tr + 63) / 64), (unsigned)S);
-            KTimer kt(c, ELMDDM_K_GEMM_QR, st);
-            k_wy_update<<<grid, wy::NT, wy::SMEM, st>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (ngroups > 1) {
+        for (int g = 0; g < ngroups; ++g) {
+            cudaEventRecord(c->ev_join[g], streams[g]);
+            cudaStreamWaitEvent(st, c->ev_join[g], 0);
         }
     }
     return cudaSuccess;
