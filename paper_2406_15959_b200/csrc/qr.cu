@@ -593,7 +593,8 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
     // subdomains are independent).
-    const int ngroups = (int)std::min<int64_t>(c->qr_groups, S);
+    // (with timing enabled the groups are serialised so that per-class event times do not overlap)
+    const int ngroups = c->timing ? 1 : (int)std::min<int64_t>(c->qr_groups, S);
     std::vector<cudaStream_t> streams(ngroups, st);
     if (ngroups > 1) {
         if ((e = c->ensure_streams(ngroups)) != cudaSuccess) return e;

@@ -1,0 +1,124 @@
+"""World-size-2 `gloo` tests (CPU) of the multi-rank plumbing of Context.run:
+partition, zero-filled globally indexed Schur buffers summed by reduce(SUM) = exact union,
+rank-0 interface solve, broadcast of u_Gamma, reduce of the slab-wise evaluation.
+
+The CUDA kernels are replaced by a fake context whose calls write slab-tagged values, so the
+test checks exactly the host-side collective sequence the GPU path uses."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+N_SUB = 9          # 3 x 3 subdomains
+SLOT = 5           # doubles per Pbuf / Sbuf slot
+G = 4
+NPTS = 12
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_ctx(rank, world):
+    from paper_2406_15959_b200 import solver as S
+
+    s0, s1 = S.partition(N_SUB, world, rank)
+
+    class Fake(S.Context):
+        def __init__(self):  # no CUDA context
+            self.sizes = {"G": G}
+            self.s_begin, self.s_end = s0, s1
+            self.calls = []
+
+        def __del__(self):
+            pass
+
+        def init_hidden(self, W, b, xi=None, stream=None):
+            self.calls.append("init_hidden")
+
+        def assemble(self, *a, **k):
+            self.calls.append("assemble")
+
+        def local_factor(self, *a, **k):
+            self.calls.append("local_factor")
+
+        def schur_accumulate(self, Kaug, At, Pbuf, Sbuf, work, stream=None):
+            self.calls.append("schur_accumulate")
+            for s in range(s0, s1):  # only own (global) slots are written
+                Pbuf[s * SLOT:(s + 1) * SLOT] = float(s + 1)
+                Sbuf[s * SLOT:(s + 1) * SLOT] = 0.5 * (s + 1)
+
+        def interface_assemble(self, Pbuf, Sbuf, Mband, g, work, stream=None):
+            self.calls.append("interface_assemble")
+            g[:] = Pbuf.sum() + Sbuf.sum()
+
+        def interface_factor_solve(self, Mband, g, uG, work, stream=None):
+            self.calls.append("interface_factor_solve")
+            uG[:] = g
+
+        def back_solve(self, Kaug, uG, coef, resid, work, stream=None):
+            self.calls.append("back_solve")
+            coef[:] = uG[0]
+
+        def evaluate(self, W, b, coef, xy, u, stream=None):
+            self.calls.append("evaluate")
+            for t in range(NPTS):  # point t "owned" by subdomain t % N_SUB
+                if s0 <= t % N_SUB < s1:
+                    u[t] = coef[0] + t
+
+    return Fake()
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = _fake_ctx(rank, world)
+        f64 = dict(dtype=torch.float64)
+        buf = {"W": torch.zeros(1, **f64), "b": torch.zeros(1, **f64), "Kaug": torch.zeros(1, **f64),
+               "At": torch.zeros(1, **f64), "tau": torch.zeros(1, **f64), "work": torch.zeros(1, **f64),
+               "Pbuf": torch.full((N_SUB * SLOT,), -7.0, **f64), "Sbuf": torch.full((N_SUB * SLOT,), -7.0, **f64),
+               "Mband": torch.zeros(1, **f64), "g": torch.zeros(G, **f64), "uG": torch.zeros(G, **f64),
+               "coef": torch.zeros(3, **f64), "resid": torch.zeros(1, **f64)}
+        xy = torch.zeros(2 * NPTS, **f64)
+        u = torch.full((NPTS,), -1.0, **f64)
+        ctx.run(buf, xy, u)
+        q.put((rank, ctx.calls, buf["Pbuf"].tolist(), buf["uG"].tolist(), buf["coef"].tolist(), u.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_collective_sequence_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=120)
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect_P = [float(s + 1) for s in range(N_SUB) for _ in range(SLOT)]
+    calls0, P0, uG0, coef0, u0 = res[0]
+    assert P0 == expect_P                                   # exact union on rank 0
+    g_expect = sum(expect_P) + 0.5 * sum(expect_P)
+    assert uG0 == [g_expect] * G
+    assert "interface_factor_solve" in calls0
+    for r in range(1, world):
+        calls, P, uG, coef, u = res[r]
+        assert "interface_assemble" not in calls and "interface_factor_solve" not in calls
+        assert uG == uG0                                    # broadcast
+        assert coef == [g_expect] * 3
+    assert u0 == [g_expect + t for t in range(NPTS)]        # slab-wise evaluation summed
