@@ -304,94 +304,137 @@ __global__ void __launch_bounds__(256, 2) k_syrk_band(double* __restrict__ Mb, i
     }
 }
 
-// forward step k: CTA 0 solves L_kk z_k = y_k; CTA t >= 1: y_{k+t} -= L_{k+t,k} z_k
-__global__ void __launch_bounds__(128) k_fwd(const double* __restrict__ Mb, int64_t LD, int k, int n,
-                                             double* __restrict__ y, double* __restrict__ z) {
-    __shared__ double L[NB][NB + 1];
-    __shared__ double xs[NB];
-    __shared__ double rd[NB];
-    const int64_t k0 = (int64_t)k * NB;
-    const double* Akk = Mb + k0 + k0 * LD;
-    for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-        int i = t % NB, j = t / NB;
-        L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < NB; t += blockDim.x) rd[t] = 1.0 / L[t][t];
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        double z0 = lane < n ? y[k0 + lane] : 0.0, z1 = lane + 32 < n ? y[k0 + lane + 32] : 0.0;
-        for (int c = 0; c < n; ++c) {
-            double xc = __shfl_sync(0xffffffffu, c < 32 ? z0 : z1, c & 31);
-            xc *= rd[c];
-            if (lane > c) z0 -= L[lane][c] * xc;
-            if (lane + 32 > c) z1 -= L[lane + 32][c] * xc;
-            if (lane == (c & 31)) {
-                if (c < 32) z0 = xc;
-                else z1 = xc;
-            }
-        }
-        xs[lane] = z0;
-        xs[lane + 32] = z1;
-    }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-        for (int t = threadIdx.x; t < n; t += blockDim.x) z[k0 + t] = xs[t];
-        return;
-    }
-    const int64_t r0 = k0 + (int64_t)blockIdx.x * NB;
-    const double* Ap = Mb + r0 + k0 * LD;
-    for (int r = threadIdx.x; r < NB; r += blockDim.x) {
-        double acc = 0.0;
-        for (int c = 0; c < n; ++c) acc += Ap[r + (int64_t)c * LD] * xs[c];
-        y[r0 + r] -= acc;
-    }
+// ------------------------------------------------------------------------------------------
+// Band triangular solve as ONE cooperative (co-resident) kernel: block-row i is owned by CTA
+// i mod gridDim.x; each CTA processes its rows in dependency order, streams the band tiles of the
+// row through a 2-stage cp.async ring, waits for the producers of the solved blocks it needs on
+// per-block completion flags (acquire/release, monotonically increasing epoch), subtracts the
+// GEMV contributions, solves with the diagonal tile and publishes its block.
+//   dir 0: L z = rhs  (row i needs z_j, j in [i-nbw, i))
+//   dir 1: L^T u = rhs (row i needs u_j, j in (i, i+nbw]; tiles (j, i) used transposed)
+// ------------------------------------------------------------------------------------------
+constexpr int TP = NB + 1;
+constexpr int TRSV_SMEM = (2 * NB * TP + 4 * NB + 3 * NB) * 8;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-// backward step k: CTA 0 solves L_kk^T u_k = z_k; CTA t >= 1: z_{k-t} -= L_{k,k-t}^T u_k
-__global__ void __launch_bounds__(128) k_bwd(const double* __restrict__ Mb, int64_t LD, int k, int n,
-                                             double* __restrict__ z, double* __restrict__ u) {
-    __shared__ double L[NB][NB + 1];
-    __shared__ double xs[NB];
-    __shared__ double rd[NB];
-    const int64_t k0 = (int64_t)k * NB;
-    const double* Akk = Mb + k0 + k0 * LD;
+__device__ __forceinline__ void load_tile_async(double* dst, const double* src, int64_t LD) {
+    // 64 x 64 column-major tile (ld LD) -> dst[c*TP + r]; 8-byte cp.async (TP is odd)
     for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-        int i = t % NB, j = t / NB;
-        L[i][j] = (i < n && j < n && i >= j) ? Akk[i + (int64_t)j * LD] : (i == j ? 1.0 : 0.0);
+        const int r = t & 63, c = t >> 6;
+        unsigned d = (unsigned)__cvta_generic_to_shared(dst + c * TP + r);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + r + (int64_t)c * LD));
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < NB; t += blockDim.x) rd[t] = 1.0 / L[t][t];
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        double z0 = lane < n ? z[k0 + lane] : 0.0, z1 = lane + 32 < n ? z[k0 + lane + 32] : 0.0;
-        for (int c = n - 1; c >= 0; --c) {
-            double xc = __shfl_sync(0xffffffffu, c < 32 ? z0 : z1, c & 31);
-            xc *= rd[c];
-            // z_l -= L[c][l] x_c for l < c
-            if (lane < c) z0 -= L[c][lane] * xc;
-            if (lane + 32 < c) z1 -= L[c][lane + 32] * xc;
-            if (lane == (c & 31)) {
-                if (c < 32) z0 = xc;
-                else z1 = xc;
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int64_t LD, int nblk, int nbw,
+                                                   const double* __restrict__ rhs, double* __restrict__ out, int* flags,
+                                                   int epoch, int dir, ElmStatus* status) {
+    extern __shared__ __align__(16) double tsm[];
+    double* tiles = tsm;                  // [2][64 cols][TP]
+    double* part = tiles + 2 * NB * TP;   // [4][64]
+    double* acc = part + 4 * NB;          // [64]
+    double* xs = acc + NB;                // [64]
+    double* rdv = xs + NB;                // [64] reciprocal diagonal
+    const int tid = threadIdx.x;
+    for (int it = blockIdx.x; it < nblk; it += gridDim.x) {
+        const int i = dir == 0 ? it : nblk - 1 - it;
+        const int64_t i0 = (int64_t)i * NB;
+        // dependency list: forward j = i-nbw .. i-1 (oldest first); backward j = i+nbw .. i+1
+        const int jlo = dir == 0 ? max(0, i - nbw) : i + 1;
+        const int jhi = dir == 0 ? i - 1 : min(nblk - 1, i + nbw);
+        const int nj = jhi - jlo + 1;
+        auto tile_of = [&](int q) -> const double* {  // q-th dependency tile, then the diagonal
+            if (q == nj) return Mb + i0 + i0 * LD;
+            const int j = dir == 0 ? jlo + q : jhi - q;
+            return dir == 0 ? Mb + i0 + (int64_t)j * NB * LD        // tile (i, j)
+                            : Mb + (int64_t)j * NB + i0 * LD;       // tile (j, i)
+        };
+        if (tid < NB) acc[tid] = rhs[i0 + tid];
+        load_tile_async(tiles, tile_of(0), LD);
+        for (int q = 0; q <= nj; ++q) {
+            const int st = q & 1;
+            if (q < nj) load_tile_async(tiles + (st ^ 1) * NB * TP, tile_of(q + 1), LD);
+            else asm volatile("cp.async.commit_group;\n" ::);
+            if (q < nj) {
+                const int j = dir == 0 ? jlo + q : jhi - q;
+                if (tid == 0) {
+                    // bounded spin (~1 s): a missing producer reports ELMDDM_ENUMERIC instead of hanging
+                    for (long long spin = 0; ld_acquire(flags + j) < epoch; ++spin) {
+                        __nanosleep(64);
+                        if (spin > (1LL << 24)) {
+                            elm_set_status(status, ELMDDM_ENUMERIC, -1 - j);
+                            break;
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
             }
+            asm volatile("cp.async.wait_group 1;\n" ::);
+            __syncthreads();
+            const double* T = tiles + st * NB * TP;
+            if (q < nj) {
+                // forward: acc[r] -= sum_c T[r][c] xs[c];  backward: acc[c] -= sum_r T[r][c] xs[r]
+                const int o = tid & 63, p = tid >> 6;
+                double s = 0.0;
+                if (dir == 0) {
+#pragma unroll 4
+                    for (int c = p * 16; c < p * 16 + 16; ++c) s += T[c * TP + o] * xs[c];
+                } else {
+#pragma unroll 4
+                    for (int r = p * 16; r < p * 16 + 16; ++r) s += T[o * TP + r] * xs[r];
+                }
+                part[p * NB + o] = s;
+                __syncthreads();
+                if (tid < NB) acc[tid] -= part[tid] + part[NB + tid] + part[2 * NB + tid] + part[3 * NB + tid];
+            } else {
+              if (tid < NB) rdv[tid] = 1.0 / T[tid * TP + tid];
+              __syncthreads();
+              if (tid < 32) {
+                // diagonal solve with the tile (i, i) (lower): warp-level, reciprocal diagonal
+                const int lane = tid;
+                double z0 = acc[lane], z1 = acc[lane + 32];
+                if (dir == 0) {
+                    for (int cc = 0; cc < NB; ++cc) {
+                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31);
+                        xc = xc * rdv[cc];
+                        if (lane > cc) z0 -= T[cc * TP + lane] * xc;
+                        if (lane + 32 > cc) z1 -= T[cc * TP + lane + 32] * xc;
+                        if (lane == (cc & 31)) {
+                            if (cc < 32) z0 = xc;
+                            else z1 = xc;
+                        }
+                    }
+                } else {
+                    for (int cc = NB - 1; cc >= 0; --cc) {
+                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31);
+                        xc = xc * rdv[cc];
+                        if (lane < cc) z0 -= T[lane * TP + cc] * xc;
+                        if (lane + 32 < cc) z1 -= T[(lane + 32) * TP + cc] * xc;
+                        if (lane == (cc & 31)) {
+                            if (cc < 32) z0 = xc;
+                            else z1 = xc;
+                        }
+                    }
+                }
+                out[i0 + lane] = z0;
+                out[i0 + lane + 32] = z1;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release(flags + i, epoch);
+              }
+            }
+            __syncthreads();
         }
-        xs[lane] = z0;
-        xs[lane + 32] = z1;
-    }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-        for (int t = threadIdx.x; t < n; t += blockDim.x) u[k0 + t] = xs[t];
-        return;
-    }
-    const int64_t c0 = k0 - (int64_t)blockIdx.x * NB;  // target block k - t
-    const double* Ap = Mb + k0 + c0 * LD;              // tile (k, k-t): rows k0.., cols c0..
-    for (int cc = threadIdx.x; cc < NB; cc += blockDim.x) {
-        double acc = 0.0;
-        for (int r = 0; r < n; ++r) acc += Ap[r + (int64_t)cc * LD] * xs[r];
-        z[c0 + cc] -= acc;
     }
 }
 
@@ -428,17 +471,34 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
-    for (int k = 0; k < nblk; ++k) {
-        const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
-        KTimer kt(c, ELMDDM_K_TRSV, st);
-        k_fwd<<<1 + nsub, 128, 0, st>>>(Mband, LD, k, NB, y, z);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    for (int k = nblk - 1; k >= 0; --k) {
-        const int nsub = k < nbw ? k : nbw;
-        KTimer kt(c, ELMDDM_K_TRSV, st);
-        k_bwd<<<1 + nsub, 128, 0, st>>>(Mband, LD, k, NB, z, uG);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // triangular solves: one cooperative wavefront kernel per direction
+    {
+        static int coop_grid = 0;
+        if (!coop_grid) {
+            if ((e = cudaFuncSetAttribute(k_band_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
+                cudaSuccess)
+                return e;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band_trsv, 256, TRSV_SMEM);
+            coop_grid = (per_sm > 0 ? 1 : 0) * c->nsm;
+            if (coop_grid <= 0) coop_grid = 1;
+        }
+        int grid = nblk < coop_grid ? nblk : coop_grid;
+        int* flags = c->d_flags;
+        for (int dir = 0; dir < 2; ++dir) {
+            int epoch = ++c->trsv_epoch;
+            const double* rhs = dir == 0 ? y : z;
+            double* out = dir == 0 ? z : uG;
+            int64_t LDv = LD;
+            int nblk_v = nblk, nbw_v = nbw;
+            ElmStatus* stp = c->d_status;
+            void* args[] = {(void*)&Mband, (void*)&LDv, (void*)&nblk_v, (void*)&nbw_v, (void*)&rhs, (void*)&out,
+                            (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
+            KTimer kt(c, ELMDDM_K_TRSV, st);
+            if ((e = cudaLaunchCooperativeKernel((void*)k_band_trsv, dim3(grid), dim3(256), args, TRSV_SMEM, st)) !=
+                cudaSuccess)
+                return e;
+        }
     }
     return cudaSuccess;
 }

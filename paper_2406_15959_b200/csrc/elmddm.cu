@@ -254,6 +254,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         int g = S >= 64 ? 4 : 1;
         if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
         c->qr_groups = g < 1 ? 1 : g;
+        if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));
@@ -283,7 +284,9 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     c->work_back = z.S * z.ld;
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
-        (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess) {
+        (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess ||
+        (e = cudaMalloc((void**)&c->d_flags, sizeof(int) * (z.G_pad / ELM_NB + 1))) != cudaSuccess ||
+        (e = cudaMemset(c->d_flags, 0, sizeof(int) * (z.G_pad / ELM_NB + 1))) != cudaSuccess) {
         elmddm_destroy(c);
         return ELMDDM_ECUDA;
     }
@@ -303,6 +306,7 @@ void elmddm_destroy(elmddm_ctx* c) {
         cudaEventDestroy(p.second.second);
     }
     cudaFree(c->d_status);
+    cudaFree(c->d_flags);
     cudaFree(c->d_sub_face);
     cudaFree(c->d_qsrc);
     cudaFree(c->d_pair_ptr);
@@ -337,7 +341,8 @@ elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {
         return cuda_fail(c, e, "elmddm_sync");
     if (h.code != 0) {
         cudaMemset(c->d_status, 0, sizeof(ElmStatus));
-        c->err = "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info);
+        c->err = h.info >= 0 ? "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info)
+                             : "interface triangular solve: block " + std::to_string(-1 - h.info) + " never completed";
         return (elmddm_status)h.code;
     }
     return ELMDDM_OK;

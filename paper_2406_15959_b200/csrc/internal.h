@@ -62,6 +62,9 @@ struct elmddm_ctx {
 
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
+    int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
+    mutable int trsv_epoch = 0;
     mutable std::vector<cudaStream_t> gstreams;
     mutable cudaEvent_t ev_fork = nullptr;
     mutable std::vector<cudaEvent_t> ev_join;

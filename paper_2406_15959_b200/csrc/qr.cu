@@ -14,6 +14,8 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <algorithm>
 #include <vector>
 #include <cstdio>
@@ -576,8 +578,258 @@ __global__ void __launch_bounds__(wy::NT, 2) k_wy_update(const double* __restric
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// TMA version of the fused compact-WY trailing update (operands staged by cp.async.bulk.tensor
+// with 128B swizzle, mbarrier-tracked 2-stage pipeline; updated C chunks written back by TMA
+// stores).  Same arithmetic as k_wy_update.  A 32-row chunk = 2 TMA boxes of 16 rows x 64 cols.
+// ------------------------------------------------------------------------------------------
+namespace wyt {
+constexpr int NT = 256, CH = 32, PADZ = 64 + 4;
+constexpr int BOX = 16 * 64;              // doubles per TMA box
+constexpr int STAGE = 4 * BOX;            // V (2 boxes) + C (2 boxes)
+constexpr int SMEM = (2 * STAGE + 64 * PADZ) * 8 + 64 + 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// element (row 0..31, col 0..63) of a 32-row chunk stored as two 128B-swizzled boxes
+#ifdef ELM_SWZ128
+// CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk index (bits 4-6) ^= 128-byte row index (bits 7-9)
+__device__ __forceinline__ int sw(int row, int col) {
+    const int r = row & 15;
+    return (row >> 4) * BOX + col * 16 + ((((r >> 1) ^ (col & 7))) << 1) + (r & 1);
+}
+#define ELM_SWIZZLE CU_TENSOR_MAP_SWIZZLE_128B
+#else
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (both DMMA fragment orientations conflict-free): 32-byte chunk index (bits 5-6) ^= bits 7-8
+__device__ __forceinline__ int sw(int row, int col) {
+    const int r = row & 15;
+    return (row >> 4) * BOX + col * 16 + ((((r >> 2) ^ (col & 3))) << 2) + (r & 3);
+}
+#define ELM_SWIZZLE CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+#endif
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load(double* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(su32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* tm, int c0, int c1, int c2, const double* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                 ::"l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(src)) : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+}  // namespace wyt
+
+__global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ CUtensorMap tmV,
+                                                       const __grid_constant__ CUtensorMap tmK,
+                                                       const double* __restrict__ Tbuf, int64_t ld, int j0, int nb,
+                                                       int c0, int N, int s_off) {
+    using namespace wyt;
+    extern __shared__ uint8_t raw[];
+    double* base = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    double* stg = base;                        // 2 stages x (V box0, V box1, C box0, C box1)
+    double* Zs = base + 2 * STAGE;             // [64 n][PADZ]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Zs + 64 * PADZ);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sl = s_off + blockIdx.y;
+    const int ncol0 = c0 + blockIdx.x * 64;
+    const int R = (int)(ld - j0), nch = R / CH;
+    const double* T = Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t par0 = 0, par1 = 0;
+    auto issue = [&](int c, int st) {
+        double* d = stg + st * STAGE;
+        mbar_expect(&bar[st], 4 * BOX * 8);
+        tma_load(d, &tmV, j0 + c * CH, 0, sl, &bar[st]);
+        tma_load(d + BOX, &tmV, j0 + c * CH + 16, 0, sl, &bar[st]);
+        tma_load(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st]);
+        tma_load(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st]);
+    };
+    auto wait_stage = [&](int st) {
+        if (st == 0) {
+            mbar_wait(&bar[0], par0);
+            par0 ^= 1;
+        } else {
+            mbar_wait(&bar[1], par1);
+            par1 ^= 1;
+        }
+    };
+    // ---------------- phase 1: W = V^T C ----------------
+    const int wm = warp & 1, wn = warp >> 1;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    if (tid == 0) issue(0, 0);
+    for (int c = 0; c < nch; ++c) {
+        const int st = c & 1;
+        if (tid == 0 && c + 1 < nch) issue(c + 1, st ^ 1);
+        wait_stage(st);
+        const double* Vs = stg + st * STAGE;
+        const double* Cs = Vs + 2 * BOX;
+#pragma unroll
+        for (int ks = 0; ks < CH / 4; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = Vs[sw(kk, wm * 32 + mt * 8 + (lane >> 2))];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Cs[sw(kk, wn * 16 + nt * 8 + (lane >> 2))];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();
+    }
+    // ---------------- phase 2: Z = -T^T W ----------------
+    double* Ts = stg;  // [64 i][PADZ]
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int i = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                Zs[n * PADZ + i] = acc[mt][nt][e];
+            }
+    for (int t = tid; t < 64 * 64; t += NT) {
+        int k = t & 63, i = t >> 6;
+        Ts[i * PADZ + k] = (i < nb && k < nb) ? T[k + 64 * i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int ks = 0; ks < 16; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double af[4], bf[2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = Ts[(wm * 32 + mt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bf[nt] = Zs[(wn * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int i = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                Zs[n * PADZ + i] = -acc[mt][nt][e];
+            }
+    __syncthreads();
+    // ---------------- phase 3: C += V (-Z) ----------------
+    const int wm3 = warp & 1, wn3 = warp >> 1;
+    if (tid == 0) issue(0, nch & 1 ? 1 : 0);  // continue the stage rotation of phase 1
+    const int sbase = nch & 1;
+    for (int c = 0; c < nch; ++c) {
+        const int st = (c + sbase) & 1;
+        if (tid == 0 && c + 1 < nch) {
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // stage st^1 stored?
+            issue(c + 1, st ^ 1);
+        }
+        wait_stage(st);
+        const double* Vs = stg + st * STAGE;
+        double* Cs = stg + st * STAGE + 2 * BOX;
+        double a3[2][2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm3 * 16 + mt * 8 + (lane >> 2), n = wn3 * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    a3[mt][nt][e] = Cs[sw(r, n)];
+                }
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[2], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) af[mt] = Vs[sw(wm3 * 16 + mt * 8 + (lane >> 2), kk)];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Zs[(wn3 * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) dmma(a3[mt][nt][0], a3[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncthreads();  // all reads of this C stage done
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    int r = wm3 * 16 + mt * 8 + (lane >> 2), n = wn3 * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    Cs[sw(r, n)] = a3[mt][nt][e];
+                }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            tma_store(&tmK, j0 + c * CH, ncol0, sl, Cs);
+            tma_store(&tmK, j0 + c * CH + 16, ncol0, sl, Cs + BOX);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * (R + 4) + 8 * 56 * 2 + RED_ELEMS + 40 + 64 + 8) * 8; }
 
+}  // namespace
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+// 3-D fp64 tensor map {d0 rows (contiguous), d1 columns (stride d0*8 B), d2 batches (stride s2 elems)},
+// box 16 x 64 x 1, 128B swizzle, out-of-bounds elements read as zero.
+bool encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s2) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    cuuint64_t strides[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(s2 * 8)};
+    cuuint32_t box[3] = {16, 64, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, ELM_SWIZZLE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 }  // namespace
 
 cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, double* work, cudaStream_t st) {
@@ -590,6 +842,14 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     if (e != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
         return e;
+    if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wyt::SMEM)) != cudaSuccess)
+        return e;
+    // TMA descriptors: K_aug {ld, ncols, S} and V {ld, nb, S} (columns >= nb read as zero), boxes 16 x 64
+    CUtensorMap tmK, tmV64, tmVlast;
+    const int nb_last = M % ELM_NB == 0 ? ELM_NB : M % ELM_NB;
+    bool use_tma = c->use_tma && encode_tmap(&tmK, Kaug, ld, ncols, S, ld * ncols) &&
+                   encode_tmap(&tmV64, Vbuf, ld, ELM_NB, S, ELM_NB * ld) &&
+                   encode_tmap(&tmVlast, Vbuf, ld, nb_last, S, ELM_NB * ld);
     // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
     // subdomains are independent).
@@ -621,7 +881,11 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             if (n_tr <= 0) continue;
             dim3 grid((unsigned)((n_tr + 63) / 64), (unsigned)(g1 - g0));
             KTimer kt(c, ELMDDM_K_GEMM_QR, streams[g]);
-            k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
+            if (use_tma)
+                k_wy_tma<<<grid, wyt::NT, wyt::SMEM, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
+                                                                   j0 + nb, n_tr, g0);
+            else
+                k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
