@@ -96,14 +96,14 @@ __device__ bool potrf_tile(double* L, double* rd) {
             }
             const int I = J + rem;
             const int ri = b0 + 8 * I + (lane >> 2), cl = b0 + 8 * J + 2 * (lane & 3);
-            double c0 = L[ri * LP + cl], c1 = L[ri * LP + cl + 1];
+            double c0 = -L[ri * LP + cl], c1 = -L[ri * LP + cl + 1];
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
                 const int kk = j0 + ks * 4 + (lane & 3);
-                dmma_c(c0, c1, -L[(b0 + 8 * I + (lane >> 2)) * LP + kk], L[(b0 + 8 * J + (lane >> 2)) * LP + kk]);
+                dmma_c(c0, c1, L[(b0 + 8 * I + (lane >> 2)) * LP + kk], L[(b0 + 8 * J + (lane >> 2)) * LP + kk]);
             }
-            L[ri * LP + cl] = c0;
-            L[ri * LP + cl + 1] = c1;
+            L[ri * LP + cl] = -c0;
+            L[ri * LP + cl + 1] = -c1;
         }
         __syncthreads();
     }
@@ -150,13 +150,13 @@ __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int
         if (b > 0 && warp < NB / 8) {
             // Xs[:, c8:c8+8] -= Xs[:, 0:c8] L[c8:c8+8, 0:c8]^T   (warp = 8-row m-tile)
             const int ri = warp * 8 + (lane >> 2), cl = c8 + 2 * (lane & 3);
-            double c0 = Xs[ri * LP + cl], c1 = Xs[ri * LP + cl + 1];
+            double c0 = -Xs[ri * LP + cl], c1 = -Xs[ri * LP + cl + 1];
             for (int ks = 0; ks < 2 * b; ++ks) {
                 const int kk = ks * 4 + (lane & 3);
-                dmma_c(c0, c1, -Xs[(warp * 8 + (lane >> 2)) * LP + kk], L[(c8 + (lane >> 2)) * LP + kk]);
+                dmma_c(c0, c1, Xs[(warp * 8 + (lane >> 2)) * LP + kk], L[(c8 + (lane >> 2)) * LP + kk]);
             }
-            Xs[ri * LP + cl] = c0;
-            Xs[ri * LP + cl + 1] = c1;
+            Xs[ri * LP + cl] = -c0;
+            Xs[ri * LP + cl + 1] = -c1;
         }
         __syncthreads();
         if (threadIdx.x < NB) {
@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int
 // while j is unchanged, A tiles are double-buffered with cp.async, C tiles are prefetched into
 // registers one tile ahead.  grid min(ntiles, 2*SMs), 256 threads, ~104 KB shared memory.
 // ------------------------------------------------------------------------------------------
-constexpr int SYRK_SMEM = 3 * NB * LP * 8;
+constexpr int SYRK_SMEM = 3 * NB * LP * 8;        // KP = 1
+constexpr int SYRK2_SMEM = 6 * NB * LP * 8;       // KP = 2
 
 __device__ __forceinline__ void cpa16(double* dst, const double* src) {
     unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -224,21 +225,30 @@ __device__ __forceinline__ void tile_of(int t, int nsub, int& i, int& j) {
     i = j + rem;
 }
 
-__global__ void __launch_bounds__(256, 2) k_syrk_band(double* __restrict__ Mb, int64_t LD, int k, int nsub, int ntiles) {
+// KP = 1: C_ij -= L_{i,k} L_{j,k}^T for the window at block k+1 (tiles 0 <= j <= i < nsub).
+// KP = 2: two Cholesky steps merged into one rank-128 update of the window at block k+2:
+//         C_ij -= L_{i,k} L_{j,k}^T + L_{i,k+1} L_{j,k+1}^T, where tiles of column k beyond the
+//         band (relative row > nbw-2) are zero and skipped.
+template <int KP>
+__global__ void __launch_bounds__(256, KP == 1 ? 2 : 1) k_syrk_band(double* __restrict__ Mb, int64_t LD, int k, int nsub,
+                                                                    int ntiles, int nbw) {
     extern __shared__ __align__(16) double ssm[];
-    double* Bs = ssm;                 // L_j  as [k][n]  (column-major tile: Bs[c*LP + r] = L_j[r][c])
-    double* As0 = ssm + NB * LP;      // L_i  as [k][row]
+    double* Bs = ssm;                   // KP tiles of column j: Bs[p][c*LP + r] = L_{j,k+p}[r][c]
+    double* As0 = ssm + KP * NB * LP;   // 2 buffers x KP tiles of row i
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
     const int per = (ntiles + gridDim.x - 1) / gridDim.x;
     const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
     if (t0 >= t1) return;
-    const int64_t k0 = (int64_t)k * NB, w0 = k0 + NB;  // window origin
-    const double* P = Mb + w0 + k0 * LD;               // panel: tile i at P + i*NB
+    const int64_t k0 = (int64_t)k * NB, w0 = k0 + KP * NB;  // window origin
+    // panel p (column k+p), relative window tile row i -> tile (k+KP+i, k+p); valid iff KP-p+i <= nbw
+    auto panel = [&](int p, int i) -> const double* { return Mb + (w0 + (int64_t)i * NB) + (k0 + (int64_t)p * NB) * LD; };
+    auto valid = [&](int p, int i) { return KP - p + i <= nbw; };
     int i, j;
     tile_of(t0, nsub, i, j);
     int jb = -1;
-    // prefetch first A tile
-    load_panel_tile(As0, P + (int64_t)i * NB, LD);
+#pragma unroll
+    for (int p = 0; p < KP; ++p)
+        if (valid(p, i)) load_panel_tile(As0 + p * NB * LP, panel(p, i), LD);
     cpa_commit();
     double cn[4][2][2];
     auto load_c = [&](int ti, int tj, double (&cr)[4][2][2]) {
@@ -257,38 +267,45 @@ __global__ void __launch_bounds__(256, 2) k_syrk_band(double* __restrict__ Mb, i
     for (int t = t0; t < t1; ++t) {
         const int ci = i, cj = j, buf = (t - t0) & 1;
         if (cj != jb) {
-            // (re)load B = L_j; previous readers of Bs are done (barrier at the end of the loop)
-            load_panel_tile(Bs, P + (int64_t)cj * NB, LD);
+#pragma unroll
+            for (int p = 0; p < KP; ++p)
+                if (valid(p, cj)) load_panel_tile(Bs + p * NB * LP, panel(p, cj), LD);
             cpa_commit();
             jb = cj;
         }
-        double acc[4][2][2];
+        double acc[4][2][2];  // holds -C: the DMMAs add A B^T, the store negates back
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = cn[mt][nt][0], acc[mt][nt][1] = cn[mt][nt][1];
-        // next tile: prefetch its A into the other buffer and its C into registers
+            for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = -cn[mt][nt][0], acc[mt][nt][1] = -cn[mt][nt][1];
         if (t + 1 < t1) {
-            tile_of(t + 1, nsub, i, j);
-            load_panel_tile(As0 + (buf ^ 1) * NB * LP, P + (int64_t)i * NB, LD);
+            if (++i == nsub) i = ++j;  // next tile of the column-major lower triangle
+#pragma unroll
+            for (int p = 0; p < KP; ++p)
+                if (valid(p, i)) load_panel_tile(As0 + ((buf ^ 1) * KP + p) * NB * LP, panel(p, i), LD);
         }
         cpa_commit();
         if (t + 1 < t1) load_c(i, j, cn);
         cpa_wait<1>();
         __syncthreads();
-        const double* As = As0 + buf * NB * LP;
+#pragma unroll
+        for (int p = 0; p < KP; ++p) {
+            if (!valid(p, ci) || !valid(p, cj)) continue;  // tile outside the band: zero contribution
+            const double* As = As0 + (buf * KP + p) * NB * LP;
+            const double* Bp = Bs + p * NB * LP;
 #pragma unroll 4
-        for (int ks = 0; ks < NB / 4; ++ks) {
-            const int kk = ks * 4 + (lane & 3);
-            double af[4], bf[2];
+            for (int ks = 0; ks < NB / 4; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                double af[4], bf[2];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) af[mt] = -As[kk * LP + wm * 32 + mt * 8 + (lane >> 2)];
+                for (int mt = 0; mt < 4; ++mt) af[mt] = As[kk * LP + wm * 32 + mt * 8 + (lane >> 2)];
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) bf[nt] = Bs[kk * LP + wn * 16 + nt * 8 + (lane >> 2)];
+                for (int nt = 0; nt < 2; ++nt) bf[nt] = Bp[kk * LP + wn * 16 + nt * 8 + (lane >> 2)];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt)
+                for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+                    for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+            }
         }
         double* Ct = Mb + (w0 + (int64_t)ci * NB) + (w0 + (int64_t)cj * NB) * LD;
 #pragma unroll
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(256, 2) k_syrk_band(double* __restrict__ Mb, i
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     int r = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
-                    Ct[r + (int64_t)c * LD] = acc[mt][nt][e];
+                    Ct[r + (int64_t)c * LD] = -acc[mt][nt][e];
                 }
         __syncthreads();  // buffers of this tile may be overwritten by the next prefetch
     }
@@ -452,24 +469,49 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     if (!attr) {
         if ((e = cudaFuncSetAttribute(k_potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_syrk_band, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM)) !=
+            (e = cudaFuncSetAttribute(k_syrk_band<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_syrk_band<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK2_SMEM)) !=
                 cudaSuccess)
             return e;
         attr = true;
     }
     if ((e = cudaMemcpyAsync(y, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-    for (int k = 0; k < nblk; ++k) {
+    auto potrf = [&](int k) -> cudaError_t {
         const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
-        { KTimer kt(c, ELMDDM_K_POTRF, st);
-        k_potrf_trsm<<<1 + nsub, 256, POTRF_SMEM, st>>>(Mband, LD, k, NB, c->d_status); }
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if (nsub > 0) {
-            const int ntiles = nsub * (nsub + 1) / 2;
-            const int grid = ntiles < 2 * c->nsm ? ntiles : 2 * c->nsm;
+        KTimer kt(c, ELMDDM_K_POTRF, st);
+        k_potrf_trsm<<<1 + nsub, 256, POTRF_SMEM, st>>>(Mband, LD, k, NB, c->d_status);
+        return cudaGetLastError();
+    };
+    auto syrk1 = [&](int k, int ntiles_limit) -> cudaError_t {  // window at k+1, first ntiles tiles
+        const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
+        if (nsub <= 0) return cudaSuccess;
+        int ntiles = nsub * (nsub + 1) / 2;
+        if (ntiles_limit >= 0 && ntiles_limit < ntiles) ntiles = ntiles_limit;
+        const int grid = ntiles < 2 * c->nsm ? ntiles : 2 * c->nsm;
+        KTimer kt(c, ELMDDM_K_GEMM_CHOL, st);
+        k_syrk_band<1><<<grid, 256, SYRK_SMEM, st>>>(Mband, LD, k, nsub, ntiles, nbw);
+        return cudaGetLastError();
+    };
+    int k = 0;
+    for (; k + 1 < nblk; k += 2) {
+        // step k, then only column k+1 of its update, step k+1, then one rank-128 update of the rest
+        const int nsub1 = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
+        if ((e = potrf(k)) != cudaSuccess) return e;
+        if ((e = syrk1(k, nsub1)) != cudaSuccess) return e;  // the first window column = block column k+1
+        if ((e = potrf(k + 1)) != cudaSuccess) return e;
+        const int nsub2 = (nblk - 2 - k) < nbw ? (nblk - 2 - k) : nbw;
+        if (nsub2 > 0) {
+            const int ntiles = nsub2 * (nsub2 + 1) / 2;
+            const int grid = ntiles < c->nsm ? ntiles : c->nsm;
             KTimer kt(c, ELMDDM_K_GEMM_CHOL, st);
-            k_syrk_band<<<grid, 256, SYRK_SMEM, st>>>(Mband, LD, k, nsub, ntiles);
+            k_syrk_band<2><<<grid, 256, SYRK2_SMEM, st>>>(Mband, LD, k, nsub2, ntiles, nbw);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
+    }
+    if (k < nblk) {
+        if ((e = potrf(k)) != cudaSuccess) return e;
+        if ((e = syrk1(k, -1)) != cudaSuccess) return e;
     }
     // triangular solves: one cooperative wavefront kernel per direction
     {
