@@ -640,7 +640,9 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
                                                        int c0, int N, int s_off) {
     using namespace wyt;
     extern __shared__ uint8_t raw[];
-    double* base = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment for the swizzled TMA boxes; pointer arithmetic on `raw` keeps the
+    // shared address space visible to the compiler (LDS, not generic LD)
+    double* base = reinterpret_cast<double*>(raw + ((1024u - (su32(raw) & 1023u)) & 1023u));
     double* stg = base;                        // 2 stages x (V box0, V box1, C box0, C box1)
     double* Zs = base + 2 * STAGE;             // [64 n][PADZ]
     uint64_t* bar = reinterpret_cast<uint64_t*>(Zs + 64 * PADZ);
