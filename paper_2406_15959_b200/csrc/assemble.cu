@@ -160,7 +160,15 @@ __device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
 __device__ __forceinline__ void tanh_derivs(double z, double& s0, double& s1, double& s2) {
     double za = fmin(fabs(z), 40.0);
     double E = exp(-2.0 * za);             // in (0, 1]
-    double d = 1.0 / (1.0 + E);
+    double d;
+    {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(1.0 + E));
+        double e = fma(-(1.0 + E), r, 1.0);
+        r = fma(r, e, r);
+        e = fma(-(1.0 + E), r, 1.0);
+        d = fma(r, e, r);
+    }
     double t = (1.0 - E) * d;               // tanh |z|
     s0 = copysign(t, z);
     s1 = 4.0 * E * d * d;                   // sech^2
@@ -170,45 +178,94 @@ __device__ __forceinline__ void tanh_derivs(double z, double& s0, double& s1, do
 constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
 constexpr int AS_NT = 256;
 
+// 1/x for x in [1, 1e30]: MUFU.RCP64H seed + two Newton steps (full double precision)
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 // Kaug[s][col][row]: grid (ceil(ncols / AS_COLS), S).
+// Neuron columns use the separable form of SURVEY §8(a): with the subdomain centre c and
+// b~ = b + w.c,  E = e^{2z} = [e^{2 w_x (x - c_x) + 2 b~}] [e^{2 w_y (y - c_y)}], the two factors
+// tabulated per neuron over the p+q+2 distinct x (resp. y) coordinates of the subdomain's rows;
+// then d = 1/(1+E), sigma = 1 - 2d, sigma' = 4 E d^2, -|w|^2 sigma'' = 2|w|^2 sigma sigma'.
+// |z| <= |w|_1 (h/2 + r) stays O(10) for the paper's initialisation, so E never overflows.
 __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
                                                     const double* __restrict__ W, const double* __restrict__ b,
                                                     double* __restrict__ Kaug) {
-    const int M = cfg.M, q = cfg.q, P = cfg.P, pp = cfg.p * cfg.p;
+    const int M = cfg.M, q = cfg.q, P = cfg.P, p = cfg.p, pp = p * p;
     const int m = pp + 4 * q;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
     const int i = s % P, j = s / P;
     const int c0 = blockIdx.x * AS_COLS;
     double* Ks = Kaug + (int64_t)sl * ld * ncols;
-    __shared__ double sw[AS_COLS][3];
-    if (threadIdx.x < AS_COLS) {
-        int col = c0 + threadIdx.x;
-        if (col < M) {
-            sw[threadIdx.x][0] = W[((int64_t)sl * M + col) * 2];
-            sw[threadIdx.x][1] = W[((int64_t)sl * M + col) * 2 + 1];
-            sw[threadIdx.x][2] = b[(int64_t)sl * M + col];
-        }
-    }
-    __syncthreads();
     if (c0 < M) {
-        // neuron columns: interior rows -|w|^2 sigma'', boundary / interface rows sigma
-        for (int r = threadIdx.x; r < ld; r += AS_NT) {
-            double x = 0.0, y = 0.0;
-            int kind = -2, k = 0;
-            if (r < m) row_point(cfg, i, j, r, x, y, kind, k);
+        extern __shared__ double tab[];      // [AS_COLS][2][ntab]
+        __shared__ double w2s[AS_COLS];
+        const int ntab = p + q + 2;
+        // distinct coordinates: [interior (p) | x0 | x0+h | edge positions (q)], same for y
+        const double cx = (double)(2 * i + 1) / (double)(2 * P), cy = (double)(2 * j + 1) / (double)(2 * P);
+        for (int t = threadIdx.x; t < AS_COLS * 2 * ntab; t += AS_NT) {
+            const int cc = t / (2 * ntab), axis = (t / ntab) & 1, k = t % ntab;
+            const int col = min(c0 + cc, M - 1);
+            const int ij = axis == 0 ? i : j;
+            double coord;
+            if (k < p) coord = (double)(ij * (p + 1) + k + 1) / (double)(P * (p + 1));
+            else if (k == p) coord = (double)ij / (double)P;
+            else if (k == p + 1) coord = (double)(ij + 1) / (double)P;
+            else coord = (double)(ij * (q + 1) + (k - p - 2) + 1) / (double)(P * (q + 1));
+            const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
+            double arg;
+            if (axis == 0) arg = 2.0 * (wx * (coord - cx) + (b[(int64_t)sl * M + col] + wx * cx + wy * cy));
+            else arg = 2.0 * wy * (coord - cy);
+            tab[t] = exp(arg);
+        }
+        if (threadIdx.x < AS_COLS) {
+            const int col = min(c0 + threadIdx.x, M - 1);
+            const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
+            w2s[threadIdx.x] = 2.0 * (wx * wx + wy * wy);
+        }
+        __syncthreads();
+        const int ncc = min(AS_COLS, M - c0);
+        // two consecutive rows per thread -> 16-byte stores
+        for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
+            int xi[2], yi[2], kind[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 2 * r2 + e;
+                if (r < pp) {
+                    xi[e] = r % p;
+                    yi[e] = r / p;
+                    kind[e] = 0;
+                } else if (r < m) {
+                    const int t = r - pp, ed = t / q, k = t % q;
+                    kind[e] = 1;
+                    xi[e] = ed == 0 ? p : (ed == 1 ? p + 1 : p + 2 + k);
+                    yi[e] = ed == 2 ? p : (ed == 3 ? p + 1 : p + 2 + k);
+                } else {
+                    kind[e] = 2;
+                    xi[e] = yi[e] = 0;
+                }
+            }
 #pragma unroll
             for (int cc = 0; cc < AS_COLS; ++cc) {
-                const int col = c0 + cc;
-                if (col >= M) break;
-                double v = 0.0;
-                if (kind != -2) {
-                    double wx = sw[cc][0], wy = sw[cc][1];
-                    double z = wx * x + wy * y + sw[cc][2];
-                    double s0, s1, s2;
-                    tanh_derivs(z, s0, s1, s2);
-                    v = (kind == -1) ? -(wx * wx + wy * wy) * s2 : s0;
+                if (cc >= ncc) break;
+                const double* tx = tab + cc * 2 * ntab;
+                const double* ty = tx + ntab;
+                double v[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double E = tx[xi[e]] * ty[yi[e]];
+                    const double d = fast_rcp(1.0 + E);
+                    const double sg = fma(-2.0, d, 1.0);
+                    const double s1 = 4.0 * E * d * d;
+                    v[e] = kind[e] == 0 ? w2s[cc] * sg * s1 : (kind[e] == 1 ? sg : 0.0);
                 }
-                Ks[(int64_t)col * ld + r] = v;
+                *reinterpret_cast<double2*>(Ks + (int64_t)(c0 + cc) * ld + 2 * r2) = make_double2(v[0], v[1]);
             }
         }
         return;
@@ -306,8 +363,9 @@ cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double
 cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
                             cudaStream_t st) {
     dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
+    const size_t tab_bytes = sizeof(double) * AS_COLS * 2 * (c->cfg.p + c->cfg.q + 2);
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
-    k_assemble<<<g1, AS_NT, 0, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug); }
+    k_assemble<<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 g2(4, (unsigned)c->sz.S);
