@@ -86,6 +86,8 @@ typedef struct {
     int64_t band_ld, band_nbw, band_elems; /* Schur matrix storage, see elmddm_band_index       */
     int64_t G_pad;                          /* G rounded up to the 64-tile                       */
     int64_t halfband;                       /* exact half-bandwidth of the Schur matrix          */
+    int64_t chol_tasks;                     /* 64 x 64 tiles of L inside the envelope             */
+    int64_t chol_flops;                     /* envelope Cholesky work: 2 * 64^3 per tile update   */
 } elmddm_sizes_t;
 
 /* ---- context ------------------------------------------------------------------------------ */
@@ -99,8 +101,13 @@ elmddm_status elmddm_sizes(const elmddm_ctx* ctx, elmddm_sizes_t* out);
 elmddm_status elmddm_sync(elmddm_ctx* ctx, void* stream);
 /* Host export of the u_Gamma ordering: xy_host[G][2] coordinates of the interface unknowns.   */
 elmddm_status elmddm_interface_points(const elmddm_ctx* ctx, double* xy_host);
-/* Offset of Schur-matrix element (i, j), i >= j, |i-j| <= halfband, in the band storage.     */
+/* Offset of Schur-matrix element (i, j), i >= j, i - j <= halfband, in the packed tile storage:
+ * tile (I, J) = (i/64, j/64) at (I*(band_nbw+1) + I-J) * 64*band_ld, element (i%64, j%64) at
+ * (i%64) + (j%64)*band_ld inside it (band_ld = 68: padded column stride).  -1 if out of range.  */
 int64_t elmddm_band_index(const elmddm_ctx* ctx, int64_t i, int64_t j);
+/* Host export of the factorisation plan: first[G_pad/64] (first nonzero tile column of every
+ * tile row of the envelope) and tasks[chol_tasks][2] = (I, J) tile of L, column by column.     */
+elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* first, int32_t* tasks);
 
 /* ---- hot path ----------------------------------------------------------------------------- */
 /* eqn:init: W[S][M][2], b[S][M] for the local subdomains; xi[S][M][2] (may be NULL)
@@ -139,7 +146,9 @@ elmddm_status elmddm_schur_accumulate(elmddm_ctx* ctx, double* Kaug, double* At,
  * and g[G_pad].  work: >= work_elems doubles.                                                 */
 elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
                                         double* g, double* work, void* stream);
-/* Cholesky M = L L^T in place (band-limited, tiles of 64) and u = M^{-1} g into uG[G_pad].
+/* Cholesky M = L L^T in place over the envelope of M (64 x 64 tiles, left-looking) and
+ * u = M^{-1} g into uG[G_pad].  On return the off-diagonal tiles of Mband hold L and the
+ * diagonal tiles hold L(J,J)^{-1} (lower triangular, zeros above).  g is not modified.
  * Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot.                     */
 elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
                                             double* work, void* stream);
@@ -168,8 +177,8 @@ enum {
     ELMDDM_K_TRSM = 4,       /* R11^{-T} At diagonal-block solves             */
     ELMDDM_K_GEMM_SCHUR = 5, /* TRSM updates, flux product, Gram (DMMA)       */
     ELMDDM_K_IFACE = 6,      /* Q-row gather, M / g assembly (+ Q^T Q GEMM)   */
-    ELMDDM_K_POTRF = 7,      /* band Cholesky diagonal + panel solves         */
-    ELMDDM_K_GEMM_CHOL = 8,  /* band Cholesky SYRK updates (DMMA)             */
+    ELMDDM_K_POTRF = 7,      /* interface Cholesky: persistent left-looking tile kernel (DMMA) */
+    ELMDDM_K_GEMM_CHOL = 8,  /* (reserved; no kernel of this class since the persistent factorisation) */
     ELMDDM_K_TRSV = 9,       /* interface forward / backward substitution     */
     ELMDDM_K_BACK = 10,      /* local back-solve                              */
     ELMDDM_K_EVAL = 11,      /* evaluation                                    */

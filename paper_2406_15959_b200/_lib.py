@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libelmddm.so")
+# ELMDDM_LIB selects an instrumented build of the same library (tools/chol_prof.py)
+LIB_PATH = os.environ.get("ELMDDM_LIB", os.path.join(HERE, "libelmddm.so"))
 
 
 class ElmddmError(RuntimeError):
@@ -30,7 +31,7 @@ class Sizes(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "N", "S", "m", "ld", "ncols", "kaug", "G", "faces", "kaug_elems", "at_elems", "tau_elems",
         "pbuf_ld", "pbuf_elems", "sbuf_ld", "sbuf_elems", "work_elems", "band_ld", "band_nbw", "band_elems",
-        "G_pad", "halfband")]
+        "G_pad", "halfband", "chol_tasks", "chol_flops")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -41,13 +42,13 @@ STATUS = {0: "ELMDDM_OK", 1: "ELMDDM_EINVAL", 2: "ELMDDM_ENUMERIC", 3: "ELMDDM_E
 # every exported entry point of include/elmddm.h
 EXPORTS = [
     "elmddm_create", "elmddm_destroy", "elmddm_last_error", "elmddm_sizes", "elmddm_sync",
-    "elmddm_interface_points", "elmddm_band_index", "elmddm_init_hidden", "elmddm_assemble",
+    "elmddm_interface_points", "elmddm_band_index", "elmddm_chol_plan", "elmddm_init_hidden", "elmddm_assemble",
     "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
     "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
     "elmddm_set_timing", "elmddm_timing", "elmddm_dmma_probe",
 ]
 
-KCLASSES = ["init", "assemble", "panel", "gemm_qr", "trsm", "gemm_schur", "iface", "potrf", "gemm_chol", "trsv",
+KCLASSES = ["init", "assemble", "panel", "gemm_qr", "trsm", "gemm_schur", "iface", "chol", "gemm_chol", "trsv",
             "back", "eval"]
 
 
@@ -78,6 +79,7 @@ def load():
     L.elmddm_interface_points.argtypes = [ctxp, vp]
     L.elmddm_band_index.argtypes = [ctxp, i64, i64]
     L.elmddm_band_index.restype = i64
+    L.elmddm_chol_plan.argtypes = [ctxp, vp, vp]
     L.elmddm_init_hidden.argtypes = [ctxp, vp, vp, vp, vp]
     L.elmddm_assemble.argtypes = [ctxp, vp, vp, vp, vp, vp]
     L.elmddm_local_factor.argtypes = [ctxp, vp, vp, vp, vp]
@@ -94,7 +96,8 @@ def load():
         f = getattr(L, name)
         if f.restype is C.c_int or name in ("elmddm_create",):
             f.restype = st
-    for name in ["elmddm_create", "elmddm_sizes", "elmddm_sync", "elmddm_interface_points", "elmddm_init_hidden",
+    for name in ["elmddm_create", "elmddm_sizes", "elmddm_sync", "elmddm_interface_points", "elmddm_chol_plan",
+                 "elmddm_init_hidden",
                  "elmddm_assemble", "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
                  "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
                  "elmddm_set_timing", "elmddm_timing", "elmddm_dmma_probe"]:

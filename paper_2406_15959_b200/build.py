@@ -26,8 +26,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=(), lib: str = LIB) -> str:
+    """Compile every csrc/*.cu for sm_100a and link `lib` (extra: additional nvcc flags, e.g. a
+    profiling variant built to another file name)."""
+    if not force and lib == LIB and not needs_build():
         return LIB
     objs = []
     for src in sources():
@@ -37,11 +39,11 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

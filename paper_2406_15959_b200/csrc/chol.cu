@@ -1,337 +1,49 @@
-// chol.cu -- band-limited tiled Cholesky of the interface Schur matrix (eqn:schur is SPD,
-// P:412; reading R12: direct Cholesky instead of the paper's CG) and the two triangular solves.
+// chol.cu -- Cholesky factorisation of the interface Schur matrix (eqn:schur is SPD, P:412;
+// reading R12: a direct solve instead of the paper's CG) and the two triangular solves.
 //
-// Storage: element (i, j) of the lower band at Mband[i + j * LD] with LD = (nbw + 2) * 64 (or
-// LD = G_pad when dense): 64 x 64 tiles of the band are plain column-major sub-matrices with
-// leading dimension LD, so the SYRK updates run on the DMMA GEMM.  Only tiles (I, J) with
-// 0 <= I - J <= nbw are ever touched (no aliasing).
+// Storage (internal.h): packed 64 x 64 tiles of the lower band, tile (I, J) with
+// 0 <= I - J <= nbw contiguous at tile_off(I, J), element (r, c) at r + c * ELM_TLD (ELM_TLD = 68).
+// A tile (or its first 32 columns) is therefore one contiguous bulk copy that lands in shared
+// memory already in the padded, bank-conflict-free layout the DMMA fragments read.
+//
+// Factorisation: ONE persistent kernel, left-looking over the tiles of the envelope (skyline)
+// of M.  Tile-row I is structurally zero left of tile column first[I] (the envelope is closed
+// under Cholesky fill), so tile (I, J) of L, first[I] <= J <= I, is
+//     C      = M(I, J) - sum_{k = max(first[I], first[J])}^{J-1} L(I, k) L(J, k)^T   (DMMA)
+//     L(J,J), Y_J = L(J,J)^{-1} from C           (I == J: unblocked Cholesky + inverse in smem)
+//     L(I,J) = C L(J,J)^{-T}                      (I > J: X0 = C Y_J^T and one refinement step
+//                                                  X = X0 + (C - X0 L(J,J)^T) Y_J^T, three 64^3 DMMAs)
+// The k-sum streams 32-column halves of L(I,k) and L(J,k) through a 3-stage TMA bulk-copy /
+// mbarrier pipeline issued by one thread.  Tasks (I, J) are listed column by column and dealt
+// round-robin to co-resident CTAs; each finished tile publishes a per-tile flag (release /
+// acquire) and bumps its column's counter.  A task waits only for tiles of earlier columns or
+// for the diagonal of its own column, so the smallest unfinished task can always run (no
+// deadlock) and the trailing work of many columns overlaps the critical path.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
-#include <cstdio>
+
+#ifdef ELM_CHOL_PROF
+// per-task timeline of the factorisation (profiling builds only): start, end, flag-wait ns,
+// data-wait ns, epilogue start, CTA
+__device__ unsigned long long g_chol_prof[400000 * 6];
+__device__ unsigned long long g_chol_dprof[4096 * 8];  // diagonal tasks: stage timestamps
+#endif
 
 namespace {
 
 constexpr int NB = ELM_NB;
+constexpr int LP = ELM_TLD;
 
 __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-
-constexpr int LP = NB + 4;  // padded row stride (== 4 mod 16): conflict-free DMMA fragments
-
-// In-place Cholesky of the 64x64 tile L[i*LP + j] (lower part used), blocked by 8 columns:
-//   8x8 diagonal block by warp 0 (lanes = rows, rsqrt, no divisions),
-//   panel solve below it (one thread per row, reciprocal diagonal),
-//   rank-8 trailing update of the lower 8x8 tiles on the FP64 tensor pipe.
-// rd[] receives the reciprocal diagonal.  Returns false on a non-positive pivot.
-__device__ bool potrf_tile(double* L, double* rd) {
-    __shared__ int bad;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) bad = -1;
-    for (int j0 = 0; j0 < NB; j0 += 8) {
-        if (warp == 0) {
-            const int r = lane & 7, i = j0 + r;
-            double row[8];
-#pragma unroll
-            for (int l = 0; l < 8; ++l) row[l] = L[i * LP + j0 + l];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                double d = row[c];
-#pragma unroll
-                for (int l = 0; l < 8; ++l)
-                    if (l < c) d -= row[l] * row[l];
-                double dc = __shfl_sync(0xffffffffu, d, c);
-                if (lane == 0 && !(dc > 0.0) && bad < 0) bad = j0 + c;
-                dc = fmax(dc, 1e-300);
-                const double rs = rsqrt(dc);
-                double lc[8];
-#pragma unroll
-                for (int l = 0; l < 8; ++l) lc[l] = __shfl_sync(0xffffffffu, row[l], c);
-                if (r > c) {
-                    double v = row[c];
-#pragma unroll
-                    for (int l = 0; l < 8; ++l)
-                        if (l < c) v -= row[l] * lc[l];
-                    row[c] = v * rs;
-                } else if (r == c) {
-                    row[c] = dc * rs;
-                }
-                if (lane == c) rd[j0 + c] = rs;
-            }
-            if (lane < 8)
-#pragma unroll
-                for (int l = 0; l < 8; ++l)
-                    if (l <= r) L[i * LP + j0 + l] = row[l];
-        }
-        __syncthreads();
-        // panel rows below the diagonal block
-        for (int i = j0 + 8 + threadIdx.x; i < NB; i += blockDim.x) {
-            double x[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = L[i * LP + j0 + c];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                double v = x[c];
-#pragma unroll
-                for (int l = 0; l < 8; ++l)
-                    if (l < c) v -= x[l] * L[(j0 + c) * LP + j0 + l];
-                x[c] = v * rd[j0 + c];
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) L[i * LP + j0 + c] = x[c];
-        }
-        __syncthreads();
-        // trailing update, lower 8x8 tiles (I >= J) of the remaining block, K = 8
-        const int b0 = j0 + 8, nt = (NB - b0) / 8;
-        const int ntiles = nt * (nt + 1) / 2;
-        for (int tt = warp; tt < ntiles; tt += blockDim.x / 32) {
-            int J = 0, rem = tt;
-            while (rem >= nt - J) {
-                rem -= nt - J;
-                ++J;
-            }
-            const int I = J + rem;
-            const int ri = b0 + 8 * I + (lane >> 2), cl = b0 + 8 * J + 2 * (lane & 3);
-            double c0 = -L[ri * LP + cl], c1 = -L[ri * LP + cl + 1];
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                const int kk = j0 + ks * 4 + (lane & 3);
-                dmma_c(c0, c1, L[(b0 + 8 * I + (lane >> 2)) * LP + kk], L[(b0 + 8 * J + (lane >> 2)) * LP + kk]);
-            }
-            L[ri * LP + cl] = -c0;
-            L[ri * LP + cl + 1] = -c1;
-        }
-        __syncthreads();
-    }
-    return bad < 0;
-}
-
-constexpr int POTRF_SMEM = (2 * NB * LP + NB) * 8;
-
-// grid 1 + nsub, 256 threads.  Every CTA factors A_kk = L L^T in shared memory; CTA 0 writes
-// L_kk, CTA t >= 1 solves X L^T = A_{k+t,k} in place: 8-column blocks, each a DMMA update with
-// the already solved columns followed by an 8x8 triangular solve per row.
-__global__ void __launch_bounds__(256) k_potrf_trsm(double* __restrict__ Mb, int64_t LD, int k, int n,
-                                                    ElmStatus* status) {
-    extern __shared__ __align__(16) double psm[];
-    double* L = psm;              // [i*LP + j]
-    double* Xs = L + NB * LP;     // [i*LP + j]  panel tile, solved in place
-    double* rd = Xs + NB * LP;
-    (void)n;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t k0 = (int64_t)k * NB;
-    double* Akk = Mb + k0 + k0 * LD;
-    for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-        int i = t % NB, j = t / NB;
-        L[i * LP + j] = (i >= j) ? Akk[i + (int64_t)j * LD] : 0.0;
-    }
-    double* Ap = Mb + (k0 + (int64_t)blockIdx.x * NB) + k0 * LD;
-    if (blockIdx.x > 0)
-        for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-            int i = t % NB, j = t / NB;
-            Xs[i * LP + j] = Ap[i + (int64_t)j * LD];
-        }
-    __syncthreads();
-    const bool ok = potrf_tile(L, rd);
-    if (blockIdx.x == 0) {
-        if (!ok && threadIdx.x == 0) elm_set_status(status, ELMDDM_ENUMERIC, (int)k0);
-        for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-            int i = t % NB, j = t / NB;
-            if (i >= j) Akk[i + (int64_t)j * LD] = L[i * LP + j];
-        }
-        return;
-    }
-    for (int b = 0; b < NB / 8; ++b) {
-        const int c8 = 8 * b;
-        if (b > 0 && warp < NB / 8) {
-            // Xs[:, c8:c8+8] -= Xs[:, 0:c8] L[c8:c8+8, 0:c8]^T   (warp = 8-row m-tile)
-            const int ri = warp * 8 + (lane >> 2), cl = c8 + 2 * (lane & 3);
-            double c0 = -Xs[ri * LP + cl], c1 = -Xs[ri * LP + cl + 1];
-            for (int ks = 0; ks < 2 * b; ++ks) {
-                const int kk = ks * 4 + (lane & 3);
-                dmma_c(c0, c1, Xs[(warp * 8 + (lane >> 2)) * LP + kk], L[(c8 + (lane >> 2)) * LP + kk]);
-            }
-            Xs[ri * LP + cl] = -c0;
-            Xs[ri * LP + cl + 1] = -c1;
-        }
-        __syncthreads();
-        if (threadIdx.x < NB) {
-            const int i = threadIdx.x;
-            double x[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = Xs[i * LP + c8 + c];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                double v = x[c];
-#pragma unroll
-                for (int l = 0; l < 8; ++l)
-                    if (l < c) v -= x[l] * L[(c8 + c) * LP + c8 + l];
-                x[c] = v * rd[c8 + c];
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) Xs[i * LP + c8 + c] = x[c];
-        }
-        __syncthreads();
-    }
-    for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-        int i = t % NB, j = t / NB;
-        Ap[i + (int64_t)j * LD] = Xs[i * LP + j];
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// Band SYRK update of step k: C_ij -= L_i L_j^T for the lower tiles 0 <= j <= i < nsub of the
-// window starting at block k+1 (L_i = tile (k+1+i, k)).  The tile list (column-major lower
-// triangle) is cut into contiguous chunks, one per CTA: the B tile L_j stays in shared memory
-// while j is unchanged, A tiles are double-buffered with cp.async, C tiles are prefetched into
-// registers one tile ahead.  grid min(ntiles, 2*SMs), 256 threads, ~104 KB shared memory.
-// ------------------------------------------------------------------------------------------
-constexpr int SYRK_SMEM = 3 * NB * LP * 8;        // KP = 1
-constexpr int SYRK2_SMEM = 6 * NB * LP * 8;       // KP = 2
-
-__device__ __forceinline__ void cpa16(double* dst, const double* src) {
-    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// tile (stored column-major in the band, rows r0.., cols c0..) -> dst[row][col] with stride LP?
-// We keep A and B as [row][k] (row-major, k = column of the panel) so that both DMMA fragments
-// read (row = lane/4, k = lane%4) with stride LP == 4 (mod 16).
-__device__ __forceinline__ void load_panel_tile(double* dst, const double* src, int64_t LD) {
-    // src: 64 rows x 64 cols column-major (ld LD); dst[r*LP + c].  16 B chunks along rows need a
-    // transpose, so copy column segments of 2 rows with two 8 B writes instead: use cp.async on
-    // the column-major layout into a [c][r] buffer and read fragments as [k][row] instead.
-    for (int ch = threadIdx.x; ch < NB * NB / 2; ch += 256) {
-        int c = ch / (NB / 2), r = (ch % (NB / 2)) * 2;
-        cpa16(dst + c * LP + r, src + r + (int64_t)c * LD);
-    }
-}
-
-__device__ __forceinline__ void tile_of(int t, int nsub, int& i, int& j) {
-    // column-major lower triangle: column j has nsub - j tiles
-    j = 0;
-    int rem = t;
-    while (rem >= nsub - j) {
-        rem -= nsub - j;
-        ++j;
-    }
-    i = j + rem;
-}
-
-// KP = 1: C_ij -= L_{i,k} L_{j,k}^T for the window at block k+1 (tiles 0 <= j <= i < nsub).
-// KP = 2: two Cholesky steps merged into one rank-128 update of the window at block k+2:
-//         C_ij -= L_{i,k} L_{j,k}^T + L_{i,k+1} L_{j,k+1}^T, where tiles of column k beyond the
-//         band (relative row > nbw-2) are zero and skipped.
-template <int KP>
-__global__ void __launch_bounds__(256, KP == 1 ? 2 : 1) k_syrk_band(double* __restrict__ Mb, int64_t LD, int k, int nsub,
-                                                                    int ntiles, int nbw) {
-    extern __shared__ __align__(16) double ssm[];
-    double* Bs = ssm;                   // KP tiles of column j: Bs[p][c*LP + r] = L_{j,k+p}[r][c]
-    double* As0 = ssm + KP * NB * LP;   // 2 buffers x KP tiles of row i
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
-    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
-    if (t0 >= t1) return;
-    const int64_t k0 = (int64_t)k * NB, w0 = k0 + KP * NB;  // window origin
-    // panel p (column k+p), relative window tile row i -> tile (k+KP+i, k+p); valid iff KP-p+i <= nbw
-    auto panel = [&](int p, int i) -> const double* { return Mb + (w0 + (int64_t)i * NB) + (k0 + (int64_t)p * NB) * LD; };
-    auto valid = [&](int p, int i) { return KP - p + i <= nbw; };
-    int i, j;
-    tile_of(t0, nsub, i, j);
-    int jb = -1;
-#pragma unroll
-    for (int p = 0; p < KP; ++p)
-        if (valid(p, i)) load_panel_tile(As0 + p * NB * LP, panel(p, i), LD);
-    cpa_commit();
-    double cn[4][2][2];
-    auto load_c = [&](int ti, int tj, double (&cr)[4][2][2]) {
-        const double* Ct = Mb + (w0 + (int64_t)ti * NB) + (w0 + (int64_t)tj * NB) * LD;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    int r = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
-                    cr[mt][nt][e] = Ct[r + (int64_t)c * LD];
-                }
-    };
-    load_c(i, j, cn);
-    for (int t = t0; t < t1; ++t) {
-        const int ci = i, cj = j, buf = (t - t0) & 1;
-        if (cj != jb) {
-#pragma unroll
-            for (int p = 0; p < KP; ++p)
-                if (valid(p, cj)) load_panel_tile(Bs + p * NB * LP, panel(p, cj), LD);
-            cpa_commit();
-            jb = cj;
-        }
-        double acc[4][2][2];  // holds -C: the DMMAs add A B^T, the store negates back
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = -cn[mt][nt][0], acc[mt][nt][1] = -cn[mt][nt][1];
-        if (t + 1 < t1) {
-            if (++i == nsub) i = ++j;  // next tile of the column-major lower triangle
-#pragma unroll
-            for (int p = 0; p < KP; ++p)
-                if (valid(p, i)) load_panel_tile(As0 + ((buf ^ 1) * KP + p) * NB * LP, panel(p, i), LD);
-        }
-        cpa_commit();
-        if (t + 1 < t1) load_c(i, j, cn);
-        cpa_wait<1>();
-        __syncthreads();
-#pragma unroll
-        for (int p = 0; p < KP; ++p) {
-            if (!valid(p, ci) || !valid(p, cj)) continue;  // tile outside the band: zero contribution
-            const double* As = As0 + (buf * KP + p) * NB * LP;
-            const double* Bp = Bs + p * NB * LP;
-#pragma unroll 4
-            for (int ks = 0; ks < NB / 4; ++ks) {
-                const int kk = ks * 4 + (lane & 3);
-                double af[4], bf[2];
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = As[kk * LP + wm * 32 + mt * 8 + (lane >> 2)];
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) bf[nt] = Bp[kk * LP + wn * 16 + nt * 8 + (lane >> 2)];
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-            }
-        }
-        double* Ct = Mb + (w0 + (int64_t)ci * NB) + (w0 + (int64_t)cj * NB) * LD;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    int r = wm * 32 + mt * 8 + (lane >> 2), c = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
-                    Ct[r + (int64_t)c * LD] = -acc[mt][nt][e];
-                }
-        __syncthreads();  // buffers of this tile may be overwritten by the next prefetch
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// Band triangular solve as ONE cooperative (co-resident) kernel: block-row i is owned by CTA
-// i mod gridDim.x; each CTA processes its rows in dependency order, streams the band tiles of the
-// row through a 2-stage cp.async ring, waits for the producers of the solved blocks it needs on
-// per-block completion flags (acquire/release, monotonically increasing epoch), subtracts the
-// GEMV contributions, solves with the diagonal tile and publishes its block.
-//   dir 0: L z = rhs  (row i needs z_j, j in [i-nbw, i))
-//   dir 1: L^T u = rhs (row i needs u_j, j in (i, i+nbw]; tiles (j, i) used transposed)
-// ------------------------------------------------------------------------------------------
-constexpr int TP = NB + 1;
-constexpr int TRSV_SMEM = (2 * NB * TP + 4 * NB + 3 * NB) * 8;
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -341,23 +53,424 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Spin until *flag >= epoch; after ~10 s report ELMDDM_ENUMERIC (info = -1 - tag) and give up
+// instead of hanging the device.
+__device__ __forceinline__ void wait_flag(const int* flag, int epoch, ElmStatus* status, int tag) {
+    if (ld_acquire(flag) >= epoch) return;
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire(flag) < epoch) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > 10000000000ull) {
+            elm_set_status(status, ELMDDM_ENUMERIC, -1 - tag);
+            return;
+        }
+    }
+}
 
-__device__ __forceinline__ void load_tile_async(double* dst, const double* src, int64_t LD) {
-    // 64 x 64 column-major tile (ld LD) -> dst[c*TP + r]; 8-byte cp.async (TP is odd)
-    for (int t = threadIdx.x; t < NB * NB; t += blockDim.x) {
-        const int r = t & 63, c = t >> 6;
-        unsigned d = (unsigned)__cvta_generic_to_shared(dst + c * TP + r);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + r + (int64_t)c * LD));
+// ---- mbarrier + bulk copy (TMA, non-tensor) -------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// ------------------------------------------------------------------------------------------
+// the left-looking tile Cholesky
+// ------------------------------------------------------------------------------------------
+namespace llc {
+constexpr int NT = 256;
+constexpr int TILE = ELM_TS;                  // doubles per packed 64-wide tile
+constexpr int HALF = 32 * LP;                 // doubles per 32-column half tile
+constexpr int NSTAGE = 3;                     // stage = (A half, B half) = one tile of smem
+constexpr uint32_t HALF_BYTES = HALF * 8;
+constexpr int SMEM = NSTAGE * TILE * 8 + 5 * NB * 8 + 8 * 8;  // stages, pivot exchange + 1/sqrt(d), mbarriers
+}  // namespace llc
+
+// acc[r][n] += sum_kk A[kk*LP + r] B[kk*LP + n], kk < KW; warp tile 32 x 16 (wm = warp & 1, wn = warp >> 1)
+template <int KW>
+__device__ __forceinline__ void mma_tile(double (&acc)[4][2][2], const double* As, const double* Bs) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp & 1, wn = warp >> 1;
+#pragma unroll 4
+    for (int ks = 0; ks < KW / 4; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double af[4], bf[2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = As[kk * LP + wm * 32 + mt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bf[nt] = Bs[kk * LP + wn * 16 + nt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) dmma_c(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+}
+
+// fragment element (mt, nt, e) of this thread -> tile coordinates (r, c)
+__device__ __forceinline__ int frag_r(int mt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    return (warp & 1) * 32 + mt * 8 + (lane >> 2);
+}
+__device__ __forceinline__ int frag_c(int nt, int e) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    return (warp >> 1) * 16 + nt * 8 + 2 * (lane & 3) + e;
+}
+#define FOR_FRAG                                     \
+    _Pragma("unroll") for (int mt = 0; mt < 4; ++mt) \
+    _Pragma("unroll") for (int nt = 0; nt < 2; ++nt) \
+    _Pragma("unroll") for (int e = 0; e < 2; ++e)
+
+// Cholesky and inverse of one SPD 64 x 64 tile, register resident.  Input A[c * LP + r] (lower
+// part valid); output L (lower, zeros above) into the same buffer and Y = L^{-1} (lower, zeros
+// above) into Y.  Thread (ti, tj) of a 16 x 16 grid holds elements (ti + 16a, tj + 16b) of the
+// combined matrix Z = [Y~(:, 0..c) | A(:, c+1..)].  Step c is the rank-1 update
+//     Z(i, j) -= (A(i,c) / d_c) v_j  for i > c,   v_j = Y~(c, j) (j < c), A(j, c) (j > c),
+// and column c of A retires into L while column c of Y~ starts as e_c - A(:,c)/d_c (right-looking
+// Cholesky fused with the column-oriented inverse).  Row i of Y~ is final after step i and is
+// scaled by 1/sqrt(d_i) at the end (Y = diag(d^{-1/2}) Y~).  The loop is branch-free: rows
+// i <= c get a zero multiplier and the unused upper triangle absorbs harmless updates.  Only the
+// pivot column / row go through shared memory (double-buffered: one barrier per step).
+// Returns the first non-positive pivot (local index) or -1.
+__device__ int potrf_inv_tile(double* A, double* Y, double* xbuf /* [2][2][64] + [64] */) {
+    const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
+    double* rsv = xbuf + 4 * NB;
+    double z[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) z[a][b] = A[(tj + 16 * b) * LP + ti + 16 * a];
+    int bad = -1;
+    __syncthreads();  // every element read before A is overwritten with L
+#pragma unroll 1
+    for (int c = 0; c < NB; ++c) {
+        double* colc = xbuf + (c & 1) * 2 * NB;
+        double* rowc = colc + NB;
+        const int cb = c >> 4, cl = c & 15;
+        if (tj == cl)
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                colc[ti + 16 * a] = cb == 0 ? z[a][0] : cb == 1 ? z[a][1] : cb == 2 ? z[a][2] : z[a][3];
+        if (ti == cl)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                rowc[tj + 16 * b] = cb == 0 ? z[0][b] : cb == 1 ? z[1][b] : cb == 2 ? z[2][b] : z[3][b];
+        __syncthreads();
+        const double d = colc[c];
+        if (!(d > 0.0) && bad < 0) bad = c;
+        const double rs = rsqrt(d > 0.0 ? d : 1e-300);
+        const double inv = rs * rs;
+        if (tid == 0) rsv[c] = rs;
+        if (tj == cl)  // column c of A retires into L
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int i = ti + 16 * a;
+                A[c * LP + i] = i >= c ? colc[i] * rs : 0.0;
+            }
+        double ci[4], vj[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ci[a] = ti + 16 * a > c ? colc[ti + 16 * a] * inv : 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = tj + 16 * b;
+            vj[b] = j < c ? rowc[j] : colc[j];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const double tr = ti + 16 * a == c ? 1.0 : -ci[a];  // new Y~(i, c)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double upd = fma(-ci[a], vj[b], z[a][b]);
+                z[a][b] = tj + 16 * b == c ? tr : upd;
+            }
+        }
+    }
+    __syncthreads();  // rsv complete
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int i = ti + 16 * a;
+        const double ri = rsv[i];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = tj + 16 * b;
+            Y[j * LP + i] = j > i ? 0.0 : z[a][b] * ri;
+        }
+    }
+    __syncthreads();
+    return bad;
+}
+
+// X = C L^{-T} for C in As (layout [c * LP + r]), L = L(J,J) in Bs and Y = L(J,J)^{-1} in Ys:
+// X0 = C Y^T, then one refinement step X = X0 + (C - X0 L^T) Y^T (three 64^3 DMMA products; the
+// inverse alone would lose accuracy on ill-conditioned diagonal blocks).  As is clobbered.
+__device__ __forceinline__ void trsm_refined(double (&x)[4][2][2], double* As, const double* Bs, const double* Ys) {
+    double r[4][2][2];
+    FOR_FRAG x[mt][nt][e] = 0.0;
+    mma_tile<NB>(x, As, Ys);                                    // X0 = C Y^T
+    FOR_FRAG r[mt][nt][e] = -As[frag_c(nt, e) * LP + frag_r(mt)];  // -C
+    __syncthreads();
+    FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = x[mt][nt][e];
+    __syncthreads();
+    mma_tile<NB>(r, As, Bs);                                    // X0 L^T - C = -R
+    __syncthreads();
+    FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -r[mt][nt][e];
+    __syncthreads();
+    mma_tile<NB>(x, As, Ys);                                    // X0 + R Y^T
+}
+
+struct CholArgs {
+    double* Mb;          // packed tiles
+    double* Ybuf;        // [nblk] packed tiles: L(J,J)^{-1}
+    double* Cbuf;        // [nblk] packed tiles: C(I, I-1) before its triangular solve
+    int* cready;         // [nblk] Cbuf[I] published (epoch)
+    const int2* tasks;   // (I, J), column by column
+    int ntasks;
+    const int* first;    // first nonzero tile column of every tile row
+    int* flags;          // [nblk][nbw + 1]: tile (I, J) at I * (nbw + 1) + (I - J)
+    int* colcnt;         // [nblk] finished tiles of column J, summed over factorisations
+    const int* ntc;      // [nblk] tiles of column J
+    int nbw;
+    int epoch;
+    ElmStatus* status;
+};
+
+__global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
+    using namespace llc;
+    extern __shared__ __align__(128) double csm[];
+    double* St = csm;                                      // NSTAGE x (A half | B half)
+    double* rsv = St + NSTAGE * TILE;                      // [2][2][64] + [64]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rsv + 5 * NB);  // [NSTAGE] chunk loads, [NSTAGE] epilogue loads
+    double* As = St;                                       // epilogue: C / X0 / R
+    double* Bs = St + TILE;                                // epilogue: L(J,J)
+    double* Ys = St + 2 * TILE;                            // epilogue: Y_J
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < 2 * NSTAGE; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int stride = a.nbw + 1;
+    auto flag = [&](int I, int J) { return a.flags + (int64_t)I * stride + (I - J); };
+    auto tile = [&](int I, int J) { return a.Mb + tile_off(I, J, a.nbw); };
+    int known = 0;        // (thread 0) every column < known is complete
+    uint32_t gchunk = 0;  // chunk loads issued by this CTA so far (stage = gchunk % NSTAGE)
+    uint32_t epi_uses = 0;
+    // thread 0: make sure L(I, k) and L(J, k) are final (column counters first, tile flags second)
+#ifdef ELM_CHOL_PROF
+    unsigned long long pf_flag = 0, pf_data = 0;
+#endif
+    auto ensure = [&](int I, int J, int k) {
+#ifdef ELM_CHOL_PROF
+        const uint64_t q0 = globaltimer();
+        struct Acc { unsigned long long& r; uint64_t q; __device__ ~Acc() { r += globaltimer() - q; } } acc_{pf_flag, q0};
+#endif
+        if (k < known) return;
+        while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
+        if (k < known) return;
+        wait_flag(flag(I, k), a.epoch, a.status, I);
+        wait_flag(flag(J, k), a.epoch, a.status, J);
+    };
+    for (int t = blockIdx.x; t < a.ntasks; t += gridDim.x) {
+        const int2 ij = a.tasks[t];
+        const int I = ij.x, J = ij.y;
+        const int k0 = max(a.first[I], a.first[J]);
+        // the diagonal task applies the last term k = J-1 itself: it solves for L(J, J-1) from the
+        // published C(J, J-1) (one flag hop less on the critical path)
+        const bool dsub = I == J && J - 1 >= k0;
+        const int nch = 2 * ((dsub ? J - 1 : J) - k0);
+#ifdef ELM_CHOL_PROF
+        const uint64_t pt0 = globaltimer();
+        pf_flag = pf_data = 0;
+#endif
+        const uint32_t g0 = gchunk;
+        // chunk c: columns [32h, 32h + 32) of L(I, k) and L(J, k), k = k0 + c/2, h = c & 1
+        auto issue = [&](int c) {  // thread 0 only
+            const int k = k0 + (c >> 1), h = c & 1;
+            const uint32_t g = g0 + c;
+            double* st = St + (g % NSTAGE) * TILE;
+            uint64_t* b = &bar[g % NSTAGE];
+            fence_proxy_async();
+            mbar_expect(b, 2 * HALF_BYTES);
+            bulk_load(st, tile(I, k) + h * HALF, HALF_BYTES, b);
+            bulk_load(st + HALF, tile(J, k) + h * HALF, HALF_BYTES, b);
+        };
+        double acc[4][2][2];  // holds -C while the updates are added
+        {
+            const double* Ct = tile(I, J);
+            FOR_FRAG acc[mt][nt][e] = -__ldcg(Ct + frag_r(mt) + frag_c(nt, e) * LP);
+        }
+        if (tid == 0)
+            for (int c = 0; c < NSTAGE - 1 && c < nch; ++c) {
+                if ((c & 1) == 0) ensure(I, J, k0 + (c >> 1));
+                issue(c);
+            }
+        for (int c = 0; c < nch; ++c) {
+            if (c > 0) __syncthreads();  // every warp is done with chunk c-1: its stage may be refilled
+            if (tid == 0 && c + NSTAGE - 1 < nch) {
+                const int cn = c + NSTAGE - 1;
+                if ((cn & 1) == 0) ensure(I, J, k0 + (cn >> 1));
+                issue(cn);
+            }
+            const uint32_t g = g0 + c;
+#ifdef ELM_CHOL_PROF
+            const uint64_t pw = globaltimer();
+#endif
+            mbar_wait(&bar[g % NSTAGE], (g / NSTAGE) & 1);
+#ifdef ELM_CHOL_PROF
+            pf_data += globaltimer() - pw;
+#endif
+            const double* st = St + (g % NSTAGE) * TILE;
+            mma_tile<32>(acc, st, st + HALF);
+        }
+        gchunk = g0 + nch;
+        __syncthreads();
+#ifdef ELM_CHOL_PROF
+        const uint64_t pte = globaltimer();
+#endif
+        double* dst = tile(I, J);
+        if (I == J) {
+#ifdef ELM_CHOL_PROF
+            uint64_t dts[8] = {globaltimer(), 0, 0, 0, 0, 0, 0, 0};
+#define DSTAMP(k) dts[k] = globaltimer()
+#else
+#define DSTAMP(k)
+#endif
+            if (dsub) {
+                uint64_t* eb = &bar[NSTAGE + (epi_uses % NSTAGE)];
+                const uint32_t epar = (epi_uses / NSTAGE) & 1;
+                ++epi_uses;
+                if (tid == 0) {
+                    wait_flag(a.cready + J, a.epoch, a.status, J);
+                    wait_flag(flag(J - 1, J - 1), a.epoch, a.status, J - 1);
+                    fence_proxy_async();
+                    mbar_expect(eb, 3 * TILE * 8);
+                    bulk_load(As, a.Cbuf + (int64_t)J * TILE, TILE * 8, eb);
+                    bulk_load(Bs, tile(J - 1, J - 1), TILE * 8, eb);
+                    bulk_load(Ys, a.Ybuf + (int64_t)(J - 1) * TILE, TILE * 8, eb);
+                }
+                DSTAMP(1);
+                mbar_wait(eb, epar);
+                DSTAMP(2);
+                double x[4][2][2];
+                trsm_refined(x, As, Bs, Ys);                      // L(J, J-1)
+                DSTAMP(3);
+                __syncthreads();
+                FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = x[mt][nt][e];
+                __syncthreads();
+                mma_tile<NB>(acc, As, As);                        // -C(J,J) + L(J,J-1) L(J,J-1)^T
+                __syncthreads();
+            }
+            FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
+            __syncthreads();
+            DSTAMP(4);
+            const int bad = potrf_inv_tile(As, Ys, rsv);
+            DSTAMP(5);
+            if (bad >= 0 && tid == 0) elm_set_status(a.status, ELMDDM_ENUMERIC, J * NB + bad);
+            double* yd = a.Ybuf + (int64_t)J * TILE;
+            for (int x = tid; x < TILE / 2; x += NT) {
+                reinterpret_cast<double2*>(dst)[x] = reinterpret_cast<const double2*>(As)[x];
+                reinterpret_cast<double2*>(yd)[x] = reinterpret_cast<const double2*>(Ys)[x];
+            }
+            DSTAMP(6);
+            __threadfence();
+            DSTAMP(7);
+#ifdef ELM_CHOL_PROF
+            if (tid == 0 && J < 4096)
+                for (int q = 0; q < 8; ++q) g_chol_dprof[8 * J + q] = dts[q];
+#endif
+#undef DSTAMP
+        } else {
+            // C -> As[c * LP + r]
+            FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
+            if (I == J + 1) {  // publish C(I, I-1) for the diagonal task of column I
+                double* cb = a.Cbuf + (int64_t)I * TILE;
+                FOR_FRAG cb[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) st_release(a.cready + I, a.epoch);
+            }
+            // L(I,J) solves X L_JJ^T = C
+            uint64_t* eb = &bar[NSTAGE + (epi_uses % NSTAGE)];
+            const uint32_t epar = (epi_uses / NSTAGE) & 1;
+            ++epi_uses;
+            if (tid == 0) {
+#ifdef ELM_CHOL_PROF
+                const uint64_t pw = globaltimer();
+#endif
+                wait_flag(flag(J, J), a.epoch, a.status, J);
+#ifdef ELM_CHOL_PROF
+                pf_flag += globaltimer() - pw;
+#endif
+                fence_proxy_async();
+                mbar_expect(eb, 2 * TILE * 8);
+                bulk_load(Ys, a.Ybuf + (int64_t)J * TILE, TILE * 8, eb);
+                bulk_load(Bs, tile(J, J), TILE * 8, eb);
+            }
+            __syncthreads();  // C visible to every warp
+            mbar_wait(eb, epar);
+            double x0[4][2][2];
+            trsm_refined(x0, As, Bs, Ys);
+            FOR_FRAG dst[frag_r(mt) + frag_c(nt, e) * LP] = x0[mt][nt][e];
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            st_release(flag(I, J), a.epoch);
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.colcnt + J) : "memory");
+#ifdef ELM_CHOL_PROF
+            if (t < 400000) {
+                unsigned long long* r = g_chol_prof + 6 * (size_t)t;
+                r[0] = pt0; r[1] = globaltimer(); r[2] = pf_flag; r[3] = pf_data; r[4] = pte; r[5] = blockIdx.x;
+            }
+#endif
+        }
+    }
+}
+#undef FOR_FRAG
+
+// ------------------------------------------------------------------------------------------
+// Triangular solves as ONE cooperative (co-resident) kernel per direction: block-row i is owned
+// by CTA i mod gridDim.x; each CTA processes its rows in dependency order, streams the tiles of
+// the row through a 2-stage cp.async ring, waits for the producers of the solved blocks it needs
+// on per-block completion flags (acquire/release, monotonically increasing epoch), subtracts the
+// GEMV contributions and solves with the diagonal tile by warp-level substitution.
+//   dir 0: L z = rhs    tiles (i, j), first[i] <= j < i
+//   dir 1: L^T u = rhs  tiles (j, i), i < j <= last[i], used transposed
+// ------------------------------------------------------------------------------------------
+constexpr int TRSV_SMEM = (2 * ELM_TS + 4 * NB + 3 * NB) * 8;
+
+__device__ __forceinline__ void load_tile_async(double* dst, const double* src) {
+    for (int t = threadIdx.x; t < ELM_TS / 2; t += blockDim.x) {
+        unsigned d = su32(dst + 2 * t);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * t));
     }
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int64_t LD, int nblk, int nbw,
+__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int nbw, int nblk,
+                                                   const int* __restrict__ first, const int* __restrict__ last,
                                                    const double* __restrict__ rhs, double* __restrict__ out, int* flags,
                                                    int epoch, int dir, ElmStatus* status) {
     extern __shared__ __align__(16) double tsm[];
-    double* tiles = tsm;                  // [2][64 cols][TP]
-    double* part = tiles + 2 * NB * TP;   // [4][64]
+    double* tiles = tsm;                  // [2][ELM_TS]
+    double* part = tiles + 2 * ELM_TS;    // [4][64]
     double* acc = part + 4 * NB;          // [64]
     double* xs = acc + NB;                // [64]
     double* rdv = xs + NB;                // [64] reciprocal diagonal
@@ -365,90 +478,81 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
     for (int it = blockIdx.x; it < nblk; it += gridDim.x) {
         const int i = dir == 0 ? it : nblk - 1 - it;
         const int64_t i0 = (int64_t)i * NB;
-        // dependency list: forward j = i-nbw .. i-1 (oldest first); backward j = i+nbw .. i+1
-        const int jlo = dir == 0 ? max(0, i - nbw) : i + 1;
-        const int jhi = dir == 0 ? i - 1 : min(nblk - 1, i + nbw);
+        const int jlo = dir == 0 ? first[i] : i + 1;
+        const int jhi = dir == 0 ? i - 1 : last[i];
         const int nj = jhi - jlo + 1;
         auto tile_of = [&](int q) -> const double* {  // q-th dependency tile, then the diagonal
-            if (q == nj) return Mb + i0 + i0 * LD;
+            if (q == nj) return Mb + tile_off(i, i, nbw);
             const int j = dir == 0 ? jlo + q : jhi - q;
-            return dir == 0 ? Mb + i0 + (int64_t)j * NB * LD        // tile (i, j)
-                            : Mb + (int64_t)j * NB + i0 * LD;       // tile (j, i)
+            return dir == 0 ? Mb + tile_off(i, j, nbw) : Mb + tile_off(j, i, nbw);
         };
         if (tid < NB) acc[tid] = rhs[i0 + tid];
-        load_tile_async(tiles, tile_of(0), LD);
+        load_tile_async(tiles, tile_of(0));
         for (int q = 0; q <= nj; ++q) {
             const int st = q & 1;
-            if (q < nj) load_tile_async(tiles + (st ^ 1) * NB * TP, tile_of(q + 1), LD);
+            if (q < nj) load_tile_async(tiles + (st ^ 1) * ELM_TS, tile_of(q + 1));
             else asm volatile("cp.async.commit_group;\n" ::);
             if (q < nj) {
                 const int j = dir == 0 ? jlo + q : jhi - q;
-                if (tid == 0) {
-                    // bounded spin (~1 s): a missing producer reports ELMDDM_ENUMERIC instead of hanging
-                    for (long long spin = 0; ld_acquire(flags + j) < epoch; ++spin) {
-                        __nanosleep(64);
-                        if (spin > (1LL << 24)) {
-                            elm_set_status(status, ELMDDM_ENUMERIC, -1 - j);
-                            break;
-                        }
-                    }
-                }
+                if (tid == 0) wait_flag(flags + j, epoch, status, j);
                 __syncthreads();
                 if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
             }
             asm volatile("cp.async.wait_group 1;\n" ::);
             __syncthreads();
-            const double* T = tiles + st * NB * TP;
+            const double* T = tiles + st * ELM_TS;
             if (q < nj) {
-                // forward: acc[r] -= sum_c T[r][c] xs[c];  backward: acc[c] -= sum_r T[r][c] xs[r]
-                const int o = tid & 63, p = tid >> 6;
                 double s = 0.0;
-                if (dir == 0) {
+                if (dir == 0) {  // s[r] = sum_c T[r][c] x[c]: thread (r, c-group of 16)
+                    const int r = tid & 63, cgp = tid >> 6;
 #pragma unroll 4
-                    for (int c = p * 16; c < p * 16 + 16; ++c) s += T[c * TP + o] * xs[c];
-                } else {
+                    for (int c = cgp * 16; c < cgp * 16 + 16; ++c) s += T[c * LP + r] * xs[c];
+                    part[cgp * NB + r] = s;
+                } else {         // s[c] = sum_r T[r][c] x[r]: thread (c, r = rq + 4 l), shuffle-reduced
+                    const int c = tid >> 2, rq = tid & 3;
 #pragma unroll 4
-                    for (int r = p * 16; r < p * 16 + 16; ++r) s += T[o * TP + r] * xs[r];
+                    for (int l = 0; l < 16; ++l) s += T[c * LP + rq + 4 * l] * xs[rq + 4 * l];
+                    s += __shfl_xor_sync(0xffffffffu, s, 1);
+                    s += __shfl_xor_sync(0xffffffffu, s, 2);
+                    if (rq == 0) part[c] = s;
                 }
-                part[p * NB + o] = s;
                 __syncthreads();
-                if (tid < NB) acc[tid] -= part[tid] + part[NB + tid] + part[2 * NB + tid] + part[3 * NB + tid];
+                if (tid < NB) acc[tid] -= dir == 0 ? part[tid] + part[NB + tid] + part[2 * NB + tid] + part[3 * NB + tid]
+                                                   : part[tid];
             } else {
-              if (tid < NB) rdv[tid] = 1.0 / T[tid * TP + tid];
-              __syncthreads();
-              if (tid < 32) {
-                // diagonal solve with the tile (i, i) (lower): warp-level, reciprocal diagonal
-                const int lane = tid;
-                double z0 = acc[lane], z1 = acc[lane + 32];
-                if (dir == 0) {
-                    for (int cc = 0; cc < NB; ++cc) {
-                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31);
-                        xc = xc * rdv[cc];
-                        if (lane > cc) z0 -= T[cc * TP + lane] * xc;
-                        if (lane + 32 > cc) z1 -= T[cc * TP + lane + 32] * xc;
-                        if (lane == (cc & 31)) {
-                            if (cc < 32) z0 = xc;
-                            else z1 = xc;
+                if (tid < NB) rdv[tid] = 1.0 / T[tid * LP + tid];
+                __syncthreads();
+                if (tid < 32) {
+                    // diagonal solve with the lower tile (i, i): warp-level substitution
+                    const int lane = tid;
+                    double z0 = acc[lane], z1 = acc[lane + 32];
+                    if (dir == 0) {
+                        for (int cc = 0; cc < NB; ++cc) {
+                            double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                            if (lane > cc) z0 -= T[cc * LP + lane] * xc;
+                            if (lane + 32 > cc) z1 -= T[cc * LP + lane + 32] * xc;
+                            if (lane == (cc & 31)) {
+                                if (cc < 32) z0 = xc;
+                                else z1 = xc;
+                            }
+                        }
+                    } else {
+                        for (int cc = NB - 1; cc >= 0; --cc) {
+                            double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                            if (lane < cc) z0 -= T[lane * LP + cc] * xc;
+                            if (lane + 32 < cc) z1 -= T[(lane + 32) * LP + cc] * xc;
+                            if (lane == (cc & 31)) {
+                                if (cc < 32) z0 = xc;
+                                else z1 = xc;
+                            }
                         }
                     }
-                } else {
-                    for (int cc = NB - 1; cc >= 0; --cc) {
-                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31);
-                        xc = xc * rdv[cc];
-                        if (lane < cc) z0 -= T[lane * TP + cc] * xc;
-                        if (lane + 32 < cc) z1 -= T[(lane + 32) * TP + cc] * xc;
-                        if (lane == (cc & 31)) {
-                            if (cc < 32) z0 = xc;
-                            else z1 = xc;
-                        }
-                    }
+                    out[i0 + lane] = z0;
+                    out[i0 + lane + 32] = z1;
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release(flags + i, epoch);
                 }
-                out[i0 + lane] = z0;
-                out[i0 + lane + 32] = z1;
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) st_release(flags + i, epoch);
-              }
             }
             __syncthreads();
         }
@@ -457,85 +561,62 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
 
 }  // namespace
 
+#ifdef ELM_CHOL_PROF
+extern "C" int elmddm_debug_chol_prof(void* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_chol_prof, sizeof(unsigned long long) * 6 * (size_t)n);
+}
+extern "C" int elmddm_debug_chol_dprof(void* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_chol_dprof, sizeof(unsigned long long) * 8 * (size_t)n);
+}
+#endif
+
 cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
                                cudaStream_t st) {
-    const int64_t Gp = c->sz.G_pad, LD = c->sz.band_ld;
+    const int64_t Gp = c->sz.G_pad;
     const int nblk = (int)(Gp / NB);
     const int nbw = (int)c->sz.band_nbw;
-    double* y = work;
-    double* z = y + Gp;
+    double* z = work;
+    double* Ybuf = work + Gp;  // [nblk] packed tiles (Gp is a multiple of 64: 16-byte aligned)
+    double* Cbuf = Ybuf + (int64_t)nblk * ELM_TS;
     cudaError_t e;
-    static bool attr = false;
-    if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM)) !=
+    static int grid_ll = 0, grid_sv = 0;
+    if (!grid_ll) {
+        if ((e = cudaFuncSetAttribute(k_chol_ll, cudaFuncAttributeMaxDynamicSharedMemorySize, llc::SMEM)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_syrk_band<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM)) !=
-                cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_syrk_band<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK2_SMEM)) !=
+            (e = cudaFuncSetAttribute(k_band_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
                 cudaSuccess)
             return e;
-        attr = true;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_ll, llc::NT, llc::SMEM);
+        if (const char* env = getenv("ELMDDM_CHOL_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(env));
+        grid_ll = (per_sm > 0 ? per_sm : 1) * c->nsm;
+        grid_sv = c->nsm;
     }
-    if ((e = cudaMemcpyAsync(y, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-    auto potrf = [&](int k) -> cudaError_t {
-        const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
+    // factorisation: one cooperative launch over the envelope's tile list
+    {
+        CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, reinterpret_cast<const int2*>(c->d_tasks), c->ntasks, c->d_first, c->d_cflags,
+                   c->d_colcnt, c->d_ntc, nbw, ++c->chol_epoch, c->d_status};
+        const int grid = c->ntasks < grid_ll ? c->ntasks : grid_ll;
+        void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
-        k_potrf_trsm<<<1 + nsub, 256, POTRF_SMEM, st>>>(Mband, LD, k, NB, c->d_status);
-        return cudaGetLastError();
-    };
-    auto syrk1 = [&](int k, int ntiles_limit) -> cudaError_t {  // window at k+1, first ntiles tiles
-        const int nsub = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
-        if (nsub <= 0) return cudaSuccess;
-        int ntiles = nsub * (nsub + 1) / 2;
-        if (ntiles_limit >= 0 && ntiles_limit < ntiles) ntiles = ntiles_limit;
-        const int grid = ntiles < 2 * c->nsm ? ntiles : 2 * c->nsm;
-        KTimer kt(c, ELMDDM_K_GEMM_CHOL, st);
-        k_syrk_band<1><<<grid, 256, SYRK_SMEM, st>>>(Mband, LD, k, nsub, ntiles, nbw);
-        return cudaGetLastError();
-    };
-    int k = 0;
-    for (; k + 1 < nblk; k += 2) {
-        // step k, then only column k+1 of its update, step k+1, then one rank-128 update of the rest
-        const int nsub1 = (nblk - 1 - k) < nbw ? (nblk - 1 - k) : nbw;
-        if ((e = potrf(k)) != cudaSuccess) return e;
-        if ((e = syrk1(k, nsub1)) != cudaSuccess) return e;  // the first window column = block column k+1
-        if ((e = potrf(k + 1)) != cudaSuccess) return e;
-        const int nsub2 = (nblk - 2 - k) < nbw ? (nblk - 2 - k) : nbw;
-        if (nsub2 > 0) {
-            const int ntiles = nsub2 * (nsub2 + 1) / 2;
-            const int grid = ntiles < c->nsm ? ntiles : c->nsm;
-            KTimer kt(c, ELMDDM_K_GEMM_CHOL, st);
-            k_syrk_band<2><<<grid, 256, SYRK2_SMEM, st>>>(Mband, LD, k, nsub2, ntiles, nbw);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-    }
-    if (k < nblk) {
-        if ((e = potrf(k)) != cudaSuccess) return e;
-        if ((e = syrk1(k, -1)) != cudaSuccess) return e;
+        if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=
+            cudaSuccess)
+            return e;
     }
     // triangular solves: one cooperative wavefront kernel per direction
     {
-        static int coop_grid = 0;
-        if (!coop_grid) {
-            if ((e = cudaFuncSetAttribute(k_band_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
-                cudaSuccess)
-                return e;
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band_trsv, 256, TRSV_SMEM);
-            coop_grid = (per_sm > 0 ? 1 : 0) * c->nsm;
-            if (coop_grid <= 0) coop_grid = 1;
-        }
-        int grid = nblk < coop_grid ? nblk : coop_grid;
+        int grid = nblk < grid_sv ? nblk : grid_sv;
         int* flags = c->d_flags;
         for (int dir = 0; dir < 2; ++dir) {
             int epoch = ++c->trsv_epoch;
-            const double* rhs = dir == 0 ? y : z;
+            const double* rhs = dir == 0 ? g : z;
             double* out = dir == 0 ? z : uG;
-            int64_t LDv = LD;
-            int nblk_v = nblk, nbw_v = nbw;
+            int nbw_v = nbw, nblk_v = nblk;
+            const int* fp = c->d_first;
+            const int* lp = c->d_last;
             ElmStatus* stp = c->d_status;
-            void* args[] = {(void*)&Mband, (void*)&LDv, (void*)&nblk_v, (void*)&nbw_v, (void*)&rhs, (void*)&out,
-                            (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
+            void* args[] = {(void*)&Mband, (void*)&nbw_v, (void*)&nblk_v, (void*)&fp, (void*)&lp, (void*)&rhs,
+                            (void*)&out, (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
             KTimer kt(c, ELMDDM_K_TRSV, st);
             if ((e = cudaLaunchCooperativeKernel((void*)k_band_trsv, dim3(grid), dim3(256), args, TRSV_SMEM, st)) !=
                 cudaSuccess)

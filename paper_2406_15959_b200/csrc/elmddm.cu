@@ -183,9 +183,42 @@ elmddm_status build_tables(elmddm_ctx* c) {
         LD = c->sz.G_pad;
     }
     c->sz.band_nbw = nbw;
-    c->sz.band_ld = LD;
-    c->sz.band_elems = c->sz.G_pad * LD + (dense ? 0 : 0);
-    if (!dense) c->sz.band_elems = (c->sz.G_pad - 1) + (c->sz.G_pad - 1) * LD + 1;
+    c->sz.band_ld = ELM_TLD;
+    c->sz.band_elems = nblk * (nbw + 1) * (int64_t)ELM_TS;
+
+    // Envelope at tile granularity: face b's rows start at column min{c : (b, c) pair} * q, so
+    // tile row I starts at the minimum over the faces it overlaps.  Cholesky fill stays inside
+    // the envelope, so tile (I, J) of L can be nonzero only for first[I] <= J <= I.
+    std::vector<int> minc(F > 0 ? F : 1, 0);
+    for (int b = 0; b < F; ++b) minc[b] = b;
+    for (auto& kv : pairs) minc[kv.first.first] = std::min(minc[kv.first.first], kv.first.second);
+    c->first_h.assign(nblk, 0);
+    std::vector<int> last(nblk, 0);
+    for (int64_t I = 0; I < nblk; ++I) {
+        int64_t r0 = I * ELM_NB, r1 = std::min<int64_t>(r0 + ELM_NB, G) - 1;
+        int64_t f = I;
+        if (r0 < G)
+            for (int64_t b = r0 / q; b <= r1 / q; ++b) f = std::min<int64_t>(f, (int64_t)minc[b] * q / ELM_NB);
+        c->first_h[I] = (int)f;
+    }
+    std::vector<int> tasks, ntc(nblk, 0);
+    int64_t nupd = 0;
+    for (int64_t J = 0; J < nblk; ++J) {
+        last[J] = (int)J;
+        for (int64_t I = J; I < nblk && I - J <= nbw; ++I) {
+            if (c->first_h[I] > J) continue;
+            tasks.push_back((int)I);
+            tasks.push_back((int)J);
+            last[J] = (int)I;
+            ++ntc[J];
+            nupd += J - std::max(c->first_h[I], c->first_h[J]);
+        }
+    }
+    c->ntasks = (int)(tasks.size() / 2);
+    c->chol_flops = nupd * 2 * (int64_t)ELM_NB * ELM_NB * ELM_NB;
+    c->tasks_h = tasks;
+    c->sz.chol_tasks = c->ntasks;
+    c->sz.chol_flops = c->chol_flops;
 
     c->qrow_ld = q;
     c->qrow_cols = 7 * q + 1;
@@ -199,6 +232,19 @@ elmddm_status build_tables(elmddm_ctx* c) {
     if ((e = upload(&c->d_terms, terms)) != cudaSuccess) return cuda_fail(c, e, "upload");
     if ((e = upload(&c->d_gterm_ptr, gptr)) != cudaSuccess) return cuda_fail(c, e, "upload");
     if ((e = upload(&c->d_gterms, gterms)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_first, c->first_h)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_last, last)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_tasks, tasks)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_ntc, ntc)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = cudaMalloc((void**)&c->d_colcnt, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMemset(c->d_colcnt, 0, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&c->d_cready, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMemset(c->d_cready, 0, sizeof(int) * nblk)) != cudaSuccess)
+        return cuda_fail(c, e, "colcnt");
+    const size_t nflags = (size_t)nblk * (size_t)(nbw + 1);
+    if ((e = cudaMalloc((void**)&c->d_cflags, sizeof(int) * nflags)) != cudaSuccess ||
+        (e = cudaMemset(c->d_cflags, 0, sizeof(int) * nflags)) != cudaSuccess)
+        return cuda_fail(c, e, "flags");
     return ELMDDM_OK;
 }
 
@@ -280,7 +326,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB);
     c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
                                                           (int64_t)c->ga_ld * c->qrow_cols),
-                                      2 * z.G_pad);
+                                      z.G_pad + 2 * (z.G_pad / ELM_NB) * ELM_TS);  // z + packed inverse diagonal tiles + C(I,I-1)
     c->work_back = z.S * z.ld;
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
@@ -314,6 +360,13 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_terms);
     cudaFree(c->d_gterm_ptr);
     cudaFree(c->d_gterms);
+    cudaFree(c->d_first);
+    cudaFree(c->d_last);
+    cudaFree(c->d_tasks);
+    cudaFree(c->d_cflags);
+    cudaFree(c->d_colcnt);
+    cudaFree(c->d_cready);
+    cudaFree(c->d_ntc);
     delete c;
 }
 
@@ -326,9 +379,18 @@ elmddm_status elmddm_sizes(const elmddm_ctx* c, elmddm_sizes_t* out) {
     return ELMDDM_OK;
 }
 
+elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* first, int32_t* tasks) {
+    CHECK_CTX(c);
+    if (!first || !tasks) return ELMDDM_EINVAL;
+    std::copy(c->first_h.begin(), c->first_h.end(), first);
+    std::copy(c->tasks_h.begin(), c->tasks_h.end(), tasks);
+    return ELMDDM_OK;
+}
+
 int64_t elmddm_band_index(const elmddm_ctx* c, int64_t i, int64_t j) {
     if (!c) return -1;
-    return i + j * c->sz.band_ld;
+    if (i < j || i - j > c->sz.halfband || i >= c->sz.G_pad) return -1;
+    return band_off(i, j, c->sz.band_nbw);
 }
 
 elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {

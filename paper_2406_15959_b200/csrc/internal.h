@@ -10,6 +10,18 @@
 
 #define ELM_NB 64      // panel width of the blocked QR, tile of the band Cholesky
 #define ELM_BB 8       // base block width inside a QR panel
+#define ELM_TLD 68     // column stride inside a packed 64 x 64 tile of the Schur matrix (== 4 mod 16)
+#define ELM_TS (ELM_NB * ELM_TLD)  // doubles per packed tile
+
+// Packed envelope storage of the Schur matrix: tile (I, J), 0 <= I - J <= nbw, is
+// stored contiguously at tile_off(I, J) with element (r, c) at r + c * ELM_TLD, so one bulk copy
+// reproduces the conflict-free padded shared-memory layout of the DMMA kernels.
+__host__ __device__ __forceinline__ int64_t tile_off(int64_t I, int64_t J, int64_t nbw) {
+    return (I * (nbw + 1) + (I - J)) * (int64_t)ELM_TS;
+}
+__host__ __device__ __forceinline__ int64_t band_off(int64_t i, int64_t j, int64_t nbw) {
+    return tile_off(i / ELM_NB, j / ELM_NB, nbw) + (i % ELM_NB) + (j % ELM_NB) * (int64_t)ELM_TLD;
+}
 
 // Device status word: [0] error code (ELMDDM_ENUMERIC), [1] info (column / index).
 struct ElmStatus {
@@ -65,6 +77,19 @@ struct elmddm_ctx {
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
     mutable int trsv_epoch = 0;
+    // envelope (skyline) of the Schur matrix at 64-tile granularity and the factorisation task list
+    std::vector<int> first_h;        // [nblk] first structurally nonzero tile column of tile row I
+    int* d_first = nullptr;          // [nblk]
+    int* d_last = nullptr;           // [nblk] last tile row I with first[I] <= J
+    int* d_tasks = nullptr;          // [ntasks][2] (I, J), column by column
+    std::vector<int> tasks_h;
+    int ntasks = 0;
+    int64_t chol_flops = 0;          // envelope Cholesky work: 2 * 64^3 per tile update
+    int* d_cflags = nullptr;         // [nblk][nbw + 1] per-tile completion flags of the factorisation
+    int* d_colcnt = nullptr;         // [nblk] finished tiles of column J (summed over factorisations)
+    int* d_ntc = nullptr;            // [nblk] tiles of column J in the envelope
+    int* d_cready = nullptr;         // [nblk] C(I, I-1) published for the diagonal task of column I
+    mutable int chol_epoch = 0;
     mutable std::vector<cudaStream_t> gstreams;
     mutable cudaEvent_t ev_fork = nullptr;
     mutable std::vector<cudaEvent_t> ev_join;

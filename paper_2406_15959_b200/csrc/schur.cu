@@ -78,13 +78,12 @@ __global__ void k_qrow(const double* __restrict__ Pbuf, int64_t pstride, int64_t
     }
 }
 
-__device__ __forceinline__ int64_t band_idx(int64_t i, int64_t j, int64_t bld) { return i + j * bld; }
 
 // M block (b, c) = sum of terms, written in the band storage (b == c: lower triangle only).
 __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restrict__ pair_bc,
                             const FaceTerm* __restrict__ terms, const double* __restrict__ Sbuf, int64_t sstride,
                             int64_t sld, const double* __restrict__ Ga, int64_t gstride, int64_t gld, int q,
-                            double* __restrict__ Mband, int64_t bld) {
+                            double* __restrict__ Mband, int64_t nbw) {
     const int p = blockIdx.x;
     const int b = pair_bc[2 * p], c = pair_bc[2 * p + 1];
     const int t0 = pair_ptr[p], t1 = pair_ptr[p + 1];
@@ -97,7 +96,7 @@ __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restr
             if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * sld];
             else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * gld];
         }
-        Mband[band_idx((int64_t)b * q + i, (int64_t)c * q + j, bld)] = v;
+        Mband[band_off((int64_t)b * q + i, (int64_t)c * q + j, nbw)] = v;
     }
 }
 
@@ -117,10 +116,10 @@ __global__ void k_gassemble(const int* __restrict__ gptr, const FaceTerm* __rest
     }
 }
 
-__global__ void k_pad(double* Mband, int64_t bld, double* g, int64_t G, int64_t G_pad) {
+__global__ void k_pad(double* Mband, int64_t nbw, double* g, int64_t G, int64_t G_pad) {
     int64_t i = G + blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G_pad) return;
-    Mband[band_idx(i, i, bld)] = 1.0;
+    Mband[band_off(i, i, nbw)] = 1.0;
     g[i] = 0.0;
 }
 
@@ -275,7 +274,7 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
         { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_massemble<<<(unsigned)c->npairs, 256, 0, st>>>(c->d_pair_ptr, c->d_pair_bc, c->d_terms, Sbuf, sstride,
                                                           c->sz.sbuf_ld, Ga, gstride, c->ga_ld, q, Mband,
-                                                          c->sz.band_ld); }
+                                                          c->sz.band_nbw); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_gassemble<<<(unsigned)F, 128, 0, st>>>(c->d_gterm_ptr, c->d_gterms, Sbuf, sstride, c->sz.sbuf_ld, Ga,
@@ -285,7 +284,7 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
     const int64_t npad = c->sz.G_pad - c->sz.G;
     if (npad > 0) {
         KTimer kt(c, ELMDDM_K_IFACE, st);
-        k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->sz.band_ld, g, c->sz.G, c->sz.G_pad);
+        k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->sz.band_nbw, g, c->sz.G, c->sz.G_pad);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -169,6 +169,17 @@ class Context:
                 "count": {k: int(t.count[i]) for i, k in enumerate(_lib.KCLASSES)},
                 "ms": {k: float(t.ms[i]) for i, k in enumerate(_lib.KCLASSES)}}
 
+    def chol_plan(self):
+        """(first[nblk], tasks[chol_tasks][2]) of the envelope factorisation (host arrays)."""
+        import numpy as np
+
+        z = self.sizes
+        first = np.zeros(z["G_pad"] // 64, dtype=np.int32)
+        tasks = np.zeros((z["chol_tasks"], 2), dtype=np.int32)
+        self._check(self.L.elmddm_chol_plan(self.h, first.ctypes.data_as(C.c_void_p), tasks.ctypes.data_as(C.c_void_p)),
+                    "chol_plan")
+        return first, tasks
+
     def band_index(self, i, j):
         return int(self.L.elmddm_band_index(self.h, i, j))
 

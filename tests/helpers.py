@@ -78,16 +78,25 @@ def sbuf_np(ctx, buf, s):
     return buf["Sbuf"].view(z["N"], z["kaug"], z["sbuf_ld"])[s].cpu().numpy().T[: z["kaug"], :]  # (kaug, kaug)
 
 
+def band_offsets(z, i, j):
+    """Offsets of elements (i, j), i >= j, in the packed tile storage of the Schur matrix
+    (include/elmddm.h: tile (I, J) at (I (nbw+1) + I - J) * 64 * band_ld, element (r, c) at r + c band_ld)."""
+    i = np.asarray(i, dtype=np.int64)
+    j = np.asarray(j, dtype=np.int64)
+    nbw, tld = z["band_nbw"], z["band_ld"]
+    I, J = i // 64, j // 64
+    return (I * (nbw + 1) + (I - J)) * 64 * tld + (i % 64) + (j % 64) * tld
+
+
 def band_to_dense(ctx, Mband):
     """Full symmetric G x G matrix from the band storage (host)."""
     z = ctx.sizes
-    G, LD, hb = z["G"], z["band_ld"], z["halfband"]
+    G, hb = z["G"], z["halfband"]
     Mb = Mband.cpu().numpy()
     D = np.zeros((G, G))
     for j in range(G):
         i1 = min(G, j + hb + 1)
-        idx = np.arange(j, i1) + j * LD
-        D[j:i1, j] = Mb[idx]
+        D[j:i1, j] = Mb[band_offsets(z, np.arange(j, i1), j)]
     return np.tril(D) + np.tril(D, -1).T
 
 

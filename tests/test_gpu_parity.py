@@ -349,21 +349,27 @@ def test_interface_points_export():
 
 
 def _band_matvec(ctx, Mband_copy, u):
-    """y = M u for the symmetric band matrix stored lower in the skewed layout (torch, GPU)."""
+    """y = M u for the symmetric matrix stored lower in packed 64 x 64 tiles (torch, GPU)."""
     import torch
 
     z = ctx.sizes
-    G, LD, hb = z["G"], z["band_ld"], z["halfband"]
-    y = torch.zeros(G, dtype=torch.float64, device=u.device)
-    for d in range(0, hb + 1):
-        n = G - d
-        if n <= 0:
-            break
-        diag = torch.as_strided(Mband_copy, (n,), (LD + 1,), d)  # M[j+d, j], j = 0..n-1
-        y[d:] += diag * u[:n]
-        if d > 0:
-            y[:n] += diag * u[d:]
-    return y
+    G, nbw, tld, Gp = z["G"], z["band_nbw"], z["band_ld"], z["G_pad"]
+    nblk = Gp // 64
+    T = Mband_copy[: nblk * (nbw + 1) * 64 * tld].view(nblk, nbw + 1, 64, tld)[..., :64]  # [I][d][c][r]
+    U = torch.zeros(Gp, dtype=torch.float64, device=u.device)
+    U[:G] = u
+    U = U.view(nblk, 64)
+    Y = torch.zeros_like(U)
+    for d in range(0, min(nbw, nblk - 1) + 1):
+        Td = T[d:, d]                           # tiles (I, I - d), I = d .. nblk-1: [I][c][r]
+        if d == 0:
+            Td = torch.tril(Td.transpose(1, 2))  # [I][r][c], lower part only
+            Td = Td + torch.tril(Td, -1).transpose(1, 2)
+            Y += torch.einsum("irc,ic->ir", Td, U)
+        else:
+            Y[d:] += torch.einsum("icr,ic->ir", Td, U[: nblk - d])
+            Y[: nblk - d] += torch.einsum("icr,ir->ic", Td, U[d:])
+    return Y.reshape(-1)[:G]
 
 
 @pytest.mark.parametrize("k", [2, 3])

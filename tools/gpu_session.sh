@@ -1,0 +1,38 @@
+#!/bin/bash
+# One gpurun session: GPU tests, smoke, bench (cfg3), ncu launch list of the same step.
+# usage (from the repo root on the box): bash tools/gpu_session.sh TAG [what...]
+#   what: tests smoke bench launches full:<kernel-regex> bench<k>
+set -u
+TAG=${1:-run}; shift
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > "$OUT/nvsmi.txt" 2>&1
+python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1 || { echo BUILD FAILED; tail -30 "$OUT/build.log"; exit 1; }
+for w in "$@"; do
+  case "$w" in
+    tests)
+      timeout 1500 python -m pytest tests -m gpu -q > "$OUT/tests.log" 2>&1; echo "tests exit $?" | tee -a "$OUT/summary.txt"
+      tail -5 "$OUT/tests.log";;
+    smoke)
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke exit $?" | tee -a "$OUT/summary.txt";;
+    bench)
+      timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench exit $?" | tee -a "$OUT/summary.txt"
+      cat "$OUT/bench.json";;
+    bench[0-9])
+      k=${w#bench}
+      timeout 900 python bench.py --config "$k" --no-cpu-baseline > "$OUT/bench_cfg$k.json" 2> "$OUT/bench_cfg$k.err"; echo "bench cfg$k exit $?" | tee -a "$OUT/summary.txt"
+      cat "$OUT/bench_cfg$k.json";;
+    ref)
+      timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/ref.json" 2> "$OUT/ref.err"; echo "ref exit $?" | tee -a "$OUT/summary.txt";;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+        --log-file "$OUT/launches.csv" python tools/profile_step.py --config 3 --steps 1 > "$OUT/ncu_launches.log" 2>&1
+      echo "launches exit $?" | tee -a "$OUT/summary.txt"
+      python tools/launches.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1; head -25 "$OUT/launches_summary.txt";;
+    full:*)
+      k=${w#full:}
+      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
+        -o "$OUT/full_${k//[^a-zA-Z0-9_]/_}" python tools/profile_step.py --config 3 --steps 1 > "$OUT/ncu_full_${k//[^a-zA-Z0-9_]/_}.log" 2>&1
+      echo "full $k exit $?" | tee -a "$OUT/summary.txt";;
+  esac
+done
