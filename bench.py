@@ -66,6 +66,7 @@ def algorithmic(c: dict, s_range) -> dict:
     bytes_asm = 0.0
     fl_schur = 0.0
     fl_wy = 0.0
+    by_wy = 0.0
     for s in range(*s_range):
         i, j = s % P, s // P
         n_if = (i > 0) + (i < P - 1) + (j > 0) + (j < P - 1)
@@ -80,7 +81,19 @@ def algorithmic(c: dict, s_range) -> dict:
             R, N = m - j0, M + k - j0 - nb
             if N > 0:
                 fl_wy += 4.0 * nb * R * N + 2.0 * nb * nb * N
-    return {"flop_qr": fl_qr, "bytes_assemble": bytes_asm, "flop_schur": fl_schur, "flop_wy": fl_wy}
+                by_wy += 8.0 * (R * nb + 2.0 * R * N)  # V once, C read + written once (algorithmic)
+    return {"flop_qr": fl_qr, "bytes_assemble": bytes_asm, "flop_schur": fl_schur, "flop_wy": fl_wy, "bytes_wy": by_wy}
+
+
+def ncu_traffic(k: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r01_traffic_cfg<k>.json, written by tools/traffic.py from an ncu run of the same
+    workload); None if there is no capture for this workload."""
+    path = os.path.join(ROOT, "profiles", f"r01_traffic_cfg{k}.json")
+    if not os.path.exists(path):
+        return None, None
+    d = json.load(open(path))
+    return d["dram_bytes_per_launch"], d["source"]
 
 
 # ------------------------------------------------------------------------------------------------
@@ -328,9 +341,12 @@ def main():
     lf_ms = phases.get("local_factor", 0.0)
     achieved_lf = work["flop_qr"] / (lf_ms * 1e-3) / 1e12 if lf_ms > 0 else None
     step_kernel_ms = max(sum(kms.values()), 1e-12)
+    traffic, traffic_src = ncu_traffic(args.config)
     roof = {"bound": "tensor", "achieved": achieved_wy, "peak": dmma, "unit": "TFLOP/s",
-            "frac": (achieved_wy / dmma) if achieved_wy and dmma else None, "traffic": None,
-            "kernel": "k_wy_update: fused compact-WY trailing update of the blocked Householder QR (FP64 DMMA)",
+            "frac": (achieved_wy / dmma) if achieved_wy and dmma else None, "traffic": traffic,
+            "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": work["bytes_wy"] / max(kt["count"]["gemm_qr"] / args.steps, 1),
+            "kernel": "k_wy_tma: fused compact-WY trailing update of the blocked Householder QR (FP64 DMMA, TMA-staged)",
             "flop_per_step": work["flop_wy"], "kernel_ms_per_step": wy_ms, "launches_per_step": kt["count"]["gemm_qr"] / args.steps,
             "share_of_step": wy_ms / step_kernel_ms,
             "peak_source": "measured on this GPU in this run: register-resident DMMA.8x8x4 loop (elmddm_dmma_probe)",
@@ -340,6 +356,12 @@ def main():
     roof_qr = {"bound": "tensor", "achieved": achieved_lf, "peak": dmma, "unit": "TFLOP/s",
                "frac": (achieved_lf / dmma) if achieved_lf and dmma else None,
                "what": "whole local_factor phase: Householder flop 2mM^2-2M^3/3+2Mk(2m-M) per subdomain / phase time"}
+    chol_ms = kms.get("chol", 0.0)
+    roof_iface = {"bound": "tensor", "achieved": ctx.sizes["chol_flops"] / (chol_ms * 1e-3) / 1e12 if chol_ms > 0 else None,
+                  "peak": dmma, "unit": "TFLOP/s", "kernel": "k_chol_ll (persistent left-looking envelope Cholesky)",
+                  "flop_per_step": ctx.sizes["chol_flops"], "kernel_ms_per_step": chol_ms,
+                  "what": "2*64^3 per tile update inside the envelope of the interface Schur matrix"}
+    roof_iface["frac"] = roof_iface["achieved"] / dmma if roof_iface["achieved"] and dmma else None
     asm_ms = kms["assemble"]
     roof_asm = {"bound": "hbm", "achieved": work["bytes_assemble"] / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
                 "peak": pk["hbm_gbs"], "unit": "GB/s"}
@@ -359,6 +381,9 @@ def main():
                            "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast"},
                 "time_to_solution_ms": ms_per_step, "rel_l2_vs_exact": err,
                 "roofline": roof, "roofline_local_factor": roof_qr, "roofline_assembly": roof_asm,
+                "roofline_interface": roof_iface,
+                "subdomain_phase_solves_per_s": N / (1e-3 * sum(phases.get(k, 0.0) for k in (
+                    "init_hidden", "assemble", "local_factor", "schur_accumulate", "back_solve"))),
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "launches_per_step": launches / args.steps, "clocks": clocks,
                 "phases_ms": phases, "kernel_class_ms": kms,

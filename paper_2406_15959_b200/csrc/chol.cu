@@ -168,16 +168,20 @@ __device__ int potrf_inv_tile(double* A, double* Y, double* xbuf /* [2][2][64] +
 #pragma unroll
             for (int a = 0; a < 4; ++a)
                 colc[ti + 16 * a] = cb == 0 ? z[a][0] : cb == 1 ? z[a][1] : cb == 2 ? z[a][2] : z[a][3];
-        if (ti == cl)
+        if (ti == cl) {
 #pragma unroll
             for (int b = 0; b < 4; ++b)
                 rowc[tj + 16 * b] = cb == 0 ? z[0][b] : cb == 1 ? z[1][b] : cb == 2 ? z[2][b] : z[3][b];
+            if (tj == cl) {  // the pivot's owner: one rsqrt per step
+                const double d = cb == 0 ? z[0][0] : cb == 1 ? z[1][1] : cb == 2 ? z[2][2] : z[3][3];
+                rsv[c] = rsqrt(d > 0.0 ? d : 1e-300);
+            }
+        }
         __syncthreads();
         const double d = colc[c];
         if (!(d > 0.0) && bad < 0) bad = c;
-        const double rs = rsqrt(d > 0.0 ? d : 1e-300);
+        const double rs = rsv[c];
         const double inv = rs * rs;
-        if (tid == 0) rsv[c] = rs;
         if (tj == cl)  // column c of A retires into L
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
@@ -194,9 +198,10 @@ __device__ int potrf_inv_tile(double* A, double* Y, double* xbuf /* [2][2][64] +
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
+            if (16 * a + 15 < c) continue;  // rows all above the pivot: nothing left to do (uniform)
             const double tr = ti + 16 * a == c ? 1.0 : -ci[a];  // new Y~(i, c)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b <= a; ++b) {  // blocks b > a lie in the (unused) upper triangle
                 const double upd = fma(-ci[a], vj[b], z[a][b]);
                 z[a][b] = tj + 16 * b == c ? tr : upd;
             }

@@ -29,9 +29,15 @@ for w in "$@"; do
         --log-file "$OUT/launches.csv" python tools/profile_step.py --config 3 --steps 1 > "$OUT/ncu_launches.log" 2>&1
       echo "launches exit $?" | tee -a "$OUT/summary.txt"
       python tools/launches.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1; head -25 "$OUT/launches_summary.txt";;
+    traffic)
+      timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+        -k regex:k_wy_tma --csv --log-file "$OUT/traffic.csv" python tools/profile_step.py --config 3 --steps 1 > "$OUT/ncu_traffic.log" 2>&1
+      echo "traffic exit $?" | tee -a "$OUT/summary.txt"
+      python tools/traffic.py "$OUT/traffic.csv" 3 "$OUT/traffic_cfg3.json";;
     full:*)
-      k=${w#full:}
-      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 2 -c 1 \
+      spec=${w#full:}; k=${spec%%:*}; skip=2
+      [ "$spec" != "$k" ] && skip=${spec#*:}
+      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$k" -s $skip -c 1 \
         -o "$OUT/full_${k//[^a-zA-Z0-9_]/_}" python tools/profile_step.py --config 3 --steps 1 > "$OUT/ncu_full_${k//[^a-zA-Z0-9_]/_}.log" 2>&1
       echo "full $k exit $?" | tee -a "$OUT/summary.txt";;
   esac
