@@ -102,7 +102,7 @@ constexpr int TILE = ELM_TS;                  // doubles per packed 64-wide tile
 constexpr int HALF = 32 * LP;                 // doubles per 32-column half tile
 constexpr int NSTAGE = 3;                     // stage = (A half, B half) = one tile of smem
 constexpr uint32_t HALF_BYTES = HALF * 8;
-constexpr int SMEM = NSTAGE * TILE * 8 + 5 * NB * 8 + 8 * 8;  // stages, pivot exchange + 1/sqrt(d), mbarriers
+constexpr int SMEM = NSTAGE * TILE * 8 + 10 * NB * 8 + 8 * 8;  // stages, potrf scratch, mbarriers
 }  // namespace llc
 
 // acc[r][n] += sum_kk A[kk*LP + r] B[kk*LP + n], kk < KW; warp tile 32 x 16 (wm = warp & 1, wn = warp >> 1)
@@ -138,88 +138,128 @@ __device__ __forceinline__ int frag_c(int nt, int e) {
     _Pragma("unroll") for (int nt = 0; nt < 2; ++nt) \
     _Pragma("unroll") for (int e = 0; e < 2; ++e)
 
-// Cholesky and inverse of one SPD 64 x 64 tile, register resident.  Input A[c * LP + r] (lower
-// part valid); output L (lower, zeros above) into the same buffer and Y = L^{-1} (lower, zeros
-// above) into Y.  Thread (ti, tj) of a 16 x 16 grid holds elements (ti + 16a, tj + 16b) of the
-// combined matrix Z = [Y~(:, 0..c) | A(:, c+1..)].  Step c is the rank-1 update
-//     Z(i, j) -= (A(i,c) / d_c) v_j  for i > c,   v_j = Y~(c, j) (j < c), A(j, c) (j > c),
-// and column c of A retires into L while column c of Y~ starts as e_c - A(:,c)/d_c (right-looking
-// Cholesky fused with the column-oriented inverse).  Row i of Y~ is final after step i and is
-// scaled by 1/sqrt(d_i) at the end (Y = diag(d^{-1/2}) Y~).  The loop is branch-free: rows
-// i <= c get a zero multiplier and the unused upper triangle absorbs harmless updates.  Only the
-// pivot column / row go through shared memory (double-buffered: one barrier per step).
-// Returns the first non-positive pivot (local index) or -1.
-__device__ int potrf_inv_tile(double* A, double* Y, double* xbuf /* [2][2][64] + [64] */) {
-    const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
-    double* rsv = xbuf + 4 * NB;
-    double z[4][4];
+// Cholesky and inverse of one SPD 64 x 64 tile.  Input A[c * LP + r] (lower part valid); output
+// L (lower, zeros above) into the same buffer and Y = L^{-1} (lower, zeros above) into Y.
+// Blocked by 8 columns: warp 0 factors the 8-wide panel with shuffles (rows c0 + lane and
+// c0 + 32 + lane in registers), then all warps apply the rank-8 trailing update on the FP64
+// tensor pipe (8 x 8 DMMA tiles, K = 8).  The inverse is blocked the same way: the 8 diagonal
+// 8 x 8 blocks are inverted in parallel (one warp each, 1/l_rr from the panel), then block row
+// i of Y is Y_ij = -Y_ii sum_{k=j}^{i-1} L_ik Y_kj (DMMA), one barrier per block row.
+// xbuf: >= 10 * 64 doubles of scratch ([64] 1/l_rr, pivot flag, [8 warps][64] staging).  Returns the first non-positive pivot (local) or -1.
+__device__ int potrf_inv_tile(double* A, double* Y, double* xbuf) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* rsv = xbuf;              // [64] 1 / l_rr
+    int* badp = reinterpret_cast<int*>(xbuf + NB);
+    if (tid == 0) *badp = -1;
+    // zero Y (the off-diagonal upper blocks stay zero)
+    for (int x = tid; x < NB * NB; x += llc::NT) Y[(x >> 6) * LP + (x & 63)] = 0.0;
+    __syncthreads();
+    for (int p = 0; p < 8; ++p) {
+        const int c0 = 8 * p;
+        if (warp == 0) {
+            const int r0 = c0 + lane, r1 = c0 + 32 + lane;
+            double x0[8], x1[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+            for (int j = 0; j < 8; ++j) {
+                x0[j] = r0 < NB ? A[(c0 + j) * LP + r0] : 0.0;
+                x1[j] = r1 < NB ? A[(c0 + j) * LP + r1] : 0.0;
+            }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) z[a][b] = A[(tj + 16 * b) * LP + ti + 16 * a];
-    int bad = -1;
-    __syncthreads();  // every element read before A is overwritten with L
-#pragma unroll 1
-    for (int c = 0; c < NB; ++c) {
-        double* colc = xbuf + (c & 1) * 2 * NB;
-        double* rowc = colc + NB;
-        const int cb = c >> 4, cl = c & 15;
-        if (tj == cl)
+            for (int k = 0; k < 8; ++k) {
+                const double d = __shfl_sync(0xffffffffu, x0[k], k);
+                if (lane == 0 && !(d > 0.0) && *badp < 0) *badp = c0 + k;
+                const double rs = rsqrt(d > 0.0 ? d : 1e-300);
+                if (lane == 0) rsv[c0 + k] = rs;
+                x0[k] = lane >= k ? x0[k] * rs : 0.0;  // column k of L (rows c0+lane >= c0+k)
+                x1[k] *= rs;
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-                colc[ti + 16 * a] = cb == 0 ? z[a][0] : cb == 1 ? z[a][1] : cb == 2 ? z[a][2] : z[a][3];
-        if (ti == cl) {
+                for (int j = k + 1; j < 8; ++j) {
+                    const double lj = __shfl_sync(0xffffffffu, x0[k], j);  // L(c0+j, c0+k)
+                    if (lane > k) x0[j] = fma(-x0[k], lj, x0[j]);
+                    x1[j] = fma(-x1[k], lj, x1[j]);
+                }
+            }
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                rowc[tj + 16 * b] = cb == 0 ? z[0][b] : cb == 1 ? z[1][b] : cb == 2 ? z[2][b] : z[3][b];
-            if (tj == cl) {  // the pivot's owner: one rsqrt per step
-                const double d = cb == 0 ? z[0][0] : cb == 1 ? z[1][1] : cb == 2 ? z[2][2] : z[3][3];
-                rsv[c] = rsqrt(d > 0.0 ? d : 1e-300);
+            for (int j = 0; j < 8; ++j) {
+                if (r0 < NB) A[(c0 + j) * LP + r0] = x0[j];
+                if (r1 < NB) A[(c0 + j) * LP + r1] = x1[j];
             }
         }
         __syncthreads();
-        const double d = colc[c];
-        if (!(d > 0.0) && bad < 0) bad = c;
-        const double rs = rsv[c];
-        const double inv = rs * rs;
-        if (tj == cl)  // column c of A retires into L
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int i = ti + 16 * a;
-                A[c * LP + i] = i >= c ? colc[i] * rs : 0.0;
+        // rank-8 trailing update of the lower 8 x 8 tiles (I >= J) of rows / columns >= c0 + 8
+        const int nt = 7 - p, ntiles = nt * (nt + 1) / 2;
+        for (int t = warp; t < ntiles; t += llc::NT / 32) {
+            int J = 0, rem = t;
+            while (rem >= nt - J) {
+                rem -= nt - J;
+                ++J;
             }
-        double ci[4], vj[4];
+            const int i0 = c0 + 8 + 8 * (J + rem), j0 = c0 + 8 + 8 * J;
+            const int ri = i0 + (lane >> 2), cj = j0 + 2 * (lane & 3);
+            double e0 = -A[cj * LP + ri], e1 = -A[(cj + 1) * LP + ri];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) ci[a] = ti + 16 * a > c ? colc[ti + 16 * a] * inv : 0.0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int j = tj + 16 * b;
-            vj[b] = j < c ? rowc[j] : colc[j];
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            if (16 * a + 15 < c) continue;  // rows all above the pivot: nothing left to do (uniform)
-            const double tr = ti + 16 * a == c ? 1.0 : -ci[a];  // new Y~(i, c)
-#pragma unroll
-            for (int b = 0; b <= a; ++b) {  // blocks b > a lie in the (unused) upper triangle
-                const double upd = fma(-ci[a], vj[b], z[a][b]);
-                z[a][b] = tj + 16 * b == c ? tr : upd;
+            for (int ks = 0; ks < 2; ++ks) {
+                const int kk = c0 + ks * 4 + (lane & 3);
+                dmma_c(e0, e1, A[kk * LP + i0 + (lane >> 2)], A[kk * LP + j0 + (lane >> 2)]);
             }
+            A[cj * LP + ri] = -e0;
+            A[(cj + 1) * LP + ri] = -e1;
         }
+        __syncthreads();
     }
-    __syncthreads();  // rsv complete
+    // zeros above the diagonal of L
+    for (int x = tid; x < NB * NB; x += llc::NT) {
+        const int r = x & 63, c = x >> 6;
+        if (r < c) A[c * LP + r] = 0.0;
+    }
+    // diagonal blocks of Y: warp w inverts L_ww (lanes 0..7: one column each)
+    if (lane < 8) {
+        const int b0 = 8 * warp, c = lane;
+        double y[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int i = ti + 16 * a;
-        const double ri = rsv[i];
+        for (int r = 0; r < 8; ++r) {
+            double s = r == c ? 1.0 : 0.0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int j = tj + 16 * b;
-            Y[j * LP + i] = j > i ? 0.0 : z[a][b] * ri;
+            for (int l = 0; l < 8; ++l)
+                if (l < r) s = fma(-A[(b0 + l) * LP + b0 + r], y[l], s);
+            y[r] = r >= c ? s * rsv[b0 + r] : 0.0;
         }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Y[(b0 + c) * LP + b0 + r] = y[r];
     }
     __syncthreads();
-    return bad;
+    // off-diagonal blocks, block row by block row: warp j < i computes Y_ij
+    for (int i = 1; i < 8; ++i) {
+        if (warp < i) {
+            const int j = warp;
+            // S = sum_{k=j}^{i-1} L_ik Y_kj   (8 x 8, K = 8 per term)
+            double s0 = 0.0, s1 = 0.0;
+            for (int k = j; k < i; ++k) {
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int kk = ks * 4 + (lane & 3);
+                    dmma_c(s0, s1, A[(8 * k + kk) * LP + 8 * i + (lane >> 2)], Y[(8 * j + (lane >> 2)) * LP + 8 * k + kk]);
+                }
+            }
+            // stage S (C fragment: row lane>>2, cols 2(lane&3)+e) as the B operand of Y_ii S
+            double* sw = xbuf + 2 * NB + warp * 64;  // per-warp 8 x 8, [col * 8 + row]
+            sw[(2 * (lane & 3)) * 8 + (lane >> 2)] = s0;
+            sw[(2 * (lane & 3) + 1) * 8 + (lane >> 2)] = s1;
+            __syncwarp();
+            double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                dmma_c(y0, y1, Y[(8 * i + kk) * LP + 8 * i + (lane >> 2)], sw[(lane >> 2) * 8 + kk]);
+            }
+            const int ri = 8 * i + (lane >> 2), cj = 8 * j + 2 * (lane & 3);
+            Y[cj * LP + ri] = -y0;
+            Y[(cj + 1) * LP + ri] = -y1;
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    return *badp;
 }
 
 // X = C L^{-T} for C in As (layout [c * LP + r]), L = L(J,J) in Bs and Y = L(J,J)^{-1} in Ys:
@@ -245,8 +285,10 @@ struct CholArgs {
     double* Ybuf;        // [nblk] packed tiles: L(J,J)^{-1}
     double* Cbuf;        // [nblk] packed tiles: C(I, I-1) before its triangular solve
     int* cready;         // [nblk] Cbuf[I] published (epoch)
-    const int2* tasks;   // (I, J), column by column
+    const int2* tasks;   // (I, J): [0, ncrit) critical chain, then the other tiles; column by column
     int ntasks;
+    int ncrit;           // tasks of the critical chain (diagonal and sub-diagonal tiles)
+    int crit_ctas;       // CTAs [0, crit_ctas) work the critical list, the rest the others
     const int* first;    // first nonzero tile column of every tile row
     int* flags;          // [nblk][nbw + 1]: tile (I, J) at I * (nbw + 1) + (I - J)
     int* colcnt;         // [nblk] finished tiles of column J, summed over factorisations
@@ -260,8 +302,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
     using namespace llc;
     extern __shared__ __align__(128) double csm[];
     double* St = csm;                                      // NSTAGE x (A half | B half)
-    double* rsv = St + NSTAGE * TILE;                      // [2][2][64] + [64]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(rsv + 5 * NB);  // [NSTAGE] chunk loads, [NSTAGE] epilogue loads
+    double* rsv = St + NSTAGE * TILE;                      // [10 * 64] potrf scratch
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rsv + 10 * NB);  // [NSTAGE] chunk loads, [NSTAGE] epilogue loads
     double* As = St;                                       // epilogue: C / X0 / R
     double* Bs = St + TILE;                                // epilogue: L(J,J)
     double* Ys = St + 2 * TILE;                            // epilogue: Y_J
@@ -292,7 +334,11 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         wait_flag(flag(I, k), a.epoch, a.status, I);
         wait_flag(flag(J, k), a.epoch, a.status, J);
     };
-    for (int t = blockIdx.x; t < a.ntasks; t += gridDim.x) {
+    const bool critw = (int)blockIdx.x < a.crit_ctas;
+    const int t_begin = critw ? (int)blockIdx.x : a.ncrit + (int)blockIdx.x - a.crit_ctas;
+    const int t_end = critw ? a.ncrit : a.ntasks;
+    const int t_step = critw ? a.crit_ctas : (int)gridDim.x - a.crit_ctas;
+    for (int t = t_begin; t < t_end; t += t_step) {
         const int2 ij = a.tasks[t];
         const int I = ij.x, J = ij.y;
         const int k0 = max(a.first[I], a.first[J]);
@@ -599,9 +645,12 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     }
     // factorisation: one cooperative launch over the envelope's tile list
     {
-        CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, reinterpret_cast<const int2*>(c->d_tasks), c->ntasks, c->d_first, c->d_cflags,
-                   c->d_colcnt, c->d_ntc, nbw, ++c->chol_epoch, c->d_status};
-        const int grid = c->ntasks < grid_ll ? c->ntasks : grid_ll;
+        int grid = grid_ll;
+        int crit = 32;
+        if (const char* env = getenv("ELMDDM_CHOL_CRIT")) crit = atoi(env);
+        crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
+        CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, reinterpret_cast<const int2*>(c->d_tasks), c->ntasks, c->ncrit, crit,
+                   c->d_first, c->d_cflags, c->d_colcnt, c->d_ntc, nbw, ++c->chol_epoch, c->d_status};
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
         if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=

@@ -201,19 +201,26 @@ elmddm_status build_tables(elmddm_ctx* c) {
             for (int64_t b = r0 / q; b <= r1 / q; ++b) f = std::min<int64_t>(f, (int64_t)minc[b] * q / ELM_NB);
         c->first_h[I] = (int)f;
     }
-    std::vector<int> tasks, ntc(nblk, 0);
+    // task lists: the critical chain (diagonal tile and sub-diagonal tile of every column) and
+    // the ordinary tiles, each column by column; the kernel gives the critical list to a few
+    // dedicated CTAs so that those accumulations run ahead as soon as their inputs exist
+    std::vector<int> crit, reg, ntc(nblk, 0);
     int64_t nupd = 0;
     for (int64_t J = 0; J < nblk; ++J) {
         last[J] = (int)J;
         for (int64_t I = J; I < nblk && I - J <= nbw; ++I) {
             if (c->first_h[I] > J) continue;
-            tasks.push_back((int)I);
-            tasks.push_back((int)J);
+            std::vector<int>& lst = (I - J <= c->crit_band) ? crit : reg;
+            lst.push_back((int)I);
+            lst.push_back((int)J);
             last[J] = (int)I;
             ++ntc[J];
             nupd += J - std::max(c->first_h[I], c->first_h[J]);
         }
     }
+    std::vector<int> tasks(crit);
+    tasks.insert(tasks.end(), reg.begin(), reg.end());
+    c->ncrit = (int)(crit.size() / 2);
     c->ntasks = (int)(tasks.size() / 2);
     c->chol_flops = nupd * 2 * (int64_t)ELM_NB * ELM_NB * ELM_NB;
     c->tasks_h = tasks;
@@ -301,6 +308,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
         c->qr_groups = g < 1 ? 1 : g;
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_CHOL_CRITBAND")) c->crit_band = std::max(1, atoi(env));
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));

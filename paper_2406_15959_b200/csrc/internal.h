@@ -84,6 +84,8 @@ struct elmddm_ctx {
     int* d_tasks = nullptr;          // [ntasks][2] (I, J), column by column
     std::vector<int> tasks_h;
     int ntasks = 0;
+    int ncrit = 0;                   // the first ncrit tasks are the critical band (I - J <= crit_band)
+    int crit_band = 3;               // ELMDDM_CHOL_CRITBAND
     int64_t chol_flops = 0;          // envelope Cholesky work: 2 * 64^3 per tile update
     int* d_cflags = nullptr;         // [nblk][nbw + 1] per-tile completion flags of the factorisation
     int* d_colcnt = nullptr;         // [nblk] finished tiles of column J (summed over factorisations)

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256, 2) k_hog(double* out, int* flag) {
 int main() {
     double* out; int* flag;
     cudaMalloc(&out, 4096 * 8); cudaMalloc(&flag, 4);
-    int smem = (2 * ELM_TS + 5 * 64) * 8;
+    int smem = (2 * ELM_TS + 10 * 64) * 8;
     cudaFuncSetAttribute(k_potrf_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     int reps = 50;
