@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "tma.cuh"
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
@@ -585,53 +586,12 @@ __global__ void __launch_bounds__(wy::NT, 2) k_wy_update(const double* __restric
 // ------------------------------------------------------------------------------------------
 namespace wyt {
 constexpr int NT = 256, CH = 32, PADZ = 64 + 4;
-constexpr int BOX = 16 * 64;              // doubles per TMA box
+using elmtma::BOX;
 constexpr int STAGE = 4 * BOX;            // V (2 boxes) + C (2 boxes)
 constexpr int SMEM = (2 * STAGE + 64 * PADZ) * 8 + 64 + 1024;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-// element (row 0..31, col 0..63) of a 32-row chunk stored as two 128B-swizzled boxes
-#ifdef ELM_SWZ128
-// CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk index (bits 4-6) ^= 128-byte row index (bits 7-9)
-__device__ __forceinline__ int sw(int row, int col) {
-    const int r = row & 15;
-    return (row >> 4) * BOX + col * 16 + ((((r >> 1) ^ (col & 7))) << 1) + (r & 1);
-}
-#define ELM_SWIZZLE CU_TENSOR_MAP_SWIZZLE_128B
-#else
-// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (both DMMA fragment orientations conflict-free): 32-byte chunk index (bits 5-6) ^= bits 7-8
-__device__ __forceinline__ int sw(int row, int col) {
-    const int r = row & 15;
-    return (row >> 4) * BOX + col * 16 + ((((r >> 2) ^ (col & 3))) << 2) + (r & 3);
-}
+using namespace elmtma;
 #define ELM_SWIZZLE CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-#endif
-__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load(double* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-        ::"r"(su32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)) : "memory");
-}
-__device__ __forceinline__ void tma_store(const CUtensorMap* tm, int c0, int c1, int c2, const double* src) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
-                 ::"l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(src)) : "memory");
-}
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
-}
 }  // namespace wyt
 
 __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ CUtensorMap tmV,
@@ -811,10 +771,11 @@ size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * (R + 4) + 8 * 56 * 2 + 
 
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+}  // namespace
 
 // 3-D fp64 tensor map {d0 rows (contiguous), d1 columns (stride d0*8 B), d2 batches (stride s2 elems)},
 // box 16 x 64 x 1, 128B swizzle, out-of-bounds elements read as zero.
-bool encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s2) {
+bool elm_encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s2) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -832,7 +793,6 @@ bool encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, in
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
-}  // namespace
 
 cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, double* work, cudaStream_t st) {
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols;
@@ -849,9 +809,9 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     // TMA descriptors: K_aug {ld, ncols, S} and V {ld, nb, S} (columns >= nb read as zero), boxes 16 x 64
     CUtensorMap tmK, tmV64, tmVlast;
     const int nb_last = M % ELM_NB == 0 ? ELM_NB : M % ELM_NB;
-    bool use_tma = c->use_tma && encode_tmap(&tmK, Kaug, ld, ncols, S, ld * ncols) &&
-                   encode_tmap(&tmV64, Vbuf, ld, ELM_NB, S, ELM_NB * ld) &&
-                   encode_tmap(&tmVlast, Vbuf, ld, nb_last, S, ELM_NB * ld);
+    bool use_tma = c->use_tma && elm_encode_tmap(&tmK, Kaug, ld, ncols, S, ld * ncols) &&
+                   elm_encode_tmap(&tmV64, Vbuf, ld, ELM_NB, S, ELM_NB * ld) &&
+                   elm_encode_tmap(&tmVlast, Vbuf, ld, nb_last, S, ELM_NB * ld);
     // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
     // subdomains are independent).

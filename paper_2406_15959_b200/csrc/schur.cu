@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "tma.cuh"
 
 namespace {
 
@@ -213,6 +214,142 @@ __global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug
     }
 }
 
+// ---- fused left-looking TRSM: W_s^T = R11^{-T} (A^s)^T, in place on At ---------------------------
+// grid (ceil(4q/64), S), 256 threads.  CTA (cb, s) owns flux rows [64cb, 64cb+64) of At[s] and
+// walks the 64-row neuron blocks i in order:
+//     C_i = At_i - sum_{k<i} R_ki^T X_k        (DMMA; R_ki and X_k staged by TMA in 32-row chunks,
+//                                               2-stage mbarrier pipeline; X_k = this CTA's
+//                                               earlier output, L2-resident)
+//     X_i = R_ii^{-T} C_i                       (forward substitution in shared memory: backward
+//                                               stable, R11 is numerically rank deficient)
+// Every output element is written once (the former 25 launches of rank-64 GEMM updates re-read
+// and re-wrote At each step).
+namespace trw {
+using namespace elmtma;
+constexpr int NT = 256;
+constexpr int STAGE = 4 * BOX;           // R chunk (2 boxes) + X chunk (2 boxes)
+constexpr int XP = 65;                   // padded stride of the diagonal-solve tiles
+constexpr int SMEM_BODY = (2 * STAGE > 2 * 64 * XP + 64 ? 2 * STAGE : 2 * 64 * XP + 64);
+constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;
+}  // namespace trw
+
+__global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ CUtensorMap tmR,
+                                                       const __grid_constant__ CUtensorMap tmA,
+                                                       const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
+                                                       double* __restrict__ At, int M, int nat) {
+    using namespace trw;
+    extern __shared__ uint8_t raw[];
+    double* base = reinterpret_cast<double*>(raw + ((1024u - (su32(raw) & 1023u)) & 1023u));
+    double* stg = base;                                   // 2 stages x (R 2 boxes | X 2 boxes)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + SMEM_BODY);
+    double* Cs = base;                                    // diagonal solve: C_i [c * XP + n]
+    double* Rs = base + 64 * XP;                          // R_ii [r * XP + c]
+    double* rinv = Rs + 64 * XP;                          // [64]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int s = blockIdx.y, n0 = blockIdx.x * 64;
+    const double* R = Kaug + (int64_t)s * ld * ncols;
+    double* A = At + (int64_t)s * M * nat;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t gch = 0;  // chunks issued so far (stage = gch & 1, parity = (gch >> 1) & 1)
+    const int nbk = (M + 63) / 64;
+    for (int i = 0; i < nbk; ++i) {
+        const int i0 = 64 * i, bi = min(64, M - i0);
+        double acc[4][2][2];  // -C while the updates are added
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    acc[mt][nt][e] = (c < bi && n0 + n < nat) ? -A[(int64_t)(n0 + n) * M + i0 + c] : 0.0;
+                }
+        const int nch = 2 * i;  // k-blocks 0..i-1, two 32-row chunks each
+        auto issue = [&](int ch, uint32_t g) {
+            double* d = stg + (g & 1) * STAGE;
+            const int r0 = 32 * ch;  // row of R11 / neuron index of X
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_expect(&bar[g & 1], 4 * BOX * 8);
+            tma_load(d, &tmR, r0, i0, s, &bar[g & 1]);
+            tma_load(d + BOX, &tmR, r0 + 16, i0, s, &bar[g & 1]);
+            tma_load(d + 2 * BOX, &tmA, r0, n0, s, &bar[g & 1]);
+            tma_load(d + 3 * BOX, &tmA, r0 + 16, n0, s, &bar[g & 1]);
+        };
+        if (tid == 0 && nch > 0) issue(0, gch);
+        for (int ch = 0; ch < nch; ++ch) {
+            const uint32_t g = gch + ch;
+            if (tid == 0 && ch + 1 < nch) issue(ch + 1, g + 1);
+            mbar_wait(&bar[g & 1], (g >> 1) & 1);
+            const double* Vs = stg + (g & 1) * STAGE;
+            const double* Xs = Vs + 2 * BOX;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                double af[4], bf[2];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Vs[sw(kk, wm * 32 + mt * 8 + (lane >> 2))];
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) bf[nt] = Xs[sw(kk, wn * 16 + nt * 8 + (lane >> 2))];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+            }
+            __syncthreads();  // stage (g & 1) is refilled by the issue of the next iteration
+        }
+        gch += nch;
+        // diagonal block: R_ii^T X = C
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    Cs[c * XP + n] = -acc[mt][nt][e];
+                }
+        for (int x = tid; x < 64 * 64; x += NT) {
+            const int r = x & 63, c = x >> 6;
+            Rs[r * XP + c] = (r <= c && c < bi) ? R[(int64_t)(i0 + c) * ld + i0 + r] : 0.0;
+        }
+        __syncthreads();
+        if (tid < bi) rinv[tid] = 1.0 / Rs[tid * XP + tid];
+        __syncthreads();
+        {
+            // thread (n = tid >> 2, q = tid & 3) owns rows c = q + 4j of column n
+            const int n = tid >> 2, q = tid & 3;
+            double xv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xv[j] = Cs[(q + 4 * j) * XP + n];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+#pragma unroll
+                for (int q0 = 0; q0 < 4; ++q0) {
+                    const int c = 4 * m + q0;
+                    if (q == q0) xv[m] *= rinv[c < bi ? c : 0];
+                    const double xc = __shfl_sync(0xffffffffu, xv[m], (lane & ~3) | q0);
+#pragma unroll
+                    for (int j = m; j < 16; ++j)
+                        if (j > m || q > q0) xv[j] = fma(-Rs[c * XP + q + 4 * j], xc, xv[j]);
+                }
+            }
+            if (n0 + n < nat)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (q + 4 * j < bi) A[(int64_t)(n0 + n) * M + i0 + q + 4 * j] = xv[j];
+        }
+        // X_i is read back through the async proxy (TMA) by the later blocks of this CTA
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
@@ -221,22 +358,21 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols, kaug = c->sz.kaug;
     const int M = c->cfg.M, q = c->cfg.q, nat = 4 * q;
     cudaError_t e;
-    // W_s^T = R11^{-T} A^T  (blocked forward substitution on At, in place)
-    for (int i0 = 0; i0 < M; i0 += 64) {
-        const int bi = (M - i0) < 64 ? (M - i0) : 64;
+    // W_s^T = R11^{-T} A^T: one fused left-looking TRSM launch (in place on At)
+    {
+        CUtensorMap tmR, tmA;
+        if (!elm_encode_tmap(&tmR, Kaug, ld, ncols, S, ld * ncols) || !elm_encode_tmap(&tmA, At, M, nat, S, (int64_t)M * nat))
+            return cudaErrorInvalidValue;
+        static bool attr = false;
+        if (!attr) {
+            if ((e = cudaFuncSetAttribute(k_trsm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, trw::SMEM)) != cudaSuccess)
+                return e;
+            attr = true;
+        }
         dim3 g((nat + 63) / 64, (unsigned)S);
-        {
-            KTimer kt(c, ELMDDM_K_TRSM, st);
-            k_trsm_lt_diag<<<g, 64, 0, st>>>(Kaug, ld, ncols, At, M, nat, i0, bi);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-        const int rest = M - (i0 + bi);
-        if (rest > 0) {
-            // At[i0+bi:, :] -= R[i0:i0+bi, i0+bi:]^T X_i
-            GemmArgs ga{rest, nat, bi, Kaug + i0 + (int64_t)(i0 + bi) * ld, ld, ld * ncols, At + i0, M,
-                        (int64_t)M * nat, At + i0 + bi, M, (int64_t)M * nat, -1.0, 1.0, (int)S, 0};
-            if ((e = gemm_launch(true, false, ga, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
-        }
+        KTimer kt(c, ELMDDM_K_TRSM, st);
+        k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const int64_t s0 = c->cfg.s_begin;
     const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
