@@ -155,26 +155,6 @@ __device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
     }
 }
 
-// tanh and its derivatives sigma' = 1 - sigma^2 written as 4E/(1+E)^2 (no cancellation),
-// sigma'' = -2 sigma sigma', from E = exp(2z) with |z| bounded (clamped at 40: tanh == +-1).
-__device__ __forceinline__ void tanh_derivs(double z, double& s0, double& s1, double& s2) {
-    double za = fmin(fabs(z), 40.0);
-    double E = exp(-2.0 * za);             // in (0, 1]
-    double d;
-    {
-        double r;
-        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(1.0 + E));
-        double e = fma(-(1.0 + E), r, 1.0);
-        r = fma(r, e, r);
-        e = fma(-(1.0 + E), r, 1.0);
-        d = fma(r, e, r);
-    }
-    double t = (1.0 - E) * d;               // tanh |z|
-    s0 = copysign(t, z);
-    s1 = 4.0 * E * d * d;                   // sech^2
-    s2 = -2.0 * s0 * s1;
-}
-
 constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
 constexpr int AS_NT = 256;
 
@@ -196,7 +176,7 @@ __device__ __forceinline__ double fast_rcp(double x) {
 // |z| <= |w|_1 (h/2 + r) stays O(10) for the paper's initialisation, so E never overflows.
 __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
                                                     const double* __restrict__ W, const double* __restrict__ b,
-                                                    double* __restrict__ Kaug) {
+                                                    double* __restrict__ Kaug, double* __restrict__ At) {
     const int M = cfg.M, q = cfg.q, P = cfg.P, p = cfg.p, pp = p * p;
     const int m = pp + 4 * q;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
@@ -224,13 +204,45 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
             else arg = 2.0 * wy * (coord - cy);
             tab[t] = exp(arg);
         }
+        __shared__ double wxs[AS_COLS], wys[AS_COLS];
         if (threadIdx.x < AS_COLS) {
             const int col = min(c0 + threadIdx.x, M - 1);
             const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
             w2s[threadIdx.x] = 2.0 * (wx * wx + wy * wy);
+            wxs[threadIdx.x] = wx;
+            wys[threadIdx.x] = wy;
         }
         __syncthreads();
         const int ncc = min(AS_COLS, M - c0);
+        // flux rows (A^s)^T for the same neurons: At[s][e*q + k][c0 .. c0+8), sigma' = 4 E d^2 at the
+        // edge point from the same tables, times w . n_e (outward axis normal); 16-byte stores
+        // of neuron pairs.  Dirichlet edges are zero.
+        {
+            double* Arow = At + (int64_t)sl * 4 * q * M;
+            for (int t = threadIdx.x; t < 4 * q * (AS_COLS / 2); t += AS_NT) {
+                const int row = t / (AS_COLS / 2), pr = (t % (AS_COLS / 2)) * 2;
+                const int e = row / q, k = row % q;
+                const bool iface = edge_is_interface(P, i, j, e);
+                const int xi = e == 0 ? p : (e == 1 ? p + 1 : p + 2 + k);
+                const int yi = e == 2 ? p : (e == 3 ? p + 1 : p + 2 + k);
+                double v[2] = {0.0, 0.0};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = pr + h;
+                    if (iface && cc < ncc) {
+                        const double* tx = tab + cc * 2 * ntab;
+                        const double E = tx[xi] * tx[ntab + yi];
+                        const double d = fast_rcp(1.0 + E);
+                        const double wn = e == 0 ? -wxs[cc] : (e == 1 ? wxs[cc] : (e == 2 ? -wys[cc] : wys[cc]));
+                        v[h] = wn * (4.0 * E * d * d);
+                    }
+                }
+                if (pr + 1 < ncc)
+                    *reinterpret_cast<double2*>(Arow + (int64_t)row * M + c0 + pr) = make_double2(v[0], v[1]);
+                else if (pr < ncc)
+                    Arow[(int64_t)row * M + c0 + pr] = v[0];
+            }
+        }
         // two consecutive rows per thread -> 16-byte stores
         for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
             int xi[2], yi[2], kind[2];
@@ -300,35 +312,6 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
     }
 }
 
-// At[s][t][j] (t = e*q + k flux row, j neuron fastest): grid (4, S), threads over j.
-__global__ void __launch_bounds__(AS_NT) k_assemble_at(elmddm_config cfg, const double* __restrict__ W,
-                                                       const double* __restrict__ b, double* __restrict__ At) {
-    const int M = cfg.M, q = cfg.q, P = cfg.P, pp = cfg.p * cfg.p;
-    const int e = blockIdx.x, sl = blockIdx.y, s = cfg.s_begin + sl;
-    const int i = s % P, j = s / P;
-    const bool iface = edge_is_interface(P, i, j, e);
-    const double nx = e == 0 ? -1.0 : (e == 1 ? 1.0 : 0.0);
-    const double ny = e == 2 ? -1.0 : (e == 3 ? 1.0 : 0.0);
-    double* A = At + (int64_t)sl * M * 4 * q;
-    for (int k = 0; k < q; ++k) {
-        double x, y;
-        int kind, kk;
-        row_point(cfg, i, j, pp + e * q + k, x, y, kind, kk);
-        double* Arow = A + (int64_t)(e * q + k) * M;
-        for (int n = threadIdx.x; n < M; n += AS_NT) {
-            double v = 0.0;
-            if (iface) {
-                double wx = W[((int64_t)sl * M + n) * 2], wy = W[((int64_t)sl * M + n) * 2 + 1];
-                double z = wx * x + wy * y + b[(int64_t)sl * M + n];
-                double s0, s1, s2;
-                tanh_derivs(z, s0, s1, s2);
-                v = (wx * nx + wy * ny) * s1;
-            }
-            Arow[n] = v;
-        }
-    }
-}
-
 __global__ void k_evaluate(elmddm_config cfg, const double* __restrict__ W, const double* __restrict__ b,
                            const double* __restrict__ coef, const double* __restrict__ xy, int64_t n,
                            double* __restrict__ u) {
@@ -365,12 +348,7 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
     dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
     const size_t tab_bytes = sizeof(double) * AS_COLS * 2 * (c->cfg.p + c->cfg.q + 2);
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
-    k_assemble<<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug); }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    dim3 g2(4, (unsigned)c->sz.S);
-    KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
-    k_assemble_at<<<g2, AS_NT, 0, st>>>(c->cfg, W, b, At);
+    k_assemble<<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At); }
     return cudaGetLastError();
 }
 

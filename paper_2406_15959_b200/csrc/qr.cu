@@ -65,43 +65,54 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-constexpr int RCH = 32;                 // rows per staged chunk of V_prev
-constexpr int RCP = RCH + 4;            // chunk column stride (== 4 mod 16)
-constexpr int RED_ELEMS = 2 * 56 * RCP; // 2-stage ring of V_prev chunks (also T staging / reduction scratch)
+constexpr int RED_ELEMS = 2 * 56 * 36; // 2-stage ring of V_prev chunks (also T staging / reduction scratch)
+constexpr int RSTAGE = RED_ELEMS / 2;   // doubles per ring stage
 
-// stage rows [c*RCH, c*RCH+RCH) of V_prev columns [0, kp) into dst[col*RCP + row] (16 B cp.async)
-__device__ __forceinline__ void vp_chunk(double* dst, const double* __restrict__ Vp, int64_t ld, int kp, int c) {
-    const int n = kp * (RCH / 2);
+// rows per staged chunk of V_prev for kp columns: as many 32-row groups as fit in one ring stage
+// with the padded stride rch + 4 (== 4 mod 16: conflict-free fragments), at most 224.  Small kp
+// (the first base blocks of a panel) thus stream in a few large chunks instead of R/32 small ones
+// (each chunk costs about one L2 round trip).
+__device__ __forceinline__ int vp_rows(int kp) {
+    const int r = ((RSTAGE / kp - 4) / 32) * 32;
+    return r < 32 ? 32 : (r > 224 ? 224 : r);
+}
+
+// stage rows [c*rch, c*rch + nr) of V_prev columns [0, kp) into dst[col*(rch+4) + row] (16 B cp.async)
+__device__ __forceinline__ void vp_chunk(double* dst, const double* __restrict__ Vp, int64_t ld, int kp, int rch,
+                                         int c, int nr) {
+    const int rcp = rch + 4, n = kp * (nr / 2);
     for (int t = threadIdx.x; t < n; t += PNT) {
-        const int col = t / (RCH / 2), r = (t % (RCH / 2)) * 2;
-        unsigned d = (unsigned)__cvta_generic_to_shared(dst + col * RCP + r);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Vp + (int64_t)col * ld + c * RCH + r));
+        const int col = t / (nr / 2), r = (t % (nr / 2)) * 2;
+        unsigned d = (unsigned)__cvta_generic_to_shared(dst + col * rcp + r);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Vp + (int64_t)col * ld + c * rch + r));
     }
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
 // G (kp x 8, column-major ld kp) = Vp^T X on the FP64 tensor pipe, V_prev streamed through the
-// ring in coalesced 32-row chunks.  Warp w owns m-tile w/2 (8 columns of V_prev) and the k-steps
-// of parity w%2 in every chunk; the two parities are summed at the end (fixed order).
+// ring in coalesced chunks of vp_rows(kp) rows.  Warp w owns m-tile w/2 (8 columns of V_prev) and
+// the k-steps of parity w%2 in every chunk; the two parities are summed at the end (fixed order).
 __device__ void vt_block(const double* __restrict__ Vp, int64_t ld, int R, int kp, const double* X, int RP, double* G,
                          double* ring, double* pairbuf) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
     const int kr = lane & 3, cn = lane >> 2;
-    const int nch = R / RCH;
+    const int rch = vp_rows(kp), rcp = rch + 4;
+    const int nch = (R + rch - 1) / rch;
     double a0 = 0.0, a1 = 0.0;
-    vp_chunk(ring, Vp, ld, kp, 0);
+    vp_chunk(ring, Vp, ld, kp, rch, 0, min(rch, R));
     for (int c = 0; c < nch; ++c) {
-        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * 56 * RCP, Vp, ld, kp, c + 1);
+        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * RSTAGE, Vp, ld, kp, rch, c + 1, min(rch, R - (c + 1) * rch));
         else asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 1;\n" ::);
         __syncthreads();
-        const double* st = ring + (c & 1) * 56 * RCP;
+        const double* st = ring + (c & 1) * RSTAGE;
+        const int nq = min(rch, R - c * rch) / 8;
         if (t < mtiles) {
-#pragma unroll
-            for (int q = 0; q < RCH / 8; ++q) {
+#pragma unroll 4
+            for (int q = 0; q < nq; ++q) {
                 const int kk = (2 * q + par) * 4 + kr;  // row inside the chunk
-                dmma8(a0, a1, st[(t * 8 + cn) * RCP + kk], X[cn * RP + c * RCH + kk]);
+                dmma8(a0, a1, st[(t * 8 + cn) * rcp + kk], X[cn * RP + c * rch + kk]);
             }
         }
         __syncthreads();
@@ -190,21 +201,23 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
             double zb[14];
 #pragma unroll
             for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
-            // V_prev streamed through the ring; warps 0-3 each own one 8-row m-tile of the chunk
-            const int nch = R / RCH;
-            vp_chunk(red, Vp, ld, kp, 0);
+            // V_prev streamed through the ring; the 8-row m-tiles of a chunk are dealt to the warps
+            const int rch = vp_rows(kp), rcp = rch + 4;
+            const int nch = (R + rch - 1) / rch;
+            vp_chunk(red, Vp, ld, kp, rch, 0, min(rch, R));
             for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) vp_chunk(red + ((c + 1) & 1) * 56 * RCP, Vp, ld, kp, c + 1);
+                if (c + 1 < nch) vp_chunk(red + ((c + 1) & 1) * RSTAGE, Vp, ld, kp, rch, c + 1, min(rch, R - (c + 1) * rch));
                 else asm volatile("cp.async.commit_group;\n" ::);
                 asm volatile("cp.async.wait_group 1;\n" ::);
                 __syncthreads();
-                const double* st = red + (c & 1) * 56 * RCP;
-                if (warp < RCH / 8) {
-                    const int r0 = c * RCH + warp * 8;
+                const double* st = red + (c & 1) * RSTAGE;
+                const int nmt = min(rch, R - c * rch) / 8;
+                for (int mt = warp; mt < nmt; mt += PNW) {
+                    const int r0 = c * rch + mt * 8;
                     double c0 = Cb[(2 * kr) * RP + r0 + rn], c1 = Cb[(2 * kr + 1) * RP + r0 + rn];
 #pragma unroll
                     for (int t = 0; t < 14; ++t)
-                        if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * RCP + warp * 8 + rn], zb[t]);
+                        if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * rcp + mt * 8 + rn], zb[t]);
                     Cb[(2 * kr) * RP + r0 + rn] = c0;
                     Cb[(2 * kr + 1) * RP + r0 + rn] = c1;
                 }

@@ -15,44 +15,6 @@
 
 namespace {
 
-// ---- TRSM diagonal block: X = R_ii^{-T} At_i  (R_ii upper 64x64 -> lower solve) --------------
-// grid (ceil(4q/64), S), 64 threads: one column of At per thread.
-__global__ void __launch_bounds__(64) k_trsm_lt_diag(const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
-                                                     double* __restrict__ At, int M, int ncol_at, int i0, int bi) {
-    __shared__ double Rs[64][65];
-    __shared__ double rdg[64];
-    const int sl = blockIdx.y;
-    const double* A = Kaug + (int64_t)sl * ld * ncols;
-    for (int t = threadIdx.x; t < bi * bi; t += 64) {
-        int r = t % bi, c = t / bi;
-        Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];  // R[r][c], upper part used
-    }
-    __syncthreads();
-    if (threadIdx.x < bi) rdg[threadIdx.x] = 1.0 / Rs[threadIdx.x][threadIdx.x];
-    __syncthreads();
-    const int col = blockIdx.x * 64 + threadIdx.x;
-    if (col >= ncol_at) return;
-    double* x = At + (int64_t)sl * M * ncol_at + (int64_t)col * M + i0;
-    double xv[64];
-#pragma unroll
-    for (int r = 0; r < 64; ++r)
-        if (r < bi) xv[r] = x[r];
-    // R^T x = a: x_r = (a_r - sum_{l<r} R[l][r] x_l) / R[r][r]
-#pragma unroll
-    for (int r = 0; r < 64; ++r) {
-        if (r < bi) {
-            double s = xv[r];
-#pragma unroll
-            for (int l = 0; l < 64; ++l)
-                if (l < r) s -= Rs[l][r] * xv[l];
-            xv[r] = s * rdg[r];
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < 64; ++r)
-        if (r < bi) x[r] = xv[r];
-}
-
 // ---- interface: Q row blocks ------------------------------------------------------------------
 // Qrow[a] (q x (7q+1), ld qrow_ld): slot t (t < 7) = sum over the (<= 2) subdomains touching both
 // face a and face nbr[a][t] of P_s[e_a rows, e_b cols]; slot 7 = sum_s q_s[e_a rows].
