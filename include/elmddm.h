@@ -152,6 +152,15 @@ elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, con
  * Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot.                     */
 elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
                                             double* work, void* stream);
+/* The paper's interface solver: unpreconditioned conjugate gradients on
+ * eqn:schur, M u = g with M from elmddm_interface_assemble (not modified), x0 = 0, stopping at
+ * ||g - M u|| <= tol ||g|| (recurrence residual; the paper uses tol = 1e-9) or after maxit
+ * iterations.  Deterministic (fixed-order reductions).  work: >= 3 G_pad + G_pad/1024 + 5
+ * doubles.  Synchronous (reads the residual back every 16 iterations).  *iters and *relres (may
+ * be NULL) receive the iteration count and final relative residual; ELMDDM_ENUMERIC if the
+ * tolerance was not reached.                                                                   */
+elmddm_status elmddm_interface_cg(elmddm_ctx* ctx, const double* Mband, const double* g, double* uG, double* work,
+                                  double tol, int32_t maxit, int32_t* iters, double* relres, void* stream);
 /* = interface_assemble + interface_factor_solve. */
 elmddm_status elmddm_interface_solve(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
                                      double* g, double* uG, double* work, void* stream);

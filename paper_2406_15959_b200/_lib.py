@@ -42,7 +42,7 @@ STATUS = {0: "ELMDDM_OK", 1: "ELMDDM_EINVAL", 2: "ELMDDM_ENUMERIC", 3: "ELMDDM_E
 # every exported entry point of include/elmddm.h
 EXPORTS = [
     "elmddm_create", "elmddm_destroy", "elmddm_last_error", "elmddm_sizes", "elmddm_sync",
-    "elmddm_interface_points", "elmddm_band_index", "elmddm_chol_plan", "elmddm_init_hidden", "elmddm_assemble",
+    "elmddm_interface_points", "elmddm_band_index", "elmddm_chol_plan", "elmddm_interface_cg", "elmddm_init_hidden", "elmddm_assemble",
     "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
     "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
     "elmddm_set_timing", "elmddm_timing", "elmddm_dmma_probe",
@@ -80,6 +80,8 @@ def load():
     L.elmddm_band_index.argtypes = [ctxp, i64, i64]
     L.elmddm_band_index.restype = i64
     L.elmddm_chol_plan.argtypes = [ctxp, vp, vp]
+    L.elmddm_interface_cg.argtypes = [ctxp, vp, vp, vp, vp, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_double), vp]
     L.elmddm_init_hidden.argtypes = [ctxp, vp, vp, vp, vp]
     L.elmddm_assemble.argtypes = [ctxp, vp, vp, vp, vp, vp]
     L.elmddm_local_factor.argtypes = [ctxp, vp, vp, vp, vp]
@@ -97,6 +99,7 @@ def load():
         if f.restype is C.c_int or name in ("elmddm_create",):
             f.restype = st
     for name in ["elmddm_create", "elmddm_sizes", "elmddm_sync", "elmddm_interface_points", "elmddm_chol_plan",
+                 "elmddm_interface_cg",
                  "elmddm_init_hidden",
                  "elmddm_assemble", "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
                  "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",

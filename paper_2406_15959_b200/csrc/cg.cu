@@ -1,0 +1,151 @@
+// cg.cu -- the paper's interface solver: conjugate gradients on eqn:schur to a
+// relative residual tolerance (1e-9 in the paper), as an alternative to the direct
+// envelope Cholesky of chol.cu (reading R12).  M is the packed-tile lower envelope written by
+// elmddm_interface_assemble; every reduction is a fixed-order two-level sum (deterministic).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr int NB = ELM_NB;
+constexpr int LP = ELM_TLD;
+
+// y_I = sum_{J <= I} M(I,J) x_J + sum_{I' > I} M(I',I)^T x_I'   (one CTA per 64-row block I,
+// 256 threads: thread (r = tid & 63, part = tid >> 6) sums a quarter of the 64 columns of each
+// tile; the diagonal tile is used as tril(T) + strict-tril(T)^T).
+__global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb, int nbw, int nblk,
+                                                  const int* __restrict__ first, const int* __restrict__ last,
+                                                  const double* __restrict__ x, double* __restrict__ y) {
+    __shared__ double xs[NB];
+    __shared__ double part[4][NB];
+    const int I = blockIdx.x, tid = threadIdx.x, r = tid & 63, p = tid >> 6;
+    double acc = 0.0;
+    // row part: tiles (I, J), first[I] <= J <= I
+    for (int J = first[I]; J <= I; ++J) {
+        __syncthreads();
+        if (tid < NB) xs[tid] = x[(int64_t)J * NB + tid];
+        __syncthreads();
+        const double* T = Mb + tile_off(I, J, nbw);
+#pragma unroll 4
+        for (int c = p * 16; c < p * 16 + 16; ++c) {
+            double v = T[c * LP + r];  // element (r, c)
+            if (J == I && c > r) v = T[r * LP + c];  // upper part of the diagonal tile = transpose
+            acc += v * xs[c];
+        }
+    }
+    // column part: tiles (I', I), I < I' <= last[I], used transposed
+    for (int Ip = I + 1; Ip <= last[I]; ++Ip) {
+        if (first[Ip] > I) continue;
+        __syncthreads();
+        if (tid < NB) xs[tid] = x[(int64_t)Ip * NB + tid];
+        __syncthreads();
+        const double* T = Mb + tile_off(Ip, I, nbw);
+#pragma unroll 4
+        for (int c = p * 16; c < p * 16 + 16; ++c) acc += T[r * LP + c] * xs[c];  // element (c, r)
+    }
+    part[p][r] = acc;
+    __syncthreads();
+    if (tid < NB) y[(int64_t)I * NB + tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+}
+
+// partial dot products: part[b] = sum over the b-th 1024-chunk of a . b  (fixed order)
+__global__ void __launch_bounds__(256) k_dot_part(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                                                  double* __restrict__ part) {
+    __shared__ double red[8];
+    const int64_t i0 = (int64_t)blockIdx.x * 1024;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < 1024; k += 256)
+        if (i0 + k < n) s += a[i0 + k] * b[i0 + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+// sum the partials (one warp, fixed order) into *out
+__global__ void k_dot_final(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nparts; k += 32) s += part[k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// scalars: sc[0] = r.r, sc[1] = p.q, sc[2] = new r.r
+// x += alpha p, r -= alpha q   with alpha = rr / pq
+__global__ void k_cg_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                        const double* __restrict__ q, const double* __restrict__ sc, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double alpha = sc[1] != 0.0 ? sc[0] / sc[1] : 0.0;
+    x[i] += alpha * p[i];
+    r[i] -= alpha * q[i];
+}
+// p = r + beta p with beta = rr_new / rr;  then rr <- rr_new (one thread after the grid: see host)
+__global__ void k_cg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ sc, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double beta = sc[0] != 0.0 ? sc[2] / sc[0] : 0.0;
+    p[i] = r[i] + beta * p[i];
+}
+__global__ void k_cg_roll(double* sc) { sc[0] = sc[2]; }
+
+}  // namespace
+
+cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
+                             double tol, int maxit, int* iters, double* relres, cudaStream_t st) {
+    const int64_t Gp = c->sz.G_pad;
+    const int nblk = (int)(Gp / NB);
+    const int nparts = (int)((Gp + 1023) / 1024);
+    double* r = work;
+    double* p = r + Gp;
+    double* q = p + Gp;
+    double* part = q + Gp;
+    double* sc = part + nparts;  // [4]: rr, pq, rr_new, gg
+    cudaError_t e;
+    const int nb = (int)((Gp + 255) / 256);
+    auto dot = [&](const double* a, const double* b, double* out) -> cudaError_t {
+        k_dot_part<<<nparts, 256, 0, st>>>(a, b, Gp, part);
+        k_dot_final<<<1, 32, 0, st>>>(part, nparts, out);
+        return cudaGetLastError();
+    };
+    // x = 0, r = p = g
+    if ((e = cudaMemsetAsync(uG, 0, sizeof(double) * Gp, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(r, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(p, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    if ((e = dot(r, r, sc)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(sc + 3, sc, sizeof(double), cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    double h[4] = {0, 0, 0, 0};
+    if ((e = cudaMemcpyAsync(h, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const double gg = h[3];
+    int it = 0;
+    double rel = gg > 0.0 ? 1.0 : 0.0;
+    const int check = 16;  // convergence is read back every `check` iterations
+    while (rel > tol && it < maxit) {
+        for (int k = 0; k < check && it < maxit; ++k, ++it) {
+            {
+                KTimer kt(c, ELMDDM_K_TRSV, st);
+                k_spmv_sym<<<nblk, 256, 0, st>>>(Mband, (int)c->sz.band_nbw, nblk, c->d_first, c->d_last, p, q);
+            }
+            if ((e = dot(p, q, sc + 1)) != cudaSuccess) return e;
+            k_cg_xr<<<nb, 256, 0, st>>>(uG, r, p, q, sc, Gp);
+            if ((e = dot(r, r, sc + 2)) != cudaSuccess) return e;
+            k_cg_p<<<nb, 256, 0, st>>>(p, r, sc, Gp);
+            k_cg_roll<<<1, 1, 0, st>>>(sc);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        if ((e = cudaMemcpyAsync(h, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        rel = gg > 0.0 ? sqrt(h[0] / gg) : 0.0;
+    }
+    if (iters) *iters = it;
+    if (relres) *relres = rel;
+    return cudaSuccess;
+}

@@ -512,6 +512,32 @@ elmddm_status elmddm_interface_factor_solve(elmddm_ctx* c, double* Mband, const 
     return elmddm_sync(c, stream);
 }
 
+elmddm_status elmddm_interface_cg(elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
+                                  double tol, int32_t maxit, int32_t* iters, double* relres, void* stream) {
+    CHECK_CTX(c);
+    CHECK_PTR(c, Mband);
+    CHECK_PTR(c, g);
+    CHECK_PTR(c, uG);
+    CHECK_PTR(c, work);
+    if (!(tol > 0.0) || maxit < 1) {
+        c->err = "elmddm_interface_cg: tol must be > 0 and maxit >= 1";
+        return ELMDDM_EINVAL;
+    }
+    DeviceGuard dg(c->device);
+    int it = 0;
+    double rr = 0.0;
+    cudaError_t e = run_interface_cg(c, Mband, g, uG, work, tol, maxit, &it, &rr, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_interface_cg");
+    if (iters) *iters = it;
+    if (relres) *relres = rr;
+    if (!(rr <= tol)) {
+        c->err = "elmddm_interface_cg: no convergence in " + std::to_string(it) + " iterations (relative residual " +
+                 std::to_string(rr) + ")";
+        return ELMDDM_ENUMERIC;
+    }
+    return ELMDDM_OK;
+}
+
 elmddm_status elmddm_interface_solve(elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband, double* g,
                                      double* uG, double* work, void* stream) {
     elmddm_status s = elmddm_interface_assemble(c, Pbuf, Sbuf, Mband, g, work, stream);

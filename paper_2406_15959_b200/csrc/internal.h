@@ -176,6 +176,8 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
                                    double* g, double* work, cudaStream_t st);
 cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
                                cudaStream_t st);
+cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
+                             double tol, int maxit, int* iters, double* relres, cudaStream_t st);
 cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,
                            double* work, cudaStream_t st);
 

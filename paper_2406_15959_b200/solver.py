@@ -55,6 +55,8 @@ class Problem:
     init_c: float = 0.125
     r_over_diam: float = 0.5
     interface_mode: int = 0
+    interface_solver: str = "cholesky"  # "cholesky" (direct, reading R12) | "cg" (the paper's)
+    cg_tol: float = 1e-9                # relative residual of the CG solver
 
     @classmethod
     def from_config(cls, c: dict) -> "Problem":
@@ -73,6 +75,8 @@ class Context:
         if s_end is None:
             s_end = N
         self.device = torch.cuda.current_device() if device is None else device
+        if prob.interface_solver not in ("cholesky", "cg"):
+            raise _lib.ElmddmError(f"unknown interface_solver {prob.interface_solver!r}")
         cfg = _lib.Config(prob.P, prob.M, prob.p, prob.q, prob.problem, prob.init_scheme, prob.init_c,
                           prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, 0)
         h = C.c_void_p()
@@ -135,6 +139,14 @@ class Context:
     def interface_factor_solve(self, Mband, g, uG, work, stream=None):
         self._check(self.L.elmddm_interface_factor_solve(self.h, _ptr(Mband), _ptr(g), _ptr(uG), _ptr(work),
                                                          _stream(stream)), "interface_factor_solve")
+
+    def interface_cg(self, Mband, g, uG, work, tol=1e-9, maxit=100000, stream=None):
+        """The paper's CG interface solver; returns (iterations, relative residual)."""
+        it = C.c_int32()
+        rr = C.c_double()
+        self._check(self.L.elmddm_interface_cg(self.h, _ptr(Mband), _ptr(g), _ptr(uG), _ptr(work), float(tol), int(maxit),
+                                               C.byref(it), C.byref(rr), _stream(stream)), "interface_cg")
+        return int(it.value), float(rr.value)
 
     def interface_solve(self, Pbuf, Sbuf, Mband, g, uG, work, stream=None):
         self._check(self.L.elmddm_interface_solve(self.h, _ptr(Pbuf), _ptr(Sbuf), _ptr(Mband), _ptr(g), _ptr(uG),
@@ -211,7 +223,11 @@ class Context:
             if rank == 0:
                 self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
                 mark("interface_assemble")
-                self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
+                if self.prob.interface_solver == "cg":
+                    self.cg_info = self.interface_cg(buf["Mband"], buf["g"], buf["uG"], buf["work"], self.prob.cg_tol,
+                                                     stream=stream)
+                else:
+                    self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
                 mark("interface_factor_solve")
             if world > 1:
                 dist.broadcast(buf["uG"], src=0, group=group)

@@ -387,3 +387,93 @@ def test_interface_solve_residual_full_size(k):
     G = ctx.sizes["G"]
     r = _band_matvec(ctx, Mc, buf["uG"][:G]) - gc[:G]
     assert float(r.norm() / gc[:G].norm()) <= 1e-11, float(r.norm() / gc[:G].norm())
+
+
+# ------------------------------------------------------------------------------------------------
+# initialisation schemes (Table 1)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", [1, 2])
+def test_init_schemes_end_to_end_parity_config1(scheme):
+    """Manual (l = 1) and He (l = sqrt(2/n_N), b = 0) hidden layers through the whole path on
+    config 1.  Manual: u on the grid matches the oracle to relative L2 1e-6.  He: all basis
+    functions look alike and K^s is numerically rank deficient by hundreds of
+    columns, so neither u between collocation points (readings R18, R24) nor even the computed
+    residual norms are determined beyond rounding (measured: r_s 1.12 vs 1.36 for the same
+    u_Gamma); what is checked is Table 1's finding on both sides -- the He solution is useless --
+    and that the residual norms are of the same size."""
+    import torch
+
+    c = WL.config(1, init_scheme=scheme)
+    xy = WL.eval_grid()
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy, nthreads=NCPU)
+    if scheme == 1:
+        assert rel_l2(u.cpu().numpy(), r["u"]) <= 1e-6
+        return
+    G = ctx.sizes["G"]
+    uG = torch.zeros(ctx.sizes["G_pad"], dtype=torch.float64, device="cuda")
+    uG[:G] = torch.as_tensor(r["uG"], device="cuda")
+    resid = torch.empty_like(buf["resid"])
+    ctx.back_solve(buf["Kaug"], uG, torch.empty_like(buf["coef"]), resid, buf["work"])
+    torch.cuda.synchronize()
+    ratio = resid.cpu().numpy() / r["resid"]
+    assert np.all((ratio > 0.5) & (ratio < 2.0)), ratio
+    ue = WL.exact(c["problem"], xy)
+    assert rel_l2(u.cpu().numpy(), ue) > 1e-2 and rel_l2(r["u"], ue) > 1e-2
+
+
+def test_init_study_direction_config1():
+    """Table 1's finding on config 1: the suggested initialisation's interface RMSE is orders of
+    magnitude below He's, computed on the GPU."""
+    xy = WL.eval_grid(21)
+    rmse = {}
+    for sch in (0, 2):
+        c = WL.config(1, init_scheme=sch)
+        ctx, buf, _ = run_gpu(c, xy)
+        pts = ctx.interface_points()
+        uG = buf["uG"].cpu().numpy()[: ctx.sizes["G"]]
+        rmse[sch] = float(np.sqrt(np.mean((uG - WL.exact(c["problem"], pts)) ** 2)))
+    assert rmse[0] < 1e-2 * rmse[2], rmse
+
+
+# ------------------------------------------------------------------------------------------------
+# the paper's CG interface solver (P:412, P:439; SURVEY §8(f) NEXT-3)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", [1, 2])
+def test_interface_cg_matches_direct_solve(k):
+    """CG on eqn:schur reaches the paper's relative residual 1e-9 (checked with an independent
+    matvec of the assembled M), and its u_Gamma agrees with the Cholesky one within the bound
+    cond(M) * 1e-9 allows."""
+    import torch
+
+    c = WL.config(k)
+    ctx, buf, _ = run_gpu(c, upto="schur")
+    ctx.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"])
+    Mc = buf["Mband"].clone()
+    gc = buf["g"].clone()
+    uc = torch.zeros_like(buf["uG"])
+    it, rr = ctx.interface_cg(Mc, gc, uc, buf["work"], tol=1e-9)
+    torch.cuda.synchronize()
+    G = ctx.sizes["G"]
+    res = _band_matvec(ctx, Mc, uc[:G]) - gc[:G]
+    true_rel = float(res.norm() / gc[:G].norm())
+    assert rr <= 1e-9 and true_rel <= 1e-8, (it, rr, true_rel)
+    ctx.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"])
+    torch.cuda.synchronize()
+    assert rel_l2(uc[:G].cpu().numpy(), buf["uG"][:G].cpu().numpy()) <= 1e-3
+
+
+def test_cg_solver_end_to_end_parity_config1():
+    """The public API with interface_solver='cg' at a tight tolerance reproduces the oracle's u on
+    the grid to relative L2 1e-6 (the oracle solves eqn:schur directly)."""
+    import paper_2406_15959_b200 as E
+
+    c = WL.config(1)
+    xy = WL.eval_grid()
+    prob = E.Problem.from_config(c)
+    prob.interface_solver, prob.cg_tol = "cg", 1e-13
+    res = E.solve(prob, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy, nthreads=NCPU)
+    assert rel_l2(res["u"].numpy(), r["u"]) <= 1e-6

@@ -33,6 +33,7 @@ def _fake_ctx(rank, world):
 
     class Fake(S.Context):
         def __init__(self):  # no CUDA context
+            self.prob = S.Problem(P=2, M=8, p=3, q=2)
             self.sizes = {"G": G}
             self.s_begin, self.s_end = s0, s1
             self.calls = []

@@ -425,3 +425,21 @@ def test_config1_accuracy_vs_exact():
     r = O.solve(c, W, b, xy)
     ue = WL.exact(0, xy)
     assert np.linalg.norm(r["u"] - ue) / np.linalg.norm(ue) < 1e-10
+
+
+def test_init_study_direction_oracle():
+    """PAPER.md Table 1: He initialisation (l = sqrt(2/n_N), b = 0) gives an
+    interface RMSE orders of magnitude above the suggested eqn:init one (8.4e-3 vs
+    2.9e-10 at 2x2).  Small 3x3 geometry; the oracle solves both."""
+    rmse = {}
+    for sch in (0, 2):
+        c = O.cfg(3, 96, 12, 12, 0, sch, 0.125, 0.5, 11)
+        W, b, _, _ = O.init_hidden(c)
+        r = O.solve(c, W, b)
+        pts = np.zeros((len(r["uG"]), 2))
+        for s in range(9):
+            xy, edge, gidx = O.rows(c, s)
+            pts[gidx[gidx >= 0]] = xy[gidx >= 0]
+        ue = np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
+        rmse[sch] = float(np.sqrt(np.mean((r["uG"] - ue) ** 2)))
+    assert rmse[0] < 1e-3 * rmse[2], rmse
