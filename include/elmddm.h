@@ -133,7 +133,8 @@ elmddm_status elmddm_local_factor(elmddm_ctx* ctx, double* Kaug, double* tau, do
 /* Elimination of c^s (eqn:eliminated -> eqn:schur), per local subdomain s:
  *   At <- R11^{-T} At (so At^T = W_s = A^s R11^{-1}, the flux operator A^s K^{s+} restricted to
  *   range(Q_1));  Pbuf[s] = W_s [R12 | y]  (4q x kaug: flux of c^s(u) = q_s + P_s u_s);
- *   Sbuf[s] = [T_E | t_F]^T [T_E | t_F]   (kaug x kaug Gram).
+ *   Sbuf[s] = [T_E | t_F]^T [T_E | t_F]   (kaug x kaug Gram, symmetric: only its lower triangle
+ *             i >= j is guaranteed; 64 x 64 tiles strictly above the diagonal are not written).
  * Pbuf and Sbuf are GLOBAL (N slots); only slots [s_begin, s_end) are written, so a sum over
  * ranks of zero-filled buffers is their exact union (the NCCL reduce of DESIGN.md §6).        */
 elmddm_status elmddm_schur_accumulate(elmddm_ctx* ctx, double* Kaug, double* At, double* Pbuf, double* Sbuf,

@@ -56,7 +56,11 @@ __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restr
         double v = 0.0;
         for (int t = t0; t < t1; ++t) {
             FaceTerm ft = terms[t];
-            if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * sld];
+            if (ft.kind == 0) {  // S is symmetric and only its lower triangle is stored
+                const int rr = ft.r0 + i, cc = ft.c0 + j;
+                v += rr >= cc ? Sbuf[(int64_t)ft.src * sstride + rr + (int64_t)cc * sld]
+                              : Sbuf[(int64_t)ft.src * sstride + cc + (int64_t)rr * sld];
+            }
             else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * gld];
         }
         Mband[band_off((int64_t)b * q + i, (int64_t)c * q + j, nbw)] = v;
@@ -72,7 +76,7 @@ __global__ void k_gassemble(const int* __restrict__ gptr, const FaceTerm* __rest
         double v = 0.0;
         for (int t = gptr[b]; t < gptr[b + 1]; ++t) {
             FaceTerm ft = gterms[t];
-            if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + (ft.r0 + i) + (int64_t)ft.c0 * sld];
+            if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + ft.c0 + (int64_t)(ft.r0 + i) * sld];  // row 4q (lower)
             else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)ft.c0 * gld];
         }
         g[(int64_t)b * q + i] = -v;
@@ -345,7 +349,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     // S_s = [T_E | t_F]^T [T_E | t_F]
     const int Kt = (int)(ld - M);
     GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
-                ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 0};
+                ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 1 /* lower tiles only */};
     return gemm_launch(true, false, gs, st, c, ELMDDM_K_GEMM_SCHUR);
 }
 

@@ -74,8 +74,10 @@ def pbuf_np(ctx, buf, s, q):
 
 
 def sbuf_np(ctx, buf, s):
+    """Gram block of subdomain s, symmetrised from its stored lower triangle (kaug, kaug)."""
     z = ctx.sizes
-    return buf["Sbuf"].view(z["N"], z["kaug"], z["sbuf_ld"])[s].cpu().numpy().T[: z["kaug"], :]  # (kaug, kaug)
+    S = buf["Sbuf"].view(z["N"], z["kaug"], z["sbuf_ld"])[s].cpu().numpy().T[: z["kaug"], :]
+    return np.tril(S) + np.tril(S, -1).T
 
 
 def band_offsets(z, i, j):
