@@ -304,7 +304,9 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     {
         // subdomain groups for the QR streams (ELMDDM_QR_GROUPS overrides; 1 disables)
         const int64_t S = cfg->s_end - cfg->s_begin;
-        int g = S >= 64 ? 4 : 1;
+        // measured (tools/rank_slab.py, config 3 slabs of 256/128/64/32 subdomains): 8 groups is
+        // best or within noise everywhere once there are at least 4 subdomains per group
+        int g = (int)std::min<int64_t>(8, std::max<int64_t>(1, S / 4));
         if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
         c->qr_groups = g < 1 ? 1 : g;
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
