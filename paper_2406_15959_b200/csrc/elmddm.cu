@@ -310,6 +310,11 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
         c->qr_groups = g < 1 ? 1 : g;
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
+        // 4-CTA cluster panels cut the per-subdomain latency chain of the QR but spend more SM
+        // time: they win for the small per-rank slabs of multi-GPU runs (config 3: 32 subdomains
+        // 38.9 -> 28.0 ms, 16: 30.9 -> 18.9 ms) and lose for large ones (256: 174 -> 211 ms)
+        c->panel_cluster = S <= 48;
+        if (const char* env = getenv("ELMDDM_PANEL_CLUSTER")) c->panel_cluster = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_CHOL_CRITBAND")) c->crit_band = std::max(1, atoi(env));
     }
     elmddm_sizes_t& z = c->sz;

@@ -75,6 +75,7 @@ struct elmddm_ctx {
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    int panel_cluster = 0;  // QR panel blocks on 4-CTA clusters (default for S <= 48; ELMDDM_PANEL_CLUSTER)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
     mutable int trsv_epoch = 0;
     // envelope (skyline) of the Schur matrix at 64-tile granularity and the factorisation task list

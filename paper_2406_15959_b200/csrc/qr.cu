@@ -15,6 +15,7 @@
 
 #include "internal.h"
 #include "tma.cuh"
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
@@ -778,6 +779,362 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Cluster version of the panel base block: one subdomain's 8-column block is factored by a
+// cluster of PCL CTAs (PCL SMs), CTA z holding the rows [z Rq, (z+1) Rq) of the panel range.
+// With a quarter of the rows resident (<= 49 KB) each CTA streams its share of V_prev through a
+// deep ring (chunks of up to 128 rows at kp = 56); the cross-CTA sums (W = V_prev^T C, the 8
+// column reductions, the Gram of the block, V_prev^T V_b) are all-reduced through distributed
+// shared memory: every CTA writes its partial into slot z of every CTA's buffer, one cluster
+// barrier, then every CTA sums the slots in the same fixed order (deterministic, and every CTA
+// computes identical alpha / tau / T).  DESIGN.md §5.2.
+// ------------------------------------------------------------------------------------------
+namespace pcl {
+constexpr int CL = 4;                 // CTAs per subdomain
+constexpr int STG = 56 * 132;         // doubles per ring stage
+constexpr int XN = 448;               // doubles per exchange slot (kp * 8 <= 448)
+}  // namespace pcl
+
+__device__ __forceinline__ int vp_rows_cl(int kp) {
+    const int r = ((pcl::STG / kp - 4) / 32) * 32;
+    return r < 32 ? 32 : (r > 256 ? 256 : r);
+}
+
+// G (kp x 8, column-major ld kp) = Vp[0:nr]^T X[0:nr] (partial over this CTA's rows)
+__device__ void vt_block_cl(const double* __restrict__ Vp, int64_t ld, int nr, int kp, const double* X, int RP,
+                            double* G, double* ring, double* pairbuf) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
+    const int kr = lane & 3, cn = lane >> 2;
+    const int rch = vp_rows_cl(kp), rcp = rch + 4;
+    const int nch = (nr + rch - 1) / rch;
+    double a0 = 0.0, a1 = 0.0;
+    if (nch > 0) vp_chunk(ring, Vp, ld, kp, rch, 0, min(rch, nr));
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * pcl::STG, Vp, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
+        else asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+        __syncthreads();
+        const double* st = ring + (c & 1) * pcl::STG;
+        const int nq = min(rch, nr - c * rch) / 8;
+        if (t < mtiles) {
+#pragma unroll 4
+            for (int q = 0; q < nq; ++q) {
+                const int kk = (2 * q + par) * 4 + kr;
+                dmma8(a0, a1, st[(t * 8 + cn) * rcp + kk], X[cn * RP + c * rch + kk]);
+            }
+        }
+        __syncthreads();
+    }
+    if (t < mtiles && par == 1) {
+        pairbuf[t * 64 + lane * 2] = a0;
+        pairbuf[t * 64 + lane * 2 + 1] = a1;
+    }
+    __syncthreads();
+    if (t < mtiles && par == 0) {
+        a0 += pairbuf[t * 64 + lane * 2];
+        a1 += pairbuf[t * 64 + lane * 2 + 1];
+        G[(2 * kr) * kp + t * 8 + cn] = a0;
+        G[(2 * kr + 1) * kp + t * 8 + cn] = a1;
+    }
+}
+
+size_t panel_cl_smem(int64_t Rq) {
+    return (size_t)(8 * (Rq + 4) + 2 * pcl::STG + 2 * pcl::CL * pcl::XN + 2 * 8 * 56 + PNW * 28 + 40 + 64 + 8 + 16) * 8;
+}
+
+__global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_panel_cl(PanelArgs a) {
+    using namespace pcl;
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    const int z = (int)cl.block_rank();
+    const int sl = a.s_off + (int)blockIdx.x / CL;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0, jb = j0 + ELM_BB * a.blk, kp = ELM_BB * a.blk;
+    const int R = (int)(ld - j0);
+    const int Rq = ((R + 32 * CL - 1) / (32 * CL)) * 32;
+    const int r0 = z * Rq, nr = max(0, min(Rq, R - r0));
+    const int RP = Rq + 4;
+    const int d0 = jb - j0;
+    const int tid = threadIdx.x;
+    double* Cb = sm;                      // [8][RP]  own rows
+    double* ring = Cb + 8 * RP;           // [2][STG]
+    double* xch = ring + 2 * STG;         // [2][CL][XN]
+    double* Wsm = xch + 2 * CL * XN;      // [8][kp]
+    double* Zsm = Wsm + 8 * 56;           // [8][kp]
+    double* red = Zsm + 8 * 56;           // [PNW][28]
+    double* tot = red + PNW * 28;         // [40]
+    double* Tbb = tot + 40;               // [8][8]
+    double* taus = Tbb + 64;              // [8]
+    double* pay = taus + 8;               // [16]
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+    const double* Vz = V + j0 + r0;       // own rows of V_prev: column c at Vz + c*ld
+    int xpar = 0;
+    // all-reduce: mine[0..n) -> slot z of every CTA's buffer; returns the local buffer ([CL][XN])
+    auto exchange = [&](const double* mine, int n) -> const double* {
+        double* buf = xch + xpar * CL * XN;
+        for (int t = tid; t < CL * n; t += PNT) {
+            const int dst = t / n, i = t % n;
+            double* rb = cl.map_shared_rank(buf, dst);
+            rb[z * XN + i] = mine[i];
+        }
+        cl.sync();
+        xpar ^= 1;
+        return buf;
+    };
+
+    // A. own rows of the block
+    for (int c = 0; c < 8; ++c) {
+        const double* src = A + (int64_t)(jb + c) * ld + j0 + r0;
+        for (int r2 = tid; r2 < nr / 2; r2 += PNT) {
+            unsigned d = (unsigned)__cvta_generic_to_shared(Cb + c * RP + 2 * r2);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * r2));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+
+    if (kp > 0) {
+        // B. W = V_prev^T C (all-reduced), Z = T^T W, C -= V_prev Z on own rows
+        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm);
+        __syncthreads();
+        const double* buf = exchange(Wsm, kp * 8);
+        for (int i = tid; i < kp * 8; i += PNT) {
+            double v = 0.0;
+            for (int s = 0; s < CL; ++s) v += buf[s * XN + i];
+            Wsm[i] = v;
+        }
+        double* Ts = ring;
+        for (int t = tid; t < kp * kp; t += PNT) {
+            const int r = t % kp, c = t / kp;
+            Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+        }
+        __syncthreads();
+        for (int t = tid; t < kp * 8; t += PNT) {
+            const int cp = t % kp, c = t / kp;
+            double s = 0.0;
+            for (int k = 0; k <= cp; ++k) s += Ts[cp * kp + k] * Wsm[c * kp + k];
+            Zsm[c * kp + cp] = s;
+        }
+        __syncthreads();
+        {
+            const int lane = tid & 31, warp = tid >> 5;
+            const int kr = lane & 3, rn = lane >> 2;
+            const int ksteps = kp >> 2;
+            double zb[14];
+#pragma unroll
+            for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
+            __syncthreads();  // Ts (ring) no longer read
+            const int rch = vp_rows_cl(kp), rcp = rch + 4;
+            const int nch = (nr + rch - 1) / rch;
+            if (nch > 0) vp_chunk(ring, Vz, ld, kp, rch, 0, min(rch, nr));
+            for (int c = 0; c < nch; ++c) {
+                if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * STG, Vz, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
+                else asm volatile("cp.async.commit_group;\n" ::);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+                __syncthreads();
+                const double* st = ring + (c & 1) * STG;
+                const int nmt = min(rch, nr - c * rch) / 8;
+                for (int mt = warp; mt < nmt; mt += PNW) {
+                    const int rr = c * rch + mt * 8;
+                    double c0 = Cb[(2 * kr) * RP + rr + rn], c1 = Cb[(2 * kr + 1) * RP + rr + rn];
+#pragma unroll
+                    for (int t = 0; t < 14; ++t)
+                        if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * rcp + mt * 8 + rn], zb[t]);
+                    Cb[(2 * kr) * RP + rr + rn] = c0;
+                    Cb[(2 * kr + 1) * RP + rr + rn] = c1;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+
+    // C. factor the 8 columns: one cluster-wide reduction per column
+    for (int c = 0; c < 8; ++c) {
+        const int d = d0 + c;                 // panel-relative row of the diagonal entry
+        const int zo = d / Rq, dl = d - zo * Rq;
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = 0.0;
+        for (int r = max(0, d + 1 - r0) + tid; r < nr; r += PNT) {
+            const double x = Cb[c * RP + r];
+            v[0] += x * x;
+#pragma unroll
+            for (int c2 = 1; c2 < 8; ++c2)
+                if (c + c2 < 8) v[c2] += x * Cb[(c + c2) * RP + r];
+        }
+        block_sum<8>(v, red, tot);
+        if (tid < 16) {
+            double p = 0.0;
+            if (tid < 8) p = tot[tid];
+            else if (z == zo) p = (tid == 8) ? Cb[c * RP + dl] : ((c + tid - 8 < 8) ? Cb[(c + tid - 8) * RP + dl] : 0.0);
+            pay[tid] = p;
+        }
+        __syncthreads();
+        const double* buf = exchange(pay, 16);
+        double ts[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            double s = 0.0;
+            for (int q = 0; q < CL; ++q) s += buf[q * XN + k];
+            ts[k] = s;
+        }
+        const double x0 = buf[zo * XN + 8];
+        const double nrm = sqrt(x0 * x0 + ts[0]);
+        double alpha = x0, tau = 0.0, scale = 0.0;
+        if (nrm != 0.0) {
+            alpha = x0 >= 0.0 ? -nrm : nrm;
+            scale = 1.0 / (x0 - alpha);
+            tau = (alpha - x0) / alpha;
+        }
+        double w[8], yd[8];
+#pragma unroll
+        for (int c2 = 1; c2 < 8; ++c2) {
+            yd[c2] = (c + c2 < 8) ? buf[zo * XN + 8 + c2] : 0.0;
+            w[c2] = tau * (yd[c2] + scale * ts[c2]);
+        }
+        if (tau != 0.0) {
+            for (int r = max(0, d + 1 - r0) + tid; r < nr; r += PNT) {
+                const double x = Cb[c * RP + r];
+                const double vs = scale * x;
+#pragma unroll
+                for (int c2 = 1; c2 < 8; ++c2)
+                    if (c + c2 < 8) Cb[(c + c2) * RP + r] -= w[c2] * vs;
+                Cb[c * RP + r] = vs;
+            }
+        }
+        if (tid == 0) {
+            if (z == zo) {
+#pragma unroll
+                for (int c2 = 1; c2 < 8; ++c2)
+                    if (c + c2 < 8) Cb[(c + c2) * RP + dl] = yd[c2] - w[c2];
+                Cb[c * RP + dl] = alpha;
+            }
+            taus[c] = tau;
+        }
+        __syncthreads();
+    }
+
+    // D. write back R (upper) + V (below the diagonal) of own rows, and tau
+    for (int c = 0; c < 8; ++c) {
+        double2* dst = reinterpret_cast<double2*>(A + (int64_t)(jb + c) * ld + j0 + r0);
+        for (int r2 = tid; r2 < nr / 2; r2 += PNT) dst[r2] = make_double2(Cb[c * RP + 2 * r2], Cb[c * RP + 2 * r2 + 1]);
+    }
+    if (z == 0 && tid < 8) a.tau[(int64_t)sl * a.M + jb + tid] = taus[tid];
+    __syncthreads();
+    // E. explicit V of the block (zeros above, unit diagonal) on own rows -> smem and Vbuf
+    for (int c = 0; c < 8; ++c) {
+        const int d = d0 + c;
+        double2* dst = reinterpret_cast<double2*>(V + (int64_t)(kp + c) * ld + j0 + r0);
+        for (int r2 = tid; r2 < nr / 2; r2 += PNT) {
+            double v2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 2 * r2 + e, gr = r0 + r;
+                v2[e] = gr < d ? 0.0 : (gr == d ? 1.0 : Cb[c * RP + r]);
+                Cb[c * RP + r] = v2[e];
+            }
+            dst[r2] = make_double2(v2[0], v2[1]);
+        }
+    }
+    __syncthreads();
+    // F. T of the block from the (all-reduced) Gram of V_b
+    {
+        double g[28];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) g[k] = 0.0;
+        for (int r = max(0, d0 - r0) + tid; r < nr; r += PNT) {
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = Cb[c * RP + r];
+            int k = 0;
+#pragma unroll
+            for (int c1 = 0; c1 < 8; ++c1)
+#pragma unroll
+                for (int c2 = c1 + 1; c2 < 8; ++c2) g[k++] += x[c1] * x[c2];
+        }
+        block_sum<28>(g, red, tot);
+        const double* buf = exchange(tot, 28);
+        if (tid < 32) {
+            const int r = tid & 7;
+            double gs[28];
+#pragma unroll
+            for (int k = 0; k < 28; ++k) {
+                double s = 0.0;
+                for (int q = 0; q < CL; ++q) s += buf[q * XN + k];
+                gs[k] = s;
+            }
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) {
+                            const int gi = (k * (15 - k)) / 2 + (i - k - 1);
+                            s += trow[k] * gs[gi];
+                        }
+                    trow[i] = -taus[i] * s;
+                }
+            }
+            if (tid < 8)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Tbb[i * 8 + r] = trow[i];
+        }
+        __syncthreads();
+    }
+    // G. T[0:kp, kp:kp+8] = -T Y, Y = (V_prev^T V_b) Tbb
+    if (kp > 0) {
+        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm);
+        __syncthreads();
+        const double* buf = exchange(Wsm, kp * 8);
+        for (int i = tid; i < kp * 8; i += PNT) {
+            double v = 0.0;
+            for (int s = 0; s < CL; ++s) v += buf[s * XN + i];
+            Wsm[i] = v;
+        }
+        __syncthreads();
+        if (z == 0) {
+            for (int t = tid; t < kp * 8; t += PNT) {
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = 0; k <= c; ++k) s += Wsm[k * kp + r] * Tbb[c * 8 + k];
+                Zsm[c * kp + r] = s;
+            }
+            double* Ts = ring;
+            for (int t = tid; t < kp * kp; t += PNT) {
+                const int r = t % kp, c = t / kp;
+                Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+            }
+            __syncthreads();
+            for (int t = tid; t < kp * 8; t += PNT) {
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = r; k < kp; ++k) s += Ts[k * kp + r] * Zsm[c * kp + k];
+                T[(kp + c) * ELM_NB + r] = -s;
+            }
+        }
+    }
+    if (z == 0) {
+        for (int t = tid; t < 64; t += PNT) {
+            const int r = t % 8, c = t / 8;
+            T[(kp + c) * ELM_NB + kp + r] = Tbb[c * 8 + r];
+        }
+        const int c = tid / ELM_NB, r = tid % ELM_NB;  // 512 threads = 8 columns x 64 rows
+        if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
+    }
+    cl.sync();  // no CTA leaves while others may still write into its shared memory
+}
+
 size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * (R + 4) + 8 * 56 * 2 + RED_ELEMS + 40 + 64 + 8) * 8; }
 
 }  // namespace
@@ -815,6 +1172,9 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     const size_t smax = panel_smem_bytes(ld);
     cudaError_t e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
     if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)panel_cl_smem(((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32))) != cudaSuccess)
+        return e;
     if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wyt::SMEM)) != cudaSuccess)
@@ -842,6 +1202,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     for (int j0 = 0; j0 < M; j0 += ELM_NB) {
         const int nb = (M - j0) < ELM_NB ? (M - j0) : ELM_NB;
         const size_t smem = panel_smem_bytes(ld - j0);
+        const size_t smem_cl = panel_cl_smem(((ld - j0 + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32);
         const int n_tr = (int)(ncols - (j0 + nb));
         for (int g = 0; g < ngroups; ++g) {
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
@@ -850,7 +1211,10 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             for (int blk = 0; blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
-                k_panel_block<<<(unsigned)(g1 - g0), PNT, smem, streams[g]>>>(pa);
+                if (c->panel_cluster)
+                    k_panel_cl<<<(unsigned)((g1 - g0) * pcl::CL), PNT, smem_cl, streams[g]>>>(pa);
+                else
+                    k_panel_block<<<(unsigned)(g1 - g0), PNT, smem, streams[g]>>>(pa);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
             if (n_tr <= 0) continue;
