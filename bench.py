@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="elmddm", choices=["elmddm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--interface-mode", type=int, default=0,
+                    help="interface factorisation order: 0 auto, 2 strip (envelope), 3 nested dissection")
     ap.add_argument("--phases", action="store_true", help="print per-phase breakdown to stderr")
     return ap.parse_args()
 
@@ -242,7 +244,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    c = WL.config(args.config)
+    c = WL.config(args.config, interface_mode=args.interface_mode)
     prob = E.Problem.from_config(c)
     N = c["P"] ** 2
     s0, s1 = E.partition(N, world, rank)
@@ -386,7 +388,8 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(args.config), "subdomains": N, "l2_flush":
                            "inputs larger than L2: every step writes K_aug (S*ld*ncols*8 B) >> 126 MB",
-                           "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast"},
+                           "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast",
+                           "interface_ordering": ["strip", "nested_dissection"][ctx.sizes["chol_ordering"]]},
                 "time_to_solution_ms": ms_per_step, "rel_l2_vs_exact": err,
                 "roofline": roof, "roofline_local_factor": roof_qr, "roofline_assembly": roof_asm,
                 "roofline_interface": roof_iface,

@@ -64,7 +64,8 @@ typedef struct {
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s) (1/2)                    */
     uint64_t seed;          /* counter-based RNG key (reading R9)                    */
     int32_t s_begin, s_end; /* subdomains owned by this rank: [s_begin, s_end) of 0..N-1       */
-    int32_t interface_mode; /* 0 auto | 1 dense | 2 banded storage of the Schur matrix         */
+    int32_t interface_mode; /* factorisation order of the Schur matrix: 0 auto (less work) |
+                               1, 2 strip order (envelope) | 3 nested dissection             */
     int32_t reserved;
 } elmddm_config;
 
@@ -86,8 +87,11 @@ typedef struct {
     int64_t band_ld, band_nbw, band_elems; /* Schur matrix storage, see elmddm_band_index       */
     int64_t G_pad;                          /* G rounded up to the 64-tile                       */
     int64_t halfband;                       /* exact half-bandwidth of the Schur matrix          */
-    int64_t chol_tasks;                     /* 64 x 64 tiles of L inside the envelope             */
-    int64_t chol_flops;                     /* envelope Cholesky work: 2 * 64^3 per tile update   */
+    int64_t chol_tasks;                     /* 64 x 64 tiles of L (symbolic factorisation)        */
+    int64_t chol_flops;                     /* Cholesky work: 2 * 64^3 per tile update            */
+    int64_t chol_n;                         /* unknowns in the factorisation order (padded, %64)  */
+    int64_t chol_blocks;                    /* chol_n / 64                                        */
+    int64_t chol_ordering;                  /* 0 strip (envelope), 1 nested dissection            */
 } elmddm_sizes_t;
 
 /* ---- context ------------------------------------------------------------------------------ */
@@ -101,13 +105,17 @@ elmddm_status elmddm_sizes(const elmddm_ctx* ctx, elmddm_sizes_t* out);
 elmddm_status elmddm_sync(elmddm_ctx* ctx, void* stream);
 /* Host export of the u_Gamma ordering: xy_host[G][2] coordinates of the interface unknowns.   */
 elmddm_status elmddm_interface_points(const elmddm_ctx* ctx, double* xy_host);
-/* Offset of Schur-matrix element (i, j), i >= j, i - j <= halfband, in the packed tile storage:
- * tile (I, J) = (i/64, j/64) at (I*(band_nbw+1) + I-J) * 64*band_ld, element (i%64, j%64) at
- * (i%64) + (j%64)*band_ld inside it (band_ld = 68: padded column stride).  -1 if out of range.  */
+/* Offset of Schur-matrix element (i, j) (interface unknowns in strip order, either triangle) in
+ * the packed tile storage of M / L: the unknowns are renumbered into the factorisation order
+ * (strip order, or nested dissection with tile-aligned padding, see chol_ordering); element
+ * (a, b), a >= b, of the renumbered lower triangle lives in tile (a/64, b/64), stored
+ * contiguously (64 columns of band_ld = 68 doubles) at tile_id * 64 * band_ld.  -1 if the
+ * element is outside the structure of L.                                                        */
 int64_t elmddm_band_index(const elmddm_ctx* ctx, int64_t i, int64_t j);
-/* Host export of the factorisation plan: first[G_pad/64] (first nonzero tile column of every
- * tile row of the envelope) and tasks[chol_tasks][2] = (I, J) tile of L, column by column.     */
-elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* first, int32_t* tasks);
+/* Host export of the factorisation plan (each pointer may be NULL): newidx[G] = factorisation-
+ * order index of every interface unknown; tile_map[chol_blocks^2] = tile id of (I, J), I >= J,
+ * or -1; tasks[chol_tasks][2] = (I, J) of every tile task in the kernel's list order.          */
+elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* newidx, int32_t* tile_map, int32_t* tasks);
 
 /* ---- hot path ----------------------------------------------------------------------------- */
 /* eqn:init: W[S][M][2], b[S][M] for the local subdomains; xi[S][M][2] (may be NULL)
@@ -156,8 +164,7 @@ elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, cons
 /* The paper's interface solver: unpreconditioned conjugate gradients on
  * eqn:schur, M u = g with M from elmddm_interface_assemble (not modified), x0 = 0, stopping at
  * ||g - M u|| <= tol ||g|| (recurrence residual; the paper uses tol = 1e-9) or after maxit
- * iterations.  Deterministic (fixed-order reductions).  work: >= 3 G_pad + G_pad/1024 + 5
- * doubles.  Synchronous (reads the residual back every 16 iterations).  *iters and *relres (may
+ * iterations.  Deterministic (fixed-order reductions).  work: >= work_elems doubles.  Synchronous (reads the residual back every 16 iterations).  *iters and *relres (may
  * be NULL) receive the iteration count and final relative residual; ELMDDM_ENUMERIC if the
  * tolerance was not reached.                                                                   */
 elmddm_status elmddm_interface_cg(elmddm_ctx* ctx, const double* Mband, const double* g, double* uG, double* work,

@@ -31,7 +31,7 @@ class Sizes(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "N", "S", "m", "ld", "ncols", "kaug", "G", "faces", "kaug_elems", "at_elems", "tau_elems",
         "pbuf_ld", "pbuf_elems", "sbuf_ld", "sbuf_elems", "work_elems", "band_ld", "band_nbw", "band_elems",
-        "G_pad", "halfband", "chol_tasks", "chol_flops")]
+        "G_pad", "halfband", "chol_tasks", "chol_flops", "chol_n", "chol_blocks", "chol_ordering")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -79,7 +79,7 @@ def load():
     L.elmddm_interface_points.argtypes = [ctxp, vp]
     L.elmddm_band_index.argtypes = [ctxp, i64, i64]
     L.elmddm_band_index.restype = i64
-    L.elmddm_chol_plan.argtypes = [ctxp, vp, vp]
+    L.elmddm_chol_plan.argtypes = [ctxp, vp, vp, vp]
     L.elmddm_interface_cg.argtypes = [ctxp, vp, vp, vp, vp, C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                       C.POINTER(C.c_double), vp]
     L.elmddm_init_hidden.argtypes = [ctxp, vp, vp, vp, vp]

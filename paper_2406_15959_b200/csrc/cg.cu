@@ -13,22 +13,26 @@ namespace {
 constexpr int NB = ELM_NB;
 constexpr int LP = ELM_TLD;
 
-// y_I = sum_{J <= I} M(I,J) x_J + sum_{I' > I} M(I',I)^T x_I'   (one CTA per 64-row block I,
-// 256 threads: thread (r = tid & 63, part = tid >> 6) sums a quarter of the 64 columns of each
-// tile; the diagonal tile is used as tril(T) + strict-tril(T)^T).
-__global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb, int nbw, int nblk,
-                                                  const int* __restrict__ first, const int* __restrict__ last,
+// y_I = sum_{J <= I} M(I,J) x_J + sum_{I' > I} M(I',I)^T x_I' in the factorisation order (one
+// CTA per 64-row block I, 256 threads: thread (r = tid & 63, part = tid >> 6) sums a quarter of
+// the 64 columns of each tile; the diagonal tile is used as tril(T) + strict-tril(T)^T).  The
+// row / column tile lists are the triangular-solve dependency lists of the plan (plan.cu).
+__global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb, const int* __restrict__ diag_tid,
+                                                  const int* __restrict__ rptr, const int2* __restrict__ rdep,
+                                                  const int* __restrict__ cptr, const int2* __restrict__ cdep,
                                                   const double* __restrict__ x, double* __restrict__ y) {
     __shared__ double xs[NB];
     __shared__ double part[4][NB];
     const int I = blockIdx.x, tid = threadIdx.x, r = tid & 63, p = tid >> 6;
     double acc = 0.0;
-    // row part: tiles (I, J), first[I] <= J <= I
-    for (int J = first[I]; J <= I; ++J) {
+    // row part: tiles (I, J), J < I, then the diagonal tile
+    const int r0 = rptr[I], nr = rptr[I + 1] - r0;
+    for (int q = 0; q <= nr; ++q) {
+        const int J = q < nr ? rdep[r0 + q].x : I;
+        const double* T = Mb + (int64_t)(q < nr ? rdep[r0 + q].y : diag_tid[I]) * ELM_TS;
         __syncthreads();
         if (tid < NB) xs[tid] = x[(int64_t)J * NB + tid];
         __syncthreads();
-        const double* T = Mb + tile_off(I, J, nbw);
 #pragma unroll 4
         for (int c = p * 16; c < p * 16 + 16; ++c) {
             double v = T[c * LP + r];  // element (r, c)
@@ -36,19 +40,37 @@ __global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb,
             acc += v * xs[c];
         }
     }
-    // column part: tiles (I', I), I < I' <= last[I], used transposed
-    for (int Ip = I + 1; Ip <= last[I]; ++Ip) {
-        if (first[Ip] > I) continue;
+    // column part: tiles (I', I), I' > I, used transposed
+    const int c0 = cptr[I], nc = cptr[I + 1] - c0;
+    for (int q = 0; q < nc; ++q) {
+        const int Ip = cdep[c0 + q].x;
+        const double* T = Mb + (int64_t)cdep[c0 + q].y * ELM_TS;
         __syncthreads();
         if (tid < NB) xs[tid] = x[(int64_t)Ip * NB + tid];
         __syncthreads();
-        const double* T = Mb + tile_off(Ip, I, nbw);
 #pragma unroll 4
         for (int c = p * 16; c < p * 16 + 16; ++c) acc += T[r * LP + c] * xs[c];  // element (c, r)
     }
     part[p][r] = acc;
     __syncthreads();
     if (tid < NB) y[(int64_t)I * NB + tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+}
+
+__global__ void k_cg_gather(const double* __restrict__ g, const int* __restrict__ fbase, int q, int64_t G,
+                            double* __restrict__ y, int64_t n) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < n) y[x] = 0.0;
+}
+__global__ void k_cg_gather2(const double* __restrict__ g, const int* __restrict__ fbase, int q, int64_t G,
+                             double* __restrict__ y) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < G) y[fbase[x / q] + x % q] = g[x];
+}
+__global__ void k_cg_scatter(const double* __restrict__ y, const int* __restrict__ fbase, int q, int64_t G,
+                             double* __restrict__ u, int64_t Gpad) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < G) u[x] = y[fbase[x / q] + x % q];
+    else if (x < Gpad) u[x] = 0.0;
 }
 
 // partial dot products: part[b] = sum over the b-th 1024-chunk of a . b  (fixed order)
@@ -100,13 +122,16 @@ __global__ void k_cg_roll(double* sc) { sc[0] = sc[2]; }
 
 cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
                              double tol, int maxit, int* iters, double* relres, cudaStream_t st) {
-    const int64_t Gp = c->sz.G_pad;
-    const int nblk = (int)(Gp / NB);
+    const CholPlan& pl = c->plan;
+    const int64_t Gp = pl.n, G = c->sz.G;
+    const int nblk = pl.nblk, qd = c->cfg.q;
     const int nparts = (int)((Gp + 1023) / 1024);
     double* r = work;
     double* p = r + Gp;
     double* q = p + Gp;
-    double* part = q + Gp;
+    double* xn = q + Gp;     // solution in the factorisation order
+    double* gn = xn + Gp;    // right-hand side in the factorisation order
+    double* part = gn + Gp;
     double* sc = part + nparts;  // [4]: rr, pq, rr_new, gg
     cudaError_t e;
     const int nb = (int)((Gp + 255) / 256);
@@ -115,10 +140,12 @@ cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const dou
         k_dot_final<<<1, 32, 0, st>>>(part, nparts, out);
         return cudaGetLastError();
     };
-    // x = 0, r = p = g
-    if ((e = cudaMemsetAsync(uG, 0, sizeof(double) * Gp, st)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(r, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(p, g, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    // x = 0, r = p = g (in the factorisation order)
+    k_cg_gather<<<nb, 256, 0, st>>>(g, c->d_fbase, qd, G, gn, Gp);
+    if (G > 0) k_cg_gather2<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(g, c->d_fbase, qd, G, gn);
+    if ((e = cudaMemsetAsync(xn, 0, sizeof(double) * Gp, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(r, gn, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(p, gn, sizeof(double) * Gp, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
     if ((e = dot(r, r, sc)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(sc + 3, sc, sizeof(double), cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
     double h[4] = {0, 0, 0, 0};
@@ -132,10 +159,10 @@ cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const dou
         for (int k = 0; k < check && it < maxit; ++k, ++it) {
             {
                 KTimer kt(c, ELMDDM_K_TRSV, st);
-                k_spmv_sym<<<nblk, 256, 0, st>>>(Mband, (int)c->sz.band_nbw, nblk, c->d_first, c->d_last, p, q);
+                k_spmv_sym<<<nblk, 256, 0, st>>>(Mband, c->d_diag_tid, c->d_fwd_ptr, c->d_fwd, c->d_bwd_ptr, c->d_bwd, p, q);
             }
             if ((e = dot(p, q, sc + 1)) != cudaSuccess) return e;
-            k_cg_xr<<<nb, 256, 0, st>>>(uG, r, p, q, sc, Gp);
+            k_cg_xr<<<nb, 256, 0, st>>>(xn, r, p, q, sc, Gp);
             if ((e = dot(r, r, sc + 2)) != cudaSuccess) return e;
             k_cg_p<<<nb, 256, 0, st>>>(p, r, sc, Gp);
             k_cg_roll<<<1, 1, 0, st>>>(sc);
@@ -145,6 +172,8 @@ cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const dou
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
         rel = gg > 0.0 ? sqrt(h[0] / gg) : 0.0;
     }
+    k_cg_scatter<<<(unsigned)((c->sz.G_pad + 255) / 256), 256, 0, st>>>(xn, c->d_fbase, qd, G, uG, c->sz.G_pad);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (iters) *iters = it;
     if (relres) *relres = rel;
     return cudaSuccess;

@@ -1,20 +1,21 @@
 // chol.cu -- Cholesky factorisation of the interface Schur matrix (eqn:schur is SPD, P:412;
 // reading R12: a direct solve instead of the paper's CG) and the two triangular solves.
 //
-// Storage (internal.h): packed 64 x 64 tiles of the lower band, tile (I, J) with
-// 0 <= I - J <= nbw contiguous at tile_off(I, J), element (r, c) at r + c * ELM_TLD (ELM_TLD = 68).
-// A tile (or its first 32 columns) is therefore one contiguous bulk copy that lands in shared
-// memory already in the padded, bank-conflict-free layout the DMMA fragments read.
+// Storage (internal.h): the 64 x 64 tiles of the lower factor's tile structure
+// (plan.cu: strip/envelope or nested-dissection order, symbolic factorisation on tiles), tile t
+// contiguous at t * ELM_TS, element (r, c) at r + c * ELM_TLD (ELM_TLD = 68).  A tile (or its
+// first 32 columns) is therefore one contiguous bulk copy that lands in shared memory already in
+// the padded, bank-conflict-free layout the DMMA fragments read.
 //
-// Factorisation: ONE persistent kernel, left-looking over the tiles of the envelope (skyline)
-// of M.  Tile-row I is structurally zero left of tile column first[I] (the envelope is closed
-// under Cholesky fill), so tile (I, J) of L, first[I] <= J <= I, is
-//     C      = M(I, J) - sum_{k = max(first[I], first[J])}^{J-1} L(I, k) L(J, k)^T   (DMMA)
+// Factorisation: ONE persistent kernel, left-looking over the tiles of L.  Tile (I, J) is
+//     C      = M(I, J) - sum_{k in klist(I, J)} L(I, k) L(J, k)^T              (DMMA)
 //     L(J,J), Y_J = L(J,J)^{-1} from C           (I == J: unblocked Cholesky + inverse in smem)
 //     L(I,J) = C L(J,J)^{-T}                      (I > J: X0 = C Y_J^T and one refinement step
 //                                                  X = X0 + (C - X0 L(J,J)^T) Y_J^T, three 64^3 DMMAs)
-// The k-sum streams 32-column halves of L(I,k) and L(J,k) through a 3-stage TMA bulk-copy /
-// mbarrier pipeline issued by one thread.  Tasks (I, J) are listed column by column and dealt
+// where klist(I, J) = {k < J : L(I, k) and L(J, k) structurally nonzero} comes with the plan
+// (pairs of tile ids).  The k-sum streams 32-column halves of L(I,k) and L(J,k) through a
+// 3-stage TMA bulk-copy / mbarrier pipeline issued by one thread.  Tasks are listed column by
+// column (critical tiles I - J <= crit_band first, worked by dedicated CTAs) and dealt
 // round-robin to co-resident CTAs; each finished tile publishes a per-tile flag (release /
 // acquire) and bumps its column's counter.  A task waits only for tiles of earlier columns or
 // for the diagonal of its own column, so the smallest unfinished task can always run (no
@@ -281,19 +282,19 @@ __device__ __forceinline__ void trsm_refined(double (&x)[4][2][2], double* As, c
 }
 
 struct CholArgs {
-    double* Mb;          // packed tiles
-    double* Ybuf;        // [nblk] packed tiles: L(J,J)^{-1}
-    double* Cbuf;        // [nblk] packed tiles: C(I, I-1) before its triangular solve
-    int* cready;         // [nblk] Cbuf[I] published (epoch)
-    const int2* tasks;   // (I, J): [0, ncrit) critical chain, then the other tiles; column by column
+    double* Mb;            // tile pool: tile id t at t * ELM_TS
+    double* Ybuf;          // [nblk] packed tiles: L(J,J)^{-1}
+    double* Cbuf;          // [nblk] packed tiles: C(I, klast(I)) before its triangular solve
+    int* cready;           // [nblk] Cbuf[I] published (epoch)
+    const TaskDesc* tasks; // [0, ncrit) critical band, then the other tiles; each column by column
     int ntasks;
-    int ncrit;           // tasks of the critical chain (diagonal and sub-diagonal tiles)
-    int crit_ctas;       // CTAs [0, crit_ctas) work the critical list, the rest the others
-    const int* first;    // first nonzero tile column of every tile row
-    int* flags;          // [nblk][nbw + 1]: tile (I, J) at I * (nbw + 1) + (I - J)
-    int* colcnt;         // [nblk] finished tiles of column J, summed over factorisations
-    const int* ntc;      // [nblk] tiles of column J
-    int nbw;
+    int ncrit;
+    int crit_ctas;         // CTAs [0, crit_ctas) work the critical list, the rest the others
+    const int4* klist;     // per-task update lists: (tile (I,k), tile (J,k), k, 0)
+    const int* diag_tid;   // [nblk] tile id of (J, J)
+    int* flags;            // [ntiles] per-tile completion (epoch)
+    int* colcnt;           // [nblk] finished tiles of column J, summed over factorisations
+    const int* ntc;        // [nblk] tiles of column J
     int epoch;
     ElmStatus* status;
 };
@@ -313,9 +314,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const int stride = a.nbw + 1;
-    auto flag = [&](int I, int J) { return a.flags + (int64_t)I * stride + (I - J); };
-    auto tile = [&](int I, int J) { return a.Mb + tile_off(I, J, a.nbw); };
+    auto tileptr = [&](int t) { return a.Mb + (int64_t)t * TILE; };
     int known = 0;        // (thread 0) every column < known is complete
     uint32_t gchunk = 0;  // chunk loads issued by this CTA so far (stage = gchunk % NSTAGE)
     uint32_t epi_uses = 0;
@@ -323,60 +322,62 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #ifdef ELM_CHOL_PROF
     unsigned long long pf_flag = 0, pf_data = 0;
 #endif
-    auto ensure = [&](int I, int J, int k) {
+    auto ensure = [&](const int4& e, int J) {
 #ifdef ELM_CHOL_PROF
         const uint64_t q0 = globaltimer();
         struct Acc { unsigned long long& r; uint64_t q; __device__ ~Acc() { r += globaltimer() - q; } } acc_{pf_flag, q0};
 #endif
+        const int k = e.z;
         if (k < known) return;
         while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
         if (k < known) return;
-        wait_flag(flag(I, k), a.epoch, a.status, I);
-        wait_flag(flag(J, k), a.epoch, a.status, J);
+        wait_flag(a.flags + e.x, a.epoch, a.status, k);
+        wait_flag(a.flags + e.y, a.epoch, a.status, k);
     };
     const bool critw = (int)blockIdx.x < a.crit_ctas;
     const int t_begin = critw ? (int)blockIdx.x : a.ncrit + (int)blockIdx.x - a.crit_ctas;
     const int t_end = critw ? a.ncrit : a.ntasks;
     const int t_step = critw ? a.crit_ctas : (int)gridDim.x - a.crit_ctas;
     for (int t = t_begin; t < t_end; t += t_step) {
-        const int2 ij = a.tasks[t];
-        const int I = ij.x, J = ij.y;
-        const int k0 = max(a.first[I], a.first[J]);
-        // the diagonal task applies the last term k = J-1 itself: it solves for L(J, J-1) from the
-        // published C(J, J-1) (one flag hop less on the critical path)
-        const bool dsub = I == J && J - 1 >= k0;
-        const int nch = 2 * ((dsub ? J - 1 : J) - k0);
+        const TaskDesc td = a.tasks[t];
+        const int I = td.I, J = td.J;
+        // the diagonal task applies its last update column klast itself: it solves for
+        // L(J, klast) from the published C(J, klast) (one flag hop less on the critical path)
+        const bool dsub = I == J && td.klast >= 0;
+        const int kb = td.kbeg, ke = dsub ? td.kend - 1 : td.kend;
+        const int nch = 2 * (ke - kb);
 #ifdef ELM_CHOL_PROF
         const uint64_t pt0 = globaltimer();
         pf_flag = pf_data = 0;
 #endif
         const uint32_t g0 = gchunk;
-        // chunk c: columns [32h, 32h + 32) of L(I, k) and L(J, k), k = k0 + c/2, h = c & 1
+        // chunk c: columns [32h, 32h + 32) of L(I, k) and L(J, k), k = klist[kb + c/2], h = c & 1
         auto issue = [&](int c) {  // thread 0 only
-            const int k = k0 + (c >> 1), h = c & 1;
+            const int4 ke4 = a.klist[kb + (c >> 1)];
+            const int h = c & 1;
             const uint32_t g = g0 + c;
             double* st = St + (g % NSTAGE) * TILE;
             uint64_t* b = &bar[g % NSTAGE];
             fence_proxy_async();
             mbar_expect(b, 2 * HALF_BYTES);
-            bulk_load(st, tile(I, k) + h * HALF, HALF_BYTES, b);
-            bulk_load(st + HALF, tile(J, k) + h * HALF, HALF_BYTES, b);
+            bulk_load(st, tileptr(ke4.x) + h * HALF, HALF_BYTES, b);
+            bulk_load(st + HALF, tileptr(ke4.y) + h * HALF, HALF_BYTES, b);
         };
         double acc[4][2][2];  // holds -C while the updates are added
         {
-            const double* Ct = tile(I, J);
+            const double* Ct = tileptr(td.tid);
             FOR_FRAG acc[mt][nt][e] = -__ldcg(Ct + frag_r(mt) + frag_c(nt, e) * LP);
         }
         if (tid == 0)
             for (int c = 0; c < NSTAGE - 1 && c < nch; ++c) {
-                if ((c & 1) == 0) ensure(I, J, k0 + (c >> 1));
+                if ((c & 1) == 0) ensure(a.klist[kb + (c >> 1)], J);
                 issue(c);
             }
         for (int c = 0; c < nch; ++c) {
             if (c > 0) __syncthreads();  // every warp is done with chunk c-1: its stage may be refilled
             if (tid == 0 && c + NSTAGE - 1 < nch) {
                 const int cn = c + NSTAGE - 1;
-                if ((cn & 1) == 0) ensure(I, J, k0 + (cn >> 1));
+                if ((cn & 1) == 0) ensure(a.klist[kb + (cn >> 1)], J);
                 issue(cn);
             }
             const uint32_t g = g0 + c;
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #ifdef ELM_CHOL_PROF
         const uint64_t pte = globaltimer();
 #endif
-        double* dst = tile(I, J);
+        double* dst = tileptr(td.tid);
         if (I == J) {
 #ifdef ELM_CHOL_PROF
             uint64_t dts[8] = {globaltimer(), 0, 0, 0, 0, 0, 0, 0};
@@ -409,23 +410,23 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 ++epi_uses;
                 if (tid == 0) {
                     wait_flag(a.cready + J, a.epoch, a.status, J);
-                    wait_flag(flag(J - 1, J - 1), a.epoch, a.status, J - 1);
+                    wait_flag(a.flags + a.diag_tid[td.klast], a.epoch, a.status, td.klast);
                     fence_proxy_async();
                     mbar_expect(eb, 3 * TILE * 8);
                     bulk_load(As, a.Cbuf + (int64_t)J * TILE, TILE * 8, eb);
-                    bulk_load(Bs, tile(J - 1, J - 1), TILE * 8, eb);
-                    bulk_load(Ys, a.Ybuf + (int64_t)(J - 1) * TILE, TILE * 8, eb);
+                    bulk_load(Bs, tileptr(a.diag_tid[td.klast]), TILE * 8, eb);
+                    bulk_load(Ys, a.Ybuf + (int64_t)td.klast * TILE, TILE * 8, eb);
                 }
                 DSTAMP(1);
                 mbar_wait(eb, epar);
                 DSTAMP(2);
                 double x[4][2][2];
-                trsm_refined(x, As, Bs, Ys);                      // L(J, J-1)
+                trsm_refined(x, As, Bs, Ys);                      // L(J, klast)
                 DSTAMP(3);
                 __syncthreads();
                 FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = x[mt][nt][e];
                 __syncthreads();
-                mma_tile<NB>(acc, As, As);                        // -C(J,J) + L(J,J-1) L(J,J-1)^T
+                mma_tile<NB>(acc, As, As);                        // -C(J,J) + L(J,klast) L(J,klast)^T
                 __syncthreads();
             }
             FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         } else {
             // C -> As[c * LP + r]
             FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
-            if (I == J + 1) {  // publish C(I, I-1) for the diagonal task of column I
+            if (td.pub) {  // publish C(I, J = klast(I)) for the diagonal task of row I
                 double* cb = a.Cbuf + (int64_t)I * TILE;
                 FOR_FRAG cb[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
                 __threadfence();
@@ -465,14 +466,14 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #ifdef ELM_CHOL_PROF
                 const uint64_t pw = globaltimer();
 #endif
-                wait_flag(flag(J, J), a.epoch, a.status, J);
+                wait_flag(a.flags + a.diag_tid[J], a.epoch, a.status, J);
 #ifdef ELM_CHOL_PROF
                 pf_flag += globaltimer() - pw;
 #endif
                 fence_proxy_async();
                 mbar_expect(eb, 2 * TILE * 8);
                 bulk_load(Ys, a.Ybuf + (int64_t)J * TILE, TILE * 8, eb);
-                bulk_load(Bs, tile(J, J), TILE * 8, eb);
+                bulk_load(Bs, tileptr(a.diag_tid[J]), TILE * 8, eb);
             }
             __syncthreads();  // C visible to every warp
             mbar_wait(eb, epar);
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-            st_release(flag(I, J), a.epoch);
+            st_release(a.flags + td.tid, a.epoch);
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.colcnt + J) : "memory");
 #ifdef ELM_CHOL_PROF
             if (t < 400000) {
@@ -515,8 +516,8 @@ __device__ __forceinline__ void load_tile_async(double* dst, const double* src) 
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int nbw, int nblk,
-                                                   const int* __restrict__ first, const int* __restrict__ last,
+__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int nblk, const int* __restrict__ diag_tid,
+                                                   const int* __restrict__ dptr, const int2* __restrict__ dep,
                                                    const double* __restrict__ rhs, double* __restrict__ out, int* flags,
                                                    int epoch, int dir, ElmStatus* status) {
     extern __shared__ __align__(16) double tsm[];
@@ -529,13 +530,10 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
     for (int it = blockIdx.x; it < nblk; it += gridDim.x) {
         const int i = dir == 0 ? it : nblk - 1 - it;
         const int64_t i0 = (int64_t)i * NB;
-        const int jlo = dir == 0 ? first[i] : i + 1;
-        const int jhi = dir == 0 ? i - 1 : last[i];
-        const int nj = jhi - jlo + 1;
+        // dependencies: forward (j, tile (i, j)) ascending j; backward (j, tile (j, i)) descending j
+        const int d0 = dptr[i], nj = dptr[i + 1] - d0;
         auto tile_of = [&](int q) -> const double* {  // q-th dependency tile, then the diagonal
-            if (q == nj) return Mb + tile_off(i, i, nbw);
-            const int j = dir == 0 ? jlo + q : jhi - q;
-            return dir == 0 ? Mb + tile_off(i, j, nbw) : Mb + tile_off(j, i, nbw);
+            return Mb + (int64_t)(q == nj ? diag_tid[i] : dep[d0 + q].y) * ELM_TS;
         };
         if (tid < NB) acc[tid] = rhs[i0 + tid];
         load_tile_async(tiles, tile_of(0));
@@ -544,7 +542,7 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
             if (q < nj) load_tile_async(tiles + (st ^ 1) * ELM_TS, tile_of(q + 1));
             else asm volatile("cp.async.commit_group;\n" ::);
             if (q < nj) {
-                const int j = dir == 0 ? jlo + q : jhi - q;
+                const int j = dep[d0 + q].x;
                 if (tid == 0) wait_flag(flags + j, epoch, status, j);
                 __syncthreads();
                 if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
@@ -610,6 +608,23 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
     }
 }
 
+// interface unknowns: strip order (the ABI's g / u_Gamma) <-> factorisation order
+__global__ void k_perm_zero(double* __restrict__ y, int64_t n) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < n) y[x] = 0.0;  // padding unknowns keep 0 (unit diagonal)
+}
+__global__ void k_perm_gather(const double* __restrict__ g, const int* __restrict__ fbase, int q, int64_t G,
+                              double* __restrict__ y) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < G) y[fbase[x / q] + x % q] = g[x];
+}
+__global__ void k_perm_scatter(const double* __restrict__ y, const int* __restrict__ fbase, int q, int64_t G,
+                               double* __restrict__ u, int64_t Gpad) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < G) u[x] = y[fbase[x / q] + x % q];
+    else if (x < Gpad) u[x] = 0.0;
+}
+
 }  // namespace
 
 #ifdef ELM_CHOL_PROF
@@ -623,11 +638,12 @@ extern "C" int elmddm_debug_chol_dprof(void* host, int n) {
 
 cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
                                cudaStream_t st) {
-    const int64_t Gp = c->sz.G_pad;
-    const int nblk = (int)(Gp / NB);
-    const int nbw = (int)c->sz.band_nbw;
-    double* z = work;
-    double* Ybuf = work + Gp;  // [nblk] packed tiles (Gp is a multiple of 64: 16-byte aligned)
+    const CholPlan& pl = c->plan;
+    const int64_t n = pl.n, G = c->sz.G;
+    const int nblk = pl.nblk, q = c->cfg.q;
+    double* yv = work;          // right-hand side, then the solution, in the factorisation order
+    double* z = yv + n;
+    double* Ybuf = z + n;       // [nblk] packed tiles (n is a multiple of 64: 16-byte aligned)
     double* Cbuf = Ybuf + (int64_t)nblk * ELM_TS;
     cudaError_t e;
     static int grid_ll = 0, grid_sv = 0;
@@ -643,14 +659,18 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         grid_ll = (per_sm > 0 ? per_sm : 1) * c->nsm;
         grid_sv = c->nsm;
     }
-    // factorisation: one cooperative launch over the envelope's tile list
+    // right-hand side into the factorisation order
+    k_perm_zero<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(yv, n);
+    if (G > 0) k_perm_gather<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(g, c->d_fbase, q, G, yv);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // factorisation: one cooperative launch over the task list
     {
         int grid = grid_ll;
         int crit = 32;
         if (const char* env = getenv("ELMDDM_CHOL_CRIT")) crit = atoi(env);
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
-        CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, reinterpret_cast<const int2*>(c->d_tasks), c->ntasks, c->ncrit, crit,
-                   c->d_first, c->d_cflags, c->d_colcnt, c->d_ntc, nbw, ++c->chol_epoch, c->d_status};
+        CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
+                   c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status};
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
         if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=
@@ -663,13 +683,14 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         int* flags = c->d_flags;
         for (int dir = 0; dir < 2; ++dir) {
             int epoch = ++c->trsv_epoch;
-            const double* rhs = dir == 0 ? g : z;
-            double* out = dir == 0 ? z : uG;
-            int nbw_v = nbw, nblk_v = nblk;
-            const int* fp = c->d_first;
-            const int* lp = c->d_last;
+            const double* rhs = dir == 0 ? yv : z;
+            double* out = dir == 0 ? z : yv;
+            int nblk_v = nblk;
+            const int* dt = c->d_diag_tid;
+            const int* dp = dir == 0 ? c->d_fwd_ptr : c->d_bwd_ptr;
+            const int2* dl = dir == 0 ? c->d_fwd : c->d_bwd;
             ElmStatus* stp = c->d_status;
-            void* args[] = {(void*)&Mband, (void*)&nbw_v, (void*)&nblk_v, (void*)&fp, (void*)&lp, (void*)&rhs,
+            void* args[] = {(void*)&Mband, (void*)&nblk_v, (void*)&dt, (void*)&dp, (void*)&dl, (void*)&rhs,
                             (void*)&out, (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
             KTimer kt(c, ELMDDM_K_TRSV, st);
             if ((e = cudaLaunchCooperativeKernel((void*)k_band_trsv, dim3(grid), dim3(256), args, TRSV_SMEM, st)) !=
@@ -677,5 +698,8 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
                 return e;
         }
     }
-    return cudaSuccess;
+    // solution back into the strip order of u_Gamma
+    const int64_t Gp = c->sz.G_pad;
+    k_perm_scatter<<<(unsigned)((Gp + 255) / 256), 256, 0, st>>>(yv, c->d_fbase, q, G, uG, Gp);
+    return cudaGetLastError();
 }

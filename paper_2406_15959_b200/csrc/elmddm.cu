@@ -55,7 +55,7 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
     int64_t N = (int64_t)cfg->P * cfg->P;
     if (cfg->s_begin < 0 || cfg->s_end > N || cfg->s_begin >= cfg->s_end) return why = "bad [s_begin, s_end)", false;
-    if (cfg->interface_mode < 0 || cfg->interface_mode > 2) return why = "bad interface_mode", false;
+    if (cfg->interface_mode < 0 || cfg->interface_mode > 3) return why = "bad interface_mode", false;
     if (cfg->q > 256) return why = "q too large", false;
     return true;
 }
@@ -174,57 +174,33 @@ elmddm_status build_tables(elmddm_ctx* c) {
     c->sz.faces = F;
     c->sz.G_pad = round_up(std::max<int64_t>(G, 1), ELM_NB);
     c->sz.halfband = F > 0 ? hb : 0;
-    const int64_t nblk = c->sz.G_pad / ELM_NB;
-    int64_t nbw = (c->sz.halfband + ELM_NB - 1) / ELM_NB;
-    int64_t LD = (nbw + 2) * ELM_NB;
-    bool dense = c->cfg.interface_mode == 1 || (c->cfg.interface_mode == 0 && LD >= c->sz.G_pad);
-    if (dense || nbw >= nblk - 1) {
-        nbw = nblk - 1;
-        LD = c->sz.G_pad;
-    }
-    c->sz.band_nbw = nbw;
-    c->sz.band_ld = ELM_TLD;
-    c->sz.band_elems = nblk * (nbw + 1) * (int64_t)ELM_TS;
-
-    // Envelope at tile granularity: face b's rows start at column min{c : (b, c) pair} * q, so
-    // tile row I starts at the minimum over the faces it overlaps.  Cholesky fill stays inside
-    // the envelope, so tile (I, J) of L can be nonzero only for first[I] <= J <= I.
-    std::vector<int> minc(F > 0 ? F : 1, 0);
-    for (int b = 0; b < F; ++b) minc[b] = b;
-    for (auto& kv : pairs) minc[kv.first.first] = std::min(minc[kv.first.first], kv.first.second);
-    c->first_h.assign(nblk, 0);
-    std::vector<int> last(nblk, 0);
-    for (int64_t I = 0; I < nblk; ++I) {
-        int64_t r0 = I * ELM_NB, r1 = std::min<int64_t>(r0 + ELM_NB, G) - 1;
-        int64_t f = I;
-        if (r0 < G)
-            for (int64_t b = r0 / q; b <= r1 / q; ++b) f = std::min<int64_t>(f, (int64_t)minc[b] * q / ELM_NB);
-        c->first_h[I] = (int)f;
-    }
-    // task lists: the critical chain (diagonal tile and sub-diagonal tile of every column) and
-    // the ordinary tiles, each column by column; the kernel gives the critical list to a few
-    // dedicated CTAs so that those accumulations run ahead as soon as their inputs exist
-    std::vector<int> crit, reg, ntc(nblk, 0);
-    int64_t nupd = 0;
-    for (int64_t J = 0; J < nblk; ++J) {
-        last[J] = (int)J;
-        for (int64_t I = J; I < nblk && I - J <= nbw; ++I) {
-            if (c->first_h[I] > J) continue;
-            std::vector<int>& lst = (I - J <= c->crit_band) ? crit : reg;
-            lst.push_back((int)I);
-            lst.push_back((int)J);
-            last[J] = (int)I;
-            ++ntc[J];
-            nupd += J - std::max(c->first_h[I], c->first_h[J]);
+    // ordering + symbolic factorisation of the Schur matrix (plan.cu): interface_mode 0 picks the
+    // ordering with less factorisation work, 1 / 2 the strip (envelope) order, 3 nested dissection
+    std::vector<std::pair<int, int>> fpairs;
+    fpairs.reserve(pairs.size());
+    for (auto& kv : pairs) fpairs.push_back(kv.first);
+    const int mode = c->cfg.interface_mode;
+    if (mode == 3) {
+        build_chol_plan(P, q, F, fpairs, 1, c->crit_band, c->plan);
+    } else {
+        build_chol_plan(P, q, F, fpairs, 0, c->crit_band, c->plan);
+        if (mode == 0 && P >= 3) {
+            CholPlan nd;
+            build_chol_plan(P, q, F, fpairs, 1, c->crit_band, nd);
+            if (nd.nupd < c->plan.nupd) c->plan = std::move(nd);
         }
     }
-    std::vector<int> tasks(crit);
-    tasks.insert(tasks.end(), reg.begin(), reg.end());
-    c->ncrit = (int)(crit.size() / 2);
-    c->ntasks = (int)(tasks.size() / 2);
-    c->chol_flops = nupd * 2 * (int64_t)ELM_NB * ELM_NB * ELM_NB;
-    c->tasks_h = tasks;
-    c->sz.chol_tasks = c->ntasks;
+    const CholPlan& pl = c->plan;
+    const int nblk = pl.nblk;
+    c->sz.band_ld = ELM_TLD;
+    c->sz.band_nbw = nblk - 1;
+    c->sz.band_elems = (int64_t)pl.ntiles * ELM_TS;
+    c->sz.chol_n = pl.n;
+    c->sz.chol_blocks = nblk;
+    c->sz.chol_ordering = pl.ordering;
+    c->ncrit = pl.ncrit;
+    c->chol_flops = pl.nupd * 2 * (int64_t)ELM_NB * ELM_NB * ELM_NB;
+    c->sz.chol_tasks = (int64_t)pl.tasks.size();
     c->sz.chol_flops = c->chol_flops;
 
     c->qrow_ld = q;
@@ -239,18 +215,19 @@ elmddm_status build_tables(elmddm_ctx* c) {
     if ((e = upload(&c->d_terms, terms)) != cudaSuccess) return cuda_fail(c, e, "upload");
     if ((e = upload(&c->d_gterm_ptr, gptr)) != cudaSuccess) return cuda_fail(c, e, "upload");
     if ((e = upload(&c->d_gterms, gterms)) != cudaSuccess) return cuda_fail(c, e, "upload");
-    if ((e = upload(&c->d_first, c->first_h)) != cudaSuccess) return cuda_fail(c, e, "upload");
-    if ((e = upload(&c->d_last, last)) != cudaSuccess) return cuda_fail(c, e, "upload");
-    if ((e = upload(&c->d_tasks, tasks)) != cudaSuccess) return cuda_fail(c, e, "upload");
-    if ((e = upload(&c->d_ntc, ntc)) != cudaSuccess) return cuda_fail(c, e, "upload");
+    if ((e = upload(&c->d_fbase, pl.fbase)) != cudaSuccess || (e = upload(&c->d_pad, pl.pad)) != cudaSuccess ||
+        (e = upload(&c->d_tile_map, pl.tile_map)) != cudaSuccess || (e = upload(&c->d_tasks, pl.tasks)) != cudaSuccess ||
+        (e = upload(&c->d_klist, pl.klist)) != cudaSuccess || (e = upload(&c->d_diag_tid, pl.diag_tid)) != cudaSuccess ||
+        (e = upload(&c->d_fwd_ptr, pl.fwd_ptr)) != cudaSuccess || (e = upload(&c->d_fwd, pl.fwd)) != cudaSuccess ||
+        (e = upload(&c->d_bwd_ptr, pl.bwd_ptr)) != cudaSuccess || (e = upload(&c->d_bwd, pl.bwd)) != cudaSuccess ||
+        (e = upload(&c->d_ntc, pl.ntc)) != cudaSuccess)
+        return cuda_fail(c, e, "upload");
     if ((e = cudaMalloc((void**)&c->d_colcnt, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMemset(c->d_colcnt, 0, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMalloc((void**)&c->d_cready, sizeof(int) * nblk)) != cudaSuccess ||
-        (e = cudaMemset(c->d_cready, 0, sizeof(int) * nblk)) != cudaSuccess)
-        return cuda_fail(c, e, "colcnt");
-    const size_t nflags = (size_t)nblk * (size_t)(nbw + 1);
-    if ((e = cudaMalloc((void**)&c->d_cflags, sizeof(int) * nflags)) != cudaSuccess ||
-        (e = cudaMemset(c->d_cflags, 0, sizeof(int) * nflags)) != cudaSuccess)
+        (e = cudaMemset(c->d_cready, 0, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&c->d_cflags, sizeof(int) * std::max(pl.ntiles, 1))) != cudaSuccess ||
+        (e = cudaMemset(c->d_cflags, 0, sizeof(int) * std::max(pl.ntiles, 1))) != cudaSuccess)
         return cuda_fail(c, e, "flags");
     return ELMDDM_OK;
 }
@@ -341,13 +318,13 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB);
     c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
                                                           (int64_t)c->ga_ld * c->qrow_cols),
-                                      z.G_pad + 2 * (z.G_pad / ELM_NB) * ELM_TS);  // z + packed inverse diagonal tiles + C(I,I-1)
+                                      5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16);
     c->work_back = z.S * z.ld;
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
         (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess ||
-        (e = cudaMalloc((void**)&c->d_flags, sizeof(int) * (z.G_pad / ELM_NB + 1))) != cudaSuccess ||
-        (e = cudaMemset(c->d_flags, 0, sizeof(int) * (z.G_pad / ELM_NB + 1))) != cudaSuccess) {
+        (e = cudaMalloc((void**)&c->d_flags, sizeof(int) * (z.chol_blocks + 1))) != cudaSuccess ||
+        (e = cudaMemset(c->d_flags, 0, sizeof(int) * (z.chol_blocks + 1))) != cudaSuccess) {
         elmddm_destroy(c);
         return ELMDDM_ECUDA;
     }
@@ -375,8 +352,15 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_terms);
     cudaFree(c->d_gterm_ptr);
     cudaFree(c->d_gterms);
-    cudaFree(c->d_first);
-    cudaFree(c->d_last);
+    cudaFree(c->d_fbase);
+    cudaFree(c->d_pad);
+    cudaFree(c->d_tile_map);
+    cudaFree(c->d_klist);
+    cudaFree(c->d_diag_tid);
+    cudaFree(c->d_fwd_ptr);
+    cudaFree(c->d_fwd);
+    cudaFree(c->d_bwd_ptr);
+    cudaFree(c->d_bwd);
     cudaFree(c->d_tasks);
     cudaFree(c->d_cflags);
     cudaFree(c->d_colcnt);
@@ -394,18 +378,31 @@ elmddm_status elmddm_sizes(const elmddm_ctx* c, elmddm_sizes_t* out) {
     return ELMDDM_OK;
 }
 
-elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* first, int32_t* tasks) {
+elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* newidx, int32_t* tile_map, int32_t* tasks) {
     CHECK_CTX(c);
-    if (!first || !tasks) return ELMDDM_EINVAL;
-    std::copy(c->first_h.begin(), c->first_h.end(), first);
-    std::copy(c->tasks_h.begin(), c->tasks_h.end(), tasks);
+    const CholPlan& pl = c->plan;
+    const int q = c->cfg.q;
+    if (newidx)
+        for (int64_t f = 0; f < c->faces; ++f)
+            for (int k = 0; k < q; ++k) newidx[f * q + k] = pl.fbase[f] + k;
+    if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
+    if (tasks)
+        for (size_t t = 0; t < pl.tasks.size(); ++t) {
+            tasks[2 * t] = pl.tasks[t].I;
+            tasks[2 * t + 1] = pl.tasks[t].J;
+        }
     return ELMDDM_OK;
 }
 
 int64_t elmddm_band_index(const elmddm_ctx* c, int64_t i, int64_t j) {
-    if (!c) return -1;
-    if (i < j || i - j > c->sz.halfband || i >= c->sz.G_pad) return -1;
-    return band_off(i, j, c->sz.band_nbw);
+    if (!c || i < 0 || j < 0 || i >= c->sz.G || j >= c->sz.G) return -1;
+    const CholPlan& pl = c->plan;
+    const int q = c->cfg.q;
+    int64_t a = pl.fbase[i / q] + i % q, b = pl.fbase[j / q] + j % q;
+    if (a < b) std::swap(a, b);
+    const int t = pl.tile_map[(size_t)(a / ELM_NB) * pl.nblk + b / ELM_NB];
+    if (t < 0) return -1;
+    return (int64_t)t * ELM_TS + a % ELM_NB + (b % ELM_NB) * (int64_t)ELM_TLD;
 }
 
 elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/elmddm.h"
@@ -13,15 +14,9 @@
 #define ELM_TLD 68     // column stride inside a packed 64 x 64 tile of the Schur matrix (== 4 mod 16)
 #define ELM_TS (ELM_NB * ELM_TLD)  // doubles per packed tile
 
-// Packed envelope storage of the Schur matrix: tile (I, J), 0 <= I - J <= nbw, is
-// stored contiguously at tile_off(I, J) with element (r, c) at r + c * ELM_TLD, so one bulk copy
-// reproduces the conflict-free padded shared-memory layout of the DMMA kernels.
-__host__ __device__ __forceinline__ int64_t tile_off(int64_t I, int64_t J, int64_t nbw) {
-    return (I * (nbw + 1) + (I - J)) * (int64_t)ELM_TS;
-}
-__host__ __device__ __forceinline__ int64_t band_off(int64_t i, int64_t j, int64_t nbw) {
-    return tile_off(i / ELM_NB, j / ELM_NB, nbw) + (i % ELM_NB) + (j % ELM_NB) * (int64_t)ELM_TLD;
-}
+// Packed tile storage of the Schur matrix: tile t of the factor's tile structure
+// (CholPlan::tile_map) is stored contiguously at t * ELM_TS with element (r, c) at r + c * ELM_TLD,
+// so one bulk copy reproduces the conflict-free padded shared-memory layout of the DMMA kernels.
 
 // Device status word: [0] error code (ELMDDM_ENUMERIC), [1] info (column / index).
 struct ElmStatus {
@@ -36,6 +31,30 @@ struct FaceTerm {
     int r0;    // row offset inside the source block
     int c0;    // column offset inside the source block
 };
+
+// one tile task of the interface Cholesky (plan.cu / chol.cu)
+struct TaskDesc {
+    int I, J;        // tile of L
+    int tid;         // its tile id (offset tid * ELM_TS in the tile pool)
+    int kbeg, kend;  // its update list klist[kbeg, kend)
+    int klast;       // diagonal tasks: the last update column (applied by the task itself), or -1
+    int pub;         // publish C(I, J) for the diagonal task of row I (J == klast(I))
+    int pad_;
+};
+
+// ordering and symbolic factorisation of the interface Schur matrix at 64-tile granularity
+struct CholPlan {
+    int ordering = 0;                 // 0 strip (envelope), 1 nested dissection
+    int64_t n = 0;                    // unknowns in the factorisation order (multiple of 64)
+    int nblk = 0, ntiles = 0, ncrit = 0;
+    int64_t nupd = 0;                 // tile updates (work = 2 * 64^3 * nupd)
+    std::vector<int> fbase, pad, tile_map, diag_tid, ntc, fwd_ptr, bwd_ptr;
+    std::vector<TaskDesc> tasks;      // critical band first, then the rest; each column by column
+    std::vector<int4> klist;
+    std::vector<int2> fwd, bwd;
+};
+int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
+                        int crit_band, CholPlan& pl);
 
 struct elmddm_ctx {
     elmddm_config cfg;
@@ -78,20 +97,25 @@ struct elmddm_ctx {
     int panel_cluster = 0;  // QR panel blocks on 4-CTA clusters (default for S <= 48; ELMDDM_PANEL_CLUSTER)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
     mutable int trsv_epoch = 0;
-    // envelope (skyline) of the Schur matrix at 64-tile granularity and the factorisation task list
-    std::vector<int> first_h;        // [nblk] first structurally nonzero tile column of tile row I
-    int* d_first = nullptr;          // [nblk]
-    int* d_last = nullptr;           // [nblk] last tile row I with first[I] <= J
-    int* d_tasks = nullptr;          // [ntasks][2] (I, J), column by column
-    std::vector<int> tasks_h;
-    int ntasks = 0;
+    // ordering + symbolic factorisation of the Schur matrix (plan.cu) and its device copies
+    CholPlan plan;
     int ncrit = 0;                   // the first ncrit tasks are the critical band (I - J <= crit_band)
     int crit_band = 3;               // ELMDDM_CHOL_CRITBAND
-    int64_t chol_flops = 0;          // envelope Cholesky work: 2 * 64^3 per tile update
-    int* d_cflags = nullptr;         // [nblk][nbw + 1] per-tile completion flags of the factorisation
+    int64_t chol_flops = 0;          // 2 * 64^3 per tile update
+    int* d_fbase = nullptr;          // [faces] first unknown of each face in the factorisation order
+    int* d_pad = nullptr;            // [npad] padding unknowns (unit diagonal, zero right-hand side)
+    int* d_tile_map = nullptr;       // [nblk * nblk] tile id of (I, J), I >= J, or -1
+    TaskDesc* d_tasks = nullptr;     // [ntasks]
+    int4* d_klist = nullptr;         // [nupd] (tile (I,k), tile (J,k), k, 0)
+    int* d_diag_tid = nullptr;       // [nblk]
+    int* d_fwd_ptr = nullptr;        // [nblk + 1] CSR of the forward-solve dependencies
+    int2* d_fwd = nullptr;           // (j, tile (i, j)), ascending j
+    int* d_bwd_ptr = nullptr;        // [nblk + 1] CSR of the backward-solve dependencies
+    int2* d_bwd = nullptr;           // (j, tile (j, i)), descending j
+    int* d_cflags = nullptr;         // [ntiles] per-tile completion flags of the factorisation
     int* d_colcnt = nullptr;         // [nblk] finished tiles of column J (summed over factorisations)
-    int* d_ntc = nullptr;            // [nblk] tiles of column J in the envelope
-    int* d_cready = nullptr;         // [nblk] C(I, I-1) published for the diagonal task of column I
+    int* d_ntc = nullptr;            // [nblk] tiles of column J
+    int* d_cready = nullptr;         // [nblk] C(I, klast(I)) published for the diagonal task of row I
     mutable int chol_epoch = 0;
     mutable std::vector<cudaStream_t> gstreams;
     mutable cudaEvent_t ev_fork = nullptr;

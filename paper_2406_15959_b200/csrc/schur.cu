@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "tma.cuh"
 
@@ -46,7 +48,8 @@ __global__ void k_qrow(const double* __restrict__ Pbuf, int64_t pstride, int64_t
 __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restrict__ pair_bc,
                             const FaceTerm* __restrict__ terms, const double* __restrict__ Sbuf, int64_t sstride,
                             int64_t sld, const double* __restrict__ Ga, int64_t gstride, int64_t gld, int q,
-                            double* __restrict__ Mband, int64_t nbw) {
+                            double* __restrict__ Mband, const int* __restrict__ fbase,
+                            const int* __restrict__ tile_map, int nblk) {
     const int p = blockIdx.x;
     const int b = pair_bc[2 * p], c = pair_bc[2 * p + 1];
     const int t0 = pair_ptr[p], t1 = pair_ptr[p + 1];
@@ -63,7 +66,15 @@ __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restr
             }
             else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * gld];
         }
-        Mband[band_off((int64_t)b * q + i, (int64_t)c * q + j, nbw)] = v;
+        // element (b q + i, c q + j) at (a, d) of the factorisation order, lower triangle
+        int a = fbase[b] + i, d = fbase[c] + j;
+        if (a < d) {
+            const int t = a;
+            a = d;
+            d = t;
+        }
+        const int tile = tile_map[(int64_t)(a / ELM_NB) * nblk + d / ELM_NB];
+        Mband[(int64_t)tile * ELM_TS + a % ELM_NB + (d % ELM_NB) * ELM_TLD] = v;
     }
 }
 
@@ -83,11 +94,15 @@ __global__ void k_gassemble(const int* __restrict__ gptr, const FaceTerm* __rest
     }
 }
 
-__global__ void k_pad(double* Mband, int64_t nbw, double* g, int64_t G, int64_t G_pad) {
-    int64_t i = G + blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= G_pad) return;
-    Mband[band_off(i, i, nbw)] = 1.0;
-    g[i] = 0.0;
+// padding unknowns of the factorisation order: unit diagonal; g beyond G (strip order): zero
+__global__ void k_pad(double* Mband, const int* __restrict__ pad, int npad, const int* __restrict__ diag_tid,
+                      double* g, int64_t G, int64_t G_pad) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < npad) {
+        const int pidx = pad[x];
+        Mband[(int64_t)diag_tid[pidx / ELM_NB] * ELM_TS + (pidx % ELM_NB) * (1 + ELM_TLD)] = 1.0;
+    }
+    if (G + x < G_pad) g[G + x] = 0.0;
 }
 
 // ---- back-solve -----------------------------------------------------------------------------
@@ -376,17 +391,18 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
         { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_massemble<<<(unsigned)c->npairs, 256, 0, st>>>(c->d_pair_ptr, c->d_pair_bc, c->d_terms, Sbuf, sstride,
                                                           c->sz.sbuf_ld, Ga, gstride, c->ga_ld, q, Mband,
-                                                          c->sz.band_nbw); }
+                                                          c->d_fbase, c->d_tile_map, c->plan.nblk); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_gassemble<<<(unsigned)F, 128, 0, st>>>(c->d_gterm_ptr, c->d_gterms, Sbuf, sstride, c->sz.sbuf_ld, Ga,
                                                   gstride, c->ga_ld, q, g); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    const int64_t npad = c->sz.G_pad - c->sz.G;
+    const int64_t npad = std::max<int64_t>((int64_t)c->plan.pad.size(), c->sz.G_pad - c->sz.G);
     if (npad > 0) {
         KTimer kt(c, ELMDDM_K_IFACE, st);
-        k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->sz.band_nbw, g, c->sz.G, c->sz.G_pad);
+        k_pad<<<(unsigned)((npad + 127) / 128), 128, 0, st>>>(Mband, c->d_pad, (int)c->plan.pad.size(), c->d_diag_tid, g,
+                                                              c->sz.G, c->sz.G_pad);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -54,7 +54,7 @@ class Problem:
     init_scheme: int = 0
     init_c: float = 0.125
     r_over_diam: float = 0.5
-    interface_mode: int = 0
+    interface_mode: int = 0             # factorisation order: 0 auto | 1, 2 strip (envelope) | 3 nested dissection
     interface_solver: str = "cholesky"  # "cholesky" (direct, reading R12) | "cg" (the paper's)
     cg_tol: float = 1e-9                # relative residual of the CG solver
 
@@ -182,15 +182,19 @@ class Context:
                 "ms": {k: float(t.ms[i]) for i, k in enumerate(_lib.KCLASSES)}}
 
     def chol_plan(self):
-        """(first[nblk], tasks[chol_tasks][2]) of the envelope factorisation (host arrays)."""
+        """(newidx[G], tile_map[chol_blocks, chol_blocks], tasks[chol_tasks, 2]) of the interface
+        factorisation (host arrays): the factorisation-order index of every interface unknown,
+        the tile id of every tile (I, J) of L (-1 outside its structure) and the task list."""
         import numpy as np
 
         z = self.sizes
-        first = np.zeros(z["G_pad"] // 64, dtype=np.int32)
+        nb = z["chol_blocks"]
+        newidx = np.zeros(max(z["G"], 1), dtype=np.int32)
+        tmap = np.zeros(nb * nb, dtype=np.int32)
         tasks = np.zeros((z["chol_tasks"], 2), dtype=np.int32)
-        self._check(self.L.elmddm_chol_plan(self.h, first.ctypes.data_as(C.c_void_p), tasks.ctypes.data_as(C.c_void_p)),
-                    "chol_plan")
-        return first, tasks
+        self._check(self.L.elmddm_chol_plan(self.h, newidx.ctypes.data_as(C.c_void_p), tmap.ctypes.data_as(C.c_void_p),
+                                            tasks.ctypes.data_as(C.c_void_p)), "chol_plan")
+        return newidx[: z["G"]], tmap.reshape(nb, nb), tasks
 
     def band_index(self, i, j):
         return int(self.L.elmddm_band_index(self.h, i, j))

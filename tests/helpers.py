@@ -80,26 +80,25 @@ def sbuf_np(ctx, buf, s):
     return np.tril(S) + np.tril(S, -1).T
 
 
-def band_offsets(z, i, j):
-    """Offsets of elements (i, j), i >= j, in the packed tile storage of the Schur matrix
-    (include/elmddm.h: tile (I, J) at (I (nbw+1) + I - J) * 64 * band_ld, element (r, c) at r + c band_ld)."""
-    i = np.asarray(i, dtype=np.int64)
-    j = np.asarray(j, dtype=np.int64)
-    nbw, tld = z["band_nbw"], z["band_ld"]
-    I, J = i // 64, j // 64
-    return (I * (nbw + 1) + (I - J)) * 64 * tld + (i % 64) + (j % 64) * tld
+def band_offsets(ctx, i, j):
+    """Offsets of Schur-matrix elements (i, j) (strip order, either triangle) in the packed tile
+    storage (include/elmddm.h elmddm_band_index, vectorised): renumber into the factorisation
+    order, take the lower element, look its tile up."""
+    newidx, tmap, _ = ctx.chol_plan()
+    a, b = newidx[np.asarray(i)], newidx[np.asarray(j)]
+    a, b = np.maximum(a, b).astype(np.int64), np.minimum(a, b).astype(np.int64)
+    tile = tmap[a // 64, b // 64].astype(np.int64)
+    tld = ctx.sizes["band_ld"]
+    return np.where(tile >= 0, tile * 64 * tld + a % 64 + (b % 64) * tld, -1)
 
 
 def band_to_dense(ctx, Mband):
-    """Full symmetric G x G matrix from the band storage (host)."""
-    z = ctx.sizes
-    G, hb = z["G"], z["halfband"]
+    """Full symmetric G x G matrix from the packed tile storage (host; small G only)."""
+    G = ctx.sizes["G"]
     Mb = Mband.cpu().numpy()
-    D = np.zeros((G, G))
-    for j in range(G):
-        i1 = min(G, j + hb + 1)
-        D[j:i1, j] = Mb[band_offsets(z, np.arange(j, i1), j)]
-    return np.tril(D) + np.tril(D, -1).T
+    ii, jj = np.meshgrid(np.arange(G), np.arange(G), indexing="ij")
+    off = band_offsets(ctx, ii.ravel(), jj.ravel())
+    return np.where(off >= 0, Mb[np.maximum(off, 0)], 0.0).reshape(G, G)
 
 
 def rel_l2(a, b):

@@ -154,8 +154,9 @@ def _interface_system(c):
     return ctx, buf, Md, g
 
 
-def test_interface_system_entrywise_config0():
-    c = WL.config(0)
+@pytest.mark.parametrize("mode", [2, 3])
+def test_interface_system_entrywise_config0(mode):
+    c = WL.config(0, interface_mode=mode)
     ctx, buf, Md, g = _interface_system(c)
     W, b, _ = _oracle_init(c)
     r = O.solve(ocfg(c), W, b, want_system=True)
@@ -275,6 +276,10 @@ def test_large_config_sampled_parity(k):
     dict(P=3, M=72, p=11, q=10, problem=2),         # 3 x 3 (interior subdomain with 4 faces)
     dict(P=2, M=8, p=3, q=2, problem=0),            # minimal sizes
     dict(P=4, M=136, p=13, q=14, problem=0, init_scheme=1),
+    dict(P=3, M=72, p=11, q=10, problem=2, interface_mode=3),    # nested dissection, 3 x 3
+    dict(P=5, M=40, p=7, q=10, problem=1, interface_mode=3),     # ND, odd grid, q not dividing 64
+    dict(P=6, M=40, p=7, q=64, problem=0, interface_mode=3),     # ND, q = one tile per face
+    dict(P=4, M=160, p=13, q=70, problem=2, interface_mode=3),   # ND, faces straddling tiles
 ])
 def test_edge_configs_end_to_end(cfgkw):
     c = small(**cfgkw)
@@ -352,35 +357,43 @@ def test_interface_points_export():
 
 
 def _band_matvec(ctx, Mband_copy, u):
-    """y = M u for the symmetric matrix stored lower in packed 64 x 64 tiles (torch, GPU)."""
+    """y = M u for the symmetric matrix stored as the lower tiles of the factorisation structure
+    (tile list and renumbering from elmddm_chol_plan; torch, GPU).  u and y in strip order."""
     import torch
 
     z = ctx.sizes
-    G, nbw, tld, Gp = z["G"], z["band_nbw"], z["band_ld"], z["G_pad"]
-    nblk = Gp // 64
-    T = Mband_copy[: nblk * (nbw + 1) * 64 * tld].view(nblk, nbw + 1, 64, tld)[..., :64]  # [I][d][c][r]
-    U = torch.zeros(Gp, dtype=torch.float64, device=u.device)
-    U[:G] = u
-    U = U.view(nblk, 64)
-    Y = torch.zeros_like(U)
-    for d in range(0, min(nbw, nblk - 1) + 1):
-        Td = T[d:, d]                           # tiles (I, I - d), I = d .. nblk-1: [I][c][r]
-        if d == 0:
-            Td = torch.tril(Td.transpose(1, 2))  # [I][r][c], lower part only
-            Td = Td + torch.tril(Td, -1).transpose(1, 2)
-            Y += torch.einsum("irc,ic->ir", Td, U)
-        else:
-            Y[d:] += torch.einsum("icr,ic->ir", Td, U[: nblk - d])
-            Y[: nblk - d] += torch.einsum("icr,ir->ic", Td, U[d:])
-    return Y.reshape(-1)[:G]
+    G, tld, n = z["G"], z["band_ld"], z["chol_n"]
+    newidx, tmap, _ = ctx.chol_plan()
+    I, J = np.nonzero(tmap >= 0)
+    tid = tmap[I, J]
+    dev = u.device
+    T = Mband_copy[: z["band_elems"]].view(-1, 64, tld)[torch.as_tensor(tid, device=dev, dtype=torch.long), :, :64]
+    T = T.transpose(1, 2)  # [tile][r][c] = element (r, c)
+    nidx = torch.as_tensor(newidx, device=dev, dtype=torch.long)
+    X = torch.zeros(n, dtype=torch.float64, device=dev)
+    X[nidx] = u
+    X = X.view(-1, 64)
+    It = torch.as_tensor(I, device=dev, dtype=torch.long)
+    Jt = torch.as_tensor(J, device=dev, dtype=torch.long)
+    diag = It == Jt
+    Td = torch.tril(T[diag])
+    Td = Td + torch.tril(Td, -1).transpose(1, 2)
+    Y = torch.zeros_like(X)
+    Y.index_add_(0, It[diag], torch.einsum("trc,tc->tr", Td, X[Jt[diag]]))
+    off = ~diag
+    To = T[off]
+    Y.index_add_(0, It[off], torch.einsum("trc,tc->tr", To, X[Jt[off]]))
+    Y.index_add_(0, Jt[off], torch.einsum("trc,tr->tc", To, X[It[off]]))
+    return Y.reshape(-1)[nidx]
 
 
-@pytest.mark.parametrize("k", [2, 3])
-def test_interface_solve_residual_full_size(k):
-    """The band Cholesky solves eqn:schur to rounding: ||M u - g|| <= 1e-11 ||g|| (any size)."""
+@pytest.mark.parametrize("k,mode", [(2, 0), (3, 0), (2, 2), (3, 2), (2, 3), (3, 3)])
+def test_interface_solve_residual_full_size(k, mode):
+    """The tile Cholesky solves eqn:schur to rounding: ||M u - g|| <= 1e-11 ||g|| (any size), in
+    the auto, strip (envelope) and nested-dissection orderings."""
     import torch
 
-    c = WL.config(k)
+    c = WL.config(k, interface_mode=mode)
     ctx, buf, _ = run_gpu(c, upto="schur")
     ctx.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"])
     Mc = buf["Mband"].clone()

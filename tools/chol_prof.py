@@ -27,7 +27,7 @@ ctx.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["wo
 ctx.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"])
 torch.cuda.synchronize()
 L = E._lib.load()
-_, tasks = ctx.chol_plan()
+_, _, tasks = ctx.chol_plan()
 n = len(tasks)
 arr = np.zeros(n * 6, dtype=np.uint64)
 L.elmddm_debug_chol_prof.argtypes = [C.c_void_p, C.c_int]
