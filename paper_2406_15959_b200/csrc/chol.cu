@@ -297,6 +297,7 @@ struct CholArgs {
     const int* ntc;        // [nblk] tiles of column J
     int epoch;
     ElmStatus* status;
+    int* next;             // non-null: tasks dealt dynamically in list order (zeroed counter)
 };
 
 __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
@@ -334,11 +335,21 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         wait_flag(a.flags + e.x, a.epoch, a.status, k);
         wait_flag(a.flags + e.y, a.epoch, a.status, k);
     };
+    // static dealing: CTAs [0, crit_ctas) take the critical list round-robin, the others the
+    // rest; dynamic dealing (a.next): every CTA takes the next task of the (list-scheduled) order
+    // when it is free.  Both deadlock-free: the lists are topological and a CTA holds one task.
+    __shared__ int s_next;
     const bool critw = (int)blockIdx.x < a.crit_ctas;
     const int t_begin = critw ? (int)blockIdx.x : a.ncrit + (int)blockIdx.x - a.crit_ctas;
-    const int t_end = critw ? a.ncrit : a.ntasks;
+    const int t_end = a.next ? a.ntasks : (critw ? a.ncrit : a.ntasks);
     const int t_step = critw ? a.crit_ctas : (int)gridDim.x - a.crit_ctas;
-    for (int t = t_begin; t < t_end; t += t_step) {
+    for (int t = t_begin;; t += t_step) {
+        if (a.next) {
+            if (tid == 0) s_next = atomicAdd(a.next, 1);
+            __syncthreads();
+            t = s_next;
+        }
+        if (t >= t_end) break;
         const TaskDesc td = a.tasks[t];
         const int I = td.I, J = td.J;
         // the diagonal task applies its last update column klast itself: it solves for
@@ -670,7 +681,9 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         if (const char* env = getenv("ELMDDM_CHOL_CRIT")) crit = atoi(env);
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
-                   c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status};
+                   c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
+                   c->chol_sched ? c->d_chol_next : nullptr};
+        if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
         if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=

@@ -190,6 +190,7 @@ elmddm_status build_tables(elmddm_ctx* c) {
             if (nd.nupd < c->plan.nupd) c->plan = std::move(nd);
         }
     }
+    if (c->chol_sched) c->chol_sim_us = schedule_chol_tasks(c->plan, 2 * c->nsm);
     const CholPlan& pl = c->plan;
     const int nblk = pl.nblk;
     c->sz.band_ld = ELM_TLD;
@@ -225,6 +226,7 @@ elmddm_status build_tables(elmddm_ctx* c) {
     if ((e = cudaMalloc((void**)&c->d_colcnt, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMemset(c->d_colcnt, 0, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMalloc((void**)&c->d_cready, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&c->d_chol_next, sizeof(int) * 4)) != cudaSuccess ||
         (e = cudaMemset(c->d_cready, 0, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMalloc((void**)&c->d_cflags, sizeof(int) * std::max(pl.ntiles, 1))) != cudaSuccess ||
         (e = cudaMemset(c->d_cflags, 0, sizeof(int) * std::max(pl.ntiles, 1))) != cudaSuccess)
@@ -293,6 +295,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         c->panel_cluster = S <= 48;
         if (const char* env = getenv("ELMDDM_PANEL_CLUSTER")) c->panel_cluster = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_CHOL_CRITBAND")) c->crit_band = std::max(1, atoi(env));
+        if (const char* env = getenv("ELMDDM_CHOL_SCHED")) c->chol_sched = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));
@@ -365,6 +368,7 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_cflags);
     cudaFree(c->d_colcnt);
     cudaFree(c->d_cready);
+    cudaFree(c->d_chol_next);
     cudaFree(c->d_ntc);
     delete c;
 }

@@ -55,6 +55,8 @@ struct CholPlan {
 };
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
                         int crit_band, CholPlan& pl);
+double schedule_chol_tasks(CholPlan& pl, int workers);
+double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers);
 
 struct elmddm_ctx {
     elmddm_config cfg;
@@ -101,6 +103,9 @@ struct elmddm_ctx {
     CholPlan plan;
     int ncrit = 0;                   // the first ncrit tasks are the critical band (I - J <= crit_band)
     int crit_band = 3;               // ELMDDM_CHOL_CRITBAND
+    int chol_sched = 1;              // ELMDDM_CHOL_SCHED: 1 list-scheduled task order, dynamic dealing
+    double chol_sim_us = 0.0;        // simulated makespan of the scheduled order
+    int* d_chol_next = nullptr;      // dynamic task counter
     int64_t chol_flops = 0;          // 2 * 64^3 per tile update
     int* d_fbase = nullptr;          // [faces] first unknown of each face in the factorisation order
     int* d_pad = nullptr;            // [npad] padding unknowns (unit diagonal, zero right-hand side)
@@ -206,6 +211,8 @@ cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const dou
 cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,
                            double* work, cudaStream_t st);
 
+#ifdef __CUDACC__
 __device__ __forceinline__ void elm_set_status(ElmStatus* st, int code, int info) {
     if (atomicCAS(&st->code, 0, code) == 0) st->info = info;
 }
+#endif

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <functional>
 #include <map>
+#include <queue>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -210,4 +211,147 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
     }
     pl.nupd = nupd;
     return nupd;
+}
+
+// Task order of the persistent factorisation kernel.  The kernel deals tasks to whichever CTA is
+// free, in list order (dynamic counter); a CTA streams the k-list of its task, waiting for each
+// update's tiles only when it reaches them, then waits for the diagonal tile and finishes.  So the
+// list must be topological (deadlock freedom), and a good list starts early what can run early.
+// Column order wastes the tree parallelism of a nested-dissection order: all CTAs wait inside one
+// subtree while the independent subtrees sit further down the list.
+//
+// Model (tools/chol_prof.py medians): one tile update UPD us, epilogue EPI_OFF (refined triangular
+// solve) or EPI_DIAG (Cholesky + inverse of the diagonal tile).  chol_eval() replays a list on
+// `workers` CTAs with exactly the kernel's dealing and waiting rules; schedule_chol_tasks() ranks
+// the tasks by their finish time with unlimited CTAs (as-soon-as-possible streaming schedule),
+// and keeps that order if the replay beats the column order.
+namespace {
+constexpr double UPD = 3.5, EPI_OFF = 10.0, EPI_DIAG = 45.0;
+
+// finish time of task t started at time s, given the finish times of the tasks before it
+double task_finish(const CholPlan& pl, const std::vector<int>& tix, const std::vector<double>& fin, int t, double s) {
+    const TaskDesc& td = pl.tasks[t];
+    double x = s;
+    const bool dsub = td.I == td.J && td.klast >= 0;
+    const int ke = dsub ? td.kend - 1 : td.kend;
+    for (int e = td.kbeg; e < ke; ++e) {
+        const int4 k4 = pl.klist[e];
+        x = std::max(x, std::max(fin[tix[k4.x]], fin[tix[k4.y]])) + UPD;
+    }
+    if (td.I > td.J) return std::max(x, fin[tix[pl.diag_tid[td.J]]]) + EPI_OFF;
+    if (dsub) {  // L(J, klast) from the published C(J, klast): needs that tile's k-sum and L(klast, klast)
+        const int4 k4 = pl.klist[td.kend - 1];
+        x = std::max(x, std::max(fin[tix[k4.x]] - EPI_OFF, fin[tix[pl.diag_tid[td.klast]]])) + EPI_OFF + UPD;
+    }
+    return x + EPI_DIAG;
+}
+}  // namespace
+
+// replay `order` (a permutation of pl.tasks, topological) with dynamic dealing on `workers` CTAs
+double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers) {
+    const int nt = (int)pl.tasks.size();
+    std::vector<int> tix(pl.ntiles, -1);
+    for (int t = 0; t < nt; ++t) tix[pl.tasks[t].tid] = t;
+    std::vector<double> fin(nt, 1e300);
+    std::priority_queue<double, std::vector<double>, std::greater<double>> freeat;
+    for (int w = 0; w < workers; ++w) freeat.push(0.0);
+    double span = 0.0;
+    for (int t : order) {
+        const double s = freeat.top();
+        freeat.pop();
+        fin[t] = task_finish(pl, tix, fin, t, s);
+        freeat.push(fin[t]);
+        span = std::max(span, fin[t]);
+    }
+    return span;
+}
+
+double schedule_chol_tasks(CholPlan& pl, int workers) {
+    const int nt = (int)pl.tasks.size();
+    if (nt == 0 || workers < 1) return 0.0;
+    std::vector<int> tix(pl.ntiles, -1);
+    for (int t = 0; t < nt; ++t) tix[pl.tasks[t].tid] = t;
+    // column order (a topological order: off-diagonal tiles of column J after (J, J))
+    std::vector<int> col(nt);
+    for (int t = 0; t < nt; ++t) col[t] = t;
+    std::stable_sort(col.begin(), col.end(), [&](int x, int y) {
+        const TaskDesc &a = pl.tasks[x], &b = pl.tasks[y];
+        if (a.J != b.J) return a.J < b.J;
+        return (a.I == a.J) > (b.I == b.J);
+    });
+    // dependency graph: the tiles of the k-list, the diagonal tile of column J (off-diagonal
+    // tiles) or of column klast (diagonal tiles)
+    auto for_deps = [&](int t, auto&& f) {
+        const TaskDesc& td = pl.tasks[t];
+        for (int e = td.kbeg; e < td.kend; ++e) {
+            const int4 k4 = pl.klist[e];
+            f(tix[k4.x]);
+            if (k4.y != k4.x) f(tix[k4.y]);
+        }
+        if (td.I > td.J) f(tix[pl.diag_tid[td.J]]);
+        else if (td.klast >= 0) f(tix[pl.diag_tid[td.klast]]);
+    };
+    std::vector<int> ndep(nt, 0), sptr(nt + 1, 0);
+    for (int t = 0; t < nt; ++t) for_deps(t, [&](int d) { ++ndep[t]; ++sptr[d + 1]; });
+    for (int t = 0; t < nt; ++t) sptr[t + 1] += sptr[t];
+    std::vector<int> succ(sptr[nt]), fill(sptr.begin(), sptr.end() - 1);
+    for (int t = 0; t < nt; ++t) for_deps(t, [&](int d) { succ[fill[d]++] = t; });
+    std::vector<double> cost(nt), blev(nt, 0.0);
+    for (int t = 0; t < nt; ++t) {
+        const TaskDesc& td = pl.tasks[t];
+        cost[t] = UPD * (td.kend - td.kbeg) + (td.I == td.J ? EPI_DIAG : EPI_OFF);
+    }
+    for (int i = nt - 1; i >= 0; --i) {  // bottom levels, reverse topological order
+        const int t = col[i];
+        double m = 0.0;
+        for (int j = sptr[t]; j < sptr[t + 1]; ++j) m = std::max(m, blev[succ[j]]);
+        blev[t] = cost[t] + m;
+    }
+    // greedy list construction with the kernel's dealing rule: the earliest-free CTA takes the
+    // next task.  Candidates are the tasks whose dependencies are all dealt (their finish times
+    // known); a candidate is "ready" at r = its stall-free start (finish with an early start minus
+    // its own cost).  Pick the ready task with the longest path to the end, else the one that
+    // gets ready first.
+    using KV = std::pair<double, int>;
+    std::priority_queue<KV, std::vector<KV>, std::greater<KV>> pending;  // (r, task)
+    std::priority_queue<KV> ready;                                        // (bottom level, task)
+    std::priority_queue<double, std::vector<double>, std::greater<double>> freeat;
+    for (int w = 0; w < workers; ++w) freeat.push(0.0);
+    std::vector<double> fin(nt, 1e300);
+    std::vector<int> left(ndep), ord;
+    ord.reserve(nt);
+    for (int t = 0; t < nt; ++t)
+        if (left[t] == 0) pending.push({0.0, t});
+    double span = 0.0;
+    while ((int)ord.size() < nt) {
+        const double s = freeat.top();
+        freeat.pop();
+        while (!pending.empty() && pending.top().first <= s) {
+            ready.push({blev[pending.top().second], pending.top().second});
+            pending.pop();
+        }
+        int t;
+        if (!ready.empty()) {
+            t = ready.top().second;
+            ready.pop();
+        } else {
+            t = pending.top().second;
+            pending.pop();
+        }
+        fin[t] = task_finish(pl, tix, fin, t, s);
+        span = std::max(span, fin[t]);
+        freeat.push(fin[t]);
+        ord.push_back(t);
+        for (int j = sptr[t]; j < sptr[t + 1]; ++j) {
+            const int u = succ[j];
+            if (--left[u] == 0) pending.push({std::max(0.0, task_finish(pl, tix, fin, u, 0.0) - cost[u]), u});
+        }
+    }
+    const double t_col = chol_eval(pl, col, workers);
+    const std::vector<int>& best = span <= t_col ? ord : col;
+    std::vector<TaskDesc> nl(nt);
+    for (int t = 0; t < nt; ++t) nl[t] = pl.tasks[best[t]];
+    pl.tasks.swap(nl);
+    pl.ncrit = 0;
+    return std::min(span, t_col);
 }

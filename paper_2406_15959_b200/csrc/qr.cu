@@ -37,6 +37,7 @@ struct PanelArgs {
     int j0;        // panel start column
     int blk;       // base block index inside the panel
     int s_off;     // first local subdomain of this launch (subdomain groups on separate streams)
+    int ring;      // doubles of the V_prev ring (k_panel_block)
 };
 
 // block-wide deterministic sum of NV values per thread; result broadcast in tot[0..NV)
@@ -66,16 +67,16 @@ __device__ __forceinline__ void dmma8(double& c0, double& c1, double a, double b
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-constexpr int RED_ELEMS = 2 * 56 * 36; // 2-stage ring of V_prev chunks (also T staging / reduction scratch)
-constexpr int RSTAGE = RED_ELEMS / 2;   // doubles per ring stage
+constexpr int RED_ELEMS = 2 * 56 * 36; // minimum V_prev ring (also T staging / reduction scratch)
+constexpr int VNS = 4;                  // ring stages (VNS - 1 chunks in flight)
 
-// rows per staged chunk of V_prev for kp columns: as many 32-row groups as fit in one ring stage
-// with the padded stride rch + 4 (== 4 mod 16: conflict-free fragments), at most 224.  Small kp
-// (the first base blocks of a panel) thus stream in a few large chunks instead of R/32 small ones
-// (each chunk costs about one L2 round trip).
-__device__ __forceinline__ int vp_rows(int kp) {
-    const int r = ((RSTAGE / kp - 4) / 32) * 32;
-    return r < 32 ? 32 : (r > 224 ? 224 : r);
+// rows per staged chunk of V_prev for kp columns in a ring stage of sst doubles: as many 16-row
+// groups as fit with the padded stride rch + 4 (== 4 mod 16: conflict-free fragments).  The ring
+// takes whatever shared memory the resident block leaves (PanelArgs::ring), so late panels
+// (short blocks) stream V_prev in large chunks with VNS - 1 of them in flight.
+__device__ __forceinline__ int vp_rows(int kp, int sst) {
+    const int r = ((sst / kp - 4) / 16) * 16;
+    return r < 16 ? 16 : r;
 }
 
 // stage rows [c*rch, c*rch + nr) of V_prev columns [0, kp) into dst[col*(rch+4) + row] (16 B cp.async)
@@ -87,28 +88,44 @@ __device__ __forceinline__ void vp_chunk(double* dst, const double* __restrict__
         unsigned d = (unsigned)__cvta_generic_to_shared(dst + col * rcp + r);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Vp + (int64_t)col * ld + c * rch + r));
     }
-    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// Stream rows [0, R) of V_prev (kp columns) through the VNS-stage ring; consume(st, c, rch, nr)
+// is called by every thread for each chunk once it is resident (stage layout st[col*(rch+4)+row]).
+// One __syncthreads per chunk: it publishes chunk c and frees the stage chunk c + VNS - 1 refills.
+template <class F>
+__device__ __forceinline__ void vp_stream(const double* __restrict__ Vp, int64_t ld, int R, int kp, double* ring,
+                                          int sst, F&& consume) {
+    const int rch = vp_rows(kp, sst);
+    const int nch = (R + rch - 1) / rch;
+#pragma unroll
+    for (int i = 0; i < VNS - 1; ++i) {
+        if (i < nch) vp_chunk(ring + i * sst, Vp, ld, kp, rch, i, min(rch, R - i * rch));
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(VNS - 2));
+        __syncthreads();
+        const int cn = c + VNS - 1;
+        if (cn < nch) vp_chunk(ring + (cn % VNS) * sst, Vp, ld, kp, rch, cn, min(rch, R - cn * rch));
+        asm volatile("cp.async.commit_group;\n" ::);
+        consume(ring + (c % VNS) * sst, c, rch, min(rch, R - c * rch));
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
 }
 
 // G (kp x 8, column-major ld kp) = Vp^T X on the FP64 tensor pipe, V_prev streamed through the
-// ring in coalesced chunks of vp_rows(kp) rows.  Warp w owns m-tile w/2 (8 columns of V_prev) and
-// the k-steps of parity w%2 in every chunk; the two parities are summed at the end (fixed order).
+// ring.  Warp w owns m-tile w/2 (8 columns of V_prev) and the k-steps of parity w%2 in every
+// chunk; the two parities are summed at the end (fixed order).
 __device__ void vt_block(const double* __restrict__ Vp, int64_t ld, int R, int kp, const double* X, int RP, double* G,
-                         double* ring, double* pairbuf) {
+                         double* ring, int sst, double* pairbuf) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
     const int kr = lane & 3, cn = lane >> 2;
-    const int rch = vp_rows(kp), rcp = rch + 4;
-    const int nch = (R + rch - 1) / rch;
     double a0 = 0.0, a1 = 0.0;
-    vp_chunk(ring, Vp, ld, kp, rch, 0, min(rch, R));
-    for (int c = 0; c < nch; ++c) {
-        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * RSTAGE, Vp, ld, kp, rch, c + 1, min(rch, R - (c + 1) * rch));
-        else asm volatile("cp.async.commit_group;\n" ::);
-        asm volatile("cp.async.wait_group 1;\n" ::);
-        __syncthreads();
-        const double* st = ring + (c & 1) * RSTAGE;
-        const int nq = min(rch, R - c * rch) / 8;
+    vp_stream(Vp, ld, R, kp, ring, sst, [&](const double* st, int c, int rch, int nr) {
+        const int rcp = rch + 4, nq = nr / 8;
         if (t < mtiles) {
 #pragma unroll 4
             for (int q = 0; q < nq; ++q) {
@@ -116,8 +133,7 @@ __device__ void vt_block(const double* __restrict__ Vp, int64_t ld, int R, int k
                 dmma8(a0, a1, st[(t * 8 + cn) * rcp + kk], X[cn * RP + c * rch + kk]);
             }
         }
-        __syncthreads();
-    }
+    });
     if (t < mtiles && par == 1) {
         pairbuf[t * 64 + lane * 2] = a0;
         pairbuf[t * 64 + lane * 2 + 1] = a1;
@@ -143,8 +159,9 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     double* Cb = sm;                  // [8][RP]
     double* Wsm = Cb + 8 * RP;        // [8][kp]  (<= 8*56)
     double* Zsm = Wsm + 8 * 56;       // [8][kp]
-    double* red = Zsm + 8 * 56;       // RED_ELEMS
-    double* tot = red + RED_ELEMS;    // [40]
+    double* red = Zsm + 8 * 56;       // a.ring doubles: V_prev ring / T staging / reduction scratch
+    double* tot = red + a.ring;       // [40]
+    const int sst = (a.ring / VNS) & ~1;
     double* Tbb = tot + 40;           // [8][8]
     double* taus = Tbb + 64;          // [8]
 
@@ -175,7 +192,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
 
     if (kp > 0) {
         // W = Vp^T Cb
-        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, Zsm);
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, sst, Zsm);
         __syncthreads();
         PSTAMP(2);
         // T (kp x kp, upper) -> smem (reuse the reduction scratch), Z = T^T W
@@ -203,16 +220,8 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
 #pragma unroll
             for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
             // V_prev streamed through the ring; the 8-row m-tiles of a chunk are dealt to the warps
-            const int rch = vp_rows(kp), rcp = rch + 4;
-            const int nch = (R + rch - 1) / rch;
-            vp_chunk(red, Vp, ld, kp, rch, 0, min(rch, R));
-            for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) vp_chunk(red + ((c + 1) & 1) * RSTAGE, Vp, ld, kp, rch, c + 1, min(rch, R - (c + 1) * rch));
-                else asm volatile("cp.async.commit_group;\n" ::);
-                asm volatile("cp.async.wait_group 1;\n" ::);
-                __syncthreads();
-                const double* st = red + (c & 1) * RSTAGE;
-                const int nmt = min(rch, R - c * rch) / 8;
+            vp_stream(Vp, ld, R, kp, red, sst, [&](const double* st, int c, int rch, int nr) {
+                const int rcp = rch + 4, nmt = nr / 8;
                 for (int mt = warp; mt < nmt; mt += PNW) {
                     const int r0 = c * rch + mt * 8;
                     double c0 = Cb[(2 * kr) * RP + r0 + rn], c1 = Cb[(2 * kr + 1) * RP + r0 + rn];
@@ -222,8 +231,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
                     Cb[(2 * kr) * RP + r0 + rn] = c0;
                     Cb[(2 * kr + 1) * RP + r0 + rn] = c1;
                 }
-                __syncthreads();
-            }
+            });
         }
         __syncthreads();
         PSTAMP(4);
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
     }
     // T[0:kp+8, kp:kp+8]
     if (kp > 0) {
-        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, Zsm);  // Gx = Vp^T Vb   (kp x 8)
+        vt_block(Vp, ld, R, kp, Cb, RP, Wsm, red, sst, Zsm);  // Gx = Vp^T Vb   (kp x 8)
         __syncthreads();
         PSTAMP(9);
         // Y = Gx Tbb (kp x 8)
@@ -810,10 +818,13 @@ __device__ void vt_block_cl(const double* __restrict__ Vp, int64_t ld, int nr, i
     const int rch = vp_rows_cl(kp), rcp = rch + 4;
     const int nch = (nr + rch - 1) / rch;
     double a0 = 0.0, a1 = 0.0;
-    if (nch > 0) vp_chunk(ring, Vp, ld, kp, rch, 0, min(rch, nr));
+    if (nch > 0) {
+        vp_chunk(ring, Vp, ld, kp, rch, 0, min(rch, nr));
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
     for (int c = 0; c < nch; ++c) {
         if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * pcl::STG, Vp, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
-        else asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 1;\n" ::);
         __syncthreads();
         const double* st = ring + (c & 1) * pcl::STG;
@@ -932,10 +943,13 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
             __syncthreads();  // Ts (ring) no longer read
             const int rch = vp_rows_cl(kp), rcp = rch + 4;
             const int nch = (nr + rch - 1) / rch;
-            if (nch > 0) vp_chunk(ring, Vz, ld, kp, rch, 0, min(rch, nr));
+            if (nch > 0) {
+                vp_chunk(ring, Vz, ld, kp, rch, 0, min(rch, nr));
+                asm volatile("cp.async.commit_group;\n" ::);
+            }
             for (int c = 0; c < nch; ++c) {
                 if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * STG, Vz, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
-                else asm volatile("cp.async.commit_group;\n" ::);
+                asm volatile("cp.async.commit_group;\n" ::);
                 asm volatile("cp.async.wait_group 1;\n" ::);
                 __syncthreads();
                 const double* st = ring + (c & 1) * STG;
@@ -1135,7 +1149,13 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
     cl.sync();  // no CTA leaves while others may still write into its shared memory
 }
 
-size_t panel_smem_bytes(int64_t R) { return (size_t)(8 * (R + 4) + 8 * 56 * 2 + RED_ELEMS + 40 + 64 + 8) * 8; }
+constexpr int PANEL_FIXED = 8 * 56 * 2 + 40 + 64 + 8;  // Wsm, Zsm, tot, Tbb, taus (doubles)
+// V_prev ring of the panel-block kernel for R resident rows: all shared memory the block leaves
+int panel_ring(int64_t R, int smem_optin) {
+    const int64_t r = ((int64_t)smem_optin / 8 - 8 * (R + 4) - PANEL_FIXED) & ~(int64_t)(2 * VNS - 1);
+    return (int)std::max<int64_t>(r, RED_ELEMS);
+}
+size_t panel_smem_bytes(int64_t R, int ring) { return (size_t)(8 * (R + 4) + PANEL_FIXED + ring) * 8; }
 
 }  // namespace
 
@@ -1169,9 +1189,13 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     const int M = c->cfg.M;
     double* Vbuf = work;
     double* Tbuf = Vbuf + S * ELM_NB * ld;
-    const size_t smax = panel_smem_bytes(ld);
-    cudaError_t e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
+    const size_t smax = panel_smem_bytes(ld, panel_ring(ld, optin));
+    if ((e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)) != cudaSuccess)
+        return e;
     if ((e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)panel_cl_smem(((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32))) != cudaSuccess)
         return e;
@@ -1201,13 +1225,14 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     }
     for (int j0 = 0; j0 < M; j0 += ELM_NB) {
         const int nb = (M - j0) < ELM_NB ? (M - j0) : ELM_NB;
-        const size_t smem = panel_smem_bytes(ld - j0);
+        const int ring = panel_ring(ld - j0, optin);
+        const size_t smem = panel_smem_bytes(ld - j0, ring);
         const size_t smem_cl = panel_cl_smem(((ld - j0 + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32);
         const int n_tr = (int)(ncols - (j0 + nb));
         for (int g = 0; g < ngroups; ++g) {
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
             if (g1 <= g0) continue;
-            PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0};
+            PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0, ring};
             for (int blk = 0; blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);

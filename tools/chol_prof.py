@@ -53,13 +53,19 @@ print(f"idle between tasks {gaps / ncta:.0f} us/CTA")
 diag = {int(j): i for i, (ii, j) in enumerate(zip(I, J)) if ii == j}
 nb = int(J.max()) + 1
 dend = np.array([en[diag[j]] for j in range(nb)])
-print("frontier (diag end) at columns 0,10%,..,100%:", [round(float(dend[int(f * (nb - 1))]), 0) for f in np.linspace(0, 1, 11)])
-steps = np.diff(dend)
-print(f"per-column frontier step: median {np.median(steps):.1f} us, mean {steps.mean():.1f} us")
-# critical chain of a middle column: diag(J-1) end -> tile (J, J-1) end -> diag J epilogue start -> diag J end
-for j in [nb // 4, nb // 2, 3 * nb // 4]:
+srt = np.sort(dend)
+print("diag ends sorted at 0,10%,..,100%:", [round(float(srt[int(f * (nb - 1))]), 0) for f in np.linspace(0, 1, 11)])
+print("last 64 columns: diag end (us):", [round(float(x)) for x in dend[-64:]])
+steps = np.diff(dend[-64:])
+print(f"last-64 frontier step: median {np.median(steps):.1f} us, mean {steps.mean():.1f} us")
+ntask_col = np.bincount(J, minlength=nb)
+print("tasks per column (last 64):", ntask_col[-64:].tolist())
+# critical chain of a column: tile (j, j-1) when it exists
+for j in [nb // 4, nb // 2, 3 * nb // 4, nb - 30, nb - 2]:
     sub = {(int(x), int(y)): i for i, (x, y) in enumerate(zip(I, J)) if y in (j - 1, j) and x <= j}
     t1 = sub.get((j, j - 1))
+    if t1 is None:
+        continue
     d0, d1 = diag[j - 1], diag[j]
     print(f"col {j}: diag{j-1} end {en[d0]:.1f}; tile({j},{j-1}) start {st[t1]:.1f} epi {ep[t1]:.1f} end {en[t1]:.1f} "
           f"(flagwait {fw[t1]:.1f}); diag{j} start {st[d1]:.1f} epi {ep[d1]:.1f} end {en[d1]:.1f} (flagwait {fw[d1]:.1f} datawait {dw[d1]:.1f})")
