@@ -294,8 +294,13 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         // 38.9 -> 28.0 ms, 16: 30.9 -> 18.9 ms) and lose for large ones (256: 174 -> 211 ms)
         c->panel_cluster = S <= 48;
         if (const char* env = getenv("ELMDDM_PANEL_CLUSTER")) c->panel_cluster = atoi(env) != 0;
+        // on-chip 8-CTA cluster panels (whole panel in distributed shared memory, right-looking):
+        // shortest per-subdomain chain, most SM time per panel -- the choice for small slabs
+        // (config 3, 32 subdomains: QR 27.8 -> 26.6 ms, 16: 18.7 -> 14.9 ms; 256: 174 -> 203 ms)
+        c->panel8 = S <= 48;
         if (const char* env = getenv("ELMDDM_CHOL_CRITBAND")) c->crit_band = std::max(1, atoi(env));
         if (const char* env = getenv("ELMDDM_CHOL_SCHED")) c->chol_sched = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_PANEL8")) c->panel8 = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));

@@ -49,6 +49,7 @@ struct CholPlan {
     int nblk = 0, ntiles = 0, ncrit = 0;
     int64_t nupd = 0;                 // tile updates (work = 2 * 64^3 * nupd)
     std::vector<int> fbase, pad, tile_map, diag_tid, ntc, fwd_ptr, bwd_ptr;
+    std::vector<int> blk_depth;       // nested-dissection depth of each tile column (0 = top separator)
     std::vector<TaskDesc> tasks;      // critical band first, then the rest; each column by column
     std::vector<int4> klist;
     std::vector<int2> fwd, bwd;
@@ -103,6 +104,7 @@ struct elmddm_ctx {
     CholPlan plan;
     int ncrit = 0;                   // the first ncrit tasks are the critical band (I - J <= crit_band)
     int crit_band = 3;               // ELMDDM_CHOL_CRITBAND
+    int panel8 = 0;                  // ELMDDM_PANEL8: on-chip 8-CTA cluster panels (qr.cu k_panel_c8)
     int chol_sched = 1;              // ELMDDM_CHOL_SCHED: 1 list-scheduled task order, dynamic dealing
     double chol_sim_us = 0.0;        // simulated makespan of the scheduled order
     int* d_chol_next = nullptr;      // dynamic task counter

@@ -36,8 +36,9 @@ FaceGeo face_geo(int P, int f) {
     return {0, t - (P - 1), j};
 }
 
-// nested-dissection node list (faces of each node, in elimination order)
-void nd_nodes(int P, std::vector<std::vector<int>>& nodes) {
+// nested-dissection node list (faces of each node, in elimination order) and each node's depth
+// in the dissection tree (0 = the top separator)
+void nd_nodes(int P, std::vector<std::vector<int>>& nodes, std::vector<int>& depth) {
     const int F = 2 * P * (P - 1);
     std::vector<int> all(F);
     for (int f = 0; f < F; ++f) all[f] = f;
@@ -46,13 +47,14 @@ void nd_nodes(int P, std::vector<std::vector<int>>& nodes) {
         return std::make_tuple(g.j, g.i, g.vertical);
     };
     auto by_pos = [&](std::vector<int>& v) { std::sort(v.begin(), v.end(), [&](int a, int b) { return key(a) < key(b); }); };
-    std::function<void(std::vector<int>&, int, int, int, int)> rec = [&](std::vector<int>& fs, int i0, int i1, int j0,
-                                                                          int j1) {
+    std::function<void(std::vector<int>&, int, int, int, int, int)> rec = [&](std::vector<int>& fs, int i0, int i1,
+                                                                               int j0, int j1, int dep) {
         if (fs.empty()) return;
         const int w = i1 - i0 + 1, h = j1 - j0 + 1;
         if ((w <= 1 && h <= 1) || fs.size() <= 2) {
             by_pos(fs);
             nodes.push_back(fs);
+            depth.push_back(dep);
             return;
         }
         std::vector<int> sep, L, R;
@@ -63,8 +65,8 @@ void nd_nodes(int P, std::vector<std::vector<int>>& nodes) {
                 const int lo = g.i, hi = g.vertical ? g.i + 1 : g.i;  // subdomain columns touched
                 (hi < cm ? L : (lo > cm ? R : sep)).push_back(f);
             }
-            rec(L, i0, cm - 1, j0, j1);
-            rec(R, cm + 1, i1, j0, j1);
+            rec(L, i0, cm - 1, j0, j1, dep + 1);
+            rec(R, cm + 1, i1, j0, j1, dep + 1);
         } else {
             const int cm = (j0 + j1) / 2;
             for (int f : fs) {
@@ -72,13 +74,14 @@ void nd_nodes(int P, std::vector<std::vector<int>>& nodes) {
                 const int lo = g.j, hi = g.vertical ? g.j : g.j + 1;  // subdomain rows touched
                 (hi < cm ? L : (lo > cm ? R : sep)).push_back(f);
             }
-            rec(L, i0, i1, j0, cm - 1);
-            rec(R, i0, i1, cm + 1, j1);
+            rec(L, i0, i1, j0, cm - 1, dep + 1);
+            rec(R, i0, i1, cm + 1, j1, dep + 1);
         }
         by_pos(sep);
         nodes.push_back(sep);
+        depth.push_back(dep);
     };
-    rec(all, 0, P - 1, 0, P - 1);
+    rec(all, 0, P - 1, 0, P - 1, 0);
 }
 
 }  // namespace
@@ -91,24 +94,34 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
     pl.ordering = ordering;
     // 1. face bases in the new order (+ padding to tile boundaries between ND nodes)
     std::vector<std::vector<int>> nodes;
+    std::vector<int> ndepth;
     if (ordering == 1 && F > 0) {
-        nd_nodes(P, nodes);
+        nd_nodes(P, nodes, ndepth);
     } else {
         nodes.emplace_back(F);
         for (int f = 0; f < F; ++f) nodes[0][f] = f;
+        ndepth.push_back(0);
     }
     pl.fbase.assign(std::max(F, 1), 0);
     int64_t off = 0;
     std::vector<char> used;
+    std::vector<int64_t> node_end;
     for (auto& nd : nodes) {
         for (int f : nd) {
             pl.fbase[f] = (int)off;
             off += q;
         }
         if (ordering == 1) off = (off + T - 1) / T * T;
+        node_end.push_back(off);
     }
     pl.n = std::max<int64_t>((off + T - 1) / T * T, T);
     pl.nblk = (int)(pl.n / T);
+    // dissection depth of every tile column (strip order: all 0)
+    pl.blk_depth.assign(pl.nblk, 0);
+    for (int J = 0, nd = 0; J < pl.nblk; ++J) {
+        while (nd + 1 < (int)node_end.size() && (int64_t)J * T >= node_end[nd]) ++nd;
+        pl.blk_depth[J] = ndepth[nd];
+    }
     used.assign(pl.n, 0);
     for (int f = 0; f < F; ++f)
         for (int k = 0; k < q; ++k) used[pl.fbase[f] + k] = 1;

@@ -1149,6 +1149,414 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
     cl.sync();  // no CTA leaves while others may still write into its shared memory
 }
 
+// ------------------------------------------------------------------------------------------
+// On-chip panel factorisation: one panel (nb <= 64 columns) of one subdomain on a cluster of 8
+// CTAs (8 SMs).  CTA z holds rows [z Rq, (z+1) Rq) of ALL panel columns in shared memory
+// (<= 190 KB at config 3), so the panel is read from and written to HBM once and nothing is
+// streamed.  Right-looking inside the panel by 8-column blocks:
+//   * column j: partial sums (||x||^2 below the diagonal, x . y for the block columns to its
+//     right) over own rows -> ONE cluster all-reduce through distributed shared memory (every CTA
+//     writes its partial into slot z of every CTA's buffer, one cluster barrier, every CTA sums
+//     the slots in the same fixed order: deterministic, and identical alpha / tau everywhere);
+//     then the rank-1 update of the block columns on own rows;
+//   * block b: G = V_b^T A_panel (8 x nb, DMMA over own rows) -> ONE all-reduce.  G holds the
+//     Gram entries of V_b against every earlier reflector and itself (kept for T) and
+//     W = V_b^T C_rest; the rest of the panel is updated locally: C_rest -= V_b (T_b^T W).
+// At the end every CTA writes its rows of R / V (in place) and of the explicit V (Vbuf); CTA 0
+// assembles T (nb x nb) from the Gram entries and the taus (column recurrence of the compact-WY
+// factor, by 8-column blocks).  Same Householder convention and formulas as k_panel_block.
+// DESIGN.md §5.2.
+// ------------------------------------------------------------------------------------------
+// remote (distributed shared memory) async stores that complete on the receiver's mbarrier:
+// an all-reduce costs one store burst and one local mbarrier wait, no cluster-wide barrier
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async2(uint32_t raddr, double x, double y, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+                 "d"(x), "d"(y), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}\n" ::"r"(elmtma::su32(b)), "r"(parity)
+        : "memory");
+}
+
+namespace p8 {
+constexpr int CL = 8;      // CTAs per subdomain
+constexpr int NT = 256;    // threads per CTA
+constexpr int NW = NT / 32;
+constexpr int XC = 16;     // column exchange: 8 partial sums + the diagonal row's 8 values
+constexpr int XB = 512;    // block exchange: G (8 x 64)
+}  // namespace p8
+
+// rows per CTA: multiple of 16 (padded column stride Rq + 4 == 4 mod 16: conflict-free fragments)
+__host__ __device__ __forceinline__ int p8_rq(int64_t R) { return (int)((R + 16 * p8::CL - 1) / (16 * p8::CL)) * 16; }
+constexpr int P8_TAIL = 2 * 64 * 64 + 64 * 8;  // CTA 0's T assembly reuses the panel region
+size_t panel8_smem(int64_t R, int nb) {
+    const int64_t Rq = p8_rq(R);
+    return (size_t)(std::max<int64_t>(nb * (Rq + 4), P8_TAIL) + 2 * p8::CL * p8::XC + p8::CL * p8::XB + p8::NW * 8 + 64 +
+                    64 + 64 + 4) * 8;
+}
+
+__global__ void __cluster_dims__(p8::CL, 1, 1) __launch_bounds__(p8::NT, 1) k_panel_c8(PanelArgs a, int nb) {
+    using namespace p8;
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    const int z = (int)cl.block_rank();
+    const int sl = a.s_off + (int)blockIdx.x / CL;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0;
+    const int R = (int)(ld - j0);
+    const int Rq = p8_rq(R);
+    const int r0 = z * Rq, nr = max(0, min(Rq, R - r0));
+    const int RP = Rq + 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* Ap = sm;                    // [nb][RP] the panel, own rows
+    double* xc = Ap + max(nb * RP, P8_TAIL);  // [2][CL][XC] column exchange (double-buffered)
+    double* xb = xc + 2 * CL * XC;      // [CL][XB] block exchange; after the sum: Gs = slot 0, Zs = slot 1
+    double* red = xb + CL * XB;         // [NW][8]
+    double* taus = red + NW * 8;        // [64]
+    double* Tb = taus + 64;             // [8][8] T of the current block: Tb[i*8 + r] = T_b(r, i)
+    double* Rsv = Tb + 64;              // [64] R part of the current diagonal block
+    uint64_t* mbx = reinterpret_cast<uint64_t*>(Rsv + 64);  // [3] mbarriers: column exchange x2, block exchange
+    double* Gs = xb;
+    double* Zs = xb + XB;               // [8][68]
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+
+    // A. own rows of the panel
+    for (int c = 0; c < nb; ++c) {
+        const double* src = A + (int64_t)(j0 + c) * ld + j0 + r0;
+        for (int r2 = tid; r2 < nr / 2; r2 += NT) {
+            unsigned d = (unsigned)__cvta_generic_to_shared(Ap + c * RP + 2 * r2);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * r2));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) elmtma::mbar_init(mbx + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl.sync();  // every CTA of the cluster has started, its mbarriers are initialised
+    const uint32_t xc_s = elmtma::su32(xc), xb_s = elmtma::su32(xb), mbx_s = elmtma::su32(mbx);
+
+    int xcnt = 0;  // column exchanges so far (buffer / mbarrier xcnt & 1, phase xcnt >> 1)
+#ifdef ELM_PANEL_PROF
+    long long q_col = 0, q_xw = 0, q_g = 0, q_upd = 0, q_t0 = clock64(), q_a, q_b;
+    long long q_p[6] = {0, 0, 0, 0, 0, 0}, q_c;
+#define QS(v) v = clock64()
+#define QA(acc, from) acc += clock64() - from
+#else
+#define QS(v)
+#define QA(acc, from)
+#endif
+    for (int b = 0; b < nb / 8; ++b) {
+        const int jb = 8 * b;
+        // B. the 8 columns of the block, one cluster all-reduce each
+        QS(q_a);
+        for (int c = 0; c < 8; ++c) {
+            const int j = jb + c;           // panel column == panel-relative row of its diagonal
+            const int zo = j / Rq, dl = j - zo * Rq;
+            const int nk = 8 - c;
+            const int jl = j - r0;          // local row of the diagonal (rows > jl take part)
+            QS(q_c);
+            // partial sums over own rows below the diagonal; thread t owns rows t, t + NT, ...
+            // for the whole panel, so the column loop needs no trailing barrier
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = 0.0;
+            for (int r = tid; r < nr; r += NT) {
+                if (r <= jl) continue;
+                const double x = Ap[j * RP + r];
+                v[0] += x * x;
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) v[k] += x * Ap[(j + k) * RP + r];
+            }
+            QA(q_p[0], q_c); QS(q_c);
+            // warp sum of the 8 values by halving exchanges (9 shuffles): lanes 4k..4k+3 end
+            // with the sum of value k
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                double h4[4], h2[2], h1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double snd = b4 ? v[i] : v[i + 4];
+                    h4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double snd = b3 ? h4[i] : h4[i + 2];
+                    h2[i] = (b3 ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+                {
+                    const double snd = b2 ? h2[0] : h2[1];
+                    h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+                }
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) red[warp * 8 + (lane >> 2)] = h1;
+            }
+            __syncthreads();
+            QA(q_p[1], q_c); QS(q_c);
+            const int xb_i = xcnt & 1;
+            double* xcb = xc + xb_i * CL * XC;
+            if (tid == 0) elmtma::mbar_expect(mbx + xb_i, CL * XC * 8);
+            if (tid < CL * XC / 2) {
+                const int dst = tid / (XC / 2), i = 2 * (tid % (XC / 2));
+                double p[2] = {0.0, 0.0};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (i + e < 8) {
+                        for (int w = 0; w < NW; ++w) p[e] += red[w * 8 + i + e];
+                    } else if (z == zo && i + e - 8 < nk) {
+                        p[e] = Ap[(j + i + e - 8) * RP + dl];
+                    }
+                }
+                st_async2(mapa_u32(xc_s + (uint32_t)((xb_i * CL * XC + z * XC + i) * 8), dst), p[0], p[1],
+                          mapa_u32(mbx_s + 8u * xb_i, dst));
+            }
+            QA(q_p[2], q_c);
+            QS(q_b);
+            mbar_wait_cluster(mbx + xb_i, (xcnt >> 1) & 1);
+            QA(q_xw, q_b);
+            ++xcnt;
+            QS(q_c);
+            // lane k < 8: sum of value k over the CTAs (fixed order); lane 8 + k: the diagonal
+            // row's value in column j + k; then broadcast within the warp
+            double mine = 0.0;
+            if (lane < 8) {
+                double s0 = xcb[0 * XC + lane] + xcb[1 * XC + lane], s1 = xcb[2 * XC + lane] + xcb[3 * XC + lane];
+                double s2 = xcb[4 * XC + lane] + xcb[5 * XC + lane], s3 = xcb[6 * XC + lane] + xcb[7 * XC + lane];
+                mine = (s0 + s1) + (s2 + s3);
+            } else if (lane < 16) {
+                mine = xcb[zo * XC + lane];
+            }
+            const double ts0 = __shfl_sync(0xffffffffu, mine, 0);
+            const double x0 = __shfl_sync(0xffffffffu, mine, 8);
+            const double nrm = sqrt(x0 * x0 + ts0);
+            double alpha = x0, tau = 0.0, scale = 0.0;
+            if (nrm != 0.0) {
+                alpha = x0 >= 0.0 ? -nrm : nrm;
+                scale = 1.0 / (x0 - alpha);
+                tau = (alpha - x0) / alpha;
+            }
+            // lane k (1..7): w_k = tau (y_k + scale t_k), y_k from lane 8 + k
+            const double ydl = __shfl_sync(0xffffffffu, mine, (lane & 7) + 8);
+            const double wl = (lane >= 1 && lane < nk) ? tau * (ydl + scale * mine) : 0.0;
+            double w[8], yd[8];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) {
+                w[k] = __shfl_sync(0xffffffffu, wl, k);
+                yd[k] = __shfl_sync(0xffffffffu, mine, k + 8);
+            }
+            QA(q_p[3], q_c); QS(q_c);
+            if (tau != 0.0) {
+                for (int r = tid; r < nr; r += NT) {
+                    if (r <= jl) continue;
+                    const double x = Ap[j * RP + r];
+                    const double vs = scale * x;
+#pragma unroll
+                    for (int k = 1; k < 8; ++k)
+                        if (k < nk) Ap[(j + k) * RP + r] -= w[k] * vs;
+                    Ap[j * RP + r] = vs;
+                }
+            }
+            if (z == zo && tid == dl % NT) {  // the owner of the diagonal row
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) Ap[(j + k) * RP + dl] = yd[k] - w[k];
+                Ap[j * RP + dl] = alpha;
+            }
+            if (tid == 0) taus[j] = tau;
+            QA(q_p[4], q_c);
+        }
+        __syncthreads();
+        QA(q_col, q_a);
+        QS(q_a);
+        // C. explicit V_b in the diagonal block (unit diagonal, zeros above; R saved)
+        const int zb = jb / Rq, db = jb - zb * Rq;
+        if (z == zb && tid < 64) {
+            const int r = tid & 7, i = tid >> 3;
+            if (r <= i) {
+                Rsv[tid] = Ap[(jb + i) * RP + db + r];
+                Ap[(jb + i) * RP + db + r] = r == i ? 1.0 : 0.0;
+            }
+        }
+        __syncthreads();
+        // D. G = V_b^T A_panel over own rows >= jb (DMMA; warp w: columns [8w, 8w+8)), all-reduced
+        const int kb0 = max(0, jb - r0);
+        const int ntile = nb / 8;
+        if (tid == 0) elmtma::mbar_expect(mbx + 2, CL * ntile * 64 * 8);
+        if (warp < ntile) {
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            const double* va = Ap + (jb + (lane >> 2)) * RP + (lane & 3);
+            const double* vbp = Ap + (8 * warp + (lane >> 2)) * RP + (lane & 3);
+            for (int k0 = kb0; k0 < nr; k0 += 8) {  // nr - kb0 is a multiple of 8
+                dmma8(a0, a1, va[k0], vbp[k0]);
+                dmma8(b0, b1, va[k0 + 4], vbp[k0 + 4]);
+            }
+            const int gi = (lane >> 2) * 64 + 8 * warp + 2 * (lane & 3);
+#pragma unroll
+            for (int dst = 0; dst < CL; ++dst)
+                st_async2(mapa_u32(xb_s + (uint32_t)((z * XB + gi) * 8), dst), a0 + b0, a1 + b1, mapa_u32(mbx_s + 16u, dst));
+        }
+        mbar_wait_cluster(mbx + 2, b & 1);
+        double gsum[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * NT;
+            double s = 0.0;
+            if ((e & 63) < nb)
+                for (int q = 0; q < CL; ++q) s += xb[q * XB + e];
+            gsum[h] = s;
+        }
+        __syncthreads();
+        Gs[tid] = gsum[0];
+        Gs[tid + NT] = gsum[1];
+        __syncthreads();
+        // E. T_b (8 x 8) from the block's Gram (Gs[k][jb + i], k < i) and its taus; CTA 0 keeps
+        //    the Gram entries of V_b against all earlier reflectors for T (global scratch in Tbuf)
+        if (tid < 8) {
+            const int r = tid;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[jb + i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) s += trow[k] * Gs[k * 64 + jb + i];
+                    trow[i] = -taus[jb + i] * s;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Tb[i * 8 + r] = trow[i];
+        }
+        if (z == 0)
+            for (int t = tid; t < 8 * (jb + 8); t += NT) {
+                const int i = t / (jb + 8), k = t % (jb + 8);
+                if (k < jb + i) T[(jb + i) * ELM_NB + k] = Gs[i * 64 + k];  // S(k, jb+i) = v_k . v_{jb+i}
+            }
+        __syncthreads();
+        QA(q_g, q_a);
+        QS(q_a);
+        // F. Z = T_b^T W on the columns right of the block; C_rest -= V_b Z on own rows >= jb
+        const int c1 = jb + 8, ncr = nb - c1;
+        if (ncr > 0) {
+            for (int t = tid; t < 8 * ncr; t += NT) {
+                const int i = t / ncr, col = c1 + t % ncr;
+                double s = 0.0;
+                for (int k = 0; k <= i; ++k) s += Tb[i * 8 + k] * Gs[k * 64 + col];
+                Zs[i * 68 + col] = s;
+            }
+            __syncthreads();
+            const int nmt = (nr - kb0) / 8, nnt = ncr / 8;
+            const int kr = lane & 3, rn = lane >> 2;
+            for (int it = warp; it < nmt * nnt; it += NW) {
+                const int mt = it % nmt, nt = it / nmt;
+                const int rb0 = kb0 + 8 * mt, cb = c1 + 8 * nt;
+                double c0 = Ap[(cb + 2 * kr) * RP + rb0 + rn], c1v = Ap[(cb + 2 * kr + 1) * RP + rb0 + rn];
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks)
+                    dmma8(c0, c1v, Ap[(jb + 4 * ks + kr) * RP + rb0 + rn], -Zs[(4 * ks + kr) * 68 + cb + rn]);
+                Ap[(cb + 2 * kr) * RP + rb0 + rn] = c0;
+                Ap[(cb + 2 * kr + 1) * RP + rb0 + rn] = c1v;
+            }
+            __syncthreads();
+        }
+        // G. restore R in the diagonal block
+        if (z == zb && tid < 64) {
+            const int r = tid & 7, i = tid >> 3;
+            if (r <= i) Ap[(jb + i) * RP + db + r] = Rsv[tid];
+        }
+        __syncthreads();
+        QA(q_upd, q_a);
+    }
+#ifdef ELM_PANEL_PROF
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 5) && (a.j0 == 256 || a.j0 == 1024))
+        printf("P8PROF j0=%d cta=%d z=%d total %lld col %lld (xwait %lld) gblk %lld upd %lld | partial %lld shfl+sync %lld send %lld param %lld apply+sync %lld\n", a.j0, blockIdx.x, z,
+               clock64() - q_t0, q_col, q_xw, q_g, q_upd, q_p[0], q_p[1], q_p[2], q_p[3], q_p[4]);
+#endif
+
+    // H. write back R + V (in place) and the explicit V of own rows; tau
+    for (int c = 0; c < nb; ++c) {
+        double2* dst = reinterpret_cast<double2*>(A + (int64_t)(j0 + c) * ld + j0 + r0);
+        double2* dv = reinterpret_cast<double2*>(V + (int64_t)c * ld + j0 + r0);
+        for (int r2 = tid; r2 < nr / 2; r2 += NT) {
+            const double x0 = Ap[c * RP + 2 * r2], x1 = Ap[c * RP + 2 * r2 + 1];
+            dst[r2] = make_double2(x0, x1);
+            const int g0 = r0 + 2 * r2;
+            dv[r2] = make_double2(g0 < c ? 0.0 : (g0 == c ? 1.0 : x0), g0 + 1 < c ? 0.0 : (g0 + 1 == c ? 1.0 : x1));
+        }
+    }
+    if (z != 0) return;
+    if (tid < nb) a.tau[(int64_t)sl * a.M + j0 + tid] = taus[tid];
+    // I. CTA 0: T = compact-WY factor of the panel from S = strictly upper part of V^T V:
+    //    T(i,i) = tau_i; by blocks, T[0:kp, kp:kp+8] = -T[0:kp,0:kp] S[0:kp, kp:kp+8] T_b
+    __syncthreads();
+    double* Ss = sm;                 // [64][64] column-major (panel smem is free now)
+    double* Ts = sm + 64 * 64;       // [64][64]
+    double* Ys = Ts + 64 * 64;       // [64][8]
+    for (int t = tid; t < 64 * 64; t += NT) {
+        const int r = t & 63, c = t >> 6;
+        Ss[t] = (r < c && c < nb) ? T[t] : 0.0;
+        Ts[t] = 0.0;
+    }
+    __syncthreads();
+    for (int b = 0; b < nb / 8; ++b) {
+        const int kp = 8 * b;
+        if (tid < 8) {  // T_b
+            const int r = tid;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[kp + i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) s += trow[k] * Ss[(kp + i) * 64 + kp + k];
+                    trow[i] = -taus[kp + i] * s;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Ts[(kp + i) * 64 + kp + r] = trow[i];
+        }
+        __syncthreads();
+        if (kp > 0) {
+            for (int t = tid; t < kp * 8; t += NT) {  // Y = S[0:kp, kp:kp+8] T_b
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = 0; k <= c; ++k) s += Ss[(kp + k) * 64 + r] * Ts[(kp + c) * 64 + kp + k];
+                Ys[c * 64 + r] = s;
+            }
+            __syncthreads();
+            for (int t = tid; t < kp * 8; t += NT) {  // T[0:kp, kp+c] = -T[0:kp,0:kp] Y
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = r; k < kp; ++k) s += Ts[k * 64 + r] * Ys[c * 64 + k];
+                Ts[(kp + c) * 64 + r] = -s;
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = tid; t < 64 * 64; t += NT) T[t] = Ts[t];
+}
+
 constexpr int PANEL_FIXED = 8 * 56 * 2 + 40 + 64 + 8;  // Wsm, Zsm, tot, Tbb, taus (doubles)
 // V_prev ring of the panel-block kernel for R resident rows: all shared memory the block leaves
 int panel_ring(int64_t R, int smem_optin) {
@@ -1201,6 +1609,9 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         return e;
     if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
         return e;
+    const bool p8_ok = c->panel8 && panel8_smem(ld, std::min<int64_t>(M, ELM_NB)) <= (size_t)optin;
+    if (p8_ok && (e = cudaFuncSetAttribute(k_panel_c8, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
+        return e;
     if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wyt::SMEM)) != cudaSuccess)
         return e;
     // TMA descriptors: K_aug {ld, ncols, S} and V {ld, nb, S} (columns >= nb read as zero), boxes 16 x 64
@@ -1233,7 +1644,12 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
             if (g1 <= g0) continue;
             PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0, ring};
-            for (int blk = 0; blk < nb / ELM_BB; ++blk) {
+            if (p8_ok) {
+                KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
+                k_panel_c8<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, panel8_smem(ld - j0, nb), streams[g]>>>(pa, nb);
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            }
+            for (int blk = 0; !p8_ok && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 if (c->panel_cluster)

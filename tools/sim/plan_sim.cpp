@@ -64,6 +64,14 @@ int main(int argc, char** argv) {
         for (auto& t : pl.tasks) work += 3.5 * (t.kend - t.kbeg) + (t.I == t.J ? 45.0 : 10.0);
         printf("  critical path (unlimited CTAs) %.2f ms, work / workers %.2f ms\n", chol_eval(pl, id2, 1 << 20) * 1e-3,
                work / workers * 1e-3);
+        if (ord == 1) {
+            std::vector<double> upd(16, 0.0), cols(16, 0.0);
+            for (auto& t : pl.tasks) upd[std::min(15, pl.blk_depth[t.J])] += t.kend - t.kbeg;
+            for (int J = 0; J < pl.nblk; ++J) cols[std::min(15, pl.blk_depth[J])] += 1;
+            printf("  updates by dissection depth of the column:");
+            for (int d = 0; d < 12; ++d) printf(" d%d %.1f%% (%g cols)", d, 100.0 * upd[d] / pl.nupd, cols[d]);
+            printf("\n");
+        }
     }
     return 0;
 }
