@@ -44,16 +44,32 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--interface-mode", type=int, default=0,
                     help="interface factorisation order: 0 auto, 2 strip (envelope), 3 nested dissection")
+    ap.add_argument("--problem", type=int, default=None, help="operator override, e.g. 6 = variable coefficient")
+    ap.add_argument("--alpha", type=float, default=16.0, help="eqn:grf alpha of problem 6")
     ap.add_argument("--phases", action="store_true", help="print per-phase breakdown to stderr")
     return ap.parse_args()
 
 
-def workload_desc(k: int) -> str:
-    c = WL.config(k)
+def bench_config(args) -> dict:
+    """BASELINE config args.config; --problem / --alpha swap in another operator (NEXT-4)."""
+    over = {"interface_mode": getattr(args, "interface_mode", 0)}
+    if getattr(args, "problem", None) is not None:
+        over["problem"] = args.problem
+        over["alpha"] = args.alpha
+    return WL.config(args.config, **over)
+
+
+def workload_desc(k: int, c: dict | None = None) -> str:
+    c = WL.config(k) if c is None else c
     m = c["p"] ** 2 + 4 * c["q"]
     names = {0: "sin(pi x)sin(pi y)", 1: "e^(x+y)sin(2pi x)cos(2pi y)", 2: "sin(4pi x)sin(4pi y)",
-             3: "sin(8pi x)sin(8pi y)"}
-    return (f"cfg{k}: 2D Poisson -Lap u=f on (0,1)^2, u={names.get(c['problem'])}, {c['P']}x{c['P']} subdomains, "
+             3: "sin(8pi x)sin(8pi y)", 4: "sin(2pi x)e^y"}
+    if c["problem"] == 6:
+        pde = (f"2D variable-coefficient Poisson -div(rho grad u)=1, u=0 on the boundary, rho=tanh(grf)+1.1, "
+               f"grf alpha={c.get('alpha', 16.0)} (eqn:varpoisson)")
+    else:
+        pde = f"2D Poisson -Lap u=f on (0,1)^2, u={names.get(c['problem'])}"
+    return (f"cfg{k}: {pde}, {c['P']}x{c['P']} subdomains, "
             f"M={c['M']} tanh neurons/subdomain, {c['p']}x{c['p']} interior + {c['q']}/edge points "
             f"(local LS {m}x{c['M']}), seed {c['seed']}, eval 101x101")
 
@@ -163,7 +179,9 @@ def run_reference(args, world, rank):
         return
     import oracle as O
 
-    c = WL.config(args.config)
+    c = bench_config(args)
+    O.set_grf(c.get("grf"))
+    O.set_grf(c.get("grf"))
     oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
     W, b, _, _ = O.init_hidden(oc)
     cores = len(os.sched_getaffinity(0))
@@ -186,7 +204,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config)},
+            "config": {"workload": workload_desc(args.config, c)},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -196,6 +214,7 @@ def cpu_baseline_leg(c, k):
     """Oracle timed on a bounded sample of the same workload (about 10-30 s)."""
     import oracle as O
 
+    O.set_grf(c.get("grf"))
     oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
     W, b, _, _ = O.init_hidden(oc)
     cores = len(os.sched_getaffinity(0))
@@ -244,7 +263,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    c = WL.config(args.config, interface_mode=args.interface_mode)
+    c = bench_config(args)
     prob = E.Problem.from_config(c)
     N = c["P"] ** 2
     s0, s1 = E.partition(N, world, rank)
@@ -284,7 +303,8 @@ def main():
 
     # accuracy of the measured solution (u on rank 0 after the reduce)
     ue = WL.exact(c["problem"], xy_host)
-    err = float(np.linalg.norm(u.cpu().numpy() - ue) / np.linalg.norm(ue)) if rank == 0 else None
+    err = (float(np.linalg.norm(u.cpu().numpy() - ue) / np.linalg.norm(ue))
+           if rank == 0 and np.all(np.isfinite(ue)) else None)
 
     # per-phase device time over K steps (events between the calls, same stream, groups overlapped)
     ph = PhaseTimer(torch, stream)
@@ -386,7 +406,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_desc(args.config), "subdomains": N, "l2_flush":
+                "config": {"workload": workload_desc(args.config, c), "subdomains": N, "l2_flush":
                            "inputs larger than L2: every step writes K_aug (S*ld*ncols*8 B) >> 126 MB",
                            "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast",
                            "interface_ordering": ["strip", "nested_dissection"][ctx.sizes["chol_ordering"]]},

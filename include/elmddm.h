@@ -58,7 +58,9 @@ typedef struct {
     int32_t q;              /* collocation points per subdomain edge (even)                    */
     int32_t problem;        /* manufactured solution: 0 sin(pi x)sin(pi y) | 1 e^{x+y}sin(2pi x)cos(2pi y)
                                | 2 sin(4pi x)sin(4pi y) | 3 sin(8pi x)sin(8pi y) | 4 sin(2pi x)e^y
-                                | 5 u = 0                                                */
+                                | 5 u = 0 | 6 variable coefficient -div(rho grad u) = 1,
+                               u = 0 on the boundary, rho = tanh(grf) + 1.1 (eqn:varpoisson,
+                               P:694-701; needs elmddm_set_coefficient)                         */
     int32_t init_scheme;    /* 0 paper eqn:init l = c sqrt(N*M) | 1 manual l = 1 | 2 He l = sqrt(2/M), b = 0 */
     double init_c;          /* c of eqn:init (1/8 for Poisson)                          */
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s) (1/2)                    */
@@ -124,7 +126,8 @@ elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* newidx, int32_t* 
 elmddm_status elmddm_init_hidden(elmddm_ctx* ctx, double* W, double* b, double* xi, void* stream);
 
 /* eqn:nonoverlap_discrete, L = -Laplacian:
- *   Kaug[S][ncols][ld]: columns 0..M-1 = K^s (interior rows -|w|^2 sigma''(z), boundary and
+ *   Kaug[S][ncols][ld]: columns 0..M-1 = K^s (interior rows -|w|^2 sigma''(z) -- problem 6:
+ *   -rho |w|^2 sigma''(z) - (grad rho . w) sigma'(z) --, boundary and
  *   interface rows sigma(z)); columns M..M+4q-1 = E_Gamma (unit column at each interface row;
  *   zero column for a Dirichlet edge point; B^s = -E_Gamma); column M+4q = F^s = [f; g; 0];
  *   rows m..ld-1 = 0.
@@ -132,6 +135,14 @@ elmddm_status elmddm_init_hidden(elmddm_ctx* ctx, double* W, double* b, double* 
  *   outward axis normals; zero for Dirichlet edges.                                            */
 elmddm_status elmddm_assemble(elmddm_ctx* ctx, const double* W, const double* b, double* Kaug, double* At,
                               void* stream);
+
+/* Problem 6 only: the coefficient field of eqn:varpoisson, rho = tanh(grf) + 1.1 with
+ * grf(x) = sum_i a_i sin(w_i . x + b_i) of eqn:grf.  params: HOST array [nterms][4] =
+ * (a_i, w_ix, w_iy, b_i) (the paper's random draws, supplied by the caller; copied, not kept).
+ * Interior rows of K^s become -rho Lap phi - grad rho . grad phi (rho and its analytic gradient at
+ * each interior point, evaluated inside elmddm_assemble).  EINVAL for another problem id, nterms
+ * outside [1, 65536] or a NULL array; elmddm_assemble of problem 6 without it is EINVAL.       */
+elmddm_status elmddm_set_coefficient(elmddm_ctx* ctx, const double* params, int32_t nterms);
 
 /* Batched blocked Householder QR (no pivoting) of every K^s, applied to all ncols columns:
  *   Q^T [K | E_Gamma | F] = [[R11, R12, y], [0, T_E, t_F]]  (in place in Kaug; Householder vectors

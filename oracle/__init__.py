@@ -45,6 +45,8 @@ def lib():
         d, i32, i64, vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
         P = C.POINTER(Cfg)
         _lib.orc_problem.argtypes = [C.c_int, d, d, C.POINTER(d), C.POINTER(d)]
+        _lib.orc_set_grf.argtypes = [vp, C.c_int]
+        _lib.orc_rho.argtypes = [d, d, C.POINTER(d), C.POINTER(d), C.POINTER(d)]
         _lib.orc_geometry.argtypes = [P, vp]
         _lib.orc_rows.argtypes = [P, C.c_int, vp, vp, vp]
         _lib.orc_init_hidden.argtypes = [P, vp, vp, vp, vp]
@@ -72,6 +74,23 @@ def _p(a):
 
 def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0) -> Cfg:
     return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed)
+
+
+def set_grf(params) -> None:
+    """Coefficient field of problem 6 (eqn:varpoisson): params [n][4] = (a_i, w_ix,
+    w_iy, b_i) of eqn:grf; empty / None clears it (oracle.c orc_set_grf)."""
+    if params is None or len(params) == 0:
+        lib().orc_set_grf(None, 0)
+        return
+    p = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 4)
+    lib().orc_set_grf(p.ctypes.data_as(C.c_void_p), int(p.shape[0]))
+
+
+def rho(x: float, y: float):
+    """(rho, d rho/dx, d rho/dy) of problem 6 at (x, y) (oracle.c orc_rho)."""
+    r, rx, ry = C.c_double(), C.c_double(), C.c_double()
+    lib().orc_rho(x, y, C.byref(r), C.byref(rx), C.byref(ry))
+    return r.value, rx.value, ry.value
 
 
 def problem(pid: int, x: float, y: float):

@@ -131,6 +131,10 @@ void orc_problem(int problem, double x, double y, double *u, double *f) {
         uu = sin(2.0 * PI * x) * exp(y);
         ff = (4.0 * PI * PI - 1.0) * uu;
         break;
+    case 6: /* variable coefficient, eqn:varpoisson: f = 1, g = 0, no closed form */
+        uu = 0.0;
+        ff = 1.0;
+        break;
     default: /* 5: homogeneous problem u = 0 */
         uu = 0.0;
         ff = 0.0;
@@ -268,8 +272,46 @@ void orc_init_hidden(const orc_cfg *c, double *W, double *b, double *xi, int32_t
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* variable coefficient (problem 6), eqn:varpoisson with eqn:grf:      */
+/*   grf(x) = sum_i a_i sin(w_i . x + b_i)  (the 256 draws a_i, w_i, b_i are an input: params  */
+/*   [i][4] = (a_i, w_ix, w_iy, b_i), from the seeded generator module, reading R26),          */
+/*   rho = tanh(grf) + 1.1, grad rho = (1 - tanh^2 grf) grad grf (analytic).        */
+/* ------------------------------------------------------------------------------------------ */
+static double *g_grf = NULL;
+static int g_grf_n = 0;
+
+void orc_set_grf(const double *params, int nterms) {
+    free(g_grf);
+    g_grf = NULL;
+    g_grf_n = 0;
+    if (nterms > 0) {
+        g_grf = (double *)malloc(sizeof(double) * 4 * (size_t)nterms);
+        memcpy(g_grf, params, sizeof(double) * 4 * (size_t)nterms);
+        g_grf_n = nterms;
+    }
+}
+
+/* rho and its gradient at (x, y) */
+void orc_rho(double x, double y, double *rho, double *rx, double *ry) {
+    double g = 0.0, gx = 0.0, gy = 0.0;
+    for (int i = 0; i < g_grf_n; ++i) {
+        const double *t = g_grf + 4 * (size_t)i;
+        double arg = t[1] * x + t[2] * y + t[3];
+        g += t[0] * sin(arg);
+        double c = t[0] * cos(arg);
+        gx += c * t[1];
+        gy += c * t[2];
+    }
+    double th = tanh(g);
+    *rho = th + 1.1;
+    *rx = (1.0 - th * th) * gx;
+    *ry = (1.0 - th * th) * gy;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* assembly: eqn:nonoverlap_discrete, Poisson L = -Lap (reading R4)               */
 /*   K^s rows: interior  -|w|^2 sigma''(z);  boundary/interface  sigma(z)                      */
+/*   problem 6 interior: -div(rho grad phi) = -rho |w|^2 sigma'' - (grad rho . w) sigma'         */
 /*   A^s rows (interface points): (w . n_s) sigma'(z), outward axis normals (reading R5)      */
 /*   F^s = [f(x_i); g(x_b); 0], g = u_exact on dOmega (reading R3)                            */
 /*   sigma = tanh, sigma' = 1 - sigma^2, sigma'' = -2 sigma sigma'                             */
@@ -302,8 +344,17 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
             double d1 = 1.0 - t * t;
             double d2 = -2.0 * t * d1;
             double val;
-            if (edge[r] < 0) val = -w2 * d2;
-            else val = t;
+            if (edge[r] < 0) {
+                if (c->problem == 6) {
+                    double rho, rx, ry;
+                    orc_rho(xy[2 * r], xy[2 * r + 1], &rho, &rx, &ry);
+                    val = -rho * w2 * d2 - (rx * wx + ry * wy) * d1;
+                } else {
+                    val = -w2 * d2;
+                }
+            } else {
+                val = t;
+            }
             K[(size_t)n * m + r] = val;
             if (edge[r] >= 0 && A) {
                 int e = edge[r];

@@ -104,6 +104,10 @@ __device__ void problem_uf(int pid, double x, double y, double& u, double& f) {
             u = s;
             f = (4.0 * kPi * kPi - 1.0) * s;
         } break;
+        case 6:  // variable coefficient, eqn:varpoisson: f = 1, g = 0
+            u = 0.0;
+            f = 1.0;
+            break;
         default:
             u = 0.0;
             f = 0.0;
@@ -155,6 +159,33 @@ __device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
     }
 }
 
+// Problem 6 coefficient at the interior collocation points, eqn:varpoisson with
+// eqn:grf: grf = sum_i a_i sin(w_i . x + b_i), rho = tanh(grf) + 1.1,
+// grad rho = (1 - tanh^2 grf) grad grf (analytic).  coef[S][p*p][4] =
+// (rho, d rho/dx, d rho/dy, 0); params[i] = (a_i, w_ix, w_iy, b_i) in global memory.
+__global__ void k_coef(elmddm_config cfg, const double4* __restrict__ params, int nterms, double4* __restrict__ coef) {
+    const int p = cfg.p, pp = p * p, P = cfg.P;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t S = cfg.s_end - cfg.s_begin;
+    if (t >= S * pp) return;
+    const int sl = (int)(t / pp), r = (int)(t % pp), s = cfg.s_begin + sl;
+    const int i = s % P, j = s / P;
+    const double den = (double)(P * (p + 1));
+    const double x = (double)(i * (p + 1) + r % p + 1) / den, y = (double)(j * (p + 1) + r / p + 1) / den;
+    double g = 0.0, gx = 0.0, gy = 0.0;
+    for (int k = 0; k < nterms; ++k) {
+        const double4 a = params[k];
+        double sn, cs;
+        sincos(a.y * x + a.z * y + a.w, &sn, &cs);
+        g = fma(a.x, sn, g);
+        const double c = a.x * cs;
+        gx = fma(c, a.y, gx);
+        gy = fma(c, a.z, gy);
+    }
+    const double th = tanh(g), d = 1.0 - th * th;
+    coef[t] = make_double4(th + 1.1, d * gx, d * gy, 0.0);
+}
+
 constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
 constexpr int AS_NT = 256;
 
@@ -174,9 +205,11 @@ __device__ __forceinline__ double fast_rcp(double x) {
 // tabulated per neuron over the p+q+2 distinct x (resp. y) coordinates of the subdomain's rows;
 // then d = 1/(1+E), sigma = 1 - 2d, sigma' = 4 E d^2, -|w|^2 sigma'' = 2|w|^2 sigma sigma'.
 // |z| <= |w|_1 (h/2 + r) stays O(10) for the paper's initialisation, so E never overflows.
+template <bool VAR>  // VAR: problem 6 (variable coefficient interior rows)
 __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
                                                     const double* __restrict__ W, const double* __restrict__ b,
-                                                    double* __restrict__ Kaug, double* __restrict__ At) {
+                                                    double* __restrict__ Kaug, double* __restrict__ At,
+                                                    const double4* __restrict__ coef) {
     const int M = cfg.M, q = cfg.q, P = cfg.P, p = cfg.p, pp = p * p;
     const int m = pp + 4 * q;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
@@ -246,6 +279,7 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
         // two consecutive rows per thread -> 16-byte stores
         for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
             int xi[2], yi[2], kind[2];
+            double4 rc[2] = {make_double4(1.0, 0.0, 0.0, 0.0), make_double4(1.0, 0.0, 0.0, 0.0)};
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int r = 2 * r2 + e;
@@ -253,6 +287,7 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     xi[e] = r % p;
                     yi[e] = r / p;
                     kind[e] = 0;
+                    if (VAR) rc[e] = coef[(int64_t)sl * pp + r];
                 } else if (r < m) {
                     const int t = r - pp, ed = t / q, k = t % q;
                     kind[e] = 1;
@@ -275,7 +310,10 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     const double d = fast_rcp(1.0 + E);
                     const double sg = fma(-2.0, d, 1.0);
                     const double s1 = 4.0 * E * d * d;
-                    v[e] = kind[e] == 0 ? w2s[cc] * sg * s1 : (kind[e] == 1 ? sg : 0.0);
+                    // interior: -Lap phi, or -rho Lap phi - grad rho . grad phi (problem 6)
+                    const double lap = VAR ? rc[e].x * (w2s[cc] * sg) - (rc[e].y * wxs[cc] + rc[e].z * wys[cc])
+                                           : w2s[cc] * sg;
+                    v[e] = kind[e] == 0 ? lap * s1 : (kind[e] == 1 ? sg : 0.0);
                 }
                 *reinterpret_cast<double2*>(Ks + (int64_t)(c0 + cc) * ld + 2 * r2) = make_double2(v[0], v[1]);
             }
@@ -348,7 +386,17 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
     dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
     const size_t tab_bytes = sizeof(double) * AS_COLS * 2 * (c->cfg.p + c->cfg.q + 2);
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
-    k_assemble<<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At); }
+    const double4* coef = nullptr;
+    if (c->cfg.problem == 6) {
+        const int64_t npt = c->sz.S * (int64_t)c->cfg.p * c->cfg.p;
+        k_coef<<<(unsigned)((npt + 127) / 128), 128, 0, st>>>(c->cfg, reinterpret_cast<const double4*>(c->d_grf), c->ngrf,
+                                                             reinterpret_cast<double4*>(c->d_coef));
+        coef = reinterpret_cast<const double4*>(c->d_coef);
+    }
+    if (coef)
+        k_assemble<true><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, coef);
+    else
+        k_assemble<false><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr); }
     return cudaGetLastError();
 }
 

@@ -92,7 +92,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// orders this thread's generic-proxy view (incl. tiles other CTAs published and this thread
+// acquired) before its following async-proxy (bulk copy) accesses, in every state space
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 
 // ------------------------------------------------------------------------------------------
 // the left-looking tile Cholesky

@@ -50,7 +50,7 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
     if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
     if (round_up(m, 32) > 3008) return why = "m too large for the shared-memory panel (ld <= 3008)", false;
-    if (cfg->problem < 0 || cfg->problem > 5) return why = "unknown problem id", false;
+    if (cfg->problem < 0 || cfg->problem > 6) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
     int64_t N = (int64_t)cfg->P * cfg->P;
@@ -374,6 +374,8 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_colcnt);
     cudaFree(c->d_cready);
     cudaFree(c->d_chol_next);
+    cudaFree(c->d_grf);
+    cudaFree(c->d_coef);
     cudaFree(c->d_ntc);
     delete c;
 }
@@ -472,9 +474,40 @@ elmddm_status elmddm_assemble(elmddm_ctx* c, const double* W, const double* b, d
     CHECK_PTR(c, b);
     CHECK_PTR(c, Kaug);
     CHECK_PTR(c, At);
+    if (c->cfg.problem == 6 && !c->d_grf) {
+        c->err = "problem 6 needs elmddm_set_coefficient before elmddm_assemble";
+        return ELMDDM_EINVAL;
+    }
     DeviceGuard dg(c->device);
     cudaError_t e = launch_assemble(c, W, b, Kaug, At, (cudaStream_t)stream);
     return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_assemble");
+}
+
+elmddm_status elmddm_set_coefficient(elmddm_ctx* c, const double* params, int32_t nterms) {
+    CHECK_CTX(c);
+    if (c->cfg.problem != 6) {
+        c->err = "elmddm_set_coefficient: only problem 6 has a coefficient field";
+        return ELMDDM_EINVAL;
+    }
+    if (nterms < 1 || nterms > 65536 || !params) {
+        c->err = "elmddm_set_coefficient: need 1 <= nterms <= 65536 and a host parameter array";
+        return ELMDDM_EINVAL;
+    }
+    DeviceGuard dg(c->device);
+    cudaError_t e = cudaSuccess;
+    if (nterms != c->ngrf) {
+        cudaFree(c->d_grf);
+        c->d_grf = nullptr;
+        c->ngrf = 0;
+        if ((e = cudaMalloc((void**)&c->d_grf, sizeof(double) * 4 * (size_t)nterms)) != cudaSuccess)
+            return cuda_fail(c, e, "elmddm_set_coefficient");
+        c->ngrf = nterms;
+    }
+    if (!c->d_coef &&
+        (e = cudaMalloc((void**)&c->d_coef, sizeof(double) * 4 * (size_t)c->sz.S * c->cfg.p * c->cfg.p)) != cudaSuccess)
+        return cuda_fail(c, e, "elmddm_set_coefficient");
+    e = cudaMemcpy(c->d_grf, params, sizeof(double) * 4 * (size_t)nterms, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_set_coefficient");
 }
 
 elmddm_status elmddm_local_factor(elmddm_ctx* c, double* Kaug, double* tau, double* work, void* stream) {

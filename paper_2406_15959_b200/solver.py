@@ -57,6 +57,7 @@ class Problem:
     interface_mode: int = 0             # factorisation order: 0 auto | 1, 2 strip (envelope) | 3 nested dissection
     interface_solver: str = "cholesky"  # "cholesky" (direct, reading R12) | "cg" (the paper's)
     cg_tol: float = 1e-9                # relative residual of the CG solver
+    grf: object = None                  # problem 6: eqn:grf draws [n][4] (a, w_x, w_y, b)
 
     @classmethod
     def from_config(cls, c: dict) -> "Problem":
@@ -89,6 +90,18 @@ class Context:
         self._check(L.elmddm_sizes(h, C.byref(sz)), "elmddm_sizes")
         self.sizes = sz.as_dict()
         self.s_begin, self.s_end = s_begin, s_end
+        if prob.problem == 6:
+            if prob.grf is None:
+                raise _lib.ElmddmError("problem 6 (variable coefficient) needs Problem.grf")
+            self.set_coefficient(prob.grf)
+
+    def set_coefficient(self, params):
+        """Coefficient field of problem 6 (eqn:varpoisson): params [n][4] = (a_i, w_ix, w_iy, b_i)."""
+        import numpy as np
+
+        p = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 4)
+        self._check(self.L.elmddm_set_coefficient(self.h, p.ctypes.data_as(C.c_void_p), int(p.shape[0])),
+                    "elmddm_set_coefficient")
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -10,6 +10,7 @@ EPS = np.finfo(float).eps
 
 
 def ocfg(c: dict):
+    O.set_grf(c.get("grf"))  # problem 6 coefficient (None clears it)
     return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0), c.get("init_c", 0.125),
                  c.get("r_over_diam", 0.5), c["seed"])
 
@@ -17,6 +18,8 @@ def ocfg(c: dict):
 def small(**kw):
     base = dict(P=2, M=16, p=6, q=4, problem=0, seed=7, init_scheme=0, init_c=0.125, r_over_diam=0.5)
     base.update(kw)
+    if base["problem"] == 6 and base.get("grf") is None:
+        base["grf"] = WL.grf_params(base.get("alpha", 4.0), base["seed"])
     return base
 
 

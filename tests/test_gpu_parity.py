@@ -524,3 +524,62 @@ def test_qr_panel_variants_config2(cluster, panel8, monkeypatch):
     W, b, _ = _oracle_init(c)
     r = O.solve(ocfg(c), W, b, xy, nthreads=NCPU)
     assert rel_l2(u.cpu().numpy(), r["u"]) <= 1e-6
+
+
+# ------------------------------------------------------------------------------------------------
+# variable coefficient, eqn:varpoisson -- SURVEY §8(f) NEXT-4
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("alpha", [4.0, 16.0])
+def test_varcoef_assembly_matches_oracle(alpha):
+    """Problem 6 rows: interior -rho Lap phi - grad rho . grad phi with rho = tanh(grf) + 1.1 from
+    the same eqn:grf draws; value / flux rows and F = [1; 0; 0] as for Poisson.  The coefficient
+    sums 256 sines of arguments up to |w||x| + 2 pi ~ alpha + 6 with |a| ~ alpha^2 / 16: the two
+    sides' sin / cos differ by a few ulps of the argument, hence the 1e-9 relative bound for
+    alpha = 16 (1e-12 for alpha = 4)."""
+    c = small(P=3, M=40, p=9, q=6, problem=6, alpha=alpha, seed=4)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, _ = _oracle_init(c)
+    oc = ocfg(c)
+    tol = 1e-12 if alpha < 8 else 1e-9
+    for s in range(9):
+        K, F, A = O.assemble(oc, s, W, b)
+        xy, edge, gidx = O.rows(oc, s)
+        m = len(edge)
+        Kg = kaug_np(ctx, buf, s)
+        scale = np.abs(K).max(axis=1, keepdims=True) + 1e-300
+        assert np.all(np.abs(Kg[:m, :c["M"]] - K) <= tol * scale), s
+        assert np.array_equal(Kg[:m, c["M"] + 4 * c["q"]], F)
+        Ag = at_np(ctx, buf, s, c["M"], c["q"])
+        assert np.allclose(Ag, A, rtol=0, atol=1e-13 * max(1.0, np.abs(A).max()))
+
+
+@pytest.mark.parametrize("cfgkw", [
+    dict(P=2, M=40, p=9, q=6, alpha=1.0),
+    dict(P=3, M=72, p=11, q=10, interface_mode=3, alpha=2.0),
+    dict(P=4, M=136, p=13, q=14, alpha=2.0),
+])
+def test_varcoef_end_to_end_parity(cfgkw):
+    """Problem 6 through the whole path: u on a grid matches the oracle to relative L2 1e-6.
+    Smooth fields (alpha <= 2, local residual <= 1e-3): at these sizes a rough field (alpha >= 4,
+    rho jumping between 0.1 and 2.1 across thin layers) is not resolved by the network -- the
+    local residuals are O(1) and, as for He initialisation (reading R24), u between collocation
+    points is not determined by the least-squares problem."""
+    c = small(problem=6, seed=3, **cfgkw)
+    xy = WL.eval_grid(21)
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy)
+    assert rel_l2(u.cpu().numpy(), r["u"]) <= 1e-6
+    O.set_grf(None)
+
+
+def test_varcoef_needs_coefficient():
+    import paper_2406_15959_b200 as E
+
+    c = small(problem=6, alpha=4.0)
+    pr = E.Problem.from_config({k: v for k, v in c.items() if k != "grf"})
+    with pytest.raises(E.ElmddmError):
+        E.Context(pr)
+    ctx, _ = gpu_ctx(small(problem=0))
+    with pytest.raises(E.ElmddmError):
+        ctx.set_coefficient(WL.grf_params(4.0, 1))

@@ -443,3 +443,87 @@ def test_init_study_direction_oracle():
         ue = np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
         rmse[sch] = float(np.sqrt(np.mean((r["uG"] - ue) ** 2)))
     assert rmse[0] < 1e-3 * rmse[2], rmse
+
+
+# ------------------------------------------------------------------------------------------------
+# variable coefficient (problem 6): eqn:varpoisson, rho = tanh(grf) + 1.1, eqn:grf
+# (P:611-615); SURVEY §8(f) NEXT-4
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("alpha", [16.0, 32.0])
+def test_varcoef_rho_range_and_gradient(alpha):
+    """rho varies in [0.1, 2.1]; its analytic gradient matches central differences of
+    rho itself (grad rho analytic, not differenced)."""
+    O.set_grf(WL.grf_params(alpha, 11))
+    rng = np.random.default_rng(3)
+    vals = [O.rho(x, y)[0] for x, y in rng.uniform(0, 1, (2000, 2))]
+    assert 0.1 <= min(vals) and max(vals) <= 2.1  # saturates: tanh(grf) = +-1 where |grf| is large
+    assert min(vals) < 0.3 and max(vals) > 1.9  # the field really spans the range
+    h = 1e-7
+    for x, y in rng.uniform(0.1, 0.9, (20, 2)):
+        r, rx, ry = O.rho(x, y)
+        fx = (O.rho(x + h, y)[0] - O.rho(x - h, y)[0]) / (2 * h)
+        fy = (O.rho(x, y + h)[0] - O.rho(x, y - h)[0]) / (2 * h)
+        scale = max(1.0, abs(rx), abs(ry))
+        assert abs(rx - fx) <= 1e-5 * scale and abs(ry - fy) <= 1e-5 * scale
+    O.set_grf(None)
+
+
+def test_varcoef_grf_statistics():
+    """The draws of eqn:grf: a ~ N(0, alpha^4/256) for the paper's 256 terms (variance alpha^4 /
+    nterms in general), w ~ N(0, alpha^2 I), b ~ U(0, 2 pi)."""
+    assert WL.grf_params(16.0, 0).shape == (256, 4)
+    n = 200000
+    p = WL.grf_params(16.0, 0, nterms=n)
+    assert abs(p[:, 0].std() - 16.0**2 / np.sqrt(n)) < 0.01 * 16.0**2 / np.sqrt(n)
+    assert abs(p[:, 1].std() - 16.0) < 0.1 and abs(p[:, 2].std() - 16.0) < 0.1
+    assert p[:, 3].min() >= 0 and p[:, 3].max() < 2 * np.pi and abs(p[:, 3].mean() - np.pi) < 0.02
+
+
+def test_varcoef_interior_rows_are_minus_div_rho_grad_phi():
+    """Interior rows of problem 6 = -div(rho grad phi), checked against central differences of
+    the flux rho grad phi (np.tanh; rho from the oracle); value / flux rows and F = [1; 0; 0]."""
+    grf = WL.grf_params(4.0, 5)
+    O.set_grf(grf)
+    c = O.cfg(2, 24, 5, 4, 6, 0, 0.125, 0.5, 5)
+    W, b, _, _ = O.init_hidden(c)
+    s = 1
+    K, F, A = O.assemble(c, s, W, b)
+    xy, edge, gidx = O.rows(c, s)
+    w, bb = W[s], b[s]
+    phi = lambda p: np.tanh(w[:, 0] * p[0] + w[:, 1] * p[1] + bb)
+    h = 1e-4
+
+    def flux(p, axis):
+        e = np.array([h, 0.0]) if axis == 0 else np.array([0.0, h])
+        dphi = (phi(p + e) - phi(p - e)) / (2 * h)
+        return O.rho(p[0], p[1])[0] * dphi
+
+    for r in range(len(edge)):
+        p = xy[r]
+        if edge[r] < 0:
+            ex, ey = np.array([h, 0.0]), np.array([0.0, h])
+            div = (flux(p + ex, 0) - flux(p - ex, 0)) / (2 * h) + (flux(p + ey, 1) - flux(p - ey, 1)) / (2 * h)
+            assert np.allclose(K[r], -div, rtol=0, atol=2e-5 * max(1.0, np.abs(div).max()))
+            assert F[r] == 1.0
+        else:
+            assert np.allclose(K[r], phi(p), rtol=0, atol=2e-15)
+            assert F[r] == 0.0
+    O.set_grf(None)
+
+
+def test_varcoef_zero_field_is_scaled_poisson():
+    """grf = 0 (all a_i = 0): rho = 1.1, grad rho = 0, so the interior rows are 1.1 x the
+    constant-coefficient rows of -Lap (a special case that reduces to problem 0's operator)."""
+    grf = WL.grf_params(8.0, 2)
+    grf[:, 0] = 0.0
+    O.set_grf(grf)
+    c6 = O.cfg(2, 16, 5, 4, 6, 0, 0.125, 0.5, 9)
+    c0 = O.cfg(2, 16, 5, 4, 0, 0, 0.125, 0.5, 9)
+    W, b, _, _ = O.init_hidden(c6)
+    K6, F6, A6 = O.assemble(c6, 2, W, b)
+    K0, F0, A0 = O.assemble(c0, 2, W, b)
+    _, edge, _ = O.rows(c6, 2)
+    inn = edge < 0
+    assert np.allclose(K6[inn], 1.1 * K0[inn], rtol=4e-16 * 4, atol=0)
+    assert np.array_equal(K6[~inn], K0[~inn]) and np.array_equal(A6, A0)
+    O.set_grf(None)

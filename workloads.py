@@ -28,7 +28,22 @@ def config(k: int, **over) -> dict:
     c = dict(CONFIGS[k])
     c.update(init_scheme=0, init_c=0.125, r_over_diam=0.5)
     c.update(over)
+    if c.get("problem") == 6 and c.get("grf") is None:
+        c["grf"] = grf_params(c.get("alpha", 16.0), c["seed"])
     return c
+
+
+def grf_params(alpha: float, seed: int, nterms: int = 256) -> np.ndarray:
+    """The random draws of eqn:grf for problem 6's coefficient rho = tanh(grf) + 1.1
+    (eqn:varpoisson): a_i ~ N(0, alpha^4 / nterms), w_i ~ N(0, alpha^2 I),
+    b_i ~ U(0, 2 pi).  Returns [nterms][4] = (a_i, w_ix, w_iy, b_i).  Seeded input generator
+    (numpy PCG64, stream 'grf' of the config seed); both the oracle and the CUDA path take it as
+    an input (reading R26)."""
+    rng = np.random.default_rng([int(seed), 0x67726600])
+    a = rng.normal(0.0, alpha * alpha / np.sqrt(nterms), nterms)
+    w = rng.normal(0.0, alpha, (nterms, 2))
+    b = rng.uniform(0.0, 2.0 * np.pi, nterms)
+    return np.ascontiguousarray(np.column_stack([a, w[:, 0], w[:, 1], b]), dtype=np.float64)
 
 
 def eval_grid(n: int = 101) -> np.ndarray:
@@ -52,4 +67,6 @@ def exact(problem: int, xy: np.ndarray) -> np.ndarray:
         return np.sin(8 * pi * x) * np.sin(8 * pi * y)
     if problem == 4:
         return np.sin(2 * pi * x) * np.exp(y)
+    if problem == 6:  # variable coefficient: no closed form (the paper's reference is FEM)
+        return np.full_like(x, np.nan)
     return np.zeros_like(x)
