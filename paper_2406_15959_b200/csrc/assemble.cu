@@ -4,6 +4,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace {
@@ -163,27 +165,61 @@ __device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
 // eqn:grf: grf = sum_i a_i sin(w_i . x + b_i), rho = tanh(grf) + 1.1,
 // grad rho = (1 - tanh^2 grf) grad grf (analytic).  coef[S][p*p][4] =
 // (rho, d rho/dx, d rho/dy, 0); params[i] = (a_i, w_ix, w_iy, b_i) in global memory.
-__global__ void k_coef(elmddm_config cfg, const double4* __restrict__ params, int nterms, double4* __restrict__ coef) {
+// Separable on the p x p interior lattice of a subdomain: e^{i(w.x + b)} = [e^{i(w_x x_a + b)}]
+// [e^{i w_y y_b}], the two factors tabulated per term over the p lattice coordinates (one CTA per
+// subdomain, terms in chunks of CT), so each point costs one complex product per term instead
+// of a sincos.
+constexpr int CT = 32;
+__global__ void __launch_bounds__(512) k_coef(elmddm_config cfg, const double4* __restrict__ params, int nterms,
+                                              double4* __restrict__ coef) {
+    extern __shared__ double ctab[];  // [CT][p][4]: (cos, sin) of the x factor, (cos, sin) of the y factor
     const int p = cfg.p, pp = p * p, P = cfg.P;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t S = cfg.s_end - cfg.s_begin;
-    if (t >= S * pp) return;
-    const int sl = (int)(t / pp), r = (int)(t % pp), s = cfg.s_begin + sl;
+    const int sl = blockIdx.x, s = cfg.s_begin + sl;
     const int i = s % P, j = s / P;
     const double den = (double)(P * (p + 1));
-    const double x = (double)(i * (p + 1) + r % p + 1) / den, y = (double)(j * (p + 1) + r / p + 1) / den;
-    double g = 0.0, gx = 0.0, gy = 0.0;
-    for (int k = 0; k < nterms; ++k) {
-        const double4 a = params[k];
-        double sn, cs;
-        sincos(a.y * x + a.z * y + a.w, &sn, &cs);
-        g = fma(a.x, sn, g);
-        const double c = a.x * cs;
-        gx = fma(c, a.y, gx);
-        gy = fma(c, a.z, gy);
+    constexpr int NPT = 8;  // points per thread (p*p <= 512 * 8 is checked by the launcher)
+    double g[NPT], gx[NPT], gy[NPT];
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) g[u] = gx[u] = gy[u] = 0.0;
+    for (int k0 = 0; k0 < nterms; k0 += CT) {
+        const int nk = min(CT, nterms - k0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nk * p; t += blockDim.x) {
+            const int k = t / p, a = t % p;
+            const double4 pr = params[k0 + k];
+            const double xa = (double)(i * (p + 1) + a + 1) / den, yb = (double)(j * (p + 1) + a + 1) / den;
+            double sx, cx, sy, cy;
+            sincos(pr.y * xa + pr.w, &sx, &cx);
+            sincos(pr.z * yb, &sy, &cy);
+            double* e = ctab + (size_t)t * 4;
+            e[0] = cx; e[1] = sx; e[2] = cy; e[3] = sy;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < NPT; ++u) {
+            const int r = threadIdx.x + u * blockDim.x;
+            if (r >= pp) break;
+            const int a = r % p, bb = r / p;
+            for (int k = 0; k < nk; ++k) {
+                const double4 pr = params[k0 + k];
+                const double* ex = ctab + ((size_t)k * p + a) * 4;
+                const double* ey = ctab + ((size_t)k * p + bb) * 4;
+                const double sn = fma(ex[1], ey[2], ex[0] * ey[3]);   // sin(A + B)
+                const double cs = fma(ex[0], ey[2], -ex[1] * ey[3]);  // cos(A + B)
+                g[u] = fma(pr.x, sn, g[u]);
+                const double c = pr.x * cs;
+                gx[u] = fma(c, pr.y, gx[u]);
+                gy[u] = fma(c, pr.z, gy[u]);
+            }
+        }
     }
-    const double th = tanh(g), d = 1.0 - th * th;
-    coef[t] = make_double4(th + 1.1, d * gx, d * gy, 0.0);
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+        const int r = threadIdx.x + u * blockDim.x;
+        if (r >= pp) break;
+        const double th = tanh(g[u]), d = 1.0 - th * th;
+        coef[(int64_t)sl * pp + r] = make_double4(th + 1.1, d * gx[u], d * gy[u], 0.0);
+    }
 }
 
 constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
@@ -388,9 +424,16 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
     const double4* coef = nullptr;
     if (c->cfg.problem == 6) {
-        const int64_t npt = c->sz.S * (int64_t)c->cfg.p * c->cfg.p;
-        k_coef<<<(unsigned)((npt + 127) / 128), 128, 0, st>>>(c->cfg, reinterpret_cast<const double4*>(c->d_grf), c->ngrf,
-                                                             reinterpret_cast<double4*>(c->d_coef));
+        const int pp = c->cfg.p * c->cfg.p;
+        const int nt = std::min(512, std::max(32, (pp + 7) / 8 + 31) / 32 * 32);
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_coef, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        k_coef<<<(unsigned)c->sz.S, nt, sizeof(double) * 4 * CT * c->cfg.p, st>>>(
+            c->cfg, reinterpret_cast<const double4*>(c->d_grf), c->ngrf, reinterpret_cast<double4*>(c->d_coef));
         coef = reinterpret_cast<const double4*>(c->d_coef);
     }
     if (coef)
