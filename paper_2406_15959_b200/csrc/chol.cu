@@ -94,7 +94,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 // orders this thread's generic-proxy view (incl. tiles other CTAs published and this thread
 // acquired) before its following async-proxy (bulk copy) accesses, in every state space
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
+// (global: tiles written by other CTAs' generic stores, read by the bulk copy; shared::cta: the
+// stage this thread's CTA read with generic loads, about to be overwritten by the async proxy.
+// The unqualified fence costs a MEMBAR.ALL.GPU, these two a CTA membar.)
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.global;\nfence.proxy.async.shared::cta;\n" ::: "memory");
+}
 
 // ------------------------------------------------------------------------------------------
 // the left-looking tile Cholesky

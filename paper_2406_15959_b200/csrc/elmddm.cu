@@ -301,6 +301,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_CHOL_CRITBAND")) c->crit_band = std::max(1, atoi(env));
         if (const char* env = getenv("ELMDDM_CHOL_SCHED")) c->chol_sched = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL8")) c->panel8 = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_PANEL_MERGED")) c->panel_merged = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));

@@ -107,6 +107,7 @@ struct elmddm_ctx {
     double* d_grf = nullptr;         // problem 6: eqn:grf parameters [ngrf][4] (elmddm_set_coefficient)
     int ngrf = 0;
     double* d_coef = nullptr;        // problem 6: [S][p*p][4] rho, grad rho at the interior points
+    int panel_merged = 1;            // ELMDDM_PANEL_MERGED: one launch per panel, merged Gram pass (k_panel_p)
     int panel8 = 0;                  // ELMDDM_PANEL8: on-chip 8-CTA cluster panels (qr.cu k_panel_c8)
     int chol_sched = 1;              // ELMDDM_CHOL_SCHED: 1 list-scheduled task order, dynamic dealing
     double chol_sim_us = 0.0;        // simulated makespan of the scheduled order

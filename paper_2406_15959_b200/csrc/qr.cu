@@ -405,6 +405,329 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_block(PanelArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// One launch per panel (k_panel_block's arithmetic, restructured): the CTA of a subdomain walks
+// the panel's 8-column blocks left-looking with the block resident in shared memory.  The
+// Gram product V_prev^T V_{b-1} that extends T by block b-1 is taken in the SAME streaming pass
+// as block b's W = V_prev^T C_b (V_{b-1} is the last 8 columns of every staged chunk), so each
+// block streams V_prev twice (W, then C -= V_prev Z) instead of three times; only the last block
+// of the panel needs its own Gram pass.  The column factorisation owns rows by thread (rows t,
+// t + 512, ...), reduces the 8 sums of a column with 9 shuffles, and needs one barrier per column.
+// ------------------------------------------------------------------------------------------
+constexpr int PANELP_FIXED = 3 * 8 * 56 + 2 * PNW * 8 + 40 + 64 + 8 + 64;  // Wsm, Zsm, Gp, red x2, tot, Tbb, taus, rowfix
+
+// T[0:kpp, kpp:kpp+8] = -T[0:kpp,0:kpp] (G Tbb), G = V[:, 0:kpp]^T V_b (kpp x 8, G[c*kpp + r]),
+// Tbb = T of the block (Tbb[c*8 + r]).  Ts, Ys: shared scratch.  Ends with a barrier.
+__device__ void t_extend(double* T, int kpp, const double* G, const double* Tbb, double* Ts, double* Ys) {
+    for (int t = threadIdx.x; t < kpp * 8; t += PNT) {
+        const int r = t % kpp, c = t / kpp;
+        double s = 0.0;
+        for (int k = 0; k <= c; ++k) s += G[k * kpp + r] * Tbb[c * 8 + k];
+        Ys[c * kpp + r] = s;
+    }
+    for (int t = threadIdx.x; t < kpp * kpp; t += PNT) {
+        const int r = t % kpp, c = t / kpp;
+        Ts[c * kpp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kpp * 8; t += PNT) {
+        const int r = t % kpp, c = t / kpp;
+        double s = 0.0;
+        for (int k = r; k < kpp; ++k) s += Ts[k * kpp + r] * Ys[c * kpp + k];
+        T[(kpp + c) * ELM_NB + r] = -s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(PNT, 1) k_panel_p(PanelArgs a, int nb) {
+    extern __shared__ __align__(16) double sm[];
+    const int sl = a.s_off + blockIdx.x;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0;
+    const int R = (int)(ld - j0);
+    const int RP = R + 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* Cb = sm;                  // [8][RP]
+    double* Wsm = Cb + 8 * RP;        // [8][kp]
+    double* Zsm = Wsm + 8 * 56;       // [8][kp]
+    double* Gp = Zsm + 8 * 56;        // [8][kp-8]
+    double* red = Gp + 8 * 56;        // [2][PNW][8] column sums (double-buffered)
+    double* ring = red + 2 * PNW * 8; // a.ring doubles: V_prev ring / T staging / reduction scratch
+    double* tot = ring + a.ring;      // [40]
+    double* Tbb = tot + 40;           // [8][8]
+    double* taus = Tbb + 64;          // [8]
+    double* rowfix = taus + 8;        // [8][8] the diagonal rows' new values (written to Cb after the loop)
+    const int sst = (a.ring / VNS) & ~1;
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+    const double* Vp = V + j0;
+    const int kr = lane & 3, cn = lane >> 2;
+
+    for (int b = 0; b < nb / 8; ++b) {
+        const int kp = 8 * b, jb = j0 + kp, d0 = kp;
+        // A. the block: rows [j0, ld) of columns [jb, jb+8)
+        for (int c = 0; c < 8; ++c) {
+            const double* src = A + (int64_t)(jb + c) * ld + j0;
+            for (int r2 = tid; r2 < R / 2; r2 += PNT) {
+                unsigned d = (unsigned)__cvta_generic_to_shared(Cb + c * RP + 2 * r2);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 2 * r2));
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        if (kp > 0) {
+            // B. one pass over V_prev: W = V_prev^T C_b and G = V_prev[:, 0:kp-8]^T V_{b-1}
+            const int kpp = kp - 8;
+            {
+                const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
+                double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+                vp_stream(Vp, ld, R, kp, ring, sst, [&](const double* st, int c, int rch, int nr) {
+                    const int rcp = rch + 4, nq = nr / 8;
+                    if (t < mtiles) {
+                        const bool two = t < mtiles - 1;
+#pragma unroll 4
+                        for (int q = 0; q < nq; ++q) {
+                            const int kk = (2 * q + par) * 4 + kr;
+                            const double av = st[(t * 8 + cn) * rcp + kk];
+                            dmma8(a0, a1, av, Cb[cn * RP + c * rch + kk]);
+                            if (two) dmma8(g0, g1, av, st[(kpp + cn) * rcp + kk]);
+                        }
+                    }
+                });
+                double* pb = Zsm;  // pair-sum scratch: [mtiles][64] x 2 products <= 896 doubles
+                if (t < mtiles && par == 1) {
+                    pb[t * 64 + lane * 2] = a0;
+                    pb[t * 64 + lane * 2 + 1] = a1;
+                    ring[t * 64 + lane * 2] = g0;
+                    ring[t * 64 + lane * 2 + 1] = g1;
+                }
+                __syncthreads();
+                if (t < mtiles && par == 0) {
+                    a0 += pb[t * 64 + lane * 2];
+                    a1 += pb[t * 64 + lane * 2 + 1];
+                    Wsm[(2 * kr) * kp + t * 8 + cn] = a0;
+                    Wsm[(2 * kr + 1) * kp + t * 8 + cn] = a1;
+                    if (t < mtiles - 1) {
+                        g0 += ring[t * 64 + lane * 2];
+                        g1 += ring[t * 64 + lane * 2 + 1];
+                        Gp[(2 * kr) * kpp + t * 8 + cn] = g0;
+                        Gp[(2 * kr + 1) * kpp + t * 8 + cn] = g1;
+                    }
+                }
+                __syncthreads();
+            }
+            // C. T extension by block b-1 (Tbb still holds its T), then Z = T^T W
+            if (kpp > 0) t_extend(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
+            {
+                double* Ts = ring;
+                for (int t = tid; t < kp * kp; t += PNT) {
+                    const int r = t % kp, c = t / kp;
+                    Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+                }
+                __syncthreads();
+                for (int t = tid; t < kp * 8; t += PNT) {
+                    const int cp = t % kp, c = t / kp;
+                    double s = 0.0;
+                    for (int k = 0; k <= cp; ++k) s += Ts[cp * kp + k] * Wsm[c * kp + k];
+                    Zsm[c * kp + cp] = s;
+                }
+                __syncthreads();
+            }
+            // D. C_b -= V_prev Z (DMMA, V_prev streamed again)
+            {
+                const int ksteps = kp >> 2;
+                double zb[14];
+#pragma unroll
+                for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[cn * kp + t * 4 + kr] : 0.0;
+                __syncthreads();  // Ts (ring) no longer read
+                vp_stream(Vp, ld, R, kp, ring, sst, [&](const double* st, int c, int rch, int nr) {
+                    const int rcp = rch + 4, nmt = nr / 8;
+                    for (int mt = warp; mt < nmt; mt += PNW) {
+                        const int r0 = c * rch + mt * 8;
+                        double c0 = Cb[(2 * kr) * RP + r0 + cn], c1 = Cb[(2 * kr + 1) * RP + r0 + cn];
+#pragma unroll
+                        for (int t = 0; t < 14; ++t)
+                            if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * rcp + mt * 8 + cn], zb[t]);
+                        Cb[(2 * kr) * RP + r0 + cn] = c0;
+                        Cb[(2 * kr + 1) * RP + r0 + cn] = c1;
+                    }
+                });
+            }
+        }
+
+        // E. factor the 8 columns; thread t owns rows t, t + PNT, ... (no trailing barrier)
+        for (int c = 0; c < 8; ++c) {
+            const int d = d0 + c, nk = 8 - c;
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = 0.0;
+            for (int r = tid; r < R; r += PNT) {
+                if (r <= d) continue;
+                const double x = Cb[c * RP + r];
+                v[0] += x * x;
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) v[k] += x * Cb[(c + k) * RP + r];
+            }
+            double* rb = red + (c & 1) * PNW * 8;
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                double h4[4], h2[2], h1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double snd = b4 ? v[i] : v[i + 4];
+                    h4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double snd = b3 ? h4[i] : h4[i + 2];
+                    h2[i] = (b3 ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+                {
+                    const double snd = b2 ? h2[0] : h2[1];
+                    h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+                }
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) rb[warp * 8 + (lane >> 2)] = h1;
+            }
+            __syncthreads();
+            // lane k < 8: the column sum k (fixed-order tree over the warps); lane 8 + k: y_k
+            double mine = 0.0;
+            if (lane < 8) {
+                double p4[4];
+#pragma unroll
+                for (int w4 = 0; w4 < 4; ++w4)
+                    p4[w4] = (rb[(4 * w4) * 8 + lane] + rb[(4 * w4 + 1) * 8 + lane]) +
+                             (rb[(4 * w4 + 2) * 8 + lane] + rb[(4 * w4 + 3) * 8 + lane]);
+                mine = (p4[0] + p4[1]) + (p4[2] + p4[3]);
+            } else if (lane < 16) {
+                mine = (lane - 8 < nk) ? Cb[(c + lane - 8) * RP + d] : 0.0;
+            }
+            const double ts0 = __shfl_sync(0xffffffffu, mine, 0);
+            const double x0 = __shfl_sync(0xffffffffu, mine, 8);
+            const double nrm = sqrt(x0 * x0 + ts0);
+            double alpha = x0, tau = 0.0, scale = 0.0;
+            if (nrm != 0.0) {
+                alpha = x0 >= 0.0 ? -nrm : nrm;
+                scale = 1.0 / (x0 - alpha);
+                tau = (alpha - x0) / alpha;
+            }
+            const double ydl = __shfl_sync(0xffffffffu, mine, (lane & 7) + 8);
+            const double wl = (lane >= 1 && lane < nk) ? tau * (ydl + scale * mine) : 0.0;
+            double w[8], yd[8];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) {
+                w[k] = __shfl_sync(0xffffffffu, wl, k);
+                yd[k] = __shfl_sync(0xffffffffu, mine, k + 8);
+            }
+            if (tau != 0.0) {
+                for (int r = tid; r < R; r += PNT) {
+                    if (r <= d) continue;
+                    const double x = Cb[c * RP + r];
+                    const double vs = scale * x;
+#pragma unroll
+                    for (int k = 1; k < 8; ++k)
+                        if (k < nk) Cb[(c + k) * RP + r] -= w[k] * vs;
+                    Cb[c * RP + r] = vs;
+                }
+            }
+            // the diagonal row's new values: other warps may still be reading row d (lanes 8..15
+            // above), and no later column reads it, so they go to Cb after the loop
+            if (tid == 0) {
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) rowfix[c * 8 + k] = yd[k] - w[k];
+                rowfix[c * 8] = alpha;
+                taus[c] = tau;
+            }
+        }
+        __syncthreads();
+        if (tid < 64) {
+            const int c = tid >> 3, k = tid & 7;
+            if (c + k < 8) Cb[(c + k) * RP + d0 + c] = rowfix[c * 8 + k];
+        }
+        __syncthreads();
+
+        // F. write back R + V and tau; explicit V of the block -> smem and Vbuf
+        for (int c = 0; c < 8; ++c) {
+            const int d = d0 + c;
+            double2* dst = reinterpret_cast<double2*>(A + (int64_t)(jb + c) * ld + j0);
+            double2* dv = reinterpret_cast<double2*>(V + (int64_t)(kp + c) * ld + j0);
+            for (int r2 = tid; r2 < R / 2; r2 += PNT) {
+                const double x0 = Cb[c * RP + 2 * r2], x1 = Cb[c * RP + 2 * r2 + 1];
+                dst[r2] = make_double2(x0, x1);
+                const int r = 2 * r2;
+                const double v0 = r < d ? 0.0 : (r == d ? 1.0 : x0);
+                const double v1 = r + 1 < d ? 0.0 : (r + 1 == d ? 1.0 : x1);
+                Cb[c * RP + r] = v0;
+                Cb[c * RP + r + 1] = v1;
+                dv[r2] = make_double2(v0, v1);
+            }
+        }
+        if (tid < 8) a.tau[(int64_t)sl * a.M + jb + tid] = taus[tid];
+        __syncthreads();
+        // G. T of the block: Tbb[i][i] = tau_i, Tbb[0:i, i] = -tau_i Tbb[0:i,0:i] (Vb^T v_i)[0:i]
+        {
+            double g[28];
+#pragma unroll
+            for (int k = 0; k < 28; ++k) g[k] = 0.0;
+            for (int r = d0 + tid; r < R; r += PNT) {
+                double x[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) x[c] = Cb[c * RP + r];
+                int k = 0;
+#pragma unroll
+                for (int c1 = 0; c1 < 8; ++c1)
+#pragma unroll
+                    for (int c2 = c1 + 1; c2 < 8; ++c2) g[k++] += x[c1] * x[c2];
+            }
+            block_sum<28>(g, ring, tot);
+            if (tid < 32) {
+                const int r = tid & 7;
+                double trow[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[i] : 0.0;
+#pragma unroll
+                for (int i = 1; i < 8; ++i) {
+                    if (r < i) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (k >= r && k < i) {
+                                const int gi = (k * (15 - k)) / 2 + (i - k - 1);
+                                s += trow[k] * tot[gi];
+                            }
+                        trow[i] = -taus[i] * s;
+                    }
+                }
+                if (tid < 8)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) Tbb[i * 8 + r] = trow[i];
+            }
+            __syncthreads();
+        }
+        for (int t = tid; t < 64; t += PNT) {
+            const int r = t % 8, c = t / 8;
+            T[(kp + c) * ELM_NB + kp + r] = Tbb[c * 8 + r];
+        }
+        {
+            const int c = tid / ELM_NB, r = tid % ELM_NB;  // 512 threads = 8 columns x 64 rows
+            if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
+        }
+        __syncthreads();
+    }
+    // H. the last block's T extension: its own Gram pass
+    const int kpp = nb - 8;
+    if (kpp > 0) {
+        vt_block(Vp, ld, R, kpp, Cb, RP, Gp, ring, sst, Zsm);
+        __syncthreads();
+        t_extend(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Fused compact-WY trailing update for one 64-column block of one subdomain:
 //     W = V^T C   (64 x 64, K = R rows)          phase 1, DMMA, 32-row chunks, 2-stage cp.async
 //     Z = -T^T W  (64 x 64)                      phase 2, DMMA
@@ -1564,6 +1887,11 @@ int panel_ring(int64_t R, int smem_optin) {
     return (int)std::max<int64_t>(r, RED_ELEMS);
 }
 size_t panel_smem_bytes(int64_t R, int ring) { return (size_t)(8 * (R + 4) + PANEL_FIXED + ring) * 8; }
+int panelp_ring(int64_t R, int smem_optin) {
+    const int64_t r = ((int64_t)smem_optin / 8 - 8 * (R + 4) - PANELP_FIXED) & ~(int64_t)(2 * VNS - 1);
+    return (int)std::max<int64_t>(r, RED_ELEMS);
+}
+size_t panelp_smem_bytes(int64_t R, int ring) { return (size_t)(8 * (R + 4) + PANELP_FIXED + ring) * 8; }
 
 }  // namespace
 
@@ -1603,6 +1931,9 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     if (e != cudaSuccess) return e;
     const size_t smax = panel_smem_bytes(ld, panel_ring(ld, optin));
     if ((e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)) != cudaSuccess)
+        return e;
+    const bool pp_ok = c->panel_merged && panelp_smem_bytes(ld, panelp_ring(ld, optin)) <= (size_t)optin;
+    if (pp_ok && (e = cudaFuncSetAttribute(k_panel_p, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)panel_cl_smem(((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32))) != cudaSuccess)
@@ -1648,8 +1979,14 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 k_panel_c8<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, panel8_smem(ld - j0, nb), streams[g]>>>(pa, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            } else if (pp_ok && !c->panel_cluster) {
+                KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
+                PanelArgs pp = pa;
+                pp.ring = panelp_ring(ld - j0, optin);
+                k_panel_p<<<(unsigned)(g1 - g0), PNT, panelp_smem_bytes(ld - j0, pp.ring), streams[g]>>>(pp, nb);
+                if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
-            for (int blk = 0; !p8_ok && blk < nb / ELM_BB; ++blk) {
+            for (int blk = 0; !p8_ok && !(pp_ok && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 if (c->panel_cluster)

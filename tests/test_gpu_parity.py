@@ -497,16 +497,18 @@ def test_cg_solver_end_to_end_parity_config1():
     assert rel_l2(res["u"].numpy(), r["u"]) <= 1e-6
 
 
-@pytest.mark.parametrize("cluster,panel8", [("0", "0"), ("1", "0"), ("0", "1")])
-def test_qr_panel_variants_config2(cluster, panel8, monkeypatch):
-    """The three QR panel implementations on config 2 -- one CTA per 8-column block (left-looking,
-    V_prev streamed), a 4-CTA cluster with the rows split, and the on-chip 8-CTA cluster panel
-    (right-looking, all-reduces through distributed shared memory): the Gram identity of the
-    factorisation and u parity with the oracle."""
+@pytest.mark.parametrize("cluster,panel8,merged", [("0", "0", "1"), ("0", "0", "0"), ("1", "0", "1"), ("0", "1", "1")])
+def test_qr_panel_variants_config2(cluster, panel8, merged, monkeypatch):
+    """The four QR panel implementations on config 2 -- one CTA per panel walking its 8-column
+    blocks left-looking with the merged Gram pass (default), one launch per 8-column block, a
+    4-CTA cluster with the rows split, and the on-chip 8-CTA cluster panel (right-looking,
+    all-reduces through distributed shared memory): the Gram identity of the factorisation and u
+    parity with the oracle."""
     import torch
 
     monkeypatch.setenv("ELMDDM_PANEL_CLUSTER", cluster)
     monkeypatch.setenv("ELMDDM_PANEL8", panel8)
+    monkeypatch.setenv("ELMDDM_PANEL_MERGED", merged)
     c = WL.config(2)
     M = c["M"]
     ctx, buf, _ = run_gpu(c, upto="assemble")
