@@ -382,9 +382,9 @@ def main():
                "what": "whole local_factor phase: Householder flop 2mM^2-2M^3/3+2Mk(2m-M) per subdomain / phase time"}
     chol_ms = kms.get("chol", 0.0)
     roof_iface = {"bound": "tensor", "achieved": ctx.sizes["chol_flops"] / (chol_ms * 1e-3) / 1e12 if chol_ms > 0 else None,
-                  "peak": dmma, "unit": "TFLOP/s", "kernel": "k_chol_ll (persistent left-looking envelope Cholesky)",
+                  "peak": dmma, "unit": "TFLOP/s", "kernel": "k_chol_ll (persistent left-looking tile Cholesky, nested-dissection order, list-scheduled)",
                   "flop_per_step": ctx.sizes["chol_flops"], "kernel_ms_per_step": chol_ms,
-                  "what": "2*64^3 per tile update inside the envelope of the interface Schur matrix"}
+                  "what": "2*64^3 per tile update of the symbolic tile factorisation of the interface Schur matrix"}
     roof_iface["frac"] = roof_iface["achieved"] / dmma if roof_iface["achieved"] and dmma else None
     asm_ms = kms["assemble"]
     roof_asm = {"bound": "hbm", "achieved": work["bytes_assemble"] / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,

@@ -166,10 +166,12 @@ elmddm_status elmddm_schur_accumulate(elmddm_ctx* ctx, double* Kaug, double* At,
  * and g[G_pad].  work: >= work_elems doubles.                                                 */
 elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
                                         double* g, double* work, void* stream);
-/* Cholesky M = L L^T in place over the envelope of M (64 x 64 tiles, left-looking) and
- * u = M^{-1} g into uG[G_pad].  On return the off-diagonal tiles of Mband hold L and the
- * diagonal tiles hold L(J,J)^{-1} (lower triangular, zeros above).  g is not modified.
- * Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot.                     */
+/* Cholesky M = L L^T in place over the tile structure of the factorisation order (64 x 64
+ * tiles of L, nested dissection by default -- see elmddm_chol_plan; one persistent left-looking
+ * kernel over a list-scheduled task order) and u = M^{-1} g into uG[G_pad] (strip order).  On
+ * return the tiles of Mband hold L (diagonal tiles: L(J,J), lower triangular).  g is not
+ * modified.  Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot (or a
+ * dependency wait exceeding 10 s).                                                             */
 elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
                                             double* work, void* stream);
 /* The paper's interface solver: unpreconditioned conjugate gradients on
