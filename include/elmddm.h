@@ -118,6 +118,14 @@ int64_t elmddm_band_index(const elmddm_ctx* ctx, int64_t i, int64_t j);
  * order index of every interface unknown; tile_map[chol_blocks^2] = tile id of (I, J), I >= J,
  * or -1; tasks[chol_tasks][2] = (I, J) of every tile task in the kernel's list order.          */
 elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* newidx, int32_t* tile_map, int32_t* tasks);
+/* Host-only planning query (no device, no context): the interface factorisation plan of a P x P
+ * grid with q points per face, ordering 0 strip / 1 nested dissection (reading R25), task list
+ * scheduled for `workers` CTAs (0: column order).  stats[6] = {n, nblk, ntiles, tile updates,
+ * tasks, simulated makespan in ns}; newidx[G], tile_map[nblk*nblk], tasks[ntasks][2] as for
+ * elmddm_chol_plan (each may be NULL; size them from a first call with NULL arrays).
+ * EINVAL for P outside [2, 1024], q outside [1, 4096], another ordering or stats == NULL.     */
+elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t workers, int64_t* stats,
+                                int32_t* newidx, int32_t* tile_map, int32_t* tasks);
 
 /* ---- hot path ----------------------------------------------------------------------------- */
 /* eqn:init: W[S][M][2], b[S][M] for the local subdomains; xi[S][M][2] (may be NULL)

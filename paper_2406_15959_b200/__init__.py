@@ -2,6 +2,6 @@
 C ABI of include/elmddm.h, with a thin Python layer (argument marshalling + torch.distributed).
 """
 from ._lib import ElmddmError, load  # noqa: F401
-from .solver import Context, Problem, partition, solve  # noqa: F401
+from .solver import Context, Problem, partition, plan_query, solve  # noqa: F401
 
-__all__ = ["Context", "Problem", "solve", "partition", "load", "ElmddmError"]
+__all__ = ["Context", "Problem", "solve", "partition", "plan_query", "load", "ElmddmError"]

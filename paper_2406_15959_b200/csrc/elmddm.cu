@@ -177,8 +177,16 @@ elmddm_status build_tables(elmddm_ctx* c) {
     // ordering + symbolic factorisation of the Schur matrix (plan.cu): interface_mode 0 picks the
     // ordering with less factorisation work, 1 / 2 the strip (envelope) order, 3 nested dissection
     std::vector<std::pair<int, int>> fpairs;
-    fpairs.reserve(pairs.size());
-    for (auto& kv : pairs) fpairs.push_back(kv.first);
+    interface_face_pairs(P, fpairs);  // the planner's pattern must be exactly the assembled one
+    {
+        bool same = fpairs.size() == pairs.size();
+        size_t k = 0;
+        for (auto it = pairs.begin(); same && it != pairs.end(); ++it, ++k) same = it->first == fpairs[k];
+        if (!same) {
+            c->err = "internal: interface pattern of the planner differs from the assembly's";
+            return ELMDDM_EINVAL;
+        }
+    }
     const int mode = c->cfg.interface_mode;
     if (mode == 3) {
         build_chol_plan(P, q, F, fpairs, 1, c->crit_band, c->plan);
@@ -397,6 +405,33 @@ elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* newidx, int32_t* ti
     if (newidx)
         for (int64_t f = 0; f < c->faces; ++f)
             for (int k = 0; k < q; ++k) newidx[f * q + k] = pl.fbase[f] + k;
+    if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
+    if (tasks)
+        for (size_t t = 0; t < pl.tasks.size(); ++t) {
+            tasks[2 * t] = pl.tasks[t].I;
+            tasks[2 * t + 1] = pl.tasks[t].J;
+        }
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t workers, int64_t* stats,
+                                int32_t* newidx, int32_t* tile_map, int32_t* tasks) {
+    if (P < 2 || P > 1024 || q < 1 || q > 4096 || ordering < 0 || ordering > 1 || !stats) return ELMDDM_EINVAL;
+    std::vector<std::pair<int, int>> fp;
+    interface_face_pairs(P, fp);
+    const int F = 2 * P * (P - 1);
+    CholPlan pl;
+    build_chol_plan(P, q, F, fp, ordering, 3, pl);
+    const double sim = workers > 0 ? schedule_chol_tasks(pl, workers) : 0.0;
+    stats[0] = pl.n;
+    stats[1] = pl.nblk;
+    stats[2] = pl.ntiles;
+    stats[3] = pl.nupd;
+    stats[4] = (int64_t)pl.tasks.size();
+    stats[5] = (int64_t)(sim * 1000.0);  // simulated makespan, ns
+    if (newidx)
+        for (int f = 0; f < F; ++f)
+            for (int k = 0; k < q; ++k) newidx[(int64_t)f * q + k] = pl.fbase[f] + k;
     if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
     if (tasks)
         for (size_t t = 0; t < pl.tasks.size(); ++t) {

@@ -57,6 +57,7 @@ struct CholPlan {
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
                         int crit_band, CholPlan& pl);
 double schedule_chol_tasks(CholPlan& pl, int workers);
+void interface_face_pairs(int P, std::vector<std::pair<int, int>>& out);
 double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers);
 
 struct elmddm_ctx {

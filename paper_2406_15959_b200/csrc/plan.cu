@@ -86,6 +86,45 @@ void nd_nodes(int P, std::vector<std::vector<int>>& nodes, std::vector<int>& dep
 
 }  // namespace
 
+// Structurally nonzero q x q face blocks (b, c), b >= c, of the interface matrix M = sum_s
+// scatter(T_E^T T_E) + Q^T Q (eqn:schur): faces of one subdomain (the S1 term), and the faces of
+// the two subdomains adjacent to a flux face (the Q^T Q term).  Strip face numbering (R14).
+void interface_face_pairs(int P, std::vector<std::pair<int, int>>& out) {
+    out.clear();
+    if (P < 2) return;
+    const int N = P * P, F = 2 * P * (P - 1), strip = 2 * P - 1;
+    auto fid = [&](int i, int j, int e) {
+        if (e == 0) return i > 0 ? j * strip + (i - 1) : -1;
+        if (e == 1) return i < P - 1 ? j * strip + i : -1;
+        if (e == 2) return j > 0 ? (j - 1) * strip + (P - 1) + i : -1;
+        return j < P - 1 ? j * strip + (P - 1) + i : -1;
+    };
+    std::vector<int> sub_of(2 * F, -1);
+    for (int s = 0; s < N; ++s)
+        for (int e = 0; e < 4; ++e) {
+            const int f = fid(s % P, s / P, e);
+            if (f >= 0) sub_of[2 * f + ((e == 1 || e == 3) ? 0 : 1)] = s;
+        }
+    std::vector<std::pair<int, int>> v;
+    for (int a = 0; a < F; ++a) {
+        int nb[9], n = 0;
+        nb[n++] = a;
+        for (int k = 0; k < 2; ++k) {
+            const int s = sub_of[2 * a + k];
+            for (int e = 0; e < 4; ++e) {
+                const int f = fid(s % P, s / P, e);
+                if (f >= 0 && f != a) nb[n++] = f;
+            }
+        }
+        for (int x = 0; x < n; ++x)
+            for (int y = 0; y < n; ++y)
+                if (nb[x] >= nb[y]) v.push_back({nb[x], nb[y]});
+    }
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    out.swap(v);
+}
+
 // Build the plan for `ordering` (0 strip, 1 nested dissection).  face_pairs: (b, c), b >= c,
 // structurally nonzero q x q face blocks of M.  Returns the work (tile updates).
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,

@@ -290,6 +290,33 @@ def solve(prob: Problem, xy_host=None, device: int | None = None, group=None, re
     return out
 
 
+def plan_query(P: int, q: int, ordering: int = 1, workers: int = 0, arrays: bool = True) -> dict:
+    """Host-only interface-factorisation plan (elmddm_plan_query; no GPU needed): stats and,
+    with arrays=True, the renumbering, tile map and task list."""
+    import numpy as np
+
+    L = _lib.load()
+    st = np.zeros(6, dtype=np.int64)
+    vp = C.c_void_p
+    rc = L.elmddm_plan_query(P, q, ordering, workers, st.ctypes.data_as(vp), None, None, None)
+    if rc != 0:
+        raise _lib.ElmddmError(f"elmddm_plan_query failed: {_lib.STATUS.get(rc, rc)}")
+    out = {"n": int(st[0]), "nblk": int(st[1]), "ntiles": int(st[2]), "nupd": int(st[3]), "ntasks": int(st[4]),
+           "sim_ms": st[5] * 1e-6}
+    if arrays:
+        G = 2 * P * (P - 1) * q
+        nb = out["nblk"]
+        newidx = np.zeros(G, dtype=np.int32)
+        tmap = np.zeros(nb * nb, dtype=np.int32)
+        tasks = np.zeros((out["ntasks"], 2), dtype=np.int32)
+        rc = L.elmddm_plan_query(P, q, ordering, workers, st.ctypes.data_as(vp), newidx.ctypes.data_as(vp),
+                                 tmap.ctypes.data_as(vp), tasks.ctypes.data_as(vp))
+        if rc != 0:
+            raise _lib.ElmddmError(f"elmddm_plan_query failed: {_lib.STATUS.get(rc, rc)}")
+        out.update(newidx=newidx, tile_map=tmap.reshape(nb, nb), tasks=tasks)
+    return out
+
+
 def dmma_peak_tflops(device: int = 0, ms: float = 200.0) -> float:
     """Measured sustained FP64 tensor (DMMA) throughput of `device` (diagnostic)."""
     L = _lib.load()
