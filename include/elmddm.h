@@ -190,6 +190,31 @@ elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, cons
  * tolerance was not reached.                                                                   */
 elmddm_status elmddm_interface_cg(elmddm_ctx* ctx, const double* Mband, const double* g, double* uG, double* work,
                                   double tol, int32_t maxit, int32_t* iters, double* relres, void* stream);
+/* ---- multi-rank interface factorisation ------------------------------
+ * Every rank keeps a full replica of the factor's tile pool (plus L(J,J)^{-1}, the published
+ * C(J, klast) and the completion flags) in one library-owned device region.  All ranks run the
+ * persistent factorisation kernel on the SAME list-scheduled task list, taking tasks through one
+ * shared counter (in rank 0's region); a finished tile is written to every replica over NVLink
+ * peer memory and its flag released in every replica (system scope), so every k-loop reads its
+ * own HBM.  Afterwards every rank holds the whole L and solves for u_Gamma itself (no broadcast).
+ * Protocol: every rank elmddm_dist_export -> all-gather the 64-byte handles -> every rank
+ * elmddm_dist_import(rank, world, handles[world][64]); then per solve: all-reduce Pbuf / Sbuf,
+ * elmddm_interface_assemble into elmddm_dist_pool's buffer, elmddm_interface_factor_solve with
+ * that buffer (every rank, the same number of times).  CUDA IPC (cudaIpcGetMemHandle /
+ * cudaIpcOpenMemHandle): one process per GPU, peer access over NVLink.  EINVAL on bad
+ * arguments / order; ECUDA if IPC fails (the caller then keeps the rank-0 path).
+ * elmddm_dist_import with world == 1 (handles may be NULL) returns to the single-rank path.    */
+elmddm_status elmddm_dist_export(elmddm_ctx* ctx, void* handle /*[64] bytes out*/);
+elmddm_status elmddm_dist_import(elmddm_ctx* ctx, int32_t rank, int32_t world, const void* handles);
+elmddm_status elmddm_dist_pool(const elmddm_ctx* ctx, double** pool);
+/* One-GPU emulation of nrep (2..8) ranks for testing: ONE cooperative launch whose CTAs are split
+ * into nrep groups, each working as one rank on its own replica (separate allocations), with the
+ * multi-rank publication protocol.  Factors a copy of the assembled Mband (not modified), solves
+ * into uG from replica 0, and returns in *ndiff the number of doubles in which the other
+ * replicas' factors differ from replica 0's (0 expected: every tile is computed once and
+ * copied).                                                                                     */
+elmddm_status elmddm_debug_dist_emulate(elmddm_ctx* ctx, int32_t nrep, const double* Mband, const double* g,
+                                        double* uG, double* work, int64_t* ndiff, void* stream);
 /* = interface_assemble + interface_factor_solve. */
 elmddm_status elmddm_interface_solve(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
                                      double* g, double* uG, double* work, void* stream);

@@ -54,6 +54,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// system scope: flags written by (or for) the other GPUs of a multi-rank factorisation
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+    asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -61,10 +70,11 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 // Spin until *flag >= epoch; after ~10 s report ELMDDM_ENUMERIC (info = -1 - tag) and give up
 // instead of hanging the device.
-__device__ __forceinline__ void wait_flag(const int* flag, int epoch, ElmStatus* status, int tag) {
-    if (ld_acquire(flag) >= epoch) return;
+__device__ __forceinline__ void wait_flag(const int* flag, int epoch, ElmStatus* status, int tag, bool sys = false) {
+    auto ld = [&]() { return sys ? ld_acquire_sys(flag) : ld_acquire(flag); };
+    if (ld() >= epoch) return;
     const uint64_t t0 = globaltimer();
-    while (ld_acquire(flag) < epoch) {
+    while (ld() < epoch) {
         __nanosleep(64);
         if (globaltimer() - t0 > 10000000000ull) {
             elm_set_status(status, ELMDDM_ENUMERIC, -1 - tag);
@@ -289,7 +299,7 @@ __device__ __forceinline__ void trsm_refined(double (&x)[4][2][2], double* As, c
 }
 
 struct CholArgs {
-    double* Mb;            // tile pool: tile id t at t * ELM_TS
+    double* Mb;            // tile pool: tile id t at t * ELM_TS (this replica)
     double* Ybuf;          // [nblk] packed tiles: L(J,J)^{-1}
     double* Cbuf;          // [nblk] packed tiles: C(I, klast(I)) before its triangular solve
     int* cready;           // [nblk] Cbuf[I] published (epoch)
@@ -305,6 +315,14 @@ struct CholArgs {
     int epoch;
     ElmStatus* status;
     int* next;             // non-null: tasks dealt dynamically in list order (zeroed counter)
+    // multi-rank factorisation (nrep > 1, dynamic dealing through the shared counter `next`):
+    // every rank holds a full replica of the tile pool, Ybuf, Cbuf and the flags; a finished tile
+    // is written to every replica, then its flag is released in every replica (system scope), so
+    // all k-loop reads stay in the rank's own HBM.  CTA b works as replica rep_base + b / ctas_per_rep
+    // (one launch per GPU: rep_base = rank, ctas_per_rep = gridDim.x; one-GPU emulation of several
+    // ranks: rep_base = 0 and the grid split among the replicas).
+    int nrep, rep_base, ctas_per_rep;
+    const CholRep* reps;   // [nrep]
 };
 
 __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
@@ -322,7 +340,26 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    auto tileptr = [&](int t) { return a.Mb + (int64_t)t * TILE; };
+    const bool dist = a.nrep > 1;
+    const int my = dist ? a.rep_base + (int)blockIdx.x / a.ctas_per_rep : 0;
+    double* const Mb = dist ? a.reps[my].Mb : a.Mb;
+    double* const Ybuf = dist ? a.reps[my].Ybuf : a.Ybuf;
+    double* const Cbuf = dist ? a.reps[my].Cbuf : a.Cbuf;
+    int* const flags = dist ? a.reps[my].flags : a.flags;
+    int* const cready = dist ? a.reps[my].cready : a.cready;
+    auto tileptr = [&](int t) { return Mb + (int64_t)t * TILE; };
+    // copy a finished 64-tile (offset off doubles in each replica's region `which`) from this
+    // replica to all the others (16-byte vector loads / stores, all threads), then make the
+    // stores visible system-wide; the caller releases the flags afterwards
+    auto push = [&](int which, int64_t off) {
+        const double2* src = reinterpret_cast<const double2*>((which == 0 ? Mb : (which == 1 ? Ybuf : Cbuf)) + off);
+        for (int r = 0; r < a.nrep; ++r) {
+            if (r == my) continue;
+            double* base = which == 0 ? a.reps[r].Mb : (which == 1 ? a.reps[r].Ybuf : a.reps[r].Cbuf);
+            double2* dst2 = reinterpret_cast<double2*>(base + off);
+            for (int x = tid; x < TILE / 2; x += NT) dst2[x] = __ldcg(src + x);
+        }
+    };
     int known = 0;        // (thread 0) every column < known is complete
     uint32_t gchunk = 0;  // chunk loads issued by this CTA so far (stage = gchunk % NSTAGE)
     uint32_t epi_uses = 0;
@@ -336,11 +373,13 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         struct Acc { unsigned long long& r; uint64_t q; __device__ ~Acc() { r += globaltimer() - q; } } acc_{pf_flag, q0};
 #endif
         const int k = e.z;
-        if (k < known) return;
-        while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
-        if (k < known) return;
-        wait_flag(a.flags + e.x, a.epoch, a.status, k);
-        wait_flag(a.flags + e.y, a.epoch, a.status, k);
+        if (!dist) {
+            if (k < known) return;
+            while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
+            if (k < known) return;
+        }
+        wait_flag(flags + e.x, a.epoch, a.status, k, dist);
+        wait_flag(flags + e.y, a.epoch, a.status, k, dist);
     };
     // static dealing: CTAs [0, crit_ctas) take the critical list round-robin, the others the
     // rest; dynamic dealing (a.next): every CTA takes the next task of the (list-scheduled) order
@@ -352,7 +391,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
     const int t_step = critw ? a.crit_ctas : (int)gridDim.x - a.crit_ctas;
     for (int t = t_begin;; t += t_step) {
         if (a.next) {
-            if (tid == 0) s_next = atomicAdd(a.next, 1);
+            if (tid == 0) s_next = dist ? atomicAdd_system(a.next, 1) : atomicAdd(a.next, 1);
             __syncthreads();
             t = s_next;
         }
@@ -427,13 +466,13 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 const uint32_t epar = (epi_uses / NSTAGE) & 1;
                 ++epi_uses;
                 if (tid == 0) {
-                    wait_flag(a.cready + J, a.epoch, a.status, J);
-                    wait_flag(a.flags + a.diag_tid[td.klast], a.epoch, a.status, td.klast);
+                    wait_flag(cready + J, a.epoch, a.status, J, dist);
+                    wait_flag(flags + a.diag_tid[td.klast], a.epoch, a.status, td.klast, dist);
                     fence_proxy_async();
                     mbar_expect(eb, 3 * TILE * 8);
-                    bulk_load(As, a.Cbuf + (int64_t)J * TILE, TILE * 8, eb);
+                    bulk_load(As, Cbuf + (int64_t)J * TILE, TILE * 8, eb);
                     bulk_load(Bs, tileptr(a.diag_tid[td.klast]), TILE * 8, eb);
-                    bulk_load(Ys, a.Ybuf + (int64_t)td.klast * TILE, TILE * 8, eb);
+                    bulk_load(Ys, Ybuf + (int64_t)td.klast * TILE, TILE * 8, eb);
                 }
                 DSTAMP(1);
                 mbar_wait(eb, epar);
@@ -453,10 +492,16 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             const int bad = potrf_inv_tile(As, Ys, rsv);
             DSTAMP(5);
             if (bad >= 0 && tid == 0) elm_set_status(a.status, ELMDDM_ENUMERIC, J * NB + bad);
-            double* yd = a.Ybuf + (int64_t)J * TILE;
+            double* yd = Ybuf + (int64_t)J * TILE;
             for (int x = tid; x < TILE / 2; x += NT) {
                 reinterpret_cast<double2*>(dst)[x] = reinterpret_cast<const double2*>(As)[x];
                 reinterpret_cast<double2*>(yd)[x] = reinterpret_cast<const double2*>(Ys)[x];
+            }
+            if (dist) {  // L(J,J) and its inverse to the other replicas
+                __threadfence_block();
+                __syncthreads();
+                push(0, (int64_t)td.tid * TILE);
+                push(1, (int64_t)J * TILE);
             }
             DSTAMP(6);
             __threadfence();
@@ -470,11 +515,20 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             // C -> As[c * LP + r]
             FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
             if (td.pub) {  // publish C(I, J = klast(I)) for the diagonal task of row I
-                double* cb = a.Cbuf + (int64_t)I * TILE;
+                double* cb = Cbuf + (int64_t)I * TILE;
                 FOR_FRAG cb[frag_c(nt, e) * LP + frag_r(mt)] = -acc[mt][nt][e];
-                __threadfence();
-                __syncthreads();
-                if (tid == 0) st_release(a.cready + I, a.epoch);
+                if (dist) {
+                    __syncthreads();
+                    push(2, (int64_t)I * TILE);
+                    __threadfence_system();
+                    __syncthreads();
+                    if (tid == 0)
+                        for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].cready + I, a.epoch);
+                } else {
+                    __threadfence();
+                    __syncthreads();
+                    if (tid == 0) st_release(cready + I, a.epoch);
+                }
             }
             // L(I,J) solves X L_JJ^T = C
             uint64_t* eb = &bar[NSTAGE + (epi_uses % NSTAGE)];
@@ -484,13 +538,13 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #ifdef ELM_CHOL_PROF
                 const uint64_t pw = globaltimer();
 #endif
-                wait_flag(a.flags + a.diag_tid[J], a.epoch, a.status, J);
+                wait_flag(flags + a.diag_tid[J], a.epoch, a.status, J, dist);
 #ifdef ELM_CHOL_PROF
                 pf_flag += globaltimer() - pw;
 #endif
                 fence_proxy_async();
                 mbar_expect(eb, 2 * TILE * 8);
-                bulk_load(Ys, a.Ybuf + (int64_t)J * TILE, TILE * 8, eb);
+                bulk_load(Ys, Ybuf + (int64_t)J * TILE, TILE * 8, eb);
                 bulk_load(Bs, tileptr(a.diag_tid[J]), TILE * 8, eb);
             }
             __syncthreads();  // C visible to every warp
@@ -498,11 +552,23 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             double x0[4][2][2];
             trsm_refined(x0, As, Bs, Ys);
             FOR_FRAG dst[frag_r(mt) + frag_c(nt, e) * LP] = x0[mt][nt][e];
+            if (dist) {  // L(I,J) to the other replicas
+                __threadfence_block();
+                __syncthreads();
+                push(0, (int64_t)td.tid * TILE);
+            }
         }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) {
-            st_release(a.flags + td.tid, a.epoch);
+        if (dist) {
+            __threadfence_system();
+            __syncthreads();
+            if (tid == 0)
+                for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].flags + td.tid, a.epoch);
+        } else {
+            __threadfence();
+            __syncthreads();
+        }
+        if (tid == 0 && !dist) {
+            st_release(flags + td.tid, a.epoch);
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.colcnt + J) : "memory");
 #ifdef ELM_CHOL_PROF
             if (t < 400000) {
@@ -654,6 +720,27 @@ extern "C" int elmddm_debug_chol_dprof(void* host, int n) {
 }
 #endif
 
+namespace {
+// multi-rank: wait until every tile of this replica has arrived (the factorisation kernel of
+// this rank can end while other ranks still push their last tiles)
+__global__ void k_drain(const int* flags, int ntiles, int epoch, ElmStatus* status) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+        wait_flag(flags + t, epoch, status, t, true);
+}
+// number of differing doubles between two buffers (one-GPU emulation check)
+__global__ void k_count_diff(const double* a, const double* b, int64_t n, unsigned long long* cnt) {
+    unsigned long long loc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        loc += __double_as_longlong(a[i]) != __double_as_longlong(b[i]);
+    if (loc) atomicAdd(cnt, loc);
+}
+}  // namespace
+
+cudaError_t dist_count_diff(const double* a, const double* b, int64_t n, unsigned long long* d_cnt, cudaStream_t st) {
+    k_count_diff<<<592, 256, 0, st>>>(a, b, n, d_cnt);
+    return cudaGetLastError();
+}
+
 cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
                                cudaStream_t st) {
     const CholPlan& pl = c->plan;
@@ -682,14 +769,44 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     if (G > 0) k_perm_gather<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(g, c->d_fbase, q, G, yv);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // factorisation: one cooperative launch over the task list
-    {
+    const DistState& ds = c->dist;
+    const bool dist = ds.nrep > 1;
+    if (dist) {
+        const int nrep = ds.nrep;
+        const int epoch = ++c->chol_epoch;
+        int grid = grid_ll, per = grid_ll;
+        if (ds.emulate) {
+            per = grid_ll / nrep;
+            grid = per * nrep;
+            if ((e = cudaMemsetAsync(ds.counter + (epoch & 1), 0, sizeof(int), st)) != cudaSuccess) return e;
+        } else if (ds.rank == 0) {
+            // slot epoch & 1 was zeroed one factorisation ago; zero the next one (no rank can
+            // still be using it: every rank finished the previous factorisation before the
+            // all-reduce that precedes this one)
+            if ((e = cudaMemsetAsync(ds.counter + ((epoch + 1) & 1), 0, sizeof(int), st)) != cudaSuccess) return e;
+        }
+        const CholRep& mine = ds.reps[ds.emulate ? 0 : ds.rank];
+        CholArgs a{mine.Mb, mine.Ybuf, mine.Cbuf, mine.cready, c->d_tasks, (int)pl.tasks.size(), 0, 0, c->d_klist,
+                   c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, c->d_status, ds.counter + (epoch & 1),
+                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps};
+        void* args[] = {(void*)&a};
+        {
+            KTimer kt(c, ELMDDM_K_POTRF, st);
+            if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=
+                cudaSuccess)
+                return e;
+        }
+        k_drain<<<(unsigned)c->nsm, 256, 0, st>>>(mine.flags, pl.ntiles, epoch, c->d_status);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        Mband = mine.Mb;  // the triangular solves read this rank's replica
+    } else {
         int grid = grid_ll;
         int crit = 32;
         if (const char* env = getenv("ELMDDM_CHOL_CRIT")) crit = atoi(env);
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
                    c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
-                   c->chol_sched ? c->d_chol_next : nullptr};
+                   c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr};
         if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);

@@ -385,6 +385,9 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_chol_next);
     cudaFree(c->d_grf);
     cudaFree(c->d_coef);
+    for (void* pr : c->dist.opened) cudaIpcCloseMemHandle(pr);
+    cudaFree(c->dist.region);
+    cudaFree(c->dist.d_reps);
     cudaFree(c->d_ntc);
     delete c;
 }
@@ -439,6 +442,169 @@ elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t 
             tasks[2 * t + 1] = pl.tasks[t].J;
         }
     return ELMDDM_OK;
+}
+
+// ---- multi-rank interface factorisation (replicated tile pools, CUDA IPC) -------------------
+namespace {
+struct RegionLayout {
+    size_t pool, ybuf, cbuf, flags, cready, counter, bytes;
+};
+RegionLayout region_layout(const elmddm_ctx* c) {
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const CholPlan& pl = c->plan;
+    RegionLayout L{};
+    size_t o = 0;
+    L.pool = o;
+    o = up(o + sizeof(double) * (size_t)pl.ntiles * ELM_TS);
+    L.ybuf = o;
+    o = up(o + sizeof(double) * (size_t)pl.nblk * ELM_TS);
+    L.cbuf = o;
+    o = up(o + sizeof(double) * (size_t)pl.nblk * ELM_TS);
+    L.flags = o;
+    o = up(o + sizeof(int) * (size_t)pl.ntiles);
+    L.cready = o;
+    o = up(o + sizeof(int) * (size_t)pl.nblk);
+    L.counter = o;
+    o = up(o + sizeof(int) * 2);
+    L.bytes = o;
+    return L;
+}
+CholRep region_rep(void* base, const RegionLayout& L) {
+    char* b = static_cast<char*>(base);
+    return CholRep{reinterpret_cast<double*>(b + L.pool), reinterpret_cast<double*>(b + L.ybuf),
+                   reinterpret_cast<double*>(b + L.cbuf), reinterpret_cast<int*>(b + L.flags),
+                   reinterpret_cast<int*>(b + L.cready)};
+}
+cudaError_t alloc_region(const RegionLayout& L, void** out) {
+    cudaError_t e = cudaMalloc(out, L.bytes);
+    if (e != cudaSuccess) return e;
+    return cudaMemset(static_cast<char*>(*out) + L.flags, 0, L.bytes - L.flags);  // flags, cready, counter
+}
+}  // namespace
+
+elmddm_status elmddm_dist_export(elmddm_ctx* c, void* handle) {
+    CHECK_CTX(c);
+    if (!handle) return ELMDDM_EINVAL;
+    DeviceGuard dg(c->device);
+    const RegionLayout L = region_layout(c);
+    cudaError_t e = cudaSuccess;
+    if (!c->dist.region) {
+        if ((e = alloc_region(L, &c->dist.region)) != cudaSuccess) return cuda_fail(c, e, "elmddm_dist_export");
+        c->dist.region_bytes = L.bytes;
+    }
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, c->dist.region)) != cudaSuccess) return cuda_fail(c, e, "elmddm_dist_export");
+    std::memcpy(handle, &h, sizeof(h));
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_dist_import(elmddm_ctx* c, int32_t rank, int32_t world, const void* handles) {
+    CHECK_CTX(c);
+    if (world == 1) {  // back to the single-rank path
+        DeviceGuard dg(c->device);
+        for (void* pr : c->dist.opened) cudaIpcCloseMemHandle(pr);
+        cudaFree(c->dist.d_reps);
+        c->dist.opened.clear();
+        c->dist.d_reps = nullptr;
+        c->dist.reps.clear();
+        c->dist.nrep = 1;
+        c->dist.rank = 0;
+        c->dist.counter = nullptr;
+        return ELMDDM_OK;
+    }
+    if (world < 2 || rank < 0 || rank >= world || !handles || !c->dist.region) {
+        c->err = "elmddm_dist_import: need world >= 2, 0 <= rank < world, handles, and elmddm_dist_export first";
+        return ELMDDM_EINVAL;
+    }
+    DeviceGuard dg(c->device);
+    const RegionLayout L = region_layout(c);
+    std::vector<CholRep> reps(world);
+    std::vector<void*> opened;
+    cudaError_t e = cudaSuccess;
+    void* rank0 = nullptr;
+    for (int r = 0; r < world; ++r) {
+        void* base = c->dist.region;
+        if (r != rank) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+            if ((e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess) {
+                for (void* pr : opened) cudaIpcCloseMemHandle(pr);
+                return cuda_fail(c, e, "elmddm_dist_import (cudaIpcOpenMemHandle)");
+            }
+            opened.push_back(base);
+        }
+        if (r == 0) rank0 = base;
+        reps[r] = region_rep(base, L);
+    }
+    CholRep* d = nullptr;
+    if ((e = cudaMalloc((void**)&d, sizeof(CholRep) * world)) != cudaSuccess ||
+        (e = cudaMemcpy(d, reps.data(), sizeof(CholRep) * world, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        for (void* pr : opened) cudaIpcCloseMemHandle(pr);
+        cudaFree(d);
+        return cuda_fail(c, e, "elmddm_dist_import");
+    }
+    for (void* pr : c->dist.opened) cudaIpcCloseMemHandle(pr);
+    cudaFree(c->dist.d_reps);
+    c->dist.opened = opened;
+    c->dist.d_reps = d;
+    c->dist.reps = reps;
+    c->dist.nrep = world;
+    c->dist.rank = rank;
+    c->dist.emulate = false;
+    c->dist.counter = reinterpret_cast<int*>(static_cast<char*>(rank0) + L.counter);
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_dist_pool(const elmddm_ctx* c, double** pool) {
+    CHECK_CTX(c);
+    if (!pool || !c->dist.region) return ELMDDM_EINVAL;
+    *pool = region_rep(c->dist.region, region_layout(c)).Mb;
+    return ELMDDM_OK;
+}
+
+elmddm_status elmddm_debug_dist_emulate(elmddm_ctx* c, int32_t nrep, const double* Mband, const double* g, double* uG,
+                                        double* work, int64_t* ndiff, void* stream) {
+    CHECK_CTX(c);
+    if (nrep < 2 || nrep > 8 || !Mband || !g || !uG || !work || !ndiff || c->dist.nrep > 1) return ELMDDM_EINVAL;
+    DeviceGuard dg(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const RegionLayout L = region_layout(c);
+    std::vector<void*> regs(nrep, nullptr);
+    std::vector<CholRep> reps(nrep);
+    cudaError_t e = cudaSuccess;
+    CholRep* d = nullptr;
+    unsigned long long* dcnt = nullptr;
+    unsigned long long hcnt = 0;
+    const DistState saved = c->dist;
+    for (int r = 0; r < nrep && e == cudaSuccess; ++r) {
+        if ((e = alloc_region(L, &regs[r])) != cudaSuccess) break;
+        reps[r] = region_rep(regs[r], L);
+        e = cudaMemcpyAsync(reps[r].Mb, Mband, sizeof(double) * (size_t)c->plan.ntiles * ELM_TS, cudaMemcpyDeviceToDevice,
+                            st);
+    }
+    if (e == cudaSuccess && (e = cudaMalloc((void**)&d, sizeof(CholRep) * nrep)) == cudaSuccess &&
+        (e = cudaMemcpy(d, reps.data(), sizeof(CholRep) * nrep, cudaMemcpyHostToDevice)) == cudaSuccess &&
+        (e = cudaMalloc((void**)&dcnt, sizeof(unsigned long long))) == cudaSuccess &&
+        (e = cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), st)) == cudaSuccess) {
+        c->dist.nrep = nrep;
+        c->dist.rank = 0;
+        c->dist.emulate = true;
+        c->dist.reps = reps;
+        c->dist.d_reps = d;
+        c->dist.counter = reinterpret_cast<int*>(static_cast<char*>(regs[0]) + L.counter);
+        e = run_cholesky_solve(c, reps[0].Mb, g, uG, work, st);
+        for (int r = 1; r < nrep && e == cudaSuccess; ++r)
+            e = dist_count_diff(reps[0].Mb, reps[r].Mb, (int64_t)c->plan.ntiles * ELM_TS, dcnt, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&hcnt, dcnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
+    c->dist = saved;
+    for (void* r : regs) cudaFree(r);
+    cudaFree(d);
+    cudaFree(dcnt);
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_debug_dist_emulate");
+    *ndiff = (int64_t)hcnt;
+    return elmddm_sync(c, stream);
 }
 
 int64_t elmddm_band_index(const elmddm_ctx* c, int64_t i, int64_t j) {

@@ -43,6 +43,27 @@ struct TaskDesc {
 };
 
 // ordering and symbolic factorisation of the interface Schur matrix at 64-tile granularity
+// One replica of the multi-rank interface factorisation (chol.cu k_chol_ll, nrep > 1).
+struct CholRep {
+    double* Mb;     // tile pool [ntiles][ELM_TS]
+    double* Ybuf;   // [nblk][ELM_TS] L(J,J)^{-1}
+    double* Cbuf;   // [nblk][ELM_TS] published C(I, klast(I))
+    int* flags;     // [ntiles] tile completion (epoch)
+    int* cready;    // [nblk] Cbuf published (epoch)
+};
+// Multi-rank state: every rank holds a full replica in one cudaMalloc'd region (exported /
+// imported with CUDA IPC); one-GPU emulation keeps all replicas in this process.
+struct DistState {
+    int nrep = 1, rank = 0;
+    bool emulate = false;
+    std::vector<CholRep> reps;   // host copy of the table
+    CholRep* d_reps = nullptr;   // device table [nrep]
+    int* counter = nullptr;      // task counter slots [2] in rank 0's region (epoch parity)
+    void* region = nullptr;      // this rank's region
+    size_t region_bytes = 0;
+    std::vector<void*> opened;   // peer regions opened through IPC (closed on destroy)
+};
+
 struct CholPlan {
     int ordering = 0;                 // 0 strip (envelope), 1 nested dissection
     int64_t n = 0;                    // unknowns in the factorisation order (multiple of 64)
@@ -108,6 +129,7 @@ struct elmddm_ctx {
     double* d_grf = nullptr;         // problem 6: eqn:grf parameters [ngrf][4] (elmddm_set_coefficient)
     int ngrf = 0;
     double* d_coef = nullptr;        // problem 6: [S][p*p][4] rho, grad rho at the interior points
+    mutable DistState dist;          // multi-rank interface factorisation (elmddm_dist_*)
     int panel_merged = 1;            // ELMDDM_PANEL_MERGED: one launch per panel, merged Gram pass (k_panel_p)
     int panel8 = 0;                  // ELMDDM_PANEL8: on-chip 8-CTA cluster panels (qr.cu k_panel_c8)
     int chol_sched = 1;              // ELMDDM_CHOL_SCHED: 1 list-scheduled task order, dynamic dealing
@@ -211,6 +233,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
                                  double* work, cudaStream_t st);
 cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
                                    double* g, double* work, cudaStream_t st);
+cudaError_t dist_count_diff(const double* a, const double* b, int64_t n, unsigned long long* d_cnt, cudaStream_t st);
 cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double* g, double* uG, double* work,
                                cudaStream_t st);
 cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,

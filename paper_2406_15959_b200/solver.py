@@ -22,6 +22,8 @@ from . import _lib
 def _ptr(t):
     if t is None:
         return None
+    if isinstance(t, int):  # raw device pointer (a library-owned buffer, e.g. elmddm_dist_pool)
+        return C.c_void_p(t)
     if not t.is_cuda:
         raise _lib.ElmddmError("elmddm arrays must be CUDA tensors")
     if t.dtype != torch.float64:
@@ -194,6 +196,14 @@ class Context:
                 "count": {k: int(t.count[i]) for i, k in enumerate(_lib.KCLASSES)},
                 "ms": {k: float(t.ms[i]) for i, k in enumerate(_lib.KCLASSES)}}
 
+    def debug_dist_emulate(self, nrep, Mband, g, uG, work, stream=None) -> int:
+        """One-GPU emulation of the multi-rank factorisation (elmddm_debug_dist_emulate); returns
+        the number of doubles in which the replicas' factors differ (0 expected)."""
+        nd = C.c_int64()
+        self._check(self.L.elmddm_debug_dist_emulate(self.h, nrep, _ptr(Mband), _ptr(g), _ptr(uG), _ptr(work),
+                                                       C.byref(nd), _stream(stream)), "elmddm_debug_dist_emulate")
+        return nd.value
+
     def chol_plan(self):
         """(newidx[G], tile_map[chol_blocks, chol_blocks], tasks[chol_tasks, 2]) of the interface
         factorisation (host arrays): the factorisation-order index of every interface unknown,
@@ -213,13 +223,72 @@ class Context:
         return int(self.L.elmddm_band_index(self.h, i, j))
 
     # ---- Algorithm 1 -------------------------------------------------------------------------
+    # ---- multi-rank interface factorisation (include/elmddm.h elmddm_dist_*) ----
+    def _dist_export(self):
+        h = (C.c_uint8 * 64)()
+        rc = self.L.elmddm_dist_export(self.h, C.cast(h, C.c_void_p))
+        return bytes(h) if rc == 0 else None
+
+    def _dist_import(self, rank, world, handles):
+        blob = b"".join(handles)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        return self.L.elmddm_dist_import(self.h, rank, world, C.cast(buf, C.c_void_p)) == 0
+
+    def _dist_disable(self):
+        self.L.elmddm_dist_import(self.h, 0, 1, None)
+
+    def _dist_pool(self):
+        p = C.c_void_p()
+        self._check(self.L.elmddm_dist_pool(self.h, C.byref(p)), "elmddm_dist_pool")
+        return int(p.value)
+
+    def dist_setup(self, group=None) -> bool:
+        """Collectively switch this context to the multi-rank interface factorisation: every
+        rank exports its replica region, the CUDA IPC handles are all-gathered, every rank opens
+        the others'.  All ranks agree on the outcome; on any failure (or ELMDDM_DIST_IFACE=0, or
+        the CG solver) every rank keeps the rank-0 path.  Returns whether it is active."""
+        import os
+
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        want = os.environ.get("ELMDDM_DIST_IFACE", "1") != "0" and self.prob.interface_solver == "cholesky"
+        want = want and self.sizes["G"] > 0
+
+        def agree(flag: bool) -> bool:
+            t = torch.tensor([1 if flag else 0], dtype=torch.int32,
+                             device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            return bool(t.item())
+
+        if not agree(want):
+            return False
+        h = self._dist_export()
+        hs = [None] * world
+        dist.all_gather_object(hs, h, group=group)
+        if not agree(all(x is not None for x in hs)):
+            return False
+        ok = self._dist_import(rank, world, hs)
+        if not agree(ok):
+            if ok:
+                self._dist_disable()
+            return False
+        self._dist_pool_ptr = self._dist_pool()
+        return True
+
     def run(self, buf: dict, xy=None, u=None, group=None, stream=None, timer=None):
-        """One pass of the hot path on this rank.  With a process group of size > 1 the Schur
-        contributions are summed on rank 0 (NCCL reduce) and u_Gamma is broadcast back."""
+        """One pass of the hot path on this rank.  With a process group of size > 1: either the
+        multi-rank interface factorisation (Schur contributions all-reduced, every rank factors
+        its share of the tiles into its replica and solves u_Gamma itself; see dist_setup), or
+        the contributions are summed on rank 0 (NCCL reduce) and u_Gamma is broadcast back."""
         import torch.distributed as dist
 
         world = dist.get_world_size(group) if (group is not None or (dist.is_available() and dist.is_initialized())) else 1
         rank = dist.get_rank(group) if world > 1 else 0
+        if world > 1 and getattr(self, "_dist", None) is None:
+            self._dist = self.dist_setup(group)
+        dmode = world > 1 and bool(getattr(self, "_dist", False))
         mark = timer.mark if timer is not None else (lambda name: None)
         self.init_hidden(buf["W"], buf["b"], None, stream)
         mark("init_hidden")
@@ -233,10 +302,20 @@ class Context:
         self.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"], stream)
         mark("schur_accumulate")
         if world > 1:
-            dist.reduce(buf["Pbuf"], dst=0, group=group)
-            dist.reduce(buf["Sbuf"], dst=0, group=group)
+            if dmode:
+                dist.all_reduce(buf["Pbuf"], group=group)
+                dist.all_reduce(buf["Sbuf"], group=group)
+            else:
+                dist.reduce(buf["Pbuf"], dst=0, group=group)
+                dist.reduce(buf["Sbuf"], dst=0, group=group)
             mark("reduce")
-        if self.sizes["G"] > 0:
+        if self.sizes["G"] > 0 and dmode:
+            pool = self._dist_pool_ptr
+            self.interface_assemble(buf["Pbuf"], buf["Sbuf"], pool, buf["g"], buf["work"], stream)
+            mark("interface_assemble")
+            self.interface_factor_solve(pool, buf["g"], buf["uG"], buf["work"], stream)
+            mark("interface_factor_solve")
+        elif self.sizes["G"] > 0:
             if rank == 0:
                 self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
                 mark("interface_assemble")

@@ -1,6 +1,9 @@
-"""World-size-2 `gloo` tests (CPU) of the multi-rank plumbing of Context.run:
+"""World-size-2/3 `gloo` tests (CPU) of the multi-rank plumbing of Context.run:
 partition, zero-filled globally indexed Schur buffers summed by reduce(SUM) = exact union,
-rank-0 interface solve, broadcast of u_Gamma, reduce of the slab-wise evaluation.
+rank-0 interface solve, broadcast of u_Gamma, reduce of the slab-wise evaluation -- and the
+multi-rank interface factorisation mode (dist_setup's collective agreement on the CUDA IPC
+exchange; all-reduce of the buffers; every rank factors and solves; no broadcast), including the
+collective fallback when one rank cannot export its region.
 
 The CUDA kernels are replaced by a fake context whose calls write slab-tagged values, so the
 test checks exactly the host-side collective sequence the GPU path uses."""
@@ -26,7 +29,7 @@ def _free_port():
     return p
 
 
-def _fake_ctx(rank, world):
+def _fake_ctx(rank, world, mode="off"):
     from paper_2406_15959_b200 import solver as S
 
     s0, s1 = S.partition(N_SUB, world, rank)
@@ -40,6 +43,22 @@ def _fake_ctx(rank, world):
 
         def __del__(self):
             pass
+
+        # CUDA IPC hooks of dist_setup (the collective logic around them is the real one)
+        def _dist_export(self):
+            self.calls.append("dist_export")
+            return None if (mode == "fail1" and rank == 1) else bytes([rank]) * 64
+
+        def _dist_import(self, r, w, handles):
+            self.calls.append("dist_import")
+            assert r == rank and w == world and [h[0] for h in handles] == list(range(world))
+            return True
+
+        def _dist_disable(self):
+            self.calls.append("dist_disable")
+
+        def _dist_pool(self):
+            return 0
 
         def init_hidden(self, W, b, xi=None, stream=None):
             self.calls.append("init_hidden")
@@ -77,11 +96,12 @@ def _fake_ctx(rank, world):
     return Fake()
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode="off"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ["ELMDDM_DIST_IFACE"] = "0" if mode == "off" else "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ctx = _fake_ctx(rank, world)
+        ctx = _fake_ctx(rank, world, mode)
         f64 = dict(dtype=torch.float64)
         buf = {"W": torch.zeros(1, **f64), "b": torch.zeros(1, **f64), "Kaug": torch.zeros(1, **f64),
                "At": torch.zeros(1, **f64), "tau": torch.zeros(1, **f64), "work": torch.zeros(1, **f64),
@@ -94,6 +114,50 @@ def _worker(rank, world, port, q):
         q.put((rank, ctx.calls, buf["Pbuf"].tolist(), buf["uG"].tolist(), buf["coef"].tolist(), u.tolist()))
     finally:
         dist.destroy_process_group()
+
+
+def _run(world, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=120)
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_interface_mode_gloo(world):
+    """Multi-rank factorisation mode: every rank sees the full union of the Schur buffers
+    (all-reduce), assembles and factors, and ends with the same u_Gamma without a broadcast."""
+    res = _run(world, "on")
+    expect_P = [float(s + 1) for s in range(N_SUB) for _ in range(SLOT)]
+    g_expect = sum(expect_P) + 0.5 * sum(expect_P)
+    for r in range(world):
+        calls, P, uG, coef, u = res[r]
+        assert calls[:2] == ["dist_export", "dist_import"]
+        assert "interface_assemble" in calls and "interface_factor_solve" in calls
+        assert P == expect_P and uG == [g_expect] * G and coef == [g_expect] * 3
+    assert res[0][4] == [g_expect + t for t in range(NPTS)]
+
+
+def test_dist_interface_collective_fallback_gloo():
+    """One rank cannot export its region: no rank imports, all keep the rank-0 path."""
+    res = _run(3, "fail1")
+    expect_P = [float(s + 1) for s in range(N_SUB) for _ in range(SLOT)]
+    g_expect = sum(expect_P) + 0.5 * sum(expect_P)
+    for r in range(3):
+        calls, P, uG, coef, u = res[r]
+        assert "dist_import" not in calls
+        assert ("interface_factor_solve" in calls) == (r == 0)
+        assert uG == [g_expect] * G
 
 
 @pytest.mark.parametrize("world", [2, 3])
