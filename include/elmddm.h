@@ -207,6 +207,11 @@ elmddm_status elmddm_interface_cg(elmddm_ctx* ctx, const double* Mband, const do
 elmddm_status elmddm_dist_export(elmddm_ctx* ctx, void* handle /*[64] bytes out*/);
 elmddm_status elmddm_dist_import(elmddm_ctx* ctx, int32_t rank, int32_t world, const void* handles);
 elmddm_status elmddm_dist_pool(const elmddm_ctx* ctx, double** pool);
+/* IPC sanity check after elmddm_dist_import (all ranks, with a host barrier between the phases):
+ * phase 0 stores a word into every peer's region (system-scope release) and adds to a counter in
+ * rank 0's region (system-scope atomic); phase 1 sets *ok = 1 iff every peer's word arrived (and,
+ * on rank 0, the counter is consistent).  Synchronous.                                         */
+elmddm_status elmddm_dist_handshake(elmddm_ctx* ctx, int32_t phase, int32_t* ok);
 /* One-GPU emulation of nrep (2..8) ranks for testing: ONE cooperative launch whose CTAs are split
  * into nrep groups, each working as one rank on its own replica (separate allocations), with the
  * multi-rank publication protocol.  Factors a copy of the assembled Mband (not modified), solves

@@ -43,7 +43,7 @@ STATUS = {0: "ELMDDM_OK", 1: "ELMDDM_EINVAL", 2: "ELMDDM_ENUMERIC", 3: "ELMDDM_E
 EXPORTS = [
     "elmddm_create", "elmddm_destroy", "elmddm_last_error", "elmddm_sizes", "elmddm_sync",
     "elmddm_interface_points", "elmddm_band_index", "elmddm_chol_plan", "elmddm_interface_cg", "elmddm_init_hidden", "elmddm_assemble",
-    "elmddm_set_coefficient", "elmddm_plan_query", "elmddm_dist_export", "elmddm_dist_import", "elmddm_dist_pool",
+    "elmddm_set_coefficient", "elmddm_plan_query", "elmddm_dist_export", "elmddm_dist_import", "elmddm_dist_pool", "elmddm_dist_handshake",
     "elmddm_debug_dist_emulate",
     "elmddm_local_factor", "elmddm_schur_accumulate", "elmddm_interface_assemble",
     "elmddm_interface_factor_solve", "elmddm_interface_solve", "elmddm_back_solve", "elmddm_evaluate",
@@ -91,6 +91,7 @@ def load():
     L.elmddm_dist_export.argtypes = [ctxp, vp]
     L.elmddm_dist_import.argtypes = [ctxp, C.c_int32, C.c_int32, vp]
     L.elmddm_dist_pool.argtypes = [ctxp, C.POINTER(C.c_void_p)]
+    L.elmddm_dist_handshake.argtypes = [ctxp, C.c_int32, C.POINTER(C.c_int32)]
     L.elmddm_debug_dist_emulate.argtypes = [ctxp, C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_int64), vp]
     L.elmddm_local_factor.argtypes = [ctxp, vp, vp, vp, vp]
     L.elmddm_schur_accumulate.argtypes = [ctxp, vp, vp, vp, vp, vp, vp]

@@ -447,7 +447,7 @@ elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t 
 // ---- multi-rank interface factorisation (replicated tile pools, CUDA IPC) -------------------
 namespace {
 struct RegionLayout {
-    size_t pool, ybuf, cbuf, flags, cready, counter, bytes;
+    size_t pool, ybuf, cbuf, flags, cready, counter, hshake, bytes;
 };
 RegionLayout region_layout(const elmddm_ctx* c) {
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -466,6 +466,8 @@ RegionLayout region_layout(const elmddm_ctx* c) {
     o = up(o + sizeof(int) * (size_t)pl.nblk);
     L.counter = o;
     o = up(o + sizeof(int) * 2);
+    L.hshake = o;  // [0..63]: one word per peer rank, [64]: atomic counter (rank 0's region)
+    o = up(o + sizeof(int) * 65);
     L.bytes = o;
     return L;
 }
@@ -543,6 +545,17 @@ elmddm_status elmddm_dist_import(elmddm_ctx* c, int32_t rank, int32_t world, con
         cudaFree(d);
         return cuda_fail(c, e, "elmddm_dist_import");
     }
+    // the task order: list-scheduled for the CTAs of all ranks (every rank computes the same
+    // order from the same plan, so the shared counter deals one list)
+    if (c->chol_sched) {
+        c->chol_sim_us = schedule_chol_tasks(c->plan, 2 * c->nsm * world);
+        if ((e = cudaMemcpy(c->d_tasks, c->plan.tasks.data(), sizeof(TaskDesc) * c->plan.tasks.size(),
+                            cudaMemcpyHostToDevice)) != cudaSuccess) {
+            for (void* pr : opened) cudaIpcCloseMemHandle(pr);
+            cudaFree(d);
+            return cuda_fail(c, e, "elmddm_dist_import");
+        }
+    }
     for (void* pr : c->dist.opened) cudaIpcCloseMemHandle(pr);
     cudaFree(c->dist.d_reps);
     c->dist.opened = opened;
@@ -552,6 +565,65 @@ elmddm_status elmddm_dist_import(elmddm_ctx* c, int32_t rank, int32_t world, con
     c->dist.rank = rank;
     c->dist.emulate = false;
     c->dist.counter = reinterpret_cast<int*>(static_cast<char*>(rank0) + L.counter);
+    return ELMDDM_OK;
+}
+
+// IPC sanity check before the factorisation relies on it: phase 0 writes a word into every
+// peer's region (system-scope release) and adds 1 to rank 0's handshake counter (system-scope
+// atomic); after a host barrier, phase 1 checks that every peer's word arrived and (rank 0)
+// that the counter reads world - 1 + its previous value.
+__global__ void k_dist_hshake(int phase, int rank, int world, int* const* hs, int magic, int* ok) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (phase == 0) {
+        for (int r = 0; r < world; ++r)
+            if (r != rank) asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(hs[r] + rank), "r"(magic) : "memory");
+        if (rank != 0) atomicAdd_system(hs[0] + 64, 1);
+        __threadfence_system();
+        return;
+    }
+    int good = 1;
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) continue;
+        int v;
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(hs[rank] + r) : "memory");
+        good &= v == magic;
+    }
+    if (rank == 0) {
+        int v;
+        asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(hs[0] + 64) : "memory");
+        good &= v % (world - 1) == 0 && v > 0;
+    }
+    *ok = good;
+}
+
+elmddm_status elmddm_dist_handshake(elmddm_ctx* c, int32_t phase, int32_t* ok) {
+    CHECK_CTX(c);
+    if (c->dist.nrep < 2 || c->dist.emulate || (phase != 0 && phase != 1) || !ok) return ELMDDM_EINVAL;
+    DeviceGuard dg(c->device);
+    const RegionLayout L = region_layout(c);
+    const int world = c->dist.nrep;
+    // region bases of every rank (own and opened)
+    std::vector<int*> hs(world);
+    for (int r = 0; r < world; ++r)
+        hs[r] = reinterpret_cast<int*>(reinterpret_cast<char*>(c->dist.reps[r].Mb) - L.pool + L.hshake);
+    int** dhs = nullptr;
+    int* dok = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc((void**)&dhs, sizeof(int*) * world)) != cudaSuccess ||
+        (e = cudaMemcpy(dhs, hs.data(), sizeof(int*) * world, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&dok, sizeof(int))) != cudaSuccess || (e = cudaMemset(dok, 0, sizeof(int))) != cudaSuccess) {
+        cudaFree(dhs);
+        cudaFree(dok);
+        return cuda_fail(c, e, "elmddm_dist_handshake");
+    }
+    k_dist_hshake<<<1, 32>>>(phase, c->dist.rank, world, dhs, 0x5a5a0000 + world, dok);
+    e = cudaDeviceSynchronize();
+    int h = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&h, dok, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(dhs);
+    cudaFree(dok);
+    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_dist_handshake");
+    *ok = phase == 0 ? 1 : h;
     return ELMDDM_OK;
 }
 

@@ -232,7 +232,12 @@ class Context:
     def _dist_import(self, rank, world, handles):
         blob = b"".join(handles)
         buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
-        return self.L.elmddm_dist_import(self.h, rank, world, C.cast(buf, C.c_void_p)) == 0
+        self._dist_imported = self.L.elmddm_dist_import(self.h, rank, world, C.cast(buf, C.c_void_p)) == 0
+        return self._dist_imported
+
+    def _dist_handshake(self, phase):
+        ok = C.c_int32(0)
+        return self.L.elmddm_dist_handshake(self.h, phase, C.byref(ok)) == 0 and ok.value == 1
 
     def _dist_disable(self):
         self.L.elmddm_dist_import(self.h, 0, 1, None)
@@ -262,6 +267,7 @@ class Context:
             dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
             return bool(t.item())
 
+        self._dist_imported = False
         if not agree(want):
             return False
         h = self._dist_export()
@@ -270,8 +276,14 @@ class Context:
         if not agree(all(x is not None for x in hs)):
             return False
         ok = self._dist_import(rank, world, hs)
+        if ok:  # peer stores and atomics really work before the factorisation relies on them
+            ok = self._dist_handshake(0)
+            dist.barrier(group=group)
+            ok = self._dist_handshake(1) and ok
+        else:
+            dist.barrier(group=group)
         if not agree(ok):
-            if ok:
+            if ok or self._dist_imported:
                 self._dist_disable()
             return False
         self._dist_pool_ptr = self._dist_pool()

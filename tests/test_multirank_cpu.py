@@ -52,7 +52,12 @@ def _fake_ctx(rank, world, mode="off"):
         def _dist_import(self, r, w, handles):
             self.calls.append("dist_import")
             assert r == rank and w == world and [h[0] for h in handles] == list(range(world))
+            self._dist_imported = True
             return True
+
+        def _dist_handshake(self, phase):
+            self.calls.append(f"dist_handshake{phase}")
+            return not (mode == "hs_fail2" and rank == 2 and phase == 1)
 
         def _dist_disable(self):
             self.calls.append("dist_disable")
@@ -142,20 +147,23 @@ def test_dist_interface_mode_gloo(world):
     g_expect = sum(expect_P) + 0.5 * sum(expect_P)
     for r in range(world):
         calls, P, uG, coef, u = res[r]
-        assert calls[:2] == ["dist_export", "dist_import"]
+        assert calls[:4] == ["dist_export", "dist_import", "dist_handshake0", "dist_handshake1"]
         assert "interface_assemble" in calls and "interface_factor_solve" in calls
         assert P == expect_P and uG == [g_expect] * G and coef == [g_expect] * 3
     assert res[0][4] == [g_expect + t for t in range(NPTS)]
 
 
-def test_dist_interface_collective_fallback_gloo():
-    """One rank cannot export its region: no rank imports, all keep the rank-0 path."""
-    res = _run(3, "fail1")
+@pytest.mark.parametrize("mode", ["fail1", "hs_fail2"])
+def test_dist_interface_collective_fallback_gloo(mode):
+    """One rank cannot export its region (no rank imports), or one rank's IPC handshake fails
+    (every rank disables the imported peers): all keep the rank-0 path."""
+    res = _run(3, mode)
     expect_P = [float(s + 1) for s in range(N_SUB) for _ in range(SLOT)]
     g_expect = sum(expect_P) + 0.5 * sum(expect_P)
     for r in range(3):
         calls, P, uG, coef, u = res[r]
-        assert "dist_import" not in calls
+        assert ("dist_import" in calls) == (mode == "hs_fail2")
+        assert ("dist_disable" in calls) == (mode == "hs_fail2")
         assert ("interface_factor_solve" in calls) == (r == 0)
         assert uG == [g_expect] * G
 
