@@ -408,7 +408,11 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(args.config, c), "subdomains": N, "l2_flush":
                            "inputs larger than L2: every step writes K_aug (S*ld*ncols*8 B) >> 126 MB",
-                           "parallelism": f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast",
+                           "parallelism": (f"subdomain slabs over {world} GPU(s); Schur buffers NCCL all-reduce; interface "
+                                           f"tile Cholesky shared by all GPUs (replicated tile pools over NVLink peer "
+                                           f"memory, CUDA IPC), every rank solves u_Gamma"
+                                           if getattr(ctx, "_dist", False) else
+                                           f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast"),
                            "interface_ordering": ["strip", "nested_dissection"][ctx.sizes["chol_ordering"]]},
                 "time_to_solution_ms": ms_per_step, "rel_l2_vs_exact": err,
                 "roofline": roof, "roofline_local_factor": roof_qr, "roofline_assembly": roof_asm,
