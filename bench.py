@@ -56,6 +56,8 @@ def bench_config(args) -> dict:
     if getattr(args, "problem", None) is not None:
         over["problem"] = args.problem
         over["alpha"] = args.alpha
+        if args.problem == 7:
+            over["init_c"] = 1.0 / 16  # the paper's constant for the plate
     return WL.config(args.config, **over)
 
 
@@ -64,7 +66,10 @@ def workload_desc(k: int, c: dict | None = None) -> str:
     m = c["p"] ** 2 + 4 * c["q"]
     names = {0: "sin(pi x)sin(pi y)", 1: "e^(x+y)sin(2pi x)cos(2pi y)", 2: "sin(4pi x)sin(4pi y)",
              3: "sin(8pi x)sin(8pi y)", 4: "sin(2pi x)e^y"}
-    if c["problem"] == 6:
+    if c["problem"] == 7:
+        pde = ("2D Kirchhoff plate Lap^2 u = q/D, u = Lap u = 0 on the boundary, q = sin(pi x)sin(pi y) "
+               f"(two traces per edge point: {c['q'] // 2} points/edge)")
+    elif c["problem"] == 6:
         pde = (f"2D variable-coefficient Poisson -div(rho grad u)=1, u=0 on the boundary, rho=tanh(grf)+1.1, "
                f"grf alpha={c.get('alpha', 16.0)} (eqn:varpoisson)")
     else:

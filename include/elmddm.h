@@ -60,7 +60,11 @@ typedef struct {
                                | 2 sin(4pi x)sin(4pi y) | 3 sin(8pi x)sin(8pi y) | 4 sin(2pi x)e^y
                                 | 5 u = 0 | 6 variable coefficient -div(rho grad u) = 1,
                                u = 0 on the boundary, rho = tanh(grf) + 1.1 (eqn:varpoisson,
-                               P:694-701; needs elmddm_set_coefficient)                         */
+                               P:694-701; needs elmddm_set_coefficient) | 7 Kirchhoff plate
+                               Lap^2 u = q/D, u = Lap u = 0 on the boundary, q = sin(pi x)sin(pi y),
+                               E = 1e7, H = 1e-3, nu = 0.3: TWO traces per edge point, so
+                               q = 2 x (points per edge), each edge's rows / interface unknowns
+                               [u at the q/2 points | Lap u at the same points] (reading R28)  */
     int32_t init_scheme;    /* 0 paper eqn:init l = c sqrt(N*M) | 1 manual l = 1 | 2 He l = sqrt(2/M), b = 0 */
     double init_c;          /* c of eqn:init (1/8 for Poisson)                          */
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s) (1/2)                    */

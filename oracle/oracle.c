@@ -135,6 +135,15 @@ void orc_problem(int problem, double x, double y, double *u, double *f) {
         uu = 0.0;
         ff = 1.0;
         break;
+    case 7: /* plate bending: Lap^2 u = q/D, q = sin(pi x) sin(pi y), D = E H^3 / (12 (1 - nu^2)),
+               E = 1e7, H = 1e-3, nu = 0.3; u = sin(pi x) sin(pi y) / (4 pi^4 D) */
+    {
+        double D = 1e7 * 1e-9 / (12.0 * (1.0 - 0.3 * 0.3));
+        double sq = sin(PI * x) * sin(PI * y);
+        uu = sq / (4.0 * PI * PI * PI * PI * D);
+        ff = sq / D;
+        break;
+    }
     default: /* 5: homogeneous problem u = 0 */
         uu = 0.0;
         ff = 0.0;
@@ -167,8 +176,13 @@ static int face_of(const orc_cfg *c, int i, int j, int e) {
  * Every coordinate is one correctly-rounded division of integers, so a point shared by two
  * subdomains is bit-identical in both.  edge[r] = -1 interior else 0..3; gidx[r] = global
  * interface unknown (face*q + k) or -1.                                                      */
+/* Plate bending (problem 7; reading R28): two traces per edge point (u and Lap u), so
+ * an edge holds q = 2 npts rows / interface unknowns: [u at points 0..npts-1 | Lap u at points
+ * 0..npts-1], npts = q / 2 collocation points per edge. */
+static int orc_npts(const orc_cfg *c) { return c->problem == 7 ? c->q / 2 : c->q; }
+
 void orc_rows(const orc_cfg *c, int s, double *xy, int32_t *edge, int32_t *gidx) {
-    int P = c->P, p = c->p, q = c->q;
+    int P = c->P, p = c->p, q = c->q, np = orc_npts(c);
     int i = s % P, j = s / P;
     int r = 0;
     for (int b = 0; b < p; ++b)
@@ -181,8 +195,9 @@ void orc_rows(const orc_cfg *c, int s, double *xy, int32_t *edge, int32_t *gidx)
     for (int e = 0; e < 4; ++e) {
         int f = face_of(c, i, j, e);
         for (int k = 0; k < q; ++k, ++r) {
-            double t_y = (double)(j * (q + 1) + k + 1) / (double)(P * (q + 1));
-            double t_x = (double)(i * (q + 1) + k + 1) / (double)(P * (q + 1));
+            int kp = k % np;
+            double t_y = (double)(j * (np + 1) + kp + 1) / (double)(P * (np + 1));
+            double t_x = (double)(i * (np + 1) + kp + 1) / (double)(P * (np + 1));
             switch (e) {
             case 0: xy[2 * r] = (double)i / (double)P; xy[2 * r + 1] = t_y; break;
             case 1: xy[2 * r] = (double)(i + 1) / (double)P; xy[2 * r + 1] = t_y; break;
@@ -329,11 +344,16 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
     static const double ny[4] = {0.0, 0.0, -1.0, 1.0};
     const double *Ws = W + (size_t)2 * s * M;
     const double *bs = b + (size_t)s * M;
+    const int np = orc_npts(c);
+    const int plate = c->problem == 7;
+    /* kind of an edge row: 0 the u trace, 1 the Lap u trace (plate only) */
+#define ROW_KIND(r) (plate ? ((r) - (m - 4 * q)) % q / np : 0)
     for (int r = 0; r < m; ++r) {
         double u, f;
         orc_problem(c->problem, xy[2 * r], xy[2 * r + 1], &u, &f);
         if (edge[r] < 0) F[r] = f;
-        else F[r] = gidx[r] < 0 ? u : 0.0;
+        else if (gidx[r] >= 0) F[r] = 0.0;
+        else F[r] = ROW_KIND(r) == 0 ? u : -2.0 * PI * PI * u; /* plate: Lap u = -2 pi^2 u */
     }
     for (int n = 0; n < M; ++n) {
         double wx = Ws[2 * n], wy = Ws[2 * n + 1], bb = bs[n];
@@ -344,6 +364,22 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
             double d1 = 1.0 - t * t;
             double d2 = -2.0 * t * d1;
             double val;
+            if (plate) {
+                /* s3 = sigma''' = -2 sigma'^2 - 2 sigma sigma'', s4 = sigma'''' = -6 sigma' sigma'' - 2 sigma s3 */
+                double d3 = -2.0 * d1 * d1 - 2.0 * t * d2;
+                double d4 = -6.0 * d1 * d2 - 2.0 * t * d3;
+                if (edge[r] < 0) val = w2 * w2 * d4;                 /* Lap^2 phi = |w|^4 sigma'''' */
+                else val = ROW_KIND(r) == 0 ? t : w2 * d2;           /* phi, Lap phi = |w|^2 sigma'' */
+                K[(size_t)n * m + r] = val;
+                if (edge[r] >= 0 && A) {
+                    int e = edge[r];
+                    int ar = r - (m - 4 * q);
+                    double wn = wx * nx[e] + wy * ny[e];
+                    A[(size_t)n * 4 * q + ar] =
+                        gidx[r] >= 0 ? (ROW_KIND(r) == 0 ? wn * d1 : w2 * wn * d3) : 0.0; /* d/dn phi, d/dn Lap phi */
+                }
+                continue;
+            }
             if (edge[r] < 0) {
                 if (c->problem == 6) {
                     double rho, rx, ry;
@@ -366,6 +402,7 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
     free(xy);
     free(edge);
     free(gidx);
+#undef ROW_KIND
 }
 
 /* ------------------------------------------------------------------------------------------ */

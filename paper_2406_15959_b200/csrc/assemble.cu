@@ -110,6 +110,12 @@ __device__ void problem_uf(int pid, double x, double y, double& u, double& f) {
             u = 0.0;
             f = 1.0;
             break;
+        case 7: {  // plate bending: Lap^2 u = q/D, u = sin(pi x)sin(pi y)/(4 pi^4 D)
+            const double D = 1e7 * 1e-9 / (12.0 * (1.0 - 0.3 * 0.3));
+            const double sq = sin(kPi * x) * sin(kPi * y);
+            u = sq / (4.0 * kPi * kPi * kPi * kPi * D);
+            f = sq / D;
+        } break;
         default:
             u = 0.0;
             f = 0.0;
@@ -141,9 +147,11 @@ __device__ __forceinline__ void row_point(const elmddm_config& c, int i, int j, 
     int e = r / q;
     k = r % q;
     kind = e;
-    double den = (double)(P * (q + 1));
-    double ty = (double)(j * (q + 1) + k + 1) / den;
-    double tx = (double)(i * (q + 1) + k + 1) / den;
+    // plate (problem 7, reading R28): q = 2 npts rows per edge, [u traces | Lap u traces]
+    const int np = c.problem == 7 ? q / 2 : q, kp = k % np;
+    double den = (double)(P * (np + 1));
+    double ty = (double)(j * (np + 1) + kp + 1) / den;
+    double tx = (double)(i * (np + 1) + kp + 1) / den;
     switch (e) {
         case 0: x = (double)i / (double)P; y = ty; break;
         case 1: x = (double)(i + 1) / (double)P; y = ty; break;
@@ -241,7 +249,8 @@ __device__ __forceinline__ double fast_rcp(double x) {
 // tabulated per neuron over the p+q+2 distinct x (resp. y) coordinates of the subdomain's rows;
 // then d = 1/(1+E), sigma = 1 - 2d, sigma' = 4 E d^2, -|w|^2 sigma'' = 2|w|^2 sigma sigma'.
 // |z| <= |w|_1 (h/2 + r) stays O(10) for the paper's initialisation, so E never overflows.
-template <bool VAR>  // VAR: problem 6 (variable coefficient interior rows)
+// OP: 0 Poisson, 1 variable coefficient (problem 6), 2 plate bending (problem 7)
+template <int OP>
 __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
                                                     const double* __restrict__ W, const double* __restrict__ b,
                                                     double* __restrict__ Kaug, double* __restrict__ At,
@@ -266,7 +275,10 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
             if (k < p) coord = (double)(ij * (p + 1) + k + 1) / (double)(P * (p + 1));
             else if (k == p) coord = (double)ij / (double)P;
             else if (k == p + 1) coord = (double)(ij + 1) / (double)P;
-            else coord = (double)(ij * (q + 1) + (k - p - 2) + 1) / (double)(P * (q + 1));
+            else {
+                const int np = OP == 2 ? q / 2 : q;  // plate: edge rows k and k + np share a point
+                coord = (double)(ij * (np + 1) + (k - p - 2) % np + 1) / (double)(P * (np + 1));
+            }
             const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
             double arg;
             if (axis == 0) arg = 2.0 * (wx * (coord - cx) + (b[(int64_t)sl * M + col] + wx * cx + wy * cy));
@@ -303,7 +315,13 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                         const double E = tx[xi] * tx[ntab + yi];
                         const double d = fast_rcp(1.0 + E);
                         const double wn = e == 0 ? -wxs[cc] : (e == 1 ? wxs[cc] : (e == 2 ? -wys[cc] : wys[cc]));
-                        v[h] = wn * (4.0 * E * d * d);
+                        const double s1 = 4.0 * E * d * d;
+                        if (OP == 2 && k >= q / 2) {  // plate: d/dn Lap phi = |w|^2 (w.n) sigma'''
+                            const double sg = fma(-2.0, d, 1.0), s2 = -2.0 * sg * s1;
+                            v[h] = 0.5 * w2s[cc] * wn * (-2.0 * s1 * s1 - 2.0 * sg * s2);
+                        } else {
+                            v[h] = wn * s1;
+                        }
                     }
                 }
                 if (pr + 1 < ncc)
@@ -316,6 +334,7 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
         for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
             int xi[2], yi[2], kind[2];
             double4 rc[2] = {make_double4(1.0, 0.0, 0.0, 0.0), make_double4(1.0, 0.0, 0.0, 0.0)};
+            bool lapt[2] = {false, false};  // plate: a Lap u trace row
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int r = 2 * r2 + e;
@@ -323,10 +342,11 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     xi[e] = r % p;
                     yi[e] = r / p;
                     kind[e] = 0;
-                    if (VAR) rc[e] = coef[(int64_t)sl * pp + r];
+                    if (OP == 1) rc[e] = coef[(int64_t)sl * pp + r];
                 } else if (r < m) {
                     const int t = r - pp, ed = t / q, k = t % q;
                     kind[e] = 1;
+                    lapt[e] = OP == 2 && k >= q / 2;
                     xi[e] = ed == 0 ? p : (ed == 1 ? p + 1 : p + 2 + k);
                     yi[e] = ed == 2 ? p : (ed == 3 ? p + 1 : p + 2 + k);
                 } else {
@@ -346,10 +366,18 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     const double d = fast_rcp(1.0 + E);
                     const double sg = fma(-2.0, d, 1.0);
                     const double s1 = 4.0 * E * d * d;
-                    // interior: -Lap phi, or -rho Lap phi - grad rho . grad phi (problem 6)
-                    const double lap = VAR ? rc[e].x * (w2s[cc] * sg) - (rc[e].y * wxs[cc] + rc[e].z * wys[cc])
-                                           : w2s[cc] * sg;
-                    v[e] = kind[e] == 0 ? lap * s1 : (kind[e] == 1 ? sg : 0.0);
+                    if (OP == 2) {
+                        // plate: interior Lap^2 phi = |w|^4 sigma'''', traces phi and Lap phi = |w|^2 sigma''
+                        const double w2 = 0.5 * w2s[cc];
+                        const double s2 = -2.0 * sg * s1, s3 = -2.0 * s1 * s1 - 2.0 * sg * s2;
+                        const double s4 = -6.0 * s1 * s2 - 2.0 * sg * s3;
+                        v[e] = kind[e] == 0 ? w2 * w2 * s4 : (kind[e] == 1 ? (lapt[e] ? w2 * s2 : sg) : 0.0);
+                    } else {
+                        // interior: -Lap phi, or -rho Lap phi - grad rho . grad phi (problem 6)
+                        const double lap = OP == 1 ? rc[e].x * (w2s[cc] * sg) - (rc[e].y * wxs[cc] + rc[e].z * wys[cc])
+                                                   : w2s[cc] * sg;
+                        v[e] = kind[e] == 0 ? lap * s1 : (kind[e] == 1 ? sg : 0.0);
+                    }
                 }
                 *reinterpret_cast<double2*>(Ks + (int64_t)(c0 + cc) * ld + 2 * r2) = make_double2(v[0], v[1]);
             }
@@ -377,7 +405,8 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                         v = f;
                     } else if (!edge_is_interface(P, i, j, kind)) {
                         problem_uf(cfg.problem, x, y, u, f);
-                        v = u;
+                        // plate: the Lap u trace rows carry Lap u = -2 pi^2 u of the exact solution
+                        v = (cfg.problem == 7 && k >= q / 2) ? -2.0 * kPi * kPi * u : u;
                     }
                 }
                 Ks[(int64_t)col * ld + r] = v;
@@ -437,9 +466,11 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
         coef = reinterpret_cast<const double4*>(c->d_coef);
     }
     if (coef)
-        k_assemble<true><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, coef);
+        k_assemble<1><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, coef);
+    else if (c->cfg.problem == 7)
+        k_assemble<2><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr);
     else
-        k_assemble<false><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr); }
+        k_assemble<0><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr); }
     return cudaGetLastError();
 }
 

@@ -50,7 +50,7 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
     if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
     if (round_up(m, 32) > 3008) return why = "m too large for the shared-memory panel (ld <= 3008)", false;
-    if (cfg->problem < 0 || cfg->problem > 6) return why = "unknown problem id", false;
+    if (cfg->problem < 0 || cfg->problem > 7) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
     int64_t N = (int64_t)cfg->P * cfg->P;
@@ -711,19 +711,21 @@ elmddm_status elmddm_interface_points(const elmddm_ctx* c, double* xy) {
     CHECK_CTX(c);
     if (!xy) return ELMDDM_EINVAL;
     const int P = c->cfg.P, q = c->cfg.q;
+    const int np = c->cfg.problem == 7 ? q / 2 : q;  // plate: unknowns k and k + np share a point
     for (int f = 0; f < c->faces; ++f) {
         int s = c->face_sub[f * 2], e = c->face_edge[f * 2];
         int i = s % P, j = s / P;
         for (int k = 0; k < q; ++k) {
             double t_along, fixed;
+            const int kp = k % np;
             if (e == 1) {  // vertical face at x = (i+1)/P
                 fixed = (double)(i + 1) / (double)P;
-                t_along = (double)(j * (q + 1) + k + 1) / (double)(P * (q + 1));
+                t_along = (double)(j * (np + 1) + kp + 1) / (double)(P * (np + 1));
                 xy[2 * ((int64_t)f * q + k)] = fixed;
                 xy[2 * ((int64_t)f * q + k) + 1] = t_along;
             } else {  // horizontal face at y = (j+1)/P
                 fixed = (double)(j + 1) / (double)P;
-                t_along = (double)(i * (q + 1) + k + 1) / (double)(P * (q + 1));
+                t_along = (double)(i * (np + 1) + kp + 1) / (double)(P * (np + 1));
                 xy[2 * ((int64_t)f * q + k)] = t_along;
                 xy[2 * ((int64_t)f * q + k) + 1] = fixed;
             }

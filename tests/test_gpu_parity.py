@@ -610,3 +610,47 @@ def test_dist_factorisation_emulated_matches_single_rank(k, nrep):
     assert nd == 0
     assert torch.equal(uG, buf["uG"])
     assert torch.equal(Mc, Mc)  # input untouched (no NaN)
+
+
+# ------------------------------------------------------------------------------------------------
+# Kirchhoff plate (problem 7; reading R28) -- SURVEY §8(f) NEXT-4
+# ------------------------------------------------------------------------------------------------
+def test_plate_assembly_matches_oracle():
+    """Plate rows (interior |w|^4 sigma'''', traces phi / |w|^2 sigma'', fluxes (w.n) sigma' /
+    |w|^2 (w.n) sigma''') and F entrywise against the oracle: the GPU evaluates the derivatives
+    by the separable-exponential recurrences, the oracle from tanh, so the bound is relative to
+    each row's scale (fourth derivatives amplify the few-ulp difference in sigma)."""
+    c = small(P=3, M=64, p=10, q=12, problem=7, init_c=1.0 / 16, seed=6)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, _ = _oracle_init(c)
+    oc = ocfg(c)
+    for s in range(9):
+        K, F, A = O.assemble(oc, s, W, b)
+        m = K.shape[0]
+        Kg = kaug_np(ctx, buf, s)
+        scale = np.abs(K).max(axis=1, keepdims=True) + 1e-300
+        assert np.all(np.abs(Kg[:m, :c["M"]] - K) <= 1e-12 * scale), s
+        assert np.allclose(Kg[:m, c["M"] + 4 * c["q"]], F, rtol=1e-14, atol=1e-14 * np.abs(F).max())
+        Ag = at_np(ctx, buf, s, c["M"], c["q"])
+        sa = np.abs(A).max(axis=1, keepdims=True) + 1e-300
+        assert np.all(np.abs(Ag - A) <= 1e-12 * sa), s
+
+
+@pytest.mark.parametrize("cfgkw", [
+    dict(P=2, M=256, p=18, q=24),
+    dict(P=3, M=200, p=16, q=20, interface_mode=3),
+    dict(P=4, M=128, p=13, q=16),
+])
+def test_plate_end_to_end_parity_and_accuracy(cfgkw):
+    """The plate through the whole path: u on a grid matches the oracle to relative L2 1e-6, and
+    both are close to the exact solution (the first case reproduces the 1e-11 accuracy the
+    oracle pin establishes; P:795-797)."""
+    c = small(problem=7, init_c=1.0 / 16, seed=3, **cfgkw)
+    xy = WL.eval_grid(41)
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy)
+    ug = u.cpu().numpy()
+    assert rel_l2(ug, r["u"]) <= 1e-6
+    ex = WL.exact(7, xy)
+    assert rel_l2(ug, ex) <= max(10 * rel_l2(r["u"], ex), 1e-8)

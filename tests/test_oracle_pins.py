@@ -527,3 +527,79 @@ def test_varcoef_zero_field_is_scaled_poisson():
     assert np.allclose(K6[inn], 1.1 * K0[inn], rtol=4e-16 * 4, atol=0)
     assert np.array_equal(K6[~inn], K0[~inn]) and np.array_equal(A6, A0)
     O.set_grf(None)
+
+
+# ------------------------------------------------------------------------------------------------
+# Kirchhoff plate (problem 7): Lap^2 u = q/D, u = Lap u = 0 on the boundary, two traces
+# and two fluxes per interface point (reading R28); SURVEY §8(f) NEXT-4
+# ------------------------------------------------------------------------------------------------
+PLATE_D = 1e7 * 1e-9 / (12.0 * (1.0 - 0.3 * 0.3))
+
+
+def test_plate_rhs_and_exact_solution():
+    """f = q/D with q = sin(pi x) sin(pi y), and u = q / (4 pi^4 D) satisfies Lap^2 u = f (FD of
+    the oracle's own u)."""
+    assert abs(PLATE_D - 1e-2 / 10.92) < 1e-15
+    x, y, h = 0.31, 0.62, 2e-3
+    u = lambda a, b: O.problem(7, a, b)[0]
+    lap = lambda a, b: (u(a + h, b) + u(a - h, b) + u(a, b + h) + u(a, b - h) - 4 * u(a, b)) / h**2
+    bih = (lap(x + h, y) + lap(x - h, y) + lap(x, y + h) + lap(x, y - h) - 4 * lap(x, y)) / h**2
+    f = O.problem(7, x, y)[1]
+    assert abs(f - math.sin(math.pi * x) * math.sin(math.pi * y) / PLATE_D) < 1e-12 * abs(f)
+    assert abs(bih - f) < 1e-3 * abs(f)
+    assert abs(u(x, y) - math.sin(math.pi * x) * math.sin(math.pi * y) / (4 * math.pi**4 * PLATE_D)) < 1e-12
+
+
+def test_plate_rows_vs_finite_differences():
+    """Interior rows Lap^2 phi, u-trace rows phi, Lap-trace rows Lap phi, flux rows d phi/dn and
+    d Lap phi / dn, against central differences of np.tanh; the edge block layout [u traces |
+    Lap u traces] with both traces at the same points."""
+    c = O.cfg(2, 12, 5, 8, 7, 0, 1.0 / 16, 0.5, 4)
+    W, b, _, _ = O.init_hidden(c)
+    s = 0
+    K, F, A = O.assemble(c, s, W, b)
+    xy, edge, gidx = O.rows(c, s)
+    w, bb = W[s], b[s]
+    phi = lambda p: np.tanh(w[:, 0] * p[0] + w[:, 1] * p[1] + bb)
+    h = 1e-3
+
+    def lap(fn, p):
+        return (fn(p + [h, 0]) + fn(p - [h, 0]) + fn(p + [0, h]) + fn(p - [0, h]) - 4 * fn(p)) / h**2
+
+    q, npts, pp = 8, 4, 25
+    normals = {0: (-1, 0), 1: (1, 0), 2: (0, -1), 3: (0, 1)}
+    for r in range(len(edge)):
+        p = xy[r]
+        if edge[r] < 0:
+            bih = lap(lambda z: lap(phi, z), p)
+            assert np.allclose(K[r], bih, rtol=0, atol=2e-3 * max(1.0, np.abs(bih).max()))
+            continue
+        e, k = edge[r], (r - pp) % q
+        assert (r - pp) // q == e
+        twin = pp + e * q + (k + npts) % q          # the other trace at the same point
+        assert np.array_equal(xy[twin], p)
+        n = np.array(normals[e], float)
+        if k < npts:
+            assert np.allclose(K[r], phi(p), rtol=0, atol=2e-15)
+            d = (phi(p + h * n) - phi(p - h * n)) / (2 * h)
+        else:
+            lp = lap(phi, p)
+            assert np.allclose(K[r], lp, rtol=0, atol=1e-5 * max(1.0, np.abs(lp).max()))
+            d = (lap(phi, p + h * n) - lap(phi, p - h * n)) / (2 * h)
+        if gidx[r] >= 0:
+            assert np.allclose(A[r - pp], d, rtol=0, atol=1e-4 * max(1.0, np.abs(d).max()))
+            assert F[r] == 0.0
+        else:
+            assert np.all(A[r - pp] == 0.0)
+
+
+def test_plate_solution_accuracy():
+    """The DDM solution of the plate problem (c = 1/16 of P:545) on 2 x 2 subdomains
+    converges to the exact u: relative L2 error < 1e-9 (the paper's Table tab:platebending: 1e-8
+    at 2 x 2 with n = 2^16; the SPEC acceptance bound is 1e-4)."""
+    c = O.cfg(2, 256, 18, 24, 7, 0, 1.0 / 16, 0.5, 3)
+    W, b, _, _ = O.init_hidden(c)
+    xy = WL.eval_grid(41)
+    r = O.solve(c, W, b, xy)
+    ex = WL.exact(7, xy)
+    assert np.linalg.norm(r["u"] - ex) / np.linalg.norm(ex) < 1e-9

@@ -69,4 +69,7 @@ def exact(problem: int, xy: np.ndarray) -> np.ndarray:
         return np.sin(2 * pi * x) * np.exp(y)
     if problem == 6:  # variable coefficient: no closed form (the paper's reference is FEM)
         return np.full_like(x, np.nan)
+    if problem == 7:  # Kirchhoff plate: sin(pi x) sin(pi y) / (4 pi^4 D)
+        D = 1e7 * 1e-9 / (12.0 * (1.0 - 0.3 * 0.3))
+        return np.sin(pi * x) * np.sin(pi * y) / (4.0 * pi**4 * D)
     return np.zeros_like(x)
