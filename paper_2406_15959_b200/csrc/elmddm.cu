@@ -310,6 +310,8 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_CHOL_SCHED")) c->chol_sched = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL8")) c->panel8 = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL_MERGED")) c->panel_merged = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_PANEL_TMEM")) c->panel_tmem = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_PANEL_PRIO")) c->panel_prio = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));
@@ -355,6 +357,9 @@ void elmddm_destroy(elmddm_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto s : c->gstreams) cudaStreamDestroy(s);
     for (auto e : c->ev_join) cudaEventDestroy(e);
+    for (auto s : c->pstreams) cudaStreamDestroy(s);
+    for (auto e : c->ev_panel) cudaEventDestroy(e);
+    for (auto e : c->ev_wy) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (auto& p : c->ev_pending) {
         cudaEventDestroy(p.second.first);

@@ -130,6 +130,8 @@ struct elmddm_ctx {
     int ngrf = 0;
     double* d_coef = nullptr;        // problem 6: [S][p*p][4] rho, grad rho at the interior points
     mutable DistState dist;          // multi-rank interface factorisation (elmddm_dist_*)
+    int panel_prio = 1;              // ELMDDM_PANEL_PRIO: panels on high-priority streams (with k_panel_t)
+    int panel_tmem = 1;              // ELMDDM_PANEL_TMEM: TMEM-resident panel block (k_panel_t)
     int panel_merged = 1;            // ELMDDM_PANEL_MERGED: one launch per panel, merged Gram pass (k_panel_p)
     int panel8 = 0;                  // ELMDDM_PANEL8: on-chip 8-CTA cluster panels (qr.cu k_panel_c8)
     int chol_sched = 1;              // ELMDDM_CHOL_SCHED: 1 list-scheduled task order, dynamic dealing
@@ -164,6 +166,26 @@ struct elmddm_ctx {
             if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
             gstreams.push_back(s);
             ev_join.push_back(ev);
+        }
+        return e;
+    }
+    // high-priority panel streams (one per subdomain group) and the panel / trailing-update
+    // hand-over events: a pending co-residable panel CTA takes the next free half-SM first
+    mutable std::vector<cudaStream_t> pstreams;
+    mutable std::vector<cudaEvent_t> ev_panel, ev_wy;
+    cudaError_t ensure_panel_streams(int n) const {
+        cudaError_t e = cudaSuccess;
+        int least = 0, greatest = 0;
+        if ((e = cudaDeviceGetStreamPriorityRange(&least, &greatest)) != cudaSuccess) return e;
+        while ((int)pstreams.size() < n) {
+            cudaStream_t s;
+            cudaEvent_t a, b;
+            if ((e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, greatest)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+            pstreams.push_back(s);
+            ev_panel.push_back(a);
+            ev_wy.push_back(b);
         }
         return e;
     }

@@ -727,6 +727,490 @@ __global__ void __launch_bounds__(PNT, 1) k_panel_p(PanelArgs a, int nb) {
     }
 }
 
+
+// block-wide deterministic sum for NWARPS warps (k_panel_t): result broadcast in tot[0..NV)
+template <int NV, int NWARPS>
+__device__ __forceinline__ void block_sum_n(double (&v)[NV], double* red, double* tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) red[warp * NV + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int w = 0; w < NWARPS; ++w) s += red[w * NV + threadIdx.x];
+        tot[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+// t_extend for NTH threads
+template <int NTH>
+__device__ void t_extend_n(double* T, int kpp, const double* G, const double* Tbb, double* Ts, double* Ys) {
+    for (int t = threadIdx.x; t < kpp * 8; t += NTH) {
+        const int r = t % kpp, c = t / kpp;
+        double s = 0.0;
+        for (int k = 0; k <= c; ++k) s += G[k * kpp + r] * Tbb[c * 8 + k];
+        Ys[c * kpp + r] = s;
+    }
+    for (int t = threadIdx.x; t < kpp * kpp; t += NTH) {
+        const int r = t % kpp, c = t / kpp;
+        Ts[c * kpp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kpp * 8; t += NTH) {
+        const int r = t % kpp, c = t / kpp;
+        double s = 0.0;
+        for (int k = r; k < kpp; ++k) s += Ts[k * kpp + r] * Ys[c * kpp + k];
+        T[(kpp + c) * ELM_NB + r] = -s;
+    }
+    __syncthreads();
+}
+// ------------------------------------------------------------------------------------------
+// TMEM-resident panel (sm_100a): k_panel_p's arithmetic with the (ld - j0) x 8 block kept in
+// tensor memory instead of shared memory, 256 threads and <= 128 registers, so that the panel
+// CTA (~116 KB of shared memory: V_prev ring + a chunk staging buffer) shares its SM with one
+// trailing-update CTA (108 KB): the latency-bound panel no longer takes a whole SM away from
+// the DMMA-bound trailing updates (one k_wy_tma CTA alone keeps 83% of two CTAs' rate).
+// TMEM layout (32-bit columns): row r of the block = 128 g + 32 q + lane lives in TMEM lane
+// 32 q + lane, columns [16 g, 16 g + 16) (the 8 doubles of the row); warp w reaches lane quarter
+// q = w % 4 and takes the row groups g = w / 4, w / 4 + 2, ...  The DMMA passes stage the rows of
+// each V_prev chunk through shared memory; the column factorisation works on TMEM rows directly
+// (thread = row, one tcgen05.ld / tcgen05.st of 16 columns per row), with the update of column c
+// fused with the partial sums of column c + 1.
+// ------------------------------------------------------------------------------------------
+namespace pt {
+constexpr int NT = 256, NW = 8;
+constexpr int RCH_MAX = 256;                 // rows per staged chunk (Cs staging buffer)
+constexpr int SMEM = 116 * 1024;             // > 228/2 KB: never two panel CTAs (TMEM) per SM;
+                                             // + 108 KB trailing-update CTA fits
+}  // namespace pt
+
+__device__ __forceinline__ uint32_t tm_addr(uint32_t base, int quarter, int col) {
+    return base + ((uint32_t)(32 * quarter) << 16) + (uint32_t)col;
+}
+__device__ __forceinline__ void tm_ld8(uint32_t addr, double (&v)[8]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = __hiloint2double((int)r[2 * c + 1], (int)r[2 * c]);
+}
+__device__ __forceinline__ void tm_st8(uint32_t addr, const double (&v)[8]) {
+    uint32_t r[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        r[2 * c] = (uint32_t)__double2loint(v[c]);
+        r[2 * c + 1] = (uint32_t)__double2hiint(v[c]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+        ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+// stage rows [c*rch, c*rch + nr) of V_prev columns [0, kp) into dst[col*(rch+4) + row], NTH threads
+template <int NTH>
+__device__ __forceinline__ void vp_chunk_n(double* dst, const double* __restrict__ Vp, int64_t ld, int kp, int rch,
+                                           int c, int nr) {
+    const int rcp = rch + 4, n = kp * (nr / 2);
+    for (int t = threadIdx.x; t < n; t += NTH) {
+        const int col = t / (nr / 2), r = (t % (nr / 2)) * 2;
+        unsigned d = (unsigned)__cvta_generic_to_shared(dst + col * rcp + r);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(Vp + (int64_t)col * ld + c * rch + r));
+    }
+}
+template <int NTH, class F>
+__device__ __forceinline__ void vp_stream_n(const double* __restrict__ Vp, int64_t ld, int R, int kp, double* ring,
+                                            int sst, int rmax, F&& consume) {
+    int rch = vp_rows(kp, sst);
+    if (rch > rmax) rch = rmax;
+    const int nch = (R + rch - 1) / rch;
+#pragma unroll
+    for (int i = 0; i < VNS - 1; ++i) {
+        if (i < nch) vp_chunk_n<NTH>(ring + i * sst, Vp, ld, kp, rch, i, min(rch, R - i * rch));
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(VNS - 2));
+        __syncthreads();
+        const int cn = c + VNS - 1;
+        if (cn < nch) vp_chunk_n<NTH>(ring + (cn % VNS) * sst, Vp, ld, kp, rch, cn, min(rch, R - cn * rch));
+        asm volatile("cp.async.commit_group;\n" ::);
+        consume(ring + (c % VNS) * sst, c, rch, min(rch, R - c * rch));
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+}
+
+constexpr int PANELT_FIXED = 3 * 8 * 56 + 8 * (pt::RCH_MAX + 4) + 2 * pt::NW * 8 + 40 + 64 + 8 + 16 + 8;
+
+__global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
+    using namespace pt;
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint32_t s_tbase;
+    const int sl = a.s_off + blockIdx.x;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0;
+    const int R = (int)(ld - j0);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int quarter = warp & 3, gpar = warp >> 2;
+    const int ngr = (R + 127) / 128;           // row groups
+    double* Wsm = sm;                          // [8][kp]
+    double* Zsm = Wsm + 8 * 56;                // [8][kp]
+    double* Gp = Zsm + 8 * 56;                 // [8][kp-8]
+    double* Cs = Gp + 8 * 56;                  // [8][RCH_MAX+4] staged block rows of a chunk
+    double* red = Cs + 8 * (RCH_MAX + 4);      // [2][NW][8]
+    double* tot = red + 2 * NW * 8;            // [40]
+    double* Tbb = tot + 40;                    // [8][8]
+    double* taus = Tbb + 64;                   // [8]
+    double* drow = taus + 8;                   // [2][8] the current diagonal row (double-buffered)
+    double* ring = drow + 16 + 8;              // a.ring doubles
+    const int sst = (a.ring / VNS) & ~1;
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+    const double* Vp = V + j0;
+    const int kr = lane & 3, cn = lane >> 2;
+
+    // TMEM: the whole 512 columns (one panel CTA per SM by construction)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&s_tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = s_tbase;
+    auto row_of = [&](int g) { return 128 * g + 32 * quarter + lane; };
+    auto taddr = [&](int g) { return tm_addr(tbase, quarter, 16 * g); };
+
+    for (int b = 0; b < nb / 8; ++b) {
+        const int kp = 8 * b, jb = j0 + kp, d0 = kp;
+        // A. the block -> TMEM (thread = row; rows >= R are zero)
+        for (int g = gpar; g < ngr; g += 2) {
+            const int r = row_of(g);
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = r < R ? __ldcg(A + (int64_t)(jb + c) * ld + j0 + r) : 0.0;
+            tm_st8(taddr(g), v);
+        }
+        __syncthreads();
+        // stage rows [r0, r0 + nr) of the block into Cs (owner threads), then a barrier
+        auto stage = [&](int r0, int nr, int rcp) {
+            const int g0 = r0 / 128, g1 = (r0 + nr - 1) / 128;
+            for (int g = g0 + ((g0 & 1) != gpar); g <= g1; g += 2) {  // warp-uniform
+                double v[8];
+                tm_ld8(taddr(g), v);
+                const int r = row_of(g);
+                if (r >= r0 && r < r0 + nr)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) Cs[c * rcp + r - r0] = v[c];
+            }
+            __syncthreads();
+        };
+        auto unstage = [&](int r0, int nr, int rcp) {
+            const int g0 = r0 / 128, g1 = (r0 + nr - 1) / 128;
+            for (int g = g0 + ((g0 & 1) != gpar); g <= g1; g += 2) {
+                double v[8];
+                tm_ld8(taddr(g), v);
+                const int r = row_of(g);
+                if (r >= r0 && r < r0 + nr) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) v[c] = Cs[c * rcp + r - r0];
+                }
+                tm_st8(taddr(g), v);
+            }
+        };
+        if (kp > 0) {
+            // B. one pass over V_prev: W = V_prev^T C_b and G = V_prev[:, 0:kp-8]^T V_{b-1}
+            const int kpp = kp - 8, mtiles = kp >> 3;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+            vp_stream_n<NT>(Vp, ld, R, kp, ring, sst, RCH_MAX, [&](const double* st, int c, int rch, int nr) {
+                const int rcp = rch + 4, nq = nr / 8;
+                stage(c * rch, nr, rcp);
+                if (warp < mtiles) {
+                    const bool two = warp < mtiles - 1;
+                    const int t = warp;
+#pragma unroll 2
+                    for (int q = 0; q < nq; ++q) {
+                        const int k0 = 8 * q + kr, k1 = k0 + 4;
+                        const double av0 = st[(t * 8 + cn) * rcp + k0], av1 = st[(t * 8 + cn) * rcp + k1];
+                        dmma8(a0, a1, av0, Cs[cn * rcp + k0]);
+                        dmma8(a2, a3, av1, Cs[cn * rcp + k1]);
+                        if (two) {
+                            dmma8(g0, g1, av0, st[(kpp + cn) * rcp + k0]);
+                            dmma8(g2, g3, av1, st[(kpp + cn) * rcp + k1]);
+                        }
+                    }
+                }
+            });
+            if (warp < mtiles) {
+                const int t = warp;
+                Wsm[(2 * kr) * kp + t * 8 + cn] = a0 + a2;
+                Wsm[(2 * kr + 1) * kp + t * 8 + cn] = a1 + a3;
+                if (warp < mtiles - 1) {
+                    Gp[(2 * kr) * kpp + t * 8 + cn] = g0 + g2;
+                    Gp[(2 * kr + 1) * kpp + t * 8 + cn] = g1 + g3;
+                }
+            }
+            __syncthreads();
+            // C. T extension by block b-1, then Z = T^T W
+            if (kpp > 0) t_extend_n<NT>(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
+            {
+                double* Ts = ring;
+                for (int t = tid; t < kp * kp; t += NT) {
+                    const int r = t % kp, c = t / kp;
+                    Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+                }
+                __syncthreads();
+                for (int t = tid; t < kp * 8; t += NT) {
+                    const int cp = t % kp, c = t / kp;
+                    double s = 0.0;
+                    for (int k = 0; k <= cp; ++k) s += Ts[cp * kp + k] * Wsm[c * kp + k];
+                    Zsm[c * kp + cp] = s;
+                }
+                __syncthreads();
+            }
+            // D. C_b -= V_prev Z (DMMA on the staged rows, written back to TMEM)
+            {
+                const int ksteps = kp >> 2;
+                double zb[14];
+#pragma unroll
+                for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[cn * kp + t * 4 + kr] : 0.0;
+                __syncthreads();
+                vp_stream_n<NT>(Vp, ld, R, kp, ring, sst, RCH_MAX, [&](const double* st, int c, int rch, int nr) {
+                    const int rcp = rch + 4, nmt = nr / 8;
+                    stage(c * rch, nr, rcp);
+                    for (int mt = warp; mt < nmt; mt += NW) {
+                        double c0 = Cs[(2 * kr) * rcp + mt * 8 + cn], c1 = Cs[(2 * kr + 1) * rcp + mt * 8 + cn];
+#pragma unroll
+                        for (int t = 0; t < 14; ++t)
+                            if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * rcp + mt * 8 + cn], zb[t]);
+                        Cs[(2 * kr) * rcp + mt * 8 + cn] = c0;
+                        Cs[(2 * kr + 1) * rcp + mt * 8 + cn] = c1;
+                    }
+                    __syncthreads();
+                    unstage(c * rch, nr, rcp);
+                });
+            }
+        }
+
+        // E. factor the 8 columns on the TMEM rows.  Partial sums of column c are accumulated
+        //    while column c-1 is applied; row d's owner publishes the diagonal row in drow.
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = 0.0;
+        for (int g = gpar; g < ngr; g += 2) {
+            double x[8];
+            tm_ld8(taddr(g), x);
+            const int r = row_of(g);
+            if (r < R && r > d0) {
+                v[0] += x[0] * x[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) v[k] += x[0] * x[k];
+            }
+            if (r == d0)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) drow[k] = x[k];
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int d = d0 + c, nk = 8 - c;
+            double* rb = red + (c & 1) * NW * 8;
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                double h4[4], h2[2], h1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double snd = b4 ? v[i] : v[i + 4];
+                    h4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double snd = b3 ? h4[i] : h4[i + 2];
+                    h2[i] = (b3 ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+                {
+                    const double snd = b2 ? h2[0] : h2[1];
+                    h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+                }
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) rb[warp * 8 + (lane >> 2)] = h1;
+            }
+            __syncthreads();
+            const double* dr = drow + (c & 1) * 8;   // diagonal row: columns c .. 7 at dr[c..7]
+            double mine = 0.0;
+            if (lane < 8) {
+                mine = ((rb[0 * 8 + lane] + rb[1 * 8 + lane]) + (rb[2 * 8 + lane] + rb[3 * 8 + lane])) +
+                       ((rb[4 * 8 + lane] + rb[5 * 8 + lane]) + (rb[6 * 8 + lane] + rb[7 * 8 + lane]));
+            } else if (lane < 16) {
+                mine = (lane - 8 < nk) ? dr[c + lane - 8] : 0.0;
+            }
+            const double ts0 = __shfl_sync(0xffffffffu, mine, 0);
+            const double x0 = __shfl_sync(0xffffffffu, mine, 8);
+            const double nrm = sqrt(x0 * x0 + ts0);
+            double alpha = x0, tau = 0.0, scale = 0.0;
+            if (nrm != 0.0) {
+                alpha = x0 >= 0.0 ? -nrm : nrm;
+                scale = 1.0 / (x0 - alpha);
+                tau = (alpha - x0) / alpha;
+            }
+            const double ydl = __shfl_sync(0xffffffffu, mine, (lane & 7) + 8);
+            const double wl = (lane >= 1 && lane < nk) ? tau * (ydl + scale * mine) : 0.0;
+            double w[8], yd[8];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) {
+                w[k] = __shfl_sync(0xffffffffu, wl, k);
+                yd[k] = __shfl_sync(0xffffffffu, mine, k + 8);
+            }
+            // apply column c to own rows (and the diagonal row's owner writes R's row d), and
+            // accumulate the partial sums of column c + 1 on the updated rows
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = 0.0;
+            double* drn = drow + ((c + 1) & 1) * 8;
+            for (int g = gpar; g < ngr; g += 2) {
+                const int r = row_of(g);
+                const int rw = r - d;  // > 0: below the diagonal; 0: the diagonal row
+                double x[8];
+                tm_ld8(taddr(g), x);
+                if (r < R && rw >= 0) {
+                    if (rw == 0) {
+#pragma unroll
+                        for (int k = 1; k < 8; ++k)
+                            if (c + k < 8) x[c + k] = yd[k] - w[k];
+                        x[c] = alpha;
+                    } else if (tau != 0.0) {
+                        const double vs = scale * x[c];
+#pragma unroll
+                        for (int k = 1; k < 8; ++k)
+                            if (c + k < 8) x[c + k] -= w[k] * vs;
+                        x[c] = vs;
+                    }
+                    if (c < 7) {
+                        if (rw == 1) {  // next column's diagonal row
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) drn[k] = x[k];
+                        } else if (rw > 1) {
+                            const double xn = x[(c + 1) & 7];
+                            v[0] += xn * xn;
+#pragma unroll
+                            for (int k = 1; k < 8; ++k)
+                                if (c + 1 + k < 8) v[k] += xn * x[(c + 1 + k) & 7];
+                        }
+                    }
+                }
+                tm_st8(taddr(g), x);  // warp-collective: every lane stores (unchanged rows too)
+            }
+            if (tid == 0) taus[c] = tau;
+        }
+        __syncthreads();
+
+        // F. write back R + V and tau; explicit V -> Vbuf; Gram of V_b for T_b
+        double gq[28];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) gq[k] = 0.0;
+        for (int g = gpar; g < ngr; g += 2) {
+            const int r = row_of(g);
+            double x[8];
+            tm_ld8(taddr(g), x);
+            if (r < R) {
+                double vx[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    A[(int64_t)(jb + c) * ld + j0 + r] = x[c];
+                    const int dc = d0 + c;
+                    vx[c] = r < dc ? 0.0 : (r == dc ? 1.0 : x[c]);
+                    V[(int64_t)(kp + c) * ld + j0 + r] = vx[c];
+                }
+                if (r >= d0) {
+                    int k = 0;
+#pragma unroll
+                    for (int c1 = 0; c1 < 8; ++c1)
+#pragma unroll
+                        for (int c2 = c1 + 1; c2 < 8; ++c2) gq[k++] += vx[c1] * vx[c2];
+                }
+            }
+        }
+        if (tid < 8) a.tau[(int64_t)sl * a.M + jb + tid] = taus[tid];
+        block_sum_n<28, NW>(gq, ring, tot);
+        if (tid < 32) {
+            const int r = tid & 7;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) {
+                            const int gi = (k * (15 - k)) / 2 + (i - k - 1);
+                            s += trow[k] * tot[gi];
+                        }
+                    trow[i] = -taus[i] * s;
+                }
+            }
+            if (tid < 8)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Tbb[i * 8 + r] = trow[i];
+        }
+        __syncthreads();
+        for (int t = tid; t < 64; t += NT) {
+            const int r = t % 8, c = t / 8;
+            T[(kp + c) * ELM_NB + kp + r] = Tbb[c * 8 + r];
+        }
+        for (int t = tid; t < 8 * ELM_NB; t += NT) {
+            const int c = t / ELM_NB, r = t % ELM_NB;
+            if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
+        }
+        __syncthreads();  // Vbuf / T writes of this block before the next block reads them
+    }
+    // G. the last block's T extension: a Gram-only pass over [V_prev | V_last] (from Vbuf)
+    const int kpp = nb - 8;
+    if (kpp > 0) {
+        const int kpl = nb, mtiles = kpp >> 3;
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+        vp_stream_n<NT>(Vp, ld, R, kpl, ring, sst, RCH_MAX, [&](const double* st, int c, int rch, int nr) {
+            const int rcp = rch + 4, nq = nr / 8;
+            if (warp < mtiles) {
+                const int t = warp;
+#pragma unroll 2
+                for (int q = 0; q < nq; ++q) {
+                    const int k0 = 8 * q + kr, k1 = k0 + 4;
+                    dmma8(g0, g1, st[(t * 8 + cn) * rcp + k0], st[(kpp + cn) * rcp + k0]);
+                    dmma8(g2, g3, st[(t * 8 + cn) * rcp + k1], st[(kpp + cn) * rcp + k1]);
+                }
+            }
+        });
+        if (warp < mtiles) {
+            Gp[(2 * kr) * kpp + warp * 8 + cn] = g0 + g2;
+            Gp[(2 * kr + 1) * kpp + warp * 8 + cn] = g1 + g3;
+        }
+        __syncthreads();
+        t_extend_n<NT>(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
 // ------------------------------------------------------------------------------------------
 // Fused compact-WY trailing update for one 64-column block of one subdomain:
 //     W = V^T C   (64 x 64, K = R rows)          phase 1, DMMA, 32-row chunks, 2-stage cp.async
@@ -1892,6 +2376,7 @@ int panelp_ring(int64_t R, int smem_optin) {
     return (int)std::max<int64_t>(r, RED_ELEMS);
 }
 size_t panelp_smem_bytes(int64_t R, int ring) { return (size_t)(8 * (R + 4) + PANELP_FIXED + ring) * 8; }
+int panelt_ring() { return (pt::SMEM / 8 - PANELT_FIXED) & ~(2 * VNS - 1); }
 
 }  // namespace
 
@@ -1933,6 +2418,9 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     if ((e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)) != cudaSuccess)
         return e;
     const bool pp_ok = c->panel_merged && panelp_smem_bytes(ld, panelp_ring(ld, optin)) <= (size_t)optin;
+    const bool pt_ok = c->panel_tmem && (ld + 127) / 128 * 16 <= 512;
+    if (pt_ok && (e = cudaFuncSetAttribute(k_panel_t, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM)) != cudaSuccess)
+        return e;
     if (pp_ok && (e = cudaFuncSetAttribute(k_panel_p, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1943,7 +2431,14 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     const bool p8_ok = c->panel8 && panel8_smem(ld, std::min<int64_t>(M, ELM_NB)) <= (size_t)optin;
     if (p8_ok && (e = cudaFuncSetAttribute(k_panel_c8, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wyt::SMEM)) != cudaSuccess)
+    // (experiment hook) ELMDDM_WY_SMEM: dynamic shared memory of the trailing update, to force
+    // one CTA per SM and measure the single-CTA throughput
+    static int wy_smem = 0;
+    if (!wy_smem) {
+        wy_smem = wyt::SMEM;
+        if (const char* env = getenv("ELMDDM_WY_SMEM")) wy_smem = std::max(wyt::SMEM, atoi(env));
+    }
+    if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wy_smem)) != cudaSuccess)
         return e;
     // TMA descriptors: K_aug {ld, ncols, S} and V {ld, nb, S} (columns >= nb read as zero), boxes 16 x 64
     CUtensorMap tmK, tmV64, tmVlast;
@@ -1956,13 +2451,20 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     // subdomains are independent).
     // (with timing enabled the groups are serialised so that per-class event times do not overlap)
     const int ngroups = c->timing ? 1 : (int)std::min<int64_t>(c->qr_groups, S);
-    std::vector<cudaStream_t> streams(ngroups, st);
+    std::vector<cudaStream_t> streams(ngroups, st), pstr(ngroups, st);
+    const bool prio = ngroups > 1 && c->panel_prio && c->panel_tmem;
     if (ngroups > 1) {
         if ((e = c->ensure_streams(ngroups)) != cudaSuccess) return e;
+        if (prio && (e = c->ensure_panel_streams(ngroups)) != cudaSuccess) return e;
         cudaEventRecord(c->ev_fork, st);
         for (int g = 0; g < ngroups; ++g) {
             streams[g] = c->gstreams[g];
             cudaStreamWaitEvent(streams[g], c->ev_fork, 0);
+            pstr[g] = streams[g];
+            if (prio) {
+                pstr[g] = c->pstreams[g];
+                cudaStreamWaitEvent(pstr[g], c->ev_fork, 0);
+            }
         }
     }
     for (int j0 = 0; j0 < M; j0 += ELM_NB) {
@@ -1979,6 +2481,21 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 k_panel_c8<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, panel8_smem(ld - j0, nb), streams[g]>>>(pa, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            } else if (pt_ok && !c->panel_cluster) {
+                // (prio: the panel runs on the group's high-priority stream after the group's
+                // previous trailing update; the next trailing update waits for it)
+                if (prio && j0 > 0) cudaStreamWaitEvent(pstr[g], c->ev_wy[g], 0);
+                {
+                    KTimer kt(c, ELMDDM_K_PANEL, pstr[g]);
+                    PanelArgs pp = pa;
+                    pp.ring = panelt_ring();
+                    k_panel_t<<<(unsigned)(g1 - g0), pt::NT, pt::SMEM, pstr[g]>>>(pp, nb);
+                    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+                }
+                if (prio) {
+                    cudaEventRecord(c->ev_panel[g], pstr[g]);
+                    cudaStreamWaitEvent(streams[g], c->ev_panel[g], 0);
+                }
             } else if (pp_ok && !c->panel_cluster) {
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 PanelArgs pp = pa;
@@ -1986,7 +2503,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 k_panel_p<<<(unsigned)(g1 - g0), PNT, panelp_smem_bytes(ld - j0, pp.ring), streams[g]>>>(pp, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
-            for (int blk = 0; !p8_ok && !(pp_ok && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
+            for (int blk = 0; !p8_ok && !((pp_ok || pt_ok) && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 if (c->panel_cluster)
@@ -1999,15 +2516,20 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             dim3 grid((unsigned)((n_tr + 63) / 64), (unsigned)(g1 - g0));
             KTimer kt(c, ELMDDM_K_GEMM_QR, streams[g]);
             if (use_tma)
-                k_wy_tma<<<grid, wyt::NT, wyt::SMEM, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
+                k_wy_tma<<<grid, wyt::NT, wy_smem, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
                                                                    j0 + nb, n_tr, g0);
             else
                 k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            if (prio) cudaEventRecord(c->ev_wy[g], streams[g]);
         }
     }
     if (ngroups > 1) {
         for (int g = 0; g < ngroups; ++g) {
+            if (prio) {  // the last panel may end after the group's last trailing update
+                cudaEventRecord(c->ev_panel[g], pstr[g]);
+                cudaStreamWaitEvent(streams[g], c->ev_panel[g], 0);
+            }
             cudaEventRecord(c->ev_join[g], streams[g]);
             cudaStreamWaitEvent(st, c->ev_join[g], 0);
         }

@@ -497,10 +497,12 @@ def test_cg_solver_end_to_end_parity_config1():
     assert rel_l2(res["u"].numpy(), r["u"]) <= 1e-6
 
 
-@pytest.mark.parametrize("cluster,panel8,merged", [("0", "0", "1"), ("0", "0", "0"), ("1", "0", "1"), ("0", "1", "1")])
-def test_qr_panel_variants_config2(cluster, panel8, merged, monkeypatch):
-    """The four QR panel implementations on config 2 -- one CTA per panel walking its 8-column
-    blocks left-looking with the merged Gram pass (default), one launch per 8-column block, a
+@pytest.mark.parametrize("cluster,panel8,merged,tmem", [("0", "0", "1", "0"), ("0", "0", "1", "1"), ("0", "0", "0", "0"),
+                                                        ("1", "0", "1", "0"), ("0", "1", "1", "0")])
+def test_qr_panel_variants_config2(cluster, panel8, merged, tmem, monkeypatch):
+    """The QR panel implementations on config 2 -- one CTA per panel walking its 8-column
+    blocks left-looking with the merged Gram pass (default; block in shared memory or, `tmem`,
+    in tensor memory so that a trailing-update CTA shares the SM), one launch per 8-column block, a
     4-CTA cluster with the rows split, and the on-chip 8-CTA cluster panel (right-looking,
     all-reduces through distributed shared memory): the Gram identity of the factorisation and u
     parity with the oracle."""
@@ -509,6 +511,7 @@ def test_qr_panel_variants_config2(cluster, panel8, merged, monkeypatch):
     monkeypatch.setenv("ELMDDM_PANEL_CLUSTER", cluster)
     monkeypatch.setenv("ELMDDM_PANEL8", panel8)
     monkeypatch.setenv("ELMDDM_PANEL_MERGED", merged)
+    monkeypatch.setenv("ELMDDM_PANEL_TMEM", tmem)
     c = WL.config(2)
     M = c["M"]
     ctx, buf, _ = run_gpu(c, upto="assemble")
