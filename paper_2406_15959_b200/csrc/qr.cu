@@ -806,6 +806,34 @@ __device__ __forceinline__ void tm_ld8(uint32_t addr, double (&v)[8]) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) v[c] = __hiloint2double((int)r[2 * c + 1], (int)r[2 * c]);
 }
+// issue a 16-column TMEM load without waiting (pair with tm_wait_ld + tm_unpack8)
+__device__ __forceinline__ void tm_ld16(uint32_t addr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_unpack8(const uint32_t (&r)[16], double (&v)[8]) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = __hiloint2double((int)r[2 * c + 1], (int)r[2 * c]);
+}
+// store 8 doubles to TMEM without waiting (tm_wait_st before reloading the same columns)
+__device__ __forceinline__ void tm_st8_nw(uint32_t addr, const double (&v)[8]) {
+    uint32_t r[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        r[2 * c] = (uint32_t)__double2loint(v[c]);
+        r[2 * c + 1] = (uint32_t)__double2hiint(v[c]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+        ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 __device__ __forceinline__ void tm_st8(uint32_t addr, const double (&v)[8]) {
     uint32_t r[16];
 #pragma unroll
@@ -898,8 +926,17 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
     auto row_of = [&](int g) { return 128 * g + 32 * quarter + lane; };
     auto taddr = [&](int g) { return tm_addr(tbase, quarter, 16 * g); };
 
+#ifdef ELM_PANEL_PROF
+    long long tq[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tq0 = clock64(), tqa, fq[4] = {0, 0, 0, 0}, fqa = 0;
+#define TQ(i) do { const long long _n = clock64(); tq[i] += _n - tqa; tqa = _n; } while (0)
+#else
+#define TQ(i)
+#endif
     for (int b = 0; b < nb / 8; ++b) {
         const int kp = 8 * b, jb = j0 + kp, d0 = kp;
+#ifdef ELM_PANEL_PROF
+        tqa = clock64();
+#endif
         // A. the block -> TMEM (thread = row; rows >= R are zero)
         for (int g = gpar; g < ngr; g += 2) {
             const int r = row_of(g);
@@ -909,10 +946,28 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             tm_st8(taddr(g), v);
         }
         __syncthreads();
+        TQ(0);
         // stage rows [r0, r0 + nr) of the block into Cs (owner threads), then a barrier
         auto stage = [&](int r0, int nr, int rcp) {
             const int g0 = r0 / 128, g1 = (r0 + nr - 1) / 128;
-            for (int g = g0 + ((g0 & 1) != gpar); g <= g1; g += 2) {  // warp-uniform
+            int g = g0 + ((g0 & 1) != gpar);
+            for (; g + 2 <= g1; g += 4) {  // two row groups per wait (warp-uniform)
+                uint32_t ra[16], rb[16];
+                tm_ld16(taddr(g), ra);
+                tm_ld16(taddr(g + 2), rb);
+                tm_wait_ld();
+                double va[8], vb[8];
+                tm_unpack8(ra, va);
+                tm_unpack8(rb, vb);
+                const int r = row_of(g), s2 = row_of(g + 2);
+                if (r >= r0 && r < r0 + nr)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) Cs[c * rcp + r - r0] = va[c];
+                if (s2 >= r0 && s2 < r0 + nr)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) Cs[c * rcp + s2 - r0] = vb[c];
+            }
+            for (; g <= g1; g += 2) {
                 double v[8];
                 tm_ld8(taddr(g), v);
                 const int r = row_of(g);
@@ -923,17 +978,25 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             __syncthreads();
         };
         auto unstage = [&](int r0, int nr, int rcp) {
+            // a lane writes its row only if the row is in the chunk: the other lanes of the warp
+            // re-store the value they hold (loaded first; TMEM stores are warp-collective)
             const int g0 = r0 / 128, g1 = (r0 + nr - 1) / 128;
             for (int g = g0 + ((g0 & 1) != gpar); g <= g1; g += 2) {
-                double v[8];
-                tm_ld8(taddr(g), v);
                 const int r = row_of(g);
-                if (r >= r0 && r < r0 + nr) {
+                const bool in = r >= r0 && r < r0 + nr;
+                double v[8];
+                if (__all_sync(0xffffffffu, in)) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) v[c] = Cs[c * rcp + r - r0];
+                } else {
+                    tm_ld8(taddr(g), v);
+                    if (in)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) v[c] = Cs[c * rcp + r - r0];
                 }
-                tm_st8(taddr(g), v);
+                tm_st8_nw(taddr(g), v);
             }
+            tm_wait_st();
         };
         if (kp > 0) {
             // B. one pass over V_prev: W = V_prev^T C_b and G = V_prev[:, 0:kp-8]^T V_{b-1}
@@ -968,6 +1031,7 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                 }
             }
             __syncthreads();
+            TQ(1);
             // C. T extension by block b-1, then Z = T^T W
             if (kpp > 0) t_extend_n<NT>(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
             {
@@ -985,6 +1049,7 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                 }
                 __syncthreads();
             }
+            TQ(2);
             // D. C_b -= V_prev Z (DMMA on the staged rows, written back to TMEM)
             {
                 const int ksteps = kp >> 2;
@@ -1009,6 +1074,7 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             }
         }
 
+        TQ(3);
         // E. factor the 8 columns on the TMEM rows.  Partial sums of column c are accumulated
         //    while column c-1 is applied; row d's owner publishes the diagonal row in drow.
         double v[8];
@@ -1031,6 +1097,9 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
         for (int c = 0; c < 8; ++c) {
             const int d = d0 + c, nk = 8 - c;
             double* rb = red + (c & 1) * NW * 8;
+#ifdef ELM_PANEL_PROF
+            fqa = clock64();
+#endif
             {
                 const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
                 double h4[4], h2[2], h1;
@@ -1053,6 +1122,9 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                 if ((lane & 3) == 0) rb[warp * 8 + (lane >> 2)] = h1;
             }
             __syncthreads();
+#ifdef ELM_PANEL_PROF
+            { const long long _n = clock64(); fq[0] += _n - fqa; fqa = _n; }
+#endif
             const double* dr = drow + (c & 1) * 8;   // diagonal row: columns c .. 7 at dr[c..7]
             double mine = 0.0;
             if (lane < 8) {
@@ -1082,12 +1154,13 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             // accumulate the partial sums of column c + 1 on the updated rows
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = 0.0;
+#ifdef ELM_PANEL_PROF
+            { const long long _n = clock64(); fq[1] += _n - fqa; fqa = _n; }
+#endif
             double* drn = drow + ((c + 1) & 1) * 8;
-            for (int g = gpar; g < ngr; g += 2) {
+            auto body = [&](int g, double (&x)[8]) {
                 const int r = row_of(g);
                 const int rw = r - d;  // > 0: below the diagonal; 0: the diagonal row
-                double x[8];
-                tm_ld8(taddr(g), x);
                 if (r < R && rw >= 0) {
                     if (rw == 0) {
 #pragma unroll
@@ -1114,12 +1187,36 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                         }
                     }
                 }
-                tm_st8(taddr(g), x);  // warp-collective: every lane stores (unchanged rows too)
+            };
+            int g = gpar;
+            for (; g + 2 < ngr; g += 4) {  // two row groups per TMEM wait (warp-uniform)
+                uint32_t ra[16], rb[16];
+                tm_ld16(taddr(g), ra);
+                tm_ld16(taddr(g + 2), rb);
+                tm_wait_ld();
+                double xa[8], xb[8];
+                tm_unpack8(ra, xa);
+                tm_unpack8(rb, xb);
+                body(g, xa);
+                body(g + 2, xb);
+                tm_st8_nw(taddr(g), xa);  // warp-collective: every lane stores (unchanged rows too)
+                tm_st8_nw(taddr(g + 2), xb);
             }
+            for (; g < ngr; g += 2) {
+                double x[8];
+                tm_ld8(taddr(g), x);
+                body(g, x);
+                tm_st8_nw(taddr(g), x);
+            }
+            tm_wait_st();
+#ifdef ELM_PANEL_PROF
+            { const long long _n = clock64(); fq[2] += _n - fqa; fqa = _n; }
+#endif
             if (tid == 0) taus[c] = tau;
         }
         __syncthreads();
 
+        TQ(4);
         // F. write back R + V and tau; explicit V -> Vbuf; Gram of V_b for T_b
         double gq[28];
 #pragma unroll
@@ -1180,7 +1277,14 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             if (r >= kp + 8) T[(kp + c) * ELM_NB + r] = 0.0;
         }
         __syncthreads();  // Vbuf / T writes of this block before the next block reads them
+        TQ(5);
     }
+#ifdef ELM_PANEL_PROF
+    if (tid == 0 && blockIdx.x == 0 && (a.j0 == 256 || a.j0 == 1024))
+        printf("PTPROF j0=%d total %lld load %lld wpass %lld z %lld upd %lld fact %lld wb %lld | red+sync %lld par %lld apply %lld\n", a.j0, clock64() - tq0,
+               tq[0], tq[1], tq[2], tq[3], tq[4], tq[5], fq[0], fq[1], fq[2]);
+#endif
+#undef TQ
     // G. the last block's T extension: a Gram-only pass over [V_prev | V_last] (from Vbuf)
     const int kpp = nb - 8;
     if (kpp > 0) {
