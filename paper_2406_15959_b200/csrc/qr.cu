@@ -865,6 +865,7 @@ __device__ __forceinline__ void vp_stream_n(const double* __restrict__ Vp, int64
                                             int sst, int rmax, F&& consume) {
     int rch = vp_rows(kp, sst);
     if (rch > rmax) rch = rmax;
+    rch = 1 << (31 - __clz(rch));  // a power of two: chunks tile the staging windows of rmax rows
     const int nch = (R + rch - 1) / rch;
 #pragma unroll
     for (int i = 0; i < VNS - 1; ++i) {
@@ -1004,7 +1005,8 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
             vp_stream_n<NT>(Vp, ld, R, kp, ring, sst, RCH_MAX, [&](const double* st, int c, int rch, int nr) {
                 const int rcp = rch + 4, nq = nr / 8;
-                stage(c * rch, nr, rcp);
+                const int r0 = c * rch, w0 = r0 & ~(RCH_MAX - 1), off = r0 - w0;  // staging window
+                if (off == 0) stage(w0, min(RCH_MAX, R - w0), RCH_MAX + 4);
                 if (warp < mtiles) {
                     const bool two = warp < mtiles - 1;
                     const int t = warp;
@@ -1012,8 +1014,8 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                     for (int q = 0; q < nq; ++q) {
                         const int k0 = 8 * q + kr, k1 = k0 + 4;
                         const double av0 = st[(t * 8 + cn) * rcp + k0], av1 = st[(t * 8 + cn) * rcp + k1];
-                        dmma8(a0, a1, av0, Cs[cn * rcp + k0]);
-                        dmma8(a2, a3, av1, Cs[cn * rcp + k1]);
+                        dmma8(a0, a1, av0, Cs[cn * (RCH_MAX + 4) + off + k0]);
+                        dmma8(a2, a3, av1, Cs[cn * (RCH_MAX + 4) + off + k1]);
                         if (two) {
                             dmma8(g0, g1, av0, st[(kpp + cn) * rcp + k0]);
                             dmma8(g2, g3, av1, st[(kpp + cn) * rcp + k1]);
@@ -1059,17 +1061,22 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
                 __syncthreads();
                 vp_stream_n<NT>(Vp, ld, R, kp, ring, sst, RCH_MAX, [&](const double* st, int c, int rch, int nr) {
                     const int rcp = rch + 4, nmt = nr / 8;
-                    stage(c * rch, nr, rcp);
+                    const int r0 = c * rch, w0 = r0 & ~(RCH_MAX - 1), off = r0 - w0, wn = min(RCH_MAX, R - w0);
+                    constexpr int WCP = RCH_MAX + 4;
+                    if (off == 0) stage(w0, wn, WCP);
                     for (int mt = warp; mt < nmt; mt += NW) {
-                        double c0 = Cs[(2 * kr) * rcp + mt * 8 + cn], c1 = Cs[(2 * kr + 1) * rcp + mt * 8 + cn];
+                        const int rr = off + mt * 8 + cn;
+                        double c0 = Cs[(2 * kr) * WCP + rr], c1 = Cs[(2 * kr + 1) * WCP + rr];
 #pragma unroll
                         for (int t = 0; t < 14; ++t)
                             if (t < ksteps) dmma8(c0, c1, st[(t * 4 + kr) * rcp + mt * 8 + cn], zb[t]);
-                        Cs[(2 * kr) * rcp + mt * 8 + cn] = c0;
-                        Cs[(2 * kr + 1) * rcp + mt * 8 + cn] = c1;
+                        Cs[(2 * kr) * WCP + rr] = c0;
+                        Cs[(2 * kr + 1) * WCP + rr] = c1;
                     }
-                    __syncthreads();
-                    unstage(c * rch, nr, rcp);
+                    if (off + nr == wn) {  // the window's last chunk: write the window back
+                        __syncthreads();
+                        unstage(w0, wn, WCP);
+                    }
                 });
             }
         }
