@@ -16,7 +16,7 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, NT = 256;
+constexpr int BM = 64, BN = 64, BK = 32, STAGES = 3, NT = 256;
 constexpr int PAD_MN = BM + 8;  // stride of [k][m|n] layouts (== 8 mod 16 doubles)
 constexpr int PAD_K = BK + 4;   // stride of [m|n][k] layouts (== 4 mod 16 doubles)
 constexpr int A_ELEMS = (BM * PAD_K > BK * PAD_MN) ? BM * PAD_K : BK * PAD_MN;
