@@ -455,12 +455,9 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
     if (c->cfg.problem == 6) {
         const int pp = c->cfg.p * c->cfg.p;
         const int nt = std::min(512, std::max(32, (pp + 7) / 8 + 31) / 32 * 32);
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_coef, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
+        // (a per-device attribute: set on every call)
+        cudaError_t e = cudaFuncSetAttribute(k_coef, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        if (e != cudaSuccess) return e;
         k_coef<<<(unsigned)c->sz.S, nt, sizeof(double) * 4 * CT * c->cfg.p, st>>>(
             c->cfg, reinterpret_cast<const double4*>(c->d_grf), c->ngrf, reinterpret_cast<double4*>(c->d_coef));
         coef = reinterpret_cast<const double4*>(c->d_coef);

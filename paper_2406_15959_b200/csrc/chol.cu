@@ -751,7 +751,9 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     double* Ybuf = z + n;       // [nblk] packed tiles (n is a multiple of 64: 16-byte aligned)
     double* Cbuf = Ybuf + (int64_t)nblk * ELM_TS;
     cudaError_t e;
-    static int grid_ll = 0, grid_sv = 0;
+    // per-context (per-device) launch configuration, set up on the first call
+    int& grid_ll = c->chol_grid;
+    int& grid_sv = c->trsv_grid;
     if (!grid_ll) {
         if ((e = cudaFuncSetAttribute(k_chol_ll, cudaFuncAttributeMaxDynamicSharedMemorySize, llc::SMEM)) !=
                 cudaSuccess ||

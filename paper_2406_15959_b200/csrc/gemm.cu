@@ -153,12 +153,9 @@ __global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
 
 template <bool TA, bool TB>
 cudaError_t launch(const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c, int cls) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // (a per-device attribute: set on every launch, a few microseconds of host time)
+    cudaError_t e = cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
     KTimer kt(c, cls, st);
     k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, st>>>(g);

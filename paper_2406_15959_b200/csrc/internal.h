@@ -153,6 +153,7 @@ struct elmddm_ctx {
     int* d_ntc = nullptr;            // [nblk] tiles of column J
     int* d_cready = nullptr;         // [nblk] C(I, klast(I)) published for the diagonal task of row I
     mutable int chol_epoch = 0;
+    mutable int chol_grid = 0, trsv_grid = 0;  // persistent-kernel grids (chol.cu, first call)
     mutable std::vector<cudaStream_t> gstreams;
     mutable cudaEvent_t ev_fork = nullptr;
     mutable std::vector<cudaEvent_t> ev_join;

@@ -2544,11 +2544,8 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         return e;
     // (experiment hook) ELMDDM_WY_SMEM: dynamic shared memory of the trailing update, to force
     // one CTA per SM and measure the single-CTA throughput
-    static int wy_smem = 0;
-    if (!wy_smem) {
-        wy_smem = wyt::SMEM;
-        if (const char* env = getenv("ELMDDM_WY_SMEM")) wy_smem = std::max(wyt::SMEM, atoi(env));
-    }
+    int wy_smem = wyt::SMEM;
+    if (const char* env = getenv("ELMDDM_WY_SMEM")) wy_smem = std::max(wyt::SMEM, atoi(env));
     if ((e = cudaFuncSetAttribute(k_wy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, wy_smem)) != cudaSuccess)
         return e;
     // TMA descriptors: K_aug {ld, ncols, S} and V {ld, nb, S} (columns >= nb read as zero), boxes 16 x 64

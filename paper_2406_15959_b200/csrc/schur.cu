@@ -344,12 +344,9 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         CUtensorMap tmR, tmA;
         if (!elm_encode_tmap(&tmR, Kaug, ld, ncols, S, ld * ncols) || !elm_encode_tmap(&tmA, At, M, nat, S, (int64_t)M * nat))
             return cudaErrorInvalidValue;
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(k_trsm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, trw::SMEM)) != cudaSuccess)
-                return e;
-            attr = true;
-        }
+        // (a per-device attribute: set on every call, a few microseconds of host time)
+        if ((e = cudaFuncSetAttribute(k_trsm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, trw::SMEM)) != cudaSuccess)
+            return e;
         dim3 g((nat + 63) / 64, (unsigned)S);
         KTimer kt(c, ELMDDM_K_TRSM, st);
         k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
