@@ -118,7 +118,7 @@ def ncu_traffic(k: int):
     if not os.path.exists(path):
         return None, None
     d = json.load(open(path))
-    return d["dram_bytes_per_launch"], d["source"]
+    return d, d["source"]
 
 
 # ------------------------------------------------------------------------------------------------
@@ -370,13 +370,18 @@ def main():
     lf_ms = phases.get("local_factor", 0.0)
     achieved_lf = work["flop_qr"] / (lf_ms * 1e-3) / 1e12 if lf_ms > 0 else None
     step_kernel_ms = max(sum(kms.values()), 1e-12)
-    traffic, traffic_src = ncu_traffic(args.config)
+    # DRAM traffic of the dominant kernel: one ncu capture of a whole step of this workload in
+    # the bench's launch configuration (tools/gpu_session.sh traffic), per launch; the algorithmic
+    # bytes per launch are taken at the same launch granularity (the capture's launch count)
+    trec, traffic_src = ncu_traffic(args.config)
+    wy_launches = trec["launches"] if trec else None
+    traffic = trec["dram_bytes_per_launch"] if trec else None
     roof = {"bound": "tensor", "achieved": achieved_wy, "peak": dmma, "unit": "TFLOP/s",
             "frac": (achieved_wy / dmma) if achieved_wy and dmma else None, "traffic": traffic,
             "traffic_source": traffic_src,
-            "algorithmic_bytes_per_launch": work["bytes_wy"] / max(kt["count"]["gemm_qr"] / args.steps, 1),
+            "algorithmic_bytes_per_launch": (work["bytes_wy"] / wy_launches) if wy_launches else None,
             "kernel": "k_wy_tma: fused compact-WY trailing update of the blocked Householder QR (FP64 DMMA, TMA-staged)",
-            "flop_per_step": work["flop_wy"], "kernel_ms_per_step": wy_ms, "launches_per_step": kt["count"]["gemm_qr"] / args.steps,
+            "flop_per_step": work["flop_wy"], "kernel_ms_per_step": wy_ms, "launches_per_step": wy_launches,
             "share_of_step": wy_ms / step_kernel_ms,
             "peak_source": "measured on this GPU in this run: register-resident DMMA.8x8x4 loop (elmddm_dmma_probe)",
             "peak_ratio_rule": fp64_ratio_peak,
