@@ -131,6 +131,7 @@ struct elmddm_ctx {
     double* d_coef = nullptr;        // problem 6: [S][p*p][4] rho, grad rho at the interior points
     mutable DistState dist;          // multi-rank interface factorisation (elmddm_dist_*)
     int panel_prio = 1;              // ELMDDM_PANEL_PRIO: panels on high-priority streams (with k_panel_t)
+    int panel8_tmem = 0;             // ELMDDM_PANEL8_TMEM: 8-CTA cluster panel in TMEM (k_panel_c8t)
     int panel_tmem = 1;              // ELMDDM_PANEL_TMEM: TMEM-resident panel block (k_panel_t)
     int panel_merged = 1;            // ELMDDM_PANEL_MERGED: one launch per panel, merged Gram pass (k_panel_p)
     int panel8 = 0;                  // ELMDDM_PANEL8: on-chip 8-CTA cluster panels (qr.cu k_panel_c8)

@@ -2475,6 +2475,436 @@ __global__ void __cluster_dims__(p8::CL, 1, 1) __launch_bounds__(p8::NT, 1) k_pa
     for (int t = tid; t < 64 * 64; t += NT) T[t] = Ts[t];
 }
 
+
+// ------------------------------------------------------------------------------------------
+// k_panel_c8 with the panel in tensor memory (k_panel_c8t): the 8-CTA cluster panel of small
+// slabs, each CTA's rows of all panel columns in TMEM (row r = 128 g + 32 q + lane -> TMEM lane
+// 32 q + lane, columns [128 g, 128 g + 128): 64 doubles), so the CTA needs ~116 KB of shared
+// memory and shares its SM with a trailing-update CTA, as k_panel_t does for large slabs.  The
+// block being factored is staged in shared memory (the column steps are k_panel_c8's), G =
+// V_b^T A_panel is computed on staged 64-row chunks, and C_rest -= V_b Z runs on the TMEM rows.
+// ------------------------------------------------------------------------------------------
+namespace p8t {
+constexpr int SMEM = 116 * 1024;
+constexpr int GCH = 64;      // rows per staged chunk of the G pass
+constexpr int GLD = 68;      // its column stride
+}  // namespace p8t
+
+__global__ void __cluster_dims__(p8::CL, 1, 1) __launch_bounds__(p8::NT, 2) k_panel_c8t(PanelArgs a, int nb) {
+    using namespace p8;
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint32_t s_tbase;
+    const int z = (int)cl.block_rank();
+    const int sl = a.s_off + (int)blockIdx.x / CL;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0;
+    const int R = (int)(ld - j0);
+    const int Rq = p8_rq(R);
+    const int r0 = z * Rq, nr = max(0, min(Rq, R - r0));
+    const int RP = Rq + 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int quarter = warp & 3, gpar = warp >> 2;
+    const int ngr = (nr + 127) / 128;
+    double* Bp = sm;                            // [8][RP] the block being factored, own rows
+    double* Gst = Bp + 8 * RP;                  // [64][GLD] staged rows of the G pass
+    double* xc = Gst + 64 * p8t::GLD;           // [2][CL][XC]
+    double* xb = xc + 2 * CL * XC;              // [CL][XB]; after the sum: Gs = slot 0, Zs = slot 1
+    double* red = xb + CL * XB;                 // [NW][8]
+    double* taus = red + NW * 8;                // [64]
+    double* Tb = taus + 64;                     // [8][8]
+    double* Rsv = Tb + 64;                      // [64]
+    uint64_t* mbx = reinterpret_cast<uint64_t*>(Rsv + 64);
+    double* Gs = xb;
+    double* Zs = xb + XB;                       // [8][68]
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* V = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&s_tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = s_tbase;
+    auto row_of = [&](int g) { return 128 * g + 32 * quarter + lane; };
+    auto taddr = [&](int g, int cb) { return tm_addr(tbase, quarter, 128 * g + 16 * cb); };
+    const int ncb = nb / 8;
+
+    // A. own rows of the panel -> TMEM (rows >= nr zero)
+    for (int g = gpar; g < ngr; g += 2) {
+        const int r = row_of(g);
+        for (int cb = 0; cb < ncb; ++cb) {
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = r < nr ? __ldcg(A + (int64_t)(j0 + 8 * cb + c) * ld + j0 + r0 + r) : 0.0;
+            tm_st8_nw(taddr(g, cb), v);
+        }
+        tm_wait_st();
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) elmtma::mbar_init(mbx + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl.sync();
+    const uint32_t xc_s = elmtma::su32(xc), xb_s = elmtma::su32(xb), mbx_s = elmtma::su32(mbx);
+    int xcnt = 0;
+
+    for (int b = 0; b < ncb; ++b) {
+        const int jb = 8 * b;
+        // stage the block (own rows) from TMEM
+        for (int g = gpar; g < ngr; g += 2) {
+            double v[8];
+            tm_ld8(taddr(g, b), v);
+            const int r = row_of(g);
+            if (r < Rq)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) Bp[c * RP + r] = v[c];
+        }
+        __syncthreads();
+        // B. the 8 columns of the block, one cluster all-reduce each
+        
+        for (int c = 0; c < 8; ++c) {
+            const int j = jb + c;           // panel column == panel-relative row of its diagonal
+            const int zo = j / Rq, dl = j - zo * Rq;
+            const int nk = 8 - c;
+            const int jl = j - r0;          // local row of the diagonal (rows > jl take part)
+            
+            // partial sums over own rows below the diagonal; thread t owns rows t, t + NT, ...
+            // for the whole panel, so the column loop needs no trailing barrier
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = 0.0;
+            for (int r = tid; r < nr; r += NT) {
+                if (r <= jl) continue;
+                const double x = Bp[c * RP + r];
+                v[0] += x * x;
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) v[k] += x * Bp[(c + k) * RP + r];
+            }
+             
+            // warp sum of the 8 values by halving exchanges (9 shuffles): lanes 4k..4k+3 end
+            // with the sum of value k
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                double h4[4], h2[2], h1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double snd = b4 ? v[i] : v[i + 4];
+                    h4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double snd = b3 ? h4[i] : h4[i + 2];
+                    h2[i] = (b3 ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+                {
+                    const double snd = b2 ? h2[0] : h2[1];
+                    h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+                }
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) red[warp * 8 + (lane >> 2)] = h1;
+            }
+            __syncthreads();
+             
+            const int xb_i = xcnt & 1;
+            double* xcb = xc + xb_i * CL * XC;
+            if (tid == 0) elmtma::mbar_expect(mbx + xb_i, CL * XC * 8);
+            if (tid < CL * XC / 2) {
+                const int dst = tid / (XC / 2), i = 2 * (tid % (XC / 2));
+                double p[2] = {0.0, 0.0};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (i + e < 8) {
+                        for (int w = 0; w < NW; ++w) p[e] += red[w * 8 + i + e];
+                    } else if (z == zo && i + e - 8 < nk) {
+                        p[e] = Bp[(c + i + e - 8) * RP + dl];
+                    }
+                }
+                st_async2(mapa_u32(xc_s + (uint32_t)((xb_i * CL * XC + z * XC + i) * 8), dst), p[0], p[1],
+                          mapa_u32(mbx_s + 8u * xb_i, dst));
+            }
+            
+            
+            mbar_wait_cluster(mbx + xb_i, (xcnt >> 1) & 1);
+            
+            ++xcnt;
+            
+            // lane k < 8: sum of value k over the CTAs (fixed order); lane 8 + k: the diagonal
+            // row's value in column j + k; then broadcast within the warp
+            double mine = 0.0;
+            if (lane < 8) {
+                double s0 = xcb[0 * XC + lane] + xcb[1 * XC + lane], s1 = xcb[2 * XC + lane] + xcb[3 * XC + lane];
+                double s2 = xcb[4 * XC + lane] + xcb[5 * XC + lane], s3 = xcb[6 * XC + lane] + xcb[7 * XC + lane];
+                mine = (s0 + s1) + (s2 + s3);
+            } else if (lane < 16) {
+                mine = xcb[zo * XC + lane];
+            }
+            const double ts0 = __shfl_sync(0xffffffffu, mine, 0);
+            const double x0 = __shfl_sync(0xffffffffu, mine, 8);
+            const double nrm = sqrt(x0 * x0 + ts0);
+            double alpha = x0, tau = 0.0, scale = 0.0;
+            if (nrm != 0.0) {
+                alpha = x0 >= 0.0 ? -nrm : nrm;
+                scale = 1.0 / (x0 - alpha);
+                tau = (alpha - x0) / alpha;
+            }
+            // lane k (1..7): w_k = tau (y_k + scale t_k), y_k from lane 8 + k
+            const double ydl = __shfl_sync(0xffffffffu, mine, (lane & 7) + 8);
+            const double wl = (lane >= 1 && lane < nk) ? tau * (ydl + scale * mine) : 0.0;
+            double w[8], yd[8];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) {
+                w[k] = __shfl_sync(0xffffffffu, wl, k);
+                yd[k] = __shfl_sync(0xffffffffu, mine, k + 8);
+            }
+             
+            if (tau != 0.0) {
+                for (int r = tid; r < nr; r += NT) {
+                    if (r <= jl) continue;
+                    const double x = Bp[c * RP + r];
+                    const double vs = scale * x;
+#pragma unroll
+                    for (int k = 1; k < 8; ++k)
+                        if (k < nk) Bp[(c + k) * RP + r] -= w[k] * vs;
+                    Bp[c * RP + r] = vs;
+                }
+            }
+            if (z == zo && tid == dl % NT) {  // the owner of the diagonal row
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (k < nk) Bp[(c + k) * RP + dl] = yd[k] - w[k];
+                Bp[c * RP + dl] = alpha;
+            }
+            if (tid == 0) taus[j] = tau;
+            
+        }
+        __syncthreads();
+        
+        
+        // C. explicit V_b in the diagonal block (unit diagonal, zeros above; R saved)
+
+        // C. explicit V_b in the diagonal block of the staged block (R saved)
+        const int zb = jb / Rq, db = jb - zb * Rq;
+        if (z == zb && tid < 64) {
+            const int r = tid & 7, i = tid >> 3;
+            if (r <= i) {
+                Rsv[tid] = Bp[i * RP + db + r];
+                Bp[i * RP + db + r] = r == i ? 1.0 : 0.0;
+            }
+        }
+        __syncthreads();
+        // D. G = V_b^T A_panel over own rows >= jb: staged 64-row chunks (block b's columns from
+        //    the staged block, the others from TMEM), DMMA, then the cluster all-reduce
+        const int kb0 = max(0, jb - r0);
+        const int ntile = ncb;
+        if (tid == 0) elmtma::mbar_expect(mbx + 2, CL * ntile * 64 * 8);
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        for (int ck = kb0 & ~(p8t::GCH - 1); ck < nr; ck += p8t::GCH) {
+            // owner threads of rows [ck, ck + GCH): groups g = ck / 128, quarters of that half
+            const int g = ck / 128;
+            if ((g & 1) == gpar) {
+                const int r = row_of(g);
+                const bool in = r >= ck && r < ck + p8t::GCH;
+                for (int cb = 0; cb < ncb; ++cb) {
+                    double v[8];
+                    tm_ld8(taddr(g, cb), v);
+                    if (in) {
+                        if (cb == b)
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) v[c] = Bp[c * RP + r];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) Gst[(8 * cb + c) * p8t::GLD + r - ck] = r < nr ? v[c] : 0.0;
+                    }
+                }
+            }
+            __syncthreads();
+            if (warp < ntile) {
+                const double* va = Gst + (jb + (lane >> 2)) * p8t::GLD + (lane & 3);
+                const double* vbp = Gst + (8 * warp + (lane >> 2)) * p8t::GLD + (lane & 3);
+                const int k1 = min(p8t::GCH, nr - ck);
+                for (int k0 = max(0, kb0 - ck); k0 < k1; k0 += 8) {
+                    dmma8(a0, a1, va[k0], vbp[k0]);
+                    dmma8(b0, b1, va[k0 + 4], vbp[k0 + 4]);
+                }
+            }
+            __syncthreads();
+        }
+        if (warp < ntile) {
+            const int gi = (lane >> 2) * 64 + 8 * warp + 2 * (lane & 3);
+#pragma unroll
+            for (int dst = 0; dst < CL; ++dst)
+                st_async2(mapa_u32(xb_s + (uint32_t)((z * XB + gi) * 8), dst), a0 + b0, a1 + b1, mapa_u32(mbx_s + 16u, dst));
+        }
+        mbar_wait_cluster(mbx + 2, b & 1);
+        double gsum[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * NT;
+            double s = 0.0;
+            if ((e & 63) < nb)
+                for (int q = 0; q < CL; ++q) s += xb[q * XB + e];
+            gsum[h] = s;
+        }
+        __syncthreads();
+        Gs[tid] = gsum[0];
+        Gs[tid + NT] = gsum[1];
+        __syncthreads();
+        // E. T_b and the Gram entries for T (as k_panel_c8)
+        if (tid < 8) {
+            const int r = tid;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[jb + i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) s += trow[k] * Gs[k * 64 + jb + i];
+                    trow[i] = -taus[jb + i] * s;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Tb[i * 8 + r] = trow[i];
+        }
+        if (z == 0)
+            for (int t = tid; t < 8 * (jb + 8); t += NT) {
+                const int i = t / (jb + 8), k = t % (jb + 8);
+                if (k < jb + i) T[(jb + i) * ELM_NB + k] = Gs[i * 64 + k];
+            }
+        __syncthreads();
+        // F. Z = T_b^T W; C_rest -= V_b Z on the TMEM rows >= jb (thread = row)
+        const int c1 = jb + 8, ncr = nb - c1;
+        if (ncr > 0) {
+            for (int t = tid; t < 8 * ncr; t += NT) {
+                const int i = t / ncr, col = c1 + t % ncr;
+                double s = 0.0;
+                for (int k = 0; k <= i; ++k) s += Tb[i * 8 + k] * Gs[k * 64 + col];
+                Zs[i * 68 + col] = s;
+            }
+            __syncthreads();
+            for (int g = gpar; g < ngr; g += 2) {
+                const int r = row_of(g);
+                const bool act = r < nr && r >= kb0;
+                double vb[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) vb[i] = act ? Bp[i * RP + r] : 0.0;
+                for (int cb = b + 1; cb < ncb; ++cb) {
+                    double x[8];
+                    tm_ld8(taddr(g, cb), x);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) s += vb[i] * Zs[i * 68 + 8 * cb + c];
+                        x[c] -= s;
+                    }
+                    tm_st8_nw(taddr(g, cb), x);
+                }
+                tm_wait_st();
+            }
+        }
+        // G. restore R in the diagonal block; the factored block back to TMEM
+        if (z == zb && tid < 64) {
+            const int r = tid & 7, i = tid >> 3;
+            if (r <= i) Bp[i * RP + db + r] = Rsv[tid];
+        }
+        __syncthreads();
+        for (int g = gpar; g < ngr; g += 2) {
+            const int r = row_of(g);
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = r < nr ? Bp[c * RP + r] : 0.0;
+            tm_st8(taddr(g, b), v);
+        }
+        __syncthreads();
+    }
+
+    // H. write back R + V (in place) and the explicit V of own rows; tau
+    for (int g = gpar; g < ngr; g += 2) {
+        const int r = row_of(g);
+        for (int cb = 0; cb < ncb; ++cb) {
+            double x[8];
+            tm_ld8(taddr(g, cb), x);
+            if (r < nr) {
+                const int gr = r0 + r;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int col = 8 * cb + c;
+                    A[(int64_t)(j0 + col) * ld + j0 + gr] = x[c];
+                    V[(int64_t)col * ld + j0 + gr] = gr < col ? 0.0 : (gr == col ? 1.0 : x[c]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    if (z != 0) return;
+    if (tid < nb) a.tau[(int64_t)sl * a.M + j0 + tid] = taus[tid];
+    // I. CTA 0: T = compact-WY factor of the panel from S = strictly upper part of V^T V:
+    //    T(i,i) = tau_i; by blocks, T[0:kp, kp:kp+8] = -T[0:kp,0:kp] S[0:kp, kp:kp+8] T_b
+    __syncthreads();
+    double* Ss = sm;                 // [64][64] column-major (panel smem is free now)
+    double* Ts = sm + 64 * 64;       // [64][64]
+    double* Ys = Ts + 64 * 64;       // [64][8]
+    for (int t = tid; t < 64 * 64; t += NT) {
+        const int r = t & 63, c = t >> 6;
+        Ss[t] = (r < c && c < nb) ? T[t] : 0.0;
+        Ts[t] = 0.0;
+    }
+    __syncthreads();
+    for (int b = 0; b < nb / 8; ++b) {
+        const int kp = 8 * b;
+        if (tid < 8) {  // T_b
+            const int r = tid;
+            double trow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) trow[i] = (i == r) ? taus[kp + i] : 0.0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                if (r < i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k >= r && k < i) s += trow[k] * Ss[(kp + i) * 64 + kp + k];
+                    trow[i] = -taus[kp + i] * s;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Ts[(kp + i) * 64 + kp + r] = trow[i];
+        }
+        __syncthreads();
+        if (kp > 0) {
+            for (int t = tid; t < kp * 8; t += NT) {  // Y = S[0:kp, kp:kp+8] T_b
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = 0; k <= c; ++k) s += Ss[(kp + k) * 64 + r] * Ts[(kp + c) * 64 + kp + k];
+                Ys[c * 64 + r] = s;
+            }
+            __syncthreads();
+            for (int t = tid; t < kp * 8; t += NT) {  // T[0:kp, kp+c] = -T[0:kp,0:kp] Y
+                const int r = t % kp, c = t / kp;
+                double s = 0.0;
+                for (int k = r; k < kp; ++k) s += Ts[k * 64 + r] * Ys[c * 64 + k];
+                Ts[(kp + c) * 64 + r] = -s;
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = tid; t < 64 * 64; t += NT) T[t] = Ts[t];
+
+}
+
 constexpr int PANEL_FIXED = 8 * 56 * 2 + 40 + 64 + 8;  // Wsm, Zsm, tot, Tbb, taus (doubles)
 // V_prev ring of the panel-block kernel for R resident rows: all shared memory the block leaves
 int panel_ring(int64_t R, int smem_optin) {
@@ -2539,7 +2969,13 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         return e;
     if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
         return e;
-    const bool p8_ok = c->panel8 && panel8_smem(ld, std::min<int64_t>(M, ELM_NB)) <= (size_t)optin;
+    // (the TMEM variant of the cluster panel measured slower: config 3 slabs of 32 / 16
+    // subdomains 26.6 -> 28.9 / 15.0 -> 16.6 ms; opt-in ELMDDM_PANEL8_TMEM=1)
+    const bool p8t_ok = c->panel8 && c->panel8_tmem && p8_rq(ld) <= 512;
+    const bool p8_ok = !p8t_ok && c->panel8 && panel8_smem(ld, std::min<int64_t>(M, ELM_NB)) <= (size_t)optin;
+    if (p8t_ok &&
+        (e = cudaFuncSetAttribute(k_panel_c8t, cudaFuncAttributeMaxDynamicSharedMemorySize, p8t::SMEM)) != cudaSuccess)
+        return e;
     if (p8_ok && (e = cudaFuncSetAttribute(k_panel_c8, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
         return e;
     // (experiment hook) ELMDDM_WY_SMEM: dynamic shared memory of the trailing update, to force
@@ -2585,7 +3021,18 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
             if (g1 <= g0) continue;
             PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0, ring};
-            if (p8_ok) {
+            if (p8t_ok) {
+                if (prio && j0 > 0) cudaStreamWaitEvent(pstr[g], c->ev_wy[g], 0);
+                {
+                    KTimer kt(c, ELMDDM_K_PANEL, pstr[g]);
+                    k_panel_c8t<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, p8t::SMEM, pstr[g]>>>(pa, nb);
+                    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+                }
+                if (prio) {
+                    cudaEventRecord(c->ev_panel[g], pstr[g]);
+                    cudaStreamWaitEvent(streams[g], c->ev_panel[g], 0);
+                }
+            } else if (p8_ok) {
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 k_panel_c8<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, panel8_smem(ld - j0, nb), streams[g]>>>(pa, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -2611,7 +3058,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 k_panel_p<<<(unsigned)(g1 - g0), PNT, panelp_smem_bytes(ld - j0, pp.ring), streams[g]>>>(pp, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
-            for (int blk = 0; !p8_ok && !((pp_ok || pt_ok) && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
+            for (int blk = 0; !p8_ok && !p8t_ok && !((pp_ok || pt_ok) && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 if (c->panel_cluster)

@@ -498,7 +498,7 @@ def test_cg_solver_end_to_end_parity_config1():
 
 
 @pytest.mark.parametrize("cluster,panel8,merged,tmem", [("0", "0", "1", "0"), ("0", "0", "1", "1"), ("0", "0", "0", "0"),
-                                                        ("1", "0", "1", "0"), ("0", "1", "1", "0")])
+                                                        ("1", "0", "1", "0"), ("0", "1", "1", "0"), ("0", "1", "1", "1")])
 def test_qr_panel_variants_config2(cluster, panel8, merged, tmem, monkeypatch):
     """The QR panel implementations on config 2 -- one CTA per panel walking its 8-column
     blocks left-looking with the merged Gram pass (default; block in shared memory or, `tmem`,
@@ -512,6 +512,7 @@ def test_qr_panel_variants_config2(cluster, panel8, merged, tmem, monkeypatch):
     monkeypatch.setenv("ELMDDM_PANEL8", panel8)
     monkeypatch.setenv("ELMDDM_PANEL_MERGED", merged)
     monkeypatch.setenv("ELMDDM_PANEL_TMEM", tmem)
+    monkeypatch.setenv("ELMDDM_PANEL8_TMEM", tmem)
     c = WL.config(2)
     M = c["M"]
     ctx, buf, _ = run_gpu(c, upto="assemble")
