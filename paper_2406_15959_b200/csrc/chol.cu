@@ -764,7 +764,13 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_ll, llc::NT, llc::SMEM);
         if (const char* env = getenv("ELMDDM_CHOL_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(env));
         grid_ll = (per_sm > 0 ? per_sm : 1) * c->nsm;
-        grid_sv = c->nsm;
+        // the solves are latency-bound (one dependent chain per tile row): as many co-resident
+        // CTAs as fit, at most 3 per SM (cfg3: 2.79 ms at 1, 2.02 ms at 3)
+        int sv_per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sv_per, k_band_trsv, 256, TRSV_SMEM);
+        sv_per = std::min(sv_per, 3);
+        if (const char* env = getenv("ELMDDM_TRSV_CTAS_PER_SM")) sv_per = std::min(sv_per, atoi(env));
+        grid_sv = std::max(sv_per, 1) * c->nsm;
     }
     // right-hand side into the factorisation order
     k_perm_zero<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(yv, n);
