@@ -313,6 +313,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_PANEL_TMEM")) c->panel_tmem = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL8_TMEM")) c->panel8_tmem = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL_PRIO")) c->panel_prio = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_SCHUR_SIDE")) c->schur_side = atoi(env) != 0;
     }
     elmddm_sizes_t& z = c->sz;
     std::memset(&z, 0, sizeof(z));

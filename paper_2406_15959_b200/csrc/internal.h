@@ -110,6 +110,7 @@ struct elmddm_ctx {
 
     // instrumentation (mutable: launch wrappers take a const context)
     mutable int timing = 0;
+    int schur_side = 1;  // S_s GEMM on a side stream beside the TRSM (ELMDDM_SCHUR_SIDE=0: in order)
     mutable int64_t launches = 0;
     mutable int64_t cls_count[ELMDDM_NCLASS] = {};
     mutable double cls_ms[ELMDDM_NCLASS] = {};

@@ -339,6 +339,22 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols, kaug = c->sz.kaug;
     const int M = c->cfg.M, q = c->cfg.q, nat = 4 * q;
     cudaError_t e;
+    // S_s = [T_E | t_F]^T [T_E | t_F] does not depend on the TRSM: it runs on a side stream beside
+    // it and fills the TRSM's last partial wave (serialised when per-class timing is on)
+    const int Kt = (int)(ld - M);
+    const int64_t s0 = c->cfg.s_begin;
+    const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
+    GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
+                ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 1 /* lower tiles only */};
+    const bool side = !c->timing && c->schur_side;
+    cudaStream_t sst = st;
+    if (side) {
+        if ((e = c->ensure_streams(1)) != cudaSuccess) return e;
+        sst = c->gstreams[0];
+        cudaEventRecord(c->ev_fork, st);
+        cudaStreamWaitEvent(sst, c->ev_fork, 0);
+        if ((e = gemm_launch(true, false, gs, sst, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
+    }
     // W_s^T = R11^{-T} A^T: one fused left-looking TRSM launch (in place on At)
     {
         CUtensorMap tmR, tmA;
@@ -352,16 +368,14 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    const int64_t s0 = c->cfg.s_begin;
-    const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
     // P_s = W_s [R12 | y]   (4q x kaug)
     GemmArgs gp{nat, (int)kaug, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
                 Pbuf + s0 * pstride, c->sz.pbuf_ld, pstride, 1.0, 0.0, (int)S, 0};
     if ((e = gemm_launch(true, false, gp, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
-    // S_s = [T_E | t_F]^T [T_E | t_F]
-    const int Kt = (int)(ld - M);
-    GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
-                ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 1 /* lower tiles only */};
+    if (side) {
+        cudaEventRecord(c->ev_join[0], sst);
+        return cudaStreamWaitEvent(st, c->ev_join[0], 0);
+    }
     return gemm_launch(true, false, gs, st, c, ELMDDM_K_GEMM_SCHUR);
 }
 
