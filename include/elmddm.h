@@ -120,12 +120,14 @@ elmddm_status elmddm_interface_points(const elmddm_ctx* ctx, double* xy_host);
 int64_t elmddm_band_index(const elmddm_ctx* ctx, int64_t i, int64_t j);
 /* Host export of the factorisation plan (each pointer may be NULL): newidx[G] = factorisation-
  * order index of every interface unknown; tile_map[chol_blocks^2] = tile id of (I, J), I >= J,
- * or -1; tasks[chol_tasks][2] = (I, J) of every tile task in the kernel's list order.          */
+ * or -1; tasks[chol_tasks][4] = (I, J, kind, updates) of every task in the kernel's list order:
+ * kind 0 a whole tile task, 1 the pre-aggregation of a split tile task (the updates from columns
+ * below J's dissection node, summed into the tile in place), 2 the rest of a split task.      */
 elmddm_status elmddm_chol_plan(const elmddm_ctx* ctx, int32_t* newidx, int32_t* tile_map, int32_t* tasks);
 /* Host-only planning query (no device, no context): the interface factorisation plan of a P x P
  * grid with q points per face, ordering 0 strip / 1 nested dissection (reading R25), task list
  * scheduled for `workers` CTAs (0: column order).  stats[6] = {n, nblk, ntiles, tile updates,
- * tasks, simulated makespan in ns}; newidx[G], tile_map[nblk*nblk], tasks[ntasks][2] as for
+ * tasks, simulated makespan in ns}; newidx[G], tile_map[nblk*nblk], tasks[ntasks][4] as for
  * elmddm_chol_plan (each may be NULL; size them from a first call with NULL arrays).
  * EINVAL for P outside [2, 1024], q outside [1, 4096], another ordering or stats == NULL.     */
 elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t workers, int64_t* stats,

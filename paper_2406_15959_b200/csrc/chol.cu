@@ -312,7 +312,8 @@ struct CholArgs {
     int* flags;            // [ntiles] per-tile completion (epoch)
     int* colcnt;           // [nblk] finished tiles of column J, summed over factorisations
     const int* ntc;        // [nblk] tiles of column J
-    int epoch;
+    int epoch;             // tile flags: 2 epoch when L(I,J) is final, 2 epoch - 1 when a split
+                           // task's pre-aggregation is in the tile; cready and colcnt count epochs
     ElmStatus* status;
     int* next;             // non-null: tasks dealt dynamically in list order (zeroed counter)
     // multi-rank factorisation (nrep > 1, dynamic dealing through the shared counter `next`):
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
     }
     __syncthreads();
     const bool dist = a.nrep > 1;
+    const int fin_ep = 2 * a.epoch, pre_ep = fin_ep - 1;
     const int my = dist ? a.rep_base + (int)blockIdx.x / a.ctas_per_rep : 0;
     double* const Mb = dist ? a.reps[my].Mb : a.Mb;
     double* const Ybuf = dist ? a.reps[my].Ybuf : a.Ybuf;
@@ -378,8 +380,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
             if (k < known) return;
         }
-        wait_flag(flags + e.x, a.epoch, a.status, k, dist);
-        wait_flag(flags + e.y, a.epoch, a.status, k, dist);
+        wait_flag(flags + e.x, fin_ep, a.status, k, dist);
+        wait_flag(flags + e.y, fin_ep, a.status, k, dist);
     };
     // static dealing: CTAs [0, crit_ctas) take the critical list round-robin, the others the
     // rest; dynamic dealing (a.next): every CTA takes the next task of the (list-scheduled) order
@@ -400,7 +402,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         const int I = td.I, J = td.J;
         // the diagonal task applies its last update column klast itself: it solves for
         // L(J, klast) from the published C(J, klast) (one flag hop less on the critical path)
-        const bool dsub = I == J && td.klast >= 0;
+        const bool pre = td.kind == 1;
+        const bool dsub = !pre && I == J && td.klast >= 0;
         const int kb = td.kbeg, ke = dsub ? td.kend - 1 : td.kend;
         const int nch = 2 * (ke - kb);
 #ifdef ELM_CHOL_PROF
@@ -421,6 +424,10 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             bulk_load(st + HALF, tileptr(ke4.y) + h * HALF, HALF_BYTES, b);
         };
         double acc[4][2][2];  // holds -C while the updates are added
+        if (td.kind == 2) {   // the tile holds M minus the pre-aggregated updates once flagged
+            if (tid == 0) wait_flag(flags + td.tid, pre_ep, a.status, J, dist);
+            __syncthreads();
+        }
         {
             const double* Ct = tileptr(td.tid);
             FOR_FRAG acc[mt][nt][e] = -__ldcg(Ct + frag_r(mt) + frag_c(nt, e) * LP);
@@ -454,7 +461,15 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         const uint64_t pte = globaltimer();
 #endif
         double* dst = tileptr(td.tid);
-        if (I == J) {
+        if (pre) {
+            // partial sum C = M - sum_{k in pre list} L(I,k) L(J,k)^T back into the tile
+            FOR_FRAG dst[frag_r(mt) + frag_c(nt, e) * LP] = -acc[mt][nt][e];
+            if (dist) {
+                __threadfence_block();
+                __syncthreads();
+                push(0, (int64_t)td.tid * TILE);
+            }
+        } else if (I == J) {
 #ifdef ELM_CHOL_PROF
             uint64_t dts[8] = {globaltimer(), 0, 0, 0, 0, 0, 0, 0};
 #define DSTAMP(k) dts[k] = globaltimer()
@@ -467,7 +482,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 ++epi_uses;
                 if (tid == 0) {
                     wait_flag(cready + J, a.epoch, a.status, J, dist);
-                    wait_flag(flags + a.diag_tid[td.klast], a.epoch, a.status, td.klast, dist);
+                    wait_flag(flags + a.diag_tid[td.klast], fin_ep, a.status, td.klast, dist);
                     fence_proxy_async();
                     mbar_expect(eb, 3 * TILE * 8);
                     bulk_load(As, Cbuf + (int64_t)J * TILE, TILE * 8, eb);
@@ -538,7 +553,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #ifdef ELM_CHOL_PROF
                 const uint64_t pw = globaltimer();
 #endif
-                wait_flag(flags + a.diag_tid[J], a.epoch, a.status, J, dist);
+                wait_flag(flags + a.diag_tid[J], fin_ep, a.status, J, dist);
 #ifdef ELM_CHOL_PROF
                 pf_flag += globaltimer() - pw;
 #endif
@@ -558,18 +573,19 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 push(0, (int64_t)td.tid * TILE);
             }
         }
+        const int fval = pre ? pre_ep : fin_ep;
         if (dist) {
             __threadfence_system();
             __syncthreads();
             if (tid == 0)
-                for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].flags + td.tid, a.epoch);
+                for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].flags + td.tid, fval);
         } else {
             __threadfence();
             __syncthreads();
         }
         if (tid == 0 && !dist) {
-            st_release(flags + td.tid, a.epoch);
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.colcnt + J) : "memory");
+            st_release(flags + td.tid, fval);
+            if (!pre) asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.colcnt + J) : "memory");
 #ifdef ELM_CHOL_PROF
             if (t < 400000) {
                 unsigned long long* r = g_chol_prof + 6 * (size_t)t;
@@ -804,7 +820,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
                 cudaSuccess)
                 return e;
         }
-        k_drain<<<(unsigned)c->nsm, 256, 0, st>>>(mine.flags, pl.ntiles, epoch, c->d_status);
+        k_drain<<<(unsigned)c->nsm, 256, 0, st>>>(mine.flags, pl.ntiles, 2 * epoch, c->d_status);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         Mband = mine.Mb;  // the triangular solves read this rank's replica
     } else {

@@ -188,13 +188,14 @@ elmddm_status build_tables(elmddm_ctx* c) {
         }
     }
     const int mode = c->cfg.interface_mode;
+    const int split = chol_split_min();
     if (mode == 3) {
-        build_chol_plan(P, q, F, fpairs, 1, c->crit_band, c->plan);
+        build_chol_plan(P, q, F, fpairs, 1, c->crit_band, c->plan, split);
     } else {
-        build_chol_plan(P, q, F, fpairs, 0, c->crit_band, c->plan);
+        build_chol_plan(P, q, F, fpairs, 0, c->crit_band, c->plan, split);
         if (mode == 0 && P >= 3) {
             CholPlan nd;
-            build_chol_plan(P, q, F, fpairs, 1, c->crit_band, nd);
+            build_chol_plan(P, q, F, fpairs, 1, c->crit_band, nd, split);
             if (nd.nupd < c->plan.nupd) c->plan = std::move(nd);
         }
     }
@@ -416,11 +417,7 @@ elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* newidx, int32_t* ti
         for (int64_t f = 0; f < c->faces; ++f)
             for (int k = 0; k < q; ++k) newidx[f * q + k] = pl.fbase[f] + k;
     if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
-    if (tasks)
-        for (size_t t = 0; t < pl.tasks.size(); ++t) {
-            tasks[2 * t] = pl.tasks[t].I;
-            tasks[2 * t + 1] = pl.tasks[t].J;
-        }
+    if (tasks) export_tasks(pl, tasks);
     return ELMDDM_OK;
 }
 
@@ -431,7 +428,7 @@ elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t 
     interface_face_pairs(P, fp);
     const int F = 2 * P * (P - 1);
     CholPlan pl;
-    build_chol_plan(P, q, F, fp, ordering, 3, pl);
+    build_chol_plan(P, q, F, fp, ordering, 3, pl, chol_split_min());
     const double sim = workers > 0 ? schedule_chol_tasks(pl, workers) : 0.0;
     stats[0] = pl.n;
     stats[1] = pl.nblk;
@@ -443,11 +440,7 @@ elmddm_status elmddm_plan_query(int32_t P, int32_t q, int32_t ordering, int32_t 
         for (int f = 0; f < F; ++f)
             for (int k = 0; k < q; ++k) newidx[(int64_t)f * q + k] = pl.fbase[f] + k;
     if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
-    if (tasks)
-        for (size_t t = 0; t < pl.tasks.size(); ++t) {
-            tasks[2 * t] = pl.tasks[t].I;
-            tasks[2 * t + 1] = pl.tasks[t].J;
-        }
+    if (tasks) export_tasks(pl, tasks);
     return ELMDDM_OK;
 }
 

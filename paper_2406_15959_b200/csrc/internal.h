@@ -39,7 +39,9 @@ struct TaskDesc {
     int kbeg, kend;  // its update list klist[kbeg, kend)
     int klast;       // diagonal tasks: the last update column (applied by the task itself), or -1
     int pub;         // publish C(I, J) for the diagonal task of row I (J == klast(I))
-    int pad_;
+    int kind;        // 0 whole task; 1 pre-aggregation: the updates from columns below J's
+                     // dissection node, summed into the tile of M in place (flag 2 epoch - 1);
+                     // 2 the rest of a split task (waits for its pre-aggregation first)
 };
 
 // ordering and symbolic factorisation of the interface Schur matrix at 64-tile granularity
@@ -71,13 +73,17 @@ struct CholPlan {
     int64_t nupd = 0;                 // tile updates (work = 2 * 64^3 * nupd)
     std::vector<int> fbase, pad, tile_map, diag_tid, ntc, fwd_ptr, bwd_ptr;
     std::vector<int> blk_depth;       // nested-dissection depth of each tile column (0 = top separator)
+    std::vector<int> blk_node0;       // first tile column of the dissection node of each column
+    int npre = 0;                     // pre-aggregation tasks (kind 1)
     std::vector<TaskDesc> tasks;      // critical band first, then the rest; each column by column
     std::vector<int4> klist;
     std::vector<int2> fwd, bwd;
 };
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
-                        int crit_band, CholPlan& pl);
+                        int crit_band, CholPlan& pl, int split_min = 0);
 double schedule_chol_tasks(CholPlan& pl, int workers);
+int chol_split_min();
+void export_tasks(const CholPlan& pl, int32_t* tasks);
 void interface_face_pairs(int P, std::vector<std::pair<int, int>>& out);
 double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers);
 

@@ -15,6 +15,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <queue>
@@ -128,7 +130,7 @@ void interface_face_pairs(int P, std::vector<std::pair<int, int>>& out) {
 // Build the plan for `ordering` (0 strip, 1 nested dissection).  face_pairs: (b, c), b >= c,
 // structurally nonzero q x q face blocks of M.  Returns the work (tile updates).
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
-                        int crit_band, CholPlan& pl) {
+                        int crit_band, CholPlan& pl, int split_min) {
     const int T = ELM_NB;
     pl.ordering = ordering;
     // 1. face bases in the new order (+ padding to tile boundaries between ND nodes)
@@ -157,9 +159,11 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
     pl.nblk = (int)(pl.n / T);
     // dissection depth of every tile column (strip order: all 0)
     pl.blk_depth.assign(pl.nblk, 0);
+    pl.blk_node0.assign(pl.nblk, 0);
     for (int J = 0, nd = 0; J < pl.nblk; ++J) {
         while (nd + 1 < (int)node_end.size() && (int64_t)J * T >= node_end[nd]) ++nd;
         pl.blk_depth[J] = ndepth[nd];
+        pl.blk_node0[J] = nd > 0 ? (int)(node_end[nd - 1] / T) : 0;
     }
     used.assign(pl.n, 0);
     for (int f = 0; f < F; ++f)
@@ -210,6 +214,7 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
         if (rows[I].size() > 1) klast[I] = rows[I][rows[I].size() - 2];
     std::vector<TaskDesc> crit, reg;
     pl.klist.clear();
+    pl.npre = 0;
     pl.ntc.assign(nb, 0);
     int64_t nupd = 0;
     for (int J = 0; J < nb; ++J) {
@@ -240,8 +245,29 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
             nupd += td.kend - td.kbeg;
             td.klast = (I == J && td.kend > td.kbeg) ? pl.klist[td.kend - 1].z : -1;
             td.pub = (I > J && klast[I] == J) ? 1 : 0;  // C(I, J) feeds the diagonal task of row I
+            td.kind = 0;
             ++pl.ntc[J];
-            (I - J <= crit_band ? crit : reg).push_back(td);
+            auto& lst = I - J <= crit_band ? crit : reg;
+            // split: the updates from columns below J's dissection node are final long before
+            // the node itself is factored; summed by a task of their own (in place into the tile
+            // of M), they no longer hold a CTA that waits for the node's columns
+            if (split_min > 0) {
+                int npre = 0;
+                while (td.kbeg + npre < td.kend && pl.klist[td.kbeg + npre].z < pl.blk_node0[J]) ++npre;
+                if (I == J && td.kend > td.kbeg) npre = std::min(npre, td.kend - td.kbeg - 1);  // klast stays
+                if (npre >= split_min) {
+                    TaskDesc pre = td;
+                    pre.kend = td.kbeg + npre;
+                    pre.klast = -1;
+                    pre.pub = 0;
+                    pre.kind = 1;
+                    lst.push_back(pre);
+                    td.kbeg += npre;
+                    td.kind = 2;
+                    ++pl.npre;
+                }
+            }
+            lst.push_back(td);
         }
     }
     pl.ncrit = (int)crit.size();
@@ -278,18 +304,39 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
 // the tasks by their finish time with unlimited CTAs (as-soon-as-possible streaming schedule),
 // and keeps that order if the replay beats the column order.
 namespace {
-constexpr double UPD = 3.5, EPI_OFF = 10.0, EPI_DIAG = 45.0;
+// model constants (us); ELMDDM_CHOL_MODEL="upd,epi_off,epi_diag,epi_pre" overrides them
+double UPD = 3.5, EPI_OFF = 10.0, EPI_DIAG = 45.0, EPI_PRE = 3.0;
+void model_from_env() {
+    if (const char* env = getenv("ELMDDM_CHOL_MODEL")) {
+        double v[4] = {UPD, EPI_OFF, EPI_DIAG, EPI_PRE};
+        if (sscanf(env, "%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3]) >= 1) {
+            UPD = v[0];
+            EPI_OFF = v[1];
+            EPI_DIAG = v[2];
+            EPI_PRE = v[3];
+        }
+    }
+}
+
+// task index of every tile's final task (tix) and of its pre-aggregation task (ptix, -1: none)
+void task_index(const CholPlan& pl, std::vector<int>& tix, std::vector<int>& ptix) {
+    tix.assign(pl.ntiles, -1);
+    ptix.assign(pl.ntiles, -1);
+    for (int t = 0; t < (int)pl.tasks.size(); ++t) (pl.tasks[t].kind == 1 ? ptix : tix)[pl.tasks[t].tid] = t;
+}
 
 // finish time of task t started at time s, given the finish times of the tasks before it
-double task_finish(const CholPlan& pl, const std::vector<int>& tix, const std::vector<double>& fin, int t, double s) {
+double task_finish(const CholPlan& pl, const std::vector<int>& tix, const std::vector<int>& ptix,
+                   const std::vector<double>& fin, int t, double s) {
     const TaskDesc& td = pl.tasks[t];
-    double x = s;
-    const bool dsub = td.I == td.J && td.klast >= 0;
+    double x = td.kind == 2 ? std::max(s, fin[ptix[td.tid]]) : s;
+    const bool dsub = td.kind != 1 && td.I == td.J && td.klast >= 0;
     const int ke = dsub ? td.kend - 1 : td.kend;
     for (int e = td.kbeg; e < ke; ++e) {
         const int4 k4 = pl.klist[e];
         x = std::max(x, std::max(fin[tix[k4.x]], fin[tix[k4.y]])) + UPD;
     }
+    if (td.kind == 1) return x + EPI_PRE;
     if (td.I > td.J) return std::max(x, fin[tix[pl.diag_tid[td.J]]]) + EPI_OFF;
     if (dsub) {  // L(J, klast) from the published C(J, klast): needs that tile's k-sum and L(klast, klast)
         const int4 k4 = pl.klist[td.kend - 1];
@@ -302,8 +349,8 @@ double task_finish(const CholPlan& pl, const std::vector<int>& tix, const std::v
 // replay `order` (a permutation of pl.tasks, topological) with dynamic dealing on `workers` CTAs
 double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers) {
     const int nt = (int)pl.tasks.size();
-    std::vector<int> tix(pl.ntiles, -1);
-    for (int t = 0; t < nt; ++t) tix[pl.tasks[t].tid] = t;
+    std::vector<int> tix, ptix;
+    task_index(pl, tix, ptix);
     std::vector<double> fin(nt, 1e300);
     std::priority_queue<double, std::vector<double>, std::greater<double>> freeat;
     for (int w = 0; w < workers; ++w) freeat.push(0.0);
@@ -311,7 +358,7 @@ double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers)
     for (int t : order) {
         const double s = freeat.top();
         freeat.pop();
-        fin[t] = task_finish(pl, tix, fin, t, s);
+        fin[t] = task_finish(pl, tix, ptix, fin, t, s);
         freeat.push(fin[t]);
         span = std::max(span, fin[t]);
     }
@@ -321,9 +368,11 @@ double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers)
 double schedule_chol_tasks(CholPlan& pl, int workers) {
     const int nt = (int)pl.tasks.size();
     if (nt == 0 || workers < 1) return 0.0;
-    std::vector<int> tix(pl.ntiles, -1);
-    for (int t = 0; t < nt; ++t) tix[pl.tasks[t].tid] = t;
-    // column order (a topological order: off-diagonal tiles of column J after (J, J))
+    model_from_env();
+    std::vector<int> tix, ptix;
+    task_index(pl, tix, ptix);
+    // column order (a topological order: off-diagonal tiles of column J after (J, J), a tile's
+    // pre-aggregation before the rest of it)
     std::vector<int> col(nt);
     for (int t = 0; t < nt; ++t) col[t] = t;
     std::stable_sort(col.begin(), col.end(), [&](int x, int y) {
@@ -332,7 +381,7 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
         return (a.I == a.J) > (b.I == b.J);
     });
     // dependency graph: the tiles of the k-list, the diagonal tile of column J (off-diagonal
-    // tiles) or of column klast (diagonal tiles)
+    // tiles) or of column klast (diagonal tiles), the tile's own pre-aggregation
     auto for_deps = [&](int t, auto&& f) {
         const TaskDesc& td = pl.tasks[t];
         for (int e = td.kbeg; e < td.kend; ++e) {
@@ -340,6 +389,8 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
             f(tix[k4.x]);
             if (k4.y != k4.x) f(tix[k4.y]);
         }
+        if (td.kind == 1) return;
+        if (td.kind == 2) f(ptix[td.tid]);
         if (td.I > td.J) f(tix[pl.diag_tid[td.J]]);
         else if (td.klast >= 0) f(tix[pl.diag_tid[td.klast]]);
     };
@@ -351,7 +402,7 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
     std::vector<double> cost(nt), blev(nt, 0.0);
     for (int t = 0; t < nt; ++t) {
         const TaskDesc& td = pl.tasks[t];
-        cost[t] = UPD * (td.kend - td.kbeg) + (td.I == td.J ? EPI_DIAG : EPI_OFF);
+        cost[t] = UPD * (td.kend - td.kbeg) + (td.kind == 1 ? EPI_PRE : (td.I == td.J ? EPI_DIAG : EPI_OFF));
     }
     for (int i = nt - 1; i >= 0; --i) {  // bottom levels, reverse topological order
         const int t = col[i];
@@ -390,13 +441,13 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
             t = pending.top().second;
             pending.pop();
         }
-        fin[t] = task_finish(pl, tix, fin, t, s);
+        fin[t] = task_finish(pl, tix, ptix, fin, t, s);
         span = std::max(span, fin[t]);
         freeat.push(fin[t]);
         ord.push_back(t);
         for (int j = sptr[t]; j < sptr[t + 1]; ++j) {
             const int u = succ[j];
-            if (--left[u] == 0) pending.push({std::max(0.0, task_finish(pl, tix, fin, u, 0.0) - cost[u]), u});
+            if (--left[u] == 0) pending.push({std::max(0.0, task_finish(pl, tix, ptix, fin, u, 0.0) - cost[u]), u});
         }
     }
     const double t_col = chol_eval(pl, col, workers);
@@ -406,4 +457,23 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
     pl.tasks.swap(nl);
     pl.ncrit = 0;
     return std::min(span, t_col);
+}
+
+// minimum pre-aggregation length of a split task (ELMDDM_CHOL_SPLIT; 0 = no split).  Measured
+// (chol kernel, configs 3 / 4): no split 17.64 / 93.15 ms, 4: 17.60 / 91.62, 16: 17.34 / 91.07.
+int chol_split_min() {
+    int v = 16;
+    if (const char* env = getenv("ELMDDM_CHOL_SPLIT")) v = std::max(0, atoi(env));
+    return v;
+}
+
+// tasks[ntasks][4] = (I, J, kind, updates) in list order
+void export_tasks(const CholPlan& pl, int32_t* tasks) {
+    for (size_t t = 0; t < pl.tasks.size(); ++t) {
+        const TaskDesc& td = pl.tasks[t];
+        tasks[4 * t] = td.I;
+        tasks[4 * t + 1] = td.J;
+        tasks[4 * t + 2] = td.kind;
+        tasks[4 * t + 3] = td.kend - td.kbeg;
+    }
 }

@@ -205,16 +205,17 @@ class Context:
         return nd.value
 
     def chol_plan(self):
-        """(newidx[G], tile_map[chol_blocks, chol_blocks], tasks[chol_tasks, 2]) of the interface
+        """(newidx[G], tile_map[chol_blocks, chol_blocks], tasks[chol_tasks, 4]) of the interface
         factorisation (host arrays): the factorisation-order index of every interface unknown,
-        the tile id of every tile (I, J) of L (-1 outside its structure) and the task list."""
+        the tile id of every tile (I, J) of L (-1 outside its structure) and the task list
+        (I, J, kind, updates; kind 1 = pre-aggregation of a split task, 2 = its rest)."""
         import numpy as np
 
         z = self.sizes
         nb = z["chol_blocks"]
         newidx = np.zeros(max(z["G"], 1), dtype=np.int32)
         tmap = np.zeros(nb * nb, dtype=np.int32)
-        tasks = np.zeros((z["chol_tasks"], 2), dtype=np.int32)
+        tasks = np.zeros((z["chol_tasks"], 4), dtype=np.int32)
         self._check(self.L.elmddm_chol_plan(self.h, newidx.ctypes.data_as(C.c_void_p), tmap.ctypes.data_as(C.c_void_p),
                                             tasks.ctypes.data_as(C.c_void_p)), "chol_plan")
         return newidx[: z["G"]], tmap.reshape(nb, nb), tasks
@@ -399,7 +400,7 @@ def plan_query(P: int, q: int, ordering: int = 1, workers: int = 0, arrays: bool
         nb = out["nblk"]
         newidx = np.zeros(G, dtype=np.int32)
         tmap = np.zeros(nb * nb, dtype=np.int32)
-        tasks = np.zeros((out["ntasks"], 2), dtype=np.int32)
+        tasks = np.zeros((out["ntasks"], 4), dtype=np.int32)
         rc = L.elmddm_plan_query(P, q, ordering, workers, st.ctypes.data_as(vp), newidx.ctypes.data_as(vp),
                                  tmap.ctypes.data_as(vp), tasks.ctypes.data_as(vp))
         if rc != 0:

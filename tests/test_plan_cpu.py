@@ -76,26 +76,45 @@ def test_plan_tiles_cover_scalar_fill(P, q, ordering):
     assert sorted(ids.tolist()) == list(range(pl["ntiles"]))
 
 
+@pytest.mark.parametrize("split", ["0", "4", "1"])
 @pytest.mark.parametrize("P,q", [(3, 5), (4, 24), (6, 10), (8, 60)])
-def test_plan_task_list_is_topological_and_counts_updates(P, q):
+def test_plan_task_list_is_topological_and_counts_updates(P, q, split, monkeypatch):
     """The list-scheduled order (dynamic dealing): every task comes after the tiles its k-list
     and its epilogue wait for -- the condition under which the persistent kernel's smallest
     unfinished task can always run -- and the update count is the number of (I, J, k) with
-    L(I,k), L(J,k) present, k < J."""
+    L(I,k), L(J,k) present, k < J.  Split tasks (ELMDDM_CHOL_SPLIT): the pre-aggregation of
+    (I, J) takes the first updates of the k-list (columns below J's dissection node, never the
+    diagonal task's last one), waits only for their tiles and comes before the rest of (I, J)."""
+    monkeypatch.setenv("ELMDDM_CHOL_SPLIT", split)
     pl = E.plan_query(P, q, 1, 296)
     have = pl["tile_map"] >= 0
-    pos = {(int(I), int(J)): t for t, (I, J) in enumerate(pl["tasks"])}
-    assert len(pos) == pl["ntasks"] == pl["ntiles"]
+    fin, pre = {}, {}
+    for t, (I, J, kind, nk) in enumerate(pl["tasks"]):
+        (pre if kind == 1 else fin)[(int(I), int(J))] = (t, int(kind), int(nk))
+    assert len(fin) == pl["ntiles"] and len(fin) + len(pre) == pl["ntasks"]
+    if split == "0":
+        assert not pre
+    elif P >= 4:
+        assert pre
     nupd = 0
-    for (I, J), t in pos.items():
+    for (I, J), (t, kind, nk) in fin.items():
         ks = np.nonzero(have[I, :J] & have[J, :J])[0]
         nupd += len(ks)
-        for k in ks:
-            assert pos[(I, int(k))] < t and pos[(J, int(k))] < t
+        npre = 0
+        if kind == 2:
+            tp, _, npre = pre[(I, J)]
+            assert tp < t and npre >= int(split) and npre + nk == len(ks)
+            for k in ks[:npre]:
+                assert fin[(I, int(k))][0] < tp and fin[(J, int(k))][0] < tp
+        else:
+            assert kind == 0 and nk == len(ks) and (I, J) not in pre
+        for k in ks[npre:]:
+            assert fin[(I, int(k))][0] < t and fin[(J, int(k))][0] < t
         if I > J:
-            assert pos[(J, J)] < t
+            assert fin[(J, J)][0] < t
         elif len(ks):
-            assert pos[(int(ks[-1]), int(ks[-1]))] < t
+            assert npre < len(ks)
+            assert fin[(int(ks[-1]), int(ks[-1]))][0] < t
     assert nupd == pl["nupd"]
 
 
@@ -106,7 +125,7 @@ def test_static_lists_are_column_ordered(P, q):
     task first -- every dependency of a task lies in an earlier column or is its own column's
     diagonal, the progress argument of the static mode."""
     pl = E.plan_query(P, q, 1, 0)
-    tasks = [(int(I), int(J)) for I, J in pl["tasks"]]
+    tasks = [(int(I), int(J)) for I, J, _, _ in pl["tasks"]]
     crit = [t for t in tasks if t[0] - t[1] <= 3]
     rest = [t for t in tasks if t[0] - t[1] > 3]
     assert tasks == crit + rest
