@@ -46,6 +46,8 @@ def parse():
                     help="interface factorisation order: 0 auto, 2 strip (envelope), 3 nested dissection")
     ap.add_argument("--problem", type=int, default=None, help="operator override, e.g. 6 = variable coefficient")
     ap.add_argument("--alpha", type=float, default=16.0, help="eqn:grf alpha of problem 6")
+    ap.add_argument("--interface-solver", default=None, choices=["cholesky", "cg"],
+                    help="interface solve: direct tile Cholesky (default) or the paper's CG (P:412)")
     ap.add_argument("--phases", action="store_true", help="print per-phase breakdown to stderr")
     return ap.parse_args()
 
@@ -53,6 +55,8 @@ def parse():
 def bench_config(args) -> dict:
     """BASELINE config args.config; --problem / --alpha swap in another operator (NEXT-4)."""
     over = {"interface_mode": getattr(args, "interface_mode", 0)}
+    if getattr(args, "interface_solver", None):
+        over["interface_solver"] = args.interface_solver
     if getattr(args, "problem", None) is not None:
         over["problem"] = args.problem
         over["alpha"] = args.alpha
@@ -74,7 +78,7 @@ def workload_desc(k: int, c: dict | None = None) -> str:
                f"grf alpha={c.get('alpha', 16.0)} (eqn:varpoisson)")
     else:
         pde = f"2D Poisson -Lap u=f on (0,1)^2, u={names.get(c['problem'])}"
-    return (f"cfg{k}: {pde}, {c['P']}x{c['P']} subdomains, "
+    return (f"{c.get('name', f'cfg{k}')}: {pde}, {c['P']}x{c['P']} subdomains, "
             f"M={c['M']} tanh neurons/subdomain, {c['p']}x{c['p']} interior + {c['q']}/edge points "
             f"(local LS {m}x{c['M']}), seed {c['seed']}, eval 101x101")
 
@@ -433,6 +437,12 @@ def main():
                 "gpu_launches": launches, "launches_per_step": launches / args.steps, "clocks": clocks,
                 "phases_ms": phases, "kernel_class_ms": kms,
                 "algorithmic": {k: v for k, v in work.items()}}
+        if c.get("interface_solver") == "cg" and getattr(ctx, "cg_info", None):
+            line["interface_cg"] = {"iterations": ctx.cg_info[0], "rel_residual": ctx.cg_info[1], "tol": prob.cg_tol}
+        if args.config in WL.PAPER_TABLE2:
+            e_p, t_p = WL.PAPER_TABLE2[args.config]
+            line["paper_table2"] = {"rel_l2": e_p, "wall_clock_s": t_p,
+                                    "note": "the paper's CPU-cluster numbers (P:597-606), other hardware: context"}
         print(json.dumps(line), flush=True)
         if args.phases:
             print(json.dumps({"phases_ms": phases, "kernel_class_ms": kms}, indent=1), file=sys.stderr)

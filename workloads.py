@@ -17,7 +17,18 @@ CONFIGS = [
     dict(name="cfg2", P=8, M=1000, p=40, q=60, problem=1, seed=2),
     dict(name="cfg3", P=16, M=1600, p=50, q=80, problem=2, seed=3),
     dict(name="cfg4", P=32, M=1024, p=40, q=64, problem=3, seed=4),
+    # the paper's own Poisson workload (Table 2; NEXT-2): u = sin(2 pi x) e^y, n = 2^16
+    # neurons in total (M = n / N per subdomain), (2^8 + 1)^2 = 66,049 training points in total
+    # (P:434-437).  Per subdomain p^2 + 4q = (256/P + 1)^2 points, the paper's count, on the
+    # face-point layout of reading R1 (q points per edge, no shared cross points).
+    # Only N = 8 x 8 and 16 x 16 fit the panel kernels' ld <= 3008.  Study configs, not parity
+    # cases: the near-square, numerically rank-deficient local problems defeat the unpivoted-QR
+    # elimination (oracle and GPU alike; DESIGN.md §10 NEXT-2).
+    dict(name="t2-8x8", P=8, M=1024, p=31, q=32, problem=4, seed=5),
+    dict(name="t2-16x16", P=16, M=256, p=15, q=16, problem=4, seed=6),
 ]
+# the paper's Table 2 (CPU cluster, context only): relative L2 error, wall-clock s
+PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43)}
 
 # the bench workload: config 3 (16 x 16 subdomains, 2820 x 1600 local LS, ~9 GB of local
 # matrices) -- the largest local least-squares problem of BASELINE.json that fits one B200.
