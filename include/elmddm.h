@@ -46,7 +46,14 @@ typedef enum {
     ELMDDM_EINVAL = 1,   /* bad argument / configuration (nothing was enqueued) */
     ELMDDM_ENUMERIC = 2, /* non-positive pivot or non-finite value detected on the device */
     ELMDDM_ECUDA = 3,    /* CUDA runtime error (text in elmddm_last_error) */
-    ELMDDM_ENOMEM = 4    /* internal table allocation failed */
+    ELMDDM_ENOMEM = 4,   /* internal table allocation failed */
+    ELMDDM_WRANK = 100   /* WARNING, not an error (SPEC factorize_ls: "warns (not errors) when
+                            sigma_min/sigma_max < 1e-14"): some subdomain's R11 has
+                            min|R11_ii| < 1e-14 max|R11_ii| (which implies sigma_min/sigma_max <
+                            1e-14 for K^s); every output is still computed.  Reported once by the
+                            next elmddm_sync / elmddm_interface_factor_solve, subdomain in
+                            elmddm_last_error.  Expected for the BASELINE configs >= 1: ELM
+                            collocation matrices are numerically rank deficient (reading R11). */
 } elmddm_status;
 
 typedef struct elmddm_ctx elmddm_ctx;
@@ -185,7 +192,7 @@ elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, con
  * kernel over a list-scheduled task order) and u = M^{-1} g into uG[G_pad] (strip order).  On
  * return the tiles of Mband hold L (diagonal tiles: L(J,J), lower triangular).  g is not
  * modified.  Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot (or a
- * dependency wait exceeding 10 s).                                                             */
+ * dependency wait exceeding 10 s), else the pending ELMDDM_WRANK warning if any.                                                             */
 elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
                                             double* work, void* stream);
 /* The paper's interface solver: unpreconditioned conjugate gradients on

@@ -37,7 +37,14 @@ class Sizes(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
-STATUS = {0: "ELMDDM_OK", 1: "ELMDDM_EINVAL", 2: "ELMDDM_ENUMERIC", 3: "ELMDDM_ECUDA", 4: "ELMDDM_ENOMEM"}
+STATUS = {0: "ELMDDM_OK", 1: "ELMDDM_EINVAL", 2: "ELMDDM_ENUMERIC", 3: "ELMDDM_ECUDA", 4: "ELMDDM_ENOMEM",
+          100: "ELMDDM_WRANK"}
+WRANK = 100
+
+
+class RankWarning(UserWarning):
+    """ELMDDM_WRANK: a subdomain's K^s is numerically rank deficient (min |R11_ii| < 1e-14 max
+    |R11_ii|); the results are still computed (include/elmddm.h)."""
 
 # every exported entry point of include/elmddm.h
 EXPORTS = [

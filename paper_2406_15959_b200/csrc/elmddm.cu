@@ -695,7 +695,7 @@ elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {
     DeviceGuard dg(c->device);
     cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_sync");
-    ElmStatus h{0, 0};
+    ElmStatus h{0, 0, 0, 0};
     if ((e = cudaMemcpy(&h, c->d_status, sizeof(h), cudaMemcpyDeviceToHost)) != cudaSuccess)
         return cuda_fail(c, e, "elmddm_sync");
     if (h.code != 0) {
@@ -703,6 +703,12 @@ elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {
         c->err = h.info >= 0 ? "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info)
                              : "interface triangular solve: block " + std::to_string(-1 - h.info) + " never completed";
         return (elmddm_status)h.code;
+    }
+    if (h.wcode != 0) {  // a warning: reported once, results valid
+        cudaMemset(c->d_status, 0, sizeof(ElmStatus));
+        c->err = "numerically rank-deficient K^s: min |R11_ii| < 1e-14 max |R11_ii| in subdomain " +
+                 std::to_string(h.winfo) + " (and possibly others); results computed";
+        return (elmddm_status)h.wcode;
     }
     return ELMDDM_OK;
 }

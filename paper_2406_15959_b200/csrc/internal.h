@@ -20,8 +20,10 @@
 
 // Device status word: [0] error code (ELMDDM_ENUMERIC), [1] info (column / index).
 struct ElmStatus {
-    int code;
+    int code;   // first error (ELMDDM_ENUMERIC ...) and its info
     int info;
+    int wcode;  // first warning (ELMDDM_WRANK) and its info (global subdomain index)
+    int winfo;
 };
 
 // One contribution to an interface-matrix face block, see schur.cu.
@@ -275,5 +277,8 @@ cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double
 #ifdef __CUDACC__
 __device__ __forceinline__ void elm_set_status(ElmStatus* st, int code, int info) {
     if (atomicCAS(&st->code, 0, code) == 0) st->info = info;
+}
+__device__ __forceinline__ void elm_set_warning(ElmStatus* st, int code, int info) {
+    if (atomicCAS(&st->wcode, 0, code) == 0) st->winfo = info;
 }
 #endif

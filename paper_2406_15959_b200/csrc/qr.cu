@@ -2946,6 +2946,38 @@ bool elm_encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1
     return r == CUDA_SUCCESS;
 }
 
+// SPEC factorize_ls: "warns (not errors) when sigma_min/sigma_max < 1e-14".  |R11_ii| bound the
+// singular values of K^s from inside (sigma_min <= min |R11_ii|, max |R11_ii| <= sigma_max), so
+// min |R11_ii| < 1e-14 max |R11_ii| is a sufficient condition (no false warnings).  grid S.
+static __global__ void __launch_bounds__(256) k_rank_check(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
+                                                    int s_begin, ElmStatus* status) {
+    __shared__ double smx[8], smn[8];
+    const double* R = Kaug + (int64_t)blockIdx.x * ld * ncols;
+    double mx = 0.0, mn = INFINITY;
+    for (int i = threadIdx.x; i < M; i += 256) {
+        const double d = fabs(R[(int64_t)i * ld + i]);
+        mx = fmax(mx, d);
+        mn = fmin(mn, d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smx[threadIdx.x >> 5] = mx;
+        smn[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            mx = fmax(mx, smx[w]);
+            mn = fmin(mn, smn[w]);
+        }
+        if (!(mn > 1e-14 * mx)) elm_set_warning(status, ELMDDM_WRANK, s_begin + (int)blockIdx.x);
+    }
+}
+
 cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, double* work, cudaStream_t st) {
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols;
     const int M = c->cfg.M;
@@ -3088,6 +3120,12 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             cudaEventRecord(c->ev_join[g], streams[g]);
             cudaStreamWaitEvent(st, c->ev_join[g], 0);
         }
+    }
+    // rank warning (ELMDDM_WRANK): min |R11_ii| < 1e-14 max |R11_ii| in some subdomain
+    {
+        KTimer kt(c, ELMDDM_K_PANEL, st);
+        k_rank_check<<<(unsigned)S, 256, 0, st>>>(Kaug, ld, ncols, M, (int)c->cfg.s_begin, c->d_status);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

@@ -112,7 +112,12 @@ class Context:
             self.h = None
 
     def _check(self, rc, what):
-        if rc != 0:
+        if rc == _lib.WRANK:  # a warning: the call completed
+            import warnings
+
+            msg = self.L.elmddm_last_error(self.h)
+            warnings.warn(f"{what}: {msg.decode() if msg else ''}", _lib.RankWarning, stacklevel=3)
+        elif rc != 0:
             msg = self.L.elmddm_last_error(self.h)
             raise _lib.ElmddmError(f"{what}: {_lib.STATUS.get(rc, rc)}: {msg.decode() if msg else ''}")
 

@@ -27,6 +27,19 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_lib.EXPORTS) == syms
 
 
+def test_status_codes_match_the_header():
+    """The binding's status table is the header's enum (incl. the ELMDDM_WRANK warning, SURVEY
+    §8(b): rank deficiency is a warning, not an error)."""
+    from paper_2406_15959_b200 import _lib
+
+    src = open(os.path.join(ROOT, "include", "elmddm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    body = src[src.index("typedef enum"):src.index("} elmddm_status")]
+    enum = {int(v): k for k, v in re.findall(r"\b(ELMDDM_[A-Z]+)\s*=\s*(\d+)", body)}
+    assert enum == _lib.STATUS
+    assert enum[_lib.WRANK] == "ELMDDM_WRANK" and issubclass(_lib.RankWarning, UserWarning)
+
+
 def test_config_validation_is_synchronous_and_cpu_safe():
     """Invalid configurations are rejected with ELMDDM_EINVAL before any CUDA call."""
     from paper_2406_15959_b200 import _lib

@@ -296,6 +296,26 @@ def test_edge_configs_end_to_end(cfgkw):
         assert np.allclose(K @ cg, K @ ref, atol=1e-9 * np.abs(F).max())
 
 
+def test_rank_warning():
+    """ELMDDM_WRANK (SPEC factorize_ls: a warning, not an error): raised as
+    E.RankWarning when some subdomain has min |R11_ii| < 1e-14 max |R11_ii| -- config 1's K^s
+    (oracle QR: ratio 8.9e-18) -- and not for a small well-conditioned case (ratio 1.3e-3); the
+    solution is computed either way."""
+    import warnings
+
+    import paper_2406_15959_b200 as E
+
+    c = small(P=2, M=16, p=6, q=4)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error", E.RankWarning)
+        run_gpu(c)
+    c1 = WL.config(1)
+    xy = WL.eval_grid(21)
+    with pytest.warns(E.RankWarning, match="rank-deficient"):
+        _, _, u = run_gpu(c1, xy)
+    assert rel_l2(u.cpu().numpy(), WL.exact(c1["problem"], xy)) < 1e-6
+
+
 def test_homogeneous_problem_is_exactly_zero():
     c = small(P=3, M=24, p=7, q=6, problem=5)
     xy = WL.eval_grid(11)
