@@ -700,8 +700,12 @@ elmddm_status elmddm_sync(elmddm_ctx* c, void* stream) {
         return cuda_fail(c, e, "elmddm_sync");
     if (h.code != 0) {
         cudaMemset(c->d_status, 0, sizeof(ElmStatus));
-        c->err = h.info >= 0 ? "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info)
-                             : "interface triangular solve: block " + std::to_string(-1 - h.info) + " never completed";
+        if (h.info >= 0)
+            c->err = "non-positive pivot in the interface Cholesky at row " + std::to_string(h.info);
+        else if (h.info <= ELM_INFO_NONFINITE_QR)
+            c->err = "non-finite value in the QR of subdomain " + std::to_string(ELM_INFO_NONFINITE_QR - h.info);
+        else
+            c->err = "interface factorisation / solve: block " + std::to_string(-1 - h.info) + " never completed";
         return (elmddm_status)h.code;
     }
     if (h.wcode != 0) {  // a warning: reported once, results valid

@@ -19,6 +19,10 @@
 // so one bulk copy reproduces the conflict-free padded shared-memory layout of the DMMA kernels.
 
 // Device status word: [0] error code (ELMDDM_ENUMERIC), [1] info (column / index).
+// ElmStatus.info of ELMDDM_ENUMERIC: >= 0 interface Cholesky row of a non-positive pivot;
+// -1 - tag: a dependency wait that exceeded 10 s; <= ELM_INFO_NONFINITE_QR: non-finite R11 of
+// subdomain ELM_INFO_NONFINITE_QR - info
+constexpr int ELM_INFO_NONFINITE_QR = -(1 << 30);
 struct ElmStatus {
     int code;   // first error (ELMDDM_ENUMERIC ...) and its info
     int info;

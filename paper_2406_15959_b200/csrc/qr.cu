@@ -2948,16 +2948,25 @@ bool elm_encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1
 
 // SPEC factorize_ls: "warns (not errors) when sigma_min/sigma_max < 1e-14".  |R11_ii| bound the
 // singular values of K^s from inside (sigma_min <= min |R11_ii|, max |R11_ii| <= sigma_max), so
-// min |R11_ii| < 1e-14 max |R11_ii| is a sufficient condition (no false warnings).  grid S.
+// min |R11_ii| < 1e-14 max |R11_ii| is a sufficient condition (no false warnings).  A non-finite
+// diagonal (a NaN / Inf anywhere in K^s reaches it through the Householder norms) is an error
+// (numerical breakdown on non-finite values): ELMDDM_ENUMERIC, info
+// ELM_INFO_NONFINITE_QR - s.  grid S.
 static __global__ void __launch_bounds__(256) k_rank_check(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
                                                     int s_begin, ElmStatus* status) {
     __shared__ double smx[8], smn[8];
     const double* R = Kaug + (int64_t)blockIdx.x * ld * ncols;
     double mx = 0.0, mn = INFINITY;
+    bool bad = false;
     for (int i = threadIdx.x; i < M; i += 256) {
         const double d = fabs(R[(int64_t)i * ld + i]);
+        bad |= !isfinite(d);
         mx = fmax(mx, d);
         mn = fmin(mn, d);
+    }
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) elm_set_status(status, ELMDDM_ENUMERIC, ELM_INFO_NONFINITE_QR - (s_begin + (int)blockIdx.x));
+        return;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

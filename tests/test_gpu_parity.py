@@ -316,6 +316,23 @@ def test_rank_warning():
     assert rel_l2(u.cpu().numpy(), WL.exact(c1["problem"], xy)) < 1e-6
 
 
+def test_nonfinite_in_qr_is_an_error():
+    """non-finite values are a numerical breakdown (ELMDDM_ENUMERIC) naming the
+    subdomain; the status is reported once, then cleared."""
+    import paper_2406_15959_b200 as E
+
+    c = small(P=2, M=16, p=6, q=4)
+    ctx, buf = gpu_ctx(c)
+    ctx.init_hidden(buf["W"], buf["b"])
+    ctx.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"])
+    z = ctx.sizes
+    buf["Kaug"].view(-1)[1 * z["ld"] * z["ncols"] + 5] = float("nan")  # subdomain 1, K(5, 0)
+    ctx.local_factor(buf["Kaug"], buf["tau"], buf["work"])
+    with pytest.raises(E.ElmddmError, match="non-finite value in the QR of subdomain 1"):
+        ctx.sync()
+    ctx.sync()
+
+
 def test_homogeneous_problem_is_exactly_zero():
     c = small(P=3, M=24, p=7, q=6, problem=5)
     xy = WL.eval_grid(11)
