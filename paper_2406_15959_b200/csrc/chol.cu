@@ -91,6 +91,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
 __device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -120,7 +123,7 @@ constexpr int TILE = ELM_TS;                  // doubles per packed 64-wide tile
 constexpr int HALF = 32 * LP;                 // doubles per 32-column half tile
 constexpr int NSTAGE = 3;                     // stage = (A half, B half) = one tile of smem
 constexpr uint32_t HALF_BYTES = HALF * 8;
-constexpr int SMEM = NSTAGE * TILE * 8 + 10 * NB * 8 + 8 * 8;  // stages, potrf scratch, mbarriers
+constexpr int SMEM = NSTAGE * TILE * 8 + 10 * NB * 8 + 16 * 8;  // stages, potrf scratch, mbarriers
 }  // namespace llc
 
 // acc[r][n] += sum_kk A[kk*LP + r] B[kk*LP + n], kk < KW; warp tile 32 x 16 (wm = warp & 1, wn = warp >> 1)
@@ -331,13 +334,15 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
     extern __shared__ __align__(128) double csm[];
     double* St = csm;                                      // NSTAGE x (A half | B half)
     double* rsv = St + NSTAGE * TILE;                      // [10 * 64] potrf scratch
-    uint64_t* bar = reinterpret_cast<uint64_t*>(rsv + 10 * NB);  // [NSTAGE] chunk loads, [NSTAGE] epilogue loads
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rsv + 10 * NB);  // [NSTAGE] chunk loads, [NSTAGE] epilogue
+                                                                  // loads, [NSTAGE] stage released by all warps
     double* As = St;                                       // epilogue: C / X0 / R
     double* Bs = St + TILE;                                // epilogue: L(J,J)
     double* Ys = St + 2 * TILE;                            // epilogue: Y_J
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int s = 0; s < 2 * NSTAGE; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&bar[2 * NSTAGE + s], NT / 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -418,6 +423,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             const uint32_t g = g0 + c;
             double* st = St + (g % NSTAGE) * TILE;
             uint64_t* b = &bar[g % NSTAGE];
+            // every warp has released the stage's previous chunk (its phase g / NSTAGE - 1)
+            if (g >= (uint32_t)NSTAGE) mbar_wait(&bar[2 * NSTAGE + g % NSTAGE], ((g / NSTAGE) - 1) & 1);
             fence_proxy_async();
             mbar_expect(b, 2 * HALF_BYTES);
             bulk_load(st, tileptr(ke4.x) + h * HALF, HALF_BYTES, b);
@@ -438,7 +445,6 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 issue(c);
             }
         for (int c = 0; c < nch; ++c) {
-            if (c > 0) __syncthreads();  // every warp is done with chunk c-1: its stage may be refilled
             if (tid == 0 && c + NSTAGE - 1 < nch) {
                 const int cn = c + NSTAGE - 1;
                 if ((cn & 1) == 0) ensure(a.klist[kb + (cn >> 1)], J);
@@ -454,6 +460,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #endif
             const double* st = St + (g % NSTAGE) * TILE;
             mma_tile<32>(acc, st, st + HALF);
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&bar[2 * NSTAGE + g % NSTAGE]);  // stage free for its refill
         }
         gchunk = g0 + nch;
         __syncthreads();

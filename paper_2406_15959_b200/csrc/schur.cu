@@ -211,7 +211,7 @@ constexpr int NT = 256;
 constexpr int STAGE = 4 * BOX;           // R chunk (2 boxes) + X chunk (2 boxes)
 constexpr int XP = 65;                   // padded stride of the diagonal-solve tiles
 constexpr int SMEM_BODY = (2 * STAGE > 2 * 64 * XP + 64 ? 2 * STAGE : 2 * 64 * XP + 64);
-constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;
+constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;  // + [2] full, [2] empty mbarriers (<= 64 B)
 }  // namespace trw
 
 __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ CUtensorMap tmR,
@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], NT / 32);  // stage 0 / 1 released by every warp
+        mbar_init(&bar[3], NT / 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
         auto issue = [&](int ch, uint32_t g) {
             double* d = stg + (g & 1) * STAGE;
             const int r0 = 32 * ch;  // row of R11 / neuron index of X
+            if (g >= 2) mbar_wait(&bar[2 + (g & 1)], ((g >> 1) - 1) & 1);  // previous chunk of the stage consumed
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             mbar_expect(&bar[g & 1], 4 * BOX * 8);
             tma_load(d, &tmR, r0, i0, s, &bar[g & 1]);
@@ -282,9 +285,11 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
             }
-            __syncthreads();  // stage (g & 1) is refilled by the issue of the next iteration
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[2 + (g & 1)]);  // stage (g & 1) may be refilled
         }
         gch += nch;
+        __syncthreads();  // every warp is done with the stages: the diagonal solve reuses them
         // diagonal block: R_ii^T X = C
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
