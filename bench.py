@@ -190,7 +190,6 @@ def run_reference(args, world, rank):
 
     c = bench_config(args)
     O.set_grf(c.get("grf"))
-    O.set_grf(c.get("grf"))
     oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
     W, b, _, _ = O.init_hidden(oc)
     cores = len(os.sched_getaffinity(0))
@@ -209,7 +208,7 @@ def run_reference(args, world, rank):
     tot_n = sum(k for _, k in times)
     val = tot_n / tot_t
     sample = (f"per step: local phase (assemble, unblocked Householder QR, literal eqn:schur pieces, back-solve) "
-              f"of {n} random subdomains of cfg{args.config} on {cores} threads; interface solve excluded")
+              f"of {n} random subdomains of {c.get('name', f'cfg{args.config}')} on {cores} threads; interface solve excluded")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -235,7 +234,7 @@ def cpu_baseline_leg(c, k):
     t = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
     return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"local phase (assemble + unblocked QR + literal Schur pieces + back-solve) of {n} random "
-                      f"subdomains of cfg{k}, {t:.1f} s on {cores} threads; interface solve excluded"}
+                      f"subdomains of {c.get('name', f'cfg{k}')}, {t:.1f} s on {cores} threads; interface solve excluded"}
 
 
 class PhaseTimer:
