@@ -190,7 +190,8 @@ def run_reference(args, world, rank):
 
     c = bench_config(args)
     O.set_grf(c.get("grf"))
-    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
+    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"],
+               c.get("tikhonov", 0.0))
     W, b, _, _ = O.init_hidden(oc)
     cores = len(os.sched_getaffinity(0))
     N = c["P"] ** 2
@@ -223,7 +224,8 @@ def cpu_baseline_leg(c, k):
     import oracle as O
 
     O.set_grf(c.get("grf"))
-    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"])
+    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"],
+               c.get("tikhonov", 0.0))
     W, b, _, _ = O.init_hidden(oc)
     cores = len(os.sched_getaffinity(0))
     N = c["P"] ** 2

@@ -80,12 +80,18 @@ typedef struct {
     int32_t interface_mode; /* factorisation order of the Schur matrix: 0 auto (less work) |
                                1, 2 strip order (envelope) | 3 nested dissection             */
     int32_t reserved;
+    double tikhonov;        /* lambda >= 0 (0: off).  lambda > 0 appends M rows lambda e_j^T (right-
+                               hand side 0) to every K^s, i.e. each local LS becomes
+                               min ||K c - r||^2 + lambda^2 ||c||^2 (reading R29): the near-square,
+                               numerically rank-deficient local problems of the paper's Table 2
+                               need such damping of K^{s+} (the paper's least-squares solver
+                               truncates).  ld = round_up(m + M, 32); r_s includes lambda ||c||.  */
 } elmddm_config;
 
 typedef struct {
     int64_t N;          /* total subdomains P*P                                               */
     int64_t S;          /* local subdomains s_end - s_begin                                   */
-    int64_t m;          /* rows of K^s: p*p + 4q                                              */
+    int64_t m;          /* collocation rows of K^s: p*p + 4q (+ M Tikhonov rows below them)   */
     int64_t ld;         /* leading dimension of K_aug (m rounded up to 32; rows m..ld-1 are 0) */
     int64_t ncols;      /* columns of K_aug: M + 4q + 1  ([K | E_Gamma | F])                  */
     int64_t kaug;       /* augmented columns 4q + 1                                            */

@@ -32,6 +32,7 @@ class Cfg(C.Structure):
         ("P", C.c_int32), ("M", C.c_int32), ("p", C.c_int32), ("q", C.c_int32),
         ("problem", C.c_int32), ("init_scheme", C.c_int32),
         ("init_c", C.c_double), ("r_over_diam", C.c_double), ("seed", C.c_uint64),
+        ("tikhonov", C.c_double),
     ]
 
 
@@ -72,8 +73,8 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0) -> Cfg:
-    return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed)
+def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0, tikhonov=0.0) -> Cfg:
+    return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed, tikhonov)
 
 
 def set_grf(params) -> None:

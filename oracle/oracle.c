@@ -40,6 +40,7 @@ typedef struct {
     double init_c;          /* c in l = c sqrt(n), P:544 (1/8 for Poisson) */
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s), P:546 (1/2) */
     uint64_t seed;
+    double tikhonov;        /* lambda >= 0: M extra rows lambda * e_j^T of K^s (reading R29) */
 } orc_cfg;
 
 static const double PI = 3.14159265358979323846;
@@ -158,6 +159,9 @@ void orc_problem(int problem, double x, double y, double *u, double *f) {
 /* ------------------------------------------------------------------------------------------ */
 /* edges: 0 left (x = x0), 1 right (x = x0+h), 2 bottom (y = y0), 3 top (y = y0+h)           */
 static int orc_m(const orc_cfg *c) { return c->p * c->p + 4 * c->q; }
+/* rows of K^s: the m collocation rows, then (reading R29, Tikhonov damping of the local LS)
+ * M rows lambda e_j^T with right-hand side 0, so that min ||K c - r||^2 + lambda^2 ||c||^2      */
+static int orc_mk(const orc_cfg *c) { return orc_m(c) + (c->tikhonov > 0.0 ? c->M : 0); }
 
 /* Face id of edge e of subdomain (i,j), or -1 if the edge lies on dOmega (Dirichlet).
  * Strip order: strip j holds V(0..P-2, j) then H(0..P-1, j) (j < P-1).                        */
@@ -185,6 +189,11 @@ void orc_rows(const orc_cfg *c, int s, double *xy, int32_t *edge, int32_t *gidx)
     int P = c->P, p = c->p, q = c->q, np = orc_npts(c);
     int i = s % P, j = s / P;
     int r = 0;
+    for (int t = orc_m(c); t < orc_mk(c); ++t) { /* Tikhonov rows: no point, edge -2 */
+        xy[2 * t] = xy[2 * t + 1] = 0.0;
+        edge[t] = -2;
+        gidx[t] = -1;
+    }
     for (int b = 0; b < p; ++b)
         for (int a = 0; a < p; ++a, ++r) {
             xy[2 * r] = (double)(i * (p + 1) + a + 1) / (double)(P * (p + 1));
@@ -213,7 +222,7 @@ void orc_rows(const orc_cfg *c, int s, double *xy, int32_t *edge, int32_t *gidx)
 /* out[0]=m  out[1]=G  out[2]=faces  out[3]=N  */
 void orc_geometry(const orc_cfg *c, int64_t *out) {
     int64_t P = c->P;
-    out[0] = orc_m(c);
+    out[0] = orc_mk(c);
     out[2] = 2 * P * (P - 1);
     out[1] = out[2] * c->q;
     out[3] = P * P;
@@ -335,11 +344,15 @@ void orc_rho(double x, double y, double *rho, double *rx, double *ry) {
  * of edge e point k (zero rows for Dirichlet edges).                                          */
 void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, double *K, double *F,
                   double *A) {
-    int M = c->M, q = c->q, m = orc_m(c);
-    double *xy = (double *)malloc(sizeof(double) * 2 * (size_t)m);
-    int32_t *edge = (int32_t *)malloc(sizeof(int32_t) * (size_t)m);
-    int32_t *gidx = (int32_t *)malloc(sizeof(int32_t) * (size_t)m);
+    int M = c->M, q = c->q, m = orc_m(c), mk = orc_mk(c);
+    double *xy = (double *)malloc(sizeof(double) * 2 * (size_t)mk);
+    int32_t *edge = (int32_t *)malloc(sizeof(int32_t) * (size_t)mk);
+    int32_t *gidx = (int32_t *)malloc(sizeof(int32_t) * (size_t)mk);
     orc_rows(c, s, xy, edge, gidx);
+    for (int r = m; r < mk; ++r) { /* reading R29: lambda e_j^T, right-hand side 0 */
+        F[r] = 0.0;
+        for (int n = 0; n < M; ++n) K[(size_t)n * mk + r] = (r - m == n) ? c->tikhonov : 0.0;
+    }
     static const double nx[4] = {-1.0, 1.0, 0.0, 0.0};
     static const double ny[4] = {0.0, 0.0, -1.0, 1.0};
     const double *Ws = W + (size_t)2 * s * M;
@@ -370,7 +383,7 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
                 double d4 = -6.0 * d1 * d2 - 2.0 * t * d3;
                 if (edge[r] < 0) val = w2 * w2 * d4;                 /* Lap^2 phi = |w|^4 sigma'''' */
                 else val = ROW_KIND(r) == 0 ? t : w2 * d2;           /* phi, Lap phi = |w|^2 sigma'' */
-                K[(size_t)n * m + r] = val;
+                K[(size_t)n * mk + r] = val;
                 if (edge[r] >= 0 && A) {
                     int e = edge[r];
                     int ar = r - (m - 4 * q);
@@ -391,7 +404,7 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
             } else {
                 val = t;
             }
-            K[(size_t)n * m + r] = val;
+            K[(size_t)n * mk + r] = val;
             if (edge[r] >= 0 && A) {
                 int e = edge[r];
                 int ar = r - (m - 4 * q); /* = e*q + k */
@@ -496,7 +509,7 @@ static void local_free(orc_local *L) {
 
 /* Steps 2-5 of the oracle for one subdomain. */
 static void local_build(const orc_cfg *c, int s, const double *W, const double *b, orc_local *L) {
-    int M = c->M, q = c->q, m = orc_m(c);
+    int M = c->M, q = c->q, m0 = orc_m(c), m = orc_mk(c); /* collocation rows, rows of K^s */
     L->m = m;
     L->M = M;
     double *xy = (double *)malloc(sizeof(double) * 2 * (size_t)m);
@@ -519,7 +532,7 @@ static void local_build(const orc_cfg *c, int s, const double *W, const double *
         if (gidx[r] >= 0) {
             L->irow[k] = r;
             L->ig[k] = gidx[r];
-            int ar = r - (m - 4 * q);
+            int ar = r - (m0 - 4 * q);
             for (int n = 0; n < M; ++n) L->Aflux[(size_t)k * M + n] = A4[(size_t)n * 4 * q + ar];
             ++k;
         }

@@ -24,6 +24,7 @@ class Config(C.Structure):
         ("problem", C.c_int32), ("init_scheme", C.c_int32),
         ("init_c", C.c_double), ("r_over_diam", C.c_double), ("seed", C.c_uint64),
         ("s_begin", C.c_int32), ("s_end", C.c_int32), ("interface_mode", C.c_int32), ("reserved", C.c_int32),
+        ("tikhonov", C.c_double),
     ]
 
 

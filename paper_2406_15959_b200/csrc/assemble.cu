@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     xi[e] = ed == 0 ? p : (ed == 1 ? p + 1 : p + 2 + k);
                     yi[e] = ed == 2 ? p : (ed == 3 ? p + 1 : p + 2 + k);
                 } else {
-                    kind[e] = 2;
+                    kind[e] = 2;  // padding, or (reading R29) the damping row lambda e_{r-m}^T
                     xi[e] = yi[e] = 0;
                 }
             }
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                                                    : w2s[cc] * sg;
                         v[e] = kind[e] == 0 ? lap * s1 : (kind[e] == 1 ? sg : 0.0);
                     }
+                    if (kind[e] == 2) v[e] = (2 * r2 + e - m == c0 + cc) ? cfg.tikhonov : 0.0;
                 }
                 *reinterpret_cast<double2*>(Ks + (int64_t)(c0 + cc) * ld + 2 * r2) = make_double2(v[0], v[1]);
             }

@@ -49,6 +49,8 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (cfg->q < 2 || cfg->q % 2 != 0) return why = "q must be even and >= 2", false;
     int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
     if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
+    if (!(cfg->tikhonov >= 0.0) || !(cfg->tikhonov < 1e300)) return why = "tikhonov must be finite and >= 0", false;
+    if (cfg->tikhonov > 0.0) m += cfg->M;  // reading R29: M damping rows below the collocation rows
     if (round_up(m, 32) > 3008) return why = "m too large for the shared-memory panel (ld <= 3008)", false;
     if (cfg->problem < 0 || cfg->problem > 7) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
@@ -322,7 +324,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     z.N = P * P;
     z.S = cfg->s_end - cfg->s_begin;
     z.m = (int64_t)cfg->p * cfg->p + 4 * q;
-    z.ld = round_up(z.m, 32);
+    z.ld = round_up(z.m + (cfg->tikhonov > 0.0 ? cfg->M : 0), 32);
     z.kaug = 4 * q + 1;
     z.ncols = M + z.kaug;
     z.kaug_elems = z.S * z.ld * z.ncols;

@@ -59,6 +59,7 @@ class Problem:
     interface_mode: int = 0             # factorisation order: 0 auto | 1, 2 strip (envelope) | 3 nested dissection
     interface_solver: str = "cholesky"  # "cholesky" (direct, reading R12) | "cg" (the paper's)
     cg_tol: float = 1e-9                # relative residual of the CG solver
+    tikhonov: float = 0.0               # lambda of the damped local LS (reading R29; 0 = off)
     grf: object = None                  # problem 6: eqn:grf draws [n][4] (a, w_x, w_y, b)
 
     @classmethod
@@ -81,7 +82,7 @@ class Context:
         if prob.interface_solver not in ("cholesky", "cg"):
             raise _lib.ElmddmError(f"unknown interface_solver {prob.interface_solver!r}")
         cfg = _lib.Config(prob.P, prob.M, prob.p, prob.q, prob.problem, prob.init_scheme, prob.init_c,
-                          prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, 0)
+                          prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, 0, prob.tikhonov)
         h = C.c_void_p()
         rc = L.elmddm_create(C.byref(cfg), self.device, C.byref(h))
         if rc != 0:

@@ -221,10 +221,11 @@ def _sampled_subdomains(P):
     return sorted({0, P - 1, P * (P // 2) + P // 2, N - 1})
 
 
-@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("k", [3, 4, 5, 6])
 def test_large_config_sampled_parity(k):
-    """Full BASELINE sizes in the bench launch configuration: for sampled subdomains the oracle
-    back-solves with the GPU's u_Gamma; r_s and u at the owned grid points must agree."""
+    """Full BASELINE sizes in the bench launch configuration (and the paper's Table 2 workloads
+    5, 6 with the damped local LS of reading R29): for sampled subdomains the oracle back-solves
+    with the GPU's u_Gamma; r_s and u at the owned grid points must agree."""
     import torch
 
     c = WL.config(k)
@@ -272,6 +273,8 @@ def test_large_config_sampled_parity(k):
 # ------------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("cfgkw", [
     dict(P=1, M=24, p=10, q=6, problem=4),          # single subdomain: classical ELM, G = 0
+    dict(P=3, M=72, p=11, q=10, problem=2, tikhonov=1e-3),       # damped local LS (reading R29)
+    dict(P=2, M=64, p=7, q=4, problem=4, tikhonov=1e-4),         # near-square (m = 65 < M + 32)
     dict(P=2, M=40, p=9, q=6, problem=1),           # M not a multiple of the 64-panel, odd p
     dict(P=3, M=72, p=11, q=10, problem=2),         # 3 x 3 (interior subdomain with 4 faces)
     dict(P=2, M=8, p=3, q=2, problem=0),            # minimal sizes

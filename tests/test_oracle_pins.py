@@ -26,7 +26,7 @@ def mkcfg(k=None, **kw):
         c = dict(P=2, M=16, p=6, q=5, problem=0, seed=7, init_scheme=0, init_c=0.125, r_over_diam=0.5)
         c.update(kw)
     return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0),
-                 c.get("init_c", 0.125), c.get("r_over_diam", 0.5), c["seed"])
+                 c.get("init_c", 0.125), c.get("r_over_diam", 0.5), c["seed"], c.get("tikhonov", 0.0))
 
 
 # ------------------------------------------------------------------------------------------------
@@ -288,12 +288,12 @@ def _global_blocks(c, W, b):
     for s in range(N):
         K, F, A4 = O.assemble(c, s, W, b)
         xy, edge, gidx = O.rows(c, s)
-        m = len(edge)
+        m = len(edge)  # collocation rows p^2 + 4q, then (tikhonov > 0) the M damping rows
         B = np.zeros((m, G))
         Ag = np.zeros((G, M))
         for r in np.where(gidx >= 0)[0]:
             B[r, gidx[r]] = -1.0
-            Ag[gidx[r]] += A4[r - (m - 4 * c.q)]
+            Ag[gidx[r]] += A4[r - c.p * c.p]
         Ks.append(K)
         Fs.append(F)
         Bs.append(B)
@@ -329,11 +329,13 @@ def test_schur_matches_literal_eqn_schur(P):
     assert np.linalg.eigvalsh(r["M"]).min() > 0      # SPD
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_schur_solution_equals_monolithic_lstsq_of_eliminated_system(P):
+@pytest.mark.parametrize("P,lam", [(2, 0.0), (3, 0.0), (2, 0.05), (3, 0.3)])
+def test_schur_solution_equals_monolithic_lstsq_of_eliminated_system(P, lam):
     """Central equivalence: (c, u_Gamma) of the Schur route == the least-squares solution of the
-    monolithic eqn:eliminated system [[K, B], [0, -AK^+B]] [c; u] = [F; -AK^+F]."""
-    c = _tiny_cfg(P)
+    monolithic eqn:eliminated system [[K, B], [0, -AK^+B]] [c; u] = [F; -AK^+F].
+    With Tikhonov damping (reading R29) K is the stacked [K; lam I] of every subdomain, B and F
+    zero on the damping rows: the same identity then pins the damped route."""
+    c = _tiny_cfg(P, tikhonov=lam)
     W, b, _, _ = O.init_hidden(c)
     K, B, A, F = _global_blocks(c, W, b)
     Kp = np.linalg.pinv(K)
@@ -603,3 +605,39 @@ def test_plate_solution_accuracy():
     r = O.solve(c, W, b, xy)
     ex = WL.exact(7, xy)
     assert np.linalg.norm(r["u"] - ex) / np.linalg.norm(ex) < 1e-9
+
+
+# ------------------------------------------------------------------------------------------------
+# Tikhonov damping of the local LS (reading R29)
+# ------------------------------------------------------------------------------------------------
+def test_tikhonov_rows_pinned():
+    """lambda > 0 appends exactly lambda I (and zero right-hand side, no interface unknown, no
+    flux) below the unchanged collocation rows."""
+    lam = 0.37
+    c0 = mkcfg(P=2, M=16, p=6, q=4, problem=2, seed=3)
+    c1 = mkcfg(P=2, M=16, p=6, q=4, problem=2, seed=3, tikhonov=lam)
+    W, b, _, _ = O.init_hidden(c0)
+    m0 = 6 * 6 + 4 * 4
+    assert O.geometry(c1)["m"] == m0 + 16 and O.geometry(c0)["m"] == m0
+    for s in range(4):
+        K0, F0, A0 = O.assemble(c0, s, W, b)
+        K1, F1, A1 = O.assemble(c1, s, W, b)
+        assert np.array_equal(K1[:m0], K0) and np.array_equal(F1[:m0], F0) and np.array_equal(A1, A0)
+        assert np.array_equal(K1[m0:], lam * np.eye(16)) and not F1[m0:].any()
+        _, edge, gidx = O.rows(c1, s)
+        assert (edge[m0:] == -2).all() and (gidx[m0:] == -1).all()
+
+
+def test_tikhonov_single_subdomain_closed_form():
+    """P = 1: c = (K^T K + lambda^2 I)^{-1} K^T F (ridge regression), r = sqrt(||Kc - F||^2 +
+    lambda^2 ||c||^2): closed forms from the normal equations, independent of the QR route."""
+    c0 = mkcfg(P=1, M=30, p=12, q=8, problem=4, seed=9, init_c=0.125)
+    W, b, _, _ = O.init_hidden(c0)
+    K, F, _ = O.assemble(c0, 0, W, b)
+    lam = 1e-3 * np.linalg.norm(K, 2)
+    c1 = mkcfg(P=1, M=30, p=12, q=8, problem=4, seed=9, init_c=0.125, tikhonov=lam)
+    r = O.solve(c1, W, b)
+    ref = np.linalg.solve(K.T @ K + lam * lam * np.eye(30), K.T @ F)
+    assert np.allclose(r["coef"][0], ref, rtol=0, atol=1e-9 * np.abs(ref).max())
+    rr = np.sqrt(np.linalg.norm(K @ ref - F) ** 2 + lam * lam * np.linalg.norm(ref) ** 2)
+    assert abs(r["resid"][0] - rr) <= 1e-9 * rr
