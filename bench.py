@@ -88,7 +88,7 @@ def workload_desc(k: int, c: dict | None = None) -> str:
 # ------------------------------------------------------------------------------------------------
 def algorithmic(c: dict, s_range) -> dict:
     P, M, p, q = c["P"], c["M"], c["p"], c["q"]
-    m = p * p + 4 * q
+    m = p * p + 4 * q + (M if c.get("tikhonov", 0.0) > 0 else 0)  # + the damping rows (reading R29)
     fl_qr = 0.0
     bytes_asm = 0.0
     bytes_asm_e = 0.0
