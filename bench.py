@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--alpha", type=float, default=16.0, help="eqn:grf alpha of problem 6")
     ap.add_argument("--interface-solver", default=None, choices=["cholesky", "cg"],
                     help="interface solve: direct tile Cholesky (default) or the paper's CG (P:412)")
+    ap.add_argument("--tikhonov", type=float, default=None, help="override the damping lambda (reading R29)")
     ap.add_argument("--phases", action="store_true", help="print per-phase breakdown to stderr")
     return ap.parse_args()
 
@@ -57,6 +58,8 @@ def bench_config(args) -> dict:
     over = {"interface_mode": getattr(args, "interface_mode", 0)}
     if getattr(args, "interface_solver", None):
         over["interface_solver"] = args.interface_solver
+    if getattr(args, "tikhonov", None) is not None:
+        over["tikhonov"] = args.tikhonov
     if getattr(args, "problem", None) is not None:
         over["problem"] = args.problem
         over["alpha"] = args.alpha

@@ -51,7 +51,9 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
     if (!(cfg->tikhonov >= 0.0) || !(cfg->tikhonov < 1e300)) return why = "tikhonov must be finite and >= 0", false;
     if (cfg->tikhonov > 0.0) m += cfg->M;  // reading R29: M damping rows below the collocation rows
-    if (round_up(m, 32) > 3008) return why = "m too large for the shared-memory panel (ld <= 3008)", false;
+    // ld <= 3008: every panel variant; taller (up to ~9.6k rows): the 4-CTA cluster block panel
+    if (round_up(m, 32) > 3008 && panel_cl_stage(round_up(m, 32), 227 * 1024) == 0)
+        return why = "m too large for the QR panels (ld <= ~9600 rows)", false;
     if (cfg->problem < 0 || cfg->problem > 7) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;

@@ -89,6 +89,7 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
                         int crit_band, CholPlan& pl, int split_min = 0);
 double schedule_chol_tasks(CholPlan& pl, int workers);
 int chol_split_min();
+int panel_cl_stage(int64_t ld, int smem_optin);  // qr.cu: ring stage of the cluster panel, 0 = ld too tall
 void export_tasks(const CholPlan& pl, int32_t* tasks);
 void interface_face_pairs(int P, std::vector<std::pair<int, int>>& out);
 double chol_eval(const CholPlan& pl, const std::vector<int>& order, int workers);

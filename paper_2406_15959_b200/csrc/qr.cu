@@ -1718,22 +1718,23 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 // ------------------------------------------------------------------------------------------
 namespace pcl {
 constexpr int CL = 4;                 // CTAs per subdomain
-constexpr int STG = 56 * 132;         // doubles per ring stage
+constexpr int STG = 56 * 132;         // doubles per ring stage (default; smaller for tall panels)
+constexpr int STG_MIN = 56 * 36;      // >= 32 rows of a 56-column V chunk, and 2 stages hold T (56^2)
 constexpr int XN = 448;               // doubles per exchange slot (kp * 8 <= 448)
 }  // namespace pcl
 
-__device__ __forceinline__ int vp_rows_cl(int kp) {
-    const int r = ((pcl::STG / kp - 4) / 32) * 32;
+__device__ __forceinline__ int vp_rows_cl(int kp, int stg) {
+    const int r = ((stg / kp - 4) / 32) * 32;
     return r < 32 ? 32 : (r > 256 ? 256 : r);
 }
 
 // G (kp x 8, column-major ld kp) = Vp[0:nr]^T X[0:nr] (partial over this CTA's rows)
 __device__ void vt_block_cl(const double* __restrict__ Vp, int64_t ld, int nr, int kp, const double* X, int RP,
-                            double* G, double* ring, double* pairbuf) {
+                            double* G, double* ring, double* pairbuf, int stg) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int mtiles = kp >> 3, t = warp >> 1, par = warp & 1;
     const int kr = lane & 3, cn = lane >> 2;
-    const int rch = vp_rows_cl(kp), rcp = rch + 4;
+    const int rch = vp_rows_cl(kp, stg), rcp = rch + 4;
     const int nch = (nr + rch - 1) / rch;
     double a0 = 0.0, a1 = 0.0;
     if (nch > 0) {
@@ -1741,11 +1742,11 @@ __device__ void vt_block_cl(const double* __restrict__ Vp, int64_t ld, int nr, i
         asm volatile("cp.async.commit_group;\n" ::);
     }
     for (int c = 0; c < nch; ++c) {
-        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * pcl::STG, Vp, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
+        if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * stg, Vp, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 1;\n" ::);
         __syncthreads();
-        const double* st = ring + (c & 1) * pcl::STG;
+        const double* st = ring + (c & 1) * stg;
         const int nq = min(rch, nr - c * rch) / 8;
         if (t < mtiles) {
 #pragma unroll 4
@@ -1769,8 +1770,17 @@ __device__ void vt_block_cl(const double* __restrict__ Vp, int64_t ld, int nr, i
     }
 }
 
-size_t panel_cl_smem(int64_t Rq) {
-    return (size_t)(8 * (Rq + 4) + 2 * pcl::STG + 2 * pcl::CL * pcl::XN + 2 * 8 * 56 + PNW * 28 + 40 + 64 + 8 + 16) * 8;
+size_t panel_cl_smem(int64_t Rq, int stg) {
+    return (size_t)(8 * (Rq + 4) + 2 * stg + 2 * pcl::CL * pcl::XN + 2 * 8 * 56 + PNW * 28 + 40 + 64 + 8 + 16) * 8;
+}
+// ring stage of the cluster panel for a panel of ld rows: the default, or as much as fits next to
+// the row block (tall panels, e.g. the damped local LS of reading R29); 0 if even STG_MIN does not fit
+int cl_stage(int64_t ld, int smem_optin) {
+    const int64_t Rq = ((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32;
+    if (panel_cl_smem(Rq, pcl::STG) <= (size_t)smem_optin) return pcl::STG;
+    const int64_t avail = ((int64_t)smem_optin - (int64_t)panel_cl_smem(Rq, 0)) / 16;  // doubles per stage
+    const int stg = (int)std::min<int64_t>(pcl::STG, avail & ~(int64_t)7);
+    return stg >= pcl::STG_MIN ? stg : 0;
 }
 
 __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_panel_cl(PanelArgs a) {
@@ -1789,8 +1799,9 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
     const int d0 = jb - j0;
     const int tid = threadIdx.x;
     double* Cb = sm;                      // [8][RP]  own rows
-    double* ring = Cb + 8 * RP;           // [2][STG]
-    double* xch = ring + 2 * STG;         // [2][CL][XN]
+    const int stg = a.ring;               // doubles per ring stage (panel_cl_stage)
+    double* ring = Cb + 8 * RP;           // [2][stg]
+    double* xch = ring + 2 * stg;         // [2][CL][XN]
     double* Wsm = xch + 2 * CL * XN;      // [8][kp]
     double* Zsm = Wsm + 8 * 56;           // [8][kp]
     double* red = Zsm + 8 * 56;           // [PNW][28]
@@ -1830,7 +1841,7 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
 
     if (kp > 0) {
         // B. W = V_prev^T C (all-reduced), Z = T^T W, C -= V_prev Z on own rows
-        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm);
+        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm, stg);
         __syncthreads();
         const double* buf = exchange(Wsm, kp * 8);
         for (int i = tid; i < kp * 8; i += PNT) {
@@ -1859,18 +1870,18 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
 #pragma unroll
             for (int t = 0; t < 14; ++t) zb[t] = t < ksteps ? -Zsm[rn * kp + t * 4 + kr] : 0.0;
             __syncthreads();  // Ts (ring) no longer read
-            const int rch = vp_rows_cl(kp), rcp = rch + 4;
+            const int rch = vp_rows_cl(kp, stg), rcp = rch + 4;
             const int nch = (nr + rch - 1) / rch;
             if (nch > 0) {
                 vp_chunk(ring, Vz, ld, kp, rch, 0, min(rch, nr));
                 asm volatile("cp.async.commit_group;\n" ::);
             }
             for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * STG, Vz, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
+                if (c + 1 < nch) vp_chunk(ring + ((c + 1) & 1) * stg, Vz, ld, kp, rch, c + 1, min(rch, nr - (c + 1) * rch));
                 asm volatile("cp.async.commit_group;\n" ::);
                 asm volatile("cp.async.wait_group 1;\n" ::);
                 __syncthreads();
-                const double* st = ring + (c & 1) * STG;
+                const double* st = ring + (c & 1) * stg;
                 const int nmt = min(rch, nr - c * rch) / 8;
                 for (int mt = warp; mt < nmt; mt += PNW) {
                     const int rr = c * rch + mt * 8;
@@ -2026,7 +2037,7 @@ __global__ void __cluster_dims__(pcl::CL, 1, 1) __launch_bounds__(PNT, 1) k_pane
     }
     // G. T[0:kp, kp:kp+8] = -T Y, Y = (V_prev^T V_b) Tbb
     if (kp > 0) {
-        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm);
+        vt_block_cl(Vz, ld, nr, kp, Cb, RP, Wsm, ring, Zsm, stg);
         __syncthreads();
         const double* buf = exchange(Wsm, kp * 8);
         for (int i = tid; i < kp * 8; i += PNT) {
@@ -2997,16 +3008,24 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     const size_t smax = panel_smem_bytes(ld, panel_ring(ld, optin));
-    if ((e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)) != cudaSuccess)
+    const bool blk_ok = smax <= (size_t)optin;  // the one-CTA block panel holds (ld - j0) x 8 in shared memory
+    if (blk_ok &&
+        (e = cudaFuncSetAttribute(k_panel_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)) != cudaSuccess)
         return e;
+    // 4-CTA cluster block panels: for small slabs (panel_cluster), and for panels too tall for one
+    // CTA (the damped local LS of reading R29), with a ring stage sized to what fits
+    const bool use_cl = c->panel_cluster || !blk_ok;
+    const int stg_cl = cl_stage(ld, optin);
+    if (use_cl && stg_cl == 0) return cudaErrorInvalidValue;  // create() validated ld against this
     const bool pp_ok = c->panel_merged && panelp_smem_bytes(ld, panelp_ring(ld, optin)) <= (size_t)optin;
     const bool pt_ok = c->panel_tmem && (ld + 127) / 128 * 16 <= 512;
     if (pt_ok && (e = cudaFuncSetAttribute(k_panel_t, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM)) != cudaSuccess)
         return e;
     if (pp_ok && (e = cudaFuncSetAttribute(k_panel_p, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)panel_cl_smem(((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32))) != cudaSuccess)
+    if (stg_cl > 0 &&
+        (e = cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)panel_cl_smem(((ld + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32, stg_cl))) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(k_wy_update, cudaFuncAttributeMaxDynamicSharedMemorySize, wy::SMEM)) != cudaSuccess)
         return e;
@@ -3056,7 +3075,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         const int nb = (M - j0) < ELM_NB ? (M - j0) : ELM_NB;
         const int ring = panel_ring(ld - j0, optin);
         const size_t smem = panel_smem_bytes(ld - j0, ring);
-        const size_t smem_cl = panel_cl_smem(((ld - j0 + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32);
+        const size_t smem_cl = panel_cl_smem(((ld - j0 + 32 * pcl::CL - 1) / (32 * pcl::CL)) * 32, stg_cl);
         const int n_tr = (int)(ncols - (j0 + nb));
         for (int g = 0; g < ngroups; ++g) {
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
@@ -3077,7 +3096,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 k_panel_c8<<<(unsigned)((g1 - g0) * p8::CL), p8::NT, panel8_smem(ld - j0, nb), streams[g]>>>(pa, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
-            } else if (pt_ok && !c->panel_cluster) {
+            } else if (pt_ok && !use_cl) {
                 // (prio: the panel runs on the group's high-priority stream after the group's
                 // previous trailing update; the next trailing update waits for it)
                 if (prio && j0 > 0) cudaStreamWaitEvent(pstr[g], c->ev_wy[g], 0);
@@ -3092,19 +3111,21 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                     cudaEventRecord(c->ev_panel[g], pstr[g]);
                     cudaStreamWaitEvent(streams[g], c->ev_panel[g], 0);
                 }
-            } else if (pp_ok && !c->panel_cluster) {
+            } else if (pp_ok && !use_cl) {
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 PanelArgs pp = pa;
                 pp.ring = panelp_ring(ld - j0, optin);
                 k_panel_p<<<(unsigned)(g1 - g0), PNT, panelp_smem_bytes(ld - j0, pp.ring), streams[g]>>>(pp, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
-            for (int blk = 0; !p8_ok && !p8t_ok && !((pp_ok || pt_ok) && !c->panel_cluster) && blk < nb / ELM_BB; ++blk) {
+            for (int blk = 0; !p8_ok && !p8t_ok && !((pp_ok || pt_ok) && !use_cl) && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
-                if (c->panel_cluster)
-                    k_panel_cl<<<(unsigned)((g1 - g0) * pcl::CL), PNT, smem_cl, streams[g]>>>(pa);
-                else
+                if (use_cl) {
+                    PanelArgs pc = pa;
+                    pc.ring = stg_cl;
+                    k_panel_cl<<<(unsigned)((g1 - g0) * pcl::CL), PNT, smem_cl, streams[g]>>>(pc);
+                } else
                     k_panel_block<<<(unsigned)(g1 - g0), PNT, smem, streams[g]>>>(pa);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
@@ -3138,3 +3159,5 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     }
     return cudaSuccess;
 }
+
+int panel_cl_stage(int64_t ld, int smem_optin) { return cl_stage(ld, smem_optin); }

@@ -21,16 +21,20 @@ CONFIGS = [
     # neurons in total (M = n / N per subdomain), (2^8 + 1)^2 = 66,049 training points in total
     # (P:434-437).  Per subdomain p^2 + 4q = (256/P + 1)^2 points, the paper's count, on the
     # face-point layout of reading R1 (q points per edge, no shared cross points).
-    # Only N = 8 x 8 and 16 x 16 fit the panel kernels' ld <= 3008 (with the M damping rows).
+    # N = 8 x 8 and 16 x 16 fit every panel kernel's ld <= 3008 (with the M damping rows).
     # The near-square, numerically rank-deficient local problems defeat the undamped unpivoted-QR
     # elimination (oracle and GPU alike), so these run the damped local LS of reading R29 with
     # lambda = 1e-9 / 1e-10 x sigma_max(K^s) of an interior subdomain (1.34e5 / 6.58e4), chosen by
     # the lambda sweep of tools/pinv_study.py (DESIGN.md §10 NEXT-2).
     dict(name="t2-8x8", P=8, M=1024, p=31, q=32, problem=4, seed=5, tikhonov=1.3e-4),
     dict(name="t2-16x16", P=16, M=256, p=15, q=16, problem=4, seed=6, tikhonov=6.6e-6),
+    # 4 x 4: m + M = 8321 rows (ld 8352) -- the QR panels run on 4-CTA clusters with a reduced
+    # ring; lambda = 1e-10 sigma_max(K^s) (2.2e5); undamped, the interface Cholesky meets a
+    # non-positive pivot
+    dict(name="t2-4x4", P=4, M=4096, p=63, q=64, problem=4, seed=7, tikhonov=2.2e-5),
 ]
 # the paper's Table 2 (CPU cluster, context only): relative L2 error, wall-clock s
-PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43)}
+PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43), 7: (1.6192e-08, 19.46)}
 
 # the bench workload: config 3 (16 x 16 subdomains, 2820 x 1600 local LS, ~9 GB of local
 # matrices) -- the largest local least-squares problem of BASELINE.json that fits one B200.
