@@ -320,6 +320,18 @@ def test_rank_warning():
     assert rel_l2(u.cpu().numpy(), WL.exact(c1["problem"], xy)) < 1e-6
 
 
+def test_paper_table2_4x4_tall_panels():
+    """The paper's Table 2 workload at 4 x 4 (config 7: 8,321-row damped local LS, QR panels on
+    4-CTA clusters with a reduced ring): accuracy vs the exact solution (the tall-panel path is
+    parity-tested against the oracle at ld 3104 in test_edge_configs_end_to_end; the oracle's
+    unblocked QR of 16 x 8321 x 4096 is too slow for a test)."""
+    c = WL.config(7)
+    xy = WL.eval_grid()
+    ctx, buf, u = run_gpu(c, xy)
+    assert ctx.sizes["ld"] > 3008
+    assert rel_l2(u.cpu().numpy(), WL.exact(c["problem"], xy)) < 2e-8   # measured 2.0e-9; paper 1.6e-8
+
+
 def test_nonfinite_in_qr_is_an_error():
     """non-finite values are a numerical breakdown (ELMDDM_ENUMERIC) naming the
     subdomain; the status is reported once, then cleared."""
