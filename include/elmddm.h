@@ -114,8 +114,10 @@ typedef struct {
 } elmddm_sizes_t;
 
 /* ---- context ------------------------------------------------------------------------------ */
-/* Validates cfg (P>=1, M%8==0, q even, p>=1, m >= M, 0<=s_begin<s_end<=N), builds the geometry
- * and face tables and uploads them to `device`.  Synchronous.                                 */
+/* Validates cfg (P>=1, M%8==0, q even <= 256, p>=1, m >= M, 0<=s_begin<s_end<=N, tikhonov finite
+ * >= 0, problem 0..7, ld = rows of K^s rounded to 32 <= ~9.6k: up to 3008 rows every QR panel
+ * variant, beyond that the 4-CTA cluster panel with a reduced ring), builds the geometry and
+ * face tables and uploads them to `device`.  Synchronous.                                     */
 elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** out);
 void elmddm_destroy(elmddm_ctx* ctx);
 const char* elmddm_last_error(const elmddm_ctx* ctx);
