@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(512) k_coef(elmddm_config cfg, const double4* 
     }
 }
 
-constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel
+constexpr int AS_COLS = 8;   // columns per CTA in the K_aug kernel: must divide 8 (M % 8 == 0 is
+                             // validated), so no CTA straddles the neuron / augmented boundary
 constexpr int AS_NT = 256;
 
 // 1/x for x in [1, 1e30]: MUFU.RCP64H seed + two Newton steps (full double precision)
