@@ -274,6 +274,7 @@ def test_large_config_sampled_parity(k):
 @pytest.mark.parametrize("cfgkw", [
     dict(P=1, M=24, p=10, q=6, problem=4),          # single subdomain: classical ELM, G = 0
     dict(P=3, M=72, p=11, q=10, problem=2, tikhonov=1e-3),       # damped local LS (reading R29)
+    dict(P=1, M=24, p=10, q=6, problem=4, tikhonov=1e-2),        # damped classical ELM (ridge regression)
     dict(P=2, M=64, p=7, q=4, problem=4, tikhonov=1e-4),         # near-square (m = 65 < M + 32)
     dict(P=2, M=1024, p=45, q=8, problem=4, tikhonov=1e-4),      # ld 3104 > 3008: the tall (cluster) panel
     dict(P=2, M=40, p=9, q=6, problem=1),           # M not a multiple of the 64-panel, odd p
