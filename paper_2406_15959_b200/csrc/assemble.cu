@@ -417,10 +417,12 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
     }
 }
 
+// one warp per point: lane l sums neurons l, l + 32, ...; fixed-order butterfly reduction
 __global__ void k_evaluate(elmddm_config cfg, const double* __restrict__ W, const double* __restrict__ b,
                            const double* __restrict__ coef, const double* __restrict__ xy, int64_t n,
                            double* __restrict__ u) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (t >= n) return;
     const int P = cfg.P, M = cfg.M;
     double x = xy[2 * t], y = xy[2 * t + 1];
@@ -434,8 +436,10 @@ __global__ void k_evaluate(elmddm_config cfg, const double* __restrict__ W, cons
     const double* bs = b + (int64_t)sl * M;
     const double* cs = coef + (int64_t)sl * M;
     double acc = 0.0;
-    for (int k = 0; k < M; ++k) acc += cs[k] * tanh(Ws[2 * k] * x + Ws[2 * k + 1] * y + bs[k]);
-    u[t] = acc;
+    for (int k = lane; k < M; k += 32) acc += cs[k] * tanh(Ws[2 * k] * x + Ws[2 * k + 1] * y + bs[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) u[t] = acc;
 }
 
 }  // namespace
@@ -476,8 +480,8 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
 cudaError_t launch_evaluate(const elmddm_ctx* c, const double* W, const double* b, const double* coef,
                             const double* xy, int64_t n, double* u, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    int nt = 128;
+    const int nt = 256;  // 8 points per CTA, one warp each
     KTimer kt(c, ELMDDM_K_EVAL, st);
-    k_evaluate<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, coef, xy, n, u);
+    k_evaluate<<<(unsigned)((n * 32 + nt - 1) / nt), nt, 0, st>>>(c->cfg, W, b, coef, xy, n, u);
     return cudaGetLastError();
 }
