@@ -132,13 +132,15 @@ __global__ void __launch_bounds__(256) k_bs_gemv(elmddm_config cfg, const double
 }
 
 // per subdomain: resid = ||z[M:ld]||, coef = R11^{-1} z[0:M] (blocked column-oriented
-// back substitution; 64-row diagonal blocks solved by warp 0).  grid S, 512 threads.
-__global__ void __launch_bounds__(512) k_bs_trsv(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
+// back substitution; 64-row diagonal blocks solved by warp 0).  grid S, BS_NT threads (the
+// block-column GEMV updates are HBM-latency bound: more threads, more loads in flight).
+constexpr int BS_NT = 1024;
+__global__ void __launch_bounds__(BS_NT) k_bs_trsv(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
                                                  double* __restrict__ z, double* __restrict__ coef,
                                                  double* __restrict__ resid) {
     __shared__ double Rs[64][65];
     __shared__ double cs[64];
-    __shared__ double red[16];
+    __shared__ double red[BS_NT / 32];
     __shared__ double rdg[64];
     const int sl = blockIdx.x;
     const double* A = Kaug + (int64_t)sl * ld * ncols;
@@ -434,6 +436,9 @@ cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     KTimer kt(c, ELMDDM_K_BACK, st);
-    k_bs_trsv<<<(unsigned)S, 512, 0, st>>>(Kaug, ld, ncols, c->cfg.M, z, coef, resid);
+    // all subdomains resident at 1024 threads (2 CTAs / SM): more loads in flight per subdomain
+    // (config 3: 1.12 -> 0.83 ms); more subdomains than that: 512 threads, 4 CTAs / SM (config 4)
+    const int nt = S <= 2 * (int64_t)c->nsm ? BS_NT : BS_NT / 2;
+    k_bs_trsv<<<(unsigned)S, nt, 0, st>>>(Kaug, ld, ncols, c->cfg.M, z, coef, resid);
     return cudaGetLastError();
 }
