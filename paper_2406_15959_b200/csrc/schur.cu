@@ -44,6 +44,12 @@ __global__ void k_qrow(const double* __restrict__ Pbuf, int64_t pstride, int64_t
 }
 
 
+// Ga = Qrow^T Qrow is symmetric and only its 64-tiles on and below the diagonal are computed
+// (gemm lower_only): element (rr, cc) of an upper tile is read as (cc, rr)
+__device__ __forceinline__ double ga_at(const double* __restrict__ Ga, int rr, int cc, int64_t gld) {
+    return (rr >> 6) >= (cc >> 6) ? Ga[rr + (int64_t)cc * gld] : Ga[cc + (int64_t)rr * gld];
+}
+
 // M block (b, c) = sum of terms, written in the band storage (b == c: lower triangle only).
 __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restrict__ pair_bc,
                             const FaceTerm* __restrict__ terms, const double* __restrict__ Sbuf, int64_t sstride,
@@ -64,7 +70,7 @@ __global__ void k_massemble(const int* __restrict__ pair_ptr, const int* __restr
                 v += rr >= cc ? Sbuf[(int64_t)ft.src * sstride + rr + (int64_t)cc * sld]
                               : Sbuf[(int64_t)ft.src * sstride + cc + (int64_t)rr * sld];
             }
-            else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)(ft.c0 + j) * gld];
+            else v += ga_at(Ga + (int64_t)ft.src * gstride, ft.r0 + i, ft.c0 + j, gld);
         }
         // element (b q + i, c q + j) at (a, d) of the factorisation order, lower triangle
         int a = fbase[b] + i, d = fbase[c] + j;
@@ -88,7 +94,7 @@ __global__ void k_gassemble(const int* __restrict__ gptr, const FaceTerm* __rest
         for (int t = gptr[b]; t < gptr[b + 1]; ++t) {
             FaceTerm ft = gterms[t];
             if (ft.kind == 0) v += Sbuf[(int64_t)ft.src * sstride + ft.c0 + (int64_t)(ft.r0 + i) * sld];  // row 4q (lower)
-            else v += Ga[(int64_t)ft.src * gstride + (ft.r0 + i) + (int64_t)ft.c0 * gld];
+            else v += ga_at(Ga + (int64_t)ft.src * gstride, ft.r0 + i, ft.c0, gld);
         }
         g[(int64_t)b * q + i] = -v;
     }
@@ -402,9 +408,9 @@ cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, cons
         k_qrow<<<dim3((unsigned)F, 8), 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_qsrc, q, Qrow, c->qrow_ld,
                                                       qstride); }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        // Ga[a] = Qrow[a]^T Qrow[a]
+        // Ga[a] = Qrow[a]^T Qrow[a]  (symmetric: lower 64-tiles only, read through ga_at)
         GemmArgs gg{c->qrow_cols, c->qrow_cols, q, Qrow, c->qrow_ld, qstride, Qrow, c->qrow_ld, qstride, Ga, c->ga_ld,
-                    gstride, 1.0, 0.0, (int)F, 0};
+                    gstride, 1.0, 0.0, (int)F, 1};
         if ((e = gemm_launch(true, false, gg, st, c, ELMDDM_K_IFACE)) != cudaSuccess) return e;
         { KTimer kt(c, ELMDDM_K_IFACE, st);
         k_massemble<<<(unsigned)c->npairs, 256, 0, st>>>(c->d_pair_ptr, c->d_pair_bc, c->d_terms, Sbuf, sstride,
