@@ -59,7 +59,10 @@ def lib():
         _lib.orc_cholesky.argtypes = [vp, i64, C.c_int]
         _lib.orc_cholesky.restype = C.c_int
         _lib.orc_chol_solve.argtypes = [vp, i64, vp]
-        _lib.orc_solve.argtypes = [P, vp, vp, C.c_int, vp, vp, vp, vp, i64, vp, vp, vp, vp]
+        _lib.orc_solve.argtypes = [P, vp, vp, C.c_int, vp, vp, vp, vp, i64, vp, vp, vp, vp, C.c_int]
+        _lib.orc_band_cholesky.argtypes = [vp, i64, i64, C.c_int]
+        _lib.orc_band_cholesky.restype = C.c_int
+        _lib.orc_band_chol_solve.argtypes = [vp, i64, i64, vp]
         _lib.orc_solve.restype = C.c_int
         _lib.orc_local_pieces.argtypes = [P, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         _lib.orc_local_pieces.restype = C.c_int
@@ -171,6 +174,21 @@ def chol_solve(L: np.ndarray, g):
     return x
 
 
+def band_cholesky(Bnd: np.ndarray, nthreads: int = 1):
+    """Plain banded Cholesky (oracle.c orc_band_cholesky) of the lower band Bnd[i, k - i + bw]
+    (row i holds columns i - bw .. i).  Returns (factor band, rc)."""
+    B = np.array(Bnd, dtype=np.float64, copy=True, order="C")
+    rc = lib().orc_band_cholesky(_p(B), B.shape[0], B.shape[1] - 1, nthreads)
+    return B, rc
+
+
+def band_chol_solve(B: np.ndarray, g):
+    Bc = np.ascontiguousarray(B)
+    x = np.array(g, dtype=np.float64, copy=True)
+    lib().orc_band_chol_solve(_p(Bc), Bc.shape[0], Bc.shape[1] - 1, _p(x))
+    return x
+
+
 def evaluate(c: Cfg, W, b, coef, xy):
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     u = np.zeros(xy.shape[0])
@@ -179,8 +197,10 @@ def evaluate(c: Cfg, W, b, coef, xy):
     return u
 
 
-def solve(c: Cfg, W, b, xy_eval=None, nthreads: int | None = None, want_system: bool = False):
-    """Algorithm 1 with the oracle's literal eqn:schur route."""
+def solve(c: Cfg, W, b, xy_eval=None, nthreads: int | None = None, want_system: bool = False, band: int = 0):
+    """Algorithm 1 with the oracle's literal eqn:schur route.  band: interface
+    Cholesky 0 auto (banded in strip order when G > 20000), 1 dense, 2 banded (want_system:
+    dense route only)."""
     geo = geometry(c)
     G, N = geo["G"], geo["N"]
     if nthreads is None:
@@ -192,10 +212,13 @@ def solve(c: Cfg, W, b, xy_eval=None, nthreads: int | None = None, want_system: 
     n_eval = 0 if xy_eval is None else xy_eval.shape[0]
     xy_eval = None if xy_eval is None else np.ascontiguousarray(xy_eval, dtype=np.float64)
     u = np.zeros(max(n_eval, 1))
+    if want_system and band == 2:
+        raise ValueError("want_system needs the dense route")
     Mout = np.zeros((G, G)) if (want_system and G > 0) else None
     gout = np.zeros(G) if (want_system and G > 0) else None
     rc = lib().orc_solve(C.byref(c), _p(np.ascontiguousarray(W)), _p(np.ascontiguousarray(b)), nthreads,
-                         _p(uG), _p(coef), _p(resid), _p(xy_eval), n_eval, _p(u), _p(Mout), _p(gout), _p(times))
+                         _p(uG), _p(coef), _p(resid), _p(xy_eval), n_eval, _p(u), _p(Mout), _p(gout), _p(times),
+                         int(band))
     if rc != 0:
         raise RuntimeError(f"oracle solve failed rc={rc}")
     out = {"uG": uG[:G], "coef": coef, "resid": resid, "u": u[:n_eval],

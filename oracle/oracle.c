@@ -19,7 +19,8 @@
  *        A^s K^{s+} = (A^s R^{-1}) Q_1^T formed once:  B^T(I-KK^+)B, B^T(I-KK^+)F,
  *        AK^+B = sum_s (A^s K^{s+}) B^s,  AK^+F = sum_s (A^s K^{s+}) F^s
  *   6. M = B^T(I-KK^+)B + (AK^+B)^T(AK^+B),  g = B^T(I-KK^+)F + (AK^+B)^T(AK^+F)
- *   7. plain Cholesky (Crout, rows in parallel), forward/back substitution
+ *   7. plain Cholesky (Crout, rows in parallel), forward/back substitution: dense, or on the
+ *      band of the strip order (reading R14) for the large interfaces (configs 3-4)
  *   8. c^s = K^{s+}(F^s - B^s u_Gamma) (Alg. 1), r_s = ||(Q^T(F+E u_s))_{M:m}||
  *   9. u(x) = owner subdomain's network (reading R15)
  *
@@ -712,6 +713,102 @@ void orc_chol_solve(const double *L, int64_t G, double *x) {
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* plain BANDED Cholesky in strip order (reading R14)                     */
+/* ------------------------------------------------------------------------------------------ */
+/* In strip order the interface matrix M of eqn:schur is banded: S1 couples the faces
+ * of one subdomain, (AK^+B)^T(AK^+B) the faces of the two subdomains beside one flux face, and
+ * both lie within (4P-1)q - 1 unknowns of each other (reading R14).  Storage: the lower band,
+ * row-major, row i holding columns i-bw .. i at B[i*(bw+1) + (k - i + bw)] (entries left of
+ * column 0 are unused zeros).  The factorisation is the same Crout recurrence as orc_cholesky,
+ *     L_jj = sqrt(M_jj - sum_k L_jk^2),   L_ij = (M_ij - sum_k L_ik L_jk) / L_jj   (i > j),
+ * with the sums running over the band only (k >= i - bw): outside the band M and L are exactly
+ * zero, so the terms dropped are exact zeros.  Rows of a column are computed in parallel; every
+ * thread forms L_jj itself from finished data (one barrier per column).                       */
+typedef struct {
+    double *B;
+    int64_t G, bw;
+    int nthreads;
+    int bad;              /* 1 + first non-positive pivot column */
+    pthread_barrier_t bar;
+} bchol_ctx;
+
+typedef struct {
+    bchol_ctx *C;
+    int tid;
+} bchol_arg;
+
+static void *bchol_main(void *a_) {
+    bchol_arg *a = (bchol_arg *)a_;
+    bchol_ctx *C = a->C;
+    const int64_t G = C->G, bw = C->bw, w = bw + 1;
+    double *B = C->B;
+    for (int64_t j = 0; j < G; ++j) {
+        double *Lj = B + (size_t)j * w;              /* Lj[k - j + bw] = L_jk */
+        int64_t lo = j - bw > 0 ? j - bw : 0;
+        double s = Lj[bw];
+        for (int64_t k = lo; k < j; ++k) s -= Lj[k - j + bw] * Lj[k - j + bw];
+        if (!(s > 0.0)) {                            /* every thread sees the same pivot */
+            if (a->tid == 0) C->bad = (int)(1 + j);
+            return NULL;
+        }
+        double d = sqrt(s);
+        int64_t iend = j + bw < G - 1 ? j + bw : G - 1;
+        for (int64_t i = j + 1 + a->tid; i <= iend; i += C->nthreads) {
+            double *Li = B + (size_t)i * w;          /* Li[k - i + bw] = L_ik */
+            int64_t klo = i - bw > 0 ? i - bw : 0;
+            double t = Li[j - i + bw];
+            for (int64_t k = klo; k < j; ++k) t -= Li[k - i + bw] * Lj[k - j + bw];
+            Li[j - i + bw] = t / d;
+        }
+        pthread_barrier_wait(&C->bar);               /* column j done; every thread has read M_jj */
+        if (a->tid == 0) Lj[bw] = d;                 /* column j+1 never reads L_jj */
+    }
+    return NULL;
+}
+
+/* returns 0 on success, 1 + column of the first non-positive pivot otherwise */
+int orc_band_cholesky(double *B, int64_t G, int64_t bw, int nthreads) {
+    bchol_ctx C;
+    C.B = B;
+    C.G = G;
+    C.bw = bw;
+    C.nthreads = nthreads < 1 ? 1 : nthreads;
+    C.bad = 0;
+    pthread_barrier_init(&C.bar, NULL, (unsigned)C.nthreads);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)C.nthreads);
+    bchol_arg *args = (bchol_arg *)malloc(sizeof(bchol_arg) * (size_t)C.nthreads);
+    for (int t = 0; t < C.nthreads; ++t) {
+        args[t].C = &C;
+        args[t].tid = t;
+        if (t > 0) pthread_create(&th[t], NULL, bchol_main, &args[t]);
+    }
+    bchol_main(&args[0]);
+    for (int t = 1; t < C.nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_barrier_destroy(&C.bar);
+    free(th);
+    free(args);
+    return C.bad;
+}
+
+/* L y = g, then L^T x = y, on the band factor (in place on x) */
+void orc_band_chol_solve(const double *B, int64_t G, int64_t bw, double *x) {
+    const int64_t w = bw + 1;
+    for (int64_t i = 0; i < G; ++i) {
+        const double *Li = B + (size_t)i * w;
+        int64_t lo = i - bw > 0 ? i - bw : 0;
+        double s = x[i];
+        for (int64_t k = lo; k < i; ++k) s -= Li[k - i + bw] * x[k];
+        x[i] = s / Li[bw];
+    }
+    for (int64_t i = G - 1; i >= 0; --i) {
+        int64_t hi = i + bw < G - 1 ? i + bw : G - 1;
+        double s = x[i];
+        for (int64_t k = i + 1; k <= hi; ++k) s -= B[(size_t)k * w + (i - k + bw)] * x[k];
+        x[i] = s / B[(size_t)i * w + bw];
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* the whole method (Algorithm 1)                                                   */
 /* ------------------------------------------------------------------------------------------ */
 typedef struct {
@@ -733,22 +830,196 @@ static void job_back(void *ctx_, int s, int tid) {
     local_back(&X->L[s], X->uG, X->coef + (size_t)s * X->c->M, &X->resid[s]);
 }
 
+/* Steps 5-7 on the band (reading R14 strip order, half-bandwidth bw = (4P-1)q - 1): the same
+ * sums as the dense route below, element by element in the same order (S1 blocks in ascending s,
+ * then the rows a of AK^+B in ascending a), stored as the lower band.  Row a of AK^+B is
+ * sum_s (A^s K^{s+}) B^s restricted to flux row a: the PB rows of the two subdomains beside the
+ * face of a, added in ascending s into a zeroed window a-bw .. a+bw.  Returns 0, 2 on a
+ * non-positive pivot, 3 if an entry falls outside the band (a geometry error).                 */
+typedef struct {
+    const orc_local *L;
+    int N;
+    int64_t G, bw;
+    const int32_t *own_s, *own_k;   /* [G][2] contributors (s ascending; -1 = none) */
+    int32_t *qnz;                   /* [G][qcap] column indices of row a of AK^+B */
+    double *qval;                   /* [G][qcap] values */
+    int32_t *qn;                    /* [G] count */
+    int qcap;
+    int bad;
+} qrow_ctx;
+
+static void job_qrow(void *ctx_, int a, int tid) {
+    (void)tid;
+    qrow_ctx *Q = (qrow_ctx *)ctx_;
+    int64_t bw = Q->bw, G = Q->G;
+    double *win = (double *)calloc((size_t)(2 * bw + 1), sizeof(double));
+    int64_t lo = G, hi = -1;
+    for (int t = 0; t < 2; ++t) {
+        int s = Q->own_s[2 * a + t];
+        if (s < 0) continue;
+        const orc_local *Ls = &Q->L[s];
+        int k = Q->own_k[2 * a + t];
+        for (int l = 0; l < Ls->mg; ++l) {
+            int64_t gl = Ls->ig[l];
+            if (gl < a - bw || gl > a + bw) { Q->bad = 1; continue; }
+            win[gl - a + bw] += Ls->PB[(size_t)k * Ls->mg + l];
+            if (gl < lo) lo = gl;
+            if (gl > hi) hi = gl;
+        }
+    }
+    int n = 0;
+    for (int64_t gl = lo; gl <= hi; ++gl) {
+        double v = win[gl - a + bw];
+        if (v != 0.0) {
+            if (n >= Q->qcap) { Q->bad = 1; break; }
+            Q->qnz[(size_t)a * Q->qcap + n] = (int32_t)gl;
+            Q->qval[(size_t)a * Q->qcap + n] = v;
+            ++n;
+        }
+    }
+    Q->qn[a] = n;
+    free(win);
+}
+
+typedef struct {
+    const qrow_ctx *Q;
+    double *Mb, *g;
+    const double *qg;
+    int nthreads;
+} qtq_ctx;
+
+/* thread t owns the band rows kx with kx % nthreads == t and adds every row a's terms to them in
+ * ascending a -- the dense route's order for each element */
+static void job_qtq(void *ctx_, int t, int tid) {
+    (void)tid;
+    qtq_ctx *X = (qtq_ctx *)ctx_;
+    const qrow_ctx *Q = X->Q;
+    int64_t bw = Q->bw, w = bw + 1;
+    for (int64_t a = 0; a < Q->G; ++a) {
+        const int32_t *nz = Q->qnz + (size_t)a * Q->qcap;
+        const double *v = Q->qval + (size_t)a * Q->qcap;
+        int n = Q->qn[a];
+        for (int x = 0; x < n; ++x) {
+            int64_t kx = nz[x];
+            if (kx % X->nthreads != t) continue;
+            double rx = v[x];
+            X->g[kx] += rx * X->qg[a];
+            double *Mk = X->Mb + (size_t)kx * w;
+            for (int y = 0; y < n; ++y) {
+                int64_t ky = nz[y];
+                if (ky <= kx) Mk[ky - kx + bw] += rx * v[y];
+            }
+        }
+    }
+}
+
+static int iface_band(const orc_cfg *c, const orc_local *L, int N, int64_t G, int nthreads, double *uG,
+                      double *tas, double *tsol) {
+    double t0 = now_s();
+    int64_t bw = (int64_t)(4 * c->P - 1) * c->q - 1;
+    if (bw > G - 1) bw = G - 1;
+    int64_t w = bw + 1;
+    double *Mb = (double *)calloc((size_t)G * (size_t)w, sizeof(double));
+    double *g = (double *)calloc((size_t)G, sizeof(double));
+    double *qg = (double *)calloc((size_t)G, sizeof(double));
+    int32_t *own_s = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)G);
+    int32_t *own_k = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)G);
+    int bad = 0;
+    if (!Mb || !g || !qg || !own_s || !own_k) return 4;
+    for (int64_t a = 0; a < 2 * G; ++a) own_s[a] = own_k[a] = -1;
+    for (int s = 0; s < N; ++s) {
+        const orc_local *Ls = &L[s];
+        for (int k = 0; k < Ls->mg; ++k) {
+            int64_t gk = Ls->ig[k];
+            g[gk] += Ls->g1[k];
+            qg[gk] += Ls->pF[k];
+            int slot = own_s[2 * gk] < 0 ? 0 : 1;
+            own_s[2 * gk + slot] = s;
+            own_k[2 * gk + slot] = k;
+            double *Mk = Mb + (size_t)gk * w;
+            for (int l = 0; l < Ls->mg; ++l) {
+                int64_t gl = Ls->ig[l];
+                if (gl > gk) continue;
+                if (gk - gl > bw) { bad = 1; continue; }
+                Mk[gl - gk + bw] += Ls->S1[(size_t)k * Ls->mg + l];
+            }
+        }
+    }
+    qrow_ctx Q;
+    Q.L = L;
+    Q.N = N;
+    Q.G = G;
+    Q.bw = bw;
+    Q.own_s = own_s;
+    Q.own_k = own_k;
+    Q.qcap = 8 * c->q;
+    Q.qnz = (int32_t *)malloc(sizeof(int32_t) * (size_t)G * Q.qcap);
+    Q.qval = (double *)malloc(sizeof(double) * (size_t)G * Q.qcap);
+    Q.qn = (int32_t *)calloc((size_t)G, sizeof(int32_t));
+    Q.bad = 0;
+    if (!Q.qnz || !Q.qval || !Q.qn) return 4;
+    run_parallel((int)G, nthreads, job_qrow, &Q);
+    qtq_ctx X = {&Q, Mb, g, qg, nthreads < 1 ? 1 : nthreads};
+    run_parallel(X.nthreads, X.nthreads, job_qtq, &X);
+    free(Q.qnz);
+    free(Q.qval);
+    free(Q.qn);
+    free(own_s);
+    free(own_k);
+    free(qg);
+    double t1 = now_s();
+    int rc = 0;
+    if (bad || Q.bad) rc = 3;
+    else if (orc_band_cholesky(Mb, G, bw, nthreads) != 0) rc = 2;
+    else {
+        memcpy(uG, g, sizeof(double) * (size_t)G);
+        orc_band_chol_solve(Mb, G, bw, uG);
+    }
+    free(Mb);
+    free(g);
+    *tas = t1 - t0;
+    *tsol = now_s() - t1;
+    return rc;
+}
+
 /* times[0] local (assemble+QR+Schur pieces), [1] interface assembly, [2] Cholesky+solve,
- * [3] back-solve, [4] evaluate.  Mout (G x G row-major, full symmetric) and gout optional.
- * Returns 0 ok, 2 if Cholesky hit a non-positive pivot, 1 if G too large for dense storage.  */
+ * [3] back-solve, [4] evaluate.  Mout (G x G row-major, full symmetric) and gout optional
+ * (dense route only).  band: 0 auto (band if G > 20000), 1 dense, 2 band.
+ * Returns 0 ok, 2 if Cholesky hit a non-positive pivot, 1 if G too large for dense storage,
+ * 3 band geometry error, 4 out of memory.                                                     */
 int orc_solve(const orc_cfg *c, const double *W, const double *b, int nthreads, double *uG,
               double *coef, double *resid, const double *xy_eval, int64_t n_eval, double *u_eval,
-              double *Mout, double *gout, double *times) {
+              double *Mout, double *gout, double *times, int band) {
     int64_t geo[4];
     orc_geometry(c, geo);
     int64_t G = geo[1];
     int N = (int)geo[3];
-    if (G > 20000) return 1;
+    if (band == 0) band = G > 20000 ? 2 : 1;
+    if (band == 1 && G > 20000) return 1;
     double t0 = now_s();
     orc_local *L = (orc_local *)calloc((size_t)N, sizeof(orc_local));
     solve_ctx X = {c, W, b, L, uG, coef, resid};
     run_parallel(N, nthreads, job_local, &X);
     double t1 = now_s();
+    if (band == 2) {
+        double tas = 0.0, tsol = 0.0;
+        int rc = G > 0 ? iface_band(c, L, N, G, nthreads, uG, &tas, &tsol) : 0;
+        double t3 = now_s();
+        if (rc == 0) run_parallel(N, nthreads, job_back, &X);
+        double t4 = now_s();
+        if (rc == 0 && xy_eval && n_eval > 0) orc_evaluate(c, W, b, coef, xy_eval, n_eval, u_eval);
+        double t5 = now_s();
+        if (times) {
+            times[0] = t1 - t0;
+            times[1] = tas;
+            times[2] = tsol;
+            times[3] = t4 - t3;
+            times[4] = t5 - t4;
+        }
+        for (int s = 0; s < N; ++s) local_free(&L[s]);
+        free(L);
+        return rc;
+    }
 
     /* global pieces: sum in ascending s (step 5-6 of SURVEY §8(c)) */
     double *Mm = (double *)calloc((size_t)(G > 0 ? G : 1) * (G > 0 ? G : 1), sizeof(double));

@@ -276,7 +276,66 @@ def test_cholesky_pins():
     assert rc == 6                        # 1 + column of the first non-positive pivot
 
 
+def _to_band(S, bw):
+    n = S.shape[0]
+    B = np.zeros((n, bw + 1))
+    for i in range(n):
+        lo = max(0, i - bw)
+        B[i, lo - i + bw:] = S[i, lo:i + 1]
+    return B
+
+
+def test_band_cholesky_pins():
+    """Banded Cholesky against numpy's dense Cholesky and solve on a random
+    SPD band matrix; a non-positive pivot is reported by its column; threads do not change it."""
+    rng = np.random.default_rng(11)
+    n, bw = 240, 17
+    X = rng.standard_normal((n, n))
+    S = np.triu(np.tril(X @ X.T, bw), -bw) + 4.0 * bw * np.eye(n)     # banded, diagonally dominant
+    B, rc = O.band_cholesky(_to_band(S, bw), nthreads=3)
+    assert rc == 0
+    Lref = np.linalg.cholesky(S)
+    assert np.allclose(_to_band(Lref, bw), B, rtol=0, atol=1e-12 * np.abs(Lref).max())
+    bb = rng.standard_normal(n)
+    assert np.allclose(O.band_chol_solve(B, bb), np.linalg.solve(S, bb), rtol=1e-10)
+    B1, _ = O.band_cholesky(_to_band(S, bw), nthreads=1)
+    assert np.array_equal(B1, B)
+    S2 = S.copy()
+    S2[37, 37] = -1.0
+    _, rc = O.band_cholesky(_to_band(S2, bw), nthreads=4)
+    assert rc == 38
+
+
+@pytest.mark.parametrize("P,q", [(3, 4), (4, 3), (5, 2)])
+def test_strip_order_half_bandwidth(P, q):
+    """Reading R14: in strip order the interface matrix M of eqn:schur has half-bandwidth
+    (4P-1)q-1 -- the band the oracle's banded route stores (a narrower band would drop entries).
+    It is attained from P = 4 on (the flux rows of a horizontal face H(i, j) couple H(i, j-1) with
+    H(i, j+1), two strips apart, which needs 1 <= j <= P-3); below, it is an upper bound."""
+    c = mkcfg(P=P, M=24, p=6, q=q, problem=2)
+    W, b, _, _ = O.init_hidden(c)
+    r = O.solve(c, W, b, want_system=True, band=1)
+    i, j = np.nonzero(r["M"])
+    hbw = int(np.abs(i - j).max())
+    assert hbw == (4 * P - 1) * q - 1 if P >= 4 else hbw <= (4 * P - 1) * q - 1
+
+
+@pytest.mark.parametrize("kw", [dict(k=1), dict(P=3, M=40, p=8, q=6, problem=1), dict(P=5, M=24, p=6, q=3, problem=2)])
+def test_band_route_equals_dense_route(kw):
+    """The banded interface route (used for configs 3-4) gives bit-identical u_Gamma, c, r_s and u
+    to the dense route on the same problem: M's entries are summed in the same order and the
+    terms the band leaves out of the Cholesky sums are exact zeros."""
+    c = mkcfg(**kw)
+    W, b, _, _ = O.init_hidden(c)
+    xy = WL.eval_grid(21)
+    r1 = O.solve(c, W, b, xy, band=1)
+    r2 = O.solve(c, W, b, xy, band=2)
+    for key in ("uG", "coef", "resid", "u"):
+        assert np.array_equal(r1[key], r2[key]), key
+
+
 # ------------------------------------------------------------------------------------------------
+# Schur system (eqn:eliminated P:351-373, LS_system P:398-406, eqn:schur P:407-410)# ------------------------------------------------------------------------------------------------
 # Schur system (eqn:eliminated P:351-373, LS_system P:398-406, eqn:schur P:407-410)
 # ------------------------------------------------------------------------------------------------
 def _global_blocks(c, W, b):
