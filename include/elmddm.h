@@ -28,7 +28,10 @@
  *  - Errors: arguments are validated synchronously before any launch (ELMDDM_EINVAL, nothing
  *    enqueued).  Numerical failures detected on the device (non-positive Cholesky pivot,
  *    non-finite value) set a device status word, reported by elmddm_sync and by the return of
- *    elmddm_interface_factor_solve (which synchronises its stream); elmddm_last_error gives text.
+ *    elmddm_interface_solve (which synchronises its stream); elmddm_last_error gives text.  The
+ *    per-phase calls, elmddm_interface_factor_solve included, never synchronise, so a whole
+ *    solve can be enqueued back to back (and captured in a CUDA graph) with one elmddm_sync at
+ *    the end.
  *  - Threading: one context per device per host thread.
  */
 #ifndef ELMDDM_H
@@ -51,7 +54,7 @@ typedef enum {
                             sigma_min/sigma_max < 1e-14"): some subdomain's R11 has
                             min|R11_ii| < 1e-14 max|R11_ii| (which implies sigma_min/sigma_max <
                             1e-14 for K^s); every output is still computed.  Reported once by the
-                            next elmddm_sync / elmddm_interface_factor_solve, subdomain in
+                            next elmddm_sync / elmddm_interface_solve, subdomain in
                             elmddm_last_error.  Expected for the BASELINE configs >= 1: ELM
                             collocation matrices are numerically rank deficient (reading R11). */
 } elmddm_status;
@@ -199,8 +202,8 @@ elmddm_status elmddm_interface_assemble(elmddm_ctx* ctx, const double* Pbuf, con
  * tiles of L, nested dissection by default -- see elmddm_chol_plan; one persistent left-looking
  * kernel over a list-scheduled task order) and u = M^{-1} g into uG[G_pad] (strip order).  On
  * return the tiles of Mband hold L (diagonal tiles: L(J,J), lower triangular).  g is not
- * modified.  Synchronises `stream`; returns ELMDDM_ENUMERIC on a non-positive pivot (or a
- * dependency wait exceeding 10 s), else the pending ELMDDM_WRANK warning if any.                                                             */
+ * modified.  Asynchronous: a non-positive pivot (or a dependency wait exceeding 10 s) sets the
+ * device status word, reported as ELMDDM_ENUMERIC by the next elmddm_sync.                                                             */
 elmddm_status elmddm_interface_factor_solve(elmddm_ctx* ctx, double* Mband, const double* g, double* uG,
                                             double* work, void* stream);
 /* The paper's interface solver: unpreconditioned conjugate gradients on
@@ -241,7 +244,8 @@ elmddm_status elmddm_dist_handshake(elmddm_ctx* ctx, int32_t phase, int32_t* ok)
  * copied).                                                                                     */
 elmddm_status elmddm_debug_dist_emulate(elmddm_ctx* ctx, int32_t nrep, const double* Mband, const double* g,
                                         double* uG, double* work, int64_t* ndiff, void* stream);
-/* = interface_assemble + interface_factor_solve. */
+/* = interface_assemble + interface_factor_solve + elmddm_sync(stream): returns ELMDDM_ENUMERIC
+ * on a non-positive pivot, else the pending ELMDDM_WRANK warning if any. */
 elmddm_status elmddm_interface_solve(elmddm_ctx* ctx, const double* Pbuf, const double* Sbuf, double* Mband,
                                      double* g, double* uG, double* work, void* stream);
 

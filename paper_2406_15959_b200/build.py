@@ -31,14 +31,19 @@ def build(force: bool = False, verbose: bool = False, extra=(), lib: str = LIB) 
     profiling variant built to another file name)."""
     if not force and lib == LIB and not needs_build():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
+    objs, cmds = [], []
     for src in sources():
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
-        if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        cmds.append([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj])
         objs.append(obj)
+    if verbose:
+        for cmd in cmds:
+            print(" ".join(cmd), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.check_call, cmd) for cmd in cmds]:
+            f.result()
     cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
     subprocess.check_call(cmd)
     for o in objs:

@@ -805,7 +805,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     const bool dist = ds.nrep > 1;
     if (dist) {
         const int nrep = ds.nrep;
-        const int epoch = ++c->chol_epoch;
+        const int epoch = ++c->dist.epoch;
         int grid = grid_ll, per = grid_ll;
         if (ds.emulate) {
             per = grid_ll / nrep;

@@ -518,8 +518,8 @@ elmddm_status elmddm_dist_import(elmddm_ctx* c, int32_t rank, int32_t world, con
         c->dist.counter = nullptr;
         return ELMDDM_OK;
     }
-    if (world < 2 || rank < 0 || rank >= world || !handles || !c->dist.region) {
-        c->err = "elmddm_dist_import: need world >= 2, 0 <= rank < world, handles, and elmddm_dist_export first";
+    if (world < 2 || world > 64 || rank < 0 || rank >= world || !handles || !c->dist.region) {
+        c->err = "elmddm_dist_import: need 2 <= world <= 64, 0 <= rank < world, handles, and elmddm_dist_export first";
         return ELMDDM_EINVAL;
     }
     DeviceGuard dg(c->device);
@@ -560,6 +560,15 @@ elmddm_status elmddm_dist_import(elmddm_ctx* c, int32_t rank, int32_t world, con
             return cuda_fail(c, e, "elmddm_dist_import");
         }
     }
+    // every rank starts the shared protocol from the same state: epoch 0 and cleared tile flags,
+    // column counters and task counters in its own region (each rank clears its own; the
+    // collective handshake that follows import orders this before any peer's first push)
+    if ((e = cudaMemset(static_cast<char*>(c->dist.region) + L.flags, 0, L.hshake - L.flags)) != cudaSuccess) {
+        for (void* pr : opened) cudaIpcCloseMemHandle(pr);
+        cudaFree(d);
+        return cuda_fail(c, e, "elmddm_dist_import");
+    }
+    c->dist.epoch = 0;
     for (void* pr : c->dist.opened) cudaIpcCloseMemHandle(pr);
     cudaFree(c->dist.d_reps);
     c->dist.opened = opened;
@@ -844,8 +853,7 @@ elmddm_status elmddm_interface_factor_solve(elmddm_ctx* c, double* Mband, const 
     CHECK_PTR(c, work);
     DeviceGuard dg(c->device);
     cudaError_t e = run_cholesky_solve(c, Mband, g, uG, work, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(c, e, "elmddm_interface_factor_solve");
-    return elmddm_sync(c, stream);
+    return e == cudaSuccess ? ELMDDM_OK : cuda_fail(c, e, "elmddm_interface_factor_solve");
 }
 
 elmddm_status elmddm_interface_cg(elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
@@ -878,7 +886,9 @@ elmddm_status elmddm_interface_solve(elmddm_ctx* c, const double* Pbuf, const do
                                      double* uG, double* work, void* stream) {
     elmddm_status s = elmddm_interface_assemble(c, Pbuf, Sbuf, Mband, g, work, stream);
     if (s != ELMDDM_OK) return s;
-    return elmddm_interface_factor_solve(c, Mband, g, uG, work, stream);
+    s = elmddm_interface_factor_solve(c, Mband, g, uG, work, stream);
+    if (s != ELMDDM_OK) return s;
+    return elmddm_sync(c, stream);
 }
 
 elmddm_status elmddm_back_solve(elmddm_ctx* c, const double* Kaug, const double* uG, double* coef, double* resid,

@@ -151,6 +151,17 @@ __global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
     }
 }
 
+// C = beta C for an empty contraction (K = 0), column-major, batched; 8 columns per CTA.
+__global__ void k_scale_c(int M, int N, double* C, int64_t ldc, int64_t sC, double beta, int lower_only) {
+    double* Cb = C + (int64_t)blockIdx.y * sC;
+    for (int j = blockIdx.x * 8 + threadIdx.x / 32; j < min(N, (int)blockIdx.x * 8 + 8); j += 8)
+        for (int i = threadIdx.x % 32; i < M; i += 32) {
+            if (lower_only && i / 64 < j / 64) continue;
+            double* cp = Cb + i + (int64_t)j * ldc;
+            *cp = beta == 0.0 ? 0.0 : beta * *cp;
+        }
+}
+
 template <bool TA, bool TB>
 cudaError_t launch(const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c, int cls) {
     // (a per-device attribute: set on every launch, a few microseconds of host time)
@@ -167,9 +178,11 @@ cudaError_t launch(const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c, int 
 cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st, const elmddm_ctx* c,
                         int cls) {
     if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-    if (g.K <= 0) {
-        // C = beta C (only used with beta = 1 in this library)
-        return cudaSuccess;
+    if (g.K <= 0) {  // empty contraction: C = beta C (beta = 0 writes zeros, even over NaN)
+        if (g.beta == 1.0) return cudaSuccess;
+        dim3 grid((g.N + 7) / 8, g.batch);
+        k_scale_c<<<grid, 256, 0, st>>>(g.M, g.N, g.C, g.ldc, g.sC, g.beta, g.lower_only);
+        return cudaGetLastError();
     }
     if (transA) return transB ? launch<true, true>(g, st, c, cls) : launch<true, false>(g, st, c, cls);
     return transB ? launch<false, true>(g, st, c, cls) : launch<false, false>(g, st, c, cls);

@@ -63,6 +63,7 @@ struct CholRep {
 // imported with CUDA IPC); one-GPU emulation keeps all replicas in this process.
 struct DistState {
     int nrep = 1, rank = 0;
+    int epoch = 0;               // factorisation epoch of the shared protocol (agreed: reset at import)
     bool emulate = false;
     std::vector<CholRep> reps;   // host copy of the table
     CholRep* d_reps = nullptr;   // device table [nrep]

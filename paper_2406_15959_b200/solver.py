@@ -2,9 +2,9 @@
 torch.distributed (NCCL) for the two exchange steps of Algorithm 1.
 
     rank r:  init_hidden -> assemble -> local_factor -> schur_accumulate        (own subdomains)
-             reduce(Pbuf, Sbuf) to rank 0                                        (NCCL, NVLink)
+             gather(Pbuf, Sbuf slabs) to rank 0                                  (NCCL, NVLink)
     rank 0:  interface_solve  (eqn:schur)
-             broadcast(u_Gamma)                                                  (NCCL)
+             broadcast(status, u_Gamma)                                          (NCCL)
     rank r:  back_solve -> evaluate                                              (own subdomains)
 
 The wrappers below do argument marshalling only; every arithmetic step runs in libelmddm.so.
@@ -38,8 +38,14 @@ def _stream(stream):
 
 
 def partition(N: int, world: int, rank: int):
-    """Contiguous row-major slab of subdomains for `rank`: ceil(N/world) each."""
-    per = -(-N // world)
+    """Contiguous row-major slab of subdomains for `rank`: ceil(N/world) each.
+    Every rank must own at least one subdomain: with slabs of ceil(N/world) that needs
+    (world - 1) * ceil(N/world) < N (e.g. world <= N for the BASELINE configs' power-of-two
+    counts); otherwise every rank raises the same error before any collective."""
+    per = -(-N // world) if world >= 1 else 0
+    if world < 1 or (world - 1) * per >= N:
+        raise _lib.ElmddmError(f"{world} ranks for {N} subdomains in slabs of {per}: some rank would own no "
+                               f"subdomain (need (world - 1) * ceil(N / world) < N, so world <= N at least)")
     s0 = min(N, rank * per)
     s1 = min(N, s0 + per)
     return s0, s1
@@ -123,6 +129,43 @@ class Context:
             raise _lib.ElmddmError(f"{what}: {_lib.STATUS.get(rc, rc)}: {msg.decode() if msg else ''}")
 
     # ---- buffers ---------------------------------------------------------------------------
+    def _slot_elems(self, key: str) -> int:
+        """Doubles per subdomain slot of the global Schur buffers (include/elmddm.h sizes)."""
+        N = self.prob.P * self.prob.P
+        return self.sizes["pbuf_elems" if key == "Pbuf" else "sbuf_elems"] // N
+
+    def _padded_slots(self, world: int | None = None) -> int:
+        import torch.distributed as dist
+
+        if world is None:
+            world = dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+        N = self.prob.P * self.prob.P
+        return -(-N // world) * world
+
+    def _gather_slots(self, t, key: str, world: int, rank: int, to_all: bool, group=None):
+        """Exchange step of Algorithm 1: every subdomain slot of the global buffer has
+        exactly ONE writer (its owner), so the exchange is a gather of the slabs -- no arithmetic,
+        bit-identical for any rank count.  to_all: every rank receives every slab (all_gather,
+        the multi-rank factorisation); else only rank 0 (gather, the rank-0 interface solve)."""
+        import torch.distributed as dist
+
+        N = self.prob.P * self.prob.P
+        per = -(-N // world)
+        slot = self._slot_elems(key)
+        need = per * world * slot
+        full = t if t.numel() >= need else torch.cat([t[: N * slot], t.new_zeros(need - N * slot)])
+        chunks = list(full[:need].view(world, per * slot).unbind(0))
+        nccl = dist.get_backend(group) == "nccl"
+        mine = chunks[rank] if nccl else chunks[rank].clone()
+        if to_all and nccl:  # in place: the input is this rank's slab of the output
+            dist.all_gather_into_tensor(full[:need], mine, group=group)
+        elif to_all:
+            dist.all_gather(chunks, mine, group=group)
+        else:
+            dist.gather(mine, gather_list=chunks if rank == 0 else None, dst=0, group=group)
+        if full is not t:
+            t[: N * slot].copy_(full[: N * slot])
+
     def alloc(self) -> dict:
         z, M = self.sizes, self.prob.M
         dev = torch.device("cuda", self.device)
@@ -132,7 +175,10 @@ class Context:
             "W": torch.empty(S * M * 2, **f), "b": torch.empty(S * M, **f), "xi": torch.empty(S * M * 2, **f),
             "Kaug": torch.empty(z["kaug_elems"], **f), "At": torch.empty(z["at_elems"], **f),
             "tau": torch.empty(z["tau_elems"], **f), "work": torch.empty(max(z["work_elems"], 2), **f),
-            "Pbuf": torch.zeros(z["pbuf_elems"], **f), "Sbuf": torch.zeros(z["sbuf_elems"], **f),
+            # padded to whole slabs of ceil(N / world) slots so the multi-rank gather is one
+            # equal-count collective (the padding slots stay zero and are never read)
+            "Pbuf": torch.zeros(self._slot_elems("Pbuf") * self._padded_slots(), **f),
+            "Sbuf": torch.zeros(self._slot_elems("Sbuf") * self._padded_slots(), **f),
             "Mband": torch.empty(max(z["band_elems"], 2), **f), "g": torch.empty(z["G_pad"], **f),
             "uG": torch.zeros(z["G_pad"], **f), "coef": torch.empty(S * M, **f), "resid": torch.empty(S, **f),
         }
@@ -257,15 +303,17 @@ class Context:
     def dist_setup(self, group=None) -> bool:
         """Collectively switch this context to the multi-rank interface factorisation: every
         rank exports its replica region, the CUDA IPC handles are all-gathered, every rank opens
-        the others'.  All ranks agree on the outcome; on any failure (or ELMDDM_DIST_IFACE=0, or
-        the CG solver) every rank keeps the rank-0 path.  Returns whether it is active."""
+        the others'.  All ranks agree on the outcome; on any failure (or unless
+        ELMDDM_DIST_IFACE=1: opt-in, it has not yet run on several GPUs; or the CG solver) every
+        rank keeps the rank-0 path.  Returns whether it is active."""
         import os
 
         import torch.distributed as dist
 
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
-        want = os.environ.get("ELMDDM_DIST_IFACE", "1") != "0" and self.prob.interface_solver == "cholesky"
+        # opt-in until the peer-memory path has run on several GPUs (this environment offers one)
+        want = os.environ.get("ELMDDM_DIST_IFACE", "0") == "1" and self.prob.interface_solver == "cholesky"
         want = want and self.sizes["G"] > 0
 
         def agree(flag: bool) -> bool:
@@ -296,11 +344,20 @@ class Context:
         self._dist_pool_ptr = self._dist_pool()
         return True
 
+    def _fence(self, device, group=None):
+        import torch.distributed as dist
+
+        dist.all_reduce(torch.zeros(1, dtype=torch.int32, device=device), group=group)
+
     def run(self, buf: dict, xy=None, u=None, group=None, stream=None, timer=None):
-        """One pass of the hot path on this rank.  With a process group of size > 1: either the
-        multi-rank interface factorisation (Schur contributions all-reduced, every rank factors
-        its share of the tiles into its replica and solves u_Gamma itself; see dist_setup), or
-        the contributions are summed on rank 0 (NCCL reduce) and u_Gamma is broadcast back."""
+        """One pass of the hot path on this rank (Algorithm 1).  With a process group of
+        size > 1 the Schur contributions of every slab are gathered to rank 0 (one NCCL gather, no
+        arithmetic: every slot has one writer), rank 0 solves the interface system and u_Gamma is
+        broadcast back -- or, opt-in (ELMDDM_DIST_IFACE=1, see dist_setup), every rank receives
+        every slab and all ranks factor the interface system together.  Errors: every rank
+        synchronises at the end and raises its own device status (non-finite QR, ...); a failed
+        rank-0 interface solve is broadcast as a status word, so every rank raises instead of
+        waiting in a collective."""
         import torch.distributed as dist
 
         world = dist.get_world_size(group) if (group is not None or (dist.is_available() and dist.is_initialized())) else 1
@@ -315,36 +372,43 @@ class Context:
         mark("assemble")
         self.local_factor(buf["Kaug"], buf["tau"], buf["work"], stream)
         mark("local_factor")
-        if world > 1:
-            buf["Pbuf"].zero_()
-            buf["Sbuf"].zero_()
         self.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"], stream)
         mark("schur_accumulate")
         if world > 1:
-            if dmode:
-                dist.all_reduce(buf["Pbuf"], group=group)
-                dist.all_reduce(buf["Sbuf"], group=group)
-            else:
-                dist.reduce(buf["Pbuf"], dst=0, group=group)
-                dist.reduce(buf["Sbuf"], dst=0, group=group)
+            self._gather_slots(buf["Pbuf"], "Pbuf", world, rank, dmode, group)
+            self._gather_slots(buf["Sbuf"], "Sbuf", world, rank, dmode, group)
             mark("reduce")
+        err = None
+        failed = None
         if self.sizes["G"] > 0 and dmode:
             pool = self._dist_pool_ptr
             self.interface_assemble(buf["Pbuf"], buf["Sbuf"], pool, buf["g"], buf["work"], stream)
+            # device-side fence: no rank's factorisation kernel may push a finished tile into a
+            # peer's replica before that peer has assembled M into it (an all-reduce completes on
+            # every rank only after every rank reached it on its stream)
+            self._fence(buf["g"].device, group)
             mark("interface_assemble")
             self.interface_factor_solve(pool, buf["g"], buf["uG"], buf["work"], stream)
             mark("interface_factor_solve")
         elif self.sizes["G"] > 0:
             if rank == 0:
-                self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
-                mark("interface_assemble")
-                if self.prob.interface_solver == "cg":
-                    self.cg_info = self.interface_cg(buf["Mband"], buf["g"], buf["uG"], buf["work"], self.prob.cg_tol,
-                                                     stream=stream)
-                else:
-                    self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
-                mark("interface_factor_solve")
+                try:
+                    self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
+                    mark("interface_assemble")
+                    if self.prob.interface_solver == "cg":
+                        self.cg_info = self.interface_cg(buf["Mband"], buf["g"], buf["uG"], buf["work"],
+                                                         self.prob.cg_tol, stream=stream)
+                    else:
+                        self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
+                    if world > 1:  # the outcome must be known before it is broadcast
+                        self.sync(stream)
+                    mark("interface_factor_solve")
+                except _lib.ElmddmError as ex:
+                    err = ex
             if world > 1:
+                failed = torch.tensor([0 if err is None else 1], dtype=torch.int32, device=buf["g"].device
+                                      if dist.get_backend(group) == "nccl" else "cpu")
+                dist.broadcast(failed, src=0, group=group)
                 dist.broadcast(buf["uG"], src=0, group=group)
                 mark("broadcast")
         self.back_solve(buf["Kaug"], buf["uG"], buf["coef"], buf["resid"], buf["work"], stream)
@@ -356,6 +420,11 @@ class Context:
             if world > 1:
                 dist.reduce(u, dst=0, group=group)
             mark("evaluate")
+        if err is not None:
+            raise err
+        self.sync(stream)  # this rank's device status: non-finite QR, pivots, rank warnings
+        if failed is not None and int(failed.item()) != 0:
+            raise _lib.ElmddmError("the rank-0 interface solve failed (see rank 0's error)")
         return buf
 
 

@@ -98,8 +98,17 @@ def test_sass_uses_fp64_tensor_pipe():
 def test_partition_covers_all_subdomains():
     from paper_2406_15959_b200 import partition
 
+    import pytest
+
+    from paper_2406_15959_b200 import ElmddmError
+
     for N in [1, 4, 16, 64, 256, 1024]:
         for world in [1, 2, 3, 4, 8]:
+            per = -(-N // world)
+            if (world - 1) * per >= N:  # some rank would own nothing: every rank raises
+                with pytest.raises(ElmddmError, match="world <= N"):
+                    partition(N, world, 0)
+                continue
             got = []
             for r in range(world):
                 s0, s1 = partition(N, world, r)

@@ -36,8 +36,8 @@ def _fake_ctx(rank, world, mode="off"):
 
     class Fake(S.Context):
         def __init__(self):  # no CUDA context
-            self.prob = S.Problem(P=2, M=8, p=3, q=2)
-            self.sizes = {"G": G}
+            self.prob = S.Problem(P=3, M=8, p=3, q=2)   # N_SUB = 9 subdomains
+            self.sizes = {"G": G, "pbuf_elems": N_SUB * SLOT, "sbuf_elems": N_SUB * SLOT}
             self.s_begin, self.s_end = s0, s1
             self.calls = []
 
@@ -86,7 +86,16 @@ def _fake_ctx(rank, world, mode="off"):
 
         def interface_factor_solve(self, Mband, g, uG, work, stream=None):
             self.calls.append("interface_factor_solve")
+            if mode == "pivot_fail":
+                raise S._lib.ElmddmError("interface_factor_solve: ELMDDM_ENUMERIC: non-positive pivot")
             uG[:] = g
+
+        def sync(self, stream=None):
+            self.calls.append("sync")
+
+        def _fence(self, device, group=None):
+            self.calls.append("fence")
+            super()._fence(device, group)
 
         def back_solve(self, Kaug, uG, coef, resid, work, stream=None):
             self.calls.append("back_solve")
@@ -101,11 +110,25 @@ def _fake_ctx(rank, world, mode="off"):
     return Fake()
 
 
+def S_err():
+    from paper_2406_15959_b200 import _lib
+
+    return _lib.ElmddmError
+
+
 def _worker(rank, world, port, q, mode="off"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    os.environ["ELMDDM_DIST_IFACE"] = "0" if mode == "off" else "1"
+    os.environ["ELMDDM_DIST_IFACE"] = "1" if mode in ("on", "fail1", "hs_fail2") else "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        if mode == "too_many":
+            from paper_2406_15959_b200 import solver as S
+
+            try:
+                S.partition(2, world, rank)
+            except S._lib.ElmddmError as ex:
+                q.put((rank, "raised", str(ex), None, None, None))
+            return
         ctx = _fake_ctx(rank, world, mode)
         f64 = dict(dtype=torch.float64)
         buf = {"W": torch.zeros(1, **f64), "b": torch.zeros(1, **f64), "Kaug": torch.zeros(1, **f64),
@@ -115,7 +138,11 @@ def _worker(rank, world, port, q, mode="off"):
                "coef": torch.zeros(3, **f64), "resid": torch.zeros(1, **f64)}
         xy = torch.zeros(2 * NPTS, **f64)
         u = torch.full((NPTS,), -1.0, **f64)
-        ctx.run(buf, xy, u)
+        try:
+            ctx.run(buf, xy, u)
+        except S_err() as ex:
+            q.put((rank, ctx.calls, "raised", str(ex), None, None))
+            return
         q.put((rank, ctx.calls, buf["Pbuf"].tolist(), buf["uG"].tolist(), buf["coef"].tolist(), u.tolist()))
     finally:
         dist.destroy_process_group()
@@ -149,6 +176,10 @@ def test_dist_interface_mode_gloo(world):
         calls, P, uG, coef, u = res[r]
         assert calls[:4] == ["dist_export", "dist_import", "dist_handshake0", "dist_handshake1"]
         assert "interface_assemble" in calls and "interface_factor_solve" in calls
+        # the cross-rank fence sits between the assembly into the replica and the factorisation
+        ia, fe, fs = calls.index("interface_assemble"), calls.index("fence"), calls.index("interface_factor_solve")
+        assert ia < fe < fs
+        assert calls[-1] == "sync"
         assert P == expect_P and uG == [g_expect] * G and coef == [g_expect] * 3
     assert res[0][4] == [g_expect + t for t in range(NPTS)]
 
@@ -195,3 +226,29 @@ def test_collective_sequence_gloo(world):
         assert uG == uG0                                    # broadcast
         assert coef == [g_expect] * 3
     assert u0 == [g_expect + t for t in range(NPTS)]        # slab-wise evaluation summed
+
+
+def test_default_is_the_rank0_path_gloo():
+    """ELMDDM_DIST_IFACE unset: the multi-rank factorisation is opt-in (it has not yet run on
+    several GPUs); the rank-0 path runs and no IPC region is exported."""
+    res = _run(2, "default")
+    for r in range(2):
+        calls = res[r][0]
+        assert "dist_export" not in calls
+        assert ("interface_factor_solve" in calls) == (r == 0)
+        assert calls[-1] == "sync"          # every rank reports its own device status
+
+
+def test_rank0_interface_failure_raises_on_every_rank_gloo():
+    """A non-positive pivot on rank 0 is broadcast as a status word: every rank raises, none
+    waits forever in the broadcast of u_Gamma."""
+    res = _run(3, "pivot_fail")
+    for r in range(3):
+        calls, tag, msg = res[r][0], res[r][1], res[r][2]
+        assert tag == "raised"
+        assert ("non-positive pivot" in msg) if r == 0 else ("rank-0 interface solve failed" in msg)
+
+
+def test_more_ranks_than_subdomains_raise_everywhere_gloo():
+    res = _run(3, "too_many")
+    assert all(res[r][0] == "raised" and "world <= N" in res[r][1] for r in range(3))
