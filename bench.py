@@ -89,10 +89,11 @@ def workload_desc(k: int, c: dict | None = None) -> str:
 # ------------------------------------------------------------------------------------------------
 # algorithmic work, per subdomain summed over the ranks' subdomains
 # ------------------------------------------------------------------------------------------------
-def algorithmic(c: dict, s_range) -> dict:
+def algorithmic(c: dict, s_range, e_impl: int = 0) -> dict:
     P, M, p, q = c["P"], c["M"], c["p"], c["q"]
     m = p * p + 4 * q + (M if c.get("tikhonov", 0.0) > 0 else 0)  # + the damping rows (reading R29)
     fl_qr = 0.0
+    fl_panel = 0.0
     bytes_asm = 0.0
     bytes_asm_e = 0.0
     fl_schur = 0.0
@@ -104,8 +105,15 @@ def algorithmic(c: dict, s_range) -> dict:
         mg = n_if * q
         k = mg + 1
         fl_qr += 2 * m * M * M - 2.0 / 3.0 * M ** 3 + 2 * M * k * (2 * m - M)
+        # the panels' own Householder work (QR of the (m - j0) x nb panel): the rest of H3 is the
+        # algorithmic work of the trailing updates
+        for j0 in range(0, M, 64):
+            nb = min(64, M - j0)
+            fl_panel += 2.0 * (m - j0) * nb * nb - 2.0 / 3.0 * nb ** 3
         bytes_asm += 8.0 * (m * M + m + mg * M)
-        bytes_asm_e += 8.0 * (m * M + m + 4 * q * M + m * 4 * q)  # as written: K, F, all 4q flux rows, E_Gamma
+        # as written: K, F, all 4q flux rows, the E_Gamma columns the assembly still writes (the
+        # implicit ones [e_impl_begin, e_impl_end) are synthesised by the first QR update)
+        bytes_asm_e += 8.0 * (m * M + m + 4 * q * M + m * (4 * q - e_impl))
         fl_schur += mg * M * M + 2 * mg * k * M + 2 * (m - M) * k * k / 2
         # compact-WY trailing updates of the 64-wide panels: W = V^T C, Z = T^T W, C -= V Z
         for j0 in range(0, M, 64):
@@ -114,7 +122,7 @@ def algorithmic(c: dict, s_range) -> dict:
             if N > 0:
                 fl_wy += 4.0 * nb * R * N + 2.0 * nb * nb * N
                 by_wy += 8.0 * (R * nb + 2.0 * R * N)  # V once, C read + written once (algorithmic)
-    return {"flop_qr": fl_qr, "bytes_assemble": bytes_asm, "bytes_assemble_written": bytes_asm_e, "flop_schur": fl_schur, "flop_wy": fl_wy, "bytes_wy": by_wy}
+    return {"flop_qr": fl_qr, "flop_panel": fl_panel, "flop_trailing": fl_qr - fl_panel, "bytes_assemble": bytes_asm, "bytes_assemble_written": bytes_asm_e, "flop_schur": fl_schur, "flop_wy": fl_wy, "bytes_wy": by_wy}
 
 
 def ncu_traffic(k: int):
@@ -174,6 +182,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
+def write_peak():
+    """Write-only HBM bandwidth measured on a B200 of this pool (tools/hbm_probe.py, committed):
+    the ceiling of the write-bound assembly kernel, beside the copy peak of MEASURED_PEAKS.json."""
+    path = os.path.join(ROOT, "profiles", "r02_hbm_probe.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    d["source"] = "profiles/r02_hbm_probe.json (torch fill_ of 16 GiB, best of 10, CUDA events)"
+    return d
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -183,63 +202,111 @@ def peaks():
 
 
 # ------------------------------------------------------------------------------------------------
-def run_reference(args, world, rank):
-    """The oracle (plain C, fp64) on the box's host cores: each step is a bounded sample of the
-    workload -- the local phase (assembly + unblocked QR + literal Schur pieces + back-solve) of
-    n_cores subdomains; value = subdomains per second."""
-    if rank != 0:
-        return
+def band_chol_cost(G: int, bw: int) -> float:
+    """Multiply-adds of the oracle's banded Cholesky (oracle.c orc_band_cholesky) of a G-row
+    matrix with half-bandwidth bw: for column j the diagonal sum has j - max(0, j - bw) terms and
+    row i in (j, j + bw] has j - max(0, i - bw) terms."""
+    j = np.arange(G, dtype=np.float64)
+    lo = np.maximum(0.0, j - bw)
+    diag = j - lo
+    nrow = np.minimum(j + bw, G - 1) - j                    # rows i = j+1 .. j+nrow
+    # sum_{d=1}^{nrow} (j - max(0, j + d - bw)) = nrow*j - sum_d max(0, j + d - bw)
+    a = np.maximum(0.0, bw - j)                             # d <= a contribute 0 to the max
+    tail = np.maximum(0.0, nrow - a)
+    s_max = tail * (np.maximum(0.0, j + a + 1 - bw) + (j + nrow - bw)) / 2.0
+    return float(np.sum(diag + nrow * j - s_max))
+
+
+def oracle_sample(c: dict, k: int, cores: int, step: int = 0):
+    """The oracle (plain C, fp64) timed on a bounded sample of the workload, extrapolated to its
+    time-to-solution: (a) the local phase (assemble + unblocked QR + literal eqn:schur pieces +
+    back-solve) of `cores` random subdomains, scaled by N / n; (b) the banded Cholesky of the
+    interface (oracle.c orc_band_cholesky) on a seeded SPD band matrix with the workload's
+    half-bandwidth and G' <= ~5000 rows, scaled by the multiply-add count of the full G-row band
+    (band_chol_cost; the dense route for G <= 20000 is timed the same way on its band).  Returns
+    (estimated time-to-solution s, wall s spent, description)."""
     import oracle as O
 
-    c = bench_config(args)
     O.set_grf(c.get("grf"))
     oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"],
                c.get("tikhonov", 0.0))
     W, b, _, _ = O.init_hidden(oc)
-    cores = len(os.sched_getaffinity(0))
     N = c["P"] ** 2
     G = O.geometry(oc)["G"]
     uG = np.zeros(max(G, 1))
-    rng = np.random.default_rng(0)
-    n = cores
-    times = []
+    n = min(N, cores)
+    s_list = np.random.default_rng(1 + step).choice(N, size=n, replace=False)
+    t_loc = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
+    t_band = 0.0
+    Gs = 0
+    bw = 0
+    if G > 0:
+        bw = min((4 * c["P"] - 1) * c["q"] - 1, G - 1)
+        Gs = min(G, 5000)
+        rng = np.random.default_rng(100 + step)
+        B = rng.uniform(-1.0, 1.0, (Gs, bw + 1))
+        B[:, bw] = 2.0 * (bw + 1)                               # diagonally dominant: SPD
+        import time as _t
+
+        t0 = _t.perf_counter()
+        _, rc = O.band_cholesky(B, nthreads=cores)
+        t_band = _t.perf_counter() - t0
+        assert rc == 0
+    est = t_loc * N / n + (t_band * band_chol_cost(G, bw) / band_chol_cost(Gs, bw) if G > 0 else 0.0)
+    desc = (f"oracle time-to-solution of {c.get('name', f'cfg{k}')} estimated from a bounded sample on {cores} "
+            f"threads: local phase (assemble, unblocked Householder QR, literal eqn:schur pieces, back-solve) of {n} "
+            f"random subdomains ({t_loc:.1f} s) x N/{n}, plus the banded interface Cholesky (half-bandwidth {bw}) "
+            f"timed on {Gs} rows ({t_band:.1f} s) x the multiply-add ratio of the full {G}-row band; interface "
+            f"assembly, back-solve and evaluation (~1% of the full oracle solve) not sampled")
+    return est, t_loc + t_band, desc
+
+
+def full_oracle_record(k: int):
+    """The committed full oracle solve of config k on the GPU box's host (tools/oracle_cache.py),
+    if any: context beside the live sample."""
+    for tag in ("r02_box", "r02_local"):
+        path = os.path.join(ROOT, "profiles", f"{tag}_oracle_cfg{k}.json")
+        if os.path.exists(path):
+            d = json.load(open(path))
+            return {"wall_s": d["wall_s"], "threads": d["threads"], "times_s": d["times_s"], "source": path[len(ROOT) + 1:]}
+    return None
+
+
+def run_reference(args, world, rank):
+    """The reference arm = the oracle (plain C, fp64) on the box's host cores: each step is a
+    bounded sample of the workload extrapolated to the oracle's time-to-solution (oracle_sample);
+    value = subdomain solves per second = N / time-to-solution."""
+    if rank != 0:
+        return
+    c = bench_config(args)
+    cores = len(os.sched_getaffinity(0))
+    N = c["P"] ** 2
+    ests, walls, desc = [], [], ""
     for it in range(args.warmup + args.steps):
-        s_list = rng.choice(N, size=min(n, N), replace=False)
-        t = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
+        est, wall, desc = oracle_sample(c, args.config, cores, it)
         if it >= args.warmup:
-            times.append((t, len(s_list)))
-    tot_t = sum(t for t, _ in times)
-    tot_n = sum(k for _, k in times)
-    val = tot_n / tot_t
-    sample = (f"per step: local phase (assemble, unblocked Householder QR, literal eqn:schur pieces, back-solve) "
-              f"of {n} random subdomains of {c.get('name', f'cfg{args.config}')} on {cores} threads; interface solve excluded")
+            ests.append(est)
+            walls.append(wall)
+    t = float(np.mean(ests))
+    val = N / t
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(args.config, c)},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "sample_wall_s_per_step": float(np.mean(walls)),
+                             "full_oracle_solve": full_oracle_record(args.config)},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_leg(c, k):
-    """Oracle timed on a bounded sample of the same workload (about 10-30 s)."""
-    import oracle as O
-
-    O.set_grf(c.get("grf"))
-    oc = O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], 0, c["init_c"], c["r_over_diam"], c["seed"],
-               c.get("tikhonov", 0.0))
-    W, b, _, _ = O.init_hidden(oc)
+    """Oracle timed on a bounded sample of the same workload (about 10-30 s), extrapolated to its
+    time-to-solution (oracle_sample)."""
     cores = len(os.sched_getaffinity(0))
-    N = c["P"] ** 2
-    G = O.geometry(oc)["G"]
-    uG = np.zeros(max(G, 1))
-    n = min(N, cores)
-    s_list = np.random.default_rng(1).choice(N, size=n, replace=False)
-    t = O.sample_local(oc, W, b, s_list, uG, nthreads=cores)
-    return {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"local phase (assemble + unblocked QR + literal Schur pieces + back-solve) of {n} random "
-                      f"subdomains of {c.get('name', f'cfg{k}')}, {t:.1f} s on {cores} threads; interface solve excluded"}
+    est, wall, desc = oracle_sample(c, k, cores)
+    return {"value": c["P"] ** 2 / est, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+            "time_to_solution_s": est, "sample_wall_s": wall, "full_oracle_solve": full_oracle_record(k)}
 
 
 class PhaseTimer:
@@ -369,12 +436,12 @@ def main():
                "ms_per_step": float(ems.item()) / args.steps}
 
     # rooflines.  Dominant kernel: the fused compact-WY trailing update (k_wy_update, DMMA).
-    work = algorithmic(c, (s0, s1))
+    work = algorithmic(c, (s0, s1), ctx.sizes["e_impl_end"] - ctx.sizes["e_impl_begin"])
     pk, src = peaks()
     dmma = E.solver.dmma_peak_tflops(local_rank, 300.0)
     fp64_ratio_peak = pk["bf16_tflops_sustained"] * NOMINAL_FP64_TFLOPS / NOMINAL_BF16_TFLOPS
     wy_ms = kms["gemm_qr"]
-    achieved_wy = work["flop_wy"] / (wy_ms * 1e-3) / 1e12 if wy_ms > 0 else None
+    achieved_wy = work["flop_trailing"] / (wy_ms * 1e-3) / 1e12 if wy_ms > 0 else None
     lf_ms = phases.get("local_factor", 0.0)
     achieved_lf = work["flop_qr"] / (lf_ms * 1e-3) / 1e12 if lf_ms > 0 else None
     step_kernel_ms = max(sum(kms.values()), 1e-12)
@@ -389,9 +456,14 @@ def main():
             "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": (work["bytes_wy"] / wy_launches) if wy_launches else None,
             "kernel": "k_wy_tma: fused compact-WY trailing update of the blocked Householder QR (FP64 DMMA, TMA-staged)",
-            "flop_per_step": work["flop_wy"], "kernel_ms_per_step": wy_ms, "launches_per_step": wy_launches,
+            "flop_per_step": work["flop_trailing"],
+            "flop_what": ("algorithmic trailing-update work: H3 = sum_s 2mM^2 - 2M^3/3 + 2Mk(2m-M) minus the panels' "
+                          "own Householder work sum 2(m-j0)nb^2 - 2nb^3/3 (the kernel also does the compact-WY "
+                          "overhead 2nb^2 per column, flop_wy, not counted)"),
+            "kernel_ms_per_step": wy_ms, "launches_per_step": wy_launches,
             "share_of_step": wy_ms / step_kernel_ms,
-            "peak_source": "measured on this GPU in this run: register-resident DMMA.8x8x4 loop (elmddm_dmma_probe)",
+            "peak_source": ("measured on this GPU in this run: register-resident DMMA.8x8x4 loop (elmddm_dmma_probe; "
+                            "profiles/r02_dmma_probe.json: 37.14 TF/s at 1965 MHz, no throttle reason)"),
             "peak_ratio_rule": fp64_ratio_peak,
             "peak_ratio_rule_source": f"{src} bf16_tflops_sustained x {NOMINAL_FP64_TFLOPS}/{NOMINAL_BF16_TFLOPS}",
             "frac_ratio_rule": (achieved_wy / fp64_ratio_peak) if achieved_wy else None}
@@ -409,11 +481,17 @@ def main():
                 "peak": pk["hbm_gbs"], "unit": "GB/s"}
     roof_asm["frac"] = roof_asm["achieved"] / roof_asm["peak"] if roof_asm["achieved"] else None
     roof_asm["what"] = ("achieved = algorithmic bytes K + F + A (interface flux rows) per subdomain / kernel time; "
-                        "achieved_written counts every byte the kernel writes, incl. the materialised unit "
-                        "columns E_Gamma of the augmented matrix [K | E_Gamma | F] and zero flux rows of Dirichlet edges")
+                        "achieved_written counts every byte the kernel writes, incl. the unit columns E_Gamma of "
+                        "[K | E_Gamma | F] it still writes (tile-aligned ones are implicit) and zero flux rows of "
+                        "Dirichlet edges")
     if asm_ms > 0:
         roof_asm["achieved_written"] = work["bytes_assemble_written"] / (asm_ms * 1e-3) / 1e9
         roof_asm["frac_written"] = roof_asm["achieved_written"] / roof_asm["peak"]
+        wpk = write_peak()
+        if wpk:
+            roof_asm["peak_write_only"] = wpk["write_fill_GBps"]
+            roof_asm["frac_of_write_only_peak"] = roof_asm["achieved_written"] / wpk["write_fill_GBps"]
+            roof_asm["peak_write_only_source"] = wpk["source"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -426,11 +504,12 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(args.config, c), "subdomains": N, "l2_flush":
                            "inputs larger than L2: every step writes K_aug (S*ld*ncols*8 B) >> 126 MB",
-                           "parallelism": (f"subdomain slabs over {world} GPU(s); Schur buffers NCCL all-reduce; interface "
+                           "parallelism": (f"subdomain slabs over {world} GPU(s); Schur slabs NCCL all-gather; interface "
                                            f"tile Cholesky shared by all GPUs (replicated tile pools over NVLink peer "
                                            f"memory, CUDA IPC), every rank solves u_Gamma"
                                            if getattr(ctx, "_dist", False) else
-                                           f"subdomain slabs over {world} GPU(s), NCCL reduce + broadcast"),
+                                           f"subdomain slabs over {world} GPU(s), NCCL gather of the Schur slabs to rank 0 + "
+                                           f"broadcast of u_Gamma"),
                            "interface_ordering": ["strip", "nested_dissection"][ctx.sizes["chol_ordering"]]},
                 "time_to_solution_ms": ms_per_step, "rel_l2_vs_exact": err,
                 "roofline": roof, "roofline_local_factor": roof_qr, "roofline_assembly": roof_asm,

@@ -114,6 +114,8 @@ typedef struct {
     int64_t chol_n;                         /* unknowns in the factorisation order (padded, %64)  */
     int64_t chol_blocks;                    /* chol_n / 64                                        */
     int64_t chol_ordering;                  /* 0 strip (envelope), 1 nested dissection            */
+    int64_t e_impl_begin, e_impl_end;       /* implicit E_Gamma columns [begin, end) of K_aug: not
+                                               written by elmddm_assemble (see there)             */
 } elmddm_sizes_t;
 
 /* ---- context ------------------------------------------------------------------------------ */
@@ -162,7 +164,9 @@ elmddm_status elmddm_init_hidden(elmddm_ctx* ctx, double* W, double* b, double* 
  *   -rho |w|^2 sigma''(z) - (grad rho . w) sigma'(z) --, boundary and
  *   interface rows sigma(z)); columns M..M+4q-1 = E_Gamma (unit column at each interface row;
  *   zero column for a Dirichlet edge point; B^s = -E_Gamma); column M+4q = F^s = [f; g; 0];
- *   rows m..ld-1 = 0.
+ *   rows m..ld-1 = 0.  The E_Gamma columns [e_impl_begin, e_impl_end) of elmddm_sizes are
+ *   IMPLICIT: not written here (their contents are unspecified until elmddm_local_factor, whose
+ *   first trailing update synthesises the unit columns on chip instead of reading them).
  *   At[S][4q][M] = (A^s)^T: flux row e*q+k holds (w_j . n_e) sigma'(z) at edge e point k,
  *   outward axis normals; zero for Dirichlet edges.                                            */
 elmddm_status elmddm_assemble(elmddm_ctx* ctx, const double* W, const double* b, double* Kaug, double* At,

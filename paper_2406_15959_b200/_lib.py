@@ -32,7 +32,8 @@ class Sizes(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "N", "S", "m", "ld", "ncols", "kaug", "G", "faces", "kaug_elems", "at_elems", "tau_elems",
         "pbuf_ld", "pbuf_elems", "sbuf_ld", "sbuf_elems", "work_elems", "band_ld", "band_nbw", "band_elems",
-        "G_pad", "halfband", "chol_tasks", "chol_flops", "chol_n", "chol_blocks", "chol_ordering")]
+        "G_pad", "halfband", "chol_tasks", "chol_flops", "chol_n", "chol_blocks", "chol_ordering",
+        "e_impl_begin", "e_impl_end")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

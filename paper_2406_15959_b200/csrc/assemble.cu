@@ -255,22 +255,34 @@ template <int OP>
 __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t ld, int64_t ncols,
                                                     const double* __restrict__ W, const double* __restrict__ b,
                                                     double* __restrict__ Kaug, double* __restrict__ At,
-                                                    const double4* __restrict__ coef) {
+                                                    const double4* __restrict__ coef, int e_impl_begin,
+                                                    int e_impl_end) {
     const int M = cfg.M, q = cfg.q, P = cfg.P, p = cfg.p, pp = p * p;
     const int m = pp + 4 * q;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
     const int i = s % P, j = s / P;
-    const int c0 = blockIdx.x * AS_COLS;
+    int c0 = blockIdx.x * AS_COLS;
+    if (c0 >= e_impl_begin) c0 += e_impl_end - e_impl_begin;  // the grid skips the implicit columns
     double* Ks = Kaug + (int64_t)sl * ld * ncols;
     if (c0 < M) {
         extern __shared__ double tab[];      // [AS_COLS][2][ntab]
-        __shared__ double w2s[AS_COLS];
+        __shared__ double w2s[AS_COLS], wxs[AS_COLS], wys[AS_COLS], bts[AS_COLS];
         const int ntab = p + q + 2;
         // distinct coordinates: [interior (p) | x0 | x0+h | edge positions (q)], same for y
         const double cx = (double)(2 * i + 1) / (double)(2 * P), cy = (double)(2 * j + 1) / (double)(2 * P);
-        for (int t = threadIdx.x; t < AS_COLS * 2 * ntab; t += AS_NT) {
-            const int cc = t / (2 * ntab), axis = (t / ntab) & 1, k = t % ntab;
-            const int col = min(c0 + cc, M - 1);
+        if (threadIdx.x < AS_COLS) {
+            const int col = min(c0 + (int)threadIdx.x, M - 1);
+            const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
+            w2s[threadIdx.x] = 2.0 * (wx * wx + wy * wy);
+            wxs[threadIdx.x] = wx;
+            wys[threadIdx.x] = wy;
+            bts[threadIdx.x] = b[(int64_t)sl * M + col] + wx * cx + wy * cy;  // b~ = b + w . c
+        }
+        __syncthreads();
+        // one coordinate per thread (one correctly rounded division, shared by the 8 neurons),
+        // then e^{2 w_x (x - c_x) + 2 b~} (axis 0) or e^{2 w_y (y - c_y)} (axis 1) for each neuron
+        for (int t = threadIdx.x; t < 2 * ntab; t += AS_NT) {
+            const int axis = t >= ntab, k = t - axis * ntab;
             const int ij = axis == 0 ? i : j;
             double coord;
             if (k < p) coord = (double)(ij * (p + 1) + k + 1) / (double)(P * (p + 1));
@@ -280,59 +292,85 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                 const int np = OP == 2 ? q / 2 : q;  // plate: edge rows k and k + np share a point
                 coord = (double)(ij * (np + 1) + (k - p - 2) % np + 1) / (double)(P * (np + 1));
             }
-            const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
-            double arg;
-            if (axis == 0) arg = 2.0 * (wx * (coord - cx) + (b[(int64_t)sl * M + col] + wx * cx + wy * cy));
-            else arg = 2.0 * wy * (coord - cy);
-            tab[t] = exp(arg);
-        }
-        __shared__ double wxs[AS_COLS], wys[AS_COLS];
-        if (threadIdx.x < AS_COLS) {
-            const int col = min(c0 + threadIdx.x, M - 1);
-            const double wx = W[((int64_t)sl * M + col) * 2], wy = W[((int64_t)sl * M + col) * 2 + 1];
-            w2s[threadIdx.x] = 2.0 * (wx * wx + wy * wy);
-            wxs[threadIdx.x] = wx;
-            wys[threadIdx.x] = wy;
+            const double dc = coord - (axis == 0 ? cx : cy);
+#pragma unroll 2
+            for (int cc = 0; cc < AS_COLS; ++cc)
+                tab[cc * 2 * ntab + t] = exp(axis == 0 ? 2.0 * (wxs[cc] * dc + bts[cc]) : 2.0 * wys[cc] * dc);
         }
         __syncthreads();
         const int ncc = min(AS_COLS, M - c0);
         // flux rows (A^s)^T for the same neurons: At[s][e*q + k][c0 .. c0+8), sigma' = 4 E d^2 at the
-        // edge point from the same tables, times w . n_e (outward axis normal); 16-byte stores
-        // of neuron pairs.  Dirichlet edges are zero.
+        // edge point from the same tables, times w . n_e (outward axis normal); one flux row per
+        // thread, four 16-byte stores of neuron pairs.  Dirichlet edges are zero.
         {
             double* Arow = At + (int64_t)sl * 4 * q * M;
-            for (int t = threadIdx.x; t < 4 * q * (AS_COLS / 2); t += AS_NT) {
-                const int row = t / (AS_COLS / 2), pr = (t % (AS_COLS / 2)) * 2;
-                const int e = row / q, k = row % q;
+            for (int row = threadIdx.x; row < 4 * q; row += AS_NT) {
+                const int e = row / q, k = row - e * q;
                 const bool iface = edge_is_interface(P, i, j, e);
                 const int xi = e == 0 ? p : (e == 1 ? p + 1 : p + 2 + k);
                 const int yi = e == 2 ? p : (e == 3 ? p + 1 : p + 2 + k);
-                double v[2] = {0.0, 0.0};
+                const bool nx = e < 2;                       // normal along x (e 0, 1) or y (e 2, 3)
+                const double sgn = (e & 1) ? 1.0 : -1.0;     // outward: left / bottom negative
+                double* dst = Arow + (int64_t)row * M + c0;
+#pragma unroll 1
+                for (int pr = 0; pr < AS_COLS; pr += 2) {
+                    double v[2];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int cc = pr + h;
-                    if (iface && cc < ncc) {
-                        const double* tx = tab + cc * 2 * ntab;
-                        const double E = tx[xi] * tx[ntab + yi];
-                        const double d = fast_rcp(1.0 + E);
-                        const double wn = e == 0 ? -wxs[cc] : (e == 1 ? wxs[cc] : (e == 2 ? -wys[cc] : wys[cc]));
-                        const double s1 = 4.0 * E * d * d;
-                        if (OP == 2 && k >= q / 2) {  // plate: d/dn Lap phi = |w|^2 (w.n) sigma'''
-                            const double sg = fma(-2.0, d, 1.0), s2 = -2.0 * sg * s1;
-                            v[h] = 0.5 * w2s[cc] * wn * (-2.0 * s1 * s1 - 2.0 * sg * s2);
-                        } else {
-                            v[h] = wn * s1;
+                    for (int h = 0; h < 2; ++h) {
+                        const int cc = pr + h;
+                        v[h] = 0.0;
+                        if (iface && cc < ncc) {
+                            const double* tx = tab + cc * 2 * ntab;
+                            const double E = tx[xi] * tx[ntab + yi];
+                            const double d = fast_rcp(1.0 + E);
+                            const double wn = sgn * (nx ? wxs[cc] : wys[cc]);
+                            const double s1 = 4.0 * E * d * d;
+                            if (OP == 2 && k >= q / 2) {  // plate: d/dn Lap phi = |w|^2 (w.n) sigma'''
+                                const double sg = fma(-2.0, d, 1.0), s2 = -2.0 * sg * s1;
+                                v[h] = 0.5 * w2s[cc] * wn * (-2.0 * s1 * s1 - 2.0 * sg * s2);
+                            } else {
+                                v[h] = wn * s1;
+                            }
                         }
                     }
+                    if (pr + 1 < ncc)
+                        *reinterpret_cast<double2*>(dst + pr) = make_double2(v[0], v[1]);
+                    else if (pr < ncc)
+                        dst[pr] = v[0];
                 }
-                if (pr + 1 < ncc)
-                    *reinterpret_cast<double2*>(Arow + (int64_t)row * M + c0 + pr) = make_double2(v[0], v[1]);
-                else if (pr < ncc)
-                    Arow[(int64_t)row * M + c0 + pr] = v[0];
             }
         }
+        // interior rows, Poisson (OP 0) with p even: a row pair (r, r+1) shares the lattice row b and
+        // starts at an even a, so both x-factors come from ONE 16-byte table load (conflict-free),
+        // the y-factor is a broadcast, and the row kind needs no per-element selection.  Only
+        // the FP64 arithmetic of the separable form remains per element.
+        int r2_begin = 0;
+        if (OP == 0 && (p & 1) == 0 && ncc == AS_COLS) {
+            double w2r[AS_COLS];
+#pragma unroll
+            for (int cc = 0; cc < AS_COLS; ++cc) w2r[cc] = w2s[cc];
+            const int npair = pp / 2;
+            for (int r2 = threadIdx.x; r2 < npair; r2 += AS_NT) {
+                const int r = 2 * r2, a = r % p, bb = r / p;
+                double* dst = Ks + (int64_t)c0 * ld + r;
+#pragma unroll
+                for (int cc = 0; cc < AS_COLS; ++cc) {
+                    const double* tx = tab + cc * 2 * ntab;
+                    const double2 ex = *reinterpret_cast<const double2*>(tx + a);
+                    const double ey = tx[ntab + bb];
+                    const double E0 = ex.x * ey, E1 = ex.y * ey;
+                    const double d0 = fast_rcp(1.0 + E0), d1 = fast_rcp(1.0 + E1);
+                    // -Lap phi = 2|w|^2 sigma sigma', sigma = 1 - 2d, sigma' = 4 E d^2
+                    const double v0 = w2r[cc] * fma(-2.0, d0, 1.0) * (4.0 * E0 * d0 * d0);
+                    const double v1 = w2r[cc] * fma(-2.0, d1, 1.0) * (4.0 * E1 * d1 * d1);
+                    *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+                    dst += ld;
+                }
+            }
+            r2_begin = npair;
+        }
         // two consecutive rows per thread -> 16-byte stores
-        for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
+        for (int r2 = r2_begin + threadIdx.x; r2 < ld / 2; r2 += AS_NT) {
             int xi[2], yi[2], kind[2];
             double4 rc[2] = {make_double4(1.0, 0.0, 0.0, 0.0), make_double4(1.0, 0.0, 0.0, 0.0)};
             bool lapt[2] = {false, false};  // plate: a Lap u trace row
@@ -390,11 +428,13 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
     for (int cc = 0; cc < AS_COLS; ++cc) {
         const int col = c0 + cc;
         if (col >= ncols) break;
-        if (col < M + 4 * q) {
+        if (col >= e_impl_begin && col < e_impl_end) continue;  // implicit: synthesised by the QR
+        if (col < M + 4 * q) {  // ld is even: 16-byte stores of row pairs
             const int t = col - M;
-            const bool iface = edge_is_interface(P, i, j, t / q);
-            for (int r = threadIdx.x; r < ld; r += AS_NT)
-                Ks[(int64_t)col * ld + r] = (iface && r == pp + t) ? 1.0 : 0.0;
+            const int one = edge_is_interface(P, i, j, t / q) ? pp + t : -1;
+            double2* dst = reinterpret_cast<double2*>(Ks + (int64_t)col * ld);
+            for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT)
+                dst[r2] = make_double2(2 * r2 == one ? 1.0 : 0.0, 2 * r2 + 1 == one ? 1.0 : 0.0);
         } else {
             for (int r = threadIdx.x; r < ld; r += AS_NT) {
                 double v = 0.0;
@@ -454,7 +494,9 @@ cudaError_t launch_init_hidden(const elmddm_ctx* c, double* W, double* b, double
 
 cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* b, double* Kaug, double* At,
                             cudaStream_t st) {
-    dim3 g1((unsigned)((c->sz.ncols + AS_COLS - 1) / AS_COLS), (unsigned)c->sz.S);
+    // (the implicit E_Gamma columns [e_impl_begin, e_impl_end) are multiples of AS_COLS apart)
+    dim3 g1((unsigned)((c->sz.ncols - (c->sz.e_impl_end - c->sz.e_impl_begin) + AS_COLS - 1) / AS_COLS),
+            (unsigned)c->sz.S);
     const size_t tab_bytes = sizeof(double) * AS_COLS * 2 * (c->cfg.p + c->cfg.q + 2);
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
     const double4* coef = nullptr;
@@ -469,11 +511,14 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
         coef = reinterpret_cast<const double4*>(c->d_coef);
     }
     if (coef)
-        k_assemble<1><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, coef);
+        k_assemble<1><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, coef,
+                                  (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end);
     else if (c->cfg.problem == 7)
-        k_assemble<2><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr);
+        k_assemble<2><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr,
+                                  (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end);
     else
-        k_assemble<0><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr); }
+        k_assemble<0><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr,
+                                  (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end); }
     return cudaGetLastError();
 }
 

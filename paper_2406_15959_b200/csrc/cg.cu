@@ -120,6 +120,33 @@ __global__ void k_cg_roll(double* sc) { sc[0] = sc[2]; }
 
 }  // namespace
 
+// y = M x for the symmetric matrix in packed tiles (the CG's matrix-vector product), for the
+// iterative refinement of the direct interface solve (chol.cu)
+static __global__ void k_resid(const double* __restrict__ g, double* __restrict__ r, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) r[i] = g[i] - r[i];
+}
+static __global__ void k_axpy1(double* __restrict__ x, const double* __restrict__ d, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] += d[i];
+}
+
+cudaError_t launch_residual(const elmddm_ctx* c, const double* Mband, const double* x, const double* g, double* r,
+                            cudaStream_t st) {
+    const CholPlan& pl = c->plan;
+    {
+        KTimer kt(c, ELMDDM_K_TRSV, st);
+        k_spmv_sym<<<pl.nblk, 256, 0, st>>>(Mband, c->d_diag_tid, c->d_fwd_ptr, c->d_fwd, c->d_bwd_ptr, c->d_bwd, x, r);
+    }
+    k_resid<<<(unsigned)((pl.n + 255) / 256), 256, 0, st>>>(g, r, pl.n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpy1(double* x, const double* d, int64_t n, cudaStream_t st) {
+    k_axpy1<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, d, n);
+    return cudaGetLastError();
+}
+
 cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const double* g, double* uG, double* work,
                              double tol, int maxit, int* iters, double* relres, cudaStream_t st) {
     const CholPlan& pl = c->plan;

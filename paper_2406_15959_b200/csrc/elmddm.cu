@@ -220,6 +220,12 @@ elmddm_status build_tables(elmddm_ctx* c) {
     c->sz.chol_n = pl.n;
     c->sz.chol_blocks = nblk;
     c->sz.chol_ordering = pl.ordering;
+    {
+        int eb = 0, ee = 0;
+        if (c->implicit_e) elm_e_implicit_range(c->cfg.M, c->cfg.q, &eb, &ee);
+        c->sz.e_impl_begin = eb;
+        c->sz.e_impl_end = ee;
+    }
     c->ncrit = pl.ncrit;
     c->chol_flops = pl.nupd * 2 * (int64_t)ELM_NB * ELM_NB * ELM_NB;
     c->sz.chol_tasks = (int64_t)pl.tasks.size();
@@ -310,6 +316,9 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_QR_GROUPS")) g = atoi(env);
         c->qr_groups = g < 1 ? 1 : g;
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_IMPLICIT_E")) c->implicit_e = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_IFACE_REFINE")) c->iface_refine = atoi(env) != 0;
+        c->implicit_e = c->implicit_e && c->use_tma;
         // 4-CTA cluster panels cut the per-subdomain latency chain of the QR but spend more SM
         // time: they win for the small per-rank slabs of multi-GPU runs (config 3: 32 subdomains
         // 38.9 -> 28.0 ms, 16: 30.9 -> 18.9 ms) and lose for large ones (256: 174 -> 211 ms)
@@ -352,7 +361,8 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB);
     c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
                                                           (int64_t)c->ga_ld * c->qrow_cols),
-                                      5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16);
+                                      5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16 +
+                                          (c->iface_refine ? z.band_elems + 2 * z.chol_n : 0));
     c->work_back = z.S * z.ld;
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||

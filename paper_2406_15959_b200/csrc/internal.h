@@ -14,6 +14,19 @@
 #define ELM_TLD 68     // column stride inside a packed 64 x 64 tile of the Schur matrix (== 4 mod 16)
 #define ELM_TS (ELM_NB * ELM_TLD)  // doubles per packed tile
 
+// Implicit E_Gamma: column col of K_aug is never written by elmddm_assemble when
+// the 64-column tile of the first trailing update (j0 = 0: tiles start at min(64, M) + 64 t)
+// holding it lies entirely inside the E_Gamma block [M, M + 4q); that update synthesises the unit
+// columns in shared memory instead of loading them.  Returns [begin, end) of those columns.
+inline void elm_e_implicit_range(int M, int q, int* begin, int* end) {
+    const int c0 = M < ELM_NB ? M : ELM_NB;
+    const int t_first = c0 + ((M - c0 + ELM_NB - 1) / ELM_NB) * ELM_NB;   // first tile start >= M
+    int t_end = c0 + ((M + 4 * q - c0) / ELM_NB) * ELM_NB;               // last tile end <= M + 4q
+    if (t_end < t_first) t_end = t_first;
+    *begin = t_first;
+    *end = t_end;
+}
+
 // Packed tile storage of the Schur matrix: tile t of the factor's tile structure
 // (CholPlan::tile_map) is stored contiguously at t * ELM_TS with element (r, c) at r + c * ELM_TLD,
 // so one bulk copy reproduces the conflict-free padded shared-memory layout of the DMMA kernels.
@@ -134,6 +147,9 @@ struct elmddm_ctx {
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)
+    int implicit_e = 1;  // E_Gamma tiles never written by the assembly, synthesised by the first
+                         // trailing update (elm_e_implicit; needs use_tma; ELMDDM_IMPLICIT_E=0 off)
     int panel_cluster = 0;  // QR panel blocks on 4-CTA clusters (default for S <= 48; ELMDDM_PANEL_CLUSTER)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
     mutable int trsv_epoch = 0;
@@ -258,6 +274,10 @@ struct GemmArgs {
     int batch;
     int lower_only;  // skip 64x64 output tiles strictly above the diagonal
 };
+// r = g - M x (packed-tile symmetric M, factorisation order; cg.cu) and x += d
+cudaError_t launch_residual(const elmddm_ctx* c, const double* Mband, const double* x, const double* g, double* r,
+                            cudaStream_t st);
+cudaError_t launch_axpy1(double* x, const double* d, int64_t n, cudaStream_t st);
 cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_t st,
                         const elmddm_ctx* c = nullptr, int cls = ELMDDM_K_GEMM_QR);
 

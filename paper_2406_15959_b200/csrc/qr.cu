@@ -1534,10 +1534,20 @@ using namespace elmtma;
 #define ELM_SWIZZLE CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
 }  // namespace wyt
 
+// Implicit E_Gamma tiles (elm_e_implicit_range): in the first trailing update (j0 = 0) a 64-column
+// tile inside [e_begin, e_end) is the unit matrix block [0; I; 0] restricted to its columns (a one
+// at row pp + (col - M) when the column's edge is an interface edge, else a zero column).  Its
+// chunks are written into shared memory instead of being loaded, and phase 1 (W = V^T C) visits
+// only the chunks that hold its ones.
+struct EsynArgs {
+    int e_begin, e_end;   // implicit columns (empty: off)
+    int M, q, pp, P, s_begin;
+};
+
 __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ CUtensorMap tmV,
                                                        const __grid_constant__ CUtensorMap tmK,
                                                        const double* __restrict__ Tbuf, int64_t ld, int j0, int nb,
-                                                       int c0, int N, int s_off) {
+                                                       int c0, int N, int s_off, EsynArgs es) {
     using namespace wyt;
     extern __shared__ uint8_t raw[];
     // 1024-byte alignment for the swizzled TMA boxes; pointer arithmetic on `raw` keeps the
@@ -1557,15 +1567,42 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // implicit E_Gamma tile (j0 = 0 only: the host passes an empty range otherwise)
+    const bool syn = ncol0 >= es.e_begin && ncol0 + 64 <= es.e_end;
+    int iface_mask = 0;
+    if (syn) {
+        const int s = es.s_begin + sl, si = s % es.P, sj = s / es.P;
+        iface_mask = (si > 0) | ((si < es.P - 1) << 1) | ((sj > 0) << 2) | ((sj < es.P - 1) << 3);
+    }
+    // the C part of a stage for chunk c of a synthetic tile: element (row, col) of the swizzled
+    // 32 x 64 chunk is 1 iff row c*CH + row == pp + (ncol0 + col - M) on an interface edge
+    auto fill = [&](double* Cs, int c) {
+        for (int t = tid; t < 2 * BOX; t += NT) {
+            const int bx = t / BOX, rem = t - bx * BOX, col = rem >> 4, x = rem & 15;
+            const int row = bx * 16 + ((((x >> 2) ^ (col & 3))) << 2) + (x & 3);
+            const int ecol = ncol0 + col - es.M;
+            Cs[t] = (c * CH + row == es.pp + ecol && ((iface_mask >> (ecol / es.q)) & 1)) ? 1.0 : 0.0;
+        }
+    };
     uint32_t par0 = 0, par1 = 0;
     auto issue = [&](int c, int st) {
         double* d = stg + st * STAGE;
-        mbar_expect(&bar[st], 4 * BOX * 8);
+        mbar_expect(&bar[st], (syn ? 2 : 4) * BOX * 8);
         tma_load(d, &tmV, j0 + c * CH, 0, sl, &bar[st]);
         tma_load(d + BOX, &tmV, j0 + c * CH + 16, 0, sl, &bar[st]);
-        tma_load(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st]);
-        tma_load(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st]);
+        if (!syn) {
+            tma_load(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st]);
+            tma_load(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st]);
+        }
     };
+    // phase-1 chunks: all, or for a synthetic tile the ones holding its ones (W = V^T C is zero
+    // on the others)
+    int cb = 0, n1 = nch;
+    if (syn) {
+        const int r_lo = es.pp + ncol0 - es.M, r_hi = r_lo + 63;
+        cb = r_lo / CH;
+        n1 = (iface_mask ? min(r_hi / CH, nch - 1) - cb + 1 : 0);
+    }
     auto wait_stage = [&](int st) {
         if (st == 0) {
             mbar_wait(&bar[0], par0);
@@ -1582,13 +1619,17 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    if (tid == 0) issue(0, 0);
-    for (int c = 0; c < nch; ++c) {
-        const int st = c & 1;
-        if (tid == 0 && c + 1 < nch) issue(c + 1, st ^ 1);
+    if (tid == 0 && n1 > 0) issue(cb, 0);
+    for (int i1 = 0; i1 < n1; ++i1) {
+        const int st = i1 & 1, c = cb + i1;
+        if (tid == 0 && i1 + 1 < n1) issue(c + 1, st ^ 1);
         wait_stage(st);
         const double* Vs = stg + st * STAGE;
         const double* Cs = Vs + 2 * BOX;
+        if (syn) {
+            fill(stg + st * STAGE + 2 * BOX, c);
+            __syncthreads();
+        }
 #pragma unroll
         for (int ks = 0; ks < CH / 4; ++ks) {
             const int kk = ks * 4 + (lane & 3);
@@ -1650,8 +1691,8 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     __syncthreads();
     // ---------------- phase 3: C += V (-Z) ----------------
     const int wm3 = warp & 1, wn3 = warp >> 1;
-    if (tid == 0) issue(0, nch & 1 ? 1 : 0);  // continue the stage rotation of phase 1
-    const int sbase = nch & 1;
+    if (tid == 0) issue(0, n1 & 1 ? 1 : 0);  // continue the stage rotation of phase 1
+    const int sbase = n1 & 1;
     for (int c = 0; c < nch; ++c) {
         const int st = (c + sbase) & 1;
         if (tid == 0 && c + 1 < nch) {
@@ -1661,6 +1702,10 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         wait_stage(st);
         const double* Vs = stg + st * STAGE;
         double* Cs = stg + st * STAGE + 2 * BOX;
+        if (syn) {  // (the stage's previous TMA store finished reading it before the last issue)
+            fill(Cs, c);
+            __syncthreads();
+        }
         double a3[2][2][2];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
@@ -3050,6 +3095,12 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     bool use_tma = c->use_tma && elm_encode_tmap(&tmK, Kaug, ld, ncols, S, ld * ncols) &&
                    elm_encode_tmap(&tmV64, Vbuf, ld, ELM_NB, S, ELM_NB * ld) &&
                    elm_encode_tmap(&tmVlast, Vbuf, ld, nb_last, S, ELM_NB * ld);
+    // implicit E_Gamma tiles of the first trailing update (the assembly did not write them)
+    const int pp_rows = (int)(c->cfg.p * c->cfg.p);
+    const EsynArgs esyn{(int)c->sz.e_impl_begin, (int)c->sz.e_impl_end, M, (int)c->cfg.q, pp_rows, (int)c->cfg.P,
+                        (int)c->cfg.s_begin};
+    const EsynArgs esyn_off{0, 0, M, (int)c->cfg.q, pp_rows, (int)c->cfg.P, (int)c->cfg.s_begin};
+    if (!use_tma && esyn.e_end > esyn.e_begin) return cudaErrorInvalidValue;  // create() ties implicit_e to use_tma
     // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
     // subdomains are independent).
@@ -3134,7 +3185,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             KTimer kt(c, ELMDDM_K_GEMM_QR, streams[g]);
             if (use_tma)
                 k_wy_tma<<<grid, wyt::NT, wy_smem, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
-                                                                   j0 + nb, n_tr, g0);
+                                                                   j0 + nb, n_tr, g0, j0 == 0 ? esyn : esyn_off);
             else
                 k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;

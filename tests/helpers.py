@@ -59,6 +59,24 @@ def kaug_np(ctx, buf, sl):
     return K.T  # (ld, ncols)
 
 
+def kaug_assembled_np(ctx, buf, sl, c: dict):
+    """K_aug of local subdomain sl as elmddm_assemble defines it: the implicit E_Gamma columns
+    [e_impl_begin, e_impl_end) (include/elmddm.h: not written, synthesised by the QR) filled with
+    their definition -- a one at row p^2 + t of column M + t when edge t // q is an interface edge."""
+    K = kaug_np(ctx, buf, sl).copy()
+    z = ctx.sizes
+    M, q, P, pp = c["M"], c["q"], c["P"], c["p"] ** 2
+    s = ctx.s_begin + sl
+    i, j = s % P, s // P
+    iface = [i > 0, i < P - 1, j > 0, j < P - 1]
+    for col in range(z["e_impl_begin"], z["e_impl_end"]):
+        t = col - M
+        K[:, col] = 0.0
+        if iface[t // q]:
+            K[pp + t, col] = 1.0
+    return K
+
+
 def at_np(ctx, buf, sl, M, q):
     return buf["At"].view(-1, 4 * q, M)[sl].cpu().numpy()  # (4q, M) = A rows
 
