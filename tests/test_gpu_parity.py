@@ -235,12 +235,12 @@ def test_end_to_end_u_parity(k):
         rhs[gidx >= 0] += r["uG"][gidx[gidx >= 0]]
         floor = 10 * m * EPS * np.linalg.norm(rhs)
         assert abs(rg[s] - r["resid"][s]) <= 1e-8 * r["resid"][s] + floor
-    # accuracy vs the exact solution is in the same range as the oracle's.  Off the collocation
-    # points u depends on how rounding resolves the near-null space of the rank-deficient K^s
-    # (reading R24): measured 1e-10 .. 6e-10 at config 2 across equivalent GPU kernel variants vs
-    # 2.5e-11 for the unblocked oracle, so the bound is 10x the oracle's or 1e-8, whichever is larger.
+    # accuracy vs the exact solution within 10x the oracle's (+1e-12): measured 1.1e-5 / 3.6e-13 /
+    # 8.8e-11 vs the oracle's 1.1e-5 / 2.0e-13 / 4.2e-11 at configs 0 / 1 / 2 -- the refined interface
+    # solve (reading R30) removed the factor the tile factorisation had added (6.5e-10 at config 2;
+    # tools/accuracy_study.py, R24)
     ue = WL.exact(c["problem"], xy)
-    assert rel_l2(ug, ue) < max(10 * rel_l2(r["u"], ue), 1e-8)
+    assert rel_l2(ug, ue) < 10 * rel_l2(r["u"], ue) + 1e-12, (rel_l2(ug, ue), rel_l2(r["u"], ue))
 
 
 def _sampled_subdomains(P):
@@ -288,11 +288,11 @@ def test_large_config_sampled_parity(k):
         if len(pts):
             uo = O.evaluate(oc, W, b, np.where(np.arange(P * P)[:, None] == s, o["coef"][None, :], coef_g), pts)
             assert rel_l2(ug[owner == s], uo) <= 1e-6
-    # and the global solution is accurate.  Off the collocation points u depends on how the
-    # near-null space of the rank-deficient K^s is resolved by rounding (R24), so this is a
-    # sanity bound, not a parity check: measured 1e-10 .. 3e-8 across equivalent kernel variants.
+    # and the global solution is accurate: BASELINE configs 3-4 within 1e-8 of the exact solution
+    # (measured 2.5e-9 / 1.5e-10; the oracle 7.9e-11 / 1.4e-9 -- the config-3 gap is the assembly's
+    # rounding, R24); the damped Table 2 workloads 5-6 within 1e-6 (1.8e-7 measured)
     ue = WL.exact(c["problem"], xy)
-    assert rel_l2(ug, ue) < 1e-6
+    assert rel_l2(ug, ue) < (1e-8 if k <= 4 else 1e-6), rel_l2(ug, ue)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -638,9 +638,11 @@ def test_init_schemes_end_to_end_parity_config1(scheme):
     config 1.  Manual: u on the grid matches the oracle to relative L2 1e-6.  He: all basis
     functions look alike and K^s is numerically rank deficient by hundreds of
     columns, so neither u between collocation points (readings R18, R24) nor even the computed
-    residual norms are determined beyond rounding (measured: GPU / oracle r_s ratios 0.43 .. 1.17
-    for the same u_Gamma); what is checked is Table 1's finding on both sides -- the He solution
-    is useless -- and that the residual norms are of the same size."""
+    residual norms are determined beyond rounding (measured: GPU / oracle r_s ratios 0.42 .. 1.24
+    for the same u_Gamma, round 2; the residuals are NOT at rounding level -- r_s / max r_s >= 0.2
+    -- but the projection I - K K^+ depends on which of the hundreds of near-null directions
+    rounding puts inside range(K)); what is checked is Table 1's finding on both sides -- the He
+    solution is useless -- and that the residual norms are of the same size (a factor 4)."""
     import torch
 
     c = WL.config(1, init_scheme=scheme)
