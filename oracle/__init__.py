@@ -32,7 +32,7 @@ class Cfg(C.Structure):
         ("P", C.c_int32), ("M", C.c_int32), ("p", C.c_int32), ("q", C.c_int32),
         ("problem", C.c_int32), ("init_scheme", C.c_int32),
         ("init_c", C.c_double), ("r_over_diam", C.c_double), ("seed", C.c_uint64),
-        ("tikhonov", C.c_double),
+        ("tikhonov", C.c_double), ("layout", C.c_int32),
     ]
 
 
@@ -64,7 +64,9 @@ def lib():
         _lib.orc_band_cholesky.restype = C.c_int
         _lib.orc_band_chol_solve.argtypes = [vp, i64, i64, vp]
         _lib.orc_solve.restype = C.c_int
-        _lib.orc_local_pieces.argtypes = [P, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_local_pieces.argtypes = [P, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_flux_eq.argtypes = [P, C.c_int, C.c_int]
+        _lib.orc_flux_eq.restype = C.c_int
         _lib.orc_local_pieces.restype = C.c_int
         _lib.orc_sample_local.argtypes = [P, vp, vp, vp, vp, C.c_int, C.c_int, vp]
         _lib.orc_sample_local.restype = C.c_double
@@ -76,8 +78,11 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0, tikhonov=0.0) -> Cfg:
-    return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed, tikhonov)
+def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0, tikhonov=0.0,
+        layout=0) -> Cfg:
+    """layout 0: face points (reading R1); 1: the paper's shared lattice with cross points (R32,
+    p == q).  tikhonov < 0: the fixed rule lambda_s = sqrt(eps) ||K^s||_F (R33)."""
+    return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed, tikhonov, layout)
 
 
 def set_grf(params) -> None:
@@ -104,9 +109,16 @@ def problem(pid: int, x: float, y: float):
 
 
 def geometry(c: Cfg) -> dict:
-    out = np.zeros(4, np.int64)
+    out = np.zeros(6, np.int64)
     lib().orc_geometry(C.byref(c), _p(out))
-    return {"m": int(out[0]), "G": int(out[1]), "faces": int(out[2]), "N": int(out[3])}
+    return {"m": int(out[0]), "G": int(out[1]), "faces": int(out[2]), "N": int(out[3]), "NE": int(out[4]),
+            "na": int(out[5])}
+
+
+def flux_eq(c: Cfg, s: int):
+    """Global flux equation of every flux row of A^s (oracle.c orc_flux_eq; -1 = none)."""
+    na = geometry(c)["na"]
+    return np.array([lib().orc_flux_eq(C.byref(c), s, a) for a in range(na)], dtype=np.int64)
 
 
 def rows(c: Cfg, s: int):
@@ -129,11 +141,13 @@ def init_hidden(c: Cfg):
 
 
 def assemble(c: Cfg, s: int, W, b):
-    """K^s (m x M), F^s (m), A (4q x M: flux row e*q+k, zero for Dirichlet edges)."""
-    m = geometry(c)["m"]
+    """K^s (m x M), F^s (m), A (na x M: flux row e*q+k, then two per corner in layout 1; zero
+    where there is no interface)."""
+    geo = geometry(c)
+    m = geo["m"]
     K = np.zeros((c.M, m))  # column-major storage == row-major (M, m)
     F = np.zeros(m)
-    A = np.zeros((c.M, 4 * c.q))
+    A = np.zeros((c.M, geo["na"]))
     lib().orc_assemble(C.byref(c), s, _p(np.ascontiguousarray(W)), _p(np.ascontiguousarray(b)), _p(K), _p(F), _p(A))
     return K.T.copy(), F, A.T.copy()
 
@@ -230,20 +244,24 @@ def solve(c: Cfg, W, b, xy_eval=None, nthreads: int | None = None, want_system: 
 
 def local_pieces(c: Cfg, s: int, W, b, uG=None):
     q = c.q
-    mgmax = 4 * q
+    mgmax = 4 * q + 4
+    mamax = geometry(c)["na"]
     S1 = np.zeros((mgmax, mgmax))
     g1 = np.zeros(mgmax)
-    PB = np.zeros((mgmax, mgmax))
-    pF = np.zeros(mgmax)
+    PB = np.zeros((mamax, mgmax))
+    pF = np.zeros(mamax)
     ig = np.zeros(mgmax, np.int32)
+    aeq = np.zeros(mamax, np.int32)
+    ma = np.zeros(1, np.int32)
     coef = np.zeros(c.M)
     resid = np.zeros(1)
     uGa = None if uG is None else np.ascontiguousarray(uG, dtype=np.float64)
     mg = lib().orc_local_pieces(C.byref(c), s, _p(np.ascontiguousarray(W)), _p(np.ascontiguousarray(b)), _p(uGa),
-                                _p(S1), _p(g1), _p(PB), _p(pF), _p(ig), _p(coef), _p(resid))
+                                _p(S1), _p(g1), _p(PB), _p(pF), _p(ig), _p(coef), _p(resid), _p(aeq), _p(ma))
+    na = int(ma[0])
     S1 = S1.reshape(-1)[: mg * mg].reshape(mg, mg)
-    PB = PB.reshape(-1)[: mg * mg].reshape(mg, mg)
-    out = {"mg": mg, "S1": S1, "g1": g1[:mg], "PB": PB, "pF": pF[:mg], "ig": ig[:mg]}
+    PB = PB.reshape(-1)[: na * mg].reshape(na, mg)
+    out = {"mg": mg, "ma": na, "S1": S1, "g1": g1[:mg], "PB": PB, "pF": pF[:na], "ig": ig[:mg], "aeq": aeq[:na]}
     if uG is not None:
         out["coef"], out["resid"] = coef, float(resid[0])
     return out

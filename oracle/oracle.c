@@ -41,7 +41,10 @@ typedef struct {
     double init_c;          /* c in l = c sqrt(n), P:544 (1/8 for Poisson) */
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s), P:546 (1/2) */
     uint64_t seed;
-    double tikhonov;        /* lambda >= 0: M extra rows lambda * e_j^T of K^s (reading R29) */
+    double tikhonov;        /* lambda >= 0: M extra rows lambda * e_j^T of K^s (reading R29);
+                               < 0: the fixed rule lambda_s = sqrt(eps) ||K^s||_F (reading R33) */
+    int32_t layout;         /* 0: face points (reading R1); 1: the paper's shared lattice with
+                               cross points (reading R32), p == q        */
 } orc_cfg;
 
 static const double PI = 3.14159265358979323846;
@@ -159,10 +162,16 @@ void orc_problem(int problem, double x, double y, double *u, double *f) {
 /* geometry (readings R1 point layout, R14 strip order)                            */
 /* ------------------------------------------------------------------------------------------ */
 /* edges: 0 left (x = x0), 1 right (x = x0+h), 2 bottom (y = y0), 3 top (y = y0+h)           */
-static int orc_m(const orc_cfg *c) { return c->p * c->p + 4 * c->q; }
+/* layout 1 adds the 4 subdomain corners as rows [BL, BR, TL, TR] after the edge rows */
+static int orc_ncorner(const orc_cfg *c) { return c->layout == 1 ? 4 : 0; }
+static int orc_m(const orc_cfg *c) { return c->p * c->p + 4 * c->q + orc_ncorner(c); }
+/* flux rows of A^s: one per edge point, and (layout 1) two per corner -- "a row to A^s for each
+ * edge to which x belongs" (the corner remark): [edge e point k at e*q + k | corner cc
+ * at 4q + 2cc + d, d = 0 the normal of the corner's vertical edge, d = 1 of its horizontal edge] */
+static int orc_na(const orc_cfg *c) { return 4 * c->q + 2 * orc_ncorner(c); }
 /* rows of K^s: the m collocation rows, then (reading R29, Tikhonov damping of the local LS)
  * M rows lambda e_j^T with right-hand side 0, so that min ||K c - r||^2 + lambda^2 ||c||^2      */
-static int orc_mk(const orc_cfg *c) { return orc_m(c) + (c->tikhonov > 0.0 ? c->M : 0); }
+static int orc_mk(const orc_cfg *c) { return orc_m(c) + (c->tikhonov != 0.0 ? c->M : 0); }
 
 /* Face id of edge e of subdomain (i,j), or -1 if the edge lies on dOmega (Dirichlet).
  * Strip order: strip j holds V(0..P-2, j) then H(0..P-1, j) (j < P-1).                        */
@@ -218,15 +227,46 @@ void orc_rows(const orc_cfg *c, int s, double *xy, int32_t *edge, int32_t *gidx)
             gidx[r] = f >= 0 ? f * q + k : -1;
         }
     }
+    /* layout 1: the corners; an interior one is a cross point, an interface unknown shared by
+     * four subdomains, numbered after the face unknowns (row-major over the (P-1)^2 crossings) */
+    for (int cc = 0; cc < orc_ncorner(c); ++cc, ++r) {
+        int ci = cc & 1, cj = cc >> 1, X = i + ci, Y = j + cj;
+        xy[2 * r] = (double)X / (double)P;
+        xy[2 * r + 1] = (double)Y / (double)P;
+        edge[r] = 4 + cc;
+        gidx[r] = (X > 0 && X < P && Y > 0 && Y < P) ? 2 * P * (P - 1) * q + (Y - 1) * (P - 1) + (X - 1) : -1;
+    }
 }
 
-/* out[0]=m  out[1]=G  out[2]=faces  out[3]=N  */
+/* Global flux equation of flux row ar (0 .. orc_na - 1) of subdomain s, or -1 (Dirichlet edge or
+ * a corner on dOmega).  Edge points: the face unknown's index f*q + k (one equation per face
+ * point, the two subdomains' rows summed: A = [A^1 ... A^N]).  Layout 1, corner cc of
+ * s at the cross point X (index x): one equation per face incident to X, numbered after the face
+ * equations at Gf + 4x + t, t = 0 the vertical face below X, 1 above, 2 the horizontal face left
+ * of X, 3 right -- each summing the rows of the two subdomains that share that face.           */
+int orc_flux_eq(const orc_cfg *c, int s, int ar) {
+    int P = c->P, q = c->q, i = s % P, j = s / P;
+    if (ar < 4 * q) {
+        int f = face_of(c, i, j, ar / q);
+        return f >= 0 ? f * q + ar % q : -1;
+    }
+    int cc = (ar - 4 * q) / 2, d = (ar - 4 * q) % 2, ci = cc & 1, cj = cc >> 1, X = i + ci, Y = j + cj;
+    if (!(X > 0 && X < P && Y > 0 && Y < P)) return -1;
+    int x = (Y - 1) * (P - 1) + (X - 1);
+    int t = d == 0 ? (cj == 1 ? 0 : 1) : (ci == 1 ? 2 : 3);
+    return 2 * P * (P - 1) * q + 4 * x + t;
+}
+
+/* out[0]=m  out[1]=G (interface unknowns)  out[2]=faces  out[3]=N  out[4]=flux equations
+ * out[5]=flux rows per subdomain */
 void orc_geometry(const orc_cfg *c, int64_t *out) {
-    int64_t P = c->P;
+    int64_t P = c->P, X = c->layout == 1 ? (P - 1) * (P - 1) : 0;
     out[0] = orc_mk(c);
     out[2] = 2 * P * (P - 1);
-    out[1] = out[2] * c->q;
+    out[1] = out[2] * c->q + X;
     out[3] = P * P;
+    out[4] = out[2] * c->q + 4 * X;
+    out[5] = orc_na(c);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -341,21 +381,20 @@ void orc_rho(double x, double y, double *rho, double *rx, double *ry) {
 /*   F^s = [f(x_i); g(x_b); 0], g = u_exact on dOmega (reading R3)                            */
 /*   sigma = tanh, sigma' = 1 - sigma^2, sigma'' = -2 sigma sigma'                             */
 /* ------------------------------------------------------------------------------------------ */
-/* K: m x M column-major (ld m).  F: m.  A: 4q x M column-major (ld 4q), row e*q+k = flux row
- * of edge e point k (zero rows for Dirichlet edges).                                          */
+/* K: m x M column-major (ld m).  F: m.  A: na x M column-major (ld na = orc_na), row e*q+k =
+ * flux row of edge e point k, rows 4q + 2cc + d of corner cc (layout 1; see orc_na); zero rows
+ * where there is no interface.                                                                 */
 void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, double *K, double *F,
                   double *A) {
-    int M = c->M, q = c->q, m = orc_m(c), mk = orc_mk(c);
+    int M = c->M, q = c->q, m = orc_m(c), mk = orc_mk(c), na = orc_na(c), pp = c->p * c->p;
     double *xy = (double *)malloc(sizeof(double) * 2 * (size_t)mk);
     int32_t *edge = (int32_t *)malloc(sizeof(int32_t) * (size_t)mk);
     int32_t *gidx = (int32_t *)malloc(sizeof(int32_t) * (size_t)mk);
     orc_rows(c, s, xy, edge, gidx);
-    for (int r = m; r < mk; ++r) { /* reading R29: lambda e_j^T, right-hand side 0 */
-        F[r] = 0.0;
-        for (int n = 0; n < M; ++n) K[(size_t)n * mk + r] = (r - m == n) ? c->tikhonov : 0.0;
-    }
     static const double nx[4] = {-1.0, 1.0, 0.0, 0.0};
     static const double ny[4] = {0.0, 0.0, -1.0, 1.0};
+    if (A)
+        for (size_t t = 0; t < (size_t)na * M; ++t) A[t] = 0.0;
     const double *Ws = W + (size_t)2 * s * M;
     const double *bs = b + (size_t)s * M;
     const int np = orc_npts(c);
@@ -389,7 +428,7 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
                     int e = edge[r];
                     int ar = r - (m - 4 * q);
                     double wn = wx * nx[e] + wy * ny[e];
-                    A[(size_t)n * 4 * q + ar] =
+                    A[(size_t)n * na + ar] =
                         gidx[r] >= 0 ? (ROW_KIND(r) == 0 ? wn * d1 : w2 * wn * d3) : 0.0; /* d/dn phi, d/dn Lap phi */
                 }
                 continue;
@@ -406,11 +445,31 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
                 val = t;
             }
             K[(size_t)n * mk + r] = val;
-            if (edge[r] >= 0 && A) {
+            if (edge[r] >= 0 && edge[r] < 4 && A) {
                 int e = edge[r];
-                int ar = r - (m - 4 * q); /* = e*q + k */
-                A[(size_t)n * 4 * q + ar] = gidx[r] >= 0 ? (wx * nx[e] + wy * ny[e]) * d1 : 0.0;
+                int ar = r - pp; /* = e*q + k */
+                A[(size_t)n * na + ar] = gidx[r] >= 0 ? (wx * nx[e] + wy * ny[e]) * d1 : 0.0;
+            } else if (edge[r] >= 4 && A && gidx[r] >= 0) {
+                /* corner remark: one flux row per edge through the corner, with that
+                 * edge's outward normal: d = 0 the vertical edge (left or right), d = 1 the
+                 * horizontal edge (bottom or top) */
+                int cc = edge[r] - 4, ci = cc & 1, cj = cc >> 1;
+                A[(size_t)n * na + 4 * q + 2 * cc] = (ci ? wx : -wx) * d1;
+                A[(size_t)n * na + 4 * q + 2 * cc + 1] = (cj ? wy : -wy) * d1;
             }
+        }
+    }
+    if (mk > m) { /* reading R29: damping rows lambda e_j^T, right-hand side 0 */
+        double lam = c->tikhonov;
+        if (lam < 0.0) { /* reading R33: lambda_s = sqrt(eps) ||K^s||_F over the collocation rows */
+            double f2 = 0.0;
+            for (int n = 0; n < M; ++n)
+                for (int r = 0; r < m; ++r) f2 += K[(size_t)n * mk + r] * K[(size_t)n * mk + r];
+            lam = sqrt(f2) * 0x1.0p-26;
+        }
+        for (int r = m; r < mk; ++r) {
+            F[r] = 0.0;
+            for (int n = 0; n < M; ++n) K[(size_t)n * mk + r] = (r - m == n) ? lam : 0.0;
         }
     }
     free(xy);
@@ -489,28 +548,29 @@ static void back_subst(int n, const double *A, int lda, double *z) {
 /* per-subdomain literal pieces of eqn:schur                                       */
 /* ------------------------------------------------------------------------------------------ */
 typedef struct {
-    int m, M, mg;         /* rows, neurons, interface points m_Gamma^s */
+    int m, M, mg, ma;     /* rows, neurons, interface points m_Gamma^s, flux rows */
     double *K;            /* factored K^s (m x M) */
     double *tau;          /* M */
     double *F;            /* m */
     int32_t *irow;        /* [mg] row of K^s for interface point k */
     int32_t *ig;          /* [mg] global index of interface point k */
-    double *Aflux;        /* [mg x M] row-major: flux rows at interface points */
+    int32_t *aeq;         /* [ma] global flux equation of flux row k (orc_flux_eq) */
+    double *Aflux;        /* [ma x M] row-major: the flux rows (layout 0: one per interface point) */
     double *S1;           /* B^T (I - K K^+) B: mg x mg */
     double *g1;           /* B^T (I - K K^+) F: mg */
-    double *PB;           /* A K^+ B: mg x mg row-major (rows = flux rows = interface points) */
-    double *pF;           /* A K^+ F: mg */
+    double *PB;           /* A K^+ B: ma x mg row-major (rows = flux rows) */
+    double *pF;           /* A K^+ F: ma */
 } orc_local;
 
 static void local_free(orc_local *L) {
-    free(L->K); free(L->tau); free(L->F); free(L->irow); free(L->ig); free(L->Aflux);
+    free(L->K); free(L->tau); free(L->F); free(L->irow); free(L->ig); free(L->aeq); free(L->Aflux);
     free(L->S1); free(L->g1); free(L->PB); free(L->pF);
     memset(L, 0, sizeof(*L));
 }
 
 /* Steps 2-5 of the oracle for one subdomain. */
 static void local_build(const orc_cfg *c, int s, const double *W, const double *b, orc_local *L) {
-    int M = c->M, q = c->q, m0 = orc_m(c), m = orc_mk(c); /* collocation rows, rows of K^s */
+    int M = c->M, m = orc_mk(c), na = orc_na(c); /* rows of K^s, flux rows of A^s */
     L->m = m;
     L->M = M;
     double *xy = (double *)malloc(sizeof(double) * 2 * (size_t)m);
@@ -525,18 +585,28 @@ static void local_build(const orc_cfg *c, int s, const double *W, const double *
     L->F = (double *)malloc(sizeof(double) * (size_t)m);
     L->irow = (int32_t *)malloc(sizeof(int32_t) * (size_t)(mg + 1));
     L->ig = (int32_t *)malloc(sizeof(int32_t) * (size_t)(mg + 1));
-    double *A4 = (double *)calloc((size_t)4 * q * M, sizeof(double));
+    double *A4 = (double *)calloc((size_t)na * M, sizeof(double));
     orc_assemble(c, s, W, b, L->K, L->F, A4);
-    L->Aflux = (double *)malloc(sizeof(double) * (size_t)(mg + 1) * M);
     int k = 0;
     for (int r = 0; r < m; ++r)
         if (gidx[r] >= 0) {
             L->irow[k] = r;
             L->ig[k] = gidx[r];
-            int ar = r - (m0 - 4 * q);
-            for (int n = 0; n < M; ++n) L->Aflux[(size_t)k * M + n] = A4[(size_t)n * 4 * q + ar];
             ++k;
         }
+    int ma = 0;
+    for (int ar = 0; ar < na; ++ar) ma += orc_flux_eq(c, s, ar) >= 0;
+    L->ma = ma;
+    L->aeq = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ma + 1));
+    L->Aflux = (double *)malloc(sizeof(double) * (size_t)(ma + 1) * M);
+    k = 0;
+    for (int ar = 0; ar < na; ++ar) {
+        int eq = orc_flux_eq(c, s, ar);
+        if (eq < 0) continue;
+        L->aeq[k] = eq;
+        for (int n = 0; n < M; ++n) L->Aflux[(size_t)k * M + n] = A4[(size_t)n * na + ar];
+        ++k;
+    }
     free(A4);
     free(xy);
     free(edge);
@@ -581,9 +651,9 @@ static void local_build(const orc_cfg *c, int s, const double *W, const double *
      * carries its own resolution of the near-null space and the flux term loses all accuracy
      * (reading R23: u_Gamma error 1.4e-2 vs 1.6e-11 at config 1).                  */
     double *wr = (double *)malloc(sizeof(double) * (size_t)M);
-    L->PB = (double *)malloc(sizeof(double) * (size_t)(mg + 1) * (mg + 1));
-    L->pF = (double *)malloc(sizeof(double) * (size_t)(mg + 1));
-    for (k = 0; k < mg; ++k) {
+    L->PB = (double *)malloc(sizeof(double) * (size_t)(ma + 1) * (mg + 1));
+    L->pF = (double *)malloc(sizeof(double) * (size_t)(ma + 1));
+    for (k = 0; k < ma; ++k) {
         const double *a = L->Aflux + (size_t)k * M;
         for (int i = 0; i < M; ++i) { /* R^T w = a, R^T lower triangular */
             double sacc = a[i];
@@ -929,13 +999,16 @@ static int iface_band(const orc_cfg *c, const orc_local *L, int N, int64_t G, in
     for (int64_t a = 0; a < 2 * G; ++a) own_s[a] = own_k[a] = -1;
     for (int s = 0; s < N; ++s) {
         const orc_local *Ls = &L[s];
+        for (int k = 0; k < Ls->ma; ++k) {  /* layout 0 (the only one on this route): equation = unknown */
+            int64_t ek = Ls->aeq[k];
+            qg[ek] += Ls->pF[k];
+            int slot = own_s[2 * ek] < 0 ? 0 : 1;
+            own_s[2 * ek + slot] = s;
+            own_k[2 * ek + slot] = k;
+        }
         for (int k = 0; k < Ls->mg; ++k) {
             int64_t gk = Ls->ig[k];
             g[gk] += Ls->g1[k];
-            qg[gk] += Ls->pF[k];
-            int slot = own_s[2 * gk] < 0 ? 0 : 1;
-            own_s[2 * gk + slot] = s;
-            own_k[2 * gk + slot] = k;
             double *Mk = Mb + (size_t)gk * w;
             for (int l = 0; l < Ls->mg; ++l) {
                 int64_t gl = Ls->ig[l];
@@ -990,12 +1063,13 @@ static int iface_band(const orc_cfg *c, const orc_local *L, int N, int64_t G, in
 int orc_solve(const orc_cfg *c, const double *W, const double *b, int nthreads, double *uG,
               double *coef, double *resid, const double *xy_eval, int64_t n_eval, double *u_eval,
               double *Mout, double *gout, double *times, int band) {
-    int64_t geo[4];
+    int64_t geo[6];
     orc_geometry(c, geo);
     int64_t G = geo[1];
     int N = (int)geo[3];
     if (band == 0) band = G > 20000 ? 2 : 1;
     if (band == 1 && G > 20000) return 1;
+    if (band == 2 && c->layout != 0) return 3; /* cross points are outside the strip-order band */
     double t0 = now_s();
     orc_local *L = (orc_local *)calloc((size_t)N, sizeof(orc_local));
     solve_ctx X = {c, W, b, L, uG, coef, resid};
@@ -1022,26 +1096,33 @@ int orc_solve(const orc_cfg *c, const double *W, const double *b, int nthreads, 
     }
 
     /* global pieces: sum in ascending s (step 5-6 of SURVEY §8(c)) */
+    const int64_t NE = geo[4]; /* flux equations: rows of A K^+ B (= G in layout 0) */
     double *Mm = (double *)calloc((size_t)(G > 0 ? G : 1) * (G > 0 ? G : 1), sizeof(double));
     double *g = (double *)calloc((size_t)(G > 0 ? G : 1), sizeof(double));
-    double *Qg = (double *)calloc((size_t)(G > 0 ? G : 1) * (G > 0 ? G : 1), sizeof(double)); /* A K^+ B */
-    double *qg = (double *)calloc((size_t)(G > 0 ? G : 1), sizeof(double));                   /* A K^+ F */
+    double *Qg = (double *)calloc((size_t)(NE > 0 ? NE : 1) * (G > 0 ? G : 1), sizeof(double)); /* A K^+ B */
+    double *qg = (double *)calloc((size_t)(NE > 0 ? NE : 1), sizeof(double));                   /* A K^+ F */
     for (int s = 0; s < N; ++s) {
         orc_local *Ls = &L[s];
         for (int k = 0; k < Ls->mg; ++k) {
             int gk = Ls->ig[k];
             g[gk] += Ls->g1[k];
-            qg[gk] += Ls->pF[k];
             for (int l = 0; l < Ls->mg; ++l) {
                 int gl = Ls->ig[l];
                 Mm[(size_t)gk * G + gl] += Ls->S1[(size_t)k * Ls->mg + l];
-                Qg[(size_t)gk * G + gl] += Ls->PB[(size_t)k * Ls->mg + l];
+            }
+        }
+        for (int k = 0; k < Ls->ma; ++k) {
+            int ek = Ls->aeq[k];
+            qg[ek] += Ls->pF[k];
+            for (int l = 0; l < Ls->mg; ++l) {
+                int gl = Ls->ig[l];
+                Qg[(size_t)ek * G + gl] += Ls->PB[(size_t)k * Ls->mg + l];
             }
         }
     }
     /* (AK^+B)^T (AK^+B) and (AK^+B)^T (AK^+F), row by row of AK^+B over its nonzeros */
     int32_t *nz = (int32_t *)malloc(sizeof(int32_t) * (size_t)(G > 0 ? G : 1));
-    for (int64_t a = 0; a < G; ++a) {
+    for (int64_t a = 0; a < NE; ++a) {
         const double *row = Qg + (size_t)a * G;
         int nnz = 0;
         for (int64_t k = 0; k < G; ++k)
@@ -1088,20 +1169,22 @@ int orc_solve(const orc_cfg *c, const double *W, const double *b, int nthreads, 
 }
 
 /* Per-subdomain pieces for sampled checks at sizes where the full oracle is too slow.
- * Outputs (nullable): S1 (mg x mg row-major), g1 (mg), PB (mg x mg), pF (mg), ig (mg),
- * and -- given a global u_Gamma -- coef (M) and resid.  Returns mg.                         */
+ * Outputs (nullable): S1 (mg x mg row-major), g1 (mg), PB (ma x mg), pF (ma), ig (mg), aeq (ma),
+ * *ma_out, and -- given a global u_Gamma -- coef (M) and resid.  Returns mg.                    */
 int orc_local_pieces(const orc_cfg *c, int s, const double *W, const double *b, const double *uG,
                      double *S1, double *g1, double *PB, double *pF, int32_t *ig, double *coef,
-                     double *resid) {
+                     double *resid, int32_t *aeq, int32_t *ma_out) {
     orc_local L;
     memset(&L, 0, sizeof(L));
     local_build(c, s, W, b, &L);
-    int mg = L.mg;
+    int mg = L.mg, ma = L.ma;
     if (S1) memcpy(S1, L.S1, sizeof(double) * (size_t)mg * mg);
     if (g1) memcpy(g1, L.g1, sizeof(double) * (size_t)mg);
-    if (PB) memcpy(PB, L.PB, sizeof(double) * (size_t)mg * mg);
-    if (pF) memcpy(pF, L.pF, sizeof(double) * (size_t)mg);
+    if (PB) memcpy(PB, L.PB, sizeof(double) * (size_t)ma * mg);
+    if (pF) memcpy(pF, L.pF, sizeof(double) * (size_t)ma);
     if (ig) memcpy(ig, L.ig, sizeof(int32_t) * (size_t)mg);
+    if (aeq) memcpy(aeq, L.aeq, sizeof(int32_t) * (size_t)ma);
+    if (ma_out) *ma_out = ma;
     if (uG && coef && resid) local_back(&L, uG, coef, resid);
     local_free(&L);
     return mg;

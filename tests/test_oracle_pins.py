@@ -26,7 +26,8 @@ def mkcfg(k=None, **kw):
         c = dict(P=2, M=16, p=6, q=5, problem=0, seed=7, init_scheme=0, init_c=0.125, r_over_diam=0.5)
         c.update(kw)
     return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0),
-                 c.get("init_c", 0.125), c.get("r_over_diam", 0.5), c["seed"], c.get("tikhonov", 0.0))
+                 c.get("init_c", 0.125), c.get("r_over_diam", 0.5), c["seed"], c.get("tikhonov", 0.0),
+                 c.get("layout", 0))
 
 
 # ------------------------------------------------------------------------------------------------
@@ -335,24 +336,25 @@ def test_band_route_equals_dense_route(kw):
 
 
 # ------------------------------------------------------------------------------------------------
-# Schur system (eqn:eliminated P:351-373, LS_system P:398-406, eqn:schur P:407-410)# ------------------------------------------------------------------------------------------------
 # Schur system (eqn:eliminated P:351-373, LS_system P:398-406, eqn:schur P:407-410)
 # ------------------------------------------------------------------------------------------------
 def _global_blocks(c, W, b):
     """Dense K (block diag), B (stacked -E), A (flux rows, globally indexed), F, from the oracle's
     assembly; numpy builds everything else."""
     geo = O.geometry(c)
-    N, G, M = geo["N"], geo["G"], c.M
+    N, G, M, NE = geo["N"], geo["G"], c.M, geo["NE"]
     Ks, Fs, Bs, As = [], [], [], []
     for s in range(N):
         K, F, A4 = O.assemble(c, s, W, b)
         xy, edge, gidx = O.rows(c, s)
-        m = len(edge)  # collocation rows p^2 + 4q, then (tikhonov > 0) the M damping rows
+        m = len(edge)  # collocation rows, then (tikhonov != 0) the M damping rows
         B = np.zeros((m, G))
-        Ag = np.zeros((G, M))
+        Ag = np.zeros((NE, M))
         for r in np.where(gidx >= 0)[0]:
             B[r, gidx[r]] = -1.0
-            Ag[gidx[r]] += A4[r - c.p * c.p]
+        for ar, eq in enumerate(O.flux_eq(c, s)):  # A = [A^1 ... A^N] by global flux equation
+            if eq >= 0:
+                Ag[eq] += A4[ar]
         Ks.append(K)
         Fs.append(F)
         Bs.append(B)
@@ -369,10 +371,11 @@ def _tiny_cfg(P=2, **kw):
     return mkcfg(**base)
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_schur_matches_literal_eqn_schur(P):
-    """Oracle M, g == B^T (I + K^{+T} A^T A K^+ - K K^+) B and ... F with np.linalg.pinv."""
-    c = _tiny_cfg(P)
+@pytest.mark.parametrize("P,layout", [(2, 0), (3, 0), (2, 1), (3, 1)])
+def test_schur_matches_literal_eqn_schur(P, layout):
+    """Oracle M, g == B^T (I + K^{+T} A^T A K^+ - K K^+) B and ... F with np.linalg.pinv (P:409);
+    layout 1: the shared lattice with cross points and the corner flux rows (R32)."""
+    c = _tiny_cfg(P, layout=layout, q=7)
     W, b, _, _ = O.init_hidden(c)
     K, B, A, F = _global_blocks(c, W, b)
     assert np.linalg.cond(K) < 1e8
@@ -388,13 +391,14 @@ def test_schur_matches_literal_eqn_schur(P):
     assert np.linalg.eigvalsh(r["M"]).min() > 0      # SPD
 
 
-@pytest.mark.parametrize("P,lam", [(2, 0.0), (3, 0.0), (2, 0.05), (3, 0.3)])
-def test_schur_solution_equals_monolithic_lstsq_of_eliminated_system(P, lam):
+@pytest.mark.parametrize("P,lam,layout", [(2, 0.0, 0), (3, 0.0, 0), (2, 0.05, 0), (3, 0.3, 0), (2, 0.0, 1),
+                                          (3, 0.0, 1), (3, 0.3, 1)])
+def test_schur_solution_equals_monolithic_lstsq_of_eliminated_system(P, lam, layout):
     """Central equivalence: (c, u_Gamma) of the Schur route == the least-squares solution of the
     monolithic eqn:eliminated system [[K, B], [0, -AK^+B]] [c; u] = [F; -AK^+F].
     With Tikhonov damping (reading R29) K is the stacked [K; lam I] of every subdomain, B and F
     zero on the damping rows: the same identity then pins the damped route."""
-    c = _tiny_cfg(P, tikhonov=lam)
+    c = _tiny_cfg(P, tikhonov=lam, layout=layout, q=7 if layout else 6)
     W, b, _, _ = O.init_hidden(c)
     K, B, A, F = _global_blocks(c, W, b)
     Kp = np.linalg.pinv(K)
@@ -700,3 +704,114 @@ def test_tikhonov_single_subdomain_closed_form():
     assert np.allclose(r["coef"][0], ref, rtol=0, atol=1e-9 * np.abs(ref).max())
     rr = np.sqrt(np.linalg.norm(K @ ref - F) ** 2 + lam * lam * np.linalg.norm(ref) ** 2)
     assert abs(r["resid"][0] - rr) <= 1e-9 * rr
+
+
+# ------------------------------------------------------------------------------------------------
+# the paper's shared lattice with cross points (readings R32, R33)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("P,n", [(2, 4), (3, 5), (4, 3)])
+def test_lattice_geometry(P, n):
+    """Layout 1: the rows of all subdomains are exactly the (P n + 1)^2 points of the global
+    lattice ("distributed to each subdomain"), (n+1)^2 per subdomain; face points are shared
+    by 2 subdomains and cross points (interior subdomain corners) by 4, each one interface unknown
+    (G = 2P(P-1)(n-1) + (P-1)^2); every flux equation (one per face point, and per cross point one
+    per incident face: the corner remark) has exactly two contributors whose normals
+    are opposite (continuity of the flux)."""
+    c = mkcfg(P=P, M=8, p=n - 1, q=n - 1, problem=0, seed=1, layout=1)
+    geo = O.geometry(c)
+    q = n - 1
+    assert geo["m"] == (n + 1) ** 2
+    assert geo["G"] == 2 * P * (P - 1) * q + (P - 1) ** 2
+    assert geo["NE"] == 2 * P * (P - 1) * q + 4 * (P - 1) ** 2
+    pts = {}
+    owners = {}
+    for s in range(P * P):
+        xy, edge, gidx = O.rows(c, s)
+        for (x, y), g in zip(xy, gidx):
+            key = (round(x * P * n), round(y * P * n))
+            assert abs(x * P * n - key[0]) < 1e-9 and abs(y * P * n - key[1]) < 1e-9
+            pts.setdefault(key, set()).add(g)
+            if g >= 0:
+                owners.setdefault(g, []).append(s)
+    assert set(pts) == {(a, b) for a in range(P * n + 1) for b in range(P * n + 1)}
+    assert all(len(v) == 1 for v in pts.values())          # one unknown per shared point
+    cnt = [len(owners[g]) for g in sorted(owners)]
+    assert sorted(owners) == list(range(geo["G"]))
+    assert cnt == [2] * (geo["G"] - (P - 1) ** 2) + [4] * (P - 1) ** 2
+    W, b, _, _ = O.init_hidden(c)
+    contrib = {}
+    for s in range(P * P):
+        _, _, A = O.assemble(c, s, W, b)
+        for ar, eq in enumerate(O.flux_eq(c, s)):
+            if eq >= 0:
+                contrib.setdefault(int(eq), []).append(A[ar])
+    assert sorted(contrib) == list(range(geo["NE"]))
+    assert all(len(rows) == 2 for rows in contrib.values())  # (opposite normals: next test)
+
+
+def test_lattice_corner_flux_rows():
+    """Corner remark: a cross point gets one flux row per edge through the corner,
+    with that edge's outward normal; each row equals the central difference of np.tanh(w.x + b)
+    along the normal.  Corners on the boundary are Dirichlet value rows (g = u_exact) with no flux
+    rows.  The two rows of every cross-point equation use opposite normals."""
+    P, n = 3, 4
+    c = mkcfg(P=P, M=6, p=n - 1, q=n - 1, problem=0, seed=3, layout=1)
+    W, b, _, _ = O.init_hidden(c)
+    q, pp = n - 1, (n - 1) ** 2
+    normals = {}
+    for s in range(P * P):
+        i, j = s % P, s // P
+        K, F, A = O.assemble(c, s, W, b)
+        xy, edge, gidx = O.rows(c, s)
+        eqs = O.flux_eq(c, s)
+        for cc in range(4):
+            r = pp + 4 * q + cc
+            ci, cj = cc & 1, cc >> 1
+            x, y = xy[r]
+            assert (x, y) == ((i + ci) / P, (j + cj) / P)
+            phi = lambda xx, yy: np.tanh(W[s][:, 0] * xx + W[s][:, 1] * yy + b[s])  # noqa: E731
+            assert np.allclose(K[r], phi(x, y), rtol=0, atol=1e-15)
+            interior = 0 < i + ci < P and 0 < j + cj < P
+            assert (gidx[r] >= 0) == interior
+            for d in range(2):
+                ar = 4 * q + 2 * cc + d
+                nrm = ((1.0 if ci else -1.0), 0.0) if d == 0 else (0.0, (1.0 if cj else -1.0))
+                if not interior:
+                    assert eqs[ar] == -1 and np.all(A[ar] == 0.0)
+                    continue
+                h = 1e-6
+                fd = (phi(x + h * nrm[0], y + h * nrm[1]) - phi(x - h * nrm[0], y - h * nrm[1])) / (2 * h)
+                assert np.allclose(A[ar], fd, rtol=1e-6, atol=1e-8)
+                normals.setdefault(int(eqs[ar]), []).append(nrm)
+            if not interior:
+                u, _ = O.problem(0, x, y)
+                assert F[r] == u
+    assert len(normals) == 4 * (P - 1) ** 2
+    for nr in normals.values():
+        assert len(nr) == 2 and nr[0][0] == -nr[1][0] and nr[0][1] == -nr[1][1]
+
+
+def test_lattice_single_subdomain_is_classical_elm():
+    """P = 1 on the lattice: all (n+1)^2 points, corners included, are collocation rows; no
+    interface, and c = argmin ||K c - F|| (the paper's N = 1 x 1 row of Table 2)."""
+    c = mkcfg(P=1, M=30, p=9, q=9, problem=4, seed=9, init_c=0.125, layout=1)
+    W, b, _, _ = O.init_hidden(c)
+    K, F, _ = O.assemble(c, 0, W, b)
+    assert K.shape[0] == 11 * 11 and O.geometry(c)["G"] == 0
+    r = O.solve(c, W, b)
+    ref = np.linalg.lstsq(K, F, rcond=None)[0]
+    assert np.allclose(K @ r["coef"][0], K @ ref, rtol=0, atol=1e-9 * np.abs(F).max())
+
+
+def test_damping_rule_sqrt_eps_frobenius():
+    """Reading R33: tikhonov < 0 selects lambda_s = sqrt(eps) ||K^s||_F (the collocation rows) in
+    every subdomain -- the damped [K; lambda I] has condition number <= ||K||_F / lambda = 2^26."""
+    c = mkcfg(P=2, M=20, p=5, q=5, problem=4, seed=2, layout=1, tikhonov=-1.0)
+    W, b, _, _ = O.init_hidden(c)
+    m = (5 + 1 + 1) ** 2
+    for s in range(4):
+        K, F, _ = O.assemble(c, s, W, b)
+        assert K.shape[0] == m + 20
+        lam = np.sqrt(np.sum(K[:m] ** 2)) * 2.0 ** -26
+        assert np.allclose(np.diag(K[m:]), lam, rtol=1e-14, atol=0)
+        assert np.all(K[m:] - np.diag(np.diag(K[m:])) == 0.0) and np.all(F[m:] == 0.0)
