@@ -82,13 +82,21 @@ typedef struct {
     int32_t s_begin, s_end; /* subdomains owned by this rank: [s_begin, s_end) of 0..N-1       */
     int32_t interface_mode; /* factorisation order of the Schur matrix: 0 auto (less work) |
                                1, 2 strip order (envelope) | 3 nested dissection             */
-    int32_t reserved;
-    double tikhonov;        /* lambda >= 0 (0: off).  lambda > 0 appends M rows lambda e_j^T (right-
+    int32_t layout;         /* collocation layout: 0 face points (reading R1: p x p interior + q per
+                               edge, endpoints excluded) | 1 the paper's shared lattice (P:436-438,
+                               reading R32; p == q == n - 1 for n lattice cells per subdomain side):
+                               the 4 subdomain corners are rows too, interior corners are cross
+                               points -- interface unknowns shared by 4 subdomains, numbered after
+                               the face unknowns -- with one flux row per edge through the corner
+                               (the corner remark); interface solved densely (G small)  */
+    double tikhonov;        /* lambda (0: off).  lambda > 0 appends M rows lambda e_j^T (right-
                                hand side 0) to every K^s, i.e. each local LS becomes
                                min ||K c - r||^2 + lambda^2 ||c||^2 (reading R29): the near-square,
                                numerically rank-deficient local problems of the paper's Table 2
                                need such damping of K^{s+} (the paper's least-squares solver
-                               truncates).  ld = round_up(m + M, 32); r_s includes lambda ||c||.  */
+                               truncates).  ld = round_up(m + M, 32); r_s includes lambda ||c||.
+                               lambda < 0: the fixed rule lambda_s = eps max(m, M) ||K^s||_F per
+                               subdomain (reading R33; the collocation rows' Frobenius norm).    */
 } elmddm_config;
 
 typedef struct {
@@ -116,6 +124,9 @@ typedef struct {
     int64_t chol_ordering;                  /* 0 strip (envelope), 1 nested dissection            */
     int64_t e_impl_begin, e_impl_end;       /* implicit E_Gamma columns [begin, end) of K_aug: not
                                                written by elmddm_assemble (see there)             */
+    int64_t ne;         /* E_Gamma columns per subdomain: 4q (layout 0) | 4q + 4 (layout 1)      */
+    int64_t na;         /* flux rows per subdomain (rows of At): 4q | 4q + 8                     */
+    int64_t n_eq;       /* global flux equations (rows of Q): G (layout 0) | faces q + 4 (P-1)^2  */
 } elmddm_sizes_t;
 
 /* ---- context ------------------------------------------------------------------------------ */

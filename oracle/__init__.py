@@ -81,7 +81,7 @@ def _p(a):
 def cfg(P, M, p, q, problem=0, init_scheme=0, init_c=0.125, r_over_diam=0.5, seed=0, tikhonov=0.0,
         layout=0) -> Cfg:
     """layout 0: face points (reading R1); 1: the paper's shared lattice with cross points (R32,
-    p == q).  tikhonov < 0: the fixed rule lambda_s = sqrt(eps) ||K^s||_F (R33)."""
+    p == q).  tikhonov < 0: the fixed rule lambda_s = eps max(m, M) ||K^s||_F (R33)."""
     return Cfg(P, M, p, q, problem, init_scheme, init_c, r_over_diam, seed, tikhonov, layout)
 
 

@@ -42,7 +42,7 @@ typedef struct {
     double r_over_diam;     /* r = r_over_diam * diam(Omega_s), P:546 (1/2) */
     uint64_t seed;
     double tikhonov;        /* lambda >= 0: M extra rows lambda * e_j^T of K^s (reading R29);
-                               < 0: the fixed rule lambda_s = sqrt(eps) ||K^s||_F (reading R33) */
+                               < 0: the fixed rule lambda_s = eps max(m, M) ||K^s||_F (R33)      */
     int32_t layout;         /* 0: face points (reading R1); 1: the paper's shared lattice with
                                cross points (reading R32), p == q        */
 } orc_cfg;
@@ -461,11 +461,11 @@ void orc_assemble(const orc_cfg *c, int s, const double *W, const double *b, dou
     }
     if (mk > m) { /* reading R29: damping rows lambda e_j^T, right-hand side 0 */
         double lam = c->tikhonov;
-        if (lam < 0.0) { /* reading R33: lambda_s = sqrt(eps) ||K^s||_F over the collocation rows */
+        if (lam < 0.0) { /* reading R33: lambda_s = eps max(m, M) ||K^s||_F over the collocation rows */
             double f2 = 0.0;
             for (int n = 0; n < M; ++n)
                 for (int r = 0; r < m; ++r) f2 += K[(size_t)n * mk + r] * K[(size_t)n * mk + r];
-            lam = sqrt(f2) * 0x1.0p-26;
+            lam = sqrt(f2) * (0x1.0p-52 * (double)(m > M ? m : M));
         }
         for (int r = m; r < mk; ++r) {
             F[r] = 0.0;

@@ -23,7 +23,7 @@ class Config(C.Structure):
         ("P", C.c_int32), ("M", C.c_int32), ("p", C.c_int32), ("q", C.c_int32),
         ("problem", C.c_int32), ("init_scheme", C.c_int32),
         ("init_c", C.c_double), ("r_over_diam", C.c_double), ("seed", C.c_uint64),
-        ("s_begin", C.c_int32), ("s_end", C.c_int32), ("interface_mode", C.c_int32), ("reserved", C.c_int32),
+        ("s_begin", C.c_int32), ("s_end", C.c_int32), ("interface_mode", C.c_int32), ("layout", C.c_int32),
         ("tikhonov", C.c_double),
     ]
 
@@ -33,7 +33,7 @@ class Sizes(C.Structure):
         "N", "S", "m", "ld", "ncols", "kaug", "G", "faces", "kaug_elems", "at_elems", "tau_elems",
         "pbuf_ld", "pbuf_elems", "sbuf_ld", "sbuf_elems", "work_elems", "band_ld", "band_nbw", "band_elems",
         "G_pad", "halfband", "chol_tasks", "chol_flops", "chol_n", "chol_blocks", "chol_ordering",
-        "e_impl_begin", "e_impl_end")]
+        "e_impl_begin", "e_impl_end", "ne", "na", "n_eq")]
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -138,6 +138,14 @@ __device__ __forceinline__ void row_point(const elmddm_config& c, int i, int j, 
         return;
     }
     r -= pp;
+    if (r >= 4 * q && c.layout == 1 && r < 4 * q + 4) {  // lattice corner cc = (ci, cj): kind 4 + cc
+        const int cc = r - 4 * q;
+        x = (double)(i + (cc & 1)) / (double)P;
+        y = (double)(j + (cc >> 1)) / (double)P;
+        kind = 4 + cc;
+        k = 0;
+        return;
+    }
     if (r >= 4 * q) {
         kind = -2;
         x = y = 0.0;
@@ -160,12 +168,18 @@ __device__ __forceinline__ void row_point(const elmddm_config& c, int i, int j, 
     }
 }
 
+// edge e < 4 of subdomain (i, j) is an interface face; e = 4 + cc: the lattice corner cc is a
+// cross point (inside the domain)
 __device__ __forceinline__ bool edge_is_interface(int P, int i, int j, int e) {
     switch (e) {
         case 0: return i > 0;
         case 1: return i < P - 1;
         case 2: return j > 0;
-        default: return j < P - 1;
+        case 3: return j < P - 1;
+        default: {
+            const int X = i + ((e - 4) & 1), Y = j + ((e - 4) >> 1);
+            return X > 0 && X < P && Y > 0 && Y < P;
+        }
     }
 }
 
@@ -258,7 +272,8 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                                                     const double4* __restrict__ coef, int e_impl_begin,
                                                     int e_impl_end) {
     const int M = cfg.M, q = cfg.q, P = cfg.P, p = cfg.p, pp = p * p;
-    const int m = pp + 4 * q;
+    const int nc = cfg.layout == 1 ? 4 : 0;  // lattice corners (rows after the edge rows)
+    const int m = pp + 4 * q + nc, na = 4 * q + 2 * nc;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
     const int i = s % P, j = s / P;
     int c0 = blockIdx.x * AS_COLS;
@@ -303,14 +318,29 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
         // edge point from the same tables, times w . n_e (outward axis normal); one flux row per
         // thread, four 16-byte stores of neuron pairs.  Dirichlet edges are zero.
         {
-            double* Arow = At + (int64_t)sl * 4 * q * M;
-            for (int row = threadIdx.x; row < 4 * q; row += AS_NT) {
-                const int e = row / q, k = row - e * q;
-                const bool iface = edge_is_interface(P, i, j, e);
-                const int xi = e == 0 ? p : (e == 1 ? p + 1 : p + 2 + k);
-                const int yi = e == 2 ? p : (e == 3 ? p + 1 : p + 2 + k);
-                const bool nx = e < 2;                       // normal along x (e 0, 1) or y (e 2, 3)
-                const double sgn = (e & 1) ? 1.0 : -1.0;     // outward: left / bottom negative
+            double* Arow = At + (int64_t)sl * na * M;
+            for (int row = threadIdx.x; row < na; row += AS_NT) {
+                int e, k, xi, yi;
+                bool nx, iface;
+                double sgn;
+                if (row < 4 * q) {
+                    e = row / q;
+                    k = row - e * q;
+                    iface = edge_is_interface(P, i, j, e);
+                    xi = e == 0 ? p : (e == 1 ? p + 1 : p + 2 + k);
+                    yi = e == 2 ? p : (e == 3 ? p + 1 : p + 2 + k);
+                    nx = e < 2;                       // normal along x (e 0, 1) or y (e 2, 3)
+                    sgn = (e & 1) ? 1.0 : -1.0;       // outward: left / bottom negative
+                } else {  // lattice corner cc, d = 0: its vertical edge's normal, d = 1: horizontal
+                    const int cc = (row - 4 * q) >> 1, d = (row - 4 * q) & 1, ci = cc & 1, cj = cc >> 1;
+                    e = 4 + cc;
+                    k = 0;
+                    iface = edge_is_interface(P, i, j, e);
+                    xi = p + ci;
+                    yi = p + cj;
+                    nx = d == 0;
+                    sgn = (d == 0 ? ci : cj) ? 1.0 : -1.0;
+                }
                 double* dst = Arow + (int64_t)row * M + c0;
 #pragma unroll 1
                 for (int pr = 0; pr < AS_COLS; pr += 2) {
@@ -382,12 +412,17 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                     yi[e] = r / p;
                     kind[e] = 0;
                     if (OP == 1) rc[e] = coef[(int64_t)sl * pp + r];
-                } else if (r < m) {
+                } else if (r < pp + 4 * q) {
                     const int t = r - pp, ed = t / q, k = t % q;
                     kind[e] = 1;
                     lapt[e] = OP == 2 && k >= q / 2;
                     xi[e] = ed == 0 ? p : (ed == 1 ? p + 1 : p + 2 + k);
                     yi[e] = ed == 2 ? p : (ed == 3 ? p + 1 : p + 2 + k);
+                } else if (r < m) {  // lattice corner: a value row at (x0 or x0+h, y0 or y0+h)
+                    const int cc = r - pp - 4 * q;
+                    kind[e] = 1;
+                    xi[e] = p + (cc & 1);
+                    yi[e] = p + (cc >> 1);
                 } else {
                     kind[e] = 2;  // padding, or (reading R29) the damping row lambda e_{r-m}^T
                     xi[e] = yi[e] = 0;
@@ -417,7 +452,8 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
                                                    : w2s[cc] * sg;
                         v[e] = kind[e] == 0 ? lap * s1 : (kind[e] == 1 ? sg : 0.0);
                     }
-                    if (kind[e] == 2) v[e] = (2 * r2 + e - m == c0 + cc) ? cfg.tikhonov : 0.0;
+                    // (tikhonov < 0, reading R33: the per-subdomain lambda is written by k_damping)
+                    if (kind[e] == 2) v[e] = (2 * r2 + e - m == c0 + cc && cfg.tikhonov > 0.0) ? cfg.tikhonov : 0.0;
                 }
                 *reinterpret_cast<double2*>(Ks + (int64_t)(c0 + cc) * ld + 2 * r2) = make_double2(v[0], v[1]);
             }
@@ -429,9 +465,9 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
         const int col = c0 + cc;
         if (col >= ncols) break;
         if (col >= e_impl_begin && col < e_impl_end) continue;  // implicit: synthesised by the QR
-        if (col < M + 4 * q) {  // ld is even: 16-byte stores of row pairs
+        if (col < M + 4 * q + nc) {  // ld is even: 16-byte stores of row pairs
             const int t = col - M;
-            const int one = edge_is_interface(P, i, j, t / q) ? pp + t : -1;
+            const int one = edge_is_interface(P, i, j, t < 4 * q ? t / q : 4 + (t - 4 * q)) ? pp + t : -1;
             double2* dst = reinterpret_cast<double2*>(Ks + (int64_t)col * ld);
             for (int r2 = threadIdx.x; r2 < ld / 2; r2 += AS_NT)
                 dst[r2] = make_double2(2 * r2 == one ? 1.0 : 0.0, 2 * r2 + 1 == one ? 1.0 : 0.0);
@@ -455,6 +491,32 @@ __global__ void __launch_bounds__(AS_NT) k_assemble(elmddm_config cfg, int64_t l
             }
         }
     }
+}
+
+// Reading R33 (tikhonov < 0): lambda_s = eps max(m, M) ||K^s||_F over the m collocation rows, written
+// on the diagonal of the damping rows m .. m+M-1 (k_assemble left them zero).  grid S, 512 threads;
+// fixed-order reduction.
+__global__ void __launch_bounds__(512) k_damping(double* __restrict__ Kaug, int64_t ld, int64_t ncols, int m,
+                                                 int M) {
+    __shared__ double red[16];
+    double* Ks = Kaug + (int64_t)blockIdx.x * ld * ncols;
+    double ss = 0.0;
+    for (int n = 0; n < M; ++n)
+        for (int r = threadIdx.x; r < m; r += 512) {
+            const double v = Ks[(int64_t)n * ld + r];
+            ss = fma(v, v, ss);
+        }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 16; ++w) t += red[w];
+        red[0] = sqrt(t) * (0x1.0p-52 * (double)(m > M ? m : M));
+    }
+    __syncthreads();
+    const double lam = red[0];
+    for (int n = threadIdx.x; n < M; n += 512) Ks[(int64_t)n * ld + m + n] = lam;
 }
 
 // one warp per point: lane l sums neurons l, l + 32, ...; fixed-order butterfly reduction
@@ -518,7 +580,11 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
                                   (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end);
     else
         k_assemble<0><<<g1, AS_NT, tab_bytes, st>>>(c->cfg, c->sz.ld, c->sz.ncols, W, b, Kaug, At, nullptr,
-                                  (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end); }
+                                  (int)c->sz.e_impl_begin, (int)c->sz.e_impl_end);
+    if (c->cfg.tikhonov < 0.0)
+        k_damping<<<(unsigned)c->sz.S, 512, 0, st>>>(Kaug, c->sz.ld, c->sz.ncols,
+                                                    (int)(c->cfg.p * c->cfg.p + 4 * c->cfg.q + (c->cfg.layout == 1 ? 4 : 0)),
+                                                    c->cfg.M); }
     return cudaGetLastError();
 }
 

@@ -151,7 +151,7 @@ cudaError_t run_interface_cg(const elmddm_ctx* c, const double* Mband, const dou
                              double tol, int maxit, int* iters, double* relres, cudaStream_t st) {
     const CholPlan& pl = c->plan;
     const int64_t Gp = pl.n, G = c->sz.G;
-    const int nblk = pl.nblk, qd = c->cfg.q;
+    const int nblk = pl.nblk, qd = c->plan_q;
     const int nparts = (int)((Gp + 1023) / 1024);
     double* r = work;
     double* p = r + Gp;

@@ -769,7 +769,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
                                cudaStream_t st) {
     const CholPlan& pl = c->plan;
     const int64_t n = pl.n, G = c->sz.G;
-    const int nblk = pl.nblk, q = c->cfg.q;
+    const int nblk = pl.nblk, q = c->plan_q;  // unknowns per plan face (64 on the dense plan of layout 1)
     double* yv = work;          // right-hand side, then the solution, in the factorisation order
     double* z = yv + n;
     double* Ybuf = z + n;       // [nblk] packed tiles (n is a multiple of 64: 16-byte aligned)

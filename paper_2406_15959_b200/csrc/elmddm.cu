@@ -54,11 +54,16 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (cfg->P < 1 || cfg->P > 1024) return why = "P out of range", false;
     if (cfg->M < 8 || cfg->M % 8 != 0) return why = "M must be a positive multiple of 8", false;
     if (cfg->p < 1) return why = "p must be >= 1", false;
-    if (cfg->q < 2 || cfg->q % 2 != 0) return why = "q must be even and >= 2", false;
-    int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q;
-    if (m < cfg->M) return why = "need m = p*p + 4q >= M (overdetermined local LS, P:288-292)", false;
-    if (!(cfg->tikhonov >= 0.0) || !(cfg->tikhonov < 1e300)) return why = "tikhonov must be finite and >= 0", false;
-    if (cfg->tikhonov > 0.0) m += cfg->M;  // reading R29: M damping rows below the collocation rows
+    if (cfg->layout < 0 || cfg->layout > 1) return why = "layout must be 0 (face points) or 1 (lattice)", false;
+    if (cfg->layout == 0 && (cfg->q < 2 || cfg->q % 2 != 0)) return why = "q must be even and >= 2", false;
+    if (cfg->layout == 1 && (cfg->q < 1 || cfg->p != cfg->q)) return why = "lattice layout: need p == q >= 1", false;
+    if (cfg->layout == 1 && cfg->problem == 7) return why = "lattice layout: plate bending not supported", false;
+    int64_t m = (int64_t)cfg->p * cfg->p + 4 * cfg->q + (cfg->layout == 1 ? 4 : 0);
+    if (m < cfg->M && cfg->tikhonov == 0.0)
+        return why = "need m >= M (overdetermined local LS, P:288-292) or damping rows", false;
+    if (!(cfg->tikhonov == cfg->tikhonov) || !(cfg->tikhonov < 1e300) || !(cfg->tikhonov > -1e300))
+        return why = "tikhonov must be finite", false;
+    if (cfg->tikhonov != 0.0) m += cfg->M;  // reading R29: M damping rows below the collocation rows
     // ld <= 3008: every panel variant; taller (up to ~9.6k rows): the 4-CTA cluster block panel
     if (round_up(m, 32) > 3008 && panel_cl_stage(round_up(m, 32), 227 * 1024) == 0)
         return why = "m too large for the QR panels (ld <= ~9600 rows)", false;
@@ -69,7 +74,103 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (cfg->s_begin < 0 || cfg->s_end > N || cfg->s_begin >= cfg->s_end) return why = "bad [s_begin, s_end)", false;
     if (cfg->interface_mode < 0 || cfg->interface_mode > 3) return why = "bad interface_mode", false;
     if (cfg->q > 256) return why = "q too large", false;
+    if (cfg->layout == 1 && (int64_t)(cfg->P - 1) * (cfg->P - 1) + 2LL * cfg->P * (cfg->P - 1) * cfg->q > 16384)
+        return why = "lattice layout: dense interface limited to G <= 16384 unknowns", false;
     return true;
+}
+
+elmddm_status finish_tables(elmddm_ctx* c, const std::vector<int>& qsrc, const std::vector<int>& pptr,
+                            const std::vector<int>& pbc, const std::vector<FaceTerm>& terms,
+                            const std::vector<int>& gptr, const std::vector<FaceTerm>& gterms);
+
+// Layout 1 (the paper's lattice, reading R32): interface unknowns G = faces q + (P-1)^2, flux
+// equations n_eq = faces q + 4 (P-1)^2 (one per face point; per cross point one per incident face,
+// the corner remark P:282-286), each with two contributors (subdomain, local flux row) kept in
+// ascending subdomain order.  The interface system is assembled densely (Q of n_eq x (G+1), its
+// Gram) and factored by the tile Cholesky on a dense plan: "faces" of 64 consecutive unknowns in
+// natural order, every tile pair coupled.
+elmddm_status build_tables_lattice(elmddm_ctx* c, const std::vector<int>& umap) {
+    const int P = c->cfg.P, q = c->cfg.q, N = P * P, F = c->faces;
+    const int64_t Gf = (int64_t)F * q, X = (int64_t)(P - 1) * (P - 1), G = Gf + X, NE = Gf + 4 * X;
+    const int na = (int)c->sz.na;
+    // unknown -> its (subdomain, local column) pairs, ascending s (2 for a face point, 4 for a
+    // cross point): the S1 gather of k_lat_mfill
+    std::vector<int> rmap((size_t)std::max<int64_t>(G, 1) * 8, -1);
+    {
+        const int ne = (int)c->sz.ne;
+        std::vector<int> fill((size_t)std::max<int64_t>(G, 1), 0);
+        for (int s = 0; s < N; ++s)
+            for (int t = 0; t < ne; ++t) {
+                const int u = umap[(size_t)s * ne + t];
+                if (u < 0) continue;
+                if (fill[u] >= 4) {
+                    c->err = "internal: an interface unknown in more than four subdomains";
+                    return ELMDDM_EINVAL;
+                }
+                rmap[(size_t)u * 8 + 2 * fill[u]] = s;
+                rmap[(size_t)u * 8 + 2 * fill[u] + 1] = t;
+                ++fill[u];
+            }
+    }
+    // flux row ar of subdomain s -> equation (as orc_flux_eq of the oracle's layout 1; its own
+    // numbering, re-derived here): face points f*q + k; cross point x, incident face t at Gf + 4x + t
+    std::vector<int> eqsrc((size_t)std::max<int64_t>(NE, 1) * 4, -1);  // [eq][(s, ar) x 2]
+    for (int s = 0; s < N; ++s) {  // ascending s: slot 0 gets the smaller subdomain
+        int i = s % P, j = s / P;
+        for (int ar = 0; ar < na; ++ar) {
+            int64_t eq = -1;
+            if (ar < 4 * q) {
+                int f = c->sub_face[s * 4 + ar / q];
+                if (f >= 0) eq = (int64_t)f * q + ar % q;
+            } else {
+                int cc = (ar - 4 * q) / 2, d = (ar - 4 * q) % 2, ci = cc & 1, cj = cc >> 1;
+                int Xi = i + ci, Yj = j + cj;
+                if (Xi > 0 && Xi < P && Yj > 0 && Yj < P) {
+                    int x = (Yj - 1) * (P - 1) + (Xi - 1);
+                    int t = d == 0 ? (cj == 1 ? 0 : 1) : (ci == 1 ? 2 : 3);
+                    eq = Gf + 4LL * x + t;
+                }
+            }
+            if (eq < 0) continue;
+            int slot = eqsrc[eq * 4] < 0 ? 0 : 1;
+            if (slot == 1 && eqsrc[eq * 4 + 2] >= 0) {
+                c->err = "internal: a flux equation with more than two contributors";
+                return ELMDDM_EINVAL;
+            }
+            eqsrc[eq * 4 + 2 * slot] = s;
+            eqsrc[eq * 4 + 2 * slot + 1] = ar;
+        }
+    }
+    c->sz.G = G;
+    c->sz.faces = F;
+    c->sz.n_eq = NE;
+    c->sz.G_pad = round_up(std::max<int64_t>(G, 1), ELM_NB);
+    c->sz.halfband = G > 0 ? G - 1 : 0;
+    // dense plan: pseudo-faces of 64 unknowns, all pairs (b >= c)
+    const int Fd = (int)((G + ELM_NB - 1) / ELM_NB);
+    std::vector<std::pair<int, int>> allp;
+    for (int b = 0; b < Fd; ++b)
+        for (int cc = 0; cc <= b; ++cc) allp.push_back({b, cc});
+    build_chol_plan(P, ELM_NB, Fd, allp, 0, c->crit_band, c->plan, chol_split_min());
+    if (c->chol_sched) c->chol_sim_us = schedule_chol_tasks(c->plan, 2 * c->nsm);
+    c->plan_q = ELM_NB;
+    c->ld_q = round_up(std::max<int64_t>(NE, 1), 32);
+    std::vector<int> tI(std::max(c->plan.ntiles, 1), 0), tJ(std::max(c->plan.ntiles, 1), 0);
+    for (int I = 0; I < c->plan.nblk; ++I)
+        for (int J = 0; J <= I; ++J) {
+            const int t = c->plan.tile_map[(size_t)I * c->plan.nblk + J];
+            if (t >= 0) {
+                tI[t] = I;
+                tJ[t] = J;
+            }
+        }
+    cudaError_t e;
+    if ((e = upload(&c->d_eqsrc, eqsrc)) != cudaSuccess || (e = upload(&c->d_rmap, rmap)) != cudaSuccess ||
+        (e = upload(&c->d_tile_I, tI)) != cudaSuccess || (e = upload(&c->d_tile_J, tJ)) != cudaSuccess)
+        return cuda_fail(c, e, "upload");
+    c->npairs = c->nterms = c->ngterms = 0;
+    return finish_tables(c, std::vector<int>(), std::vector<int>(1, 0), std::vector<int>(), std::vector<FaceTerm>(),
+                         std::vector<int>(1, 0), std::vector<FaceTerm>());
 }
 
 elmddm_status build_tables(elmddm_ctx* c) {
@@ -91,6 +192,29 @@ elmddm_status build_tables(elmddm_ctx* c) {
             c->face_edge[f * 2 + slot] = e;
         }
     }
+    // local interface column t of subdomain s -> global unknown (strip-order face unknown f*q + k,
+    // layout 1: then the cross points row-major), -1 on the boundary (the back-solve gather)
+    const int lat = c->cfg.layout == 1;
+    const int64_t Gf = (int64_t)F * q;
+    const int ne = 4 * q + (lat ? 4 : 0), na = 4 * q + (lat ? 8 : 0);
+    std::vector<int> umap((size_t)N * ne, -1);
+    for (int s = 0; s < N; ++s) {
+        int i = s % P, j = s / P;
+        for (int t = 0; t < 4 * q; ++t) {
+            int f = c->sub_face[s * 4 + t / q];
+            umap[(size_t)s * ne + t] = f >= 0 ? f * q + t % q : -1;
+        }
+        for (int cc = 0; cc < ne - 4 * q; ++cc) {
+            int Xi = i + (cc & 1), Yj = j + (cc >> 1);
+            if (Xi > 0 && Xi < P && Yj > 0 && Yj < P)
+                umap[(size_t)s * ne + 4 * q + cc] = (int)(Gf + (Yj - 1) * (P - 1) + (Xi - 1));
+        }
+    }
+    c->sz.ne = ne;
+    c->sz.na = na;
+    cudaError_t e0 = upload(&c->d_umap, umap);
+    if (e0 != cudaSuccess) return cuda_fail(c, e0, "upload");
+    if (lat) return build_tables_lattice(c, umap);
     // neighbour slots of each flux face a: [a, other faces of sub 0, other faces of sub 1]
     c->nbr.assign((size_t)F * 7, -1);
     std::vector<int> qsrc((size_t)F * 8 * 6, -1);
@@ -183,6 +307,7 @@ elmddm_status build_tables(elmddm_ctx* c) {
 
     const int64_t G = (int64_t)F * q;
     c->sz.G = G;
+    c->sz.n_eq = G;
     c->sz.faces = F;
     c->sz.G_pad = round_up(std::max<int64_t>(G, 1), ELM_NB);
     c->sz.halfband = F > 0 ? hb : 0;
@@ -212,6 +337,15 @@ elmddm_status build_tables(elmddm_ctx* c) {
         }
     }
     if (c->chol_sched) c->chol_sim_us = schedule_chol_tasks(c->plan, 2 * c->nsm);
+    c->plan_q = q;
+    return finish_tables(c, qsrc, pptr, pbc, terms, gptr, gterms);
+}
+
+// plan sizes, device tables and flags (both layouts)
+elmddm_status finish_tables(elmddm_ctx* c, const std::vector<int>& qsrc, const std::vector<int>& pptr,
+                            const std::vector<int>& pbc, const std::vector<FaceTerm>& terms,
+                            const std::vector<int>& gptr, const std::vector<FaceTerm>& gterms) {
+    const int q = c->cfg.q;
     const CholPlan& pl = c->plan;
     const int nblk = pl.nblk;
     c->sz.band_ld = ELM_TLD;
@@ -222,7 +356,7 @@ elmddm_status build_tables(elmddm_ctx* c) {
     c->sz.chol_ordering = pl.ordering;
     {
         int eb = 0, ee = 0;
-        if (c->implicit_e) elm_e_implicit_range(c->cfg.M, c->cfg.q, &eb, &ee);
+        if (c->implicit_e) elm_e_implicit_range(c->cfg.M, (int)c->sz.ne, &eb, &ee);
         c->sz.e_impl_begin = eb;
         c->sz.e_impl_end = ee;
     }
@@ -342,14 +476,17 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     const int64_t P = cfg->P, M = cfg->M, q = cfg->q;
     z.N = P * P;
     z.S = cfg->s_end - cfg->s_begin;
-    z.m = (int64_t)cfg->p * cfg->p + 4 * q;
-    z.ld = round_up(z.m + (cfg->tikhonov > 0.0 ? cfg->M : 0), 32);
-    z.kaug = 4 * q + 1;
+    const int lat = cfg->layout == 1;
+    z.ne = 4 * q + (lat ? 4 : 0);  // E_Gamma columns: edge points (+ the 4 corners, layout 1)
+    z.na = 4 * q + (lat ? 8 : 0);  // flux rows: edge points (+ 2 per corner, layout 1)
+    z.m = (int64_t)cfg->p * cfg->p + 4 * q + (lat ? 4 : 0);
+    z.ld = round_up(z.m + (cfg->tikhonov != 0.0 ? cfg->M : 0), 32);
+    z.kaug = z.ne + 1;
     z.ncols = M + z.kaug;
     z.kaug_elems = z.S * z.ld * z.ncols;
-    z.at_elems = z.S * M * 4 * q;
+    z.at_elems = z.S * M * z.na;
     z.tau_elems = z.S * M;
-    z.pbuf_ld = 4 * q;
+    z.pbuf_ld = z.na;
     z.pbuf_elems = z.N * z.pbuf_ld * z.kaug;
     z.sbuf_ld = z.kaug + 1;
     z.sbuf_elems = z.N * z.sbuf_ld * z.kaug;
@@ -363,6 +500,8 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
                                                           (int64_t)c->ga_ld * c->qrow_cols),
                                       5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16 +
                                           (c->iface_refine ? z.band_elems + 2 * z.chol_n : 0));
+    if (lat)  // dense Q [ld_q][G + 1] and its Gram [G + 1][G + 1] (elmddm_interface_assemble)
+        c->work_iface = std::max(c->work_iface, c->ld_q * (z.G + 1) + (z.G + 1) * (z.G + 1) + 64);
     c->work_back = z.S * z.ld;
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
@@ -394,6 +533,11 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_flags);
     cudaFree(c->d_sub_face);
     cudaFree(c->d_qsrc);
+    cudaFree(c->d_umap);
+    cudaFree(c->d_eqsrc);
+    cudaFree(c->d_rmap);
+    cudaFree(c->d_tile_I);
+    cudaFree(c->d_tile_J);
     cudaFree(c->d_pair_ptr);
     cudaFree(c->d_pair_bc);
     cudaFree(c->d_terms);
@@ -434,10 +578,8 @@ elmddm_status elmddm_sizes(const elmddm_ctx* c, elmddm_sizes_t* out) {
 elmddm_status elmddm_chol_plan(const elmddm_ctx* c, int32_t* newidx, int32_t* tile_map, int32_t* tasks) {
     CHECK_CTX(c);
     const CholPlan& pl = c->plan;
-    const int q = c->cfg.q;
-    if (newidx)
-        for (int64_t f = 0; f < c->faces; ++f)
-            for (int k = 0; k < q; ++k) newidx[f * q + k] = pl.fbase[f] + k;
+    if (newidx)  // factorisation-order index of every interface unknown (strip order)
+        for (int64_t x = 0; x < c->sz.G; ++x) newidx[x] = pl.fbase[x / c->plan_q] + (int)(x % c->plan_q);
     if (tile_map) std::copy(pl.tile_map.begin(), pl.tile_map.end(), tile_map);
     if (tasks) export_tasks(pl, tasks);
     return ELMDDM_OK;
@@ -713,7 +855,7 @@ elmddm_status elmddm_debug_dist_emulate(elmddm_ctx* c, int32_t nrep, const doubl
 int64_t elmddm_band_index(const elmddm_ctx* c, int64_t i, int64_t j) {
     if (!c || i < 0 || j < 0 || i >= c->sz.G || j >= c->sz.G) return -1;
     const CholPlan& pl = c->plan;
-    const int q = c->cfg.q;
+    const int q = c->plan_q;
     int64_t a = pl.fbase[i / q] + i % q, b = pl.fbase[j / q] + j % q;
     if (a < b) std::swap(a, b);
     const int t = pl.tile_map[(size_t)(a / ELM_NB) * pl.nblk + b / ELM_NB];
@@ -773,6 +915,13 @@ elmddm_status elmddm_interface_points(const elmddm_ctx* c, double* xy) {
             }
         }
     }
+    if (c->cfg.layout == 1)  // the cross points, row-major, after the face unknowns
+        for (int Y = 1; Y < P; ++Y)
+            for (int X = 1; X < P; ++X) {
+                const int64_t u = (int64_t)c->faces * q + (int64_t)(Y - 1) * (P - 1) + (X - 1);
+                xy[2 * u] = (double)X / (double)P;
+                xy[2 * u + 1] = (double)Y / (double)P;
+            }
     return ELMDDM_OK;
 }
 

@@ -16,12 +16,13 @@
 
 // Implicit E_Gamma: column col of K_aug is never written by elmddm_assemble when
 // the 64-column tile of the first trailing update (j0 = 0: tiles start at min(64, M) + 64 t)
-// holding it lies entirely inside the E_Gamma block [M, M + 4q); that update synthesises the unit
-// columns in shared memory instead of loading them.  Returns [begin, end) of those columns.
-inline void elm_e_implicit_range(int M, int q, int* begin, int* end) {
+// holding it lies entirely inside the E_Gamma block [M, M + ne) (ne = 4q, or 4q + 4 with the
+// lattice's corners); that update synthesises the unit columns in shared memory instead of loading
+// them.  Returns [begin, end) of those columns.
+inline void elm_e_implicit_range(int M, int ne, int* begin, int* end) {
     const int c0 = M < ELM_NB ? M : ELM_NB;
     const int t_first = c0 + ((M - c0 + ELM_NB - 1) / ELM_NB) * ELM_NB;   // first tile start >= M
-    int t_end = c0 + ((M + 4 * q - c0) / ELM_NB) * ELM_NB;               // last tile end <= M + 4q
+    int t_end = c0 + ((M + ne - c0) / ELM_NB) * ELM_NB;                  // last tile end <= M + ne
     if (t_end < t_first) t_end = t_first;
     *begin = t_first;
     *end = t_end;
@@ -131,6 +132,13 @@ struct elmddm_ctx {
     FaceTerm* d_terms = nullptr; // contributions of each pair
     int* d_gterm_ptr = nullptr;  // CSR over faces b for g terms
     FaceTerm* d_gterms = nullptr;
+    int* d_umap = nullptr;       // [N][ne] local interface column -> global unknown or -1 (both layouts)
+    int* d_eqsrc = nullptr;      // layout 1: [n_eq][2 contributors][(s, flux row)], ascending s
+    int* d_rmap = nullptr;       // layout 1: [G][4][(s, local column)], ascending s, -1 padded
+    int* d_tile_I = nullptr;     // layout 1: tile id -> (I, J) of the dense plan
+    int* d_tile_J = nullptr;
+    int plan_q = 0;              // unknowns per plan "face" (q, or 64 for the dense plan of layout 1)
+    int64_t ld_q = 0;            // layout 1: leading dimension of the dense Q (n_eq rounded up)
     int npairs = 0, nterms = 0, ngterms = 0;
     int qrow_ld = 0, qrow_cols = 0, ga_ld = 0;  // Q row block: q x (7q+1), ld qrow_ld; Ga: ga_ld^2
     int64_t work_factor = 0, work_iface = 0, work_back = 0;
@@ -275,6 +283,8 @@ struct GemmArgs {
     int lower_only;  // skip 64x64 output tiles strictly above the diagonal
 };
 // r = g - M x (packed-tile symmetric M, factorisation order; cg.cu) and x += d
+cudaError_t run_interface_assemble_lattice(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
+                                           double* g, double* work, cudaStream_t st);
 cudaError_t launch_residual(const elmddm_ctx* c, const double* Mband, const double* x, const double* g, double* r,
                             cudaStream_t st);
 cudaError_t launch_axpy1(double* x, const double* d, int64_t n, cudaStream_t st);

@@ -1542,6 +1542,7 @@ using namespace elmtma;
 struct EsynArgs {
     int e_begin, e_end;   // implicit columns (empty: off)
     int M, q, pp, P, s_begin;
+    int lattice;          // layout 1: columns M + 4q .. M + 4q + 3 are the corners (cross points)
 };
 
 __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ CUtensorMap tmV,
@@ -1573,6 +1574,11 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     if (syn) {
         const int s = es.s_begin + sl, si = s % es.P, sj = s / es.P;
         iface_mask = (si > 0) | ((si < es.P - 1) << 1) | ((sj > 0) << 2) | ((sj < es.P - 1) << 3);
+        if (es.lattice)  // corner cc = (ci, cj) is a cross point iff it is inside the domain
+            for (int cc = 0; cc < 4; ++cc) {
+                const int X = si + (cc & 1), Y = sj + (cc >> 1);
+                iface_mask |= (X > 0 && X < es.P && Y > 0 && Y < es.P) << (4 + cc);
+            }
     }
     // the C part of a stage for chunk c of a synthetic tile: element (row, col) of the swizzled
     // 32 x 64 chunk is 1 iff row c*CH + row == pp + (ncol0 + col - M) on an interface edge
@@ -1581,7 +1587,8 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
             const int bx = t / BOX, rem = t - bx * BOX, col = rem >> 4, x = rem & 15;
             const int row = bx * 16 + ((((x >> 2) ^ (col & 3))) << 2) + (x & 3);
             const int ecol = ncol0 + col - es.M;
-            Cs[t] = (c * CH + row == es.pp + ecol && ((iface_mask >> (ecol / es.q)) & 1)) ? 1.0 : 0.0;
+            const int bit = ecol < 4 * es.q ? ecol / es.q : 4 + (ecol - 4 * es.q);
+            Cs[t] = (c * CH + row == es.pp + ecol && ((iface_mask >> bit) & 1)) ? 1.0 : 0.0;
         }
     };
     uint32_t par0 = 0, par1 = 0;
@@ -3098,8 +3105,8 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     // implicit E_Gamma tiles of the first trailing update (the assembly did not write them)
     const int pp_rows = (int)(c->cfg.p * c->cfg.p);
     const EsynArgs esyn{(int)c->sz.e_impl_begin, (int)c->sz.e_impl_end, M, (int)c->cfg.q, pp_rows, (int)c->cfg.P,
-                        (int)c->cfg.s_begin};
-    const EsynArgs esyn_off{0, 0, M, (int)c->cfg.q, pp_rows, (int)c->cfg.P, (int)c->cfg.s_begin};
+                        (int)c->cfg.s_begin, (int)(c->cfg.layout == 1)};
+    const EsynArgs esyn_off{0, 0, M, (int)c->cfg.q, pp_rows, (int)c->cfg.P, (int)c->cfg.s_begin, 0};
     if (!use_tma && esyn.e_end > esyn.e_begin) return cudaErrorInvalidValue;  // create() ties implicit_e to use_tma
     // Subdomain groups on separate streams: the latency-bound panel factorisation of one group
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different

@@ -114,17 +114,16 @@ __global__ void k_pad(double* Mband, const int* __restrict__ pad, int npad, cons
 // ---- back-solve -----------------------------------------------------------------------------
 // z[s][r] = sum_t Kaug[s][r][M + t] v_t, v = [u_s ; 1].   grid (ceil(ld/256), S)
 __global__ void __launch_bounds__(256) k_bs_gemv(elmddm_config cfg, const double* __restrict__ Kaug, int64_t ld,
-                                                 int64_t ncols, const int* __restrict__ sub_face,
+                                                 int64_t ncols, const int* __restrict__ umap, int ne,
                                                  const double* __restrict__ uG, double* __restrict__ z) {
     extern __shared__ double v[];
-    const int M = cfg.M, q = cfg.q, kaug = 4 * q + 1;
+    const int M = cfg.M, kaug = ne + 1;
     const int sl = blockIdx.y, s = cfg.s_begin + sl;
     for (int t = threadIdx.x; t < kaug; t += blockDim.x) {
-        double val = 1.0;
-        if (t < 4 * q) {
-            int e = t / q, k = t % q;
-            int f = sub_face[s * 4 + e];
-            val = f >= 0 ? uG[(int64_t)f * q + k] : 0.0;
+        double val = 1.0;  // u_s gathered through the local -> global map, 0 on the boundary
+        if (t < ne) {
+            const int u = umap[(int64_t)s * ne + t];
+            val = u >= 0 ? uG[u] : 0.0;
         }
         v[t] = val;
     }
@@ -344,13 +343,114 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
     }
 }
 
+// ---- interface, layout 1 (the lattice with cross points, reading R32): dense assembly ----------
+// Q_aug[e][u] (column-major, ld ldq): row e = flux equation e, the sum over its (<= 2) contributors
+// (s, flux row ar) -- ascending s, one pass each -- of P_s[ar, t] at u = umap[s][t]; column G holds
+// q_e = sum P_s[ar, ne] (the y column).  The buffer is zero on entry.  grid n_eq.
+__global__ void k_qdense(const double* __restrict__ Pbuf, int64_t pstride, int64_t pld, const int* __restrict__ eqsrc,
+                         const int* __restrict__ umap, int ne, int64_t G, double* __restrict__ Q, int64_t ldq) {
+    const int64_t e = blockIdx.x;
+    for (int c = 0; c < 2; ++c) {
+        const int s = eqsrc[e * 4 + 2 * c], ar = eqsrc[e * 4 + 2 * c + 1];
+        if (s >= 0)
+            for (int t = threadIdx.x; t <= ne; t += blockDim.x) {
+                const int64_t u = t < ne ? (int64_t)umap[(int64_t)s * ne + t] : G;
+                if (u >= 0) Q[e + u * ldq] += Pbuf[(int64_t)s * pstride + ar + (int64_t)t * pld];
+            }
+        __syncthreads();
+    }
+}
+
+// symmetric matrices of which only the lower 64-tiles are stored (the batched GEMM's lower_only)
+__device__ __forceinline__ double lower_at(const double* __restrict__ A, int64_t r, int64_t c, int64_t ld) {
+    return (r >> 6) >= (c >> 6) ? A[r + c * ld] : A[c + r * ld];
+}
+
+// M = sum_s scatter(S1_s) + Q^T Q and g = -sum_s scatter(T_E^T t_F) - Q^T q into the dense plan's
+// packed tiles (natural order, every lower tile present); element (a, b): the Gram of Q_aug plus
+// the S1 entries of the subdomains holding both unknowns (rmap: up to 4 (s, t) per unknown,
+// ascending s, -1 padded); unknowns >= G get a unit diagonal.  grid ntiles, 256 threads.
+__global__ void k_lat_mfill(const double* __restrict__ Maug, int64_t ldm, const double* __restrict__ Sbuf,
+                            int64_t sstride, int64_t sld, const int* __restrict__ rmap, int64_t G,
+                            const int* __restrict__ tile_I, const int* __restrict__ tile_J,
+                            double* __restrict__ Mband) {
+    const int t = blockIdx.x, I = tile_I[t], J = tile_J[t];
+    double* T = Mband + (int64_t)t * ELM_TS;
+    for (int x = threadIdx.x; x < ELM_NB * ELM_NB; x += blockDim.x) {
+        const int r = x % ELM_NB, cc = x / ELM_NB;
+        if (I == J && r < cc) continue;
+        const int64_t a = (int64_t)I * ELM_NB + r, b = (int64_t)J * ELM_NB + cc;
+        double v;
+        if (a >= G || b >= G) {
+            v = a == b ? 1.0 : 0.0;
+        } else {
+            v = 0.0;
+            for (int ka = 0; ka < 4; ++ka) {
+                const int sa = rmap[a * 8 + 2 * ka];
+                if (sa < 0) break;
+                for (int kb = 0; kb < 4; ++kb) {
+                    const int sb = rmap[b * 8 + 2 * kb];
+                    if (sb < 0) break;
+                    if (sb == sa)
+                        v += lower_at(Sbuf + (int64_t)sa * sstride, rmap[a * 8 + 2 * ka + 1], rmap[b * 8 + 2 * kb + 1], sld);
+                }
+            }
+            v += lower_at(Maug, a, b, ldm);
+        }
+        T[r + (int64_t)cc * ELM_TLD] = v;
+    }
+}
+
+__global__ void k_lat_g(const double* __restrict__ Maug, int64_t ldm, const double* __restrict__ Sbuf, int64_t sstride,
+                        int64_t sld, const int* __restrict__ rmap, int ne, int64_t G, int64_t G_pad,
+                        double* __restrict__ g) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= G_pad) return;
+    if (a >= G) {
+        g[a] = 0.0;
+        return;
+    }
+    double v = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        const int s = rmap[a * 8 + 2 * k];
+        if (s < 0) break;
+        v -= lower_at(Sbuf + (int64_t)s * sstride, rmap[a * 8 + 2 * k + 1], ne, sld);
+    }
+    g[a] = v - lower_at(Maug, a, G, ldm);
+}
+
 }  // namespace
+
+cudaError_t run_interface_assemble_lattice(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
+                                           double* g, double* work, cudaStream_t st) {
+    const int64_t G = c->sz.G, NE = c->sz.n_eq, kaug = c->sz.kaug, ldq = c->ld_q, ldm = G + 1;
+    const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
+    double* Q = work;                 // [G + 1][ldq]
+    double* Maug = Q + ldq * (G + 1);  // [G + 1][G + 1], lower tiles
+    cudaError_t e;
+    if (G <= 0) return cudaSuccess;
+    if ((e = cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (G + 1), st)) != cudaSuccess) return e;
+    {
+        KTimer kt(c, ELMDDM_K_IFACE, st);
+        k_qdense<<<(unsigned)NE, 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_eqsrc, c->d_umap, (int)c->sz.ne, G, Q,
+                                                ldq);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    GemmArgs gq{(int)(G + 1), (int)(G + 1), (int)NE, Q, ldq, 0, Q, ldq, 0, Maug, ldm, 0, 1.0, 0.0, 1, 1};
+    if ((e = gemm_launch(true, false, gq, st, c, ELMDDM_K_IFACE)) != cudaSuccess) return e;
+    KTimer kt(c, ELMDDM_K_IFACE, st);
+    k_lat_mfill<<<(unsigned)c->plan.ntiles, 256, 0, st>>>(Maug, ldm, Sbuf, sstride, c->sz.sbuf_ld, c->d_rmap, G,
+                                                          c->d_tile_I, c->d_tile_J, Mband);
+    k_lat_g<<<(unsigned)((c->sz.G_pad + 255) / 256), 256, 0, st>>>(Maug, ldm, Sbuf, sstride, c->sz.sbuf_ld, c->d_rmap,
+                                                                   (int)c->sz.ne, G, c->sz.G_pad, g);
+    return cudaGetLastError();
+}
 
 cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
                                  double* work, cudaStream_t st) {
     (void)work;
     const int64_t S = c->sz.S, ld = c->sz.ld, ncols = c->sz.ncols, kaug = c->sz.kaug;
-    const int M = c->cfg.M, q = c->cfg.q, nat = 4 * q;
+    const int M = c->cfg.M, nat = (int)c->sz.na;  // flux rows (4q, or 4q + 8 on the lattice)
     cudaError_t e;
     // S_s = [T_E | t_F]^T [T_E | t_F] does not depend on the TRSM: it runs on a side stream beside
     // it and fills the TRSM's last partial wave (serialised when per-class timing is on)
@@ -381,7 +481,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    // P_s = W_s [R12 | y]   (4q x kaug)
+    // P_s = W_s [R12 | y]   (na x kaug)
     GemmArgs gp{nat, (int)kaug, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
                 Pbuf + s0 * pstride, c->sz.pbuf_ld, pstride, 1.0, 0.0, (int)S, 0};
     if ((e = gemm_launch(true, false, gp, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
@@ -394,6 +494,7 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
 
 cudaError_t run_interface_assemble(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
                                    double* g, double* work, cudaStream_t st) {
+    if (c->cfg.layout == 1) return run_interface_assemble_lattice(c, Pbuf, Sbuf, Mband, g, work, st);
     const int q = c->cfg.q;
     const int64_t F = c->faces, kaug = c->sz.kaug;
     const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
@@ -438,7 +539,8 @@ cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double
     double* z = work;
     dim3 g1((unsigned)((ld + 255) / 256), (unsigned)S);
     { KTimer kt(c, ELMDDM_K_BACK, st);
-    k_bs_gemv<<<g1, 256, sizeof(double) * c->sz.kaug, st>>>(c->cfg, Kaug, ld, ncols, c->d_sub_face, uG, z); }
+    k_bs_gemv<<<g1, 256, sizeof(double) * c->sz.kaug, st>>>(c->cfg, Kaug, ld, ncols, c->d_umap, (int)c->sz.ne, uG,
+                                                            z); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     KTimer kt(c, ELMDDM_K_BACK, st);

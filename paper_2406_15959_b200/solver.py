@@ -65,7 +65,9 @@ class Problem:
     interface_mode: int = 0             # factorisation order: 0 auto | 1, 2 strip (envelope) | 3 nested dissection
     interface_solver: str = "cholesky"  # "cholesky" (direct, reading R12) | "cg" (the paper's)
     cg_tol: float = 1e-9                # relative residual of the CG solver
-    tikhonov: float = 0.0               # lambda of the damped local LS (reading R29; 0 = off)
+    tikhonov: float = 0.0               # lambda of the damped local LS (reading R29; 0 = off; < 0 the
+                                        # rule lambda_s = eps max(m, M) ||K^s||_F, reading R33)
+    layout: int = 0                     # 0 face points (R1) | 1 the paper's lattice with cross points (R32)
     grf: object = None                  # problem 6: eqn:grf draws [n][4] (a, w_x, w_y, b)
 
     @classmethod
@@ -88,7 +90,8 @@ class Context:
         if prob.interface_solver not in ("cholesky", "cg"):
             raise _lib.ElmddmError(f"unknown interface_solver {prob.interface_solver!r}")
         cfg = _lib.Config(prob.P, prob.M, prob.p, prob.q, prob.problem, prob.init_scheme, prob.init_c,
-                          prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, 0, prob.tikhonov)
+                          prob.r_over_diam, prob.seed, s_begin, s_end, prob.interface_mode, prob.layout,
+                          prob.tikhonov)
         h = C.c_void_p()
         rc = L.elmddm_create(C.byref(cfg), self.device, C.byref(h))
         if rc != 0:
@@ -314,6 +317,7 @@ class Context:
         rank = dist.get_rank(group)
         # opt-in until the peer-memory path has run on several GPUs (this environment offers one)
         want = os.environ.get("ELMDDM_DIST_IFACE", "0") == "1" and self.prob.interface_solver == "cholesky"
+        want = want and self.prob.layout == 0
         want = want and self.sizes["G"] > 0
 
         def agree(flag: bool) -> bool:

@@ -69,16 +69,17 @@ def kaug_assembled_np(ctx, buf, sl, c: dict):
     s = ctx.s_begin + sl
     i, j = s % P, s // P
     iface = [i > 0, i < P - 1, j > 0, j < P - 1]
+    iface += [0 < i + (cc & 1) < P and 0 < j + (cc >> 1) < P for cc in range(4)]  # lattice corners
     for col in range(z["e_impl_begin"], z["e_impl_end"]):
         t = col - M
         K[:, col] = 0.0
-        if iface[t // q]:
+        if iface[t // q if t < 4 * q else 4 + t - 4 * q]:
             K[pp + t, col] = 1.0
     return K
 
 
 def at_np(ctx, buf, sl, M, q):
-    return buf["At"].view(-1, 4 * q, M)[sl].cpu().numpy()  # (4q, M) = A rows
+    return buf["At"].view(-1, ctx.sizes["na"], M)[sl].cpu().numpy()  # (na, M) = A rows
 
 
 def local_iface_index(c: dict, s: int):

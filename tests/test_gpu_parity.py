@@ -884,3 +884,65 @@ def test_plate_end_to_end_parity_and_accuracy(cfgkw):
     assert rel_l2(ug, r["u"]) <= 1e-6
     ex = WL.exact(7, xy)
     assert rel_l2(ug, ex) <= max(10 * rel_l2(r["u"], ex), 1e-8)
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-2: the paper's shared lattice with cross points (layout 1; R32, R33)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfgkw", [
+    dict(P=3, M=24, p=5, q=5, problem=4, layout=1),
+    dict(P=2, M=40, p=7, q=7, problem=2, layout=1),
+    dict(P=4, M=16, p=3, q=3, problem=0, layout=1),
+    dict(P=3, M=48, p=5, q=5, problem=4, layout=1, tikhonov=-1.0),     # near-square, damping rule R33
+    dict(P=1, M=48, p=9, q=9, problem=4, layout=1, tikhonov=-1.0),     # 1 x 1: classical ELM on the lattice
+])
+def test_lattice_end_to_end_parity(cfgkw):
+    """Layout 1 end to end against the oracle: the assembly entrywise (corner value rows, corner
+    flux rows with the normals of both edges through the corner), u_Gamma (faces, then cross
+    points) and u on the grid to relative L2 1e-6."""
+    c = small(**cfgkw)
+    xy = WL.eval_grid(21)
+    ctx, buf, _ = run_gpu(c, upto="assemble")
+    W, b, _ = _oracle_init(c)
+    oc = ocfg(c)
+    M = c["M"]
+    for s in range(c["P"] ** 2):
+        K, F, A = O.assemble(oc, s, W, b)
+        Kg = kaug_assembled_np(ctx, buf, s, c)
+        m = K.shape[0]
+        scale = np.abs(K).max(axis=1, keepdims=True) + 1e-300
+        assert np.all(np.abs(Kg[:m, :M] - K) <= 1e-12 * scale), s
+        assert np.allclose(Kg[:m, M + ctx.sizes["ne"]], F, rtol=0, atol=1e-13 * max(1.0, np.abs(F).max()))
+        Ag = at_np(ctx, buf, s, M, c["q"])
+        assert Ag.shape == A.shape
+        assert np.allclose(Ag, A, rtol=0, atol=1e-12 * max(1.0, np.abs(A).max())), s
+    ctx, buf, u = run_gpu(c, xy)
+    r = O.solve(oc, W, b, xy)
+    assert rel_l2(u.cpu().numpy(), r["u"]) <= 1e-6, rel_l2(u.cpu().numpy(), r["u"])
+    G = ctx.sizes["G"]
+    if G:
+        assert rel_l2(buf["uG"][:G].cpu().numpy(), r["uG"]) <= 1e-6
+        pts = ctx.interface_points()
+        for s in range(c["P"] ** 2):  # the exported coordinates are the oracle's interface points
+            xs, _, gidx = O.rows(oc, s)
+            sel = gidx >= 0
+            assert np.array_equal(pts[gidx[sel]], xs[sel])
+
+
+@pytest.mark.parametrize("k", [8, 9])
+def test_lattice_paper_table2(k):
+    """The paper's Table 2 workload on its own (2^8+1)^2 lattice (configs 8 / 9: 16 x 16 and 8 x 8
+    subdomains, 2^16 neurons, cross points, damping rule R33) against the full oracle solve:
+    u relative L2 <= 1e-6; the error vs the exact solution sin(2 pi x) e^y is reported beside the
+    paper's (1.0e-7 / 2.6e-8, Table 2, CPU cluster, context only)."""
+    c = WL.config(k)
+    xy = WL.eval_grid()
+    ctx, buf, u = run_gpu(c, xy)
+    W, b, _ = _oracle_init(c)
+    r = O.solve(ocfg(c), W, b, xy, nthreads=NCPU)
+    ug = u.cpu().numpy()
+    ue = WL.exact(c["problem"], xy)
+    print(f"{c['name']}: rel L2 vs oracle {rel_l2(ug, r['u']):.3e}; vs exact GPU {rel_l2(ug, ue):.3e}, "
+          f"oracle {rel_l2(r['u'], ue):.3e}, paper {WL.PAPER_TABLE2[k][0]:.3e}")
+    assert rel_l2(ug, r["u"]) <= 1e-6
+    assert rel_l2(ug, ue) < 1e-5

@@ -803,15 +803,16 @@ def test_lattice_single_subdomain_is_classical_elm():
     assert np.allclose(K @ r["coef"][0], K @ ref, rtol=0, atol=1e-9 * np.abs(F).max())
 
 
-def test_damping_rule_sqrt_eps_frobenius():
-    """Reading R33: tikhonov < 0 selects lambda_s = sqrt(eps) ||K^s||_F (the collocation rows) in
-    every subdomain -- the damped [K; lambda I] has condition number <= ||K||_F / lambda = 2^26."""
+def test_damping_rule_eps_frobenius():
+    """Reading R33: tikhonov < 0 selects lambda_s = eps max(m, M) ||K^s||_F (the collocation rows) in
+    every subdomain -- the Tikhonov analogue of the numerical-rank cut rcond = eps max(m, n) that
+    PyTorch's least squares (the paper's tool) applies by default."""
     c = mkcfg(P=2, M=20, p=5, q=5, problem=4, seed=2, layout=1, tikhonov=-1.0)
     W, b, _, _ = O.init_hidden(c)
     m = (5 + 1 + 1) ** 2
     for s in range(4):
         K, F, _ = O.assemble(c, s, W, b)
         assert K.shape[0] == m + 20
-        lam = np.sqrt(np.sum(K[:m] ** 2)) * 2.0 ** -26
+        lam = np.sqrt(np.sum(K[:m] ** 2)) * np.finfo(float).eps * max(m, 20)
         assert np.allclose(np.diag(K[m:]), lam, rtol=1e-14, atol=0)
         assert np.all(K[m:] - np.diag(np.diag(K[m:])) == 0.0) and np.all(F[m:] == 0.0)

@@ -27,7 +27,7 @@ import workloads as WL  # noqa: E402
 
 def ocfg(c):
     return O.cfg(c["P"], c["M"], c["p"], c["q"], c["problem"], c.get("init_scheme", 0), c.get("init_c", 0.125),
-                 c.get("r_over_diam", 0.5), c["seed"], c.get("tikhonov", 0.0))
+                 c.get("r_over_diam", 0.5), c["seed"], c.get("tikhonov", 0.0), c.get("layout", 0))
 
 
 def main():

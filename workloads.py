@@ -33,12 +33,25 @@ CONFIGS = [
     # non-positive pivot
     dict(name="t2-4x4", P=4, M=4096, p=63, q=64, problem=4, seed=7, tikhonov=2.2e-5),
 ]
+# the paper's own workload ON ITS OWN LATTICE (NEXT-2, reading R32): the (2^8 + 1)^2 points are
+# one global lattice shared by the subdomains (layout 1): every subdomain holds its (256/P + 1)^2
+# lattice points, corners included; interior subdomain corners are cross points, interface
+# unknowns shared by four subdomains with one flux row per incident edge (the corner remark,
+# P:282-286).  n = 2^16 neurons in total.  The near-square local LS (m - M = 33 / 65 / 129) take
+# the damped K^{s+} with the fixed rule lambda_s = eps max(m, M) ||K^s||_F (reading R33, not tuned).
+CONFIGS += [
+    dict(name="lat-16x16", P=16, M=256, p=15, q=15, problem=4, seed=8, layout=1, tikhonov=-1.0),
+    dict(name="lat-8x8", P=8, M=1024, p=31, q=31, problem=4, seed=9, layout=1, tikhonov=-1.0),
+    dict(name="lat-4x4", P=4, M=4096, p=63, q=63, problem=4, seed=10, layout=1, tikhonov=-1.0),
+]
 # the paper's Table 2 (CPU cluster, context only): relative L2 error, wall-clock s
-PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43), 7: (1.6192e-08, 19.46)}
+PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43), 7: (1.6192e-08, 19.46),
+                8: (1.0212e-07, 10.43), 9: (2.6392e-08, 3.48), 10: (1.6192e-08, 19.46)}
 
-# the bench workload: config 3 (16 x 16 subdomains, 2820 x 1600 local LS, ~9 GB of local
-# matrices) -- the largest local least-squares problem of BASELINE.json that fits one B200.
-BENCH_CONFIG = 3
+# the bench workload: config 4 (32 x 32 = 1024 subdomains, 1856 x 1024 local LS, 19.5 GB of
+# augmented local matrices, G = 126,976 interface unknowns) -- the largest BASELINE.json
+# configuration, and it fits one B200; config 3 (the largest local LS) is profiled beside it.
+BENCH_CONFIG = 4
 
 
 def config(k: int, **over) -> dict:
