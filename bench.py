@@ -70,7 +70,7 @@ def bench_config(args) -> dict:
 
 def workload_desc(k: int, c: dict | None = None) -> str:
     c = WL.config(k) if c is None else c
-    m = c["p"] ** 2 + 4 * c["q"]
+    m = c["p"] ** 2 + 4 * c["q"] + (4 if c.get("layout", 0) == 1 else 0)
     names = {0: "sin(pi x)sin(pi y)", 1: "e^(x+y)sin(2pi x)cos(2pi y)", 2: "sin(4pi x)sin(4pi y)",
              3: "sin(8pi x)sin(8pi y)", 4: "sin(2pi x)e^y"}
     if c["problem"] == 7:
@@ -81,9 +81,15 @@ def workload_desc(k: int, c: dict | None = None) -> str:
                f"grf alpha={c.get('alpha', 16.0)} (eqn:varpoisson)")
     else:
         pde = f"2D Poisson -Lap u=f on (0,1)^2, u={names.get(c['problem'])}"
+    if c.get("layout", 0) == 1:
+        pts = (f"the paper's shared ({c['P'] * (c['q'] + 1)}+1)^2 lattice: {m} points/subdomain incl. corners, "
+               f"cross points as interface unknowns")
+    else:
+        pts = f"{c['p']}x{c['p']} interior + {c['q']}/edge points"
+    damp = "" if not c.get("tikhonov") else (", damped (lambda_s = eps max(m,M) ||K^s||_F)" if c["tikhonov"] < 0
+                                             else f", damped (lambda {c['tikhonov']:g})")
     return (f"{c.get('name', f'cfg{k}')}: {pde}, {c['P']}x{c['P']} subdomains, "
-            f"M={c['M']} tanh neurons/subdomain, {c['p']}x{c['p']} interior + {c['q']}/edge points "
-            f"(local LS {m}x{c['M']}), seed {c['seed']}, eval 101x101")
+            f"M={c['M']} tanh neurons/subdomain, {pts} (local LS {m}x{c['M']}{damp}), seed {c['seed']}, eval 101x101")
 
 
 # ------------------------------------------------------------------------------------------------
@@ -91,7 +97,9 @@ def workload_desc(k: int, c: dict | None = None) -> str:
 # ------------------------------------------------------------------------------------------------
 def algorithmic(c: dict, s_range, e_impl: int = 0) -> dict:
     P, M, p, q = c["P"], c["M"], c["p"], c["q"]
-    m = p * p + 4 * q + (M if c.get("tikhonov", 0.0) > 0 else 0)  # + the damping rows (reading R29)
+    lat = c.get("layout", 0) == 1
+    # (+ the 4 lattice corners, reading R32; + the damping rows, readings R29 / R33)
+    m = p * p + 4 * q + (4 if lat else 0) + (M if c.get("tikhonov", 0.0) != 0 else 0)
     fl_qr = 0.0
     fl_panel = 0.0
     bytes_asm = 0.0
@@ -103,6 +111,8 @@ def algorithmic(c: dict, s_range, e_impl: int = 0) -> dict:
         i, j = s % P, s // P
         n_if = (i > 0) + (i < P - 1) + (j > 0) + (j < P - 1)
         mg = n_if * q
+        if lat:  # the subdomain's corners that are cross points
+            mg += sum(0 < i + ci < P and 0 < j + cj < P for ci in (0, 1) for cj in (0, 1))
         k = mg + 1
         fl_qr += 2 * m * M * M - 2.0 / 3.0 * M ** 3 + 2 * M * k * (2 * m - M)
         # the panels' own Householder work (QR of the (m - j0) x nb panel): the rest of H3 is the

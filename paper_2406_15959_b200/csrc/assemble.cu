@@ -560,6 +560,12 @@ cudaError_t launch_assemble(const elmddm_ctx* c, const double* W, const double* 
     dim3 g1((unsigned)((c->sz.ncols - (c->sz.e_impl_end - c->sz.e_impl_begin) + AS_COLS - 1) / AS_COLS),
             (unsigned)c->sz.S);
     const size_t tab_bytes = sizeof(double) * AS_COLS * 2 * (c->cfg.p + c->cfg.q + 2);
+    if (tab_bytes > 48 * 1024) {  // (the lattice's 1 x 1: 512 coordinates per axis)
+        cudaError_t e = cudaFuncSetAttribute(c->cfg.problem == 7 ? k_assemble<2> : (c->cfg.problem == 6 ? k_assemble<1>
+                                                                                                 : k_assemble<0>),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_bytes);
+        if (e != cudaSuccess) return e;
+    }
     { KTimer kt(c, ELMDDM_K_ASSEMBLE, st);
     const double4* coef = nullptr;
     if (c->cfg.problem == 6) {

@@ -64,9 +64,11 @@ bool validate(const elmddm_config* cfg, std::string& why) {
     if (!(cfg->tikhonov == cfg->tikhonov) || !(cfg->tikhonov < 1e300) || !(cfg->tikhonov > -1e300))
         return why = "tikhonov must be finite", false;
     if (cfg->tikhonov != 0.0) m += cfg->M;  // reading R29: M damping rows below the collocation rows
-    // ld <= 3008: every panel variant; taller (up to ~9.6k rows): the 4-CTA cluster block panel
-    if (round_up(m, 32) > 3008 && panel_cl_stage(round_up(m, 32), 227 * 1024) == 0)
-        return why = "m too large for the QR panels (ld <= ~9600 rows)", false;
+    // ld <= 3008: every panel variant; taller (up to ~9.6k rows): the 4-CTA cluster block panel;
+    // taller still: the cooperative grid panel, which needs every subdomain's CTAs co-resident
+    if (round_up(m, 32) > 3008 && panel_cl_stage(round_up(m, 32), 227 * 1024) == 0 &&
+        (int64_t)(cfg->s_end - cfg->s_begin) > 64)
+        return why = "very tall local problems (ld > ~9600 rows) need <= 64 subdomains per context", false;
     if (cfg->problem < 0 || cfg->problem > 7) return why = "unknown problem id", false;
     if (cfg->init_scheme < 0 || cfg->init_scheme > 2) return why = "unknown init_scheme", false;
     if (!(cfg->init_c > 0) || !(cfg->r_over_diam >= 0)) return why = "init_c must be > 0, r_over_diam >= 0", false;
@@ -452,6 +454,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_IMPLICIT_E")) c->implicit_e = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_IFACE_REFINE")) c->iface_refine = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_PANEL_GRID")) c->panel_grid = atoi(env) != 0;
         c->implicit_e = c->implicit_e && c->use_tma;
         // 4-CTA cluster panels cut the per-subdomain latency chain of the QR but spend more SM
         // time: they win for the small per-rank slabs of multi-GPU runs (config 3: 32 subdomains
@@ -495,14 +498,15 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         elmddm_destroy(c);
         return st;
     }
-    c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB);
+    // V, T of the current panel; the grid panel's partial sums (<= 2 CTAs / SM) and counters
+    c->work_factor = z.S * (ELM_NB * z.ld + ELM_NB * ELM_NB) + 2LL * c->nsm * (ELM_NB * (ELM_NB + 1) / 2) + z.S + 16;
     c->work_iface = std::max<int64_t>((int64_t)c->faces * ((int64_t)c->qrow_ld * c->qrow_cols +
                                                           (int64_t)c->ga_ld * c->qrow_cols),
                                       5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16 +
                                           (c->iface_refine ? z.band_elems + 2 * z.chol_n : 0));
     if (lat)  // dense Q [ld_q][G + 1] and its Gram [G + 1][G + 1] (elmddm_interface_assemble)
         c->work_iface = std::max(c->work_iface, c->ld_q * (z.G + 1) + (z.G + 1) * (z.G + 1) + 64);
-    c->work_back = z.S * z.ld;
+    c->work_back = z.S * z.ld + z.S + 8;  // z, and the grid back-substitution's counters
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
         (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess ||

@@ -155,6 +155,7 @@ struct elmddm_ctx {
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    int panel_grid = 0;    // cooperative grid panel (automatic for very tall local problems; ELMDDM_PANEL_GRID=1)
     int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)
     int implicit_e = 1;  // E_Gamma tiles never written by the assembly, synthesised by the first
                          // trailing update (elm_e_implicit; needs use_tma; ELMDDM_IMPLICIT_E=0 off)

@@ -1758,6 +1758,209 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 }
 
 
+
+// ------------------------------------------------------------------------------------------
+// Grid panel for very tall local problems (the paper's N = 1 x 1 / 2 x 2 lattice workloads:
+// 33k / 132k damped rows, beyond the cluster panels).  One cooperative launch per panel: the
+// CTAs of a subdomain split its rows [j0, ld) into contiguous slices, the 64-column panel stays
+// in K_aug (L2-resident), and every column is one unblocked Householder step (reading R20) with
+// two barriers among the subdomain's CTAs: (1) partial sums of the column's squares -> every CTA
+// reduces them in the same fixed order and forms alpha, tau, v; (2) partial dot products of v
+// with the panel's remaining columns -> the same fixed-order reduction -> rank-1 update of the
+// own slice.  Then V (explicit, to Vbuf), tau, and T from the Gram V^T V (fixed-order partial
+// sums) by the forward recurrence T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j).  Deterministic.
+// ------------------------------------------------------------------------------------------
+namespace gp {
+constexpr int NT = 256, NW = NT / 32;
+constexpr int NG = ELM_NB * (ELM_NB + 1) / 2;  // Gram entries (upper triangle incl. diagonal)
+}  // namespace gp
+
+__device__ __forceinline__ unsigned gp_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// barrier among the nper CTAs of one subdomain (cooperative launch: all co-resident);
+// a monotone counter zeroed before the launch
+__device__ __forceinline__ void gp_barrier(unsigned* cnt, unsigned nper, unsigned& gen) {
+    __syncthreads();
+    ++gen;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1u);
+        while (gp_ld_acquire(cnt) < gen * nper) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(gp::NT) k_panel_grid(PanelArgs a, int nb, int nper, double* __restrict__ part,
+                                                       unsigned* __restrict__ cnt) {
+    using namespace gp;
+    extern __shared__ double dsm[];  // Gs [64][65] | Ts [64][65] | vs [64][33]
+    double* Gs = dsm;
+    double* Ts = Gs + ELM_NB * (ELM_NB + 1);
+    double* vs = Ts + ELM_NB * (ELM_NB + 1);
+    __shared__ double red[NW];
+    __shared__ double wsh[ELM_NB];
+    __shared__ double prm[4];  // alpha, tau, scale
+    const int sd = blockIdx.x / nper, cta = blockIdx.x % nper;
+    const int sl = a.s_off + sd;
+    const int64_t ld = a.ld;
+    const int j0 = a.j0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* A = a.Kaug + (int64_t)sl * ld * a.ncols;
+    double* Vb = a.Vbuf + (int64_t)sl * ELM_NB * ld;
+    double* T = a.Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
+    double* P = part + (int64_t)sd * nper * NG;  // [cta][NG] partials of this subdomain
+    unsigned* C = cnt + sd;
+    unsigned gen = 0;
+    const int64_t R = ld - j0, per = (R + nper - 1) / nper;
+    const int64_t r0 = j0 + (int64_t)cta * per, r1 = (ld < r0 + per ? ld : r0 + per);  // own rows [r0, r1)
+    for (int c = 0; c < nb; ++c) {
+        const int64_t jc = j0 + c;
+        const bool own_jc = jc >= r0 && jc < r1;
+        double* x = A + jc * ld;
+        const int64_t i0 = r0 > jc + 1 ? r0 : jc + 1;
+        // (1) ||x[jc+1:]||^2 over the own rows
+        double ss = 0.0;
+        for (int64_t i = i0 + tid; i < r1; i += NT) ss = fma(x[i], x[i], ss);
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) red[warp] = ss;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NW; ++w) t += red[w];
+            P[(int64_t)cta * NG] = t;
+            // row jc of the panel's later columns, published by its owner before anyone updates it
+            if (own_jc)
+                for (int k = 0; k < nb - 1 - c; ++k) P[(int64_t)cta * NG + ELM_NB + k] = A[(jc + 1 + k) * ld + jc];
+        }
+        gp_barrier(C, nper, gen);
+        if (tid == 0) {
+            double t = 0.0;
+            for (int k = 0; k < nper; ++k) t += P[(int64_t)k * NG];
+            const int owner = (int)((jc - j0) / per);
+            const double x0 = A[jc * ld + jc];
+            const double nrm = sqrt(x0 * x0 + t);
+            double alpha = x0, tau = 0.0, scale = 0.0;
+            if (nrm != 0.0) {
+                alpha = x0 >= 0.0 ? -nrm : nrm;
+                scale = 1.0 / (x0 - alpha);
+                tau = (alpha - x0) / alpha;
+            }
+            prm[0] = alpha;
+            prm[1] = tau;
+            prm[2] = scale;
+            prm[3] = (double)owner;
+        }
+        __syncthreads();
+        const double tau = prm[1], scale = prm[2];
+        const int owner = (int)prm[3];
+        // v = x / (x0 - alpha) below the diagonal (own rows)
+        for (int64_t i = i0 + tid; i < r1; i += NT) x[i] *= scale;
+        __syncthreads();
+        // (2) partial sums_{i > jc} v_i A[i, k] for the remaining panel columns
+        const int nk = nb - 1 - c;
+        for (int k = warp; k < nk; k += NW) {
+            const double* y = A + (jc + 1 + k) * ld;
+            double d = 0.0;
+            for (int64_t i = i0 + lane; i < r1; i += 32) d = fma(x[i], y[i], d);
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if (lane == 0) P[(int64_t)cta * NG + 1 + k] = d;
+        }
+        gp_barrier(C, nper, gen);
+        if (tid < nk) {  // w_k = tau (A[jc, k] + sum_i v_i A[i, k]), fixed order
+            double d = P[(int64_t)owner * NG + ELM_NB + tid];
+            for (int k2 = 0; k2 < nper; ++k2) d += P[(int64_t)k2 * NG + 1 + tid];
+            wsh[tid] = tau * d;
+        }
+        __syncthreads();
+        for (int k = warp; k < nk; k += NW) {
+            double* y = A + (jc + 1 + k) * ld;
+            const double w = wsh[k];
+            for (int64_t i = i0 + lane; i < r1; i += 32) y[i] = fma(-w, x[i], y[i]);
+            if (lane == 0 && own_jc) y[jc] -= w;  // row jc: v_jc = 1 (the owner)
+        }
+        if (tid == 0 && own_jc) {
+            x[jc] = prm[0];  // R_jj
+            a.tau[(int64_t)sl * a.M + jc] = tau;
+        }
+        gp_barrier(C, nper, gen);  // the next column reads rows updated by other CTAs' owners
+    }
+    // explicit V (absolute rows, unit diagonal, zero above) of the own rows
+    for (int c = 0; c < ELM_NB; ++c) {
+        const int64_t jc = j0 + c;
+        for (int64_t i = r0 + tid; i < r1; i += NT)
+            Vb[(int64_t)c * ld + i] = c >= nb ? 0.0 : (i < jc ? 0.0 : (i == jc ? 1.0 : A[jc * ld + i]));
+    }
+    // partial Gram V^T V (upper, k <= l) over the own rows, 32-row chunks staged in shared memory
+    double acc[(NG + NT - 1) / NT];
+#pragma unroll
+    for (int u = 0; u < (NG + NT - 1) / NT; ++u) acc[u] = 0.0;
+    __syncthreads();
+    for (int64_t b0 = r0; b0 < r1; b0 += 32) {
+        const int nr = (int)(r1 - b0 < 32 ? r1 - b0 : 32);
+        for (int e = tid; e < ELM_NB * 32; e += NT) {
+            const int c = e / 32, r = e % 32;
+            vs[c * 33 + r] = r < nr ? Vb[(int64_t)c * ld + b0 + r] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < (NG + NT - 1) / NT; ++u) {
+            const int e = tid + u * NT;
+            if (e < NG) {
+                int k = 0, rem = e;
+                while (rem >= ELM_NB - k) {
+                    rem -= ELM_NB - k;
+                    ++k;
+                }
+                const int l = k + rem;
+                double sacc = acc[u];
+                for (int r = 0; r < 32; ++r) sacc = fma(vs[k * 33 + r], vs[l * 33 + r], sacc);
+                acc[u] = sacc;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < (NG + NT - 1) / NT; ++u)
+        if (tid + u * NT < NG) P[(int64_t)cta * NG + tid + u * NT] = acc[u];
+    gp_barrier(C, nper, gen);
+    if (cta != 0) return;
+    // T (64 x 64, column-major, upper) by the forward recurrence, one CTA per subdomain
+    for (int e = tid; e < NG; e += NT) {
+        int k = 0, rem = e;
+        while (rem >= ELM_NB - k) {
+            rem -= ELM_NB - k;
+            ++k;
+        }
+        const int l = k + rem;
+        double sacc = 0.0;
+        for (int k2 = 0; k2 < nper; ++k2) sacc += P[(int64_t)k2 * NG + e];
+        Gs[k * (ELM_NB + 1) + l] = sacc;
+    }
+    for (int e = tid; e < ELM_NB * (ELM_NB + 1); e += NT) Ts[e] = 0.0;
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+        const double tj = a.tau[(int64_t)sl * a.M + j0 + j];
+        if (tid < j) {  // T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
+            double sacc = 0.0;
+            for (int k = tid; k < j; ++k) sacc += Ts[tid * (ELM_NB + 1) + k] * Gs[k * (ELM_NB + 1) + j];
+            Ts[tid * (ELM_NB + 1) + j] = -tj * sacc;
+        }
+        if (tid == 0) Ts[j * (ELM_NB + 1) + j] = tj;
+        __syncthreads();
+    }
+    for (int e = tid; e < ELM_NB * ELM_NB; e += NT) {
+        const int r = e % ELM_NB, c = e / ELM_NB;
+        T[(int64_t)c * ELM_NB + r] = (r < nb && c < nb) ? Ts[r * (ELM_NB + 1) + c] : 0.0;
+    }
+}
+
+constexpr int GP_SMEM = (2 * ELM_NB * (ELM_NB + 1) + ELM_NB * 33) * 8;
+
 // ------------------------------------------------------------------------------------------
 // Cluster version of the panel base block: one subdomain's 8-column block is factored by a
 // cluster of PCL CTAs (PCL SMs), CTA z holding the rows [z Rq, (z+1) Rq) of the panel range.
@@ -3066,9 +3269,21 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
         return e;
     // 4-CTA cluster block panels: for small slabs (panel_cluster), and for panels too tall for one
     // CTA (the damped local LS of reading R29), with a ring stage sized to what fits
-    const bool use_cl = c->panel_cluster || !blk_ok;
-    const int stg_cl = cl_stage(ld, optin);
-    if (use_cl && stg_cl == 0) return cudaErrorInvalidValue;  // create() validated ld against this
+    // very tall local problems (the lattice's N <= 2 x 2): the cooperative grid panel
+    const bool use_grid = c->panel_grid || (!blk_ok && cl_stage(ld, optin) == 0);
+    const bool use_cl = !use_grid && (c->panel_cluster || !blk_ok);
+    const int stg_cl = use_grid ? 0 : cl_stage(ld, optin);
+    if (use_cl && stg_cl == 0) return cudaErrorInvalidValue;
+    int gp_per = 0;
+    if (use_grid) {
+        if ((e = cudaFuncSetAttribute(k_panel_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, GP_SMEM)) != cudaSuccess)
+            return e;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_panel_grid, gp::NT, GP_SMEM);
+        const int64_t cap = std::min<int64_t>((int64_t)std::max(occ, 1) * c->nsm, 2LL * c->nsm);
+        gp_per = (int)std::max<int64_t>(1, std::min<int64_t>(cap / S, (ld + 255) / 256));
+        if (gp_per * S > cap) return cudaErrorInvalidValue;  // more subdomains than co-resident CTAs
+    }
     const bool pp_ok = c->panel_merged && panelp_smem_bytes(ld, panelp_ring(ld, optin)) <= (size_t)optin;
     const bool pt_ok = c->panel_tmem && (ld + 127) / 128 * 16 <= 512;
     if (pt_ok && (e = cudaFuncSetAttribute(k_panel_t, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM)) != cudaSuccess)
@@ -3112,7 +3327,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
     // overlaps the DMMA-bound trailing updates of the others (the factorisations of different
     // subdomains are independent).
     // (with timing enabled the groups are serialised so that per-class event times do not overlap)
-    const int ngroups = c->timing ? 1 : (int)std::min<int64_t>(c->qr_groups, S);
+    const int ngroups = (c->timing || use_grid) ? 1 : (int)std::min<int64_t>(c->qr_groups, S);
     std::vector<cudaStream_t> streams(ngroups, st), pstr(ngroups, st);
     const bool prio = ngroups > 1 && c->panel_prio && c->panel_tmem;
     if (ngroups > 1) {
@@ -3139,7 +3354,17 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             const int g0 = (int)(S * g / ngroups), g1 = (int)(S * (g + 1) / ngroups);
             if (g1 <= g0) continue;
             PanelArgs pa{Kaug, ld, ncols, tau, M, Vbuf, Tbuf, j0, 0, g0, ring};
-            if (p8t_ok) {
+            if (use_grid) {
+                double* part = Tbuf + S * ELM_NB * ELM_NB;
+                unsigned* cnt = reinterpret_cast<unsigned*>(part + (int64_t)gp_per * S * gp::NG);
+                if ((e = cudaMemsetAsync(cnt, 0, sizeof(unsigned) * S, streams[g])) != cudaSuccess) return e;
+                int nb_v = nb, per_v = gp_per;
+                void* args[] = {(void*)&pa, (void*)&nb_v, (void*)&per_v, (void*)&part, (void*)&cnt};
+                KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
+                if ((e = cudaLaunchCooperativeKernel((void*)k_panel_grid, dim3((unsigned)(gp_per * (g1 - g0))),
+                                                     dim3(gp::NT), args, GP_SMEM, streams[g])) != cudaSuccess)
+                    return e;
+            } else if (p8t_ok) {
                 if (prio && j0 > 0) cudaStreamWaitEvent(pstr[g], c->ev_wy[g], 0);
                 {
                     KTimer kt(c, ELMDDM_K_PANEL, pstr[g]);
@@ -3176,7 +3401,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 k_panel_p<<<(unsigned)(g1 - g0), PNT, panelp_smem_bytes(ld - j0, pp.ring), streams[g]>>>(pp, nb);
                 if ((e = cudaGetLastError()) != cudaSuccess) return e;
             }
-            for (int blk = 0; !p8_ok && !p8t_ok && !((pp_ok || pt_ok) && !use_cl) && blk < nb / ELM_BB; ++blk) {
+            for (int blk = 0; !use_grid && !p8_ok && !p8t_ok && !((pp_ok || pt_ok) && !use_cl) && blk < nb / ELM_BB; ++blk) {
                 pa.blk = blk;
                 KTimer kt(c, ELMDDM_K_PANEL, streams[g]);
                 if (use_cl) {

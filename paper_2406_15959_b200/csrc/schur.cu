@@ -343,6 +343,106 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
     }
 }
 
+
+// Back substitution c = R11^{-1} z for very large M (the lattice's N <= 2 x 2: M = 16384 / 65536)
+// with the CTAs of a cooperative launch split per subdomain (nper each): block row ib from the
+// bottom, CTA 0 of the subdomain solves the 64 x 64 diagonal block (warp-level substitution as in
+// k_bs_trsv), then every CTA updates its slice of z[0:i0] -= R[0:i0, i0:i0+64] c_i.  Two barriers
+// per block; r_s = ||z[M:ld]|| by CTA 0 first.  Deterministic.
+__device__ __forceinline__ unsigned bs_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void bs_barrier(unsigned* cnt, unsigned nper, unsigned& gen) {
+    __syncthreads();
+    ++gen;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1u);
+        while (bs_ld_acquire(cnt) < gen * nper) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_bs_trsv_grid(const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
+                                                      int M, double* __restrict__ z, double* __restrict__ coef,
+                                                      double* __restrict__ resid, int nper, unsigned* __restrict__ cnt) {
+    __shared__ double Rs[64][65];
+    __shared__ double cs[64];
+    __shared__ double red[8];
+    __shared__ double rdg[64];
+    const int sl = blockIdx.x / nper, cta = blockIdx.x % nper;
+    const double* A = Kaug + (int64_t)sl * ld * ncols;
+    double* zs = z + (int64_t)sl * ld;
+    unsigned* C = cnt + sl;
+    unsigned gen = 0;
+    if (cta == 0) {
+        double ss = 0.0;
+        for (int64_t r = M + threadIdx.x; r < ld; r += blockDim.x) ss += zs[r] * zs[r];
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += red[w];
+            resid[sl] = sqrt(t);
+        }
+    }
+    const int nblk = (M + 63) / 64;
+    for (int ib = nblk - 1; ib >= 0; --ib) {
+        const int i0 = ib * 64, bi = min(64, M - i0);
+        if (cta == 0) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < bi * bi; t += blockDim.x) {
+                int r = t % bi, c = t / bi;
+                Rs[r][c] = A[(int64_t)(i0 + c) * ld + i0 + r];
+            }
+            __syncthreads();
+            if (threadIdx.x < bi) rdg[threadIdx.x] = 1.0 / Rs[threadIdx.x][threadIdx.x];
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const int lane = threadIdx.x;
+                double z0 = lane < bi ? zs[i0 + lane] : 0.0;
+                double z1 = lane + 32 < bi ? zs[i0 + lane + 32] : 0.0;
+                for (int r = bi - 1; r >= 0; --r) {
+                    double cr = r >= 32 ? __shfl_sync(0xffffffffu, z1, r - 32) : __shfl_sync(0xffffffffu, z0, r);
+                    cr = cr * rdg[r];
+                    if (lane < r) z0 -= Rs[lane][r] * cr;
+                    if (lane + 32 < r) z1 -= Rs[lane + 32][r] * cr;
+                    if (lane == (r & 31)) {
+                        if (r >= 32) z1 = cr;
+                        else z0 = cr;
+                    }
+                }
+                if (lane < bi) {
+                    coef[(int64_t)sl * M + i0 + lane] = z0;
+                    zs[i0 + lane] = z0;  // the solved block, read by every CTA after the barrier
+                }
+                if (lane + 32 < bi) {
+                    coef[(int64_t)sl * M + i0 + lane + 32] = z1;
+                    zs[i0 + lane + 32] = z1;
+                }
+            }
+        }
+        bs_barrier(C, nper, gen);
+        if (i0 > 0) {
+            if (threadIdx.x < bi) cs[threadIdx.x] = zs[i0 + threadIdx.x];
+            __syncthreads();
+            // z[0:i0] -= R[0:i0, i0:i0+bi] c_i over the own rows
+            const int per = (i0 + nper - 1) / nper, ra = cta * per, rb = min(i0, ra + per);
+            for (int r = ra + threadIdx.x; r < rb; r += blockDim.x) {
+                double acc = 0.0;
+                for (int k = 0; k < bi; ++k) acc += A[(int64_t)(i0 + k) * ld + r] * cs[k];
+                zs[r] -= acc;
+            }
+            bs_barrier(C, nper, gen);
+        }
+    }
+}
+
 // ---- interface, layout 1 (the lattice with cross points, reading R32): dense assembly ----------
 // Q_aug[e][u] (column-major, ld ldq): row e = flux equation e, the sum over its (<= 2) contributors
 // (s, flux row ar) -- ascending s, one pass each -- of P_s[ar, t] at u = umap[s][t]; column G holds
@@ -544,9 +644,24 @@ cudaError_t run_back_solve(const elmddm_ctx* c, const double* Kaug, const double
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     KTimer kt(c, ELMDDM_K_BACK, st);
+    const int M = c->cfg.M;
+    static const bool force_grid = [] {
+        const char* env = getenv("ELMDDM_BS_GRID");
+        return env && atoi(env) != 0;
+    }();
+    if ((M >= 8192 || force_grid) && S <= 64) {  // very large networks, few subdomains: all SMs' CTAs
+        const int nper = (int)std::max<int64_t>(1, (2LL * c->nsm) / S);
+        unsigned* cnt = reinterpret_cast<unsigned*>(z + S * ld);
+        if ((e = cudaMemsetAsync(cnt, 0, sizeof(unsigned) * S, st)) != cudaSuccess) return e;
+        int64_t ld_v = ld, nc_v = ncols;
+        int M_v = M, per_v = nper;
+        void* args[] = {(void*)&Kaug, (void*)&ld_v, (void*)&nc_v, (void*)&M_v, (void*)&z, (void*)&coef, (void*)&resid,
+                        (void*)&per_v, (void*)&cnt};
+        return cudaLaunchCooperativeKernel((void*)k_bs_trsv_grid, dim3((unsigned)(nper * S)), dim3(256), args, 0, st);
+    }
     // all subdomains resident at 1024 threads (2 CTAs / SM): more loads in flight per subdomain
     // (config 3: 1.12 -> 0.83 ms); more subdomains than that: 512 threads, 4 CTAs / SM (config 4)
     const int nt = S <= 2 * (int64_t)c->nsm ? BS_NT : BS_NT / 2;
-    k_bs_trsv<<<(unsigned)S, nt, 0, st>>>(Kaug, ld, ncols, c->cfg.M, z, coef, resid);
+    k_bs_trsv<<<(unsigned)S, nt, 0, st>>>(Kaug, ld, ncols, M, z, coef, resid);
     return cudaGetLastError();
 }

@@ -43,10 +43,15 @@ CONFIGS += [
     dict(name="lat-16x16", P=16, M=256, p=15, q=15, problem=4, seed=8, layout=1, tikhonov=-1.0),
     dict(name="lat-8x8", P=8, M=1024, p=31, q=31, problem=4, seed=9, layout=1, tikhonov=-1.0),
     dict(name="lat-4x4", P=4, M=4096, p=63, q=63, problem=4, seed=10, layout=1, tikhonov=-1.0),
+    # N = 2 x 2 and the classical ELM 1 x 1 (66,049 x 65,536, the run the paper could not do on a
+    # GPU): local LS of 33,025 / 131,585 damped rows -> the cooperative grid panel
+    dict(name="lat-2x2", P=2, M=16384, p=127, q=127, problem=4, seed=11, layout=1, tikhonov=-1.0),
+    dict(name="lat-1x1", P=1, M=65536, p=255, q=255, problem=4, seed=12, layout=1, tikhonov=-1.0),
 ]
 # the paper's Table 2 (CPU cluster, context only): relative L2 error, wall-clock s
 PAPER_TABLE2 = {5: (2.6392e-08, 3.48), 6: (1.0212e-07, 10.43), 7: (1.6192e-08, 19.46),
-                8: (1.0212e-07, 10.43), 9: (2.6392e-08, 3.48), 10: (1.6192e-08, 19.46)}
+                8: (1.0212e-07, 10.43), 9: (2.6392e-08, 3.48), 10: (1.6192e-08, 19.46),
+                11: (1.0748e-10, 315.83), 12: (8.1550e-11, 8617.13)}
 
 # the bench workload: config 4 (32 x 32 = 1024 subdomains, 1856 x 1024 local LS, 19.5 GB of
 # augmented local matrices, G = 126,976 interface unknowns) -- the largest BASELINE.json
