@@ -139,11 +139,12 @@ def ncu_traffic(k: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
     (profiles/r01_traffic_cfg<k>.json, written by tools/traffic.py from an ncu run of the same
     workload); None if there is no capture for this workload."""
-    path = os.path.join(ROOT, "profiles", f"r01_traffic_cfg{k}.json")
-    if not os.path.exists(path):
-        return None, None
-    d = json.load(open(path))
-    return d, d["source"]
+    for tag in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{tag}_traffic_cfg{k}.json")
+        if os.path.exists(path):
+            d = json.load(open(path))
+            return d, d["source"]
+    return None, None
 
 
 # ------------------------------------------------------------------------------------------------

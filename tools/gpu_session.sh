@@ -22,6 +22,10 @@ for w in "$@"; do
       k=${w#bench}
       timeout 900 python bench.py --config "$k" --no-cpu-baseline > "$OUT/bench_cfg$k.json" 2> "$OUT/bench_cfg$k.err"; echo "bench cfg$k exit $?" | tee -a "$OUT/summary.txt"
       cat "$OUT/bench_cfg$k.json";;
+    cfg:*)
+      k=${w#cfg:}
+      timeout 1200 python bench.py --config "$k" --no-cpu-baseline --no-e2e --steps 3 --warmup 1 > "$OUT/bench_cfg$k.json" 2> "$OUT/bench_cfg$k.err"; echo "bench cfg$k exit $?" | tee -a "$OUT/summary.txt"
+      python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[1], d['ms_per_step'], d.get('rel_l2_vs_exact'))" "$OUT/bench_cfg$k.json";;
     nd[0-9]|strip[0-9])
       k=${w: -1}; m=3; [ "${w:0:5}" = strip ] && m=2
       timeout 900 python bench.py --config "$k" --interface-mode $m --no-cpu-baseline --no-e2e > "$OUT/bench_${w}.json" 2> "$OUT/bench_${w}.err"; echo "bench $w exit $?" | tee -a "$OUT/summary.txt"
