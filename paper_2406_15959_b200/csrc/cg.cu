@@ -21,35 +21,30 @@ __global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb,
                                                   const int* __restrict__ rptr, const int2* __restrict__ rdep,
                                                   const int* __restrict__ cptr, const int2* __restrict__ cdep,
                                                   const double* __restrict__ x, double* __restrict__ y) {
-    __shared__ double xs[NB];
+    // thread (r, column group p of 16): x segments read straight from global memory (L1-cached,
+    // shared by the 64 rows), no barrier per tile; one fixed-order reduction at the end
     __shared__ double part[4][NB];
     const int I = blockIdx.x, tid = threadIdx.x, r = tid & 63, p = tid >> 6;
     double acc = 0.0;
-    // row part: tiles (I, J), J < I, then the diagonal tile
     const int r0 = rptr[I], nr = rptr[I + 1] - r0;
     for (int q = 0; q <= nr; ++q) {
         const int J = q < nr ? rdep[r0 + q].x : I;
         const double* T = Mb + (int64_t)(q < nr ? rdep[r0 + q].y : diag_tid[I]) * ELM_TS;
-        __syncthreads();
-        if (tid < NB) xs[tid] = x[(int64_t)J * NB + tid];
-        __syncthreads();
+        const double* xs = x + (int64_t)J * NB;
 #pragma unroll 4
         for (int c = p * 16; c < p * 16 + 16; ++c) {
             double v = T[c * LP + r];  // element (r, c)
             if (J == I && c > r) v = T[r * LP + c];  // upper part of the diagonal tile = transpose
-            acc += v * xs[c];
+            acc += v * __ldg(xs + c);
         }
     }
-    // column part: tiles (I', I), I' > I, used transposed
     const int c0 = cptr[I], nc = cptr[I + 1] - c0;
     for (int q = 0; q < nc; ++q) {
         const int Ip = cdep[c0 + q].x;
         const double* T = Mb + (int64_t)cdep[c0 + q].y * ELM_TS;
-        __syncthreads();
-        if (tid < NB) xs[tid] = x[(int64_t)Ip * NB + tid];
-        __syncthreads();
+        const double* xs = x + (int64_t)Ip * NB;
 #pragma unroll 4
-        for (int c = p * 16; c < p * 16 + 16; ++c) acc += T[r * LP + c] * xs[c];  // element (c, r)
+        for (int c = p * 16; c < p * 16 + 16; ++c) acc += T[r * LP + c] * __ldg(xs + c);  // element (c, r)
     }
     part[p][r] = acc;
     __syncthreads();

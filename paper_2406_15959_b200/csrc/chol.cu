@@ -635,7 +635,14 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
     double* xs = acc + NB;                // [64]
     double* rdv = xs + NB;                // [64] reciprocal diagonal
     const int tid = threadIdx.x;
-    for (int it = blockIdx.x; it < nblk; it += gridDim.x) {
+    // rows dealt in order through one counter (flags[nblk], zeroed before the launch): a CTA held up
+    // by a long dependency wait does not delay rows a static round robin would have given it
+    __shared__ int s_next;
+    for (;;) {
+        if (tid == 0) s_next = atomicAdd(flags + nblk, 1);
+        __syncthreads();
+        const int it = s_next;
+        if (it >= nblk) break;
         const int i = dir == 0 ? it : nblk - 1 - it;
         const int64_t i0 = (int64_t)i * NB;
         // dependencies: forward (j, tile (i, j)) ascending j; backward (j, tile (j, i)) descending j
@@ -644,75 +651,80 @@ __global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb
             return Mb + (int64_t)(q == nj ? diag_tid[i] : dep[d0 + q].y) * ELM_TS;
         };
         if (tid < NB) acc[tid] = rhs[i0 + tid];
+        // the dependency tiles' products are accumulated in registers (thread (r, column group) for
+        // the forward direction, (c, row quarter) for the backward one) and reduced once per block
+        // row, in a fixed order: two barriers per tile instead of four
+        double sacc = 0.0;
         load_tile_async(tiles, tile_of(0));
-        for (int q = 0; q <= nj; ++q) {
+        for (int q = 0; q < nj; ++q) {
             const int st = q & 1;
-            if (q < nj) load_tile_async(tiles + (st ^ 1) * ELM_TS, tile_of(q + 1));
-            else asm volatile("cp.async.commit_group;\n" ::);
-            if (q < nj) {
-                const int j = dep[d0 + q].x;
-                if (tid == 0) wait_flag(flags + j, epoch, status, j);
-                __syncthreads();
-                if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
-            }
+            const int j = dep[d0 + q].x;
+            if (tid == 0) wait_flag(flags + j, epoch, status, j);
+            __syncthreads();  // x_j published; every thread done with tile q-1 and xs
+            if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
+            load_tile_async(tiles + (st ^ 1) * ELM_TS, tile_of(q + 1));  // (q + 1 == nj: the diagonal)
             asm volatile("cp.async.wait_group 1;\n" ::);
-            __syncthreads();
+            __syncthreads();  // tile q and xs visible
             const double* T = tiles + st * ELM_TS;
-            if (q < nj) {
-                double s = 0.0;
-                if (dir == 0) {  // s[r] = sum_c T[r][c] x[c]: thread (r, c-group of 16)
-                    const int r = tid & 63, cgp = tid >> 6;
+            if (dir == 0) {  // s[r] += sum_c T[r][c] x[c]: thread (r, c-group of 16)
+                const int r = tid & 63, cgp = tid >> 6;
 #pragma unroll 4
-                    for (int c = cgp * 16; c < cgp * 16 + 16; ++c) s += T[c * LP + r] * xs[c];
-                    part[cgp * NB + r] = s;
-                } else {         // s[c] = sum_r T[r][c] x[r]: thread (c, r = rq + 4 l), shuffle-reduced
-                    const int c = tid >> 2, rq = tid & 3;
+                for (int c = cgp * 16; c < cgp * 16 + 16; ++c) sacc += T[c * LP + r] * xs[c];
+            } else {         // s[c] += sum_r T[r][c] x[r]: thread (c, r = rq + 4 l)
+                const int c = tid >> 2, rq = tid & 3;
 #pragma unroll 4
-                    for (int l = 0; l < 16; ++l) s += T[c * LP + rq + 4 * l] * xs[rq + 4 * l];
-                    s += __shfl_xor_sync(0xffffffffu, s, 1);
-                    s += __shfl_xor_sync(0xffffffffu, s, 2);
-                    if (rq == 0) part[c] = s;
-                }
-                __syncthreads();
-                if (tid < NB) acc[tid] -= dir == 0 ? part[tid] + part[NB + tid] + part[2 * NB + tid] + part[3 * NB + tid]
-                                                   : part[tid];
-            } else {
-                if (tid < NB) rdv[tid] = 1.0 / T[tid * LP + tid];
-                __syncthreads();
-                if (tid < 32) {
-                    // diagonal solve with the lower tile (i, i): warp-level substitution
-                    const int lane = tid;
-                    double z0 = acc[lane], z1 = acc[lane + 32];
-                    if (dir == 0) {
-                        for (int cc = 0; cc < NB; ++cc) {
-                            double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
-                            if (lane > cc) z0 -= T[cc * LP + lane] * xc;
-                            if (lane + 32 > cc) z1 -= T[cc * LP + lane + 32] * xc;
-                            if (lane == (cc & 31)) {
-                                if (cc < 32) z0 = xc;
-                                else z1 = xc;
-                            }
-                        }
-                    } else {
-                        for (int cc = NB - 1; cc >= 0; --cc) {
-                            double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
-                            if (lane < cc) z0 -= T[lane * LP + cc] * xc;
-                            if (lane + 32 < cc) z1 -= T[(lane + 32) * LP + cc] * xc;
-                            if (lane == (cc & 31)) {
-                                if (cc < 32) z0 = xc;
-                                else z1 = xc;
-                            }
+                for (int l = 0; l < 16; ++l) sacc += T[c * LP + rq + 4 * l] * xs[rq + 4 * l];
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);  // the diagonal tile
+        // reduce the partial products in a fixed order
+        if (dir == 0) {
+            part[(tid >> 6) * NB + (tid & 63)] = sacc;
+        } else {
+            sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+            sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+            if ((tid & 3) == 0) part[tid >> 2] = sacc;
+        }
+        __syncthreads();
+        if (tid < NB && nj > 0)
+            acc[tid] -= dir == 0 ? (part[tid] + part[NB + tid]) + (part[2 * NB + tid] + part[3 * NB + tid]) : part[tid];
+        {
+            const double* T = tiles + (nj & 1) * ELM_TS;  // the diagonal tile (i, i)
+            if (tid < NB) rdv[tid] = 1.0 / T[tid * LP + tid];
+            __syncthreads();
+            if (tid < 32) {
+                // diagonal solve with the lower tile (i, i): warp-level substitution
+                const int lane = tid;
+                double z0 = acc[lane], z1 = acc[lane + 32];
+                if (dir == 0) {
+                    for (int cc = 0; cc < NB; ++cc) {
+                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                        if (lane > cc) z0 -= T[cc * LP + lane] * xc;
+                        if (lane + 32 > cc) z1 -= T[cc * LP + lane + 32] * xc;
+                        if (lane == (cc & 31)) {
+                            if (cc < 32) z0 = xc;
+                            else z1 = xc;
                         }
                     }
-                    out[i0 + lane] = z0;
-                    out[i0 + lane + 32] = z1;
-                    __threadfence();
-                    __syncwarp();
-                    if (lane == 0) st_release(flags + i, epoch);
+                } else {
+                    for (int cc = NB - 1; cc >= 0; --cc) {
+                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                        if (lane < cc) z0 -= T[lane * LP + cc] * xc;
+                        if (lane + 32 < cc) z1 -= T[(lane + 32) * LP + cc] * xc;
+                        if (lane == (cc & 31)) {
+                            if (cc < 32) z0 = xc;
+                            else z1 = xc;
+                        }
+                    }
                 }
+                out[i0 + lane] = z0;
+                out[i0 + lane + 32] = z1;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release(flags + i, epoch);
             }
-            __syncthreads();
         }
+        __syncthreads();
     }
 }
 
@@ -871,6 +883,8 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
             ElmStatus* stp = c->d_status;
             void* args[] = {(void*)&Mband, (void*)&nblk_v, (void*)&dt, (void*)&dp, (void*)&dl, (void*)&rhs,
                             (void*)&out, (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
+            cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the row counter
+            if (e1 != cudaSuccess) return e1;
             KTimer kt(c, ELMDDM_K_TRSV, st);
             cudaError_t e2 = cudaLaunchCooperativeKernel((void*)k_band_trsv, dim3(grid), dim3(256), args, TRSV_SMEM, st);
             if (e2 != cudaSuccess) return e2;

@@ -1621,6 +1621,10 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     };
     // ---------------- phase 1: W = V^T C ----------------
     const int wm = warp & 1, wn = warp >> 1;
+    // valid columns of this tile: the last tile of every update holds only the F column (and any
+    // rest of the E_Gamma block); warps whose 16 columns are all out of range skip their DMMAs
+    const int ncv = N - (int)blockIdx.x * 64;
+    const bool act = wn * 16 < ncv;
     double acc[4][2][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1639,6 +1643,7 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         }
 #pragma unroll
         for (int ks = 0; ks < CH / 4; ++ks) {
+            if (!act) break;
             const int kk = ks * 4 + (lane & 3);
             double af[4], bf[2];
 #pragma unroll
@@ -1674,6 +1679,7 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll 4
     for (int ks = 0; ks < 16; ++ks) {
+        if (!act) break;
         const int kk = ks * 4 + (lane & 3);
         double af[4], bf[2];
 #pragma unroll
@@ -1725,6 +1731,7 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
                 }
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
+            if (!act) break;  // (wn3 == wn: the same column group as in phase 1)
             const int kk = ks * 4 + (lane & 3);
             double af[2], bf[2];
 #pragma unroll
