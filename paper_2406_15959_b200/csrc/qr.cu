@@ -759,9 +759,12 @@ __device__ void t_extend_n(double* T, int kpp, const double* G, const double* Tb
         for (int k = 0; k <= c; ++k) s += G[k * kpp + r] * Tbb[c * 8 + k];
         Ys[c * kpp + r] = s;
     }
-    for (int t = threadIdx.x; t < kpp * kpp; t += NTH) {
-        const int r = t % kpp, c = t / kpp;
-        Ts[c * kpp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+    for (int c = threadIdx.x >> 5; c < kpp; c += NTH / 32) {  // warp per column, coalesced
+        const int lane = threadIdx.x & 31;
+        double v0 = lane <= c ? T[c * ELM_NB + lane] : 0.0;
+        double v1 = lane + 32 <= c && lane + 32 < kpp ? T[c * ELM_NB + lane + 32] : 0.0;
+        if (lane < kpp) Ts[c * kpp + lane] = v0;
+        if (lane + 32 < kpp) Ts[c * kpp + lane + 32] = v1;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < kpp * 8; t += NTH) {
@@ -1038,9 +1041,12 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             if (kpp > 0) t_extend_n<NT>(T, kpp, Gp, Tbb, ring, ring + kpp * kpp);
             {
                 double* Ts = ring;
-                for (int t = tid; t < kp * kp; t += NT) {
-                    const int r = t % kp, c = t / kp;
-                    Ts[c * kp + r] = r <= c ? T[c * ELM_NB + r] : 0.0;
+                // (warp per column, lanes over rows: coalesced, independent loads in flight)
+                for (int c = warp; c < kp; c += NW) {
+                    double v0 = lane <= c ? T[c * ELM_NB + lane] : 0.0;
+                    double v1 = lane + 32 <= c && lane + 32 < kp ? T[c * ELM_NB + lane + 32] : 0.0;
+                    if (lane < kp) Ts[c * kp + lane] = v0;
+                    if (lane + 32 < kp) Ts[c * kp + lane + 32] = v1;
                 }
                 __syncthreads();
                 for (int t = tid; t < kp * 8; t += NT) {
