@@ -157,6 +157,52 @@ elmddm_status build_tables_lattice(elmddm_ctx* c, const std::vector<int>& umap) 
     if (c->chol_sched) c->chol_sim_us = schedule_chol_tasks(c->plan, 2 * c->nsm);
     c->plan_q = ELM_NB;
     c->ld_q = round_up(std::max<int64_t>(NE, 1), 32);
+    // face equation blocks: face f's q point equations, then the (<= 2) cross-point equations of its
+    // endpoints, all contributed by the same two subdomains (s1 < s2); Q_f's columns are
+    // [s1's ne local columns | s2's | rhs], its Gram G_f = Q_f^T Q_f.  flist[u]: the (face,
+    // column) copies of unknown u (every face of every subdomain holding u), ascending face.
+    const int ne = (int)c->sz.ne, nrow = q + 2;
+    std::vector<int> feq((size_t)std::max(F, 1) * nrow, -1), fpair((size_t)std::max(F, 1) * 2, -1);
+    std::vector<int> fcnt((size_t)std::max(F, 1), 0);
+    for (int64_t eq = 0; eq < NE; ++eq) {
+        const int s1 = eqsrc[eq * 4], a1 = eqsrc[eq * 4 + 1];
+        // the face: for a face point f*q + k; for a cross-point equation the face holding the
+        // contributors' shared edge (found from s1's flux row: its edge through the corner)
+        int f;
+        if (eq < Gf) {
+            f = (int)(eq / q);
+        } else {
+            const int cc = (a1 - 4 * q) / 2, d = (a1 - 4 * q) % 2;
+            const int e = d == 0 ? ((cc & 1) ? 1 : 0) : ((cc >> 1) ? 3 : 2);  // right/left, top/bottom
+            f = c->sub_face[s1 * 4 + e];
+        }
+        if (f < 0 || fcnt[f] >= nrow) {
+            c->err = "internal: flux equation outside its face block";
+            return ELMDDM_EINVAL;
+        }
+        feq[(size_t)f * nrow + fcnt[f]++] = (int)eq;
+        fpair[(size_t)f * 2] = std::min(s1, eqsrc[eq * 4 + 2]);
+        fpair[(size_t)f * 2 + 1] = std::max(s1, eqsrc[eq * 4 + 2]);
+    }
+    const int FL = 16;
+    std::vector<int> flist((size_t)std::max<int64_t>(G, 1) * FL * 2, -1), fn((size_t)std::max<int64_t>(G, 1), 0);
+    for (int f = 0; f < F; ++f)
+        for (int slot = 0; slot < 2; ++slot) {
+            const int s = fpair[(size_t)f * 2 + slot];
+            if (s < 0) continue;
+            for (int t = 0; t < ne; ++t) {
+                const int u = umap[(size_t)s * ne + t];
+                if (u < 0) continue;
+                if (fn[u] >= FL) {
+                    c->err = "internal: an unknown in more than 16 face blocks";
+                    return ELMDDM_EINVAL;
+                }
+                flist[((size_t)u * FL + fn[u]) * 2] = f;
+                flist[((size_t)u * FL + fn[u]) * 2 + 1] = slot * ne + t;
+                ++fn[u];
+            }
+        }
+    c->lat_nrow = nrow;
     std::vector<int> tI(std::max(c->plan.ntiles, 1), 0), tJ(std::max(c->plan.ntiles, 1), 0);
     for (int I = 0; I < c->plan.nblk; ++I)
         for (int J = 0; J <= I; ++J) {
@@ -167,6 +213,9 @@ elmddm_status build_tables_lattice(elmddm_ctx* c, const std::vector<int>& umap) 
             }
         }
     cudaError_t e;
+    if ((e = upload(&c->d_feq, feq)) != cudaSuccess || (e = upload(&c->d_fpair, fpair)) != cudaSuccess ||
+        (e = upload(&c->d_flist, flist)) != cudaSuccess)
+        return cuda_fail(c, e, "upload");
     if ((e = upload(&c->d_eqsrc, eqsrc)) != cudaSuccess || (e = upload(&c->d_rmap, rmap)) != cudaSuccess ||
         (e = upload(&c->d_tile_I, tI)) != cudaSuccess || (e = upload(&c->d_tile_J, tJ)) != cudaSuccess)
         return cuda_fail(c, e, "upload");
@@ -504,8 +553,9 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
                                                           (int64_t)c->ga_ld * c->qrow_cols),
                                       5 * z.chol_n + 2 * z.chol_blocks * (int64_t)ELM_TS + z.chol_n / 1024 + 16 +
                                           (c->iface_refine ? z.band_elems + 2 * z.chol_n : 0));
-    if (lat)  // dense Q [ld_q][G + 1] and its Gram [G + 1][G + 1] (elmddm_interface_assemble)
-        c->work_iface = std::max(c->work_iface, c->ld_q * (z.G + 1) + (z.G + 1) * (z.G + 1) + 64);
+    if (lat)  // face equation blocks Q_f [q + 2][2 ne + 1] and their Grams [2 ne + 2][2 ne + 1]
+        c->work_iface = std::max(c->work_iface, (int64_t)c->faces * ((int64_t)(c->lat_nrow + 3) / 4 * 4 * (2 * z.ne + 1) +
+                                                                     (2 * z.ne + 2) * (2 * z.ne + 1)) + 64);
     c->work_back = z.S * z.ld + z.S + 8;  // z, and the grid back-substitution's counters
     z.work_elems = std::max(c->work_factor, std::max(c->work_iface, c->work_back));
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
@@ -542,6 +592,9 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_rmap);
     cudaFree(c->d_tile_I);
     cudaFree(c->d_tile_J);
+    cudaFree(c->d_feq);
+    cudaFree(c->d_fpair);
+    cudaFree(c->d_flist);
     cudaFree(c->d_pair_ptr);
     cudaFree(c->d_pair_bc);
     cudaFree(c->d_terms);

@@ -137,6 +137,10 @@ struct elmddm_ctx {
     int* d_rmap = nullptr;       // layout 1: [G][4][(s, local column)], ascending s, -1 padded
     int* d_tile_I = nullptr;     // layout 1: tile id -> (I, J) of the dense plan
     int* d_tile_J = nullptr;
+    int* d_feq = nullptr;        // layout 1: [faces][q + 2] equations of each face block (-1 padded)
+    int* d_fpair = nullptr;      // layout 1: [faces][2] the block's two subdomains (ascending)
+    int* d_flist = nullptr;      // layout 1: [G][16][(face, column)] copies of every unknown
+    int lat_nrow = 0;            // layout 1: rows of a face block (q + 2)
     int plan_q = 0;              // unknowns per plan "face" (q, or 64 for the dense plan of layout 1)
     int64_t ld_q = 0;            // layout 1: leading dimension of the dense Q (n_eq rounded up)
     int npairs = 0, nterms = 0, ngterms = 0;

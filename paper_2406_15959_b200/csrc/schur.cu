@@ -443,21 +443,36 @@ __global__ void __launch_bounds__(256) k_bs_trsv_grid(const double* __restrict__
     }
 }
 
-// ---- interface, layout 1 (the lattice with cross points, reading R32): dense assembly ----------
-// Q_aug[e][u] (column-major, ld ldq): row e = flux equation e, the sum over its (<= 2) contributors
-// (s, flux row ar) -- ascending s, one pass each -- of P_s[ar, t] at u = umap[s][t]; column G holds
-// q_e = sum P_s[ar, ne] (the y column).  The buffer is zero on entry.  grid n_eq.
-__global__ void k_qdense(const double* __restrict__ Pbuf, int64_t pstride, int64_t pld, const int* __restrict__ eqsrc,
-                         const int* __restrict__ umap, int ne, int64_t G, double* __restrict__ Q, int64_t ldq) {
-    const int64_t e = blockIdx.x;
-    for (int c = 0; c < 2; ++c) {
-        const int s = eqsrc[e * 4 + 2 * c], ar = eqsrc[e * 4 + 2 * c + 1];
-        if (s >= 0)
-            for (int t = threadIdx.x; t <= ne; t += blockDim.x) {
-                const int64_t u = t < ne ? (int64_t)umap[(int64_t)s * ne + t] : G;
-                if (u >= 0) Q[e + u * ldq] += Pbuf[(int64_t)s * pstride + ar + (int64_t)t * pld];
+// ---- interface, layout 1 (the lattice with cross points, reading R32) ----------------------------
+// Face equation blocks: Q_f[r][col] (column-major, ld nrow) for the (q + 2) flux equations of face
+// f -- its point equations and the cross-point equations of its endpoints -- over the columns
+// [s1's ne local columns | s2's ne | rhs]: each contributor (s, flux row ar) writes its own column
+// range (no conflicts), the rhs q_e = P_s1[ar1, ne] + P_s2[ar2, ne] in ascending s.  The buffer is
+// zero on entry.  grid F.
+__global__ void k_qface(const double* __restrict__ Pbuf, int64_t pstride, int64_t pld, const int* __restrict__ eqsrc,
+                        const int* __restrict__ feq, const int* __restrict__ fpair, int nrow, int ldr, int ne,
+                        double* __restrict__ Qf, int64_t fstride) {
+    const int f = blockIdx.x;
+    double* Q = Qf + (int64_t)f * fstride;
+    const int s1 = fpair[f * 2];
+    for (int x = threadIdx.x; x < nrow * (2 * ne + 1); x += blockDim.x) {
+        const int r = x % nrow, col = x / nrow;
+        const int eq = feq[f * nrow + r];
+        if (eq < 0) continue;
+        double v = 0.0;
+        if (col < 2 * ne) {
+            const int slot = col / ne, t = col - slot * ne;
+            for (int cc = 0; cc < 2; ++cc) {
+                const int s = eqsrc[eq * 4 + 2 * cc], ar = eqsrc[eq * 4 + 2 * cc + 1];
+                if (s >= 0 && (s == s1 ? 0 : 1) == slot) v = Pbuf[(int64_t)s * pstride + ar + (int64_t)t * pld];
             }
-        __syncthreads();
+        } else {
+            for (int cc = 0; cc < 2; ++cc) {
+                const int s = eqsrc[eq * 4 + 2 * cc], ar = eqsrc[eq * 4 + 2 * cc + 1];
+                if (s >= 0) v += Pbuf[(int64_t)s * pstride + ar + (int64_t)ne * pld];
+            }
+        }
+        Q[r + (int64_t)col * ldr] = v;
     }
 }
 
@@ -466,13 +481,15 @@ __device__ __forceinline__ double lower_at(const double* __restrict__ A, int64_t
     return (r >> 6) >= (c >> 6) ? A[r + c * ld] : A[c + r * ld];
 }
 
-// M = sum_s scatter(S1_s) + Q^T Q and g = -sum_s scatter(T_E^T t_F) - Q^T q into the dense plan's
-// packed tiles (natural order, every lower tile present); element (a, b): the Gram of Q_aug plus
-// the S1 entries of the subdomains holding both unknowns (rmap: up to 4 (s, t) per unknown,
-// ascending s, -1 padded); unknowns >= G get a unit diagonal.  grid ntiles, 256 threads.
-__global__ void k_lat_mfill(const double* __restrict__ Maug, int64_t ldm, const double* __restrict__ Sbuf,
-                            int64_t sstride, int64_t sld, const int* __restrict__ rmap, int64_t G,
-                            const int* __restrict__ tile_I, const int* __restrict__ tile_J,
+// M = sum_s scatter(S1_s) + sum_f scatter(G_f) and g = -sum_s scatter(T_E^T t_F) - sum_f scatter(
+// Q_f^T q_f) into the dense plan's packed tiles (natural order, every lower tile present).  Element
+// (a, b): the S1 entries of the subdomains holding both unknowns (rmap: up to 4 (s, t) per unknown,
+// ascending s) plus the Gram entries of every copy pair in the face blocks holding both (flist: up
+// to 16 (face, column) per unknown, ascending face); unknowns >= G get a unit diagonal.
+constexpr int LAT_FL = 16;
+__global__ void k_lat_mfill(const double* __restrict__ Gf, int64_t gstride, int64_t gld, const int* __restrict__ flist,
+                            const double* __restrict__ Sbuf, int64_t sstride, int64_t sld, const int* __restrict__ rmap,
+                            int64_t G, const int* __restrict__ tile_I, const int* __restrict__ tile_J,
                             double* __restrict__ Mband) {
     const int t = blockIdx.x, I = tile_I[t], J = tile_J[t];
     double* T = Mband + (int64_t)t * ELM_TS;
@@ -495,15 +512,20 @@ __global__ void k_lat_mfill(const double* __restrict__ Maug, int64_t ldm, const 
                         v += lower_at(Sbuf + (int64_t)sa * sstride, rmap[a * 8 + 2 * ka + 1], rmap[b * 8 + 2 * kb + 1], sld);
                 }
             }
-            v += lower_at(Maug, a, b, ldm);
+            const int* la = flist + a * LAT_FL * 2;
+            const int* lb = flist + b * LAT_FL * 2;
+            for (int ka = 0; ka < LAT_FL && la[2 * ka] >= 0; ++ka)
+                for (int kb = 0; kb < LAT_FL && lb[2 * kb] >= 0; ++kb)
+                    if (la[2 * ka] == lb[2 * kb])
+                        v += lower_at(Gf + (int64_t)la[2 * ka] * gstride, la[2 * ka + 1], lb[2 * kb + 1], gld);
         }
         T[r + (int64_t)cc * ELM_TLD] = v;
     }
 }
 
-__global__ void k_lat_g(const double* __restrict__ Maug, int64_t ldm, const double* __restrict__ Sbuf, int64_t sstride,
-                        int64_t sld, const int* __restrict__ rmap, int ne, int64_t G, int64_t G_pad,
-                        double* __restrict__ g) {
+__global__ void k_lat_g(const double* __restrict__ Gf, int64_t gstride, int64_t gld, const int* __restrict__ flist,
+                        const double* __restrict__ Sbuf, int64_t sstride, int64_t sld, const int* __restrict__ rmap,
+                        int ne, int64_t G, int64_t G_pad, double* __restrict__ g) {
     const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= G_pad) return;
     if (a >= G) {
@@ -516,33 +538,40 @@ __global__ void k_lat_g(const double* __restrict__ Maug, int64_t ldm, const doub
         if (s < 0) break;
         v -= lower_at(Sbuf + (int64_t)s * sstride, rmap[a * 8 + 2 * k + 1], ne, sld);
     }
-    g[a] = v - lower_at(Maug, a, G, ldm);
+    const int* la = flist + a * LAT_FL * 2;
+    for (int k = 0; k < LAT_FL && la[2 * k] >= 0; ++k)
+        v -= lower_at(Gf + (int64_t)la[2 * k] * gstride, la[2 * k + 1], 2 * ne, gld);
+    g[a] = v;
 }
 
 }  // namespace
 
 cudaError_t run_interface_assemble_lattice(const elmddm_ctx* c, const double* Pbuf, const double* Sbuf, double* Mband,
                                            double* g, double* work, cudaStream_t st) {
-    const int64_t G = c->sz.G, NE = c->sz.n_eq, kaug = c->sz.kaug, ldq = c->ld_q, ldm = G + 1;
+    const int64_t G = c->sz.G, F = c->faces, kaug = c->sz.kaug, ne = c->sz.ne, nrow = c->lat_nrow;
     const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
-    double* Q = work;                 // [G + 1][ldq]
-    double* Maug = Q + ldq * (G + 1);  // [G + 1][G + 1], lower tiles
+    // (leading dimensions even: the GEMM stages 16-byte pairs of doubles)
+    const int64_t ldr = (nrow + 3) / 4 * 4, ncol = 2 * ne + 1, fstride = ldr * ncol, gld = (ncol + 2) / 2 * 2,
+                  gstride = gld * ncol;
+    double* Qf = work;                // [F][ncol][nrow]
+    double* Gf = Qf + F * fstride;    // [F][ncol][gld], lower tiles
     cudaError_t e;
     if (G <= 0) return cudaSuccess;
-    if ((e = cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (G + 1), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(Qf, 0, sizeof(double) * F * fstride, st)) != cudaSuccess) return e;
     {
         KTimer kt(c, ELMDDM_K_IFACE, st);
-        k_qdense<<<(unsigned)NE, 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_eqsrc, c->d_umap, (int)c->sz.ne, G, Q,
-                                                ldq);
+        k_qface<<<(unsigned)F, 256, 0, st>>>(Pbuf, pstride, c->sz.pbuf_ld, c->d_eqsrc, c->d_feq, c->d_fpair, (int)nrow,
+                                             (int)ldr, (int)ne, Qf, fstride);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    GemmArgs gq{(int)(G + 1), (int)(G + 1), (int)NE, Q, ldq, 0, Q, ldq, 0, Maug, ldm, 0, 1.0, 0.0, 1, 1};
+    // G_f = Q_f^T Q_f (symmetric: lower 64-tiles only)
+    GemmArgs gq{(int)ncol, (int)ncol, (int)nrow, Qf, ldr, fstride, Qf, ldr, fstride, Gf, gld, gstride, 1.0, 0.0, (int)F, 1};
     if ((e = gemm_launch(true, false, gq, st, c, ELMDDM_K_IFACE)) != cudaSuccess) return e;
     KTimer kt(c, ELMDDM_K_IFACE, st);
-    k_lat_mfill<<<(unsigned)c->plan.ntiles, 256, 0, st>>>(Maug, ldm, Sbuf, sstride, c->sz.sbuf_ld, c->d_rmap, G,
-                                                          c->d_tile_I, c->d_tile_J, Mband);
-    k_lat_g<<<(unsigned)((c->sz.G_pad + 255) / 256), 256, 0, st>>>(Maug, ldm, Sbuf, sstride, c->sz.sbuf_ld, c->d_rmap,
-                                                                   (int)c->sz.ne, G, c->sz.G_pad, g);
+    k_lat_mfill<<<(unsigned)c->plan.ntiles, 256, 0, st>>>(Gf, gstride, gld, c->d_flist, Sbuf, sstride, c->sz.sbuf_ld,
+                                                          c->d_rmap, G, c->d_tile_I, c->d_tile_J, Mband);
+    k_lat_g<<<(unsigned)((c->sz.G_pad + 255) / 256), 256, 0, st>>>(Gf, gstride, gld, c->d_flist, Sbuf, sstride,
+                                                                   c->sz.sbuf_ld, c->d_rmap, (int)ne, G, c->sz.G_pad, g);
     return cudaGetLastError();
 }
 
