@@ -23,15 +23,14 @@ CONFIGS = [
     # face-point layout of reading R1 (q points per edge, no shared cross points).
     # N = 8 x 8 and 16 x 16 fit every panel kernel's ld <= 3008 (with the M damping rows).
     # The near-square, numerically rank-deficient local problems defeat the undamped unpivoted-QR
-    # elimination (oracle and GPU alike), so these run the damped local LS of reading R29 with
-    # lambda = 1e-9 / 1e-10 x sigma_max(K^s) of an interior subdomain (1.34e5 / 6.58e4), chosen by
-    # the lambda sweep of tools/pinv_study.py (DESIGN.md §10 NEXT-2).
-    dict(name="t2-8x8", P=8, M=1024, p=31, q=32, problem=4, seed=5, tikhonov=1.3e-4),
-    dict(name="t2-16x16", P=16, M=256, p=15, q=16, problem=4, seed=6, tikhonov=6.6e-6),
-    # 4 x 4: m + M = 8321 rows (ld 8352) -- the QR panels run on 4-CTA clusters with a reduced
-    # ring; lambda = 1e-10 sigma_max(K^s) (2.2e5); undamped, the interface Cholesky meets a
-    # non-positive pivot
-    dict(name="t2-4x4", P=4, M=4096, p=63, q=64, problem=4, seed=7, tikhonov=2.2e-5),
+    # elimination (oracle and GPU alike), so these run the damped local LS with the a-priori rule
+    # lambda_s = eps max(m, M) ||K^s||_F (reading R33; round 1 swept a uniform lambda against the
+    # exact solution instead, tools/pinv_study.py -- superseded: the rule is both untuned and more
+    # accurate, oracle 1.5e-9 / 4.2e-9 at 8x8 / 16x16 vs 7.8e-8 / 1.8e-7).
+    dict(name="t2-8x8", P=8, M=1024, p=31, q=32, problem=4, seed=5, tikhonov=-1.0),
+    dict(name="t2-16x16", P=16, M=256, p=15, q=16, problem=4, seed=6, tikhonov=-1.0),
+    # 4 x 4: m + M = 8321 rows (ld 8352) -- the QR panels run on 4-CTA clusters with a reduced ring
+    dict(name="t2-4x4", P=4, M=4096, p=63, q=64, problem=4, seed=7, tikhonov=-1.0),
 ]
 # the paper's own workload ON ITS OWN LATTICE (NEXT-2, reading R32): the (2^8 + 1)^2 points are
 # one global lattice shared by the subdomains (layout 1): every subdomain holds its (256/P + 1)^2
