@@ -123,10 +123,14 @@ __global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
                 int n = wn * 16 + nt * 8 + (lane >> 2);
                 bf[nt] = TB ? Bs[kk * PAD_MN + n] : Bs[n * PAD_K + kk];
             }
+            // (8 x 8 sub-tiles wholly outside the valid rows / columns -- the last row or column
+            // tile of a batch, e.g. kaug = 4q + 1 -- are skipped: warp-uniform predicates)
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+                for (int nt = 0; nt < 2; ++nt)
+                    if (wm * 32 + mt * 8 < mv && wn * 16 + nt * 8 < nv)
+                        dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
         }
     }
     cp_wait<0>();
