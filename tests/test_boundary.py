@@ -51,11 +51,14 @@ def test_config_validation_is_synchronous_and_cpu_safe():
         dict(P=2, M=512, p=16, q=16),    # m < M (underdetermined local LS)
         dict(P=0, M=64, p=16, q=16),
         dict(P=2, M=64, p=16, q=16, s_begin=3, s_end=2),
-        dict(P=2, M=64, p=100, q=16),    # ld > 3008
+        dict(P=9, M=64, p=100, q=16),    # ld > ~9.6k (grid panel) with more than 64 subdomains
+        dict(P=2, M=64, p=16, q=15, layout=1),   # lattice: needs p == q
+        dict(P=2, M=64, p=16, q=16, layout=2),   # unknown layout
+        dict(P=2, M=64, p=16, q=16, problem=7, layout=1),   # plate on the lattice: not supported
     ]
     for b in bad:
-        cfg = _lib.Config(b["P"], b["M"], b["p"], b["q"], 0, 0, 0.125, 0.5, 0, b.get("s_begin", 0),
-                          b.get("s_end", max(b["P"] ** 2, 1)), 0, 0)
+        cfg = _lib.Config(b["P"], b["M"], b["p"], b["q"], b.get("problem", 0), 0, 0.125, 0.5, 0, b.get("s_begin", 0),
+                          b.get("s_end", max(b["P"] ** 2, 1)), 0, b.get("layout", 0))
         h = C.c_void_p()
         assert L.elmddm_create(C.byref(cfg), 0, C.byref(h)) == 1
         assert not h.value
