@@ -38,17 +38,36 @@ __global__ void __launch_bounds__(256) k_spmv_sym(const double* __restrict__ Mb,
             acc += v * __ldg(xs + c);
         }
     }
+    // transposed part: y[j] += sum_i T(i, j) x[i] over the column tiles (I', I); warp w owns the
+    // columns j in [8w, 8w + 8), lanes the rows i = lane, lane + 32 -- coalesced tile reads, one
+    // warp reduction per column at the end
+    __shared__ double part2[NB];
+    const int lane = tid & 31, w = tid >> 5;
+    double tacc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tacc[u] = 0.0;
     const int c0 = cptr[I], nc = cptr[I + 1] - c0;
     for (int q = 0; q < nc; ++q) {
         const int Ip = cdep[c0 + q].x;
         const double* T = Mb + (int64_t)cdep[c0 + q].y * ELM_TS;
         const double* xs = x + (int64_t)Ip * NB;
-#pragma unroll 4
-        for (int c = p * 16; c < p * 16 + 16; ++c) acc += T[r * LP + c] * __ldg(xs + c);  // element (c, r)
+        const double x0 = __ldg(xs + lane), x1 = __ldg(xs + lane + 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = 8 * w + u;
+            tacc[u] += T[lane + j * LP] * x0 + T[lane + 32 + j * LP] * x1;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        double v = tacc[u];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) part2[8 * w + u] = v;
     }
     part[p][r] = acc;
     __syncthreads();
-    if (tid < NB) y[(int64_t)I * NB + tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+    if (tid < NB)
+        y[(int64_t)I * NB + tid] = ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid])) + part2[tid];
 }
 
 __global__ void k_cg_gather(const double* __restrict__ g, const int* __restrict__ fbase, int q, int64_t G,

@@ -606,15 +606,19 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
 #undef FOR_FRAG
 
 // ------------------------------------------------------------------------------------------
-// Triangular solves as ONE cooperative (co-resident) kernel per direction: block-row i is owned
-// by CTA i mod gridDim.x; each CTA processes its rows in dependency order, streams the tiles of
-// the row through a 2-stage cp.async ring, waits for the producers of the solved blocks it needs
-// on per-block completion flags (acquire/release, monotonically increasing epoch), subtracts the
-// GEMV contributions and solves with the diagonal tile by warp-level substitution.
-//   dir 0: L z = rhs    tiles (i, j), first[i] <= j < i
-//   dir 1: L^T u = rhs  tiles (j, i), i < j <= last[i], used transposed
+// Triangular solves as ONE cooperative (co-resident) kernel per direction.  Tasks (block rows, or
+// chunks of a block row's dependency list: plan.cu build_trsv_tasks) are dealt in list order
+// through a counter; a CTA streams the dependency tiles of its task straight from global memory
+// into registers (no shared-memory staging, no block barrier per tile), each warp on its own:
+// lane k checks the completion flag of dependency q + k (acquire), one ballot tells the warp how
+// many of the next 32 dependencies are published, and those tiles are consumed without further
+// polling, two at a time for memory-level parallelism.  The products are reduced once per task
+// in a fixed order, then the diagonal tile (prefetched into shared memory) is solved by
+// warp-level substitution and the block's flag released.
+//   dir 0: L z = rhs    tiles (i, j), first[i] <= j < i     thread (row r, column group of 16)
+//   dir 1: L^T u = rhs  tiles (j, i), i < j <= last[i]      warp: 8 columns c, lanes: rows r, r + 32
 // ------------------------------------------------------------------------------------------
-constexpr int TRSV_SMEM = (2 * ELM_TS + 4 * NB + 3 * NB) * 8;
+constexpr int TRSV_SMEM = (ELM_TS + 4 * NB + 2 * NB) * 8;
 
 __device__ __forceinline__ void load_tile_async(double* dst, const double* src) {
     for (int t = threadIdx.x; t < ELM_TS / 2; t += blockDim.x) {
@@ -624,105 +628,193 @@ __device__ __forceinline__ void load_tile_async(double* dst, const double* src) 
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
-__global__ void __launch_bounds__(256) k_band_trsv(const double* __restrict__ Mb, int nblk, const int* __restrict__ diag_tid,
-                                                   const int* __restrict__ dptr, const int2* __restrict__ dep,
-                                                   const double* __restrict__ rhs, double* __restrict__ out, int* flags,
-                                                   int epoch, int dir, ElmStatus* status) {
+#ifdef ELM_CHOL_PROF
+// per task of the last launch of each direction: start, end, flag-wait ns, CTA (tools/trsv_prof.py)
+__device__ unsigned long long g_trsv_prof[2][400000][4];
+#endif
+
+template <int DIR>
+__device__ __forceinline__ void trsv_tile(const double* __restrict__ Mb, int2 d, const double* out, int r, int cg,
+                                          int lane, int w, double& sacc, double (&tacc)[8]) {
+    const double* T = Mb + (int64_t)d.y * ELM_TS;
+    const double* xj = out + (int64_t)d.x * NB;
+    if (DIR == 0) {  // s[r] += sum_c T(r, c) x_j[c]; element (r, c) at r + c LP
+        double tv[16], xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            tv[u] = __ldg(T + (cg * 16 + u) * LP + r);
+            xv[u] = __ldcg(xj + cg * 16 + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sacc += tv[u] * xv[u];
+    } else {         // s[c] += sum_r T(r, c) x_j[r]
+        const double x0 = __ldcg(xj + lane), x1 = __ldcg(xj + lane + 32);
+        double t0[8], t1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            t0[u] = __ldg(T + (8 * w + u) * LP + lane);
+            t1[u] = __ldg(T + (8 * w + u) * LP + lane + 32);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tacc[u] += t0[u] * x0 + t1[u] * x1;
+    }
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__ Mb, int ntasks, int nblk,
+                                                      const int* __restrict__ diag_tid, const int4* __restrict__ tasks,
+                                                      const int* __restrict__ rowslot, const int2* __restrict__ dep,
+                                                      const double* __restrict__ rhs, double* out, int* flags,
+                                                      int* pflags, double* __restrict__ ppart, int epoch,
+                                                      ElmStatus* status) {
     extern __shared__ __align__(16) double tsm[];
-    double* tiles = tsm;                  // [2][ELM_TS]
-    double* part = tiles + 2 * ELM_TS;    // [4][64]
+    double* dtile = tsm;                  // [ELM_TS] the diagonal tile (i, i)
+    double* part = dtile + ELM_TS;        // [4][64]
     double* acc = part + 4 * NB;          // [64]
-    double* xs = acc + NB;                // [64]
-    double* rdv = xs + NB;                // [64] reciprocal diagonal
-    const int tid = threadIdx.x;
-    // rows dealt in order through one counter (flags[nblk], zeroed before the launch): a CTA held up
-    // by a long dependency wait does not delay rows a static round robin would have given it
+    double* rdv = acc + NB;               // [64] reciprocal diagonal
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int r = tid & 63, cg = tid >> 6;
     __shared__ int s_next;
     for (;;) {
         if (tid == 0) s_next = atomicAdd(flags + nblk, 1);
         __syncthreads();
         const int it = s_next;
-        if (it >= nblk) break;
-        const int i = dir == 0 ? it : nblk - 1 - it;
+        if (it >= ntasks) break;
+        const int4 tk = tasks[it];
+        const int i = tk.x;
+        const bool fin = tk.w < 0;
         const int64_t i0 = (int64_t)i * NB;
-        // dependencies: forward (j, tile (i, j)) ascending j; backward (j, tile (j, i)) descending j
-        const int d0 = dptr[i], nj = dptr[i + 1] - d0;
-        auto tile_of = [&](int q) -> const double* {  // q-th dependency tile, then the diagonal
-            return Mb + (int64_t)(q == nj ? diag_tid[i] : dep[d0 + q].y) * ELM_TS;
-        };
-        if (tid < NB) acc[tid] = rhs[i0 + tid];
-        // the dependency tiles' products are accumulated in registers (thread (r, column group) for
-        // the forward direction, (c, row quarter) for the backward one) and reduced once per block
-        // row, in a fixed order: two barriers per tile instead of four
-        double sacc = 0.0;
-        load_tile_async(tiles, tile_of(0));
-        for (int q = 0; q < nj; ++q) {
-            const int st = q & 1;
-            const int j = dep[d0 + q].x;
-            if (tid == 0) wait_flag(flags + j, epoch, status, j);
-            __syncthreads();  // x_j published; every thread done with tile q-1 and xs
-            if (tid < NB) xs[tid] = __ldcg(out + (int64_t)j * NB + tid);
-            load_tile_async(tiles + (st ^ 1) * ELM_TS, tile_of(q + 1));  // (q + 1 == nj: the diagonal)
-            asm volatile("cp.async.wait_group 1;\n" ::);
-            __syncthreads();  // tile q and xs visible
-            const double* T = tiles + st * ELM_TS;
-            if (dir == 0) {  // s[r] += sum_c T[r][c] x[c]: thread (r, c-group of 16)
-                const int r = tid & 63, cgp = tid >> 6;
-#pragma unroll 4
-                for (int c = cgp * 16; c < cgp * 16 + 16; ++c) sacc += T[c * LP + r] * xs[c];
-            } else {         // s[c] += sum_r T[r][c] x[r]: thread (c, r = rq + 4 l)
-                const int c = tid >> 2, rq = tid & 3;
-#pragma unroll 4
-                for (int l = 0; l < 16; ++l) sacc += T[c * LP + rq + 4 * l] * xs[rq + 4 * l];
+        const int d0 = tk.y, nj = tk.z - tk.y;
+#ifdef ELM_CHOL_PROF
+        unsigned long long pt0 = globaltimer(), pfw = 0;
+#endif
+        if (fin) {
+            load_tile_async(dtile, Mb + (int64_t)diag_tid[i] * ELM_TS);
+            if (tid < NB) acc[tid] = rhs[i0 + tid];
+        }
+        double sacc = 0.0, tacc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tacc[u] = 0.0;
+        for (int q = 0, ready = 0; q < nj;) {
+            if (q >= ready) {
+                // lane k: is dependency q + k published?  (the first unpublished one bounds the batch)
+#ifdef ELM_CHOL_PROF
+                const unsigned long long w0 = globaltimer();
+#endif
+                uint64_t t0 = 0;
+                for (;;) {
+                    int ok = 1;
+                    if (q + lane < nj) ok = ld_acquire(flags + dep[d0 + q + lane].x) >= epoch;
+                    const unsigned nr = ~__ballot_sync(0xffffffffu, ok);
+                    const int n = nr ? __ffs(nr) - 1 : 32;
+                    if (n > 0) {
+                        ready = q + n;
+                        break;
+                    }
+                    if (!t0) {
+                        t0 = globaltimer();
+                    } else if (globaltimer() - t0 > 10000000000ull) {  // as wait_flag: report, give up
+                        if (lane == 0) elm_set_status(status, ELMDDM_ENUMERIC, -1 - i);
+                        ready = nj;
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+                __syncwarp();
+#ifdef ELM_CHOL_PROF
+                if (tid == 0) pfw += globaltimer() - w0;
+#endif
+            }
+            const int qe = ready < nj ? ready : nj;
+            for (; q + 1 < qe; q += 2) {
+                trsv_tile<DIR>(Mb, dep[d0 + q], out, r, cg, lane, w, sacc, tacc);
+                trsv_tile<DIR>(Mb, dep[d0 + q + 1], out, r, cg, lane, w, sacc, tacc);
+            }
+            if (q < qe) trsv_tile<DIR>(Mb, dep[d0 + q++], out, r, cg, lane, w, sacc, tacc);
+        }
+        // reduce the partial products in a fixed order
+        if (DIR == 0) {
+            part[cg * NB + r] = sacc;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                double v = tacc[u];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) part[8 * w + u] = v;
             }
         }
         asm volatile("cp.async.wait_group 0;\n" ::);  // the diagonal tile
-        // reduce the partial products in a fixed order
-        if (dir == 0) {
-            part[(tid >> 6) * NB + (tid & 63)] = sacc;
-        } else {
-            sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-            sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-            if ((tid & 3) == 0) part[tid >> 2] = sacc;
+        __syncthreads();
+        if (!fin) {  // partial task: publish the chunk's 64 sums in slot tk.w
+            if (tid < NB) {
+                ppart[(int64_t)tk.w * NB + tid] =
+                    DIR == 0 ? (part[tid] + part[NB + tid]) + (part[2 * NB + tid] + part[3 * NB + tid]) : part[tid];
+                __threadfence();
+            }
+            __syncthreads();
+            if (tid == 0) st_release(pflags + tk.w, epoch);
+#ifdef ELM_CHOL_PROF
+            if (tid == 0 && it < 400000) {
+                unsigned long long* rp = g_trsv_prof[DIR][it];
+                rp[0] = pt0; rp[1] = globaltimer(); rp[2] = pfw; rp[3] = blockIdx.x;
+            }
+#endif
+            continue;
+        }
+        const int nparts = -1 - tk.w;
+        const int s0 = rowslot[i];
+        if (nparts > 0) {  // the row's partial tasks (earlier in the list) have published their slots
+            if (tid == 0)
+                for (int c = 0; c < nparts; ++c) wait_flag(pflags + s0 + c, epoch, status, i);
+            __syncthreads();
+        }
+        if (tid < NB) {
+            if (nj > 0) {
+                const double own = DIR == 0 ? (part[tid] + part[NB + tid]) + (part[2 * NB + tid] + part[3 * NB + tid]) : part[tid];
+                double tot = 0.0;  // the chunks' sums in fixed order, the own (last) chunk last
+                for (int c = 0; c < nparts; ++c) tot += __ldcg(ppart + (int64_t)(s0 + c) * NB + tid);
+                acc[tid] -= nparts == 0 ? own : tot + own;
+            }
+            rdv[tid] = 1.0 / dtile[tid * LP + tid];
         }
         __syncthreads();
-        if (tid < NB && nj > 0)
-            acc[tid] -= dir == 0 ? (part[tid] + part[NB + tid]) + (part[2 * NB + tid] + part[3 * NB + tid]) : part[tid];
-        {
-            const double* T = tiles + (nj & 1) * ELM_TS;  // the diagonal tile (i, i)
-            if (tid < NB) rdv[tid] = 1.0 / T[tid * LP + tid];
-            __syncthreads();
-            if (tid < 32) {
-                // diagonal solve with the lower tile (i, i): warp-level substitution
-                const int lane = tid;
-                double z0 = acc[lane], z1 = acc[lane + 32];
-                if (dir == 0) {
-                    for (int cc = 0; cc < NB; ++cc) {
-                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
-                        if (lane > cc) z0 -= T[cc * LP + lane] * xc;
-                        if (lane + 32 > cc) z1 -= T[cc * LP + lane + 32] * xc;
-                        if (lane == (cc & 31)) {
-                            if (cc < 32) z0 = xc;
-                            else z1 = xc;
-                        }
-                    }
-                } else {
-                    for (int cc = NB - 1; cc >= 0; --cc) {
-                        double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
-                        if (lane < cc) z0 -= T[lane * LP + cc] * xc;
-                        if (lane + 32 < cc) z1 -= T[(lane + 32) * LP + cc] * xc;
-                        if (lane == (cc & 31)) {
-                            if (cc < 32) z0 = xc;
-                            else z1 = xc;
-                        }
+        if (tid < 32) {
+            // diagonal solve with the lower tile (i, i): warp-level substitution
+            const double* T = dtile;
+            double z0 = acc[lane], z1 = acc[lane + 32];
+            if (DIR == 0) {
+                for (int cc = 0; cc < NB; ++cc) {
+                    double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                    if (lane > cc) z0 -= T[cc * LP + lane] * xc;
+                    if (lane + 32 > cc) z1 -= T[cc * LP + lane + 32] * xc;
+                    if (lane == (cc & 31)) {
+                        if (cc < 32) z0 = xc;
+                        else z1 = xc;
                     }
                 }
-                out[i0 + lane] = z0;
-                out[i0 + lane + 32] = z1;
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) st_release(flags + i, epoch);
+            } else {
+                for (int cc = NB - 1; cc >= 0; --cc) {
+                    double xc = __shfl_sync(0xffffffffu, cc < 32 ? z0 : z1, cc & 31) * rdv[cc];
+                    if (lane < cc) z0 -= T[lane * LP + cc] * xc;
+                    if (lane + 32 < cc) z1 -= T[(lane + 32) * LP + cc] * xc;
+                    if (lane == (cc & 31)) {
+                        if (cc < 32) z0 = xc;
+                        else z1 = xc;
+                    }
+                }
             }
+            out[i0 + lane] = z0;
+            out[i0 + lane + 32] = z1;
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release(flags + i, epoch);
+#ifdef ELM_CHOL_PROF
+            if (lane == 0 && it < 400000) {
+                unsigned long long* rp = g_trsv_prof[DIR][it];
+                rp[0] = pt0; rp[1] = globaltimer(); rp[2] = pfw; rp[3] = blockIdx.x;
+            }
+#endif
         }
         __syncthreads();
     }
@@ -750,6 +842,14 @@ __global__ void k_perm_scatter(const double* __restrict__ y, const int* __restri
 #ifdef ELM_CHOL_PROF
 extern "C" int elmddm_debug_chol_prof(void* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_chol_prof, sizeof(unsigned long long) * 6 * (size_t)n);
+}
+extern "C" int elmddm_debug_trsv_tasks(const elmddm_ctx* c, int dir, void* host) {  // int4[sv_ntasks[dir]]
+    if (!host) return c->sv_ntasks[dir];
+    return (int)cudaMemcpy(host, c->d_sv_tasks[dir], sizeof(int4) * c->sv_ntasks[dir], cudaMemcpyDeviceToHost);
+}
+extern "C" int elmddm_debug_trsv_prof(void* host, int dir, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_trsv_prof, sizeof(unsigned long long) * 4 * (size_t)n,
+                                     sizeof(unsigned long long) * 4 * 400000 * (size_t)dir);
 }
 extern "C" int elmddm_debug_chol_dprof(void* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_chol_dprof, sizeof(unsigned long long) * 8 * (size_t)n);
@@ -797,7 +897,9 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     if (!grid_ll) {
         if ((e = cudaFuncSetAttribute(k_chol_ll, cudaFuncAttributeMaxDynamicSharedMemorySize, llc::SMEM)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_band_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
+            (e = cudaFuncSetAttribute(k_band_trsv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_band_trsv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM)) !=
                 cudaSuccess)
             return e;
         int per_sm = 0;
@@ -807,7 +909,12 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         // the solves are latency-bound (one dependent chain per tile row): as many co-resident
         // CTAs as fit, at most 3 per SM (cfg3: 2.79 ms at 1, 2.02 ms at 3)
         int sv_per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sv_per, k_band_trsv, 256, TRSV_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sv_per, k_band_trsv<1>, 256, TRSV_SMEM);
+        {
+            int sv0 = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sv0, k_band_trsv<0>, 256, TRSV_SMEM);
+            sv_per = std::min(sv_per, sv0);
+        }
         sv_per = std::min(sv_per, 3);
         if (const char* env = getenv("ELMDDM_TRSV_CTAS_PER_SM")) sv_per = std::min(sv_per, atoi(env));
         grid_sv = std::max(sv_per, 1) * c->nsm;
@@ -870,23 +977,27 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     }
     // triangular solves: one cooperative wavefront kernel per direction (b -> z -> x)
     auto solve = [&](double* b, double* x) -> cudaError_t {
-        int grid = nblk < grid_sv ? nblk : grid_sv;
         int* flags = c->d_flags;
         for (int dir = 0; dir < 2; ++dir) {
             int epoch = ++c->trsv_epoch;
             const double* rhs = dir == 0 ? b : z;
             double* out = dir == 0 ? z : x;
-            int nblk_v = nblk;
+            int nblk_v = nblk, ntasks = c->sv_ntasks[dir];
+            const int grid = ntasks < grid_sv ? ntasks : grid_sv;
             const int* dt = c->d_diag_tid;
-            const int* dp = dir == 0 ? c->d_fwd_ptr : c->d_bwd_ptr;
+            const int4* tl = c->d_sv_tasks[dir];
+            const int* rs = c->d_sv_slot[dir];
             const int2* dl = dir == 0 ? c->d_fwd : c->d_bwd;
+            int* pf = c->d_pflags;
+            double* pp = c->d_ppart;
             ElmStatus* stp = c->d_status;
-            void* args[] = {(void*)&Mband, (void*)&nblk_v, (void*)&dt, (void*)&dp, (void*)&dl, (void*)&rhs,
-                            (void*)&out, (void*)&flags, (void*)&epoch, (void*)&dir, (void*)&stp};
+            void* args[] = {(void*)&Mband, (void*)&ntasks, (void*)&nblk_v, (void*)&dt, (void*)&tl, (void*)&rs,
+                            (void*)&dl,    (void*)&rhs,    (void*)&out,    (void*)&flags, (void*)&pf, (void*)&pp,
+                            (void*)&epoch, (void*)&stp};
             cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the row counter
             if (e1 != cudaSuccess) return e1;
             KTimer kt(c, ELMDDM_K_TRSV, st);
-            cudaError_t e2 = cudaLaunchCooperativeKernel((void*)k_band_trsv, dim3(grid), dim3(256), args, TRSV_SMEM, st);
+            cudaError_t e2 = cudaLaunchCooperativeKernel(dir == 0 ? (void*)k_band_trsv<0> : (void*)k_band_trsv<1>, dim3(grid), dim3(256), args, TRSV_SMEM, st);
             if (e2 != cudaSuccess) return e2;
         }
         return cudaSuccess;

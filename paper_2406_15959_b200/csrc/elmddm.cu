@@ -435,6 +435,23 @@ elmddm_status finish_tables(elmddm_ctx* c, const std::vector<int>& qsrc, const s
         (e = upload(&c->d_bwd_ptr, pl.bwd_ptr)) != cudaSuccess || (e = upload(&c->d_bwd, pl.bwd)) != cudaSuccess ||
         (e = upload(&c->d_ntc, pl.ntc)) != cudaSuccess)
         return cuda_fail(c, e, "upload");
+    {
+        // triangular-solve task lists (heavy block rows split into chunks, plan.cu)
+        int nslots = 0;
+        for (int dir = 0; dir < 2; ++dir) {
+            std::vector<int4> svt;
+            std::vector<int> rs;
+            nslots = std::max(nslots, build_trsv_tasks(pl, dir, c->trsv_chunk, svt, rs));
+            c->sv_ntasks[dir] = (int)svt.size();
+            if ((e = upload(&c->d_sv_tasks[dir], svt)) != cudaSuccess || (e = upload(&c->d_sv_slot[dir], rs)) != cudaSuccess)
+                return cuda_fail(c, e, "upload");
+        }
+        nslots = std::max(nslots, 1);
+        if ((e = cudaMalloc((void**)&c->d_pflags, sizeof(int) * nslots)) != cudaSuccess ||
+            (e = cudaMemset(c->d_pflags, 0, sizeof(int) * nslots)) != cudaSuccess ||
+            (e = cudaMalloc((void**)&c->d_ppart, sizeof(double) * ELM_NB * nslots)) != cudaSuccess)
+            return cuda_fail(c, e, "trsv slots");
+    }
     if ((e = cudaMalloc((void**)&c->d_colcnt, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMemset(c->d_colcnt, 0, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMalloc((void**)&c->d_cready, sizeof(int) * nblk)) != cudaSuccess ||
@@ -504,6 +521,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_IMPLICIT_E")) c->implicit_e = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_IFACE_REFINE")) c->iface_refine = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL_GRID")) c->panel_grid = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_TRSV_CHUNK")) c->trsv_chunk = atoi(env);
         c->implicit_e = c->implicit_e && c->use_tma;
         // 4-CTA cluster panels cut the per-subdomain latency chain of the QR but spend more SM
         // time: they win for the small per-rank slabs of multi-GPU runs (config 3: 32 subdomains
@@ -605,6 +623,12 @@ void elmddm_destroy(elmddm_ctx* c) {
     cudaFree(c->d_tile_map);
     cudaFree(c->d_klist);
     cudaFree(c->d_diag_tid);
+    for (int dir = 0; dir < 2; ++dir) {
+        cudaFree(c->d_sv_tasks[dir]);
+        cudaFree(c->d_sv_slot[dir]);
+    }
+    cudaFree(c->d_pflags);
+    cudaFree(c->d_ppart);
     cudaFree(c->d_fwd_ptr);
     cudaFree(c->d_fwd);
     cudaFree(c->d_bwd_ptr);

@@ -103,6 +103,13 @@ struct CholPlan {
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
                         int crit_band, CholPlan& pl, int split_min = 0);
 double schedule_chol_tasks(CholPlan& pl, int workers);
+// Task list of one triangular-solve direction (dir 0 forward, 1 backward; chol.cu k_band_trsv):
+// the dependency list of a block row longer than `chunk` tiles is split into balanced chunks;
+// every chunk but the last is a partial task {i, q0, q1, slot} writing its 64 partial sums to a
+// slot, placed in the list right after the row its latest dependency waits for; the row's final
+// task {i, q0, q1, -1 - nparts} takes the last chunk, the partial slots rowslot[i] ..
+// rowslot[i] + nparts - 1 in fixed order, and the diagonal solve.  Returns the slot count.
+int build_trsv_tasks(const CholPlan& pl, int dir, int chunk, std::vector<int4>& tasks, std::vector<int>& rowslot);
 int chol_split_min();
 int panel_cl_stage(int64_t ld, int smem_optin);  // qr.cu: ring stage of the cluster panel, 0 = ld too tall
 void export_tasks(const CholPlan& pl, int32_t* tasks);
@@ -166,6 +173,13 @@ struct elmddm_ctx {
     int panel_cluster = 0;  // QR panel blocks on 4-CTA clusters (default for S <= 48; ELMDDM_PANEL_CLUSTER)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
     mutable int trsv_epoch = 0;
+    int trsv_chunk = 0;                 // dependency tiles per triangular-solve task, 0 = whole rows
+                                        // (ELMDDM_TRSV_CHUNK; 32 / 64 measured slower at config 4)
+    int4* d_sv_tasks[2] = {nullptr, nullptr};  // per direction: the task lists of build_trsv_tasks
+    int* d_sv_slot[2] = {nullptr, nullptr};    // per direction: first partial slot of each block row
+    int sv_ntasks[2] = {0, 0};
+    int* d_pflags = nullptr;            // [slots] completion flags of the partial tasks
+    double* d_ppart = nullptr;          // [slots][64] partial sums
     // ordering + symbolic factorisation of the Schur matrix (plan.cu) and its device copies
     CholPlan plan;
     int ncrit = 0;                   // the first ncrit tasks are the critical band (I - J <= crit_band)

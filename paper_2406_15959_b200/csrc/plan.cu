@@ -291,6 +291,64 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
     return nupd;
 }
 
+int build_trsv_tasks(const CholPlan& pl, int dir, int chunk, std::vector<int4>& tasks, std::vector<int>& rowslot) {
+    const int nb = pl.nblk;
+    const std::vector<int>& ptr = dir == 0 ? pl.fwd_ptr : pl.bwd_ptr;
+    const std::vector<int2>& dep = dir == 0 ? pl.fwd : pl.bwd;
+    if (chunk < 1) chunk = 1 << 30;
+    // 1. tasks in solve order: a row's partial chunks, then its final task
+    std::vector<int4> lst;
+    rowslot.assign(nb, 0);
+    int nslots = 0;
+    for (int t = 0; t < nb; ++t) {
+        const int i = dir == 0 ? t : nb - 1 - t;
+        const int d0 = ptr[i], nj = ptr[i + 1] - d0;
+        const int nch = nj <= chunk ? 1 : (nj + chunk - 1) / chunk;
+        rowslot[i] = nslots;
+        for (int c = 0; c + 1 < nch; ++c)
+            lst.push_back(int4{i, d0 + (int)((int64_t)nj * c / nch), d0 + (int)((int64_t)nj * (c + 1) / nch), nslots++});
+        lst.push_back(int4{i, d0 + (int)((int64_t)nj * (nch - 1) / nch), d0 + nj, -nch});  // -1 - nparts
+    }
+    // 2. list order = earliest-start order of a latency model of the kernel (unbounded CTAs): a task
+    //    consumes its tiles in order, each no earlier than TL/2 after its block's solution is
+    //    published, TT per tile; a final task adds the partial sums and the diagonal solve.  The
+    //    key of a task, the model time its last input is published, is strictly larger than the
+    //    key of every task it waits for, so the sorted list stays topological (deadlock freedom of
+    //    the in-order dealing).  The row order alone leaves the backward solve's CTAs blocked on
+    //    the top separators' chain while ready rows wait further down the list.
+    const double TT = 1.0, TL = 3.0, TD = 1.5;
+    std::vector<double> fin_row(nb, 0.0), fin_task(lst.size(), 0.0), key(lst.size(), 0.0);
+    for (size_t k = 0; k < lst.size(); ++k) {
+        const int4 tk = lst[k];
+        double t = 0.0, last_in = 0.0;
+        for (int q = tk.y; q < tk.z; ++q) {
+            const double rdy = fin_row[dep[q].x];
+            last_in = std::max(last_in, rdy);
+            t = std::max(t, rdy + TL / 2) + TT;
+        }
+        if (tk.w < 0) {
+            const int np = -1 - tk.w;
+            for (int c = 0; c < np; ++c) {
+                const double rdy = fin_task[k - np + c];  // the row's partial tasks precede it
+                last_in = std::max(last_in, rdy);
+                t = std::max(t, rdy + TL / 2);
+            }
+            t += TL / 2 + TD;
+            fin_row[tk.x] = t;
+        } else {
+            t += TL / 2;
+        }
+        fin_task[k] = t;
+        key[k] = last_in;
+    }
+    std::vector<int> ord(lst.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = (int)k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return key[x] < key[y]; });
+    tasks.clear();
+    for (int k : ord) tasks.push_back(lst[k]);
+    return nslots;
+}
+
 // Task order of the persistent factorisation kernel.  The kernel deals tasks to whichever CTA is
 // free, in list order (dynamic counter); a CTA streams the k-list of its task, waiting for each
 // update's tiles only when it reaches them, then waits for the diagonal tile and finishes.  So the

@@ -889,7 +889,37 @@ __device__ __forceinline__ void vp_stream_n(const double* __restrict__ Vp, int64
 
 constexpr int PANELT_FIXED = 3 * 8 * 56 + 8 * (pt::RCH_MAX + 4) + 2 * pt::NW * 8 + 40 + 64 + 8 + 16 + 8;
 
+#ifdef ELM_QR_PROF
+// per-CTA timeline of the QR phase (tools/qr_prof.py): t0, t1, smid | kind << 16, j0 << 20 | subdomain
+__device__ unsigned long long g_qr_prof[1 << 20][4];
+__device__ unsigned g_qr_n;
+struct QrProf {
+    unsigned long long t0, aux;
+    int kind;
+    __device__ QrProf(int k, unsigned long long x) : aux(x), kind(k) {
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
+    __device__ ~QrProf() {
+        if (threadIdx.x != 0) return;
+        unsigned long long t1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        const unsigned i = atomicAdd(&g_qr_n, 1u);
+        if (i < (1u << 20)) {
+            g_qr_prof[i][0] = t0;
+            g_qr_prof[i][1] = t1;
+            g_qr_prof[i][2] = sm | ((unsigned long long)kind << 16);
+            g_qr_prof[i][3] = aux;
+        }
+    }
+};
+#define QR_PROF(k, x) QrProf qr_prof_(k, x)
+#else
+#define QR_PROF(k, x)
+#endif
 __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
+    QR_PROF(0, ((unsigned long long)a.j0 << 20) | (unsigned)(a.s_off + blockIdx.x));
     using namespace pt;
     extern __shared__ __align__(16) double sm[];
     __shared__ uint32_t s_tbase;
@@ -1555,6 +1585,7 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
                                                        const __grid_constant__ CUtensorMap tmK,
                                                        const double* __restrict__ Tbuf, int64_t ld, int j0, int nb,
                                                        int c0, int N, int s_off, EsynArgs es) {
+    QR_PROF(1, ((unsigned long long)j0 << 20) | (unsigned)(s_off + blockIdx.y));
     using namespace wyt;
     extern __shared__ uint8_t raw[];
     // 1024-byte alignment for the swizzled TMA boxes; pointer arithmetic on `raw` keeps the
@@ -3457,3 +3488,16 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
 }
 
 int panel_cl_stage(int64_t ld, int smem_optin) { return cl_stage(ld, smem_optin); }
+
+#ifdef ELM_QR_PROF
+extern "C" int elmddm_debug_qr_prof(void* host, int n) {  // n records (host: [n][4] u64); returns the count
+    unsigned cnt = 0;
+    cudaMemcpyFromSymbol(&cnt, g_qr_n, sizeof(unsigned));
+    if (host && n > 0) cudaMemcpyFromSymbol(host, g_qr_prof, sizeof(unsigned long long) * 4 * (size_t)n);
+    return (int)cnt;
+}
+extern "C" int elmddm_debug_qr_prof_reset() {
+    unsigned z = 0;
+    return (int)cudaMemcpyToSymbol(g_qr_n, &z, sizeof(unsigned));
+}
+#endif
