@@ -1323,7 +1323,7 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
         TQ(5);
     }
 #ifdef ELM_PANEL_PROF
-    if (tid == 0 && blockIdx.x == 0 && (a.j0 == 256 || a.j0 == 1024))
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 64) && (a.j0 == 0 || a.j0 == 256 || a.j0 == 512 || a.j0 == 1024))
         printf("PTPROF j0=%d total %lld load %lld wpass %lld z %lld upd %lld fact %lld wb %lld | red+sync %lld par %lld apply %lld\n", a.j0, clock64() - tq0,
                tq[0], tq[1], tq[2], tq[3], tq[4], tq[5], fq[0], fq[1], fq[2]);
 #endif
