@@ -327,6 +327,9 @@ struct CholArgs {
     // ranks: rep_base = 0 and the grid split among the replicas).
     int nrep, rep_base, ctas_per_rep;
     const CholRep* reps;   // [nrep]
+    double* Msave;         // non-null (one rank): every task that reads an assembled tile of M
+                           // (kinds 0 and 1) also stores it here -- the copy of M the
+                           // refinement step's residual needs, without a separate copy pass
 };
 
 __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
@@ -367,26 +370,49 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             for (int x = tid; x < TILE / 2; x += NT) dst2[x] = __ldcg(src + x);
         }
     };
-    int known = 0;        // (thread 0) every column < known is complete
     uint32_t gchunk = 0;  // chunk loads issued by this CTA so far (stage = gchunk % NSTAGE)
     uint32_t epi_uses = 0;
-    // thread 0: make sure L(I, k) and L(J, k) are final (column counters first, tile flags second)
 #ifdef ELM_CHOL_PROF
     unsigned long long pf_flag = 0, pf_data = 0;
 #endif
-    auto ensure = [&](const int4& e, int J) {
+    // warp 0 (all lanes, q warp-uniform): make sure L(I, k) and L(J, k) of update klist[q] are
+    // final.  Lane l checks the two tile flags of update q + l, one ballot gives the number of
+    // consecutive ready updates from q (kept in rdy): one L2 round trip per 32 updates instead
+    // of two per update on the thread that issues the chunk loads (the loads of the next chunk
+    // -- and so every warp -- waited for it)
+    int rdy = 0;
+    auto ensure_w = [&](int q, int qend, int J) {
+        if (q < rdy) return;
 #ifdef ELM_CHOL_PROF
         const uint64_t q0 = globaltimer();
-        struct Acc { unsigned long long& r; uint64_t q; __device__ ~Acc() { r += globaltimer() - q; } } acc_{pf_flag, q0};
 #endif
-        const int k = e.z;
-        if (!dist) {
-            if (k < known) return;
-            while (known < J && ld_acquire(a.colcnt + known) >= a.epoch * a.ntc[known]) ++known;
-            if (k < known) return;
+        const int lane = tid & 31;
+        uint64_t t0 = 0;
+        for (;;) {
+            int ok = 1;
+            if (q + lane < qend) {
+                const int4 e = a.klist[q + lane];
+                ok = (dist ? ld_acquire_sys(flags + e.x) : ld_acquire(flags + e.x)) >= fin_ep &&
+                     (dist ? ld_acquire_sys(flags + e.y) : ld_acquire(flags + e.y)) >= fin_ep;
+            }
+            const unsigned nr = ~__ballot_sync(0xffffffffu, ok);
+            const int nready = nr ? __ffs(nr) - 1 : 32;
+            if (nready > 0) {
+                rdy = q + nready;
+                break;
+            }
+            if (!t0) {
+                t0 = globaltimer();
+            } else if (globaltimer() - t0 > 10000000000ull) {  // as wait_flag: report, give up
+                if (lane == 0) elm_set_status(a.status, ELMDDM_ENUMERIC, -1 - a.klist[q].z);
+                rdy = qend;
+                break;
+            }
+            __nanosleep(64);
         }
-        wait_flag(flags + e.x, fin_ep, a.status, k, dist);
-        wait_flag(flags + e.y, fin_ep, a.status, k, dist);
+#ifdef ELM_CHOL_PROF
+        pf_flag += globaltimer() - q0;
+#endif
     };
     // static dealing: CTAs [0, crit_ctas) take the critical list round-robin, the others the
     // rest; dynamic dealing (a.next): every CTA takes the next task of the (list-scheduled) order
@@ -438,17 +464,25 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         {
             const double* Ct = tileptr(td.tid);
             FOR_FRAG acc[mt][nt][e] = -__ldcg(Ct + frag_r(mt) + frag_c(nt, e) * LP);
-        }
-        if (tid == 0)
-            for (int c = 0; c < NSTAGE - 1 && c < nch; ++c) {
-                if ((c & 1) == 0) ensure(a.klist[kb + (c >> 1)], J);
-                issue(c);
+            if (a.Msave && td.kind != 2) {
+                double* ms = a.Msave + (int64_t)td.tid * TILE;
+                FOR_FRAG __stcs(ms + frag_r(mt) + frag_c(nt, e) * LP, -acc[mt][nt][e]);
             }
+        }
+        rdy = kb;
+        if (tid < 32) {
+            for (int c = 0; c < NSTAGE - 1 && c < nch; ++c) {
+                if ((c & 1) == 0) ensure_w(kb + (c >> 1), ke, J);
+                if (tid == 0) issue(c);
+            }
+            __syncwarp();
+        }
         for (int c = 0; c < nch; ++c) {
-            if (tid == 0 && c + NSTAGE - 1 < nch) {
+            if (tid < 32 && c + NSTAGE - 1 < nch) {
                 const int cn = c + NSTAGE - 1;
-                if ((cn & 1) == 0) ensure(a.klist[kb + (cn >> 1)], J);
-                issue(cn);
+                if ((cn & 1) == 0) ensure_w(kb + (cn >> 1), ke, J);
+                if (tid == 0) issue(cn);
+                __syncwarp();
             }
             const uint32_t g = g0 + c;
 #ifdef ELM_CHOL_PROF
@@ -923,15 +957,16 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     k_perm_zero<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(yv, n);
     if (G > 0) k_perm_gather<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(g, c->d_fbase, q, G, yv);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (c->iface_refine) {
-        if ((e = cudaMemcpyAsync(Mcopy, Mband, sizeof(double) * c->sz.band_elems, cudaMemcpyDeviceToDevice, st)) !=
-                cudaSuccess ||
-            (e = cudaMemcpyAsync(gn, yv, sizeof(double) * n, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-            return e;
-    }
     // factorisation: one cooperative launch over the task list
     const DistState& ds = c->dist;
     const bool dist = ds.nrep > 1;
+    if (c->iface_refine) {
+        // (one rank: the factorisation kernel saves the tiles of M as it reads them)
+        if ((dist && (e = cudaMemcpyAsync(Mcopy, Mband, sizeof(double) * c->sz.band_elems, cudaMemcpyDeviceToDevice,
+                                          st)) != cudaSuccess) ||
+            (e = cudaMemcpyAsync(gn, yv, sizeof(double) * n, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+            return e;
+    }
     if (dist) {
         const int nrep = ds.nrep;
         const int epoch = ++c->dist.epoch;
@@ -949,7 +984,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         const CholRep& mine = ds.reps[ds.emulate ? 0 : ds.rank];
         CholArgs a{mine.Mb, mine.Ybuf, mine.Cbuf, mine.cready, c->d_tasks, (int)pl.tasks.size(), 0, 0, c->d_klist,
                    c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, c->d_status, ds.counter + (epoch & 1),
-                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps};
+                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr};
         void* args[] = {(void*)&a};
         {
             KTimer kt(c, ELMDDM_K_POTRF, st);
@@ -967,7 +1002,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
                    c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
-                   c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr};
+                   c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr, c->iface_refine ? Mcopy : nullptr};
         if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);

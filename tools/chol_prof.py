@@ -82,3 +82,23 @@ sel = sel[(sel[:, 1] > 0)]
 d = np.diff(sel, axis=1)
 print("diag-task stage medians (us):", {n: round(float(np.median(d[:, i])), 1) for i, n in enumerate(names)})
 print("diag-task stage means   (us):", {n: round(float(np.mean(d[:, i])), 1) for i, n in enumerate(names)})
+
+# ---- the top dissection node: when do its tiles' pre-aggregation tasks (kind 1) and the rest run?
+kind = tasks[:, 2].astype(int)
+nupd_t = tasks[:, 3]
+np.savez_compressed(os.path.join(ROOT, "gpurun_out", f"chol_prof_cfg{k}.npz"), tasks=tasks, st=st, en=en, fw=fw, dw=dw,
+                    ep=ep, cta=cta)
+top0 = nb - 64
+for kd in (0, 1, 2):
+    m = (J >= top0) & (kind == kd)
+    if m.sum():
+        nk = None
+        print(f"top-64 columns, kind {kd}: {m.sum()} tasks, {nupd_t[m].sum()} updates, start {np.percentile(st[m], [0, 50, 100]).round(0).tolist()} "
+              f"end {np.percentile(en[m], [0, 50, 100]).round(0).tolist()} us, CTA time {(en[m] - st[m]).sum() / 1e3:.0f} ms "
+              f"(flag waits {fw[m].sum() / 1e3:.0f} ms)")
+# CTA activity in the last 30% of the span: what were the CTAs doing?
+t_tail = 0.7 * span
+m = en > t_tail
+busy_tail = (np.minimum(en[m], span) - np.maximum(st[m], t_tail)).sum()
+print(f"last 30% of the span: CTA-time {busy_tail / 1e3:.0f} ms of {ncta * 0.3 * span / 1e3:.0f} ms available; "
+      f"tasks overlapping it by kind: {np.bincount(kind[m], minlength=3).tolist()}, by column >= top0: {(J[m] >= top0).sum()}")
