@@ -286,10 +286,12 @@ __device__ int potrf_inv_tile(double* A, double* Y, double* xbuf) {
 // X = C L^{-T} for C in As (layout [c * LP + r]), L = L(J,J) in Bs and Y = L(J,J)^{-1} in Ys:
 // X0 = C Y^T, then one refinement step X = X0 + (C - X0 L^T) Y^T (three 64^3 DMMA products; the
 // inverse alone would lose accuracy on ill-conditioned diagonal blocks).  As is clobbered.
-__device__ __forceinline__ void trsm_refined(double (&x)[4][2][2], double* As, const double* Bs, const double* Ys) {
+__device__ __forceinline__ void trsm_refined(double (&x)[4][2][2], double* As, const double* Bs, const double* Ys,
+                                             bool refine = true) {
     double r[4][2][2];
     FOR_FRAG x[mt][nt][e] = 0.0;
     mma_tile<NB>(x, As, Ys);                                    // X0 = C Y^T
+    if (!refine) return;
     FOR_FRAG r[mt][nt][e] = -As[frag_c(nt, e) * LP + frag_r(mt)];  // -C
     __syncthreads();
     FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = x[mt][nt][e];
@@ -330,6 +332,7 @@ struct CholArgs {
     double* Msave;         // non-null (one rank): every task that reads an assembled tile of M
                            // (kinds 0 and 1) also stores it here -- the copy of M the
                            // refinement step's residual needs, without a separate copy pass
+    int trsm_refine;       // 1: one refinement step in every tile solve X = C L(J,J)^{-T}
 };
 
 __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 mbar_wait(eb, epar);
                 DSTAMP(2);
                 double x[4][2][2];
-                trsm_refined(x, As, Bs, Ys);                      // L(J, klast)
+                trsm_refined(x, As, Bs, Ys, a.trsm_refine);       // L(J, klast)
                 DSTAMP(3);
                 __syncthreads();
                 FOR_FRAG As[frag_c(nt, e) * LP + frag_r(mt)] = x[mt][nt][e];
@@ -607,7 +610,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
             __syncthreads();  // C visible to every warp
             mbar_wait(eb, epar);
             double x0[4][2][2];
-            trsm_refined(x0, As, Bs, Ys);
+            trsm_refined(x0, As, Bs, Ys, a.trsm_refine);
             FOR_FRAG dst[frag_r(mt) + frag_c(nt, e) * LP] = x0[mt][nt][e];
             if (dist) {  // L(I,J) to the other replicas
                 __threadfence_block();
@@ -984,7 +987,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         const CholRep& mine = ds.reps[ds.emulate ? 0 : ds.rank];
         CholArgs a{mine.Mb, mine.Ybuf, mine.Cbuf, mine.cready, c->d_tasks, (int)pl.tasks.size(), 0, 0, c->d_klist,
                    c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, c->d_status, ds.counter + (epoch & 1),
-                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr};
+                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr, c->chol_trsm_refine};
         void* args[] = {(void*)&a};
         {
             KTimer kt(c, ELMDDM_K_POTRF, st);
@@ -1002,7 +1005,8 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
                    c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
-                   c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr, c->iface_refine ? Mcopy : nullptr};
+                   c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr, c->iface_refine ? Mcopy : nullptr,
+                   c->chol_trsm_refine};
         if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
