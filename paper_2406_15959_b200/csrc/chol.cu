@@ -670,30 +670,80 @@ __device__ __forceinline__ void load_tile_async(double* dst, const double* src) 
 __device__ unsigned long long g_trsv_prof[2][400000][4];
 #endif
 
+// The solution blocks are their own completion flags: the output vector is filled with an
+// all-ones NaN pattern before the launch (no arithmetic result has it: computed NaNs are the
+// canonical 0x7FF8...), a block's 64 values are written once with relaxed stores, and a consumer
+// reads them with relaxed loads until none is the pattern (8-byte accesses are single-copy
+// atomic).  One L2 round trip per dependency instead of a flag poll plus a data load, and no
+// fence + release on the producer's side of the chain.
+constexpr long long TRSV_EMPTY = -1LL;
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+
+// One dependency tile in registers: forward, thread (r, cg) holds T(r, 16 cg + u), u < 16, and lane
+// l holds x_j[16 cg + l % 16] (broadcast by shuffles); backward, lane l of warp w holds
+// T(l, 8 w + u), T(l + 32, 8 w + u), u < 8, and x_j[l], x_j[l + 32].  Loaded one tile ahead, so
+// the next tile's loads are in flight while this one is checked and consumed.
 template <int DIR>
-__device__ __forceinline__ void trsv_tile(const double* __restrict__ Mb, int2 d, const double* out, int r, int cg,
-                                          int lane, int w, double& sacc, double (&tacc)[8]) {
+struct TrsvTile {
+    double t[16];
+    double x0, x1;
+};
+template <int DIR>
+__device__ __forceinline__ void trsv_load(TrsvTile<DIR>& v, const double* __restrict__ Mb, int2 d, const double* out,
+                                          int r, int cg, int lane, int w) {
     const double* T = Mb + (int64_t)d.y * ELM_TS;
     const double* xj = out + (int64_t)d.x * NB;
-    if (DIR == 0) {  // s[r] += sum_c T(r, c) x_j[c]; element (r, c) at r + c LP
-        double tv[16], xv[16];
+    if (DIR == 0) {  // element (r, c) at r + c LP
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            tv[u] = __ldg(T + (cg * 16 + u) * LP + r);
-            xv[u] = __ldcg(xj + cg * 16 + u);
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) sacc += tv[u] * xv[u];
-    } else {         // s[c] += sum_r T(r, c) x_j[r]
-        const double x0 = __ldcg(xj + lane), x1 = __ldcg(xj + lane + 32);
-        double t0[8], t1[8];
+        for (int u = 0; u < 16; ++u) v.t[u] = __ldg(T + (cg * 16 + u) * LP + r);
+        v.x0 = ld_relaxed_f64(xj + cg * 16 + (lane & 15));
+    } else {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            t0[u] = __ldg(T + (8 * w + u) * LP + lane);
-            t1[u] = __ldg(T + (8 * w + u) * LP + lane + 32);
+            v.t[u] = __ldg(T + (8 * w + u) * LP + lane);
+            v.t[u + 8] = __ldg(T + (8 * w + u) * LP + lane + 32);
         }
+        v.x0 = ld_relaxed_f64(xj + lane);
+        v.x1 = ld_relaxed_f64(xj + lane + 32);
+    }
+}
+// wait until the x_j values of the tile are published (re-reading them), then accumulate:
+// s[r] += sum_c T(r, c) x_j[c] (forward) / s[c] += sum_r T(r, c) x_j[r] (backward)
+template <int DIR>
+__device__ __forceinline__ void trsv_use(TrsvTile<DIR>& v, int2 d, const double* out, int cg, int lane,
+                                         double& sacc, double (&tacc)[8], ElmStatus* status, int tag) {
+    uint64_t t0 = 0;
+    for (;;) {
+        const bool ok = __double_as_longlong(v.x0) != TRSV_EMPTY && (DIR == 0 || __double_as_longlong(v.x1) != TRSV_EMPTY);
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (!t0) {
+            t0 = globaltimer();
+        } else if (globaltimer() - t0 > 10000000000ull) {  // as wait_flag: report, give up
+            if (lane == 0) elm_set_status(status, ELMDDM_ENUMERIC, -1 - tag);
+            break;
+        }
+        __nanosleep(32);
+        const double* xj = out + (int64_t)d.x * NB;
+        if (DIR == 0) {
+            v.x0 = ld_relaxed_f64(xj + cg * 16 + (lane & 15));
+        } else {
+            v.x0 = ld_relaxed_f64(xj + lane);
+            v.x1 = ld_relaxed_f64(xj + lane + 32);
+        }
+    }
+    if (DIR == 0) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tacc[u] += t0[u] * x0 + t1[u] * x1;
+        for (int u = 0; u < 16; ++u) sacc += v.t[u] * __shfl_sync(0xffffffffu, v.x0, u);
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tacc[u] += v.t[u] * v.x0 + v.t[u + 8] * v.x1;
     }
 }
 
@@ -732,42 +782,24 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
         double sacc = 0.0, tacc[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) tacc[u] = 0.0;
-        for (int q = 0, ready = 0; q < nj;) {
-            if (q >= ready) {
-                // lane k: is dependency q + k published?  (the first unpublished one bounds the batch)
-#ifdef ELM_CHOL_PROF
-                const unsigned long long w0 = globaltimer();
-#endif
-                uint64_t t0 = 0;
-                for (;;) {
-                    int ok = 1;
-                    if (q + lane < nj) ok = ld_acquire(flags + dep[d0 + q + lane].x) >= epoch;
-                    const unsigned nr = ~__ballot_sync(0xffffffffu, ok);
-                    const int n = nr ? __ffs(nr) - 1 : 32;
-                    if (n > 0) {
-                        ready = q + n;
-                        break;
-                    }
-                    if (!t0) {
-                        t0 = globaltimer();
-                    } else if (globaltimer() - t0 > 10000000000ull) {  // as wait_flag: report, give up
-                        if (lane == 0) elm_set_status(status, ELMDDM_ENUMERIC, -1 - i);
-                        ready = nj;
-                        break;
-                    }
-                    __nanosleep(32);
+        if (nj > 0) {
+            TrsvTile<DIR> ta, tb;
+            int2 da = dep[d0], db;
+            trsv_load<DIR>(ta, Mb, da, out, r, cg, lane, w);
+            for (int q = 0;;) {
+                if (q + 1 < nj) {
+                    db = dep[d0 + q + 1];
+                    trsv_load<DIR>(tb, Mb, db, out, r, cg, lane, w);
                 }
-                __syncwarp();
-#ifdef ELM_CHOL_PROF
-                if (tid == 0) pfw += globaltimer() - w0;
-#endif
+                trsv_use<DIR>(ta, da, out, cg, lane, sacc, tacc, status, i);
+                if (++q >= nj) break;
+                if (q + 1 < nj) {
+                    da = dep[d0 + q + 1];
+                    trsv_load<DIR>(ta, Mb, da, out, r, cg, lane, w);
+                }
+                trsv_use<DIR>(tb, db, out, cg, lane, sacc, tacc, status, i);
+                if (++q >= nj) break;
             }
-            const int qe = ready < nj ? ready : nj;
-            for (; q + 1 < qe; q += 2) {
-                trsv_tile<DIR>(Mb, dep[d0 + q], out, r, cg, lane, w, sacc, tacc);
-                trsv_tile<DIR>(Mb, dep[d0 + q + 1], out, r, cg, lane, w, sacc, tacc);
-            }
-            if (q < qe) trsv_tile<DIR>(Mb, dep[d0 + q++], out, r, cg, lane, w, sacc, tacc);
         }
         // reduce the partial products in a fixed order
         if (DIR == 0) {
@@ -841,11 +873,8 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
                     }
                 }
             }
-            out[i0 + lane] = z0;
-            out[i0 + lane + 32] = z1;
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) st_release(flags + i, epoch);
+            st_relaxed_f64(out + i0 + lane, z0);  // (the values are the block's completion flag)
+            st_relaxed_f64(out + i0 + lane + 32, z1);
 #ifdef ELM_CHOL_PROF
             if (lane == 0 && it < 400000) {
                 unsigned long long* rp = g_trsv_prof[DIR][it];
@@ -1033,7 +1062,8 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
             void* args[] = {(void*)&Mband, (void*)&ntasks, (void*)&nblk_v, (void*)&dt, (void*)&tl, (void*)&rs,
                             (void*)&dl,    (void*)&rhs,    (void*)&out,    (void*)&flags, (void*)&pf, (void*)&pp,
                             (void*)&epoch, (void*)&stp};
-            cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the row counter
+            cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the task counter
+            if (e1 == cudaSuccess) e1 = cudaMemsetAsync(out, 0xFF, sizeof(double) * nblk * NB, st);  // TRSV_EMPTY
             if (e1 != cudaSuccess) return e1;
             KTimer kt(c, ELMDDM_K_TRSV, st);
             cudaError_t e2 = cudaLaunchCooperativeKernel(dir == 0 ? (void*)k_band_trsv<0> : (void*)k_band_trsv<1>, dim3(grid), dim3(256), args, TRSV_SMEM, st);
