@@ -575,6 +575,44 @@ cudaError_t run_interface_assemble_lattice(const elmddm_ctx* c, const double* Pb
     return cudaGetLastError();
 }
 
+// The F column of P_s = W_s [R12 | y] and the F row of S_s = [T_E | t_F]^T [T_E | t_F]
+// (kaug = ne + 1: left to the 64-tiled GEMMs, the lone F column costs a whole tile row / column of
+// CTAs, 20-33% of their work): per subdomain, warp-level dot products in a fixed order.
+//   P[i, F] = sum_k W_s^T[k, i] y[k]          i < na      (W_s^T = At[s], [k + i M])
+//   S[F, j] = sum_r T[r, j] t_F[r]            j <= F      (T = rows M.. of columns M.. of K_aug)
+namespace {
+__global__ void __launch_bounds__(256) k_fcol(const double* __restrict__ Kaug, int64_t ld, int64_t ncols, int M,
+                                              int kaug, int Kt, const double* __restrict__ At, int nat,
+                                              double* __restrict__ P, int64_t pld, int64_t pstride,
+                                              double* __restrict__ Sg, int64_t sld, int64_t sstride) {
+    const int64_t s = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int F = kaug - 1;
+    const double* K = Kaug + s * ld * ncols;
+    const double* y = K + (int64_t)(M + F) * ld;      // rows [0, M) of column M + F
+    const double* tF = y + M;                        // rows [M, M + Kt)
+    const double* W = At + s * (int64_t)M * nat;
+    for (int i = w; i < nat; i += 8) {
+        double v = 0.0;
+        for (int k = lane; k < M; k += 32) v += W[(int64_t)i * M + k] * y[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) P[s * pstride + i + (int64_t)F * pld] = v;
+    }
+    for (int j = w; j <= F; j += 8) {
+        const double* tj = K + M + (int64_t)(M + j) * ld;
+        double v = 0.0;
+        for (int r = lane; r < Kt; r += 32) v += tj[r] * tF[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {  // (both triangles: the consumers read diagonal 64-tiles in full)
+            Sg[s * sstride + F + (int64_t)j * sld] = v;
+            Sg[s * sstride + j + (int64_t)F * sld] = v;
+        }
+    }
+}
+}  // namespace
+
 cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, double* Pbuf, double* Sbuf,
                                  double* work, cudaStream_t st) {
     (void)work;
@@ -586,7 +624,8 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
     const int Kt = (int)(ld - M);
     const int64_t s0 = c->cfg.s_begin;
     const int64_t pstride = c->sz.pbuf_ld * kaug, sstride = c->sz.sbuf_ld * kaug;
-    GemmArgs gs{(int)kaug, (int)kaug, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
+    const int ke = (int)kaug - 1;  // the 64-tiled GEMMs cover the E columns; k_fcol the F column / row
+    GemmArgs gs{ke, ke, Kt, Kaug + M + (int64_t)M * ld, ld, ld * ncols, Kaug + M + (int64_t)M * ld, ld,
                 ld * ncols, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride, 1.0, 0.0, (int)S, 1 /* lower tiles only */};
     const bool side = !c->timing && c->schur_side;
     cudaStream_t sst = st;
@@ -611,9 +650,15 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // P_s = W_s [R12 | y]   (na x kaug)
-    GemmArgs gp{nat, (int)kaug, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
+    GemmArgs gp{nat, ke, M, At, M, (int64_t)M * nat, Kaug + (int64_t)M * ld, ld, ld * ncols,
                 Pbuf + s0 * pstride, c->sz.pbuf_ld, pstride, 1.0, 0.0, (int)S, 0};
     if ((e = gemm_launch(true, false, gp, st, c, ELMDDM_K_GEMM_SCHUR)) != cudaSuccess) return e;
+    {
+        KTimer kt(c, ELMDDM_K_GEMM_SCHUR, st);
+        k_fcol<<<(unsigned)S, 256, 0, st>>>(Kaug, ld, ncols, M, (int)kaug, Kt, At, nat, Pbuf + s0 * pstride,
+                                             c->sz.pbuf_ld, pstride, Sbuf + s0 * sstride, c->sz.sbuf_ld, sstride);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if (side) {
         cudaEventRecord(c->ev_join[0], sst);
         return cudaStreamWaitEvent(st, c->ev_join[0], 0);
