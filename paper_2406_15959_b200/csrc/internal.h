@@ -166,6 +166,10 @@ struct elmddm_ctx {
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    // k_panel_t on <= 2048 rows with 256 TMEM columns / 112 KB, so that two panel CTAs can share an SM
+    // (ELMDDM_PANEL_PAIR=0: 512 / 116 KB, one per SM).  Config 4 local_factor 195.0 -> 193.0 ms
+    // (8 groups); with 1 group (panels never beside trailing updates) 216.0 -> 199.1 ms
+    int panel_pair = 1;
     int panel_grid = 0;    // cooperative grid panel (automatic for very tall local problems; ELMDDM_PANEL_GRID=1)
     int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)
     int implicit_e = 1;  // E_Gamma tiles never written by the assembly, synthesised by the first

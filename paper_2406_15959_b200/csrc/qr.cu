@@ -38,6 +38,7 @@ struct PanelArgs {
     int blk;       // base block index inside the panel
     int s_off;     // first local subdomain of this launch (subdomain groups on separate streams)
     int ring;      // doubles of the V_prev ring (k_panel_block)
+    int tcols;     // k_panel_t: TMEM columns to allocate (0: 512; 256 lets two panel CTAs share an SM)
 };
 
 // block-wide deterministic sum of NV values per thread; result broadcast in tot[0..NV)
@@ -921,6 +922,7 @@ struct QrProf {
 __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
     QR_PROF(0, ((unsigned long long)a.j0 << 20) | (unsigned)(a.s_off + blockIdx.x));
     using namespace pt;
+    const uint32_t tcols = a.tcols > 0 ? (uint32_t)a.tcols : 512u;
     extern __shared__ __align__(16) double sm[];
     __shared__ uint32_t s_tbase;
     const int sl = a.s_off + blockIdx.x;
@@ -949,8 +951,8 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
 
     // TMEM: the whole 512 columns (one panel CTA per SM by construction)
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&s_tbase)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&s_tbase)), "r"(tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1355,7 +1357,7 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(tcols));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -3227,7 +3229,10 @@ int panelp_ring(int64_t R, int smem_optin) {
     return (int)std::max<int64_t>(r, RED_ELEMS);
 }
 size_t panelp_smem_bytes(int64_t R, int ring) { return (size_t)(8 * (R + 4) + PANELP_FIXED + ring) * 8; }
-int panelt_ring() { return (pt::SMEM / 8 - PANELT_FIXED) & ~(2 * VNS - 1); }
+int panelt_ring(int smem = pt::SMEM) { return (smem / 8 - PANELT_FIXED) & ~(2 * VNS - 1); }
+// panels of <= 2048 rows allocate 256 TMEM columns and 112 KB of shared memory, so that two panel
+// CTAs can share an SM (ELMDDM_PANEL_PAIR=0: the whole TMEM and 116 KB, one per SM)
+constexpr int PT_SMEM_PAIR = 112 * 1024;
 
 }  // namespace
 
@@ -3430,8 +3435,10 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
                 {
                     KTimer kt(c, ELMDDM_K_PANEL, pstr[g]);
                     PanelArgs pp = pa;
-                    pp.ring = panelt_ring();
-                    k_panel_t<<<(unsigned)(g1 - g0), pt::NT, pt::SMEM, pstr[g]>>>(pp, nb);
+                    const bool pair = c->panel_pair && (ld + 127) / 128 * 16 <= 256;
+                    pp.ring = panelt_ring(pair ? PT_SMEM_PAIR : pt::SMEM);
+                    pp.tcols = pair ? 256 : 512;
+                    k_panel_t<<<(unsigned)(g1 - g0), pt::NT, pair ? PT_SMEM_PAIR : pt::SMEM, pstr[g]>>>(pp, nb);
                     if ((e = cudaGetLastError()) != cudaSuccess) return e;
                 }
                 if (prio) {
