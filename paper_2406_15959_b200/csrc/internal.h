@@ -170,6 +170,10 @@ struct elmddm_ctx {
     // (ELMDDM_PANEL_PAIR=0: 512 / 116 KB, one per SM).  Config 4 local_factor 195.0 -> 193.0 ms
     // (8 groups); with 1 group (panels never beside trailing updates) 216.0 -> 199.1 ms
     int panel_pair = 1;
+    // Schur TRSM with the flux-row tiles of a subdomain as one cluster, R11 chunks TMA-multicast
+    // (ELMDDM_TRSM_CLUSTER=1; bit-identical, but config 4 TRSM 10.6 -> 12.5 ms: the per-chunk
+    // cluster-wide empty handshake makes the slowest CTA gate all four)
+    int trsm_cluster = 0;
     int panel_grid = 0;    // cooperative grid panel (automatic for very tall local problems; ELMDDM_PANEL_GRID=1)
     int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)
     int implicit_e = 1;  // E_Gamma tiles never written by the assembly, synthesised by the first

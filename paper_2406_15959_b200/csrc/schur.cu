@@ -221,6 +221,37 @@ constexpr int SMEM_BODY = (2 * STAGE > 2 * 64 * XP + 64 ? 2 * STAGE : 2 * 64 * X
 constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;  // + [2] full, [2] empty mbarriers (<= 64 B)
 }  // namespace trw
 
+// Cluster version (launched with a cluster of gridDim.x CTAs, all flux-row tiles of one
+// subdomain; nc = 1 without a cluster): the 4 (or nc) CTAs of a subdomain read the SAME chunks of
+// R11, so the cluster's rank-0 CTA loads each R chunk once and multicasts it into every CTA's
+// stage (cp.async.bulk.tensor ... .multicast::cluster; each CTA's full barrier expects the R and
+// its own X bytes); before refilling a stage it waits on its cluster-wide empty barrier, which
+// every warp of every CTA arrives on (remote mbarrier arrive) when done with the stage.  The
+// diagonal solve reuses the stages as scratch, so the CTAs meet at a cluster barrier after every
+// block.  Per-CTA arithmetic and order are unchanged (bit-identical to nc = 1).
+__device__ __forceinline__ uint32_t trw_mapa(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void trw_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void trw_mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(elmtma::su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void trw_tma_load_mc(double* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                                uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
+        ::"r"(elmtma::su32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(elmtma::su32(bar)), "h"(mask) : "memory");
+}
+
 __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ CUtensorMap tmR,
                                                        const __grid_constant__ CUtensorMap tmA,
                                                        const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
@@ -238,14 +269,25 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
     const int s = blockIdx.y, n0 = blockIdx.x * 64;
     const double* R = Kaug + (int64_t)s * ld * ncols;
     double* A = At + (int64_t)s * M * nat;
+    uint32_t nc, crank;
+    asm("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(nc));
+    asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    const bool lead = crank == 0;
+    const uint16_t mask = (uint16_t)((1u << nc) - 1u);
+    // bar[0..1] full (local expect), bar[2..3] empty (this CTA's warps), bar[4..5] cluster empty
+    // (the leader's: every warp of every CTA)
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        mbar_init(&bar[2], NT / 32);  // stage 0 / 1 released by every warp
+        mbar_init(&bar[2], NT / 32);
         mbar_init(&bar[3], NT / 32);
+        mbar_init(&bar[4], (int)(nc * (NT / 32)));
+        mbar_init(&bar[5], (int)(nc * (NT / 32)));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    if (nc > 1) trw_cluster_sync();  // barriers initialised cluster-wide before any remote arrive
+    const uint32_t cempty0 = trw_mapa(su32(&bar[4]), 0);  // the leader's cluster empty barriers (8 B apart)
     uint32_t gch = 0;  // chunks issued so far (stage = gch & 1, parity = (gch >> 1) & 1)
     const int nbk = (M + 63) / 64;
     for (int i = 0; i < nbk; ++i) {
@@ -261,14 +303,20 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
                     acc[mt][nt][e] = (c < bi && n0 + n < nat) ? -A[(int64_t)(n0 + n) * M + i0 + c] : 0.0;
                 }
         const int nch = 2 * i;  // k-blocks 0..i-1, two 32-row chunks each
-        auto issue = [&](int ch, uint32_t g) {
+        auto issue = [&](int ch, uint32_t g) {  // thread 0
             double* d = stg + (g & 1) * STAGE;
             const int r0 = 32 * ch;  // row of R11 / neuron index of X
-            if (g >= 2) mbar_wait(&bar[2 + (g & 1)], ((g >> 1) - 1) & 1);  // previous chunk of the stage consumed
+            if (g >= 2) mbar_wait(&bar[2 + (g & 1)], ((g >> 1) - 1) & 1);  // this CTA consumed the stage
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            mbar_expect(&bar[g & 1], 4 * BOX * 8);
-            tma_load(d, &tmR, r0, i0, s, &bar[g & 1]);
-            tma_load(d + BOX, &tmR, r0 + 16, i0, s, &bar[g & 1]);
+            mbar_expect(&bar[g & 1], 4 * BOX * 8);  // R (multicast or own) + X (own)
+            if (nc == 1) {
+                tma_load(d, &tmR, r0, i0, s, &bar[g & 1]);
+                tma_load(d + BOX, &tmR, r0 + 16, i0, s, &bar[g & 1]);
+            } else if (lead) {
+                if (g >= 2) trw_mbar_wait_cluster(&bar[4 + (g & 1)], ((g >> 1) - 1) & 1);  // every CTA did
+                trw_tma_load_mc(d, &tmR, r0, i0, s, &bar[g & 1], mask);
+                trw_tma_load_mc(d + BOX, &tmR, r0 + 16, i0, s, &bar[g & 1], mask);
+            }
             tma_load(d + 2 * BOX, &tmA, r0, n0, s, &bar[g & 1]);
             tma_load(d + 3 * BOX, &tmA, r0 + 16, n0, s, &bar[g & 1]);
         };
@@ -293,7 +341,12 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
                     for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar[2 + (g & 1)]);  // stage (g & 1) may be refilled
+            if (lane == 0) {
+                mbar_arrive(&bar[2 + (g & 1)]);  // stage (g & 1) may be refilled (own X)
+                if (nc > 1)                       // ... and, once every CTA is done, by the multicast R
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
+                                     cempty0 + 8u * (g & 1)) : "memory");
+            }
         }
         gch += nch;
         __syncthreads();  // every warp is done with the stages: the diagonal solve reuses them
@@ -340,7 +393,11 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
         // X_i is read back through the async proxy (TMA) by the later blocks of this CTA
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
         __syncthreads();
+        // no CTA of the cluster may receive the next block's multicast chunks while another
+        // still uses its stages as diagonal-solve scratch
+        if (nc > 1) trw_cluster_sync();
     }
+    if (nc > 1) trw_cluster_sync();  // no CTA exits while a multicast into it may be in flight
 }
 
 
@@ -645,8 +702,28 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         if ((e = cudaFuncSetAttribute(k_trsm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, trw::SMEM)) != cudaSuccess)
             return e;
         dim3 g((nat + 63) / 64, (unsigned)S);
+        // the flux-row tiles of a subdomain form one cluster (R11 chunks multicast), up to 8
+        const int ncl = (c->trsm_cluster && g.x >= 2 && g.x <= 8) ? (int)g.x : 1;
         KTimer kt(c, ELMDDM_K_TRSM, st);
-        k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
+        if (ncl > 1) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = g;
+            cfg.blockDim = dim3(trw::NT);
+            cfg.dynamicSmemBytes = trw::SMEM;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)ncl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if ((e = cudaLaunchKernelEx(&cfg, k_trsm_w, tmR, tmA, (const double*)Kaug, (int64_t)ld, (int64_t)ncols, At, M,
+                                        nat)) != cudaSuccess)
+                return e;
+        } else {
+            k_trsm_w<<<g, trw::NT, trw::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
+        }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // P_s = W_s [R12 | y]   (na x kaug)

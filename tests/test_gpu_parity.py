@@ -122,6 +122,25 @@ def test_implicit_e_columns_bit_identical(cfgkw, monkeypatch):
     assert torch.equal(K1, K0) and torch.equal(t1, t0)
 
 
+@pytest.mark.parametrize("cfgkw", [dict(k=2), dict(P=3, M=96, p=9, q=80, problem=2),
+                                   dict(P=2, M=64, p=31, q=31, problem=4, layout=1)])
+def test_trsm_cluster_bit_identical(cfgkw, monkeypatch):
+    """Schur TRSM with the flux-row tiles of a subdomain as one thread-block cluster and the R11
+    chunks multicast by TMA (ELMDDM_TRSM_CLUSTER=1; clusters of 4, 5 and 3 CTAs here): the per-CTA arithmetic
+    and order are unchanged, so P_s and S_s are bit-identical to the unclustered launch."""
+    import torch
+
+    c = WL.config(cfgkw["k"]) if "k" in cfgkw else small(**cfgkw)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("ELMDDM_TRSM_CLUSTER", flag)
+        ctx, buf, _ = run_gpu(c, upto="schur")
+        torch.cuda.synchronize()
+        outs.append((buf["Pbuf"].clone(), buf["Sbuf"].clone(), buf["At"].clone()))
+    (P1, S1, A1), (P0, S0, A0) = outs
+    assert torch.equal(A1, A0) and torch.equal(P1, P0) and torch.equal(S1, S0)
+
+
 @pytest.mark.parametrize("k", [0, 1, 2])
 def test_qr_backward_stable(k):
     """Q^T [K|E|F] = R_aug: the Gram identity A^T A = R_aug^T R_aug holds to rounding, and the
