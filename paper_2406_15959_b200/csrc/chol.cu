@@ -333,6 +333,7 @@ struct CholArgs {
                            // (kinds 0 and 1) also stores it here -- the copy of M the
                            // refinement step's residual needs, without a separate copy pass
     int trsm_refine;       // 1: one refinement step in every tile solve X = C L(J,J)^{-T}
+    const unsigned char* tile_m;  // [ntiles] 1: tile of M (saved to Msave), 0: fill (zero in M)
 };
 
 __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
         {
             const double* Ct = tileptr(td.tid);
             FOR_FRAG acc[mt][nt][e] = -__ldcg(Ct + frag_r(mt) + frag_c(nt, e) * LP);
-            if (a.Msave && td.kind != 2) {
+            if (a.Msave && td.kind != 2 && a.tile_m[td.tid]) {  // (fill tiles: never read by the SpMV)
                 double* ms = a.Msave + (int64_t)td.tid * TILE;
                 FOR_FRAG __stcs(ms + frag_r(mt) + frag_c(nt, e) * LP, -acc[mt][nt][e]);
             }
@@ -1016,7 +1017,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         const CholRep& mine = ds.reps[ds.emulate ? 0 : ds.rank];
         CholArgs a{mine.Mb, mine.Ybuf, mine.Cbuf, mine.cready, c->d_tasks, (int)pl.tasks.size(), 0, 0, c->d_klist,
                    c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, c->d_status, ds.counter + (epoch & 1),
-                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr, c->chol_trsm_refine};
+                   nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr, c->chol_trsm_refine, c->d_tile_m};
         void* args[] = {(void*)&a};
         {
             KTimer kt(c, ELMDDM_K_POTRF, st);
@@ -1035,7 +1036,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
                    c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
                    c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr, c->iface_refine ? Mcopy : nullptr,
-                   c->chol_trsm_refine};
+                   c->chol_trsm_refine, c->d_tile_m};
         if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);

@@ -433,7 +433,10 @@ elmddm_status finish_tables(elmddm_ctx* c, const std::vector<int>& qsrc, const s
         (e = upload(&c->d_klist, pl.klist)) != cudaSuccess || (e = upload(&c->d_diag_tid, pl.diag_tid)) != cudaSuccess ||
         (e = upload(&c->d_fwd_ptr, pl.fwd_ptr)) != cudaSuccess || (e = upload(&c->d_fwd, pl.fwd)) != cudaSuccess ||
         (e = upload(&c->d_bwd_ptr, pl.bwd_ptr)) != cudaSuccess || (e = upload(&c->d_bwd, pl.bwd)) != cudaSuccess ||
-        (e = upload(&c->d_ntc, pl.ntc)) != cudaSuccess)
+        (e = upload(&c->d_ntc, pl.ntc)) != cudaSuccess || (e = upload(&c->d_mrow_ptr, pl.mrow_ptr)) != cudaSuccess ||
+        (e = upload(&c->d_tile_m, pl.tile_m)) != cudaSuccess ||
+        (e = upload(&c->d_mrow, pl.mrow)) != cudaSuccess || (e = upload(&c->d_mcol_ptr, pl.mcol_ptr)) != cudaSuccess ||
+        (e = upload(&c->d_mcol, pl.mcol)) != cudaSuccess)
         return cuda_fail(c, e, "upload");
     {
         // triangular-solve task lists (heavy block rows split into chunks, plan.cu)
@@ -633,6 +636,11 @@ void elmddm_destroy(elmddm_ctx* c) {
     }
     cudaFree(c->d_pflags);
     cudaFree(c->d_ppart);
+    cudaFree(c->d_tile_m);
+    cudaFree(c->d_mrow_ptr);
+    cudaFree(c->d_mrow);
+    cudaFree(c->d_mcol_ptr);
+    cudaFree(c->d_mcol);
     cudaFree(c->d_fwd_ptr);
     cudaFree(c->d_fwd);
     cudaFree(c->d_bwd_ptr);

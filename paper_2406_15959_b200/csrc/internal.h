@@ -99,6 +99,12 @@ struct CholPlan {
     std::vector<TaskDesc> tasks;      // critical band first, then the rest; each column by column
     std::vector<int4> klist;
     std::vector<int2> fwd, bwd;
+    // the tiles of M itself (before fill): row lists (J, tile (I, J)), J < I, and column lists
+    // (J, tile (J, I)), J > I, descending -- the packed-tile SpMV of M (refinement residual, CG)
+    // reads only these (the fill tiles of the factorisation are zero in M)
+    std::vector<int> mrow_ptr, mcol_ptr;
+    std::vector<unsigned char> tile_m;  // [ntiles] 1: a tile of M itself, 0: fill
+    std::vector<int2> mrow, mcol;
 };
 int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, int>>& face_pairs, int ordering,
                         int crit_band, CholPlan& pl, int split_min = 0);
@@ -219,6 +225,11 @@ struct elmddm_ctx {
     int2* d_fwd = nullptr;           // (j, tile (i, j)), ascending j
     int* d_bwd_ptr = nullptr;        // [nblk + 1] CSR of the backward-solve dependencies
     int2* d_bwd = nullptr;           // (j, tile (j, i)), descending j
+    unsigned char* d_tile_m = nullptr;  // [ntiles] CholPlan::tile_m
+    int* d_mrow_ptr = nullptr;       // CSR of M's own off-diagonal tiles (CholPlan::mrow / mcol)
+    int2* d_mrow = nullptr;
+    int* d_mcol_ptr = nullptr;
+    int2* d_mcol = nullptr;
     int* d_cflags = nullptr;         // [ntiles] per-tile completion flags of the factorisation
     int* d_colcnt = nullptr;         // [nblk] finished tiles of column J (summed over factorisations)
     int* d_ntc = nullptr;            // [nblk] tiles of column J

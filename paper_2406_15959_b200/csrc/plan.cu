@@ -186,6 +186,12 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
         for (int I = a0; I <= a1; ++I)
             for (int J = b0; J <= b1; ++J) cols[std::min(I, J)].push_back(std::max(I, J));
     }
+    std::vector<std::vector<int>> mcols(nb);  // M's own tile structure (lower), kept for the SpMV lists
+    for (int J = 0; J < nb; ++J) {
+        mcols[J] = cols[J];
+        std::sort(mcols[J].begin(), mcols[J].end());
+        mcols[J].erase(std::unique(mcols[J].begin(), mcols[J].end()), mcols[J].end());
+    }
     // 3. symbolic factorisation (children merge into their elimination-tree parent)
     for (int J = 0; J < nb; ++J) {
         auto& c = cols[J];
@@ -206,6 +212,32 @@ int64_t build_chol_plan(int P, int q, int F, const std::vector<std::pair<int, in
             rows[I].push_back(J);  // ascending J
         }
     pl.ntiles = tid;
+    {
+        std::vector<std::vector<int2>> mr(nb), mc(nb);
+        for (int J = 0; J < nb; ++J)
+            for (int I : mcols[J])
+                if (I > J) {
+                    const int t = pl.tile_map[(size_t)I * nb + J];
+                    mr[I].push_back({J, t});
+                    mc[J].push_back({I, t});
+                }
+        pl.tile_m.assign(tid, 0);
+        for (int J = 0; J < nb; ++J)
+            for (int I : mcols[J]) pl.tile_m[pl.tile_map[(size_t)I * nb + J]] = 1;
+        for (int J = 0; J < nb; ++J) pl.tile_m[pl.tile_map[(size_t)J * nb + J]] = 1;  // (padding diagonals)
+        pl.mrow_ptr.assign(nb + 1, 0);
+        pl.mcol_ptr.assign(nb + 1, 0);
+        pl.mrow.clear();
+        pl.mcol.clear();
+        for (int I = 0; I < nb; ++I) {
+            std::sort(mr[I].begin(), mr[I].end(), [](const int2& x, const int2& y) { return x.x < y.x; });
+            std::sort(mc[I].begin(), mc[I].end(), [](const int2& x, const int2& y) { return x.x > y.x; });
+            pl.mrow.insert(pl.mrow.end(), mr[I].begin(), mr[I].end());
+            pl.mcol.insert(pl.mcol.end(), mc[I].begin(), mc[I].end());
+            pl.mrow_ptr[I + 1] = (int)pl.mrow.size();
+            pl.mcol_ptr[I + 1] = (int)pl.mcol.size();
+        }
+    }
     pl.diag_tid.assign(nb, 0);
     for (int J = 0; J < nb; ++J) pl.diag_tid[J] = pl.tile_map[(size_t)J * nb + J];
     // 5. tasks and k-lists
