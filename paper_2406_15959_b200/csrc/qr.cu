@@ -1602,8 +1602,12 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     const int R = (int)(ld - j0), nch = R / CH;
     const double* T = Tbuf + (int64_t)sl * ELM_NB * ELM_NB;
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
+        mbar_init(&bar[0], 1);  // [0..1] stage full (TMA)
         mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], NT / 32);  // [2..3] phase 1: every warp done with the stage
+        mbar_init(&bar[3], NT / 32);
+        mbar_init(&bar[4], NT / 32);  // [4..5] phase 3: every warp's C part written back into the stage
+        mbar_init(&bar[5], NT / 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -1669,10 +1673,21 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    // Stage hand-off without CTA-wide barriers (except for synthesised E tiles): a warp arrives on
+    // the stage's mbarrier when done with it, and only thread 0 waits there before refilling the
+    // stage (phase 1) or before storing the written-back C chunk by TMA (phase 3).
+    const bool mb = !syn;
+    uint32_t epar = 0u, dpar = 0u;  // (thread 0) parity bits (bit s: stage s) of bar[2..3], bar[4..5]
     if (tid == 0 && n1 > 0) issue(cb, 0);
     for (int i1 = 0; i1 < n1; ++i1) {
         const int st = i1 & 1, c = cb + i1;
-        if (tid == 0 && i1 + 1 < n1) issue(c + 1, st ^ 1);
+        if (tid == 0 && i1 + 1 < n1) {
+            if (mb && i1 >= 1) {  // every warp is done with chunk i1 - 1 in stage st ^ 1
+                mbar_wait(&bar[2 + (st ^ 1)], (epar >> (st ^ 1)) & 1u);
+                epar ^= 1u << (st ^ 1);
+            }
+            issue(c + 1, st ^ 1);
+        }
         wait_stage(st);
         const double* Vs = stg + st * STAGE;
         const double* Cs = Vs + 2 * BOX;
@@ -1694,8 +1709,14 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
         }
-        __syncthreads();
+        if (mb) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[2 + st]);
+        } else {
+            __syncthreads();
+        }
     }
+    __syncthreads();  // every warp is done with the stages: phase 2 stages T there
     // ---------------- phase 2: Z = -T^T W ----------------
     double* Ts = stg;  // [64 i][PADZ]
 #pragma unroll
@@ -1782,7 +1803,8 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) dmma(a3[mt][nt][0], a3[mt][nt][1], af[mt], bf[nt]);
         }
-        __syncthreads();  // all reads of this C stage done
+        // (a warp writes back exactly the C part it read: no barrier before the write-back)
+        if (!mb) __syncthreads();  // all reads of this C stage done
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1793,7 +1815,16 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
                     Cs[sw(r, n)] = a3[mt][nt][e];
                 }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncthreads();
+        if (mb) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[4 + st]);
+            if (tid == 0) {  // every warp's part written (and its reads of the stage done)
+                mbar_wait(&bar[4 + st], (dpar >> st) & 1u);
+                dpar ^= 1u << st;
+            }
+        } else {
+            __syncthreads();
+        }
         if (tid == 0) {
             tma_store(&tmK, j0 + c * CH, ncol0, sl, Cs);
             tma_store(&tmK, j0 + c * CH + 16, ncol0, sl, Cs + BOX);
