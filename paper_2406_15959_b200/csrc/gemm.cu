@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "tma.cuh"
 
 namespace {
 
@@ -155,6 +156,102 @@ __global__ void __launch_bounds__(NT, 2) k_gemm(GemmArgs g) {
     }
 }
 
+// TMA version for C = alpha A^T B + beta C with both operands k-contiguous (A[k + i lda],
+// B[k + n ldb]: every GEMM of the path): 64 x 64 output tile, K in chunks of 32 rows staged by
+// cp.async.bulk.tensor (two 16 x 64 boxes per operand, 128B swizzle, out-of-range rows / columns
+// read as zero) through a 3-stage ring; a warp arrives on the stage's mbarrier when done with it
+// and only the issuing thread waits there -- no CTA-wide barrier per chunk.  Same warp tiling
+// and DMMA order per output element as k_gemm<1, 0>.
+namespace gt {
+constexpr int NST = 3;
+constexpr int STAGE = 4 * elmtma::BOX;
+constexpr int SMEM = NST * STAGE * 8 + 64 + 1024;
+}  // namespace gt
+
+__global__ void __launch_bounds__(NT, 2) k_gemm_tn_tma(const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+    using namespace elmtma;
+    using namespace gt;
+    extern __shared__ uint8_t raw[];
+    double* base = reinterpret_cast<double*>(raw + ((1024u - (su32(raw) & 1023u)) & 1023u));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + NST * STAGE);  // [NST] full, [NST] empty
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, bz = blockIdx.z;
+    if (g.lower_only && m0 + BM <= n0) return;
+    const int mv = min(BM, g.M - m0), nv = min(BN, g.N - n0);
+    const int nk = (g.K + 31) / 32;
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&bar[s], 1);
+            mbar_init(&bar[NST + s], NT / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int kc) {  // thread 0
+        const int s = kc % NST;
+        double* d = base + s * STAGE;
+        if (kc >= NST) mbar_wait(&bar[NST + s], ((kc / NST) - 1) & 1);  // every warp done with its last use
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect(&bar[s], 4 * BOX * 8);
+        const int k0 = 32 * kc;
+        tma_load(d, &tmA, k0, m0, bz, &bar[s]);
+        tma_load(d + BOX, &tmA, k0 + 16, m0, bz, &bar[s]);
+        tma_load(d + 2 * BOX, &tmB, k0, n0, bz, &bar[s]);
+        tma_load(d + 3 * BOX, &tmB, k0 + 16, n0, bz, &bar[s]);
+    };
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    if (tid == 0)
+        for (int kc = 0; kc < NST - 1 && kc < nk; ++kc) issue(kc);
+    for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % NST;
+        if (tid == 0 && kc + NST - 1 < nk) issue(kc + NST - 1);
+        mbar_wait(&bar[s], (kc / NST) & 1);
+        const double* As = base + s * STAGE;
+        const double* Bs = As + 2 * BOX;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int kk = ks * 4 + (lane & 3);
+            double af[4], bf[2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = As[sw(kk, wm * 32 + mt * 8 + (lane >> 2))];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) bf[nt] = Bs[sw(kk, wn * 16 + nt * 8 + (lane >> 2))];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+                    if (wm * 32 + mt * 8 < mv && wn * 16 + nt * 8 < nv)
+                        dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[NST + s]);
+    }
+    double* C = g.C + (int64_t)bz * g.sC;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        const int i = wm * 32 + mt * 8 + (lane >> 2);
+        if (i >= mv) continue;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                if (j >= nv) continue;
+                double* cp = C + (m0 + i) + (int64_t)(n0 + j) * g.ldc;
+                double v = g.alpha * acc[mt][nt][e];
+                if (g.beta != 0.0) v += g.beta * *cp;
+                *cp = v;
+            }
+        }
+    }
+}
+
 // C = beta C for an empty contraction (K = 0), column-major, batched; 8 columns per CTA.
 __global__ void k_scale_c(int M, int N, double* C, int64_t ldc, int64_t sC, double beta, int lower_only) {
     double* Cb = C + (int64_t)blockIdx.y * sC;
@@ -187,6 +284,18 @@ cudaError_t gemm_launch(bool transA, bool transB, const GemmArgs& g, cudaStream_
         dim3 grid((g.N + 7) / 8, g.batch);
         k_scale_c<<<grid, 256, 0, st>>>(g.M, g.N, g.C, g.ldc, g.sC, g.beta, g.lower_only);
         return cudaGetLastError();
+    }
+    if (transA && !transB && c->gemm_tma) {
+        CUtensorMap tA, tB;
+        if (elm_encode_tmap_s(&tA, g.A, g.K, g.M, g.batch, g.lda, g.sA) &&
+            elm_encode_tmap_s(&tB, g.B, g.K, g.N, g.batch, g.ldb, g.sB)) {
+            cudaError_t e = cudaFuncSetAttribute(k_gemm_tn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, gt::SMEM);
+            if (e != cudaSuccess) return e;
+            dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
+            KTimer kt(c, cls, st);
+            k_gemm_tn_tma<<<grid, NT, gt::SMEM, st>>>(tA, tB, g);
+            return cudaGetLastError();
+        }
     }
     if (transA) return transB ? launch<true, true>(g, st, c, cls) : launch<true, false>(g, st, c, cls);
     return transB ? launch<false, true>(g, st, c, cls) : launch<false, false>(g, st, c, cls);

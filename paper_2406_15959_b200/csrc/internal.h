@@ -180,6 +180,7 @@ struct elmddm_ctx {
     // (ELMDDM_TRSM_CLUSTER=1; bit-identical, but config 4 TRSM 10.6 -> 12.5 ms: the per-chunk
     // cluster-wide empty handshake makes the slowest CTA gate all four)
     int trsm_cluster = 0;
+    int gemm_tma = 1;      // batched A^T B GEMMs through the TMA / mbarrier kernel (ELMDDM_GEMM_TMA=0: cp.async)
     int panel_grid = 0;    // cooperative grid panel (automatic for very tall local problems; ELMDDM_PANEL_GRID=1)
     int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)
     int implicit_e = 1;  // E_Gamma tiles never written by the assembly, synthesised by the first

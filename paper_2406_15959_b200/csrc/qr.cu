@@ -3273,6 +3273,27 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 // 3-D fp64 tensor map {d0 rows (contiguous), d1 columns (stride d0*8 B), d2 batches (stride s2 elems)},
 // box 16 x 64 x 1, 128B swizzle, out-of-bounds elements read as zero.
+bool elm_encode_tmap_s(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s1,
+                       int64_t s2) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (d0 < 1 || d1 < 1 || d2 < 1 || (s1 * 8) % 16 != 0 || (s2 * 8) % 16 != 0 || ((uintptr_t)base & 15) != 0) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    cuuint64_t strides[2] = {(cuuint64_t)(s1 * 8), (cuuint64_t)(s2 * 8)};
+    cuuint32_t box[3] = {16, 64, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, ELM_SWIZZLE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool elm_encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s2) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;

@@ -53,3 +53,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // 3-D fp64 tensor map {d0 (contiguous), d1 (stride d0*8 B), d2 (stride s2 elements)}, box 16 x 64 x 1,
 // 128B_ATOM_32B swizzle, out-of-bounds elements read as zero (qr.cu).
 bool elm_encode_tmap(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s2);
+// the same with an explicit dim-1 stride s1 (elements; a d0-row window of a taller array); false if
+// TMA's 16-byte alignment rules are not met (the caller falls back to the cp.async kernels)
+bool elm_encode_tmap_s(CUtensorMap* tm, const double* base, int64_t d0, int64_t d1, int64_t d2, int64_t s1,
+                       int64_t s2);
