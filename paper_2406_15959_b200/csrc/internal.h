@@ -180,6 +180,10 @@ struct elmddm_ctx {
     // (ELMDDM_TRSM_CLUSTER=1; bit-identical, but config 4 TRSM 10.6 -> 12.5 ms: the per-chunk
     // cluster-wide empty handshake makes the slowest CTA gate all four)
     int trsm_cluster = 0;
+    // Schur TRSM with 128 flux rows per CTA (ELMDDM_TRSM_WIDE=1; bit-identical, halves the R11
+    // traffic, but config 4 TRSM 10.7 -> 11.4 ms: one 512-thread CTA per SM has no second CTA to
+    // fill the pipe during its diagonal solves)
+    int trsm_wide = 0;
     int gemm_tma = 1;      // batched A^T B GEMMs through the TMA / mbarrier kernel (ELMDDM_GEMM_TMA=0: cp.async)
     int panel_grid = 0;    // cooperative grid panel (automatic for very tall local problems; ELMDDM_PANEL_GRID=1)
     int iface_refine = 1;  // one step of iterative refinement of the interface solve (ELMDDM_IFACE_REFINE)

@@ -401,6 +401,146 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
 }
 
 
+// 128 flux rows per CTA (512 threads, 16 warps of 32 x 16): each R11 chunk serves twice the
+// columns, halving the R11 traffic of the 64-column version (config 4: 16.9 GB of DRAM reads for
+// 4.3 GB of R11, the four CTAs of a subdomain drift apart and miss L2).  One CTA per SM (the
+// 16 warps of two 64-column CTAs); per-element arithmetic and order as k_trsm_w (bit-identical).
+namespace trw2 {
+using namespace elmtma;
+constexpr int NT = 512, NCOL = 128;
+constexpr int STAGE = 6 * BOX;           // R chunk (2 boxes) + X chunk (2 x 2 boxes)
+constexpr int XP = 65, CP = 129;         // padded strides: R_ii [r * XP + c], C_i [c * CP + n]
+constexpr int DIAG = 64 * CP + 64 * XP + 64;
+constexpr int SMEM_BODY = (2 * STAGE > DIAG ? 2 * STAGE : DIAG);
+constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;
+}  // namespace trw2
+
+__global__ void __launch_bounds__(trw2::NT, 1) k_trsm_w2(const __grid_constant__ CUtensorMap tmR,
+                                                         const __grid_constant__ CUtensorMap tmA,
+                                                         const double* __restrict__ Kaug, int64_t ld, int64_t ncols,
+                                                         double* __restrict__ At, int M, int nat) {
+    using namespace trw2;
+    extern __shared__ uint8_t raw[];
+    double* base = reinterpret_cast<double*>(raw + ((1024u - (su32(raw) & 1023u)) & 1023u));
+    double* stg = base;                                   // 2 stages x (R 2 boxes | X 4 boxes)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + SMEM_BODY);
+    double* Cs = base;                                    // diagonal solve: C_i [c * CP + n]
+    double* Rs = base + 64 * CP;                          // R_ii [r * XP + c]
+    double* rinv = Rs + 64 * XP;                          // [64]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;              // 2 x 8 warps of 32 rows x 16 columns
+    const int s = blockIdx.y, n0 = blockIdx.x * NCOL;
+    const double* R = Kaug + (int64_t)s * ld * ncols;
+    double* A = At + (int64_t)s * M * nat;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], NT / 32);  // stage 0 / 1 released by every warp
+        mbar_init(&bar[3], NT / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t gch = 0;  // chunks issued so far (stage = gch & 1, parity = (gch >> 1) & 1)
+    const int nbk = (M + 63) / 64;
+    for (int i = 0; i < nbk; ++i) {
+        const int i0 = 64 * i, bi = min(64, M - i0);
+        double acc[4][2][2];  // -C while the updates are added
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    acc[mt][nt][e] = (c < bi && n0 + n < nat) ? -A[(int64_t)(n0 + n) * M + i0 + c] : 0.0;
+                }
+        const int nch = 2 * i;  // k-blocks 0..i-1, two 32-row chunks each
+        auto issue = [&](int ch, uint32_t g) {  // thread 0
+            double* d = stg + (g & 1) * STAGE;
+            const int r0 = 32 * ch;  // row of R11 / neuron index of X
+            if (g >= 2) mbar_wait(&bar[2 + (g & 1)], ((g >> 1) - 1) & 1);  // previous chunk of the stage consumed
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_expect(&bar[g & 1], 6 * BOX * 8);
+            tma_load(d, &tmR, r0, i0, s, &bar[g & 1]);
+            tma_load(d + BOX, &tmR, r0 + 16, i0, s, &bar[g & 1]);
+            tma_load(d + 2 * BOX, &tmA, r0, n0, s, &bar[g & 1]);
+            tma_load(d + 3 * BOX, &tmA, r0 + 16, n0, s, &bar[g & 1]);
+            tma_load(d + 4 * BOX, &tmA, r0, n0 + 64, s, &bar[g & 1]);
+            tma_load(d + 5 * BOX, &tmA, r0 + 16, n0 + 64, s, &bar[g & 1]);
+        };
+        if (tid == 0 && nch > 0) issue(0, gch);
+        for (int ch = 0; ch < nch; ++ch) {
+            const uint32_t g = gch + ch;
+            if (tid == 0 && ch + 1 < nch) issue(ch + 1, g + 1);
+            mbar_wait(&bar[g & 1], (g >> 1) & 1);
+            const double* Vs = stg + (g & 1) * STAGE;
+            const double* Xs = Vs + 2 * BOX + (wn >> 2) * 2 * BOX;  // this warp's 64-column half
+            const int wq = wn & 3;                                   // 16-column group in the half
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                double af[4], bf[2];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Vs[sw(kk, wm * 32 + mt * 8 + (lane >> 2))];
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) bf[nt] = Xs[sw(kk, wq * 16 + nt * 8 + (lane >> 2))];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[2 + (g & 1)]);  // stage (g & 1) may be refilled
+        }
+        gch += nch;
+        __syncthreads();  // every warp is done with the stages: the diagonal solve reuses them
+        // diagonal block: R_ii^T X = C
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+                    Cs[c * CP + n] = -acc[mt][nt][e];
+                }
+        for (int x = tid; x < 64 * 64; x += NT) {
+            const int r = x & 63, c = x >> 6;
+            Rs[r * XP + c] = (r <= c && c < bi) ? R[(int64_t)(i0 + c) * ld + i0 + r] : 0.0;
+        }
+        __syncthreads();
+        if (tid < bi) rinv[tid] = 1.0 / Rs[tid * XP + tid];
+        __syncthreads();
+        {
+            // thread (n = tid >> 2, q = tid & 3) owns rows c = q + 4j of column n
+            const int n = tid >> 2, q = tid & 3;
+            double xv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xv[j] = Cs[(q + 4 * j) * CP + n];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+#pragma unroll
+                for (int q0 = 0; q0 < 4; ++q0) {
+                    const int c = 4 * m + q0;
+                    if (q == q0) xv[m] *= rinv[c < bi ? c : 0];
+                    const double xc = __shfl_sync(0xffffffffu, xv[m], (lane & ~3) | q0);
+#pragma unroll
+                    for (int j = m; j < 16; ++j)
+                        if (j > m || q > q0) xv[j] = fma(-Rs[c * XP + q + 4 * j], xc, xv[j]);
+                }
+            }
+            if (n0 + n < nat)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (q + 4 * j < bi) A[(int64_t)(n0 + n) * M + i0 + q + 4 * j] = xv[j];
+        }
+        // X_i is read back through the async proxy (TMA) by the later blocks of this CTA
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __syncthreads();
+    }
+}
+
+
 // Back substitution c = R11^{-1} z for very large M (the lattice's N <= 2 x 2: M = 16384 / 65536)
 // with the CTAs of a cooperative launch split per subdomain (nper each): block row ib from the
 // bottom, CTA 0 of the subdomain solves the 64 x 64 diagonal block (warp-level substitution as in
@@ -705,7 +845,13 @@ cudaError_t run_schur_accumulate(const elmddm_ctx* c, double* Kaug, double* At, 
         // the flux-row tiles of a subdomain form one cluster (R11 chunks multicast), up to 8
         const int ncl = (c->trsm_cluster && g.x >= 2 && g.x <= 8) ? (int)g.x : 1;
         KTimer kt(c, ELMDDM_K_TRSM, st);
-        if (ncl > 1) {
+        if (ncl == 1 && c->trsm_wide && nat > 64) {  // 128 flux rows per CTA
+            if ((e = cudaFuncSetAttribute(k_trsm_w2, cudaFuncAttributeMaxDynamicSharedMemorySize, trw2::SMEM)) !=
+                cudaSuccess)
+                return e;
+            dim3 g2((nat + 127) / 128, (unsigned)S);
+            k_trsm_w2<<<g2, trw2::NT, trw2::SMEM, st>>>(tmR, tmA, Kaug, ld, ncols, At, M, nat);
+        } else if (ncl > 1) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = g;
             cfg.blockDim = dim3(trw::NT);

@@ -124,21 +124,24 @@ def test_implicit_e_columns_bit_identical(cfgkw, monkeypatch):
 
 @pytest.mark.parametrize("cfgkw", [dict(k=2), dict(P=3, M=96, p=9, q=80, problem=2),
                                    dict(P=2, M=64, p=31, q=31, problem=4, layout=1)])
-def test_trsm_cluster_bit_identical(cfgkw, monkeypatch):
-    """Schur TRSM with the flux-row tiles of a subdomain as one thread-block cluster and the R11
-    chunks multicast by TMA (ELMDDM_TRSM_CLUSTER=1; clusters of 4, 5 and 3 CTAs here): the per-CTA arithmetic
-    and order are unchanged, so P_s and S_s are bit-identical to the unclustered launch."""
+def test_trsm_variants_bit_identical(cfgkw, monkeypatch):
+    """Schur TRSM variants: 64 flux rows per CTA (the default), 128 per CTA (ELMDDM_TRSM_WIDE=1),
+    and 64 per CTA with the flux-row tiles of a subdomain as one thread-block cluster and the R11
+    chunks multicast by TMA (ELMDDM_TRSM_CLUSTER=1; clusters of 4, 5 and 3 CTAs here): the
+    per-element arithmetic and order are the same, so W_s, P_s and S_s are bit-identical."""
     import torch
 
     c = WL.config(cfgkw["k"]) if "k" in cfgkw else small(**cfgkw)
     outs = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("ELMDDM_TRSM_CLUSTER", flag)
+    for wide, cl in (("0", "0"), ("1", "0"), ("0", "1")):
+        monkeypatch.setenv("ELMDDM_TRSM_WIDE", wide)
+        monkeypatch.setenv("ELMDDM_TRSM_CLUSTER", cl)
         ctx, buf, _ = run_gpu(c, upto="schur")
         torch.cuda.synchronize()
         outs.append((buf["Pbuf"].clone(), buf["Sbuf"].clone(), buf["At"].clone()))
-    (P1, S1, A1), (P0, S0, A0) = outs
-    assert torch.equal(A1, A0) and torch.equal(P1, P0) and torch.equal(S1, S0)
+    for P1, S1, A1 in outs[1:]:
+        P0, S0, A0 = outs[0]
+        assert torch.equal(A1, A0) and torch.equal(P1, P0) and torch.equal(S1, S0)
 
 
 @pytest.mark.parametrize("k", [0, 1, 2])
