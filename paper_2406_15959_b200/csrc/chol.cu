@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
                                                       const int* __restrict__ rowslot, const int2* __restrict__ dep,
                                                       const double* __restrict__ rhs, double* out, int* flags,
                                                       int* pflags, double* __restrict__ ppart, int epoch,
-                                                      ElmStatus* status) {
+                                                      ElmStatus* status, const double* __restrict__ Yb) {
     extern __shared__ __align__(16) double tsm[];
     double* dtile = tsm;                  // [ELM_TS] the diagonal tile (i, i)
     double* part = dtile + ELM_TS;        // [4][64]
@@ -776,8 +776,8 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
 #ifdef ELM_CHOL_PROF
         unsigned long long pt0 = globaltimer(), pfw = 0;
 #endif
-        if (fin) {
-            load_tile_async(dtile, Mb + (int64_t)diag_tid[i] * ELM_TS);
+        if (fin) {  // the diagonal block's inverse Y = L(i,i)^{-1} (Yb), else the tile L(i,i)
+            load_tile_async(dtile, Yb ? Yb + i0 * LP : Mb + (int64_t)diag_tid[i] * ELM_TS);
             if (tid < NB) acc[tid] = rhs[i0 + tid];
         }
         double sacc = 0.0, tacc[8];
@@ -846,10 +846,29 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
                 for (int c = 0; c < nparts; ++c) tot += __ldcg(ppart + (int64_t)(s0 + c) * NB + tid);
                 acc[tid] -= nparts == 0 ? own : tot + own;
             }
-            rdv[tid] = 1.0 / dtile[tid * LP + tid];
+            if (!Yb) rdv[tid] = 1.0 / dtile[tid * LP + tid];
         }
         __syncthreads();
-        if (tid < 32) {
+        if (Yb) {  // x_i = Y acc (forward) / Y^T acc (backward): one 64 x 64 GEMV, no serial chain
+            if (DIR == 0) {
+                const int r = tid & 63, cg = tid >> 6;
+                double p = 0.0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) p += dtile[r + (16 * cg + u) * LP] * acc[16 * cg + u];
+                part[cg * NB + r] = p;  // (part was read into acc before the barrier above)
+                __syncthreads();
+                if (tid < NB)
+                    st_relaxed_f64(out + i0 + tid, (part[tid] + part[NB + tid]) + (part[2 * NB + tid] + part[3 * NB + tid]));
+            } else {
+                const int r = tid >> 2, q = tid & 3;
+                double p = 0.0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) p += dtile[(q + 4 * u) + r * LP] * acc[q + 4 * u];
+                p += __shfl_xor_sync(0xffffffffu, p, 1);
+                p += __shfl_xor_sync(0xffffffffu, p, 2);
+                if (q == 0) st_relaxed_f64(out + i0 + r, p);
+            }
+        } else if (tid < 32) {
             // diagonal solve with the lower tile (i, i): warp-level substitution
             const double* T = dtile;
             double z0 = acc[lane], z1 = acc[lane + 32];
@@ -993,6 +1012,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     // factorisation: one cooperative launch over the task list
     const DistState& ds = c->dist;
     const bool dist = ds.nrep > 1;
+    const double* Ybuf_solve = Ybuf;  // L(J,J)^{-1} tiles of the replica the solves read
     if (c->iface_refine) {
         // (one rank: the factorisation kernel saves the tiles of M as it reads them)
         if ((dist && (e = cudaMemcpyAsync(Mcopy, Mband, sizeof(double) * c->sz.band_elems, cudaMemcpyDeviceToDevice,
@@ -1028,6 +1048,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         k_drain<<<(unsigned)c->nsm, 256, 0, st>>>(mine.flags, pl.ntiles, 2 * epoch, c->d_status);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         Mband = mine.Mb;  // the triangular solves read this rank's replica
+        Ybuf_solve = mine.Ybuf;
     } else {
         int grid = grid_ll;
         int crit = 32;
@@ -1060,9 +1081,10 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
             int* pf = c->d_pflags;
             double* pp = c->d_ppart;
             ElmStatus* stp = c->d_status;
+            const double* yinv = c->trsv_inv ? Ybuf_solve : nullptr;
             void* args[] = {(void*)&Mband, (void*)&ntasks, (void*)&nblk_v, (void*)&dt, (void*)&tl, (void*)&rs,
                             (void*)&dl,    (void*)&rhs,    (void*)&out,    (void*)&flags, (void*)&pf, (void*)&pp,
-                            (void*)&epoch, (void*)&stp};
+                            (void*)&epoch, (void*)&stp,  (void*)&yinv};
             cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the task counter
             if (e1 == cudaSuccess) e1 = cudaMemsetAsync(out, 0xFF, sizeof(double) * nblk * NB, st);  // TRSV_EMPTY
             if (e1 != cudaSuccess) return e1;

@@ -529,6 +529,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         if (const char* env = getenv("ELMDDM_GEMM_TMA")) c->gemm_tma = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_TRSM_WIDE")) c->trsm_wide = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_TRSV_CHUNK")) c->trsv_chunk = atoi(env);
+        if (const char* env = getenv("ELMDDM_TRSV_INV")) c->trsv_inv = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_CHOL_TRSM_REFINE")) c->chol_trsm_refine = atoi(env) != 0;
         if (c->chol_trsm_refine < 0) c->chol_trsm_refine = !c->iface_refine;
         c->implicit_e = c->implicit_e && c->use_tma;

@@ -196,6 +196,7 @@ struct elmddm_ctx {
     // default: only when the solution-level refinement step R30 is off -- with it, config 4
     // 84.1 -> 80.2 ms factorisation, error vs exact 1.2e-11 -> 6.1e-11, config 3 3.1e-9 -> 6.3e-10)
     int chol_trsm_refine = -1;
+    int trsv_inv = 1;                   // triangular solves: diagonal blocks by their explicit inverse (ELMDDM_TRSV_INV)
     int trsv_chunk = 0;                 // dependency tiles per triangular-solve task, 0 = whole rows
                                         // (ELMDDM_TRSV_CHUNK; 32 / 64 measured slower at config 4)
     int4* d_sv_tasks[2] = {nullptr, nullptr};  // per direction: the task lists of build_trsv_tasks
