@@ -1180,12 +1180,16 @@ __global__ void __launch_bounds__(pt::NT, 2) k_panel_t(PanelArgs a, int nb) {
             }
             const double ts0 = __shfl_sync(0xffffffffu, mine, 0);
             const double x0 = __shfl_sync(0xffffffffu, mine, 8);
-            const double nrm = sqrt(x0 * x0 + ts0);
+            // (R20's alpha = -sign(x0) ||x||, tau = (alpha - x0) / alpha = 1 + |x0| / ||x||,
+            // 1 / (x0 - alpha) = sign(x0) / (|x0| + ||x||): one rsqrt and one reciprocal on the
+            // column's serial chain instead of a square root and two divisions)
+            const double ss = fma(x0, x0, ts0);
             double alpha = x0, tau = 0.0, scale = 0.0;
-            if (nrm != 0.0) {
+            if (ss != 0.0) {
+                const double rs = rsqrt(ss), nrm = ss * rs, ax = fabs(x0);
                 alpha = x0 >= 0.0 ? -nrm : nrm;
-                scale = 1.0 / (x0 - alpha);
-                tau = (alpha - x0) / alpha;
+                tau = fma(ax, rs, 1.0);
+                scale = (x0 >= 0.0 ? 1.0 : -1.0) / (ax + nrm);
             }
             const double ydl = __shfl_sync(0xffffffffu, mine, (lane & 7) + 8);
             const double wl = (lane >= 1 && lane < nk) ? tau * (ydl + scale * mine) : 0.0;
