@@ -1614,6 +1614,16 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         mbar_init(&bar[5], NT / 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    // T (nb x nb, zero outside) is fetched into the Z area while phase 1 runs (cp.async; the Z
+    // area is free until phase 2, which then takes W into the stage area instead)
+    for (int t = tid; t < 64 * 32; t += NT) {
+        const int i = t >> 5, k2 = (t & 31) * 2;
+        const int bytes = (i < nb && k2 < nb) ? (k2 + 1 < nb ? 16 : 8) : 0;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(Zs + i * PADZ + k2);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(bytes ? T + k2 + 64 * i : T),
+                     "r"(bytes));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
     __syncthreads();
     // implicit E_Gamma tile (j0 = 0 only: the host passes an empty range otherwise)
     const bool syn = ncol0 >= es.e_begin && ncol0 + 64 <= es.e_end;
@@ -1720,9 +1730,10 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
             __syncthreads();
         }
     }
-    __syncthreads();  // every warp is done with the stages: phase 2 stages T there
+    __syncthreads();  // every warp is done with the stages: phase 2 keeps W there
     // ---------------- phase 2: Z = -T^T W ----------------
-    double* Ts = stg;  // [64 i][PADZ]
+    const double* Ts = Zs;  // [64 i][PADZ] (prefetched)
+    double* Ws = stg;       // [64 n][PADZ]
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -1730,12 +1741,9 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 int i = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
-                Zs[n * PADZ + i] = acc[mt][nt][e];
+                Ws[n * PADZ + i] = acc[mt][nt][e];
             }
-    for (int t = tid; t < 64 * 64; t += NT) {
-        int k = t & 63, i = t >> 6;
-        Ts[i * PADZ + k] = (i < nb && k < nb) ? T[k + 64 * i] : 0.0;
-    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1749,13 +1757,13 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) af[mt] = Ts[(wm * 32 + mt * 8 + (lane >> 2)) * PADZ + kk];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bf[nt] = Zs[(wn * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
+        for (int nt = 0; nt < 2; ++nt) bf[nt] = Ws[(wn * 16 + nt * 8 + (lane >> 2)) * PADZ + kk];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
     }
-    __syncthreads();
+    __syncthreads();  // T read: the Z area takes Z
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
