@@ -218,7 +218,8 @@ constexpr int NT = 256;
 constexpr int STAGE = 4 * BOX;           // R chunk (2 boxes) + X chunk (2 boxes)
 constexpr int XP = 65;                   // padded stride of the diagonal-solve tiles
 constexpr int SMEM_BODY = (2 * STAGE > 2 * 64 * XP + 64 ? 2 * STAGE : 2 * 64 * XP + 64);
-constexpr int SMEM = SMEM_BODY * 8 + 64 + 1024;  // + [2] full, [2] empty mbarriers (<= 64 B)
+constexpr int RSP = 4 * BOX;             // the diagonal block R_ii, TMA-prefetched (4 boxes of 16 rows)
+constexpr int SMEM = (SMEM_BODY + RSP) * 8 + 64 + 1024;  // + mbarriers (<= 64 B)
 }  // namespace trw
 
 // Cluster version (launched with a cluster of gridDim.x CTAs, all flux-row tiles of one
@@ -260,14 +261,14 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
     extern __shared__ uint8_t raw[];
     double* base = reinterpret_cast<double*>(raw + ((1024u - (su32(raw) & 1023u)) & 1023u));
     double* stg = base;                                   // 2 stages x (R 2 boxes | X 2 boxes)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + SMEM_BODY);
+    double* RsP = base + SMEM_BODY;                       // R_ii prefetched by TMA (swizzled boxes)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(RsP + RSP);
     double* Cs = base;                                    // diagonal solve: C_i [c * XP + n]
     double* Rs = base + 64 * XP;                          // R_ii [r * XP + c]
     double* rinv = Rs + 64 * XP;                          // [64]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
     const int s = blockIdx.y, n0 = blockIdx.x * 64;
-    const double* R = Kaug + (int64_t)s * ld * ncols;
     double* A = At + (int64_t)s * M * nat;
     uint32_t nc, crank;
     asm("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(nc));
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
         mbar_init(&bar[3], NT / 32);
         mbar_init(&bar[4], (int)(nc * (NT / 32)));
         mbar_init(&bar[5], (int)(nc * (NT / 32)));
+        mbar_init(&bar[6], 1);  // R_ii landed
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -302,6 +304,12 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
                     const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
                     acc[mt][nt][e] = (c < bi && n0 + n < nat) ? -A[(int64_t)(n0 + n) * M + i0 + c] : 0.0;
                 }
+        if (tid == 0) {  // R_ii behind the block's GEMM (RsP was last read before the previous block ended)
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_expect(&bar[6], 4 * BOX * 8);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) tma_load(RsP + h * BOX, &tmR, i0 + 16 * h, i0, s, &bar[6]);
+        }
         const int nch = 2 * i;  // k-blocks 0..i-1, two 32-row chunks each
         auto issue = [&](int ch, uint32_t g) {  // thread 0
             double* d = stg + (g & 1) * STAGE;
@@ -360,9 +368,10 @@ __global__ void __launch_bounds__(trw::NT, 2) k_trsm_w(const __grid_constant__ C
                     const int c = wm * 32 + mt * 8 + (lane >> 2), n = wn * 16 + nt * 8 + 2 * (lane & 3) + e;
                     Cs[c * XP + n] = -acc[mt][nt][e];
                 }
+        mbar_wait(&bar[6], i & 1);
         for (int x = tid; x < 64 * 64; x += NT) {
             const int r = x & 63, c = x >> 6;
-            Rs[r * XP + c] = (r <= c && c < bi) ? R[(int64_t)(i0 + c) * ld + i0 + r] : 0.0;
+            Rs[r * XP + c] = (r <= c && c < bi) ? RsP[sw(r, c)] : 0.0;
         }
         __syncthreads();
         if (tid < bi) rinv[tid] = 1.0 / Rs[tid * XP + tid];
@@ -789,17 +798,35 @@ __global__ void __launch_bounds__(256) k_fcol(const double* __restrict__ Kaug, i
     const double* y = K + (int64_t)(M + F) * ld;      // rows [0, M) of column M + F
     const double* tF = y + M;                        // rows [M, M + Kt)
     const double* W = At + s * (int64_t)M * nat;
+    // (four independent partial sums per lane: four loads in flight per lane, fixed order)
     for (int i = w; i < nat; i += 8) {
-        double v = 0.0;
-        for (int k = lane; k < M; k += 32) v += W[(int64_t)i * M + k] * y[k];
+        const double* wi = W + (int64_t)i * M;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int k = lane;
+        for (; k + 96 < M; k += 128) {
+            v0 += wi[k] * y[k];
+            v1 += wi[k + 32] * y[k + 32];
+            v2 += wi[k + 64] * y[k + 64];
+            v3 += wi[k + 96] * y[k + 96];
+        }
+        for (; k < M; k += 32) v0 += wi[k] * y[k];
+        double v = (v0 + v1) + (v2 + v3);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) P[s * pstride + i + (int64_t)F * pld] = v;
     }
     for (int j = w; j <= F; j += 8) {
         const double* tj = K + M + (int64_t)(M + j) * ld;
-        double v = 0.0;
-        for (int r = lane; r < Kt; r += 32) v += tj[r] * tF[r];
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int r = lane;
+        for (; r + 96 < Kt; r += 128) {
+            v0 += tj[r] * tF[r];
+            v1 += tj[r + 32] * tF[r + 32];
+            v2 += tj[r + 64] * tF[r + 64];
+            v3 += tj[r + 96] * tF[r + 96];
+        }
+        for (; r < Kt; r += 32) v0 += tj[r] * tF[r];
+        double v = (v0 + v1) + (v2 + v3);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) {  // (both triangles: the consumers read diagonal 64-tiles in full)
