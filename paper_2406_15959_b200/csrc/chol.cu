@@ -319,6 +319,9 @@ struct CholArgs {
     const int* ntc;        // [nblk] tiles of column J
     int epoch;             // tile flags: 2 epoch when L(I,J) is final, 2 epoch - 1 when a split
                            // task's pre-aggregation is in the tile; cready and colcnt count epochs
+    const int* epoch_dev;  // non-null: the epoch is read from here at kernel entry (one rank: a
+                           // device counter bumped in-stream by k_launch_prep, so a captured CUDA
+                           // graph advances it on every replay); null: `epoch` (multi-rank path)
     ElmStatus* status;
     int* next;             // non-null: tasks dealt dynamically in list order (zeroed counter)
     // multi-rank factorisation (nrep > 1, dynamic dealing through the shared counter `next`):
@@ -354,7 +357,8 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
     }
     __syncthreads();
     const bool dist = a.nrep > 1;
-    const int fin_ep = 2 * a.epoch, pre_ep = fin_ep - 1;
+    const int epoch = a.epoch_dev ? *a.epoch_dev : a.epoch;
+    const int fin_ep = 2 * epoch, pre_ep = fin_ep - 1;
     const int my = dist ? a.rep_base + (int)blockIdx.x / a.ctas_per_rep : 0;
     double* const Mb = dist ? a.reps[my].Mb : a.Mb;
     double* const Ybuf = dist ? a.reps[my].Ybuf : a.Ybuf;
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                 const uint32_t epar = (epi_uses / NSTAGE) & 1;
                 ++epi_uses;
                 if (tid == 0) {
-                    wait_flag(cready + J, a.epoch, a.status, J, dist);
+                    wait_flag(cready + J, epoch, a.status, J, dist);
                     wait_flag(flags + a.diag_tid[td.klast], fin_ep, a.status, td.klast, dist);
                     fence_proxy_async();
                     mbar_expect(eb, 3 * TILE * 8);
@@ -584,11 +588,11 @@ __global__ void __launch_bounds__(llc::NT, 2) k_chol_ll(CholArgs a) {
                     __threadfence_system();
                     __syncthreads();
                     if (tid == 0)
-                        for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].cready + I, a.epoch);
+                        for (int r = 0; r < a.nrep; ++r) st_release_sys(a.reps[r].cready + I, epoch);
                 } else {
                     __threadfence();
                     __syncthreads();
-                    if (tid == 0) st_release(cready + I, a.epoch);
+                    if (tid == 0) st_release(cready + I, epoch);
                 }
             }
             // L(I,J) solves X L_JJ^T = C
@@ -753,8 +757,10 @@ __global__ void __launch_bounds__(256, 2) k_band_trsv(const double* __restrict__
                                                       const int* __restrict__ diag_tid, const int4* __restrict__ tasks,
                                                       const int* __restrict__ rowslot, const int2* __restrict__ dep,
                                                       const double* __restrict__ rhs, double* out, int* flags,
-                                                      int* pflags, double* __restrict__ ppart, int epoch,
-                                                      ElmStatus* status, const double* __restrict__ Yb) {
+                                                      int* pflags, double* __restrict__ ppart,
+                                                      const int* __restrict__ epoch_dev, ElmStatus* status,
+                                                      const double* __restrict__ Yb) {
+    const int epoch = *epoch_dev;  // bumped in-stream by k_launch_prep (graph-replay safe)
     extern __shared__ __align__(16) double tsm[];
     double* dtile = tsm;                  // [ELM_TS] the diagonal tile (i, i)
     double* part = dtile + ELM_TS;        // [4][64]
@@ -945,6 +951,16 @@ extern "C" int elmddm_debug_chol_dprof(void* host, int n) {
 namespace {
 // multi-rank: wait until every tile of this replica has arrived (the factorisation kernel of
 // this rank can end while other ranks still push their last tiles)
+// Before a persistent launch on one rank: zero its task counter (if any) and advance its epoch
+// counter in-stream, so that the kernel's flag comparisons stay fresh when the whole solve is
+// captured once in a CUDA graph and replayed (a host-side epoch would be frozen into the graph).
+__global__ void k_launch_prep(int* counter, int* epoch) {
+    if (threadIdx.x == 0) {
+        if (counter) *counter = 0;
+        *epoch += 1;
+    }
+}
+
 __global__ void k_drain(const int* flags, int ntiles, int epoch, ElmStatus* status) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
         wait_flag(flags + t, epoch, status, t, true);
@@ -1036,7 +1052,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         }
         const CholRep& mine = ds.reps[ds.emulate ? 0 : ds.rank];
         CholArgs a{mine.Mb, mine.Ybuf, mine.Cbuf, mine.cready, c->d_tasks, (int)pl.tasks.size(), 0, 0, c->d_klist,
-                   c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, c->d_status, ds.counter + (epoch & 1),
+                   c->d_diag_tid, mine.flags, c->d_colcnt, c->d_ntc, epoch, nullptr, c->d_status, ds.counter + (epoch & 1),
                    nrep, ds.emulate ? 0 : ds.rank, per, ds.d_reps, nullptr, c->chol_trsm_refine, c->d_tile_m};
         void* args[] = {(void*)&a};
         {
@@ -1055,10 +1071,11 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
         if (const char* env = getenv("ELMDDM_CHOL_CRIT")) crit = atoi(env);
         crit = std::max(1, std::min(crit, grid / 4));  // grid >= 148 on this part: both groups non-empty
         CholArgs a{Mband, Ybuf, Cbuf, c->d_cready, c->d_tasks, (int)pl.tasks.size(), pl.ncrit, crit, c->d_klist,
-                   c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, ++c->chol_epoch, c->d_status,
+                   c->d_diag_tid, c->d_cflags, c->d_colcnt, c->d_ntc, 0, c->d_epoch, c->d_status,
                    c->chol_sched ? c->d_chol_next : nullptr, 1, 0, grid, nullptr, c->iface_refine ? Mcopy : nullptr,
                    c->chol_trsm_refine, c->d_tile_m};
-        if (c->chol_sched && (e = cudaMemsetAsync(c->d_chol_next, 0, sizeof(int), st)) != cudaSuccess) return e;
+        k_launch_prep<<<1, 32, 0, st>>>(c->chol_sched ? c->d_chol_next : nullptr, c->d_epoch);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
         void* args[] = {(void*)&a};
         KTimer kt(c, ELMDDM_K_POTRF, st);
         if ((e = cudaLaunchCooperativeKernel((void*)k_chol_ll, dim3(grid), dim3(llc::NT), args, llc::SMEM, st)) !=
@@ -1069,7 +1086,7 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
     auto solve = [&](double* b, double* x) -> cudaError_t {
         int* flags = c->d_flags;
         for (int dir = 0; dir < 2; ++dir) {
-            int epoch = ++c->trsv_epoch;
+            int* epoch = c->d_epoch + 1;
             const double* rhs = dir == 0 ? b : z;
             double* out = dir == 0 ? z : x;
             int nblk_v = nblk, ntasks = c->sv_ntasks[dir];
@@ -1085,7 +1102,8 @@ cudaError_t run_cholesky_solve(const elmddm_ctx* c, double* Mband, const double*
             void* args[] = {(void*)&Mband, (void*)&ntasks, (void*)&nblk_v, (void*)&dt, (void*)&tl, (void*)&rs,
                             (void*)&dl,    (void*)&rhs,    (void*)&out,    (void*)&flags, (void*)&pf, (void*)&pp,
                             (void*)&epoch, (void*)&stp,  (void*)&yinv};
-            cudaError_t e1 = cudaMemsetAsync(flags + nblk, 0, sizeof(int), st);  // the task counter
+            k_launch_prep<<<1, 32, 0, st>>>(flags + nblk, epoch);  // the task counter, the epoch
+            cudaError_t e1 = cudaGetLastError();
             if (e1 == cudaSuccess) e1 = cudaMemsetAsync(out, 0xFF, sizeof(double) * nblk * NB, st);  // TRSV_EMPTY
             if (e1 != cudaSuccess) return e1;
             KTimer kt(c, ELMDDM_K_TRSV, st);

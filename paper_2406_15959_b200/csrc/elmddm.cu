@@ -589,7 +589,9 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
     if ((e = cudaMalloc((void**)&c->d_status, sizeof(ElmStatus))) != cudaSuccess ||
         (e = cudaMemset(c->d_status, 0, sizeof(ElmStatus))) != cudaSuccess ||
         (e = cudaMalloc((void**)&c->d_flags, sizeof(int) * (z.chol_blocks + 1))) != cudaSuccess ||
-        (e = cudaMemset(c->d_flags, 0, sizeof(int) * (z.chol_blocks + 1))) != cudaSuccess) {
+        (e = cudaMemset(c->d_flags, 0, sizeof(int) * (z.chol_blocks + 1))) != cudaSuccess ||
+        (e = cudaMalloc((void**)&c->d_epoch, sizeof(int) * 2)) != cudaSuccess ||
+        (e = cudaMemset(c->d_epoch, 0, sizeof(int) * 2)) != cudaSuccess) {
         elmddm_destroy(c);
         return ELMDDM_ECUDA;
     }
@@ -613,6 +615,7 @@ void elmddm_destroy(elmddm_ctx* c) {
     }
     cudaFree(c->d_status);
     cudaFree(c->d_flags);
+    cudaFree(c->d_epoch);
     cudaFree(c->d_sub_face);
     cudaFree(c->d_qsrc);
     cudaFree(c->d_umap);

@@ -191,7 +191,8 @@ struct elmddm_ctx {
                          // trailing update (elm_e_implicit; needs use_tma; ELMDDM_IMPLICIT_E=0 off)
     int panel_cluster = 0;  // QR panel blocks on 4-CTA clusters (default for S <= 48; ELMDDM_PANEL_CLUSTER)
     int* d_flags = nullptr;          // per 64-block completion flags of the wavefront triangular solves
-    mutable int trsv_epoch = 0;
+    int* d_epoch = nullptr;          // [2] device epoch counters: factorisation, triangular solves
+                                     // (advanced in-stream by k_launch_prep: graph-replay safe)
     // refinement step in the factorisation's tile solves X = C L(J,J)^{-T} (ELMDDM_CHOL_TRSM_REFINE;
     // default: only when the solution-level refinement step R30 is off -- with it, config 4
     // 84.1 -> 80.2 ms factorisation, error vs exact 1.2e-11 -> 6.1e-11, config 3 3.1e-9 -> 6.3e-10)
@@ -240,7 +241,6 @@ struct elmddm_ctx {
     int* d_colcnt = nullptr;         // [nblk] finished tiles of column J (summed over factorisations)
     int* d_ntc = nullptr;            // [nblk] tiles of column J
     int* d_cready = nullptr;         // [nblk] C(I, klast(I)) published for the diagonal task of row I
-    mutable int chol_epoch = 0;
     mutable int chol_grid = 0, trsv_grid = 0;  // persistent-kernel grids (chol.cu, first call)
     mutable std::vector<cudaStream_t> gstreams;
     mutable cudaEvent_t ev_fork = nullptr;

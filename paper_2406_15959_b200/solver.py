@@ -353,6 +353,41 @@ class Context:
 
         dist.all_reduce(torch.zeros(1, dtype=torch.int32, device=device), group=group)
 
+    def enqueue(self, buf: dict, xy=None, u=None, stream=None):
+        """One rank's whole hot path (H1-H9 of Algorithm 1) enqueued on `stream` with no
+        host synchronisation -- so it can be captured once in a CUDA graph (capture_graph) and
+        replayed.  Single rank, direct interface solve only: the CG solver checks convergence on
+        the host and the multi-rank path exchanges through NCCL between phases.  Device-side
+        errors surface at the next sync()."""
+        if self.prob.interface_solver != "cholesky":
+            raise _lib.ElmddmError("enqueue / capture_graph: only the direct interface solver runs without host syncs")
+        self.init_hidden(buf["W"], buf["b"], None, stream)
+        self.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"], stream)
+        self.local_factor(buf["Kaug"], buf["tau"], buf["work"], stream)
+        self.schur_accumulate(buf["Kaug"], buf["At"], buf["Pbuf"], buf["Sbuf"], buf["work"], stream)
+        if self.sizes["G"] > 0:
+            self.interface_assemble(buf["Pbuf"], buf["Sbuf"], buf["Mband"], buf["g"], buf["work"], stream)
+            self.interface_factor_solve(buf["Mband"], buf["g"], buf["uG"], buf["work"], stream)
+        self.back_solve(buf["Kaug"], buf["uG"], buf["coef"], buf["resid"], buf["work"], stream)
+        if xy is not None:
+            self.evaluate(buf["W"], buf["b"], buf["coef"], xy, u, stream)
+
+    def capture_graph(self, buf: dict, xy=None, u=None):
+        """Capture enqueue() once into a torch.cuda.CUDAGraph; graph.replay() then re-runs the whole
+        solve on the same buffers with one launch from the host (follow it with sync() to read
+        the device status).  One eager pass first creates the library's internal streams and its
+        per-context launch state, so nothing is allocated while capturing."""
+        if self.prob.interface_solver == "cholesky":
+            self.enqueue(buf, xy, u)
+            self.sync()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=buf["W"].device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+            self.enqueue(buf, xy, u, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
     def run(self, buf: dict, xy=None, u=None, group=None, stream=None, timer=None):
         """One pass of the hot path on this rank (Algorithm 1).  With a process group of
         size > 1 the Schur contributions of every slab are gathered to rank 0 (one NCCL gather, no
