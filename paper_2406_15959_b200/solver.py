@@ -361,6 +361,10 @@ class Context:
         errors surface at the next sync()."""
         if self.prob.interface_solver != "cholesky":
             raise _lib.ElmddmError("enqueue / capture_graph: only the direct interface solver runs without host syncs")
+        N = self.prob.P * self.prob.P
+        if (self.s_begin, self.s_end) != (0, N):
+            raise _lib.ElmddmError(f"enqueue / capture_graph: one rank owning every subdomain (this context owns "
+                                   f"[{self.s_begin}, {self.s_end}) of {N}); the multi-rank path is run()")
         self.init_hidden(buf["W"], buf["b"], None, stream)
         self.assemble(buf["W"], buf["b"], buf["Kaug"], buf["At"], stream)
         self.local_factor(buf["Kaug"], buf["tau"], buf["work"], stream)
@@ -377,9 +381,8 @@ class Context:
         solve on the same buffers with one launch from the host (follow it with sync() to read
         the device status).  One eager pass first creates the library's internal streams and its
         per-context launch state, so nothing is allocated while capturing."""
-        if self.prob.interface_solver == "cholesky":
-            self.enqueue(buf, xy, u)
-            self.sync()
+        self.enqueue(buf, xy, u)  # (raises for the CG solver before any capture starts)
+        self.sync()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(device=buf["W"].device)
         s.wait_stream(torch.cuda.current_stream())

@@ -489,6 +489,12 @@ def test_cuda_graph_replay_bit_identical(k):
         assert torch.equal(u, u_ref)
         for key in ("uG", "coef", "resid"):
             assert torch.equal(buf[key], b_ref[key]), key
+    if k == 1:  # a slab context (one rank's share) is not a whole solve: refused, nothing captured
+        import paper_2406_15959_b200 as E
+
+        part, pbuf = gpu_ctx(c, 0, 8)
+        with pytest.raises(E.ElmddmError, match="one rank owning every subdomain"):
+            part.capture_graph(pbuf)
 
 
 def test_interface_points_export():
