@@ -1590,7 +1590,7 @@ struct EsynArgs {
 __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ CUtensorMap tmV,
                                                        const __grid_constant__ CUtensorMap tmK,
                                                        const double* __restrict__ Tbuf, int64_t ld, int j0, int nb,
-                                                       int c0, int N, int s_off, EsynArgs es) {
+                                                       int c0, int N, int s_off, EsynArgs es, int rev3) {
     QR_PROF(1, ((unsigned long long)j0 << 20) | (unsigned)(s_off + blockIdx.y));
     using namespace wyt;
     extern __shared__ uint8_t raw[];
@@ -1775,14 +1775,17 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
             }
     __syncthreads();
     // ---------------- phase 3: C += V (-Z) ----------------
+    // rev3: the chunks bottom-up, so that the first ones are those phase 1 read last and that
+    // are still in L2 (each chunk is independent here: the same bits in either order)
     const int wm3 = warp & 1, wn3 = warp >> 1;
-    if (tid == 0) issue(0, n1 & 1 ? 1 : 0);  // continue the stage rotation of phase 1
+    auto chunk3 = [&](int i) { return rev3 ? nch - 1 - i : i; };
+    if (tid == 0) issue(chunk3(0), n1 & 1 ? 1 : 0);  // continue the stage rotation of phase 1
     const int sbase = n1 & 1;
-    for (int c = 0; c < nch; ++c) {
-        const int st = (c + sbase) & 1;
-        if (tid == 0 && c + 1 < nch) {
+    for (int i3 = 0; i3 < nch; ++i3) {
+        const int st = (i3 + sbase) & 1, c = chunk3(i3);
+        if (tid == 0 && i3 + 1 < nch) {
             asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // stage st^1 stored?
-            issue(c + 1, st ^ 1);
+            issue(chunk3(i3 + 1), st ^ 1);
         }
         wait_stage(st);
         const double* Vs = stg + st * STAGE;
@@ -3532,7 +3535,8 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             KTimer kt(c, ELMDDM_K_GEMM_QR, streams[g]);
             if (use_tma)
                 k_wy_tma<<<grid, wyt::NT, wy_smem, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
-                                                                   j0 + nb, n_tr, g0, j0 == 0 ? esyn : esyn_off);
+                                                                   j0 + nb, n_tr, g0, j0 == 0 ? esyn : esyn_off,
+                                                                   c->wy_rev3);
             else
                 k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
