@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -505,8 +506,18 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
     // known); a candidate is "ready" at r = its stall-free start (finish with an early start minus
     // its own cost).  Pick the ready task with the longest path to the end, else the one that
     // gets ready first.
+    // (ELMDDM_CHOL_LOCALITY = bucket width in us, experiment: bottom levels within one bucket
+    // rank equal and the tie goes to the lower column J, then row I, so that tasks sharing the
+    // tiles L(J, k) are dealt together and read them while they are in L2)
+    double loc_w = 0.0;
+    if (const char* env = getenv("ELMDDM_CHOL_LOCALITY")) loc_w = std::max(0.0, atof(env));
     using KV = std::pair<double, int>;
     std::priority_queue<KV, std::vector<KV>, std::greater<KV>> pending;  // (r, task)
+    auto rkey = [&](int t) {
+        if (loc_w <= 0.0) return blev[t];
+        const TaskDesc& td = pl.tasks[t];
+        return std::floor(blev[t] / loc_w) * 1e9 - (double)td.J * 1e5 - (double)td.I;
+    };
     std::priority_queue<KV> ready;                                        // (bottom level, task)
     std::priority_queue<double, std::vector<double>, std::greater<double>> freeat;
     for (int w = 0; w < workers; ++w) freeat.push(0.0);
@@ -520,7 +531,7 @@ double schedule_chol_tasks(CholPlan& pl, int workers) {
         const double s = freeat.top();
         freeat.pop();
         while (!pending.empty() && pending.top().first <= s) {
-            ready.push({blev[pending.top().second], pending.top().second});
+            ready.push({rkey(pending.top().second), pending.top().second});
             pending.pop();
         }
         int t;
