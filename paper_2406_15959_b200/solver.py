@@ -243,6 +243,7 @@ class Context:
 
     def set_timing(self, enable: bool):
         self._check(self.L.elmddm_set_timing(self.h, 1 if enable else 0), "set_timing")
+        self._timing = bool(enable)
 
     def timing(self, reset: bool = True) -> dict:
         t = _lib.Timing()
@@ -381,6 +382,8 @@ class Context:
         solve on the same buffers with one launch from the host (follow it with sync() to read
         the device status).  One eager pass first creates the library's internal streams and its
         per-context launch state, so nothing is allocated while capturing."""
+        if getattr(self, "_timing", False):
+            raise _lib.ElmddmError("capture_graph: per-kernel timing (set_timing) records host-read events; turn it off")
         self.enqueue(buf, xy, u)  # (raises for the CG solver before any capture starts)
         self.sync()
         g = torch.cuda.CUDAGraph()
