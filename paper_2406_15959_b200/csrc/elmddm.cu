@@ -522,6 +522,7 @@ elmddm_status elmddm_create(const elmddm_config* cfg, int device, elmddm_ctx** o
         c->qr_groups = g < 1 ? 1 : g;
         if (const char* env = getenv("ELMDDM_TMA")) c->use_tma = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_WY_REV3")) c->wy_rev3 = atoi(env) != 0;
+        if (const char* env = getenv("ELMDDM_WY_HINT3")) c->wy_hint3 = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_IMPLICIT_E")) c->implicit_e = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_IFACE_REFINE")) c->iface_refine = atoi(env) != 0;
         if (const char* env = getenv("ELMDDM_PANEL_GRID")) c->panel_grid = atoi(env) != 0;

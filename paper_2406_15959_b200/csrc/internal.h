@@ -172,6 +172,7 @@ struct elmddm_ctx {
     // internal streams for the subdomain groups of the QR (fork / join with events)
     int qr_groups = 4;
     int use_tma = 1;  // TMA-staged trailing update (ELMDDM_TMA=0 selects the cp.async kernel)
+    int wy_hint3 = 1;  // trailing update phase 3: C loads / stores evict-first in L2 (ELMDDM_WY_HINT3)
     int wy_rev3 = 1;  // trailing update phase 3 bottom-up (L2 reuse of phase 1's last chunks; ELMDDM_WY_REV3)
     // k_panel_t on <= 2048 rows with 256 TMEM columns / 112 KB, so that two panel CTAs can share an SM
     // (ELMDDM_PANEL_PAIR=0: 512 / 116 KB, one per SM).  Config 4 local_factor 195.0 -> 193.0 ms

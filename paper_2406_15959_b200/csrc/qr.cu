@@ -1649,14 +1649,23 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
         }
     };
     uint32_t par0 = 0, par1 = 0;
-    auto issue = [&](int c, int st) {
+    // (flags bit 1: phase 3's C chunks are last-use -- loaded and stored evict-first, so that L2
+    // keeps the other CTAs' phase-1 chunks for their phase 3 instead)
+    const bool hint3 = (rev3 & 2) != 0;
+    const uint64_t pol = hint3 && tid == 0 ? l2_evict_first() : 0ull;
+    auto issue = [&](int c, int st, bool last_use = false) {
         double* d = stg + st * STAGE;
         mbar_expect(&bar[st], (syn ? 2 : 4) * BOX * 8);
         tma_load(d, &tmV, j0 + c * CH, 0, sl, &bar[st]);
         tma_load(d + BOX, &tmV, j0 + c * CH + 16, 0, sl, &bar[st]);
         if (!syn) {
-            tma_load(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st]);
-            tma_load(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st]);
+            if (last_use && hint3) {
+                tma_load_hint(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st], pol);
+                tma_load_hint(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st], pol);
+            } else {
+                tma_load(d + 2 * BOX, &tmK, j0 + c * CH, ncol0, sl, &bar[st]);
+                tma_load(d + 3 * BOX, &tmK, j0 + c * CH + 16, ncol0, sl, &bar[st]);
+            }
         }
     };
     // phase-1 chunks: all, or for a synthetic tile the ones holding its ones (W = V^T C is zero
@@ -1778,14 +1787,14 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
     // rev3: the chunks bottom-up, so that the first ones are those phase 1 read last and that
     // are still in L2 (each chunk is independent here: the same bits in either order)
     const int wm3 = warp & 1, wn3 = warp >> 1;
-    auto chunk3 = [&](int i) { return rev3 ? nch - 1 - i : i; };
-    if (tid == 0) issue(chunk3(0), n1 & 1 ? 1 : 0);  // continue the stage rotation of phase 1
+    auto chunk3 = [&](int i) { return (rev3 & 1) ? nch - 1 - i : i; };
+    if (tid == 0) issue(chunk3(0), n1 & 1 ? 1 : 0, true);  // continue the stage rotation of phase 1
     const int sbase = n1 & 1;
     for (int i3 = 0; i3 < nch; ++i3) {
         const int st = (i3 + sbase) & 1, c = chunk3(i3);
         if (tid == 0 && i3 + 1 < nch) {
             asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // stage st^1 stored?
-            issue(chunk3(i3 + 1), st ^ 1);
+            issue(chunk3(i3 + 1), st ^ 1, true);
         }
         wait_stage(st);
         const double* Vs = stg + st * STAGE;
@@ -1841,8 +1850,13 @@ __global__ void __launch_bounds__(wyt::NT, 2) k_wy_tma(const __grid_constant__ C
             __syncthreads();
         }
         if (tid == 0) {
-            tma_store(&tmK, j0 + c * CH, ncol0, sl, Cs);
-            tma_store(&tmK, j0 + c * CH + 16, ncol0, sl, Cs + BOX);
+            if (hint3) {
+                tma_store_hint(&tmK, j0 + c * CH, ncol0, sl, Cs, pol);
+                tma_store_hint(&tmK, j0 + c * CH + 16, ncol0, sl, Cs + BOX, pol);
+            } else {
+                tma_store(&tmK, j0 + c * CH, ncol0, sl, Cs);
+                tma_store(&tmK, j0 + c * CH + 16, ncol0, sl, Cs + BOX);
+            }
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
     }
@@ -3536,7 +3550,7 @@ cudaError_t run_local_factor(const elmddm_ctx* c, double* Kaug, double* tau, dou
             if (use_tma)
                 k_wy_tma<<<grid, wyt::NT, wy_smem, streams[g]>>>(nb == ELM_NB ? tmV64 : tmVlast, tmK, Tbuf, ld, j0, nb,
                                                                    j0 + nb, n_tr, g0, j0 == 0 ? esyn : esyn_off,
-                                                                   c->wy_rev3);
+                                                                   c->wy_rev3 | (c->wy_hint3 << 1));
             else
                 k_wy_update<<<grid, wy::NT, wy::SMEM, streams[g]>>>(Vbuf, Tbuf, Kaug, ld, ncols, j0, nb, j0 + nb, n_tr, g0);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -43,6 +43,23 @@ __device__ __forceinline__ void tma_store(const CUtensorMap* tm, int c0, int c1,
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
                  ::"l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(src)) : "memory");
 }
+// L2 policy for last-use data (bulk tensor copies with .L2::cache_hint)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_hint(double* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
+        ::"r"(su32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_store_hint(const CUtensorMap* tm, int c0, int c1, int c2, const double* src,
+                                               uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;\n"
+                 ::"l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(su32(src)), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
