@@ -76,9 +76,9 @@ def test_plan_tiles_cover_scalar_fill(P, q, ordering):
     assert sorted(ids.tolist()) == list(range(pl["ntiles"]))
 
 
-@pytest.mark.parametrize("split", ["0", "4", "1"])
+@pytest.mark.parametrize("split,locality", [("0", "0"), ("4", "0"), ("1", "0"), ("4", "500"), ("0", "5000")])
 @pytest.mark.parametrize("P,q", [(3, 5), (4, 24), (6, 10), (8, 60)])
-def test_plan_task_list_is_topological_and_counts_updates(P, q, split, monkeypatch):
+def test_plan_task_list_is_topological_and_counts_updates(P, q, split, locality, monkeypatch):
     """The list-scheduled order (dynamic dealing): every task comes after the tiles its k-list
     and its epilogue wait for -- the condition under which the persistent kernel's smallest
     unfinished task can always run -- and the update count is the number of (I, J, k) with
@@ -86,6 +86,7 @@ def test_plan_task_list_is_topological_and_counts_updates(P, q, split, monkeypat
     (I, J) takes the first updates of the k-list (columns below J's dissection node, never the
     diagonal task's last one), waits only for their tiles and comes before the rest of (I, J)."""
     monkeypatch.setenv("ELMDDM_CHOL_SPLIT", split)
+    monkeypatch.setenv("ELMDDM_CHOL_LOCALITY", locality)  # (the opt-in locality tie-break keeps it topological)
     pl = E.plan_query(P, q, 1, 296)
     have = pl["tile_map"] >= 0
     fin, pre = {}, {}
