@@ -1941,7 +1941,8 @@ __global__ void __launch_bounds__(gp::NT) k_panel_grid(PanelArgs a, int nb, int 
             P[(int64_t)cta * NG] = t;
             // row jc of the panel's later columns, published by its owner before anyone updates it
             if (own_jc)
-                for (int k = 0; k < nb - 1 - c; ++k) P[(int64_t)cta * NG + ELM_NB + k] = A[(jc + 1 + k) * ld + jc];
+                for (int k = 0; k < nb - 1 - c; ++k)
+                    P[(int64_t)cta * NG + ELM_NB * (1 + (c & 1)) + k] = A[(jc + 1 + k) * ld + jc];
         }
         gp_barrier(C, nper, gen);
         if (tid == 0) {
@@ -1978,7 +1979,7 @@ __global__ void __launch_bounds__(gp::NT) k_panel_grid(PanelArgs a, int nb, int 
         }
         gp_barrier(C, nper, gen);
         if (tid < nk) {  // w_k = tau (A[jc, k] + sum_i v_i A[i, k]), fixed order
-            double d = P[(int64_t)owner * NG + ELM_NB + tid];
+            double d = P[(int64_t)owner * NG + ELM_NB * (1 + (c & 1)) + tid];
             for (int k2 = 0; k2 < nper; ++k2) d += P[(int64_t)k2 * NG + 1 + tid];
             wsh[tid] = tau * d;
         }
@@ -1986,14 +1987,35 @@ __global__ void __launch_bounds__(gp::NT) k_panel_grid(PanelArgs a, int nb, int 
         for (int k = warp; k < nk; k += NW) {
             double* y = A + (jc + 1 + k) * ld;
             const double w = wsh[k];
-            for (int64_t i = i0 + lane; i < r1; i += 32) y[i] = fma(-w, x[i], y[i]);
+            // four rows per lane loaded before any store (the store to y[i] may alias, for the
+            // compiler, the next rows' loads: one row at a time serialised every load on the
+            // previous store -- ncu: 23% of the kernel's stall samples on this FMA)
+            int64_t i = i0 + lane;
+            for (; i + 96 < r1; i += 128) {
+                const double x0 = x[i], x1 = x[i + 32], x2 = x[i + 64], x3 = x[i + 96];
+                const double y0 = y[i], y1 = y[i + 32], y2 = y[i + 64], y3 = y[i + 96];
+                y[i] = fma(-w, x0, y0);
+                y[i + 32] = fma(-w, x1, y1);
+                y[i + 64] = fma(-w, x2, y2);
+                y[i + 96] = fma(-w, x3, y3);
+            }
+            for (; i < r1; i += 32) y[i] = fma(-w, x[i], y[i]);
             if (lane == 0 && own_jc) y[jc] -= w;  // row jc: v_jc = 1 (the owner)
         }
         if (tid == 0 && own_jc) {
             x[jc] = prm[0];  // R_jj
             a.tau[(int64_t)sl * a.M + jc] = tau;
         }
-        gp_barrier(C, nper, gen);  // the next column reads rows updated by other CTAs' owners
+        // No grid barrier at the end of a column (a CTA barrier suffices: the next column's norm
+        // reads the own rows other warps just updated): the next column's first grid barrier
+        // already orders every CTA's update of its own rows (the next diagonal element included)
+        // before anyone reads them, and the published diagonal row alternates between two slots
+        // by column parity, so a CTA running ahead never overwrites the one a slower CTA still
+        // reads.  After the last column the Gram partials below reuse every slot: a grid barrier.
+        if (c == nb - 1)
+            gp_barrier(C, nper, gen);
+        else
+            __syncthreads();
     }
     // explicit V (absolute rows, unit diagonal, zero above) of the own rows
     for (int c = 0; c < ELM_NB; ++c) {
