@@ -122,17 +122,18 @@ def test_implicit_e_columns_bit_identical(cfgkw, monkeypatch):
     assert torch.equal(K1, K0) and torch.equal(t1, t0)
 
 
+@pytest.mark.parametrize("knob", ["ELMDDM_WY_REV3", "ELMDDM_WY_HINT3"])
 @pytest.mark.parametrize("cfgkw", [dict(k=2), dict(P=3, M=40, p=9, q=16, problem=1)])
-def test_trailing_update_chunk_order_bit_identical(cfgkw, monkeypatch):
-    """The trailing update's phase 3 (C += V Z, chunk by chunk) runs bottom-up by default
-    (ELMDDM_WY_REV3, L2 reuse of phase 1's last chunks); each chunk is independent, so the
-    factorisation is bit-identical to the top-down order."""
+def test_trailing_update_chunk_order_bit_identical(cfgkw, knob, monkeypatch):
+    """Order-only knobs of the trailing update are bit-identical on and off: its phase 3
+    (C += V Z, chunk by chunk) bottom-up (ELMDDM_WY_REV3, L2 reuse of phase 1's last chunks;
+    each chunk is independent) and with L2 evict-first hints (ELMDDM_WY_HINT3)."""
     import torch
 
     c = WL.config(cfgkw["k"]) if "k" in cfgkw else small(**cfgkw)
     outs = []
     for flag in ("1", "0"):
-        monkeypatch.setenv("ELMDDM_WY_REV3", flag)
+        monkeypatch.setenv(knob, flag)
         _, buf, _ = run_gpu(c, upto="factor")
         outs.append((buf["Kaug"].clone(), buf["tau"].clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
