@@ -1939,11 +1939,13 @@ __global__ void __launch_bounds__(gp::NT) k_panel_grid(PanelArgs a, int nb, int 
             double t = 0.0;
             for (int w = 0; w < NW; ++w) t += red[w];
             P[(int64_t)cta * NG] = t;
-            // row jc of the panel's later columns, published by its owner before anyone updates it
-            if (own_jc)
-                for (int k = 0; k < nb - 1 - c; ++k)
-                    P[(int64_t)cta * NG + ELM_NB * (1 + (c & 1)) + k] = A[(jc + 1 + k) * ld + jc];
         }
+        // row jc of the panel's later columns, published by its owner before anyone updates it
+        // (one element per thread: by thread 0 alone, each strided load waited for the previous
+        // store, ~60 L2 round trips on the owner CTA while every other CTA waited at the barrier)
+        if (own_jc)
+            for (int k = tid; k < nb - 1 - c; k += NT)
+                P[(int64_t)cta * NG + ELM_NB * (1 + (c & 1)) + k] = A[(jc + 1 + k) * ld + jc];
         gp_barrier(C, nper, gen);
         if (tid == 0) {
             double t = 0.0;
